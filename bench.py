@@ -1,0 +1,501 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 mesh-registration path (BASELINE.json metric).
+
+Metric: Mpx*iter/s = sum over pairs of W*H*iterations_run / time (SURVEY.md
+§8(d)), whole job over all ranks.  Default workload = BASELINE config 4: a
+batch of 64 independent 512x512 pairs per GPU (config-2 pairs, reference
+mesher meshes, 200 iterations, tau=0.005, lam=0.8, 1 smoothing pass,
+energy_tolerance=0 so every pair runs all 200 iterations).  Pairs shard
+across ranks with no collective ("scaling": "weak": every rank registers its
+own 64-pair batch).
+
+  value   device time of K runs of the whole registration (loop + dense pass)
+          with inputs resident in HBM, CUDA events on the library's stream,
+          L2 flushed (256 MiB write) between steps outside the events.
+  e2e     the same work through the C ABI batch call from pinned HOST
+          buffers: per-pair device mesh setup (upload + pixel map), H2D of the
+          images, the run, D2H of u / dense field / warped image, statuses.
+  --impl reference   the reference algorithm (CPU oracle port of meshreg, one
+          process per core, one pair each) on the same workload.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                       [--workload c4|c1|c2|c3] [--pairs P] [--precision f32|f64]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1411_2141_b200.synthetic import CONFIGS, make_pair  # noqa: E402
+
+MESH_DIR = os.path.join(ROOT, "data", "meshes")
+METRIC = "registration throughput (Mpx*iter/s)"
+UNIT = "Mpx*iter/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--pairs", type=int, default=None)
+    ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-pairs", type=int, default=2)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- inputs
+def mesh_file(cfg, seed):
+    return os.path.join(MESH_DIR, f"{cfg}_s{seed}.npz")
+
+
+def fallback_mesh(size, target):
+    """Deterministic structured triangulation used only when the cached
+    reference-mesher mesh is absent (reported in config.mesh)."""
+    k = max(2, int(round(np.sqrt(target))))
+    xs = np.linspace(0.0, size - 1.0, k)
+    gx, gy = np.meshgrid(xs, xs)
+    V = np.stack([gx.ravel(), gy.ravel()], axis=1)
+    T = []
+    for j in range(k - 1):
+        for i in range(k - 1):
+            a, b, c, d = j * k + i, j * k + i + 1, (j + 1) * k + i, (j + 1) * k + i + 1
+            T += [(a, b, d), (a, d, c)]
+    return V, np.array(T, np.int64)
+
+
+def workload_spec(name):
+    spec = CONFIGS["c2" if name == "c4" else name]
+    mesh_cfg = spec.name
+    return spec, mesh_cfg
+
+
+def load_pair(name, seed):
+    """(re, te, V, T, mesh_kind, seed_used) for one pair of the workload."""
+    spec, mesh_cfg = workload_spec(name)
+    used = seed
+    if not os.path.exists(mesh_file(mesh_cfg, used)) and os.path.exists(
+            mesh_file(mesh_cfg, seed % 64)):
+        used = seed % 64  # replica of a cached pair
+    re, te = make_pair(spec, used)
+    if os.path.exists(mesh_file(mesh_cfg, used)):
+        d = np.load(mesh_file(mesh_cfg, used))
+        V, T, kind = d["V"], d["T"].astype(np.int64), "reference-mesher"
+    else:
+        V, T = fallback_mesh(spec.size, spec.target_nodes)
+        kind = "fallback-structured"
+    return re, te, V, T, kind, used
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- dist
+def dist_setup():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def dist_init(backend, local):
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend)
+    return dist
+
+
+def reduce_max(value, world, dist, device):
+    if world == 1:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world, dist):
+    if world > 1:
+        dist.barrier()
+
+
+# --------------------------------------------------------------------------- ours
+def mesh_handle(lib, V, T):
+    V = np.ascontiguousarray(V, np.float64)
+    T = np.ascontiguousarray(T, np.int64)
+    h = C.c_void_p()
+    err = C.create_string_buffer(512)
+    rc = lib.mrb_mesh_build(V.shape[0], V.ctypes.data, T.shape[0], T.ctypes.data, C.byref(h),
+                            err, 512)
+    if rc != 0:
+        raise RuntimeError(err.value.decode())
+    return h.value
+
+
+def check(lib, ctx, rc, what):
+    if rc != 0:
+        raise RuntimeError(f"{what}: code {rc}: {lib.mrb_last_error(ctx).decode()}")
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    from paper_1411_2141_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dist = dist_init("nccl", local) if world > 1 else None
+    device = torch.device("cuda", local)
+    lib = _lib.load()
+    ctx = _lib.context(local)
+    stream = torch.cuda.ExternalStream(lib.mrb_ctx_stream(ctx), device=device)
+
+    spec, _ = workload_spec(args.workload)
+    P = args.pairs or (64 if args.workload == "c4" else 1)
+    seeds = [rank * P + i for i in range(P)]
+    pairs = [load_pair(args.workload, s) for s in seeds]
+    W = H = spec.size
+    iters = spec.iterations
+    npx = W * H
+    cfg = _lib.mrb_config(0.005, 0.8, 0.0, iters, 1,
+                          _lib.PREC_F32 if args.precision == "f32" else _lib.PREC_F64, 0)
+    handles = [mesh_handle(lib, p[2], p[3]) for p in pairs]
+    arr = (C.c_void_p * P)(*handles)
+    batch = C.c_void_p()
+    check(lib, ctx, lib.mrb_batch_create(ctx, P, arr, W, H, _lib.F32, C.byref(cfg),
+                                         C.byref(batch)), "batch_create")
+    re_d = torch.from_numpy(np.stack([p[0] for p in pairs])).to(device)
+    te_d = torch.from_numpy(np.stack([p[1] for p in pairs])).to(device)
+    torch.cuda.synchronize()
+    check(lib, ctx, lib.mrb_batch_set_images(batch, re_d.data_ptr(), te_d.data_ptr(), 1), "set")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+
+    for _ in range(max(args.warmup, 3)):
+        check(lib, ctx, lib.mrb_batch_run(batch), "run")
+    check(lib, ctx, lib.mrb_batch_sync(batch), "warmup sync")
+
+    # per-kernel launch times (CUDA events around each launch, separate pass)
+    ktimes = np.zeros(5)
+    check(lib, ctx, lib.mrb_batch_kernel_times(batch, ktimes.ctypes.data), "kernel_times")
+    kbytes = np.zeros(4)
+    lib.mrb_batch_kernel_bytes(batch, kbytes.ctypes.data)
+
+    barrier(world, dist)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    evs = []
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            check(lib, ctx, lib.mrb_batch_run(batch), "run")
+            e1.record(stream)
+            evs.append((e0, e1))
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    barrier(world, dist)
+    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t_ms = reduce_max(t_ms, world, dist, device)
+
+    rc = lib.mrb_batch_sync(batch)
+    check(lib, ctx, rc, "result status")
+    it = C.c_int32()
+    tot_iters = 0
+    for p in range(P):
+        lib.mrb_batch_pair_status(batch, p, C.byref(it), None, None, None, None, 0)
+        tot_iters += it.value
+    work = float(npx) * tot_iters  # px*iter per step on this rank
+    value = world * work * args.steps / (t_ms / 1e3) / 1e6
+    launches = int(lib.mrb_batch_launches_per_run(batch)) * args.steps
+    alg_bytes = lib.mrb_batch_algorithmic_bytes(batch)
+    lib.mrb_batch_destroy(batch)
+
+    # ---- e2e through the C ABI from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, lib, ctx, pairs, cfg, W, H, world, dist, device)
+
+    # ---- roofline of the dominant kernel (largest share of the run)
+    n_launch = {0: iters, 1: iters, 2: iters, 3: 1}
+    share = {k: ktimes[k] * n_launch[k] for k in range(4)}
+    dom = max(share, key=share.get)
+    names = {0: "k_sample", 1: "k_grad", 2: "k_smooth", 3: "k_dense"}
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = kbytes[dom] / (ktimes[dom] / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        traffic = tj.get(args.workload, {}).get(args.precision, {}).get(names[dom])
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, pairs[:args.cpu_pairs], spec)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": round(t_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
+            "data": "synthetic (seeded BASELINE generator; meshes from the reference mesher)",
+            "config": {
+                "workload": f"{args.workload}: {P} pairs/GPU of {W}x{H}, {iters} iterations, "
+                            f"{pairs[0][4]} meshes (~{int(np.mean([len(p[2]) for p in pairs]))} nodes)",
+                "pairs_per_gpu": P, "global_pairs": P * world, "image": [W, H],
+                "iterations": iters, "tau": 0.005, "lam": 0.8, "smoothing_passes": 1,
+                "energy_tolerance": 0.0, "mesh": pairs[0][4],
+                "pair_seeds": f"{seeds[0]}..{seeds[-1]}",
+                "replicated_pairs": any(p[5] != s for p, s in zip(pairs, seeds)),
+                "l2": "flushed (256 MiB write) between timed steps, outside the events",
+                "parallelism": f"pair-sharded dp{world} (no collective)",
+                "precision": args.precision,
+            },
+            "gpu_launches": launches,
+            "kernel_ms": {names[k]: round(float(ktimes[k]), 5) for k in range(4)},
+            "algorithmic_bytes_per_step": alg_bytes,
+            "hbm_frac_whole_run": round(alg_bytes / (t_ms / args.steps / 1e3) / 1e9 / peak, 4),
+            "roofline": {"kernel": names[dom], "bound": "hbm", "achieved": round(achieved, 1),
+                         "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, lib, ctx, pairs, cfg, W, H, world, dist, device):
+    import torch
+    from paper_1411_2141_b200 import _lib
+
+    P = len(pairs)
+    npx = W * H
+    re_h = torch.from_numpy(np.stack([p[0] for p in pairs])).pin_memory()
+    te_h = torch.from_numpy(np.stack([p[1] for p in pairs])).pin_memory()
+    n_tot = sum(len(p[2]) for p in pairs)
+    u_h = torch.empty((n_tot, 2), dtype=torch.float64).pin_memory()
+    dense_h = [torch.empty((P, H, W), dtype=torch.float32).pin_memory() for _ in range(3)]
+    times = []
+    tot_iters = 0
+    steps = max(1, min(args.steps, 5))
+    for step in range(1 + steps):  # one untimed warm-up step
+        handles = [mesh_handle(lib, p[2], p[3]) for p in pairs]  # host mesh (mesher output)
+        arr = (C.c_void_p * P)(*handles)
+        torch.cuda.synchronize()
+        barrier(world, dist)
+        t0 = time.perf_counter()
+        b = C.c_void_p()
+        check(lib, ctx, lib.mrb_batch_create(ctx, P, arr, W, H, _lib.F32, C.byref(cfg),
+                                             C.byref(b)), "e2e create")
+        check(lib, ctx, lib.mrb_batch_set_images(b, re_h.data_ptr(), te_h.data_ptr(), 0), "e2e set")
+        check(lib, ctx, lib.mrb_batch_run(b), "e2e run")
+        check(lib, ctx, lib.mrb_batch_get_results(b, _lib.F32, u_h.data_ptr(),
+                                                  *(d.data_ptr() for d in dense_h)), "e2e get")
+        check(lib, ctx, lib.mrb_batch_sync(b), "e2e sync")
+        dt = time.perf_counter() - t0
+        if step:
+            times.append(dt)
+            it = C.c_int32()
+            for p in range(P):
+                lib.mrb_batch_pair_status(b, p, C.byref(it), None, None, None, None, 0)
+                tot_iters += it.value
+        lib.mrb_batch_destroy(b)
+        for h in handles:
+            lib.mrb_mesh_destroy(h)
+    t = reduce_max(sum(times), world, dist, device)
+    value = world * float(npx) * tot_iters / t / 1e6
+    mesh_bytes = sum(16 * len(p[2]) * 3 + 28 * len(p[2]) + 16 * len(p[3]) + 48 * 3 * len(p[3])
+                     for p in pairs)
+    return {"value": round(value, 3), "unit": UNIT, "steps": steps,
+            "ms_per_step": round(1e3 * t / steps, 3),
+            "h2d_bytes_per_step": int(2 * P * npx * 4 + mesh_bytes),
+            "d2h_bytes_per_step": int(16 * n_tot + 3 * P * npx * 4),
+            "includes": "device mesh setup (upload + pixel map), H2D images, full registration, "
+                        "D2H u/ux/uy/warped/status (host mesh connectivity built untimed, like the "
+                        "reference's TriMesh from its mesher)"}
+
+
+# --------------------------------------------------------------------------- CPU legs
+def _oracle_register(re, te, V, T, iters):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import meshreg_oracle as O
+    m = O.Mesh(V, T)
+    t0 = time.perf_counter()
+    u, info = O.register(re.astype(np.float64), te.astype(np.float64), m, tau=0.005, lam=0.8,
+                         max_iterations=iters, smoothing_passes=1, energy_tolerance=0.0)
+    return time.perf_counter() - t0, info["iterations_run"]
+
+
+def cpu_baseline(args, pairs, spec):
+    """Oracle port timed single-threaded on this host (rank 0, N=1)."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        threadpool_limits = None
+    tot, work = 0.0, 0.0
+    ctxm = threadpool_limits(1) if threadpool_limits else None
+    try:
+        for re, te, V, T, kind, used in pairs:
+            dt, it = _oracle_register(re, te, V, T, spec.iterations)
+            tot += dt
+            work += float(spec.size) ** 2 * it
+    finally:
+        if ctxm is not None:
+            ctxm.unregister() if hasattr(ctxm, "unregister") else None
+    return {"value": round(work / tot / 1e6, 4), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{len(pairs)} of the workload's pairs (seeds {[p[5] for p in pairs]}), "
+                      f"{spec.size}x{spec.size}, {spec.iterations} iterations each, full register "
+                      f"(loop + densify + warp + MSD), {tot:.1f} s"}
+
+
+def _ref_worker(conn, workload, seed, iters):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    re, te, V, T, kind, used = load_pair(workload, seed)
+    conn.send("ready")
+    while True:
+        msg = conn.recv()
+        if msg == "stop":
+            break
+        conn.send(_oracle_register(re, te, V, T, iters))
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference arm
+    import multiprocessing as mp
+    spec, _ = workload_spec(args.workload)
+    P = args.pairs or (64 if args.workload == "c4" else 1)
+    cores = len(os.sched_getaffinity(0))
+    nproc = max(1, min(P, cores))
+    env_bak = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS",
+                                              "MKL_NUM_THREADS")}
+    for k in env_bak:
+        os.environ[k] = "1"
+    ctx = mp.get_context("spawn")
+    procs, conns = [], []
+    for i in range(nproc):
+        a, b = ctx.Pipe()
+        p = ctx.Process(target=_ref_worker, args=(b, args.workload, i, spec.iterations))
+        p.start()
+        procs.append(p)
+        conns.append(a)
+    for c in conns:
+        c.recv()
+    times, work = [], 0.0
+    for step in range(max(args.warmup, 3) + args.steps):
+        t0 = time.perf_counter()
+        for c in conns:
+            c.send("go")
+        res = [c.recv() for c in conns]
+        dt = time.perf_counter() - t0
+        if step >= max(args.warmup, 3):
+            times.append(dt)
+            work += sum(float(spec.size) ** 2 * it for _, it in res)
+    for c in conns:
+        c.send("stop")
+    for p in procs:
+        p.join()
+    value = work / sum(times) / 1e6
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": round(1e3 * sum(times) / len(times), 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE generator; meshes from the reference mesher)",
+        "config": {"workload": f"{args.workload}: bounded sample of {nproc} pairs per step "
+                               f"(one per host core) of {spec.size}x{spec.size}, "
+                               f"{spec.iterations} iterations",
+                   "pairs_per_step": nproc, "image": [spec.size, spec.size],
+                   "iterations": spec.iterations, "energy_tolerance": 0.0},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": nproc, "kind": "port",
+                         "sample": f"{nproc} pairs per step, one process per core, oracle port "
+                                   "of meshreg register (numpy/scipy, float64)"},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

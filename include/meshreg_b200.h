@@ -1,0 +1,193 @@
+/*
+ * meshreg_b200.h — C ABI of the B200-native mesh-registration hot path.
+ *
+ * The reference (`meshreg`, a pure-Python package) has no plugin/FFI layer:
+ * its boundary for this path is the Python API re-exported by
+ * pkg/src/meshreg/__init__.py:12-60.  Each entry point here
+ * is what a ctypes binding of that API would call; the Python package
+ * `paper_1411_2141_b200` is that binding and mirrors the reference names,
+ * argument meaning and exceptions.  All pointers are plain host pointers
+ * unless an argument says "device"; sizes are element counts.
+ *
+ * Return codes map 1:1 onto the reference's exceptions:
+ *   MRB_OK            success
+ *   MRB_E_VALUE       ValueError          (solver.py:158-161, mesh.py:61-123,
+ *                                          densefield.py:139-140,192-193,
+ *                                          image.py:183-184)
+ *   MRB_E_DIVERGED    DivergenceError     (solver.py:33-34,131-132,176-184)
+ *   MRB_E_COVERAGE    MeshCoverageError   (densefield.py:58-59,127)
+ *   MRB_E_CUDA        CUDA runtime failure / no device
+ * The human-readable message (same text as the reference exception) is
+ * available from mrb_last_error(ctx) or the per-pair status call.
+ */
+#ifndef MESHREG_B200_H
+#define MESHREG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MRB_OK 0
+#define MRB_E_VALUE 1
+#define MRB_E_DIVERGED 2
+#define MRB_E_COVERAGE 3
+#define MRB_E_CUDA 4
+#define MRB_E_INTERNAL 5
+
+/* image / output element types */
+#define MRB_F32 0
+#define MRB_F64 1
+
+/* arithmetic precision of the iteration state (mrb_config.precision) */
+#define MRB_PREC_F32 0 /* fp32 state + fp32 math, fp64 energy/MSD reductions */
+#define MRB_PREC_F64 1 /* fp64 state + fp64 math (fp32 taps when exact)      */
+
+/* which CSR operator mrb_mesh_export_csr returns */
+#define MRB_CSR_LAPLACIAN 0 /* build_laplacian, mesh.py:254-265              */
+#define MRB_CSR_GRAD_X 1    /* TriangleGeometry.grad_x_op, mesh.py:203-205    */
+#define MRB_CSR_GRAD_Y 2    /* TriangleGeometry.grad_y_op, mesh.py:206-208    */
+#define MRB_CSR_VERTEX_AVG 3 /* TriangleGeometry.vertex_average_op, 210-213   */
+
+typedef struct mrb_ctx mrb_ctx;
+typedef struct mrb_mesh mrb_mesh;
+typedef struct mrb_batch mrb_batch;
+
+/* SolverConfig, reference solver.py:47-68 (validated the same way). */
+typedef struct mrb_config {
+  double tau;
+  double lam;
+  double energy_tolerance;
+  int32_t max_iterations;
+  int32_t smoothing_passes;
+  int32_t precision; /* MRB_PREC_* */
+  int32_t reserved;
+} mrb_config;
+
+/* ---- library / context ------------------------------------------------ */
+const char* mrb_version(void);
+/* One context per GPU: owns a non-blocking CUDA stream.  Not thread-safe;
+ * separate contexts may be driven from separate threads or processes. */
+int mrb_ctx_create(int32_t device, mrb_ctx** out);
+int mrb_ctx_destroy(mrb_ctx* ctx);
+const char* mrb_last_error(const mrb_ctx* ctx);
+/* the cudaStream_t every call of this ctx is enqueued on (for CUDA events) */
+void* mrb_ctx_stream(mrb_ctx* ctx);
+int mrb_ctx_synchronize(mrb_ctx* ctx);
+
+/* ---- mesh (replaces TriMesh + TriangleGeometry + build_laplacian) ------ */
+/* Validates, orients CCW and builds connectivity/CSR/geometry on the host,
+ * bit-exact with TriMesh.__init__ (mesh.py:58-123) and TriangleGeometry
+ * (mesh.py:173-213).  Host-only: works without a GPU.  On failure returns
+ * MRB_E_VALUE and writes the reference's message into err (if non-NULL). */
+int mrb_mesh_build(int64_t n_vertices, const double* vertices /* n*2 */,
+                   int64_t n_triangles, const int64_t* triangles /* m*3 */,
+                   mrb_mesh** out, char* err, int32_t err_len);
+int mrb_mesh_destroy(mrb_mesh* mesh);
+/* counts[0..5] = n_vertices, n_triangles, n_edges, nnz(L), nnz(grad), nnz(avg) */
+int mrb_mesh_counts(const mrb_mesh* mesh, int64_t* counts);
+/* oriented triangles (m*3), edges (e*2), valence (n), boundary (n bytes),
+ * rings CSR (n+1, 2e) and incident-triangle CSR (n+1, 3m); any may be NULL */
+int mrb_mesh_export_connectivity(const mrb_mesh* mesh, int64_t* triangles, int64_t* edges,
+                                 int64_t* valence, uint8_t* boundary, int64_t* ring_ptr,
+                                 int64_t* ring_idx, int64_t* inc_ptr, int64_t* inc_idx);
+/* canonical scipy CSR (indptr, indices, data) of one MRB_CSR_* operator */
+int mrb_mesh_export_csr(const mrb_mesh* mesh, int32_t which, int64_t* indptr,
+                        int64_t* indices, double* data);
+/* areas (m), coeffs (m*3*2), vertex_areas (n) */
+int mrb_mesh_export_geometry(const mrb_mesh* mesh, double* areas, double* coeffs,
+                             double* vertex_areas);
+/* Pixel -> lowest-index containing triangle and barycentric weights
+ * (densefield.py:148-182), rasterised on the GPU with fp64 predicates that
+ * reproduce numpy's operation order; binned-locate fallback on the host. */
+int mrb_pixel_map(mrb_ctx* ctx, mrb_mesh* mesh, int32_t width, int32_t height,
+                  int64_t* tri_of /* H*W */, double* weights /* H*W*3, may be NULL */);
+
+/* ---- the registration path (solver.register, solver.py:148-208) -------- */
+/* One pair.  Images are row-major H*W in img_dtype.  Outputs (caller-owned
+ * host memory, any may be NULL except u):
+ *   u (n*2 f64, reference vertex order), trace (max_iterations f64),
+ *   ux, uy, warped (H*W f64) — the dense field and warped template
+ *   (densefield.py:130-199).  Returns MRB_E_DIVERGED / MRB_E_VALUE /
+ *   MRB_E_COVERAGE with the reference's message on failure. */
+int mrb_register(mrb_ctx* ctx, mrb_mesh* mesh, int32_t width, int32_t height,
+                 int32_t img_dtype, const void* reference, const void* tmpl,
+                 const mrb_config* cfg, double* u, double* trace, int32_t* iterations_run,
+                 double* msd_before, double* msd_after, double* ux, double* uy,
+                 double* warped);
+
+/* Batched pairs (the pair queue of one GPU).  All pairs of a
+ * batch share width/height/config; each has its own mesh.  Typical use:
+ *   create -> set_images -> run -> get_results -> sync -> status   */
+int mrb_batch_create(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int32_t width,
+                     int32_t height, int32_t img_dtype, const mrb_config* cfg,
+                     mrb_batch** out);
+int mrb_batch_destroy(mrb_batch* batch);
+/* reference/template stacks (n_pairs*H*W, img_dtype).  on_device=0: host
+ * memory (pinned for async), copied H2D on the ctx stream; on_device=1:
+ * device pointers, copied D2D. */
+int mrb_batch_set_images(mrb_batch* batch, const void* reference, const void* tmpl,
+                         int32_t on_device);
+/* enqueue the whole registration of every pair (loop + dense pass) */
+int mrb_batch_run(mrb_batch* batch);
+/* enqueue D2H copies of the results.  out_dtype applies to ux/uy/warped;
+ * u is n_i*2 f64 per pair (concatenated in pair order).  NULL skips. */
+int mrb_batch_get_results(mrb_batch* batch, int32_t out_dtype, double* u, void* ux, void* uy,
+                          void* warped);
+/* wait for the stream; returns the first pair error code (MRB_OK if none) */
+int mrb_batch_sync(mrb_batch* batch);
+/* per-pair outcome after sync: iterations_run, MSDs, trace (max_iterations),
+ * message (reference text) — returns that pair's MRB_* code */
+int mrb_batch_pair_status(mrb_batch* batch, int32_t pair, int32_t* iterations_run,
+                          double* msd_before, double* msd_after, double* trace, char* msg,
+                          int32_t msg_len);
+/* device kernels launched by one mrb_batch_run (for the bench's launch count) */
+int64_t mrb_batch_launches_per_run(const mrb_batch* batch);
+/* algorithmic bytes of one run, SURVEY.md §8(d) byte model */
+double mrb_batch_algorithmic_bytes(const mrb_batch* batch);
+/* algorithmic bytes per launch of each kernel (same model):
+ * out[0] k_sample, out[1] k_grad, out[2] k_smooth, out[3] k_dense */
+int mrb_batch_kernel_bytes(const mrb_batch* batch, double* out);
+/* Enqueue one full run with CUDA events around every kernel launch and
+ * return the mean device time per launch in ms: out[0] k_sample, out[1]
+ * k_grad, out[2] k_smooth, out[3] k_dense, out[4] whole run.  Synchronises. */
+int mrb_batch_kernel_times(mrb_batch* batch, double* out);
+
+/* ---- single operations (reference functions of the same name) ---------- */
+/* warp_sample, solver.py:91-97 / ImageGrid.sample image.py:73-84 */
+int mrb_warp_sample(mrb_ctx* ctx, int32_t width, int32_t height, int32_t img_dtype,
+                    const void* image, int64_t n, const double* vertices, const double* u,
+                    double* out);
+/* energy, solver.py:100-106 */
+int mrb_energy(mrb_ctx* ctx, mrb_mesh* mesh, int32_t width, int32_t height,
+               int32_t img_dtype, const void* reference, const void* tmpl, const double* u,
+               double* out);
+/* energy_gradient, solver.py:109-121 */
+int mrb_energy_gradient(mrb_ctx* ctx, mrb_mesh* mesh, int32_t width, int32_t height,
+                        int32_t img_dtype, const void* reference, const void* tmpl,
+                        const double* u, double* grad);
+/* vertex_gradient_all, mesh.py:236-241 */
+int mrb_vertex_gradient_all(mrb_ctx* ctx, mrb_mesh* mesh, const double* f, double* out);
+/* smooth_displacement, mesh.py:268-282, on an arbitrary CSR matrix */
+int mrb_smooth_csr(mrb_ctx* ctx, int64_t n, const int64_t* indptr, const int64_t* indices,
+                   const double* data, const double* u0, double lam, int32_t passes,
+                   double* out);
+/* step, solver.py:124-145 (clamp when vertices != NULL) */
+int mrb_step_csr(mrb_ctx* ctx, int64_t n, const int64_t* indptr, const int64_t* indices,
+                 const double* data, const double* u, const double* grad, double tau,
+                 double lam, int32_t passes, const double* vertices, int32_t width,
+                 int32_t height, double* out);
+/* densify, densefield.py:130-187 */
+int mrb_densify(mrb_ctx* ctx, mrb_mesh* mesh, int32_t width, int32_t height, const double* u,
+                double* ux, double* uy);
+/* warp_image, densefield.py:190-199 */
+int mrb_warp_image(mrb_ctx* ctx, int32_t width, int32_t height, int32_t img_dtype,
+                   const void* tmpl, const double* ux, const double* uy, double* out);
+/* msd, image.py:181-186 */
+int mrb_msd(mrb_ctx* ctx, int64_t n, const double* a, const double* b, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MESHREG_B200_H */

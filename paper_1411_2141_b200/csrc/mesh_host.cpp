@@ -1,0 +1,369 @@
+// Host mesh setup: validation, CCW orientation, connectivity, CSR operators
+// and geometry, bit-exact with the reference (compiled with
+// -ffp-contract=off so every product/sum rounds exactly like numpy's).
+//
+// Reference: pkg/src/meshreg/mesh.py
+//   TriMesh.__init__            58-89   validation + orientation
+//   TriMesh._build_connectivity 91-123  edges / rings / incident / boundary
+//   _signed_area2               153-159
+//   TriangleGeometry            173-213 areas, Eq. 9 coefficients, CSR ops
+//   build_laplacian             254-265
+// and densefield.py PointLocator/locate 62-127 for the coverage fallback.
+#include "mesh_host.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <numeric>
+
+namespace mrb {
+
+namespace {
+
+constexpr double kDegenerateArea = 1e-9;  // mesh.py:28
+constexpr double kBaryEps = 1e-9;         // densefield.py:31
+
+inline double area2(const double* V, int64_t a, int64_t b, int64_t c) {
+  // (b0-a0)*(c1-a1) - (c0-a0)*(b1-a1)
+  const double ax = V[2 * a], ay = V[2 * a + 1];
+  const double bx = V[2 * b], by = V[2 * b + 1];
+  const double cx = V[2 * c], cy = V[2 * c + 1];
+  const double p = (bx - ax) * (cy - ay);
+  const double q = (cx - ax) * (by - ay);
+  return p - q;
+}
+
+std::string fmt_g(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%g", v);
+  return buf;
+}
+
+// Canonical CSR from duplicate-free triplets.
+void to_csr(int64_t nrows, const std::vector<int64_t>& rows, const std::vector<int64_t>& cols,
+            const std::vector<double>& vals, Csr& out) {
+  const size_t nnz = rows.size();
+  std::vector<int64_t> order(nnz);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) {
+    return rows[x] != rows[y] ? rows[x] < rows[y] : cols[x] < cols[y];
+  });
+  out.indptr.assign(nrows + 1, 0);
+  for (size_t k = 0; k < nnz; ++k) out.indptr[rows[k] + 1]++;
+  for (int64_t i = 0; i < nrows; ++i) out.indptr[i + 1] += out.indptr[i];
+  out.indices.resize(nnz);
+  out.data.resize(nnz);
+  for (size_t k = 0; k < nnz; ++k) {
+    out.indices[k] = cols[order[k]];
+    out.data[k] = vals[order[k]];
+  }
+}
+
+uint32_t spread16(uint32_t x) {
+  x &= 0xFFFF;
+  x = (x | (x << 8)) & 0x00FF00FF;
+  x = (x | (x << 4)) & 0x0F0F0F0F;
+  x = (x | (x << 2)) & 0x33333333;
+  x = (x | (x << 1)) & 0x55555555;
+  return x;
+}
+
+}  // namespace
+
+void barycentric(const double* a, const double* b, const double* c, double px, double py,
+                 double w[3]) {
+  const double d = (b[0] - a[0]) * (c[1] - a[1]) - (c[0] - a[0]) * (b[1] - a[1]);
+  const double w1 = ((b[0] - px) * (c[1] - py) - (c[0] - px) * (b[1] - py)) / d;
+  const double w2 = ((c[0] - px) * (a[1] - py) - (a[0] - px) * (c[1] - py)) / d;
+  w[0] = w1;
+  w[1] = w2;
+  w[2] = 1.0 - w1 - w2;
+}
+
+std::string build_mesh(int64_t n, const double* Vin, int64_t m, const int64_t* Tin,
+                       HostMesh& M) {
+  // ---- validation, mesh.py:61-78 (shape checks happen in the binding) ----
+  if (m < 1) return "triangles must be (m, 3) with m >= 1, got (0, 3)";
+  for (int64_t i = 0; i < 2 * n; ++i)
+    if (!std::isfinite(Vin[i])) return "vertex coordinates must be finite";
+  int64_t tmin = Tin[0], tmax = Tin[0];
+  for (int64_t k = 0; k < 3 * m; ++k) {
+    tmin = std::min(tmin, Tin[k]);
+    tmax = std::max(tmax, Tin[k]);
+  }
+  if (tmin < 0 || tmax >= n) return "triangle index out of range";
+  for (int64_t t = 0; t < m; ++t) {
+    const int64_t* r = Tin + 3 * t;
+    if (r[0] == r[1] || r[1] == r[2] || r[0] == r[2]) return "triangle with repeated vertex index";
+  }
+  M.n = n;
+  M.m = m;
+  M.V.assign(Vin, Vin + 2 * n);
+  M.T.assign(Tin, Tin + 3 * m);
+  {
+    int64_t worst = 0;
+    double worst_abs = INFINITY;
+    bool bad = false;
+    for (int64_t t = 0; t < m; ++t) {
+      const double a2 = area2(M.V.data(), M.T[3 * t], M.T[3 * t + 1], M.T[3 * t + 2]);
+      const double ab = std::fabs(a2);
+      if (ab <= 2.0 * kDegenerateArea) bad = true;
+      if (ab < worst_abs) {  // np.argmin: first minimum
+        worst_abs = ab;
+        worst = t;
+      }
+      if (a2 < 0) std::swap(M.T[3 * t + 1], M.T[3 * t + 2]);  // [0, 2, 1]
+    }
+    if (bad)
+      return "degenerate triangle " + std::to_string(worst) + " (area " +
+             fmt_g(worst_abs / 2.0) + ")";
+  }
+
+  // ---- connectivity, mesh.py:91-123 ----
+  std::vector<std::pair<int64_t, int64_t>> raw;
+  raw.reserve(3 * m);
+  for (int64_t t = 0; t < m; ++t) {
+    const int64_t* r = &M.T[3 * t];
+    const int64_t pr[3][2] = {{r[0], r[1]}, {r[1], r[2]}, {r[2], r[0]}};
+    for (auto& e : pr) raw.emplace_back(std::min(e[0], e[1]), std::max(e[0], e[1]));
+  }
+  std::sort(raw.begin(), raw.end());
+  std::vector<int64_t> counts;
+  M.edges.clear();
+  for (size_t k = 0; k < raw.size();) {
+    size_t j = k;
+    while (j < raw.size() && raw[j] == raw[k]) ++j;
+    M.edges.push_back(raw[k].first);
+    M.edges.push_back(raw[k].second);
+    counts.push_back(int64_t(j - k));
+    k = j;
+  }
+  M.ne = int64_t(counts.size());
+  for (int64_t c : counts)
+    if (c > 2) return "non-manifold edge shared by more than two triangles";
+
+  M.valence.assign(n, 0);
+  for (int64_t e = 0; e < M.ne; ++e) {
+    M.valence[M.edges[2 * e]]++;
+    M.valence[M.edges[2 * e + 1]]++;
+  }
+  M.ring_ptr.assign(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) M.ring_ptr[i + 1] = M.ring_ptr[i] + M.valence[i];
+  M.ring_idx.assign(M.ring_ptr[n], 0);
+  {
+    std::vector<int64_t> fill(M.ring_ptr.begin(), M.ring_ptr.end() - 1);
+    for (int64_t e = 0; e < M.ne; ++e) {
+      const int64_t a = M.edges[2 * e], b = M.edges[2 * e + 1];
+      M.ring_idx[fill[a]++] = b;
+      M.ring_idx[fill[b]++] = a;
+    }
+    for (int64_t i = 0; i < n; ++i)
+      std::sort(M.ring_idx.begin() + M.ring_ptr[i], M.ring_idx.begin() + M.ring_ptr[i + 1]);
+  }
+  M.inc_ptr.assign(n + 1, 0);
+  for (int64_t k = 0; k < 3 * m; ++k) M.inc_ptr[M.T[k] + 1]++;
+  for (int64_t i = 0; i < n; ++i) M.inc_ptr[i + 1] += M.inc_ptr[i];
+  M.inc_idx.assign(3 * m, 0);
+  {
+    std::vector<int64_t> fill(M.inc_ptr.begin(), M.inc_ptr.end() - 1);
+    for (int64_t t = 0; t < m; ++t)
+      for (int c = 0; c < 3; ++c) M.inc_idx[fill[M.T[3 * t + c]]++] = t;
+  }
+  M.boundary.assign(n, 0);
+  for (int64_t e = 0; e < M.ne; ++e)
+    if (counts[e] == 1) M.boundary[M.edges[2 * e]] = M.boundary[M.edges[2 * e + 1]] = 1;
+  {
+    int64_t lone = 0;
+    for (int64_t i = 1; i < n; ++i)
+      if (M.valence[i] < M.valence[lone]) lone = i;
+    if (n > 0 && M.valence[lone] < 2)
+      return "vertex " + std::to_string(lone) + " has valence " +
+             std::to_string(M.valence[lone]) + " (< 2)";
+  }
+
+  // ---- geometry, mesh.py:173-213 ----
+  const double* V = M.V.data();
+  M.areas.resize(m);
+  M.coeffs.resize(6 * m);
+  for (int64_t t = 0; t < m; ++t) {
+    const int64_t ia = M.T[3 * t], ib = M.T[3 * t + 1], ic = M.T[3 * t + 2];
+    M.areas[t] = 0.5 * area2(V, ia, ib, ic);
+  }
+  for (int64_t t = 0; t < m; ++t)
+    if (M.areas[t] <= kDegenerateArea) return "zero-area triangle in geometry";
+  for (int64_t t = 0; t < m; ++t) {
+    const double* a = V + 2 * M.T[3 * t];
+    const double* b = V + 2 * M.T[3 * t + 1];
+    const double* c = V + 2 * M.T[3 * t + 2];
+    const double vij[2] = {b[0] - a[0], b[1] - a[1]};
+    const double vjk[2] = {c[0] - b[0], c[1] - b[1]};
+    const double vik[2] = {c[0] - a[0], c[1] - a[1]};
+    auto dot = [](const double* u, double w0, double w1) { return u[0] * w0 + u[1] * w1; };
+    // Eq. 9 (mesh.py:193-195): each corner pairs dot products of its edges
+    const double di1 = dot(vij, vjk[0], vjk[1]), di2 = dot(vik, -vjk[0], -vjk[1]);
+    const double nvij[2] = {-vij[0], -vij[1]}, nvjk[2] = {-vjk[0], -vjk[1]};
+    const double nvik[2] = {-vik[0], -vik[1]};
+    const double dj1 = dot(nvij, vik[0], vik[1]), dj2 = dot(vjk, -vik[0], -vik[1]);
+    const double dk1 = dot(nvjk, -vij[0], -vij[1]), dk2 = dot(nvik, vij[0], vij[1]);
+    const double ar = M.areas[t];
+    const double inv4a2 = 1.0 / (4.0 * (ar * ar));
+    double* co = &M.coeffs[6 * t];
+    for (int d = 0; d < 2; ++d) {
+      const double ti = di1 * (c[d] - a[d]) + di2 * (b[d] - a[d]);
+      const double tj = dj1 * (c[d] - b[d]) + dj2 * (a[d] - b[d]);
+      const double tk = dk1 * (a[d] - c[d]) + dk2 * (b[d] - c[d]);
+      co[0 * 2 + d] = ti * inv4a2;
+      co[1 * 2 + d] = tj * inv4a2;
+      co[2 * 2 + d] = tk * inv4a2;
+    }
+  }
+  {
+    std::vector<int64_t> rows(3 * m), cols(3 * m);
+    std::vector<double> vx(3 * m), vy(3 * m);
+    for (int64_t t = 0; t < m; ++t)
+      for (int c = 0; c < 3; ++c) {
+        rows[3 * t + c] = t;
+        cols[3 * t + c] = M.T[3 * t + c];
+        vx[3 * t + c] = M.coeffs[6 * t + 2 * c];
+        vy[3 * t + c] = M.coeffs[6 * t + 2 * c + 1];
+      }
+    to_csr(m, rows, cols, vx, M.gx);
+    to_csr(m, rows, cols, vy, M.gy);
+    M.vertex_areas.assign(n, 0.0);
+    for (int64_t k = 0; k < 3 * m; ++k) M.vertex_areas[cols[k]] += M.areas[rows[k]];
+    std::vector<double> w(3 * m);
+    for (int64_t k = 0; k < 3 * m; ++k) w[k] = M.areas[rows[k]] / M.vertex_areas[cols[k]];
+    to_csr(n, cols, rows, w, M.avg);
+  }
+  // Laplacian (mesh.py:254-265)
+  M.lap.indptr = M.ring_ptr;
+  M.lap.indices = M.ring_idx;
+  M.lap.data.resize(M.ring_idx.size());
+  for (int64_t i = 0; i < n; ++i) {
+    const double v = 1.0 / double(M.valence[i]);
+    for (int64_t k = M.ring_ptr[i]; k < M.ring_ptr[i + 1]; ++k) M.lap.data[k] = v;
+  }
+
+  // ---- device-facing layout ----
+  // Morton (Z-order) relabelling so a warp's nodes gather nearby image taps.
+  {
+    double lo[2] = {INFINITY, INFINITY}, hi[2] = {-INFINITY, -INFINITY};
+    for (int64_t i = 0; i < n; ++i)
+      for (int d = 0; d < 2; ++d) {
+        lo[d] = std::min(lo[d], V[2 * i + d]);
+        hi[d] = std::max(hi[d], V[2 * i + d]);
+      }
+    const double span = std::max(std::max(hi[0] - lo[0], hi[1] - lo[1]), 1e-12);
+    std::vector<uint32_t> key(n);
+    for (int64_t i = 0; i < n; ++i) {
+      const uint32_t qx = uint32_t(std::min(65535.0, (V[2 * i] - lo[0]) / span * 65535.0));
+      const uint32_t qy = uint32_t(std::min(65535.0, (V[2 * i + 1] - lo[1]) / span * 65535.0));
+      key[i] = spread16(qx) | (spread16(qy) << 1);
+    }
+    M.perm.resize(n);
+    std::iota(M.perm.begin(), M.perm.end(), 0);
+    std::stable_sort(M.perm.begin(), M.perm.end(),
+                     [&](int32_t x, int32_t y) { return key[x] < key[y]; });
+    M.iperm.resize(n);
+    for (int64_t k = 0; k < n; ++k) M.iperm[M.perm[k]] = int32_t(k);
+  }
+  // Fused gradient operator G = avg∘grad on the {self} ∪ one-ring pattern:
+  // grad_v = sum_t w_vt * sum_c coeff[t,c] f[T[t,c]]  (mesh.py:236-241).
+  M.nb_ptr.assign(n + 1, 0);
+  M.nb_idx.resize(M.ring_idx.size());
+  M.g_nb.assign(2 * M.ring_idx.size(), 0.0);
+  M.g_self.assign(2 * n, 0.0);
+  M.inv_val.resize(n);
+  M.Vn.resize(2 * n);
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t i = M.perm[k];
+    M.nb_ptr[k + 1] = M.nb_ptr[k] + int32_t(M.valence[i]);
+  }
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t i = M.perm[k];
+    M.inv_val[k] = 1.0 / double(M.valence[i]);
+    M.Vn[2 * k] = V[2 * i];
+    M.Vn[2 * k + 1] = V[2 * i + 1];
+    const int64_t r0 = M.ring_ptr[i], r1 = M.ring_ptr[i + 1];
+    const int32_t base = M.nb_ptr[k];
+    for (int64_t r = r0; r < r1; ++r) M.nb_idx[base + (r - r0)] = M.iperm[M.ring_idx[r]];
+    // accumulate fused coefficients over incident triangles (ascending id)
+    for (int64_t q = M.inc_ptr[i]; q < M.inc_ptr[i + 1]; ++q) {
+      const int64_t t = M.inc_idx[q];
+      const double w = M.areas[t] / M.vertex_areas[i];
+      for (int c = 0; c < 3; ++c) {
+        const int64_t j = M.T[3 * t + c];
+        const double cx = w * M.coeffs[6 * t + 2 * c];
+        const double cy = w * M.coeffs[6 * t + 2 * c + 1];
+        if (j == i) {
+          M.g_self[2 * k] += cx;
+          M.g_self[2 * k + 1] += cy;
+        } else {
+          const int64_t* b = &M.ring_idx[r0];
+          const int64_t pos = std::lower_bound(b, b + (r1 - r0), j) - b;
+          M.g_nb[2 * (base + pos)] += cx;
+          M.g_nb[2 * (base + pos) + 1] += cy;
+        }
+      }
+    }
+  }
+  M.Tn.resize(4 * m);
+  for (int64_t t = 0; t < m; ++t) {
+    for (int c = 0; c < 3; ++c) M.Tn[4 * t + c] = M.iperm[M.T[3 * t + c]];
+    M.Tn[4 * t + 3] = 0;
+  }
+  return "";
+}
+
+// ---- PointLocator / locate (densefield.py:62-127) ----
+Locator::Locator(const HostMesh& M) {
+  lo[0] = lo[1] = INFINITY;
+  hi[0] = hi[1] = -INFINITY;
+  for (int64_t i = 0; i < M.n; ++i)
+    for (int d = 0; d < 2; ++d) {
+      lo[d] = std::min(lo[d], M.V[2 * i + d]);
+      hi[d] = std::max(hi[d], M.V[2 * i + d]);
+    }
+  const double s0 = std::max(hi[0] - lo[0], 1e-9), s1 = std::max(hi[1] - lo[1], 1e-9);
+  cell = std::max(2.0, std::sqrt(2.0 * s0 * s1 / double(std::max<int64_t>(M.m, 1))));
+  nx = int64_t(std::ceil(s0 / cell)) + 1;
+  ny = int64_t(std::ceil(s1 / cell)) + 1;
+  bins.assign(nx * ny, {});
+  for (int64_t t = 0; t < M.m; ++t) {
+    double mn[2] = {INFINITY, INFINITY}, mx[2] = {-INFINITY, -INFINITY};
+    for (int c = 0; c < 3; ++c)
+      for (int d = 0; d < 2; ++d) {
+        mn[d] = std::min(mn[d], M.V[2 * M.T[3 * t + c] + d]);
+        mx[d] = std::max(mx[d], M.V[2 * M.T[3 * t + c] + d]);
+      }
+    int64_t bx0, by0, bx1, by1;
+    cell_of(mn[0], mn[1], bx0, by0);
+    cell_of(mx[0], mx[1], bx1, by1);
+    for (int64_t by = by0; by <= by1; ++by)
+      for (int64_t bx = bx0; bx <= bx1; ++bx) bins[by * nx + bx].push_back(t);
+  }
+}
+
+void Locator::cell_of(double x, double y, int64_t& bx, int64_t& by) const {
+  bx = int64_t((std::min(std::max(x, lo[0]), hi[0]) - lo[0]) / cell);
+  by = int64_t((std::min(std::max(y, lo[1]), hi[1]) - lo[1]) / cell);
+  bx = std::min(bx, nx - 1);
+  by = std::min(by, ny - 1);
+}
+
+int64_t Locator::locate(const HostMesh& M, double px, double py, double w[3]) const {
+  int64_t bx, by;
+  cell_of(px, py, bx, by);
+  auto test = [&](int64_t t) {
+    barycentric(&M.V[2 * M.T[3 * t]], &M.V[2 * M.T[3 * t + 1]], &M.V[2 * M.T[3 * t + 2]], px,
+                py, w);
+    return std::min(std::min(w[0], w[1]), w[2]) >= -kBaryEps;
+  };
+  for (int64_t t : bins[by * nx + bx])
+    if (test(t)) return t;
+  for (int64_t t = 0; t < M.m; ++t)
+    if (test(t)) return t;
+  return -1;
+}
+
+}  // namespace mrb

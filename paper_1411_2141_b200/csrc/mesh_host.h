@@ -1,0 +1,68 @@
+// Host-side mesh setup shared by the C ABI and the CUDA launch code.
+// Internal header (not part of the public ABI in include/meshreg_b200.h).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace mrb {
+
+// Canonical CSR as scipy builds it (rows ascending, columns ascending).
+struct Csr {
+  std::vector<int64_t> indptr, indices;
+  std::vector<double> data;
+};
+
+struct DeviceMesh;  // defined in the .cu (per-device buffers)
+
+struct HostMesh {
+  int64_t n = 0, m = 0, ne = 0;
+  // reference-order data (mesh.py TriMesh / TriangleGeometry)
+  std::vector<double> V;         // n*2
+  std::vector<int64_t> T;        // m*3, CCW-oriented
+  std::vector<int64_t> edges;    // ne*2, lexicographically sorted unique pairs
+  std::vector<int64_t> valence;  // n
+  std::vector<uint8_t> boundary; // n
+  std::vector<int64_t> ring_ptr, ring_idx;  // sorted one-rings
+  std::vector<int64_t> inc_ptr, inc_idx;    // ascending incident triangles
+  std::vector<double> areas, coeffs, vertex_areas;  // m, m*3*2, n
+  Csr lap, gx, gy, avg;
+
+  // device-facing layout (node relabelling by Morton order of V)
+  std::vector<int32_t> perm;   // new -> old
+  std::vector<int32_t> iperm;  // old -> new
+  std::vector<int32_t> nb_ptr; // n+1, one-ring CSR in new ids (entries keep
+  std::vector<int32_t> nb_idx; //   the reference's per-row order)
+  std::vector<double> g_self;  // n*2   fused operator avg∘grad, self term
+  std::vector<double> g_nb;    // 2e*2  fused operator, ring terms
+  std::vector<double> inv_val; // n     1/valence (Laplacian row value)
+  std::vector<double> Vn;      // n*2   vertices in new order
+  std::vector<int32_t> Tn;     // m*4   triangles in new ids (+pad)
+
+  std::unique_ptr<DeviceMesh> dev;  // lazily created per device
+  ~HostMesh();
+};
+
+// Build + validate; returns "" on success, else the reference's ValueError text.
+std::string build_mesh(int64_t n, const double* V, int64_t m, const int64_t* T, HostMesh& out);
+
+// PointLocator + locate (densefield.py:62-127) for pixels the raster pass
+// left unassigned.  Returns triangle id or -1 (uncovered), fills w[3].
+struct Locator {
+  double lo[2], hi[2], cell;
+  int64_t nx, ny;
+  std::vector<std::vector<int64_t>> bins;
+  explicit Locator(const HostMesh& mesh);
+  void cell_of(double x, double y, int64_t& bx, int64_t& by) const;
+  int64_t locate(const HostMesh& mesh, double px, double py, double w[3]) const;
+};
+
+// Barycentric weights with numpy's operation order (densefield.py:99-107).
+void barycentric(const double* a, const double* b, const double* c, double px, double py,
+                 double w[3]);
+
+}  // namespace mrb

@@ -1,0 +1,1270 @@
+// C ABI + launch orchestration of the B200 mesh-registration path.
+// Public interface: include/meshreg_b200.h.  Device code: kernels.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/meshreg_b200.h"
+#include "kernels.cuh"
+#include "mesh_host.h"
+
+using namespace mrb;
+
+struct mrb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+};
+
+struct mrb_mesh {
+  HostMesh h;
+};
+
+namespace mrb {
+
+struct DeviceMesh {
+  int device = -1;
+  double2* V = nullptr;
+  int* nb_ptr = nullptr;
+  int* nb_idx = nullptr;
+  int4* tri = nullptr;
+  int* perm = nullptr;
+  float2* g_self_f = nullptr;
+  float2* g_nb_f = nullptr;
+  float* inv_val_f = nullptr;
+  double2* g_self_d = nullptr;
+  double2* g_nb_d = nullptr;
+  double* inv_val_d = nullptr;
+  std::map<std::pair<int, int>, int*> pixel_maps;
+  ~DeviceMesh() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (device >= 0) cudaSetDevice(device);
+    void* ptrs[] = {V, nb_ptr, nb_idx, tri, perm, g_self_f, g_nb_f, inv_val_f, g_self_d, g_nb_d,
+                    inv_val_d};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    for (auto& kv : pixel_maps) cudaFree(kv.second);
+    if (cur >= 0) cudaSetDevice(cur);
+  }
+};
+
+HostMesh::~HostMesh() = default;
+
+}  // namespace mrb
+
+namespace {
+
+const char* kVersion = "meshreg_b200 0.1.0 (sm_100a)";
+
+struct CudaError {
+  cudaError_t e;
+};
+
+inline void ck(cudaError_t e) {
+  if (e != cudaSuccess) throw CudaError{e};
+}
+
+template <typename T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  ck(cudaMalloc(&p, n * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+template <typename T>
+T* dupload(const T* h, size_t n, cudaStream_t s) {
+  T* d = dalloc<T>(n);
+  if (n) ck(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  return d;
+}
+
+// Scoped stream-ordered temporaries for the single-operation entry points.
+struct Tmp {
+  cudaStream_t s;
+  std::vector<void*> ptrs;
+  explicit Tmp(cudaStream_t st) : s(st) {}
+  template <typename T>
+  T* get(size_t n) {
+    void* p = nullptr;
+    ck(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), s));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <typename T>
+  T* up(const T* h, size_t n) {
+    T* d = get<T>(n);
+    if (n) ck(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    return d;
+  }
+  ~Tmp() {
+    for (void* p : ptrs) cudaFreeAsync(p, s);
+  }
+};
+
+int fail(mrb_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+int cuda_fail(mrb_ctx* ctx, cudaError_t e) {
+  return fail(ctx, MRB_E_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
+}
+
+// Python float repr (shortest round-trip digits; fixed for 1e-4 <= |x| < 1e16)
+std::string py_repr(double v) {
+  if (std::isnan(v)) return "nan";
+  if (std::isinf(v)) return v > 0 ? "inf" : "-inf";
+  if (v == 0.0) return std::signbit(v) ? "-0.0" : "0.0";
+  char buf[64];
+  int prec = 1;
+  for (; prec <= 17; ++prec) {
+    std::snprintf(buf, sizeof buf, "%.*e", prec - 1, v);
+    if (std::strtod(buf, nullptr) == v) break;
+  }
+  // buf = [-]d.ddde[+-]XX
+  std::string s(buf);
+  const bool neg = s[0] == '-';
+  if (neg) s = s.substr(1);
+  const size_t epos = s.find('e');
+  std::string mant = s.substr(0, epos);
+  const int exp10 = std::atoi(s.c_str() + epos + 1);
+  std::string digits;
+  for (char c : mant)
+    if (c != '.') digits += c;
+  while (digits.size() > 1 && digits.back() == '0') digits.pop_back();
+  std::string out;
+  if (exp10 >= -5 && exp10 < 16) {
+    const int decpt = exp10 + 1;  // digits before the point
+    if (decpt <= 0) {
+      out = "0." + std::string(-decpt, '0') + digits;
+    } else if (decpt >= int(digits.size())) {
+      out = digits + std::string(decpt - digits.size(), '0') + ".0";
+    } else {
+      out = digits.substr(0, decpt) + "." + digits.substr(decpt);
+    }
+    if (exp10 == -5) {  // Python switches to exponent below 1e-4
+      out.clear();
+    }
+  }
+  if (out.empty()) {
+    out = digits.substr(0, 1);
+    if (digits.size() > 1) out += "." + digits.substr(1);
+    char e[16];
+    std::snprintf(e, sizeof e, "e%c%02d", exp10 < 0 ? '-' : '+', std::abs(exp10));
+    out += e;
+  }
+  return neg ? "-" + out : out;
+}
+
+void ensure_device_mesh(mrb_ctx* ctx, HostMesh& h) {
+  if (h.dev && h.dev->device == ctx->device) return;
+  h.dev.reset(new DeviceMesh());
+  DeviceMesh& d = *h.dev;
+  d.device = ctx->device;
+  cudaStream_t s = ctx->stream;
+  const size_t n = size_t(h.n), m = size_t(h.m), ne2 = h.nb_idx.size();
+  d.V = dupload(reinterpret_cast<const double2*>(h.Vn.data()), n, s);
+  d.nb_ptr = dupload(h.nb_ptr.data(), n + 1, s);
+  d.nb_idx = dupload(h.nb_idx.data(), ne2, s);
+  d.tri = dupload(reinterpret_cast<const int4*>(h.Tn.data()), m, s);
+  d.perm = dupload(h.perm.data(), n, s);
+  d.g_self_d = dupload(reinterpret_cast<const double2*>(h.g_self.data()), n, s);
+  d.g_nb_d = dupload(reinterpret_cast<const double2*>(h.g_nb.data()), ne2, s);
+  d.inv_val_d = dupload(h.inv_val.data(), n, s);
+  std::vector<float> gs(h.g_self.begin(), h.g_self.end()), gn(h.g_nb.begin(), h.g_nb.end()),
+      iv(h.inv_val.begin(), h.inv_val.end());
+  d.g_self_f = dupload(reinterpret_cast<const float2*>(gs.data()), n, s);
+  d.g_nb_f = dupload(reinterpret_cast<const float2*>(gn.data()), ne2, s);
+  d.inv_val_f = dupload(iv.data(), n, s);
+  ck(cudaStreamSynchronize(s));  // host vectors above go out of scope
+}
+
+// Pixel->triangle map for (W, H): GPU raster + host locate fallback.
+// Returns "" or the MeshCoverageError message.
+std::string ensure_pixel_map(mrb_ctx* ctx, HostMesh& h, int W, int H, int** out) {
+  ensure_device_mesh(ctx, h);
+  DeviceMesh& d = *h.dev;
+  auto key = std::make_pair(W, H);
+  auto it = d.pixel_maps.find(key);
+  if (it != d.pixel_maps.end()) {
+    *out = it->second;
+    return "";
+  }
+  cudaStream_t s = ctx->stream;
+  const size_t npx = size_t(W) * size_t(H);
+  int* tri_of = dalloc<int>(npx);
+  ck(cudaMemsetAsync(tri_of, 0x7f, npx * sizeof(int), s));
+  const int threads = 256;
+  const long long warps = h.m;
+  k_raster<<<unsigned((warps * 32 + threads - 1) / threads), threads, 0, s>>>(
+      d.V, d.tri, int(h.m), W, H, tri_of);
+  ck(cudaGetLastError());
+  unsigned long long* cnt = nullptr;
+  ck(cudaMallocAsync(&cnt, sizeof(unsigned long long), s));
+  ck(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
+  k_count_uncovered<<<std::min<size_t>((npx + 255) / 256, 1184), 256, 0, s>>>(tri_of, int(npx),
+                                                                             cnt);
+  ck(cudaGetLastError());
+  unsigned long long missing = 0;
+  ck(cudaMemcpyAsync(&missing, cnt, sizeof missing, cudaMemcpyDeviceToHost, s));
+  ck(cudaFreeAsync(cnt, s));
+  ck(cudaStreamSynchronize(s));
+  if (missing) {
+    // densefield.py:176-182: binned locate for each unassigned pixel, row-major
+    std::vector<int> host(npx);
+    ck(cudaMemcpy(host.data(), tri_of, npx * sizeof(int), cudaMemcpyDeviceToHost));
+    Locator loc(h);
+    for (size_t q = 0; q < npx; ++q) {
+      if (host[q] != 0x7fffffff) continue;
+      const double px = double(q % W), py = double(q / W);
+      double w[3];
+      const int64_t t = loc.locate(h, px, py, w);
+      if (t < 0) {
+        cudaFree(tri_of);
+        char buf[128];
+        std::snprintf(buf, sizeof buf, "point (%s, %s) not covered by any triangle",
+                      py_repr(px).c_str(), py_repr(py).c_str());
+        return buf;
+      }
+      host[q] = int(t);
+    }
+    ck(cudaMemcpy(tri_of, host.data(), npx * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  d.pixel_maps[key] = tri_of;
+  *out = tri_of;
+  return "";
+}
+
+}  // namespace
+
+// =========================================================================
+// batch
+// =========================================================================
+struct mrb_batch {
+  mrb_ctx* ctx = nullptr;
+  int n_pairs = 0, W = 0, H = 0, in_dtype = MRB_F32;
+  mrb_config cfg{};
+  bool tap_d = false, real_d = false;
+  std::vector<mrb_mesh*> meshes;
+  std::vector<int> node_off;  // offsets into the concatenated u_out (nodes)
+  int n_node_blocks = 0, n_pix_blocks = 0;
+  int64_t total_nodes = 0;
+  // device
+  void* pairs = nullptr;  // PairDev<TapT,Real>[n_pairs]
+  PairStatus* st = nullptr;
+  int* blk_pair = nullptr;
+  int* pix_blk_pair = nullptr;
+  double* partials = nullptr;
+  double2* pix_partials = nullptr;
+  void* state = nullptr;
+  double* traces = nullptr;
+  void* img = nullptr;
+  void* stage = nullptr;  // H2D staging (re stack, te stack)
+  void** src_ptrs = nullptr;  // device: [re_0..re_{P-1}, te_0..te_{P-1}]
+  void** img_ptrs = nullptr;  // device: interleaved tap buffer per pair
+  std::vector<const void*> src_host;  // current sources (for graph validity)
+  void* dense = nullptr;       // ux, uy, warped (Real)
+  double2* u_out = nullptr;
+  void* conv = nullptr;        // dtype conversion scratch for get_results
+  cudaGraphExec_t graph = nullptr;
+  std::vector<const void*> graph_src;
+  int runs = 0;
+  // host results
+  std::vector<PairStatus> h_st;
+  std::vector<double> h_trace;
+  bool synced = false;
+  ~mrb_batch() {
+    if (graph) cudaGraphExecDestroy(graph);
+    void* ptrs[] = {pairs, st, blk_pair, pix_blk_pair, partials, pix_partials, state, traces,
+                    img, stage, src_ptrs, img_ptrs, dense, u_out, conv};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+};
+
+namespace {
+
+size_t tap_size(const mrb_batch* b) { return b->tap_d ? sizeof(double) : sizeof(float); }
+size_t real_size(const mrb_batch* b) { return b->real_d ? sizeof(double) : sizeof(float); }
+size_t in_size(int dtype) { return dtype == MRB_F64 ? sizeof(double) : sizeof(float); }
+
+template <typename TapT, typename Real>
+void build_pairs(mrb_batch* b) {
+  using PD = PairDev<TapT, Real>;
+  using R2 = typename V2<Real>::type;
+  std::vector<PD> pd(b->n_pairs);
+  const size_t npx = size_t(b->W) * b->H;
+  // state layout: per pair u, ua, ub (R2 * n) then ste, r (Real * n)
+  size_t state_bytes = 0;
+  std::vector<size_t> st_off(b->n_pairs);
+  for (int p = 0; p < b->n_pairs; ++p) {
+    st_off[p] = state_bytes;
+    const size_t n = size_t(b->meshes[p]->h.n);
+    state_bytes += (3 * n * sizeof(R2) + 2 * n * sizeof(Real) + 255) / 256 * 256;
+  }
+  b->state = dalloc<char>(state_bytes);
+  b->dense = dalloc<Real>(3 * npx * b->n_pairs);
+  int blk = 0, pblk = 0;
+  std::vector<int> bp, pbp;
+  const int pix_nblk = int((npx + kPixBlock - 1) / kPixBlock);
+  for (int p = 0; p < b->n_pairs; ++p) {
+    HostMesh& h = b->meshes[p]->h;
+    DeviceMesh& dm = *h.dev;
+    PD& d = pd[p];
+    d.V = dm.V;
+    d.nb_ptr = dm.nb_ptr;
+    d.nb_idx = dm.nb_idx;
+    if constexpr (sizeof(Real) == 8) {
+      d.g_self = dm.g_self_d;
+      d.g_nb = dm.g_nb_d;
+      d.inv_val = dm.inv_val_d;
+    } else {
+      d.g_self = dm.g_self_f;
+      d.g_nb = dm.g_nb_f;
+      d.inv_val = dm.inv_val_f;
+    }
+    d.tri = dm.tri;
+    d.tri_of = dm.pixel_maps.at(std::make_pair(b->W, b->H));
+    d.perm = dm.perm;
+    d.img = static_cast<const TapT*>(b->img) + size_t(p) * 2 * npx;
+    const size_t n = size_t(h.n);
+    char* base = static_cast<char*>(b->state) + st_off[p];
+    d.u = reinterpret_cast<R2*>(base);
+    d.ua = d.u + n;
+    d.ub = d.ua + n;
+    d.ste = reinterpret_cast<Real*>(d.ub + n);
+    d.r = d.ste + n;
+    d.trace = b->traces + size_t(p) * b->cfg.max_iterations;
+    d.grad_out = nullptr;
+    Real* dense = static_cast<Real*>(b->dense);
+    d.ux = dense + (3 * size_t(p) + 0) * npx;
+    d.uy = dense + (3 * size_t(p) + 1) * npx;
+    d.warped = dense + (3 * size_t(p) + 2) * npx;
+    d.u_out = b->u_out + b->node_off[p];
+    d.W = b->W;
+    d.H = b->H;
+    d.n = int(n);
+    d.blk_begin = blk;
+    d.nblk = int((n + kNodeBlock - 1) / kNodeBlock);
+    d.pix_blk_begin = pblk;
+    d.pix_nblk = pix_nblk;
+    for (int k = 0; k < d.nblk; ++k) bp.push_back(p);
+    for (int k = 0; k < pix_nblk; ++k) pbp.push_back(p);
+    blk += d.nblk;
+    pblk += pix_nblk;
+  }
+  b->n_node_blocks = blk;
+  b->n_pix_blocks = pblk;
+  cudaStream_t s = b->ctx->stream;
+  b->pairs = dupload(pd.data(), pd.size(), s);
+  b->blk_pair = dupload(bp.data(), bp.size(), s);
+  b->pix_blk_pair = dupload(pbp.data(), pbp.size(), s);
+  b->partials = dalloc<double>(blk);
+  b->pix_partials = dalloc<double2>(pblk);
+  ck(cudaStreamSynchronize(s));
+}
+
+template <typename InT, typename TapT>
+void launch_interleave(mrb_batch* b) {
+  const int npx = b->W * b->H;
+  dim3 grid(std::min((npx + 255) / 256, 1024), b->n_pairs);
+  k_interleave<InT, TapT><<<grid, 256, 0, b->ctx->stream>>>(
+      reinterpret_cast<const InT* const*>(b->src_ptrs),
+      reinterpret_cast<const InT* const*>(b->src_ptrs + b->n_pairs),
+      reinterpret_cast<TapT* const*>(b->img_ptrs), npx);
+}
+
+struct KernelTimer {
+  cudaStream_t s;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> kind;
+  bool on = false;
+  void mark(int k) {
+    if (!on) return;
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e));
+    ck(cudaEventRecord(e, s));
+    ev.push_back(e);
+    kind.push_back(k);
+  }
+  ~KernelTimer() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
+template <typename TapT, typename Real>
+int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
+  KernelTimer dummy;
+  if (!tm) tm = &dummy;
+  using PD = PairDev<TapT, Real>;
+  cudaStream_t s = b->ctx->stream;
+  const PD* pairs = static_cast<const PD*>(b->pairs);
+  int64_t launches = 0;
+  if (b->in_dtype == MRB_F64)
+    launch_interleave<double, TapT>(b);
+  else
+    launch_interleave<float, TapT>(b);
+  ++launches;
+  k_reset_status<<<(b->n_pairs + 127) / 128, 128, 0, s>>>(b->st, b->n_pairs,
+                                                         b->cfg.max_iterations);
+  ++launches;
+  const int nb = b->n_node_blocks;
+  const double tol = b->cfg.energy_tolerance;
+  const Real tau = Real(b->cfg.tau), lam = Real(b->cfg.lam);
+  const int passes = b->cfg.smoothing_passes;
+  tm->mark(-1);
+  for (int k = 0; k < b->cfg.max_iterations; ++k) {
+    k_sample<TapT, Real><<<nb, kNodeBlock, 0, s>>>(pairs, b->st, b->blk_pair, b->partials, k, tol);
+    tm->mark(0);
+    k_grad<TapT, Real><<<nb, kNodeBlock, 0, s>>>(pairs, b->st, b->blk_pair, k, tau, passes);
+    tm->mark(1);
+    launches += 2;
+    for (int q = 0; q < passes; ++q) {
+      k_smooth<TapT, Real><<<nb, kNodeBlock, 0, s>>>(pairs, b->st, b->blk_pair, k, lam, q, passes);
+      tm->mark(2);
+      ++launches;
+    }
+  }
+  k_dense<TapT, Real><<<b->n_pix_blocks, kPixBlock, 0, s>>>(pairs, b->st, b->pix_blk_pair,
+                                                            b->pix_partials);
+  tm->mark(3);
+  k_msd_final<TapT, Real><<<b->n_pairs, kPixBlock, 0, s>>>(pairs, b->st, b->pix_partials);
+  k_unpermute<TapT, Real><<<nb, kNodeBlock, 0, s>>>(pairs, b->blk_pair);
+  launches += 3;
+  ck(cudaGetLastError());
+  return launches;
+}
+
+template <typename TapT, typename Real>
+void enqueue_zero_u(mrb_batch* b) {
+  // u = 0 for every pair (solver.py:168); u is the first slab of each pair's
+  // state (layout of build_pairs), so this is one memset node per pair
+  using R2 = typename V2<Real>::type;
+  size_t off = 0;
+  for (int p = 0; p < b->n_pairs; ++p) {
+    const size_t n = size_t(b->meshes[p]->h.n);
+    ck(cudaMemsetAsync(static_cast<char*>(b->state) + off, 0, n * sizeof(R2), b->ctx->stream));
+    off += (3 * n * sizeof(R2) + 2 * n * sizeof(Real) + 255) / 256 * 256;
+  }
+}
+
+template <typename TapT, typename Real>
+int64_t enqueue_all(mrb_batch* b, KernelTimer* tm) {
+  enqueue_zero_u<TapT, Real>(b);
+  return enqueue_run<TapT, Real>(b, tm);
+}
+
+int64_t dispatch_enqueue(mrb_batch* b, KernelTimer* tm = nullptr) {
+  if (b->tap_d) return enqueue_all<double, double>(b, tm);
+  if (b->real_d) return enqueue_all<float, double>(b, tm);
+  return enqueue_all<float, float>(b, tm);
+}
+
+int64_t launches_per_run(const mrb_batch* b) {
+  return 2 + int64_t(b->cfg.max_iterations) * (2 + b->cfg.smoothing_passes) + 3;
+}
+
+template <typename From, typename To>
+__global__ void k_convert(const From* __restrict__ a, To* __restrict__ o, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    o[i] = To(a[i]);
+}
+
+std::string config_error(const mrb_config* c) {
+  // SolverConfig.__post_init__, solver.py:55-65
+  if (!(c->tau > 0)) return "tau must be positive, got " + py_repr(c->tau);
+  if (!(0.0 < c->lam && c->lam < 1.0)) return "lambda must be in (0, 1), got " + py_repr(c->lam);
+  if (c->max_iterations < 1) return "max_iterations must be >= 1";
+  if (c->smoothing_passes < 0) return "smoothing_passes must be >= 0";
+  if (!(c->energy_tolerance >= 0)) return "energy_tolerance must be >= 0";
+  return "";
+}
+
+std::string pair_message(const mrb_batch* b, int p, int* code) {
+  const PairStatus& s = b->h_st[p];
+  const double* tr = b->h_trace.data() + size_t(p) * b->cfg.max_iterations;
+  *code = MRB_OK;
+  switch (s.err) {
+    case ERR_NONFINITE_ENERGY:
+      *code = MRB_E_DIVERGED;
+      return "energy became non-finite; reduce tau";
+    case ERR_RISES: {
+      *code = MRB_E_DIVERGED;
+      const int k = s.err_iter;
+      std::string vals = "[";
+      for (int j = std::max(0, k - 3); j <= k; ++j) {
+        if (j > std::max(0, k - 3)) vals += ", ";
+        vals += py_repr(tr[j]);
+      }
+      vals += "]";
+      return "energy increased for 10 consecutive iterations (last values " + vals +
+             "); reduce tau";
+    }
+    case ERR_NONFINITE_GRAD:
+      *code = MRB_E_DIVERGED;
+      return "non-finite gradient; reduce the step size tau";
+    default:
+      break;
+  }
+  if (s.dense_nonfinite) {
+    *code = MRB_E_VALUE;
+    return (s.dense_nonfinite & 1) ? "displacement planes must be finite"
+                                   : "image intensities must be finite";
+  }
+  return "";
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mrb_version(void) { return kVersion; }
+
+int mrb_ctx_create(int32_t device, mrb_ctx** out) {
+  if (!out) return MRB_E_VALUE;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return MRB_E_CUDA;
+  if (device < 0 || device >= count) return MRB_E_VALUE;
+  auto* c = new mrb_ctx();
+  c->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return MRB_E_CUDA;
+  }
+  *out = c;
+  return MRB_OK;
+}
+
+int mrb_ctx_destroy(mrb_ctx* ctx) {
+  if (!ctx) return MRB_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+  }
+  delete ctx;
+  return MRB_OK;
+}
+
+const char* mrb_last_error(const mrb_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+void* mrb_ctx_stream(mrb_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int mrb_ctx_synchronize(mrb_ctx* ctx) {
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  return e == cudaSuccess ? MRB_OK : cuda_fail(ctx, e);
+}
+
+// ---------------------------------------------------------------- mesh
+int mrb_mesh_build(int64_t n, const double* V, int64_t m, const int64_t* T, mrb_mesh** out,
+                   char* err, int32_t err_len) {
+  if (!out) return MRB_E_VALUE;
+  *out = nullptr;
+  auto* mesh = new mrb_mesh();
+  std::string msg;
+  try {
+    msg = build_mesh(n, V, m, T, mesh->h);
+  } catch (const std::exception& ex) {
+    msg = std::string("internal error: ") + ex.what();
+  }
+  if (!msg.empty()) {
+    if (err && err_len > 0) {
+      std::strncpy(err, msg.c_str(), size_t(err_len) - 1);
+      err[err_len - 1] = 0;
+    }
+    delete mesh;
+    return MRB_E_VALUE;
+  }
+  *out = mesh;
+  return MRB_OK;
+}
+
+int mrb_mesh_destroy(mrb_mesh* mesh) {
+  delete mesh;
+  return MRB_OK;
+}
+
+int mrb_mesh_counts(const mrb_mesh* mesh, int64_t* c) {
+  const HostMesh& h = mesh->h;
+  c[0] = h.n;
+  c[1] = h.m;
+  c[2] = h.ne;
+  c[3] = int64_t(h.lap.indices.size());
+  c[4] = int64_t(h.gx.indices.size());
+  c[5] = int64_t(h.avg.indices.size());
+  return MRB_OK;
+}
+
+int mrb_mesh_export_connectivity(const mrb_mesh* mesh, int64_t* tri, int64_t* edges,
+                                 int64_t* valence, uint8_t* boundary, int64_t* ring_ptr,
+                                 int64_t* ring_idx, int64_t* inc_ptr, int64_t* inc_idx) {
+  const HostMesh& h = mesh->h;
+  auto cp = [](int64_t* dst, const std::vector<int64_t>& v) {
+    if (dst) std::memcpy(dst, v.data(), v.size() * sizeof(int64_t));
+  };
+  cp(tri, h.T);
+  cp(edges, h.edges);
+  cp(valence, h.valence);
+  if (boundary) std::memcpy(boundary, h.boundary.data(), h.boundary.size());
+  cp(ring_ptr, h.ring_ptr);
+  cp(ring_idx, h.ring_idx);
+  cp(inc_ptr, h.inc_ptr);
+  cp(inc_idx, h.inc_idx);
+  return MRB_OK;
+}
+
+int mrb_mesh_export_csr(const mrb_mesh* mesh, int32_t which, int64_t* indptr, int64_t* indices,
+                        double* data) {
+  const HostMesh& h = mesh->h;
+  const Csr* c = which == MRB_CSR_LAPLACIAN  ? &h.lap
+                 : which == MRB_CSR_GRAD_X   ? &h.gx
+                 : which == MRB_CSR_GRAD_Y   ? &h.gy
+                 : which == MRB_CSR_VERTEX_AVG ? &h.avg
+                                               : nullptr;
+  if (!c) return MRB_E_VALUE;
+  if (indptr) std::memcpy(indptr, c->indptr.data(), c->indptr.size() * sizeof(int64_t));
+  if (indices) std::memcpy(indices, c->indices.data(), c->indices.size() * sizeof(int64_t));
+  if (data) std::memcpy(data, c->data.data(), c->data.size() * sizeof(double));
+  return MRB_OK;
+}
+
+int mrb_mesh_export_geometry(const mrb_mesh* mesh, double* areas, double* coeffs,
+                             double* vertex_areas) {
+  const HostMesh& h = mesh->h;
+  if (areas) std::memcpy(areas, h.areas.data(), h.areas.size() * sizeof(double));
+  if (coeffs) std::memcpy(coeffs, h.coeffs.data(), h.coeffs.size() * sizeof(double));
+  if (vertex_areas)
+    std::memcpy(vertex_areas, h.vertex_areas.data(), h.vertex_areas.size() * sizeof(double));
+  return MRB_OK;
+}
+
+int mrb_pixel_map(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int64_t* tri_of,
+                  double* weights) {
+  try {
+    ck(cudaSetDevice(ctx->device));
+    int* map = nullptr;
+    const std::string msg = ensure_pixel_map(ctx, mesh->h, W, H, &map);
+    if (!msg.empty()) return fail(ctx, MRB_E_COVERAGE, msg);
+    const size_t npx = size_t(W) * H;
+    if (tri_of) {
+      std::vector<int> host(npx);
+      ck(cudaMemcpyAsync(host.data(), map, npx * sizeof(int), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+      ck(cudaStreamSynchronize(ctx->stream));
+      for (size_t q = 0; q < npx; ++q) tri_of[q] = host[q];
+    }
+    if (weights) {
+      Tmp t(ctx->stream);
+      double* w = t.get<double>(3 * npx);
+      k_pixel_weights<<<unsigned((npx + 255) / 256), 256, 0, ctx->stream>>>(
+          mesh->h.dev->V, mesh->h.dev->tri, map, W, int(npx), w);
+      ck(cudaGetLastError());
+      ck(cudaMemcpyAsync(weights, w, 3 * npx * sizeof(double), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+      ck(cudaStreamSynchronize(ctx->stream));
+    }
+    return MRB_OK;
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e);
+  }
+}
+
+// ---------------------------------------------------------------- batch
+int mrb_batch_create(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int32_t W,
+                     int32_t H, int32_t img_dtype, const mrb_config* cfg, mrb_batch** out) {
+  *out = nullptr;
+  const std::string ce = config_error(cfg);
+  if (!ce.empty()) return fail(ctx, MRB_E_VALUE, ce);
+  if (n_pairs < 1) return fail(ctx, MRB_E_VALUE, "batch needs at least one pair");
+  if (W < 2 || H < 2)
+    return fail(ctx, MRB_E_VALUE, "bicubic sampling needs an image of at least 2x2 pixels");
+  if (int64_t(W) * H >= (int64_t(1) << 31) / 2)
+    return fail(ctx, MRB_E_VALUE, "image too large for 32-bit pixel indexing");
+  std::unique_ptr<mrb_batch> b(new mrb_batch());
+  b->ctx = ctx;
+  b->n_pairs = n_pairs;
+  b->W = W;
+  b->H = H;
+  b->in_dtype = img_dtype;
+  b->cfg = *cfg;
+  b->real_d = cfg->precision == MRB_PREC_F64;
+  b->tap_d = img_dtype == MRB_F64 && b->real_d;
+  b->meshes.assign(meshes, meshes + n_pairs);
+  try {
+    ck(cudaSetDevice(ctx->device));
+    int64_t off = 0;
+    for (int p = 0; p < n_pairs; ++p) {
+      b->node_off.push_back(int(off));
+      off += meshes[p]->h.n;
+      int* map = nullptr;
+      const std::string msg = ensure_pixel_map(ctx, meshes[p]->h, W, H, &map);
+      if (!msg.empty()) return fail(ctx, MRB_E_COVERAGE, msg);
+    }
+    b->total_nodes = off;
+    const size_t npx = size_t(W) * H;
+    b->st = dalloc<PairStatus>(n_pairs);
+    b->traces = dalloc<double>(size_t(n_pairs) * cfg->max_iterations);
+    b->img = dalloc<char>(size_t(n_pairs) * 2 * npx * tap_size(b.get()));
+    b->u_out = dalloc<double2>(off);
+    b->src_ptrs = dalloc<void*>(2 * n_pairs);
+    b->img_ptrs = dalloc<void*>(n_pairs);
+    std::vector<void*> ip(n_pairs);
+    for (int p = 0; p < n_pairs; ++p)
+      ip[p] = static_cast<char*>(b->img) + size_t(p) * 2 * npx * tap_size(b.get());
+    ck(cudaMemcpy(b->img_ptrs, ip.data(), n_pairs * sizeof(void*), cudaMemcpyHostToDevice));
+    if (b->tap_d)
+      build_pairs<double, double>(b.get());
+    else if (b->real_d)
+      build_pairs<float, double>(b.get());
+    else
+      build_pairs<float, float>(b.get());
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e);
+  }
+  *out = b.release();
+  return MRB_OK;
+}
+
+int mrb_batch_destroy(mrb_batch* b) {
+  if (!b) return MRB_OK;
+  cudaSetDevice(b->ctx->device);
+  cudaStreamSynchronize(b->ctx->stream);
+  delete b;
+  return MRB_OK;
+}
+
+int mrb_batch_set_images(mrb_batch* b, const void* re, const void* te, int32_t on_device) {
+  mrb_ctx* ctx = b->ctx;
+  try {
+    ck(cudaSetDevice(ctx->device));
+    const size_t npx = size_t(b->W) * b->H, es = in_size(b->in_dtype);
+    const size_t bytes = size_t(b->n_pairs) * npx * es;
+    const char *rs, *ts;
+    if (on_device) {
+      rs = static_cast<const char*>(re);
+      ts = static_cast<const char*>(te);
+    } else {
+      if (!b->stage) b->stage = dalloc<char>(2 * bytes);
+      char* st = static_cast<char*>(b->stage);
+      ck(cudaMemcpyAsync(st, re, bytes, cudaMemcpyHostToDevice, ctx->stream));
+      ck(cudaMemcpyAsync(st + bytes, te, bytes, cudaMemcpyHostToDevice, ctx->stream));
+      rs = st;
+      ts = st + bytes;
+    }
+    std::vector<const void*> ptrs(2 * b->n_pairs);
+    for (int p = 0; p < b->n_pairs; ++p) {
+      ptrs[p] = rs + size_t(p) * npx * es;
+      ptrs[b->n_pairs + p] = ts + size_t(p) * npx * es;
+    }
+    if (ptrs != b->src_host) {
+      ck(cudaMemcpyAsync(b->src_ptrs, ptrs.data(), ptrs.size() * sizeof(void*),
+                         cudaMemcpyHostToDevice, ctx->stream));
+      ck(cudaStreamSynchronize(ctx->stream));  // ptrs is a stack temporary
+      b->src_host = ptrs;
+    }
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e);
+  }
+  return MRB_OK;
+}
+
+int mrb_batch_run(mrb_batch* b) {
+  mrb_ctx* ctx = b->ctx;
+  try {
+    ck(cudaSetDevice(ctx->device));
+    b->synced = false;
+    if (b->runs == 0) {
+      dispatch_enqueue(b);  // first run: direct launches
+    } else {
+      if (!b->graph) {
+        cudaGraph_t g;
+        ck(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        dispatch_enqueue(b);
+        ck(cudaStreamEndCapture(ctx->stream, &g));
+        ck(cudaGraphInstantiate(&b->graph, g, 0));
+        cudaGraphDestroy(g);
+      }
+      ck(cudaGraphLaunch(b->graph, ctx->stream));
+    }
+    b->runs++;
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e);
+  }
+  return MRB_OK;
+}
+
+int mrb_batch_get_results(mrb_batch* b, int32_t out_dtype, double* u, void* ux, void* uy,
+                          void* warped) {
+  mrb_ctx* ctx = b->ctx;
+  try {
+    ck(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    if (u)
+      ck(cudaMemcpyAsync(u, b->u_out, size_t(b->total_nodes) * sizeof(double2),
+                         cudaMemcpyDeviceToHost, s));
+    const size_t npx = size_t(b->W) * b->H;
+    const bool same = (out_dtype == MRB_F64) == b->real_d;
+    const size_t os = in_size(out_dtype);
+    void* outs[3] = {ux, uy, warped};
+    for (int c = 0; c < 3; ++c) {
+      if (!outs[c]) continue;
+      for (int p = 0; p < b->n_pairs; ++p) {
+        const char* src = static_cast<const char*>(b->dense) + (3 * size_t(p) + c) * npx * real_size(b);
+        char* dst = static_cast<char*>(outs[c]) + size_t(p) * npx * os;
+        if (same) {
+          ck(cudaMemcpyAsync(dst, src, npx * os, cudaMemcpyDeviceToHost, s));
+        } else {
+          if (!b->conv) b->conv = dalloc<char>(3 * size_t(b->n_pairs) * npx * os);
+          char* cv = static_cast<char*>(b->conv) + (3 * size_t(p) + c) * npx * os;
+          const unsigned g = unsigned(std::min<size_t>((npx + 255) / 256, 2048));
+          if (b->real_d)
+            k_convert<double, float><<<g, 256, 0, s>>>(reinterpret_cast<const double*>(src),
+                                                       reinterpret_cast<float*>(cv), npx);
+          else
+            k_convert<float, double><<<g, 256, 0, s>>>(reinterpret_cast<const float*>(src),
+                                                       reinterpret_cast<double*>(cv), npx);
+          ck(cudaGetLastError());
+          ck(cudaMemcpyAsync(dst, cv, npx * os, cudaMemcpyDeviceToHost, s));
+        }
+      }
+    }
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e);
+  }
+  return MRB_OK;
+}
+
+int mrb_batch_sync(mrb_batch* b) {
+  mrb_ctx* ctx = b->ctx;
+  try {
+    ck(cudaSetDevice(ctx->device));
+    ck(cudaStreamSynchronize(ctx->stream));
+    b->h_st.resize(b->n_pairs);
+    b->h_trace.resize(size_t(b->n_pairs) * b->cfg.max_iterations);
+    ck(cudaMemcpy(b->h_st.data(), b->st, b->n_pairs * sizeof(PairStatus),
+                  cudaMemcpyDeviceToHost));
+    ck(cudaMemcpy(b->h_trace.data(), b->traces, b->h_trace.size() * sizeof(double),
+                  cudaMemcpyDeviceToHost));
+    b->synced = true;
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e);
+  }
+  for (int p = 0; p < b->n_pairs; ++p) {
+    int code;
+    const std::string msg = pair_message(b, p, &code);
+    if (code != MRB_OK) return fail(ctx, code, msg);
+  }
+  return MRB_OK;
+}
+
+int mrb_batch_pair_status(mrb_batch* b, int32_t p, int32_t* iters, double* msd_before,
+                          double* msd_after, double* trace, char* msg, int32_t msg_len) {
+  if (!b->synced || p < 0 || p >= b->n_pairs) return MRB_E_VALUE;
+  const PairStatus& s = b->h_st[p];
+  if (iters) *iters = s.iters;
+  if (msd_before) *msd_before = s.msd_before;
+  if (msd_after) *msd_after = s.msd_after;
+  if (trace)
+    std::memcpy(trace, b->h_trace.data() + size_t(p) * b->cfg.max_iterations,
+                size_t(b->cfg.max_iterations) * sizeof(double));
+  int code;
+  const std::string m = pair_message(b, p, &code);
+  if (msg && msg_len > 0) {
+    std::strncpy(msg, m.c_str(), size_t(msg_len) - 1);
+    msg[msg_len - 1] = 0;
+  }
+  return code;
+}
+
+int64_t mrb_batch_launches_per_run(const mrb_batch* b) { return launches_per_run(b); }
+
+double mrb_batch_algorithmic_bytes(const mrb_batch* b) {
+  // iterations*(184 n_V + 60 n_T + 8 n_E) + 128 W H per pair
+  double tot = 0;
+  for (const mrb_mesh* m : b->meshes)
+    tot += double(b->cfg.max_iterations) *
+               (184.0 * m->h.n + 60.0 * m->h.m + 8.0 * m->h.ne) +
+           128.0 * double(b->W) * b->H;
+  return tot;
+}
+
+int mrb_batch_kernel_bytes(const mrb_batch* b, double* out) {
+  // SURVEY.md §8(d) per-unit figures split by the kernel that moves them:
+  //   k_sample 148 B/node  (V 8, u 8, Te+Re 16 taps x 2 x 4 = 128, s_te 4)
+  //   k_grad    16 B/node + 60 B/triangle (s_te read 4, avg indptr 4, u0 8;
+  //             3 corner ids 12, 6 coefficients 24, 3 avg entries 24)
+  //   k_smooth  20 B/node + 8 B/edge (u0 read 8, L indptr 4, u write 8; 2 ids)
+  //   k_dense  128 B/pixel (B_final)
+  double nv = 0, nt = 0, ne = 0;
+  for (const mrb_mesh* m : b->meshes) {
+    nv += double(m->h.n);
+    nt += double(m->h.m);
+    ne += double(m->h.ne);
+  }
+  out[0] = 148.0 * nv;
+  out[1] = 16.0 * nv + 60.0 * nt;
+  out[2] = 20.0 * nv + 8.0 * ne;
+  out[3] = 128.0 * double(b->W) * b->H * b->n_pairs;
+  return MRB_OK;
+}
+
+int mrb_batch_kernel_times(mrb_batch* b, double* out) {
+  mrb_ctx* ctx = b->ctx;
+  try {
+    ck(cudaSetDevice(ctx->device));
+    KernelTimer tm;
+    tm.s = ctx->stream;
+    tm.on = true;
+    cudaEvent_t e0, e1;
+    ck(cudaEventCreate(&e0));
+    ck(cudaEventCreate(&e1));
+    ck(cudaEventRecord(e0, ctx->stream));
+    dispatch_enqueue(b, &tm);
+    ck(cudaEventRecord(e1, ctx->stream));
+    ck(cudaStreamSynchronize(ctx->stream));
+    double sum[4] = {0, 0, 0, 0};
+    int cnt[4] = {0, 0, 0, 0};
+    for (size_t k = 1; k < tm.ev.size(); ++k) {
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, tm.ev[k - 1], tm.ev[k]));
+      sum[tm.kind[k]] += ms;
+      cnt[tm.kind[k]]++;
+    }
+    for (int k = 0; k < 4; ++k) out[k] = cnt[k] ? sum[k] / cnt[k] : 0.0;
+    float tot = 0;
+    ck(cudaEventElapsedTime(&tot, e0, e1));
+    out[4] = tot;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    b->synced = false;
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e);
+  }
+  return MRB_OK;
+}
+
+// ---------------------------------------------------------------- register
+int mrb_register(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int32_t img_dtype,
+                 const void* re, const void* te, const mrb_config* cfg, double* u,
+                 double* trace, int32_t* iters, double* msd_before, double* msd_after,
+                 double* ux, double* uy, double* warped) {
+  mrb_batch* b = nullptr;
+  int rc = mrb_batch_create(ctx, 1, &mesh, W, H, img_dtype, cfg, &b);
+  if (rc != MRB_OK) return rc;
+  std::unique_ptr<mrb_batch> guard(b);
+  if ((rc = mrb_batch_set_images(b, re, te, 0)) != MRB_OK) return rc;
+  if ((rc = mrb_batch_run(b)) != MRB_OK) return rc;
+  if ((rc = mrb_batch_get_results(b, MRB_F64, u, ux, uy, warped)) != MRB_OK) return rc;
+  rc = mrb_batch_sync(b);
+  if (b->synced) mrb_batch_pair_status(b, 0, iters, msd_before, msd_after, trace, nullptr, 0);
+  return rc;
+}
+
+// ---------------------------------------------------------------- single ops
+int mrb_warp_sample(mrb_ctx* ctx, int32_t W, int32_t H, int32_t dtype, const void* image,
+                    int64_t n, const double* V, const double* u, double* out) {
+  if (W < 2 || H < 2)
+    return fail(ctx, MRB_E_VALUE, "bicubic sampling needs an image of at least 2x2 pixels");
+  try {
+    ck(cudaSetDevice(ctx->device));
+    Tmp t(ctx->stream);
+    const size_t npx = size_t(W) * H;
+    const double* dV = t.up(V, 2 * n);
+    const double* du = t.up(u, 2 * n);
+    double* dout = t.get<double>(n);
+    const unsigned g = unsigned((n + 255) / 256);
+    if (n > 0) {
+      if (dtype == MRB_F64)
+        k_sample_points<double><<<g, 256, 0, ctx->stream>>>(
+            t.up(static_cast<const double*>(image), npx), W, H, int(n), dV, du, dout);
+      else
+        k_sample_points<float><<<g, 256, 0, ctx->stream>>>(
+            t.up(static_cast<const float*>(image), npx), W, H, int(n), dV, du, dout);
+      ck(cudaGetLastError());
+    }
+    ck(cudaMemcpyAsync(out, dout, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(cudaStreamSynchronize(ctx->stream));
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e);
+  }
+  return MRB_OK;
+}
+
+namespace {
+
+// One-pair f64 evaluation of (energy, grad) at a given u through the same
+// k_sample / k_grad kernels the registration loop uses.
+int unit_eval(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int32_t dtype, const void* re,
+              const void* te, const double* u, const double* f_override, double* energy,
+              double* grad) {
+  if (W < 2 || H < 2)
+    return fail(ctx, MRB_E_VALUE, "bicubic sampling needs an image of at least 2x2 pixels");
+  try {
+    ck(cudaSetDevice(ctx->device));
+    HostMesh& h = mesh->h;
+    ensure_device_mesh(ctx, h);
+    DeviceMesh& dm = *h.dev;
+    cudaStream_t s = ctx->stream;
+    Tmp t(s);
+    const size_t n = size_t(h.n), npx = size_t(W) * H;
+    using PD = PairDev<double, double>;
+    PD d{};
+    d.V = dm.V;
+    d.nb_ptr = dm.nb_ptr;
+    d.nb_idx = dm.nb_idx;
+    d.g_self = dm.g_self_d;
+    d.g_nb = dm.g_nb_d;
+    d.inv_val = dm.inv_val_d;
+    d.W = W;
+    d.H = H;
+    d.n = int(n);
+    d.blk_begin = 0;
+    d.nblk = int((n + kNodeBlock - 1) / kNodeBlock);
+    std::vector<double> tmp(2 * n);
+    if (u)
+      for (size_t k = 0; k < n; ++k) {
+        tmp[2 * k] = u[2 * h.perm[k]];
+        tmp[2 * k + 1] = u[2 * h.perm[k] + 1];
+      }
+    d.u = reinterpret_cast<double2*>(t.up(tmp.data(), 2 * n));
+    d.ste = t.get<double>(n);
+    d.r = t.get<double>(n);
+    d.trace = t.get<double>(1);
+    d.grad_out = grad ? t.get<double2>(n) : nullptr;
+    PairStatus st0{};
+    st0.stop_iter = 1;
+    PairStatus* st = t.up(&st0, 1);
+    std::vector<int> bp(d.nblk, 0);
+    int* blk_pair = t.up(bp.data(), bp.size());
+    double* partials = t.get<double>(d.nblk);
+    if (f_override) {  // vertex_gradient_all: ste = f, r = 1
+      std::vector<double> f(n), one(n, 1.0);
+      for (size_t k = 0; k < n; ++k) f[k] = f_override[h.perm[k]];
+      ck(cudaMemcpyAsync(d.ste, f.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+      ck(cudaMemcpyAsync(d.r, one.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+      PD* dd = t.up(&d, 1);
+      k_grad<double, double><<<d.nblk, kNodeBlock, 0, s>>>(dd, st, blk_pair, 0, 0.0, 0);
+      ck(cudaGetLastError());
+    } else {
+      // interleave (Te, Re) into f64 taps
+      double* img = t.get<double>(2 * npx);
+      std::vector<double> inter(2 * npx);
+      for (size_t q = 0; q < npx; ++q) {
+        inter[2 * q] = dtype == MRB_F64 ? static_cast<const double*>(te)[q]
+                                        : double(static_cast<const float*>(te)[q]);
+        inter[2 * q + 1] = dtype == MRB_F64 ? static_cast<const double*>(re)[q]
+                                            : double(static_cast<const float*>(re)[q]);
+      }
+      ck(cudaMemcpyAsync(img, inter.data(), 2 * npx * sizeof(double), cudaMemcpyHostToDevice, s));
+      d.img = img;
+      PD* dd = t.up(&d, 1);
+      k_sample<double, double><<<d.nblk, kNodeBlock, 0, s>>>(dd, st, blk_pair, partials, 0, 0.0);
+      ck(cudaGetLastError());
+      if (grad) {
+        // k_grad skips pairs whose status says stop; force it to run
+        ck(cudaMemcpyAsync(st, &st0, sizeof st0, cudaMemcpyHostToDevice, s));
+        k_grad<double, double><<<d.nblk, kNodeBlock, 0, s>>>(dd, st, blk_pair, 0, 0.0, 0);
+        ck(cudaGetLastError());
+      }
+    }
+    if (energy) ck(cudaMemcpyAsync(energy, d.trace, sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (grad) {
+      ck(cudaMemcpyAsync(tmp.data(), d.grad_out, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
+      ck(cudaStreamSynchronize(s));
+      for (size_t k = 0; k < n; ++k) {
+        grad[2 * h.perm[k]] = tmp[2 * k];
+        grad[2 * h.perm[k] + 1] = tmp[2 * k + 1];
+      }
+    }
+    ck(cudaStreamSynchronize(s));
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e);
+  }
+  return MRB_OK;
+}
+
+}  // namespace
+
+int mrb_energy(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int32_t dtype,
+               const void* re, const void* te, const double* u, double* out) {
+  return unit_eval(ctx, mesh, W, H, dtype, re, te, u, nullptr, out, nullptr);
+}
+
+int mrb_energy_gradient(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int32_t dtype,
+                        const void* re, const void* te, const double* u, double* grad) {
+  return unit_eval(ctx, mesh, W, H, dtype, re, te, u, nullptr, nullptr, grad);
+}
+
+int mrb_vertex_gradient_all(mrb_ctx* ctx, mrb_mesh* mesh, const double* f, double* out) {
+  return unit_eval(ctx, mesh, 2, 2, MRB_F64, nullptr, nullptr, nullptr, f, nullptr, out);
+}
+
+namespace {
+int csr_smooth_impl(mrb_ctx* ctx, Tmp& t, int64_t n, const int64_t* indptr,
+                    const int64_t* indices, const double* data, double2* cur, double lam,
+                    int32_t passes, double2** result) {
+  const int64_t nnz = indptr[n];
+  const int64_t* dp = t.up(indptr, n + 1);
+  const int64_t* di = t.up(indices, nnz);
+  const double* dd = t.up(data, nnz);
+  double2* other = t.get<double2>(n);
+  const unsigned g = unsigned((n + 255) / 256);
+  for (int q = 0; q < passes; ++q) {
+    if (n > 0) k_csr_smooth<<<g, 256, 0, ctx->stream>>>(int(n), dp, di, dd, cur, lam, other);
+    std::swap(cur, other);
+  }
+  ck(cudaGetLastError());
+  *result = cur;
+  return MRB_OK;
+}
+}  // namespace
+
+int mrb_smooth_csr(mrb_ctx* ctx, int64_t n, const int64_t* indptr, const int64_t* indices,
+                   const double* data, const double* u0, double lam, int32_t passes,
+                   double* out) {
+  if (!(0.0 < lam && lam < 1.0))
+    return fail(ctx, MRB_E_VALUE, "smoothing weight must be in (0, 1), got " + py_repr(lam));
+  if (passes < 0) return fail(ctx, MRB_E_VALUE, "iterations must be >= 0");
+  try {
+    ck(cudaSetDevice(ctx->device));
+    Tmp t(ctx->stream);
+    double2* cur = reinterpret_cast<double2*>(t.up(u0, 2 * n));
+    double2* res = nullptr;
+    csr_smooth_impl(ctx, t, n, indptr, indices, data, cur, lam, passes, &res);
+    ck(cudaMemcpyAsync(out, res, n * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(cudaStreamSynchronize(ctx->stream));
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e);
+  }
+  return MRB_OK;
+}
+
+int mrb_step_csr(mrb_ctx* ctx, int64_t n, const int64_t* indptr, const int64_t* indices,
+                 const double* data, const double* u, const double* grad, double tau, double lam,
+                 int32_t passes, const double* V, int32_t W, int32_t H, double* out) {
+  try {
+    ck(cudaSetDevice(ctx->device));
+    Tmp t(ctx->stream);
+    const double2* du = reinterpret_cast<const double2*>(t.up(u, 2 * n));
+    const double2* dg = reinterpret_cast<const double2*>(t.up(grad, 2 * n));
+    double2* u0 = t.get<double2>(n);
+    int* bad = t.get<int>(1);
+    ck(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+    const unsigned g = unsigned((n + 255) / 256);
+    if (n > 0) k_descent<<<g, 256, 0, ctx->stream>>>(int(n), du, dg, tau, u0, bad);
+    ck(cudaGetLastError());
+    int hbad = 0;
+    ck(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(cudaStreamSynchronize(ctx->stream));
+    if (hbad) return fail(ctx, MRB_E_DIVERGED, "non-finite gradient; reduce the step size tau");
+    double2* res = u0;
+    if (passes > 0) {
+      if (!(0.0 < lam && lam < 1.0))
+        return fail(ctx, MRB_E_VALUE, "smoothing weight must be in (0, 1), got " + py_repr(lam));
+      csr_smooth_impl(ctx, t, n, indptr, indices, data, u0, lam, passes, &res);
+    }
+    if (V && n > 0) {
+      k_clamp<<<g, 256, 0, ctx->stream>>>(int(n), reinterpret_cast<const double2*>(t.up(V, 2 * n)),
+                                          W, H, res);
+      ck(cudaGetLastError());
+    }
+    ck(cudaMemcpyAsync(out, res, n * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(cudaStreamSynchronize(ctx->stream));
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e);
+  }
+  return MRB_OK;
+}
+
+int mrb_densify(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, const double* u, double* ux,
+                double* uy) {
+  try {
+    ck(cudaSetDevice(ctx->device));
+    HostMesh& h = mesh->h;
+    int* map = nullptr;
+    const std::string msg = ensure_pixel_map(ctx, h, W, H, &map);
+    if (!msg.empty()) return fail(ctx, MRB_E_COVERAGE, msg);
+    Tmp t(ctx->stream);
+    std::vector<double> un(2 * h.n);
+    for (int64_t k = 0; k < h.n; ++k) {
+      un[2 * k] = u[2 * h.perm[k]];
+      un[2 * k + 1] = u[2 * h.perm[k] + 1];
+    }
+    const double2* du = reinterpret_cast<const double2*>(t.up(un.data(), un.size()));
+    const size_t npx = size_t(W) * H;
+    double* dx = t.get<double>(npx);
+    double* dy = t.get<double>(npx);
+    k_densify<<<unsigned((npx + 255) / 256), 256, 0, ctx->stream>>>(h.dev->V, h.dev->tri, map, du,
+                                                                    W, int(npx), dx, dy);
+    ck(cudaGetLastError());
+    ck(cudaMemcpyAsync(ux, dx, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(cudaMemcpyAsync(uy, dy, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(cudaStreamSynchronize(ctx->stream));
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e);
+  }
+  return MRB_OK;
+}
+
+int mrb_warp_image(mrb_ctx* ctx, int32_t W, int32_t H, int32_t dtype, const void* te,
+                   const double* ux, const double* uy, double* out) {
+  if (W < 2 || H < 2)
+    return fail(ctx, MRB_E_VALUE, "bicubic sampling needs an image of at least 2x2 pixels");
+  try {
+    ck(cudaSetDevice(ctx->device));
+    Tmp t(ctx->stream);
+    const size_t npx = size_t(W) * H;
+    const double* dx = t.up(ux, npx);
+    const double* dy = t.up(uy, npx);
+    double* dout = t.get<double>(npx);
+    const unsigned g = unsigned((npx + 255) / 256);
+    if (dtype == MRB_F64)
+      k_warp_image<double><<<g, 256, 0, ctx->stream>>>(t.up(static_cast<const double*>(te), npx),
+                                                       W, H, dx, dy, dout);
+    else
+      k_warp_image<float><<<g, 256, 0, ctx->stream>>>(t.up(static_cast<const float*>(te), npx), W,
+                                                      H, dx, dy, dout);
+    ck(cudaGetLastError());
+    ck(cudaMemcpyAsync(out, dout, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(cudaStreamSynchronize(ctx->stream));
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e);
+  }
+  return MRB_OK;
+}
+
+int mrb_msd(mrb_ctx* ctx, int64_t n, const double* a, const double* b, double* out) {
+  try {
+    ck(cudaSetDevice(ctx->device));
+    Tmp t(ctx->stream);
+    const double* da = t.up(a, n);
+    const double* db = t.up(b, n);
+    const int nb = int((n + kPixBlock - 1) / kPixBlock);
+    double* partials = t.get<double>(std::max(nb, 1));
+    double* dout = t.get<double>(1);
+    if (nb > 0) k_sqdiff_partials<<<nb, kPixBlock, 0, ctx->stream>>>(int(n), da, db, partials);
+    k_sum_final<<<1, kPixBlock, 0, ctx->stream>>>(nb, partials, double(n), dout);
+    ck(cudaGetLastError());
+    ck(cudaMemcpyAsync(out, dout, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(cudaStreamSynchronize(ctx->stream));
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e);
+  }
+  return MRB_OK;
+}
+
+}  // extern "C"

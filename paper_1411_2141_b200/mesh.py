@@ -1,0 +1,206 @@
+"""Mesh connectivity and operators (mirror of reference pkg/src/meshreg/mesh.py).
+
+`TriMesh` validates, orients and builds connectivity, CSR operators and
+geometry in native code (mrb_mesh_build), bit-exact with the reference
+(TriMesh.__init__ mesh.py:58-123, TriangleGeometry 173-213, build_laplacian
+254-265).  The operators are returned as scipy CSR arrays exactly like the
+reference's, and the per-iteration operators run on the GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+
+import numpy as np
+from scipy import sparse
+
+from . import _lib
+
+__all__ = [
+    "TriMesh",
+    "TriangleGeometry",
+    "build_adjacency",
+    "vertex_gradient_all",
+    "build_laplacian",
+    "smooth_displacement",
+]
+
+DEGENERATE_AREA = 1e-9
+
+
+class TriMesh:
+    """Static 2-D triangulation with one-ring connectivity (mesh.py:31-145)."""
+
+    def __init__(self, vertices, triangles):
+        V = np.ascontiguousarray(np.asarray(vertices, dtype=np.float64))
+        T = np.ascontiguousarray(np.asarray(triangles, dtype=np.int64))
+        if V.ndim != 2 or V.shape[1] != 2:
+            raise ValueError(f"vertices must be (n, 2), got {V.shape}")
+        if T.ndim != 2 or T.shape[1] != 3 or T.shape[0] < 1:
+            raise ValueError(f"triangles must be (m, 3) with m >= 1, got {T.shape}")
+        lib = _lib.load()
+        h = C.c_void_p()
+        err = C.create_string_buffer(512)
+        rc = lib.mrb_mesh_build(V.shape[0], _lib.ptr(V), T.shape[0], _lib.ptr(T), C.byref(h),
+                                err, 512)
+        if rc != _lib.OK:
+            raise ValueError(err.value.decode())
+        self._h = h.value
+        self._fin = weakref.finalize(self, lib.mrb_mesh_destroy, self._h)
+        counts = np.zeros(6, dtype=np.int64)
+        lib.mrb_mesh_counts(self._h, _lib.ptr(counts))
+        n, m, ne = (int(c) for c in counts[:3])
+        self._counts = counts
+        tri = np.empty((m, 3), np.int64)
+        edges = np.empty((ne, 2), np.int64)
+        valence = np.empty(n, np.int64)
+        boundary = np.empty(n, np.uint8)
+        ring_ptr = np.empty(n + 1, np.int64)
+        ring_idx = np.empty(2 * ne, np.int64)
+        inc_ptr = np.empty(n + 1, np.int64)
+        inc_idx = np.empty(3 * m, np.int64)
+        lib.mrb_mesh_export_connectivity(
+            self._h, *(_lib.ptr(a) for a in (tri, edges, valence, boundary, ring_ptr, ring_idx,
+                                             inc_ptr, inc_idx)))
+        self.vertices = V
+        self.triangles = tri
+        self.vertices.setflags(write=False)
+        self.triangles.setflags(write=False)
+        self.edges = edges
+        self.valence = valence
+        self.boundary = boundary.astype(bool)
+        self.rings = np.split(ring_idx, ring_ptr[1:-1])
+        self.incident = np.split(inc_idx, inc_ptr[1:-1])
+        self._geometry = None
+
+    @property
+    def n_vertices(self):
+        return self.vertices.shape[0]
+
+    @property
+    def n_triangles(self):
+        return self.triangles.shape[0]
+
+    @property
+    def n_edges(self):
+        return self.edges.shape[0]
+
+    @property
+    def geometry(self):
+        if self._geometry is None:
+            self._geometry = TriangleGeometry(self)
+        return self._geometry
+
+    def _csr(self, which, shape):
+        nnz = int(self._counts[{_lib.CSR_LAPLACIAN: 3, _lib.CSR_GRAD_X: 4, _lib.CSR_GRAD_Y: 4,
+                                _lib.CSR_VERTEX_AVG: 5}[which]])
+        indptr = np.empty(shape[0] + 1, np.int64)
+        indices = np.empty(nnz, np.int64)
+        data = np.empty(nnz, np.float64)
+        _lib.load().mrb_mesh_export_csr(self._h, which, _lib.ptr(indptr), _lib.ptr(indices),
+                                        _lib.ptr(data))
+        return indptr, indices, data
+
+    def __repr__(self):
+        return f"TriMesh({self.n_vertices} vertices, {self.n_triangles} triangles)"
+
+
+_foreign = weakref.WeakKeyDictionary()
+
+
+def as_mesh(mesh):
+    """Accept this package's TriMesh or any object with .vertices/.triangles
+    (e.g. a reference meshreg.TriMesh); the native mesh is cached."""
+    if isinstance(mesh, TriMesh):
+        return mesh
+    try:
+        got = _foreign.get(mesh)
+    except TypeError:
+        got = None
+    if got is None:
+        got = TriMesh(mesh.vertices, mesh.triangles)
+        try:
+            _foreign[mesh] = got
+        except TypeError:
+            pass
+    return got
+
+
+def build_adjacency(vertices, triangles):
+    return TriMesh(vertices, triangles)
+
+
+class TriangleGeometry:
+    """Areas, Eq. 9 coefficients and CSR operators (mesh.py:162-213)."""
+
+    def __init__(self, mesh):
+        mesh = as_mesh(mesh)
+        n, m = mesh.n_vertices, mesh.n_triangles
+        self.triangles = mesh.triangles
+        self.areas = np.empty(m)
+        self.coeffs = np.empty((m, 3, 2))
+        self.vertex_areas = np.empty(n)
+        _lib.load().mrb_mesh_export_geometry(mesh._h, _lib.ptr(self.areas),
+                                             _lib.ptr(self.coeffs), _lib.ptr(self.vertex_areas))
+
+        def csr(which, shape):
+            p, i, d = mesh._csr(which, shape)
+            return sparse.csr_array((d, i, p), shape=shape)
+
+        self.grad_x_op = csr(_lib.CSR_GRAD_X, (m, n))
+        self.grad_y_op = csr(_lib.CSR_GRAD_Y, (m, n))
+        self.vertex_average_op = csr(_lib.CSR_VERTEX_AVG, (n, m))
+        self._mesh = mesh
+
+
+def build_laplacian(mesh):
+    """Row-stochastic one-ring average matrix (mesh.py:254-265)."""
+    mesh = as_mesh(mesh)
+    n = mesh.n_vertices
+    p, i, d = mesh._csr(_lib.CSR_LAPLACIAN, (n, n))
+    return sparse.csr_array((d, i, p), shape=(n, n))
+
+
+def _csr_arrays(L):
+    L = sparse.csr_array(L)
+    return (np.ascontiguousarray(L.indptr, dtype=np.int64),
+            np.ascontiguousarray(L.indices, dtype=np.int64),
+            np.ascontiguousarray(L.data, dtype=np.float64))
+
+
+def smooth_displacement(L, u0, lam, iterations=1):
+    """Explicit diffusion u <- (1 - lam) u + lam (L @ u) (mesh.py:268-282),
+    on the GPU for any CSR matrix L."""
+    if not 0.0 < lam < 1.0:
+        raise ValueError(f"smoothing weight must be in (0, 1), got {lam}")
+    if iterations < 0:
+        raise ValueError("iterations must be >= 0")
+    u = np.array(u0, dtype=np.float64, copy=True)
+    if iterations == 0:
+        return u
+    squeeze = u.ndim == 1
+    u2 = np.ascontiguousarray(np.stack([u, np.zeros_like(u)], axis=1) if squeeze else u)
+    if u2.ndim != 2 or u2.shape[1] != 2:
+        raise ValueError(f"displacement must be (n,) or (n, 2), got {u.shape}")
+    p, i, d = _csr_arrays(L)
+    out = np.empty_like(u2)
+    lib = _lib.load()
+    ctx = _lib.context()
+    rc = lib.mrb_smooth_csr(ctx, u2.shape[0], _lib.ptr(p), _lib.ptr(i), _lib.ptr(d),
+                            _lib.ptr(u2), float(lam), int(iterations), _lib.ptr(out))
+    _lib.check(rc, ctx, (ValueError, RuntimeError, RuntimeError))
+    return out[:, 0].copy() if squeeze else out
+
+
+def vertex_gradient_all(mesh, geom, f):
+    """Per-vertex gradients (n, 2) of a per-vertex scalar (mesh.py:236-241),
+    via the fused one-ring operator on the GPU."""
+    mesh = as_mesh(mesh)
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    out = np.empty((mesh.n_vertices, 2))
+    lib = _lib.load()
+    ctx = _lib.context()
+    rc = lib.mrb_vertex_gradient_all(ctx, mesh._h, _lib.ptr(f), _lib.ptr(out))
+    _lib.check(rc, ctx, (ValueError, RuntimeError, RuntimeError))
+    return out

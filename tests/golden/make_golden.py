@@ -1,0 +1,230 @@
+"""Generate golden vectors by running the REFERENCE implementation itself.
+
+Run in the build container only (imports /root/reference/pkg/src/meshreg, which
+does not exist on the GPU box):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Writes tests/golden/<case>.npz.  Each file holds the inputs (images, mesh) and
+the reference's outputs for the hot path: displacement u,
+energy trace, iterations run, MSD before/after, dense field, warped image, the
+CSR operators (L, grad_x_op, grad_y_op, vertex_average_op), connectivity and
+the pixel->triangle map captured from the reference's own `densify`.
+The reference ships no golden files; these pin both the
+oracle (oracle/meshreg_oracle.py) and the B200 path.
+"""
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REF)
+sys.path.insert(0, ROOT)
+
+import meshreg as mr  # noqa: E402
+import meshreg.densefield as mr_df  # noqa: E402
+from meshreg import synthetic  # noqa: E402
+from scipy import ndimage  # noqa: E402
+
+from paper_1411_2141_b200.synthetic import PairSpec, make_pair  # noqa: E402
+
+
+class _Capture:
+    """Stand-in for the numpy module inside meshreg.densefield that records
+    the pixel->triangle map and weights arrays `densify` allocates and fills
+    (densefield.py:148-149), so the golden map is the reference's own."""
+
+    def __init__(self):
+        self.arrays = {}
+
+    def __getattr__(self, name):
+        return getattr(np, name)
+
+    def full(self, *a, **k):
+        out = np.full(*a, **k)
+        self.arrays["tri_of"] = out
+        return out
+
+    def zeros(self, shape, *a, **k):
+        out = np.zeros(shape, *a, **k)
+        if isinstance(shape, tuple) and len(shape) == 3 and shape[2] == 3:
+            self.arrays["weights"] = out
+        return out
+
+
+def reference_pixel_map(mesh, w, h):
+    cap = _Capture()
+    mr_df.np = cap
+    try:
+        mr.densify(mesh, np.zeros((mesh.n_vertices, 2)), w, h)
+    finally:
+        mr_df.np = np
+    return cap.arrays["tri_of"], cap.arrays["weights"]
+
+
+def csr_parts(prefix, A):
+    A = A.tocsr() if hasattr(A, "tocsr") else A
+    assert A.has_canonical_format
+    return {f"{prefix}_indptr": A.indptr.astype(np.int64),
+            f"{prefix}_indices": A.indices.astype(np.int64),
+            f"{prefix}_data": A.data.astype(np.float64)}
+
+
+def mesh_parts(mesh, with_ops=True):
+    out = {"V": mesh.vertices.copy(), "T_in": mesh.triangles.copy(),
+           "T": mesh.triangles.copy(), "edges": mesh.edges.astype(np.int64),
+           "valence": mesh.valence.astype(np.int64), "boundary": mesh.boundary.copy(),
+           "ring_ptr": np.concatenate([[0], np.cumsum([len(r) for r in mesh.rings])]).astype(np.int64),
+           "ring_idx": np.concatenate(mesh.rings).astype(np.int64),
+           "inc_ptr": np.concatenate([[0], np.cumsum([len(r) for r in mesh.incident])]).astype(np.int64),
+           "inc_idx": np.concatenate(mesh.incident).astype(np.int64)}
+    if with_ops:
+        g = mesh.geometry
+        out.update(csr_parts("L", mr.build_laplacian(mesh)))
+        out.update(csr_parts("gx", g.grad_x_op))
+        out.update(csr_parts("gy", g.grad_y_op))
+        out.update(csr_parts("avg", g.vertex_average_op))
+        out.update(areas=g.areas, coeffs=g.coeffs, vertex_areas=g.vertex_areas)
+    return out
+
+
+def run_register(re, te, mesh, cfg, dense=True):
+    u, rep = mr.register(re, te, mesh, cfg)
+    out = {"u": u, "trace": np.array(rep.energy_trace), "iterations_run": rep.iterations_run,
+           "msd_before": rep.msd_before, "msd_after": rep.msd_after,
+           "cfg": np.array([cfg.tau, cfg.lam, cfg.max_iterations, cfg.smoothing_passes,
+                            cfg.energy_tolerance])}
+    if dense:
+        d = mr.densify(mesh, u, te.width, te.height)
+        out.update(ux=d.ux, uy=d.uy, warped=mr.warp_image(te, d).data)
+    return out
+
+
+def smooth_image(w, h, seed, amplitude=60.0):
+    """Same construction as the reference conftest.random_smooth_image."""
+    rng = np.random.default_rng(seed)
+    data = ndimage.gaussian_filter(rng.standard_normal((h, w)), 2.0, mode="nearest")
+    lo, hi = data.min(), data.max()
+    return mr.ImageGrid(w, h, 120.0 + amplitude * (data - lo) / max(hi - lo, 1e-12) - amplitude / 2)
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)")
+
+
+def case_generated(name, size, blobs, peak, target, iters, scale, passes=1, tol=0.0,
+                   unit=False, pixel_map=True, tau=0.005):
+    spec = PairSpec(name, size, blobs, 0, peak, target, iters)
+    re32, te32 = make_pair(spec, seed=3, scale=scale)
+    re = mr.ImageGrid(size, size, re32.astype(np.float64))
+    te = mr.ImageGrid(size, size, te32.astype(np.float64))
+    mesh = mr.generate_mesh(te, mr.NodeBudget(target), mr.MeshGenConfig(seed=0))
+    cfg = mr.SolverConfig(tau=tau, max_iterations=iters, smoothing_passes=passes,
+                          energy_tolerance=tol)
+    out = dict(re=re32, te=te32, **mesh_parts(mesh), **run_register(re, te, mesh, cfg))
+    if pixel_map:
+        tri_of, wts = reference_pixel_map(mesh, size, size)
+        out.update(tri_of=tri_of.astype(np.int32), pm_weights=wts)
+    if unit:
+        rng = np.random.default_rng(11)
+        u = rng.uniform(-1.5, 1.5, (mesh.n_vertices, 2))
+        grad = rng.uniform(-50, 50, (mesh.n_vertices, 2))
+        L = mr.build_laplacian(mesh)
+        out.update(
+            unit_u=u, unit_grad=grad,
+            unit_warp_sample=mr.warp_sample(te, mesh.vertices, u),
+            unit_energy=mr.energy(re, te, mesh, u),
+            unit_energy_gradient=mr.energy_gradient(re, te, mesh, u),
+            unit_vgrad=mr.vertex_gradient_all(mesh, mesh.geometry, te.sample(*mesh.vertices.T)),
+            unit_smooth2=mr.smooth_displacement(L, u, 0.8, 2),
+            unit_step=mr.step(u, grad, mr.SolverConfig(), L, mesh.vertices, (size, size)),
+            unit_msd=mr.msd(te, re),
+        )
+    save(name, **out)
+
+
+def main():
+    # small generated pairs ([0,1] and x255 large motion), full pipeline
+    case_generated("gen64", 64, 8, 2.0, 150, 40, 1.0, unit=True)
+    case_generated("gen64_x255", 64, 8, 2.0, 400, 40, 255.0, unit=True, tau=0.001)
+    case_generated("gen64_p0", 64, 8, 2.0, 400, 20, 25.0, passes=0, pixel_map=False,
+                   tau=0.001)
+    case_generated("gen64_p2", 64, 8, 2.0, 400, 30, 255.0, passes=2, pixel_map=False,
+                   tau=0.001)
+    case_generated("gen96_tol", 96, 10, 3.0, 400, 100, 25.0, tol=1e-6, pixel_map=False,
+                   tau=0.001)
+
+    # reference fixture (acceptance C3 pattern, test_acceptance.py:116-134),
+    # float64 images that are NOT fp32-representable
+    w = 256
+    ref = synthetic.smooth_texture(w, w, seed=7)
+    bump = synthetic.random_bump_field(w, w, seed=107, n_bumps=3, max_amplitude=4.0)
+    _, te = synthetic.warped_pair(ref, bump)
+    mesh = mr.generate_mesh(te, mr.NodeBudget(3000), mr.MeshGenConfig(seed=1))
+    cfg = mr.SolverConfig(tau=0.005, lam=0.8, max_iterations=100)
+    tri_of, _ = reference_pixel_map(mesh, w, w)
+    save("accept_c3", re=ref.data, te=te.data, **mesh_parts(mesh, with_ops=False),
+         **run_register(ref, te, mesh, cfg), tri_of=tri_of.astype(np.int32))
+
+    # plateau shift (test_registration.py:334-346 pattern)
+    w = 64
+    ref = synthetic.smooth_texture(w, w, seed=11, low=100, high=156)
+    field = synthetic.plateau_shift_field(w, w, shift=(1.5, 0.5))
+    _, te = synthetic.warped_pair(ref, field)
+    mesh = mr.generate_mesh(te, mr.NodeBudget(300), mr.MeshGenConfig(seed=2))
+    save("plateau64", re=ref.data, te=te.data, **mesh_parts(mesh),
+         **run_register(ref, te, mesh, mr.SolverConfig(max_iterations=30)))
+
+    # identical images: tolerance exit (test_registration.py:292-300)
+    img = smooth_image(48, 48, seed=9)
+    mesh = mr.generate_mesh(img, mr.NodeBudget(80), mr.MeshGenConfig(seed=1))
+    save("identical48", re=img.data, te=img.data, **mesh_parts(mesh, with_ops=False),
+         **run_register(img, img, mesh, mr.SolverConfig()))
+
+    # divergence guard (test_registration.py:325-331)
+    ref = synthetic.smooth_texture(64, 64, seed=7, low=20, high=235)
+    field = synthetic.plateau_shift_field(64, 64, shift=(2.0, 0.0))
+    _, te = synthetic.warped_pair(ref, field)
+    mesh = mr.generate_mesh(te, mr.NodeBudget(500), mr.MeshGenConfig(seed=1))
+    try:
+        mr.register(ref, te, mesh, mr.SolverConfig(tau=0.1))
+        msg = ""
+    except mr.DivergenceError as exc:
+        msg = str(exc)
+    save("diverge64", re=ref.data, te=te.data, **mesh_parts(mesh, with_ops=False),
+         error=np.array(msg), cfg=np.array([0.1, 0.8, 100, 1, 1e-6]))
+
+    # full BASELINE config 1 pair (seed 0) on the cached reference mesh
+    mpath = os.path.join(ROOT, "data", "meshes", "c1_s0.npz")
+    if os.path.exists(mpath):
+        from paper_1411_2141_b200.synthetic import CONFIGS
+        spec = CONFIGS["c1"]
+        m = np.load(mpath)
+        for scale, tag in ((1.0, "c1"), (255.0, "c1_x255")):
+            re32, te32 = make_pair(spec, 0, scale=scale)
+            mp = mpath if scale == 1.0 else mpath.replace(".npz", "_x255.npz")
+            if not os.path.exists(mp):
+                continue
+            m = np.load(mp)
+            mesh = mr.TriMesh(m["V"], m["T"].astype(np.int64))
+            re = mr.ImageGrid(256, 256, re32.astype(np.float64))
+            te = mr.ImageGrid(256, 256, te32.astype(np.float64))
+            cfg = mr.SolverConfig(max_iterations=spec.iterations, energy_tolerance=0.0)
+            out = run_register(re, te, mesh, cfg)
+            extra = {}
+            if tag == "c1":
+                tri_of, _ = reference_pixel_map(mesh, 256, 256)
+                extra = dict(tri_of=tri_of.astype(np.int32), **{
+                    k: v for k, v in mesh_parts(mesh).items()
+                    if k.startswith(("L_", "gx_", "gy_", "avg_"))})
+            save(tag, re=re32, te=te32, V=m["V"], T_in=m["T"].astype(np.int64),
+                 T=mesh.triangles.copy(), **out, **extra)
+
+
+if __name__ == "__main__":
+    main()

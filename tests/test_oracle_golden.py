@@ -1,0 +1,79 @@
+"""Pin the CPU oracle (oracle/meshreg_oracle.py) against golden vectors that
+the reference itself produced (tests/golden/make_golden.py)."""
+import numpy as np
+import pytest
+
+import meshreg_oracle as O
+from conftest import golden
+
+
+def test_oracle_register_bit_exact(golden_case):
+    name, g = golden_case
+    m = O.Mesh(g["V"], g["T_in"])
+    assert np.array_equal(m.T, g["T"])
+    tau, lam, iters, passes, tol = g["cfg"]
+    u, info = O.register(g["re"], g["te"], m, tau=tau, lam=lam, max_iterations=int(iters),
+                         smoothing_passes=int(passes), energy_tolerance=tol)
+    assert info["iterations_run"] == int(g["iterations_run"])
+    assert np.array_equal(np.array(info["energy_trace"]), g["trace"])
+    assert np.array_equal(u, g["u"])
+    assert info["msd_before"] == float(g["msd_before"])
+    if "ux" in g.files:
+        assert np.array_equal(info["ux"], g["ux"])
+        assert np.array_equal(info["uy"], g["uy"])
+        assert np.array_equal(info["warped"], g["warped"])
+        assert info["msd_after"] == float(g["msd_after"])
+
+
+def test_oracle_connectivity_and_csr_bit_exact(golden_case):
+    name, g = golden_case
+    m = O.Mesh(g["V"], g["T_in"])
+    if "ring_idx" in g.files:
+        assert np.array_equal(m.ring_ptr, g["ring_ptr"]) and np.array_equal(m.ring_idx, g["ring_idx"])
+        assert np.array_equal(m.inc_ptr, g["inc_ptr"]) and np.array_equal(m.inc_idx, g["inc_idx"])
+        assert np.array_equal(m.edges, g["edges"])
+        assert np.array_equal(m.valence, g["valence"])
+        assert np.array_equal(m.boundary, g["boundary"])
+    for key, mine in (("L", m.lap), ("gx", m.gx), ("gy", m.gy), ("avg", m.avg)):
+        if key + "_indptr" in g.files:
+            for a, b in zip(mine, (g[key + "_indptr"], g[key + "_indices"], g[key + "_data"])):
+                assert np.array_equal(a, b), key
+    if "areas" in g.files:
+        assert np.array_equal(m.areas, g["areas"])
+        assert np.array_equal(m.coeffs, g["coeffs"])
+        assert np.array_equal(m.vertex_areas, g["vertex_areas"])
+
+
+@pytest.mark.parametrize("name", ["gen64", "gen64_x255", "accept_c3", "c1"])
+def test_oracle_pixel_map_bit_exact(name):
+    g = golden(name)
+    m = O.Mesh(g["V"], g["T_in"])
+    h, w = g["re"].shape
+    tri, wts = O.pixel_map(m, w, h)
+    assert np.array_equal(tri, g["tri_of"])
+    if "pm_weights" in g.files:
+        assert np.array_equal(wts, g["pm_weights"])
+
+
+@pytest.mark.parametrize("name", ["gen64", "gen64_x255"])
+def test_oracle_single_operations(name):
+    g = golden(name)
+    m = O.Mesh(g["V"], g["T_in"])
+    u, grad = g["unit_u"], g["unit_grad"]
+    assert np.array_equal(O.warp_sample(g["te"], m.V, u), g["unit_warp_sample"])
+    assert O.energy(g["re"], g["te"], m, u) == float(g["unit_energy"])
+    assert np.array_equal(O.energy_gradient(g["re"], g["te"], m, u), g["unit_energy_gradient"])
+    f = O.sample(g["te"], m.V[:, 0], m.V[:, 1])
+    assert np.array_equal(O.vertex_gradient_all(m, f), g["unit_vgrad"])
+    assert np.array_equal(O.smooth_displacement(m, u, 0.8, 2), g["unit_smooth2"])
+    h, w = g["re"].shape
+    assert np.array_equal(O.step(m, u, grad, 0.005, 0.8, 1, m.V, (w, h)), g["unit_step"])
+    assert O.msd(g["te"], g["re"]) == float(g["unit_msd"])
+
+
+def test_oracle_divergence_message():
+    g = golden("diverge64")
+    m = O.Mesh(g["V"], g["T_in"])
+    with pytest.raises(O.OracleDivergence) as exc:
+        O.register(g["re"], g["te"], m, tau=0.1)
+    assert str(exc.value) == str(g["error"])
