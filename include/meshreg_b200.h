@@ -142,6 +142,9 @@ int mrb_batch_sync(mrb_batch* batch);
 int mrb_batch_pair_status(mrb_batch* batch, int32_t pair, int32_t* iterations_run,
                           double* msd_before, double* msd_after, double* trace, char* msg,
                           int32_t msg_len);
+/* execution path chosen for the batch: 0 = generic three-kernel loop, else the
+ * cluster size of the persistent cluster kernel (fp32, <= 16 x 768 nodes) */
+int32_t mrb_batch_path(const mrb_batch* batch);
 /* device kernels launched by one mrb_batch_run (for the bench's launch count) */
 int64_t mrb_batch_launches_per_run(const mrb_batch* batch);
 /* algorithmic bytes of one run, SURVEY.md §8(d) byte model */

@@ -26,6 +26,8 @@ namespace mrb {
 
 constexpr int kNodeBlock = 256;
 constexpr int kPixBlock = 256;
+// pixel-map sentinel: what cudaMemset(..., 0x7f, ...) leaves in every int
+constexpr int kUnassigned = 0x7f7f7f7f;
 
 enum : int {
   ERR_NONE = 0,
@@ -587,7 +589,7 @@ __global__ void k_count_uncovered(const int* __restrict__ tri_of, int npx,
                                   unsigned long long* __restrict__ count) {
   int local = 0;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < npx; q += gridDim.x * blockDim.x)
-    local += (tri_of[q] == 0x7fffffff);
+    local += (tri_of[q] == kUnassigned);
   for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, (unsigned long long)local);
 }

@@ -10,9 +10,11 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/meshreg_b200.h"
+#include "cluster.cuh"
 #include "kernels.cuh"
 #include "mesh_host.h"
 
@@ -44,6 +46,14 @@ struct DeviceMesh {
   double2* g_nb_d = nullptr;
   double* inv_val_d = nullptr;
   std::map<std::pair<int, int>, int*> pixel_maps;
+  // cluster fast path: register topology packed for a given chunk size
+  struct Topo {
+    uint16_t* codes = nullptr;
+    float2* g = nullptr;
+    unsigned char* deg = nullptr;
+  };
+  std::map<int, Topo> topo;
+  int max_deg = 0;
   ~DeviceMesh() {
     int cur = -1;
     cudaGetDevice(&cur);
@@ -53,6 +63,11 @@ struct DeviceMesh {
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (auto& kv : pixel_maps) cudaFree(kv.second);
+    for (auto& kv : topo) {
+      cudaFree(kv.second.codes);
+      cudaFree(kv.second.g);
+      cudaFree(kv.second.deg);
+    }
     if (cur >= 0) cudaSetDevice(cur);
   }
 };
@@ -186,7 +201,36 @@ void ensure_device_mesh(mrb_ctx* ctx, HostMesh& h) {
   d.g_self_f = dupload(reinterpret_cast<const float2*>(gs.data()), n, s);
   d.g_nb_f = dupload(reinterpret_cast<const float2*>(gn.data()), ne2, s);
   d.inv_val_f = dupload(iv.data(), n, s);
+  for (int64_t k = 0; k < h.n; ++k) d.max_deg = std::max(d.max_deg, h.nb_ptr[k + 1] - h.nb_ptr[k]);
   ck(cudaStreamSynchronize(s));  // host vectors above go out of scope
+}
+
+// Register-resident topology of the cluster kernel for chunk size `chunk`:
+// entry-major [kMaxDeg][n] neighbour codes (owning CTA rank << 12 | local
+// index) and fused-gradient coefficients, plus the valence.
+const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int chunk) {
+  DeviceMesh& d = *h.dev;
+  auto it = d.topo.find(chunk);
+  if (it != d.topo.end()) return it->second;
+  const size_t n = size_t(h.n);
+  std::vector<uint16_t> codes(kMaxDeg * n, 0);
+  std::vector<float2> g(kMaxDeg * n, make_float2(0.f, 0.f));
+  std::vector<unsigned char> deg(n);
+  for (size_t i = 0; i < n; ++i) {
+    const int b = h.nb_ptr[i], e = h.nb_ptr[i + 1];
+    deg[i] = (unsigned char)(e - b);
+    for (int q = b; q < e; ++q) {
+      const int j = h.nb_idx[q];
+      codes[size_t(q - b) * n + i] = uint16_t(((j / chunk) << 12) | (j % chunk));
+      g[size_t(q - b) * n + i] = make_float2(float(h.g_nb[2 * q]), float(h.g_nb[2 * q + 1]));
+    }
+  }
+  DeviceMesh::Topo t;
+  t.codes = dupload(codes.data(), codes.size(), ctx->stream);
+  t.g = dupload(g.data(), g.size(), ctx->stream);
+  t.deg = dupload(deg.data(), deg.size(), ctx->stream);
+  ck(cudaStreamSynchronize(ctx->stream));
+  return d.topo[chunk] = t;
 }
 
 // Pixel->triangle map for (W, H): GPU raster + host locate fallback.
@@ -225,7 +269,7 @@ std::string ensure_pixel_map(mrb_ctx* ctx, HostMesh& h, int W, int H, int** out)
     ck(cudaMemcpy(host.data(), tri_of, npx * sizeof(int), cudaMemcpyDeviceToHost));
     Locator loc(h);
     for (size_t q = 0; q < npx; ++q) {
-      if (host[q] != 0x7fffffff) continue;
+      if (host[q] != kUnassigned) continue;
       const double px = double(q % W), py = double(q / W);
       double w[3];
       const int64_t t = loc.locate(h, px, py, w);
@@ -278,6 +322,9 @@ struct mrb_batch {
   void* conv = nullptr;        // dtype conversion scratch for get_results
   cudaGraphExec_t graph = nullptr;
   std::vector<const void*> graph_src;
+  // cluster fast path (0 = generic three-kernel loop)
+  int cluster_cs = 0;
+  void* cpairs = nullptr;  // ClusterPair[n_pairs]
   int runs = 0;
   // host results
   std::vector<PairStatus> h_st;
@@ -286,7 +333,7 @@ struct mrb_batch {
   ~mrb_batch() {
     if (graph) cudaGraphExecDestroy(graph);
     void* ptrs[] = {pairs, st, blk_pair, pix_blk_pair, partials, pix_partials, state, traces,
-                    img, stage, src_ptrs, img_ptrs, dense, u_out, conv};
+                    img, stage, src_ptrs, img_ptrs, dense, u_out, conv, cpairs};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
@@ -402,6 +449,72 @@ struct KernelTimer {
   }
 };
 
+template <int CS>
+void launch_cluster_t(mrb_batch* b) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(unsigned(b->n_pairs * CS));
+  lc.blockDim = dim3(kClusterThreads);
+  lc.dynamicSmemBytes = kClusterDynSmem;
+  lc.stream = b->ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  ck(cudaLaunchKernelEx(&lc, k_cluster_register<CS>,
+                        static_cast<const ClusterPair*>(b->cpairs), b->st,
+                        int(b->cfg.max_iterations), double(b->cfg.energy_tolerance),
+                        float(b->cfg.tau), float(b->cfg.lam), int(b->cfg.smoothing_passes)));
+}
+
+template <int CS>
+int cluster_occupancy() {
+  cudaFuncSetAttribute(k_cluster_register<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_cluster_register<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(kClusterDynSmem));
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(unsigned(CS));
+  lc.blockDim = dim3(kClusterThreads);
+  lc.dynamicSmemBytes = kClusterDynSmem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_cluster_register<CS>, &lc) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int cluster_occupancy_cs(int cs) {
+  switch (cs) {
+    case 1: return cluster_occupancy<1>();
+    case 2: return cluster_occupancy<2>();
+    case 4: return cluster_occupancy<4>();
+    case 8: return cluster_occupancy<8>();
+    case 16: return cluster_occupancy<16>();
+  }
+  return 0;
+}
+
+int64_t launch_cluster(mrb_batch* b) {
+  switch (b->cluster_cs) {
+    case 1: launch_cluster_t<1>(b); break;
+    case 2: launch_cluster_t<2>(b); break;
+    case 4: launch_cluster_t<4>(b); break;
+    case 8: launch_cluster_t<8>(b); break;
+    case 16: launch_cluster_t<16>(b); break;
+  }
+  return 1;
+}
+
 template <typename TapT, typename Real>
 int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
   KernelTimer dummy;
@@ -419,6 +532,20 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
                                                          b->cfg.max_iterations);
   ++launches;
   const int nb = b->n_node_blocks;
+  if (b->cluster_cs) {
+    if constexpr (std::is_same<TapT, float>::value && std::is_same<Real, float>::value) {
+      tm->mark(-1);
+      launches += launch_cluster(b);
+      tm->mark(0);
+      k_dense<TapT, Real><<<b->n_pix_blocks, kPixBlock, 0, s>>>(pairs, b->st, b->pix_blk_pair,
+                                                                b->pix_partials);
+      tm->mark(3);
+      k_msd_final<TapT, Real><<<b->n_pairs, kPixBlock, 0, s>>>(pairs, b->st, b->pix_partials);
+      launches += 2;
+      ck(cudaGetLastError());
+      return launches;
+    }
+  }
   const double tol = b->cfg.energy_tolerance;
   const Real tau = Real(b->cfg.tau), lam = Real(b->cfg.lam);
   const int passes = b->cfg.smoothing_passes;
@@ -471,7 +598,54 @@ int64_t dispatch_enqueue(mrb_batch* b, KernelTimer* tm = nullptr) {
 }
 
 int64_t launches_per_run(const mrb_batch* b) {
+  if (b->cluster_cs) return 2 + 1 + 2;  // interleave, reset, cluster loop, dense, msd
   return 2 + int64_t(b->cfg.max_iterations) * (2 + b->cfg.smoothing_passes) + 3;
+}
+
+// Choose the cluster fast path when it applies: fp32, every pair fits one
+// cluster of <= 16 CTAs x 768 nodes, one-rings of <= kMaxDeg entries.
+void setup_cluster_path(mrb_batch* b) {
+  b->cluster_cs = 0;
+  const char* env = std::getenv("MESHREG_B200_PATH");
+  if (env && std::string(env) == "generic") return;
+  if (b->real_d || b->tap_d) return;
+  int64_t nmax = 0;
+  for (mrb_mesh* m : b->meshes) {
+    nmax = std::max<int64_t>(nmax, m->h.n);
+    if (m->h.dev->max_deg > kMaxDeg) return;
+  }
+  int cs = 1;
+  while (cs < 16 && (nmax + cs - 1) / cs > kClusterThreads) cs *= 2;
+  if ((nmax + cs - 1) / cs > kClusterThreads) return;
+  if (cluster_occupancy_cs(cs) < 1) return;
+  std::vector<ClusterPair> cp(b->n_pairs);
+  std::vector<PairDev<float, float>> host(b->n_pairs);
+  ck(cudaMemcpy(host.data(), b->pairs, b->n_pairs * sizeof(PairDev<float, float>),
+                cudaMemcpyDeviceToHost));
+  for (int p = 0; p < b->n_pairs; ++p) {
+    HostMesh& h = b->meshes[p]->h;
+    const int chunk = int((h.n + cs - 1) / cs);
+    const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, h, chunk);
+    ClusterPair& c = cp[p];
+    c.V = h.dev->V;
+    c.codes = t.codes;
+    c.g = t.g;
+    c.g_self = h.dev->g_self_f;
+    c.inv_val = h.dev->inv_val_f;
+    c.deg = t.deg;
+    c.img = host[p].img;
+    c.u = host[p].u;
+    c.u_out = host[p].u_out;
+    c.perm = h.dev->perm;
+    c.trace = host[p].trace;
+    c.n = int(h.n);
+    c.chunk = chunk;
+    c.W = b->W;
+    c.H = b->H;
+  }
+  b->cpairs = dupload(cp.data(), cp.size(), b->ctx->stream);
+  ck(cudaStreamSynchronize(b->ctx->stream));
+  b->cluster_cs = cs;
 }
 
 template <typename From, typename To>
@@ -732,6 +906,7 @@ int mrb_batch_create(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int
       build_pairs<float, double>(b.get());
     else
       build_pairs<float, float>(b.get());
+    setup_cluster_path(b.get());
   } catch (const CudaError& e) {
     return cuda_fail(ctx, e.e);
   }
@@ -892,6 +1067,8 @@ int mrb_batch_pair_status(mrb_batch* b, int32_t p, int32_t* iters, double* msd_b
 
 int64_t mrb_batch_launches_per_run(const mrb_batch* b) { return launches_per_run(b); }
 
+int32_t mrb_batch_path(const mrb_batch* b) { return b->cluster_cs; }
+
 double mrb_batch_algorithmic_bytes(const mrb_batch* b) {
   // iterations*(184 n_V + 60 n_T + 8 n_E) + 128 W H per pair
   double tot = 0;
@@ -919,6 +1096,10 @@ int mrb_batch_kernel_bytes(const mrb_batch* b, double* out) {
   out[1] = 16.0 * nv + 60.0 * nt;
   out[2] = 20.0 * nv + 8.0 * ne;
   out[3] = 128.0 * double(b->W) * b->H * b->n_pairs;
+  if (b->cluster_cs) {  // one launch runs every iteration of every pair
+    out[0] = double(b->cfg.max_iterations) * (184.0 * nv + 60.0 * nt + 8.0 * ne);
+    out[1] = out[2] = 0.0;
+  }
   return MRB_OK;
 }
 

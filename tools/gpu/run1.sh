@@ -1,0 +1,8 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
+tail -5 gpurun_out/smoke.log
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+tail -40 gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --pairs 16 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench1.log 2>&1; echo bench rc=$?
+tail -5 gpurun_out/bench1.log
