@@ -273,6 +273,7 @@ def run_ours(args, rank, world, local):
     work = float(npx) * tot_iters  # px*iter per step on this rank
     value = world * work * args.steps / (t_ms / 1e3) / 1e6
     launches = int(lib.mrb_batch_launches_per_run(batch)) * args.steps
+    path_cs = int(lib.mrb_batch_path(batch))
     alg_bytes = lib.mrb_batch_algorithmic_bytes(batch)
     lib.mrb_batch_destroy(batch)
 
@@ -285,7 +286,12 @@ def run_ours(args, rank, world, local):
     n_launch = {0: iters, 1: iters, 2: iters, 3: 1}
     share = {k: ktimes[k] * n_launch[k] for k in range(4)}
     dom = max(share, key=share.get)
-    names = {0: "k_sample", 1: "k_grad", 2: "k_smooth", 3: "k_dense"}
+    names = {0: "k_cluster_register" if path_cs else "k_sample", 1: "k_grad", 2: "k_smooth",
+             3: "k_dense"}
+    if path_cs:
+        n_launch = {0: 1, 1: 0, 2: 0, 3: 1}
+        share = {k: ktimes[k] * n_launch[k] for k in range(4)}
+        dom = max(share, key=share.get)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
@@ -320,6 +326,8 @@ def run_ours(args, rank, world, local):
                 "precision": args.precision,
             },
             "gpu_launches": launches,
+            "path": (f"persistent cluster kernel (cluster of {path_cs} CTAs per pair)" if path_cs
+                     else "generic 3-kernel loop (CUDA graph)"),
             "kernel_ms": {names[k]: round(float(ktimes[k]), 5) for k in range(4)},
             "algorithmic_bytes_per_step": alg_bytes,
             "hbm_frac_whole_run": round(alg_bytes / (t_ms / args.steps / 1e3) / 1e9 / peak, 4),

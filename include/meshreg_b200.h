@@ -145,6 +145,9 @@ int mrb_batch_pair_status(mrb_batch* batch, int32_t pair, int32_t* iterations_ru
 /* execution path chosen for the batch: 0 = generic three-kernel loop, else the
  * cluster size of the persistent cluster kernel (fp32, <= 16 x 768 nodes) */
 int32_t mrb_batch_path(const mrb_batch* batch);
+/* debug: per-CTA phase timestamps of the cluster kernel (first 8 iterations,
+ * 16 slots each) when MESHREG_B200_PROFILE_PHASES is set at batch creation */
+int mrb_batch_phase_profile(mrb_batch* batch, long long* out, int64_t n);
 /* device kernels launched by one mrb_batch_run (for the bench's launch count) */
 int64_t mrb_batch_launches_per_run(const mrb_batch* batch);
 /* algorithmic bytes of one run, SURVEY.md §8(d) byte model */

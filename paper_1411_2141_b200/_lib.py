@@ -60,6 +60,7 @@ _SIGS = {
     "mrb_batch_pair_status": (C.c_int, [_vp, _i32, C.POINTER(_i32), _dp, _dp, _vp, C.c_char_p,
                                         _i32]),
     "mrb_batch_path": (_i32, [_vp]),
+    "mrb_batch_phase_profile": (C.c_int, [_vp, _vp, _i64]),
     "mrb_batch_launches_per_run": (_i64, [_vp]),
     "mrb_batch_algorithmic_bytes": (C.c_double, [_vp]),
     "mrb_batch_kernel_bytes": (C.c_int, [_vp, _vp]),

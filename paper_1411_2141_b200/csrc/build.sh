@@ -10,6 +10,6 @@ $NVCC -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a \
   -Xcompiler -fPIC,-ffp-contract=off -Xptxas -v -shared \
   -I"$HERE/../../include" \
   "$HERE/meshreg_b200.cu" "$HERE/mesh_host.cpp" -o "$OUT.tmp" 2> "$HERE/../../build_ptxas.log" || {
-    cat "$HERE/../../build_ptxas.log"; exit 1; }
+    grep -v "^ptxas info\|^    [0-9]* bytes stack" "$HERE/../../build_ptxas.log" | head -40; exit 1; }
 mv "$OUT.tmp" "$OUT"
 echo "built $OUT"

@@ -1,17 +1,31 @@
-// Persistent thread-block-cluster registration kernel (fast path).
+// Persistent thread-block-cluster registration kernel (fp32 fast path).
 //
 // One cluster of CS CTAs (CS <= 16) owns one pair for the whole descent loop
-// (solver.py:171-195).  Each thread owns one mesh node (device/Morton order);
-// its one-ring topology — neighbour codes and the fused gradient operator
-// G = avg∘grad (mesh.py:236-241) — is staged once into shared memory in an
-// entry-major [entry][thread] layout (bank-conflict-free) and reused for all
-// iterations; the node state (V, u, r) stays in registers.
-// The two neighbour exchanges per iteration (s_te for the gradient, u0 for the
-// umbrella smoothing) go through distributed shared memory, ordered by
-// hardware cluster barriers; nothing round-trips through global memory except
-// the image taps.  The fp64 energy partial of every CTA is reduced in a fixed
-// order by every CTA, so all CTAs take the same divergence / tolerance
-// decision (solver.py:174-195) without another barrier.
+// (solver.py:171-195).  CTA r owns the contiguous chunk [r*chunk, (r+1)*chunk)
+// of the device (Morton) node order; thread t owns slots t, t+768, ... (NPT
+// slots).  Per-node constants live in shared memory; u and r in registers.
+//
+// Neighbour exchange = ghost (halo) exchange over DSMEM: each CTA keeps its
+// own values followed by a halo region holding copies of the remote nodes its
+// one-rings reference.  After each cluster barrier the CTA pulls exactly its
+// halo (one ld.shared::cluster per halo node), so every one-ring gather of the
+// fused gradient operator G = avg∘grad (mesh.py:236-241) and of the umbrella
+// Laplacian (mesh.py:254-282) is a local LDS through a 16-bit index.  The
+// one-ring topology is staged once in a SELL-32 layout (entry-major per 32-slot
+// slice, padded to the slice's largest one-ring): bank-conflict-free.
+//
+// Per iteration k:
+//   A  sample (Te, Re) at V+u: 4 rows x one 256-bit load from one of four
+//      32-byte-aligned shifted copies of the padded image; residual; energy
+//      partial per warp (double-buffered by k & 1).
+//   == cluster barrier; read the decision of iteration k-1 (stop -> the field
+//      after step k-1 is final); pull the s_te halo; CTA barrier
+//   B  grad = r * G s_te, u0 = u - tau*grad (solver.py:133,189)
+//   == cluster barrier; pull u0 halo; CTA barrier
+//   C  umbrella smoothing (one more exchange per extra pass) + domain clamp;
+//      then the control warp reduces every CTA's energy partials of iteration
+//      k in one fixed order (identical in every CTA) and runs the divergence /
+//      tolerance logic of solver.py:174-195 off the critical path.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -22,62 +36,88 @@ namespace mrb {
 
 namespace cg = cooperative_groups;
 
-constexpr int kClusterThreads = 768;  // nodes per CTA (one per thread)
-constexpr int kMaxDeg = 12;           // one-ring entries staged per node
-// dynamic shared memory of the kernel: G coefficients + neighbour codes
-constexpr size_t kClusterDynSmem =
-    size_t(kMaxDeg) * kClusterThreads * (sizeof(float2) + sizeof(uint16_t));
+constexpr int kClusterThreads = 768;  // threads per CTA
+constexpr int kMaxDeg = 16;           // largest one-ring the fast path accepts
+constexpr int kWarps = kClusterThreads / 32;
+constexpr int kCtlWarp = kWarps - 1;  // owns the fewest nodes when chunk < SLOTS
 
 struct ClusterPair {
   const double2* V;           // device-order vertices
-  const uint16_t* codes;      // [kMaxDeg][n]: rank << 12 | local index
-  const float2* g;            // [kMaxDeg][n]: fused gradient coefficients
   const float2* g_self;       // [n]
   const float* inv_val;       // [n]
+  // SELL-32 topology, CTA r's block at r * topo_stride entries:
+  const uint16_t* codes;      // local index: own slot, or SLOTS + halo index
+  const float2* g;            // fused gradient coefficients
+  const uint32_t* slice_off;  // [CS][slices]: entry offset of each 32-slot slice
+  const uint32_t* halo;       // [CS][halo_stride]: rank << 16 | slot to pull
+  const int* n_halo;          // [CS]
   const unsigned char* deg;   // [n]
-  const float* img;           // interleaved (Te, Re), H*W*2
+  const float2* img4;         // 4 shifted copies of the padded (Te, Re) image
   float2* u;                  // [n] final displacement (device order)
   double2* u_out;             // [n] reference order
   const int* perm;
   double* trace;
+  long long* prof;            // optional phase timestamps (MESHREG_B200_PROFILE_PHASES)
   int n, chunk, W, H;
+  int topo_stride, slices, halo_stride, pitch;
+  int plane;
 };
 
-// Sampling with the border path kept out of line (register pressure).
-__device__ __noinline__ Px<float, float, 2> cr_sample_border(const float* img, int W, int H,
-                                                             double x, double y) {
-  return cr_sample<float, float, 2>(img, W, H, x, y);
+// Four copies of the padded (H+2)x(W+2) (Te, Re) image; copy s holds padded
+// element x at column x + s of a row of `pitch` (a multiple of 4) float2, so
+// any 4-tap row starting at column cx is one 32-byte-aligned 256-bit load in
+// copy (4 - cx % 4) % 4.  The ring holds the reference's extrapolation
+// (image.py:62-71,134-148), computed in fp64 and rounded to fp32.
+__global__ void k_pad_image4(const float* __restrict__ img, size_t img_stride, int W, int H,
+                             float2* __restrict__ out, int pitch, size_t plane,
+                             size_t out_stride) {
+  const int Wp = W + 2, Hp = H + 2;
+  const float* src = img + blockIdx.y * img_stride;
+  float2* dst = out + blockIdx.y * out_stride;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Wp * Hp; q += gridDim.x * blockDim.x) {
+    const int r = q / Wp, c = q - r * Wp;
+    const Px<float, double, 2> v = ext_tap<float, double, 2>(src, W, H, r, c);
+    const float2 f = make_float2(float(v.v[0]), float(v.v[1]));
+#pragma unroll
+    for (int s = 0; s < 4; ++s) dst[s * plane + size_t(r) * pitch + c + s] = f;
+  }
 }
 
-__device__ __forceinline__ Px<float, float, 2> cr_sample_fast(const float* __restrict__ img,
-                                                             int W, int H, double x, double y) {
-  const double xc = fmin(fmax(x, 0.0), double(W) - 1.0);
-  const double yc = fmin(fmax(y, 0.0), double(H) - 1.0);
-  const int cx = min(int(floor(xc)), W - 2);
-  const int cy = min(int(floor(yc)), H - 2);
-  if (!(cx >= 1 && cx <= W - 3 && cy >= 1 && cy <= H - 3)) return cr_sample_border(img, W, H, x, y);
-  float wx[4], wy[4];
-  cr_weights<float>(float(xc - double(cx)), wx);
-  cr_weights<float>(float(yc - double(cy)), wy);
-  const float2* base = reinterpret_cast<const float2*>(img) + (size_t(cy - 1) * W + (cx - 1));
-  Px<float, float, 2> acc;
-  acc.v[0] = acc.v[1] = 0.f;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const float2* row = base + size_t(j) * W;
-    const float2 t0 = __ldg(row), t1 = __ldg(row + 1), t2 = __ldg(row + 2), t3 = __ldg(row + 3);
-    float rt = wx[0] * t0.x;
-    rt = fmaf(wx[1], t1.x, rt);
-    rt = fmaf(wx[2], t2.x, rt);
-    rt = fmaf(wx[3], t3.x, rt);
-    float rr = wx[0] * t0.y;
-    rr = fmaf(wx[1], t1.y, rr);
-    rr = fmaf(wx[2], t2.y, rr);
-    rr = fmaf(wx[3], t3.y, rr);
-    acc.v[0] = fmaf(wy[j], rt, acc.v[0]);
-    acc.v[1] = fmaf(wy[j], rr, acc.v[1]);
-  }
-  return acc;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(rank));
+  return out;
+}
+
+__device__ __forceinline__ float ld_dsmem_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ float2 ld_dsmem_f32x2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];"
+               : "=f"(v.x), "=f"(v.y)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ double ld_dsmem_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ int ld_dsmem_s32(uint32_t addr) {
+  int v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -86,221 +126,362 @@ __device__ __forceinline__ void cluster_sync_all() {
                "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-template <int CS>
+// one 4-tap (Te, Re) row: a single 256-bit read-only load
+__device__ __forceinline__ void ld_row4(const float2* p, float2 (&t)[4]) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(t[0].x), "=f"(t[0].y), "=f"(t[1].x), "=f"(t[1].y), "=f"(t[2].x),
+                 "=f"(t[2].y), "=f"(t[3].x), "=f"(t[3].y)
+               : "l"(p));
+}
+
+// Catmull-Rom window of (Te, Re) at (x, y) (ImageGrid.sample, image.py:73-84,
+// _locate 105-116) in the aligned padded copies: base row pointer + weights.
+struct Window {
+  const float2* base;
+  float wx[4], wy[4];
+};
+
+__device__ __forceinline__ Window locate(const ClusterPair& d, double x, double y) {
+  const double xc = fmin(fmax(x, 0.0), double(d.W) - 1.0);
+  const double yc = fmin(fmax(y, 0.0), double(d.H) - 1.0);
+  const int cx = min(int(xc), d.W - 2);  // xc >= 0: truncation == floor
+  const int cy = min(int(yc), d.H - 2);
+  Window w;
+  cr_weights<float>(float(xc - double(cx)), w.wx);
+  cr_weights<float>(float(yc - double(cy)), w.wy);
+  const int s = (4 - (cx & 3)) & 3;
+  w.base = d.img4 + size_t(s) * d.plane + size_t(cy) * d.pitch + cx + s;
+  return w;
+}
+
+__device__ __forceinline__ float2 combine(const Window& w, const float2 (&t)[4][4]) {
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float rt = w.wx[0] * t[j][0].x, rr = w.wx[0] * t[j][0].y;
+#pragma unroll
+    for (int i = 1; i < 4; ++i) {
+      rt = fmaf(w.wx[i], t[j][i].x, rt);
+      rr = fmaf(w.wx[i], t[j][i].y, rr);
+    }
+    acc.x = fmaf(w.wy[j], rt, acc.x);
+    acc.y = fmaf(w.wy[j], rr, acc.y);
+  }
+  return acc;
+}
+
+// np.clip(u1, -V, (W-1) - V) (solver.py:140-144) evaluated in fp64 and
+// rounded to fp32 equals the fp32 clip against the rounded bounds (rounding
+// is monotonic), which is what this computes.
+__device__ __forceinline__ float2 clamp_dom(float2 v, double2 V, int W, int H) {
+  const float lox = float(-V.x), hix = float((double(W) - 1.0) - V.x);
+  const float loy = float(-V.y), hiy = float((double(H) - 1.0) - V.y);
+  return make_float2(fminf(fmaxf(v.x, lox), hix), fminf(fmaxf(v.y, loy), hiy));
+}
+
+// Dynamic shared memory layout (host: cluster_dyn_smem).
+struct ClusterSmem {
+  double2* V;
+  float2 *gs, *xu0, *xu1;
+  float *iv, *xs;
+  unsigned char* deg;
+  uint32_t* halo;
+  float2* g;
+  uint16_t* code;
+  uint32_t* soff;
+};
+
+template <int NPT>
+__device__ __forceinline__ ClusterSmem carve(unsigned char* p, const ClusterPair& d, bool two) {
+  constexpr int SLOTS = kClusterThreads * NPT;
+  const int X = SLOTS + d.halo_stride;  // own slots followed by the halo
+  ClusterSmem s;
+  s.V = reinterpret_cast<double2*>(p);
+  s.gs = reinterpret_cast<float2*>(s.V + SLOTS);
+  s.xu0 = s.gs + SLOTS;
+  s.xu1 = s.xu0 + X;
+  s.iv = reinterpret_cast<float*>(s.xu1 + (two ? X : 0));
+  s.xs = s.iv + SLOTS;
+  s.halo = reinterpret_cast<uint32_t*>(s.xs + X);
+  s.g = reinterpret_cast<float2*>(s.halo + d.halo_stride);  // halo_stride % 2 == 0
+  s.code = reinterpret_cast<uint16_t*>(s.g + d.topo_stride);
+  s.soff = reinterpret_cast<uint32_t*>(s.code + d.topo_stride);  // topo_stride % 2 == 0
+  s.deg = reinterpret_cast<unsigned char*>(s.soff + d.slices);
+  return s;
+}
+
+// one-ring gather: sum_e coef(e) * val[code(e)] for the SELL entries of a slot,
+// codes fetched in batches of 8 ahead of the values they index
+template <typename F>
+__device__ __forceinline__ void ring_gather(const ClusterSmem& sm, uint32_t so, int deg, F&& f) {
+#pragma unroll
+  for (int e0 = 0; e0 < kMaxDeg; e0 += 8) {
+    if (e0 < deg) {
+      uint32_t c[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) c[e] = (e0 + e < deg) ? sm.code[so + 32u * (e0 + e)] : 0u;
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (e0 + e < deg) f(e0 + e, c[e]);
+    }
+  }
+}
+
+template <int CS, int NPT>
 __global__ void __launch_bounds__(kClusterThreads, 1)
     k_cluster_register(const ClusterPair* __restrict__ pairs, PairStatus* __restrict__ st,
                        int max_iter, double tol, float tau, float lam, int passes) {
+  constexpr int SLOTS = kClusterThreads * NPT;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = int(cluster.block_rank());
   const int p = blockIdx.x / CS;
   const ClusterPair& d = pairs[p];
-  const int t = threadIdx.x;
-  const int i = rank * d.chunk + t;
-  const bool own = (t < d.chunk) && (i < d.n);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
 
-  __shared__ float s_ste[kClusterThreads];
-  __shared__ float2 s_u0[kClusterThreads];
-  __shared__ float2 s_u1[kClusterThreads];
-  __shared__ double s_part;     // this CTA's energy partial
-  __shared__ int s_gradbad;     // non-finite gradient seen in this CTA
-  __shared__ double s_warp[kClusterThreads / 32];
-  __shared__ int s_ctl[2];      // [0] = stop after this iteration, [1] = error
-  // descent control state (thread 0 only; identical in every CTA)
+  __shared__ double s_wpart[2][kWarps];  // per-warp energy partials, by iteration parity
+  __shared__ int s_gradbad;              // non-finite gradient seen in this CTA
+  __shared__ int s_stop;                 // decision so far: 0 go, 1 error, 2 converged
+  __shared__ int s_nhalo;
+  // descent control state (control warp lane 0 only; identical in every CTA)
   __shared__ double s_hist[6];
   __shared__ double s_prev;
-  __shared__ int s_cs[4];       // rises, iters, err, err_iter
-  __shared__ const float* s_rste[CS];
-  __shared__ const float2* s_ru0[CS];
-  __shared__ const float2* s_ru1[CS];
+  __shared__ int s_cs[4];                // rises, iters, err, err_iter
   extern __shared__ __align__(16) unsigned char s_dyn[];
-  float2* s_g = reinterpret_cast<float2*>(s_dyn);                          // [e][t]
-  uint16_t* s_code = reinterpret_cast<uint16_t*>(s_g + kMaxDeg * kClusterThreads);  // [e][t]
+  const ClusterSmem sm = carve<NPT>(s_dyn, d, passes >= 2);
 
-  if (t < CS) {
-    s_rste[t] = cluster.map_shared_rank(s_ste, t);
-    s_ru0[t] = cluster.map_shared_rank(s_u0, t);
-    s_ru1[t] = cluster.map_shared_rank(s_u1, t);
-  }
   if (t == 0) {
     s_gradbad = 0;
+    s_stop = 0;
     s_prev = 0.0;
     s_cs[0] = s_cs[1] = s_cs[2] = s_cs[3] = 0;
+    s_nhalo = d.n_halo[rank];
   }
-
-  // ---- node state into registers, one-ring topology into shared memory
-  double2 V = make_double2(0.0, 0.0);
-  float2 gs = make_float2(0.f, 0.f);
-  float iv = 0.f;
-  int deg = 0;
-  if (own) {
-    V = d.V[i];
-    gs = d.g_self[i];
-    iv = d.inv_val[i];
-    deg = d.deg[i];
-    for (int e = 0; e < deg; ++e) {
-      s_code[e * kClusterThreads + t] = d.codes[size_t(e) * d.n + i];
-      s_g[e * kClusterThreads + t] = d.g[size_t(e) * d.n + i];
+  // ---- stage this CTA's topology and halo list (coalesced block copies)
+  {
+    const size_t tb = size_t(rank) * d.topo_stride;
+    for (int q = t; q < d.topo_stride; q += kClusterThreads) {
+      sm.g[q] = d.g[tb + q];
+      sm.code[q] = d.codes[tb + q];
     }
+    for (int q = t; q < d.slices; q += kClusterThreads)
+      sm.soff[q] = d.slice_off[size_t(rank) * d.slices + q];
+    for (int q = t; q < d.halo_stride; q += kClusterThreads)
+      sm.halo[q] = d.halo[size_t(rank) * d.halo_stride + q];
   }
-  float2 u = make_float2(0.f, 0.f);
-  float r = 0.f;
-  cluster_sync_all();  // remote smem pointers / flags initialised everywhere
+  // ---- per-node constants into shared memory, evolving state in registers
+  float2 u[NPT];
+  float r[NPT];
+  unsigned own_mask = 0;
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) {
+    const int slot = t + j * kClusterThreads;
+    const int nd = rank * d.chunk + slot;
+    const bool o = slot < d.chunk && nd < d.n;
+    own_mask |= unsigned(o) << j;
+    sm.V[slot] = o ? d.V[nd] : make_double2(0.0, 0.0);
+    sm.gs[slot] = o ? d.g_self[nd] : make_float2(0.f, 0.f);
+    sm.iv[slot] = o ? d.inv_val[nd] : 0.f;
+    sm.deg[slot] = o ? d.deg[nd] : 0;
+    u[j] = make_float2(0.f, 0.f);
+    r[j] = 0.f;
+  }
+#define OWN(j) ((own_mask >> (j)) & 1u)
+  const uint32_t wpart_addr = smem_u32(&s_wpart[0][0]), bad_addr = smem_u32(&s_gradbad);
+  const uint32_t xs_addr = smem_u32(sm.xs), xu0_addr = smem_u32(sm.xu0),
+                 xu1_addr = smem_u32(sm.xu1);
+  cluster_sync_all();  // every CTA started and staged
+  const int nhalo = s_nhalo;
+
+  long long* const prof =
+      (d.prof && t == 0) ? d.prof + (size_t(blockIdx.x) * 8) * 16 : nullptr;
+#define PROF(k, slot) \
+  if (prof && (k) < 8) prof[(k) * 16 + (slot)] = clock64();
+
+  // Control step of iteration kk (control warp, all CTAs identically):
+  // fixed-order cluster reduction of the energy partials, then the logic of
+  // solver.py:176-195 in the reference's order (energy checks, the step's
+  // gradient check, tolerance).
+  auto control = [&](int kk) {
+    double v = 0.0;
+    for (int idx = lane; idx < CS * kWarps; idx += 32)
+      v += ld_dsmem_f64(mapa_u32(wpart_addr, idx / kWarps) +
+                        8u * ((kk & 1) * kWarps + idx % kWarps));
+    int gb = lane < CS ? ld_dsmem_s32(mapa_u32(bad_addr, lane)) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v += __shfl_down_sync(0xffffffffu, v, o);
+      gb |= __shfl_down_sync(0xffffffffu, gb, o);
+    }
+    if (lane == 0 && s_stop == 0) {
+      int stop = 0, rises = s_cs[0], err = ERR_NONE, err_iter = 0;
+      const double e = 0.5 * v;
+      const double prev = s_prev;
+      if (!isfinite(e)) {  // solver.py:176-177
+        err = ERR_NONFINITE_ENERGY;
+        err_iter = kk;
+        stop = 1;
+      } else if (kk > 0 && e > __dadd_rn(__dmul_rn(prev, 1.0 + 1e-4), 1e-12)) {
+        if (++rises >= 10) {  // material_rise, solver.py:43-44,178-184
+          err = ERR_RISES;
+          err_iter = kk;
+          stop = 1;
+        }
+      } else if (kk > 0 && e <= prev) {
+        rises = 0;  // solver.py:185-186
+      }
+      if (!stop && gb) {  // step(): non-finite gradient, solver.py:131-132
+        err = ERR_NONFINITE_GRAD;
+        err_iter = kk;
+        stop = 1;
+      }
+      if (!stop) {
+        s_cs[1] = kk + 1;
+        s_hist[kk % 6] = e;
+        if (kk + 1 >= 6) {  // solver.py:192-195; trace[-6] == hist[(kk+1)%6]
+          const double base = s_hist[(kk + 1) % 6];
+          if (fabs(__dsub_rn(e, base)) <= __dmul_rn(tol, fmax(fabs(base), 1e-12))) stop = 2;
+        }
+      }
+      if (rank == 0) d.trace[kk] = e;
+      s_prev = e;
+      s_cs[0] = rises;
+      s_cs[2] = err;
+      s_cs[3] = err_iter;
+      s_stop = stop;
+    }
+  };
 
   int k = 0;
   for (; k < max_iter; ++k) {
+    PROF(k, 0)
     // -------- phase A: sample Te, Re at V + u; residual; energy partial
-    double e2 = 0.0;
-    if (own) {
-      const Px<float, float, 2> s = cr_sample_fast(d.img, d.W, d.H, V.x + double(u.x),
-                                                   V.y + double(u.y));
-      r = s.v[0] - s.v[1];
-      s_ste[t] = s.v[0];
-      e2 = double(r) * double(r);
-    }
+    {
+      double e2 = 0.0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) e2 += __shfl_down_sync(0xffffffffu, e2, o);
-    if ((t & 31) == 0) s_warp[t >> 5] = e2;
-    __syncthreads();
-    if (t == 0) {
-      double s = 0.0;
+      for (int j = 0; j < NPT; ++j) {  // one node at a time: no register spills
+        if (OWN(j)) {
+          const double2 V = sm.V[t + j * kClusterThreads];
+          const Window w = locate(d, V.x + double(u[j].x), V.y + double(u[j].y));
+          float2 tap[4][4];
 #pragma unroll
-      for (int w = 0; w < kClusterThreads / 32; ++w) s += s_warp[w];
-      s_part = s;
-    }
-    cluster_sync_all();  // #1: s_ste and partials visible cluster-wide
-    if (t < 32) {
-      // fixed-order cluster reduction, identical in every CTA
-      double v = 0.0;
-      int gb = 0;
-      if (t < CS) {
-        v = *cluster.map_shared_rank(&s_part, t);
-        gb = *cluster.map_shared_rank(&s_gradbad, t);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        v += __shfl_down_sync(0xffffffffu, v, o);
-        gb |= __shfl_down_sync(0xffffffffu, gb, o);
-      }
-      if (t == 0) {
-        int stop = 0;
-        int rises = s_cs[0], err = s_cs[2];
-        if (gb) {  // non-finite gradient in the previous step (solver.py:131-132)
-          err = ERR_NONFINITE_GRAD;
-          s_cs[3] = k - 1;
-          stop = 1;
-        } else {
-          const double e = 0.5 * v;
-          const double prev = s_prev;
-          if (!isfinite(e)) {  // solver.py:176-177
-            err = ERR_NONFINITE_ENERGY;
-            s_cs[3] = k;
-            stop = 1;
-          } else {
-            if (k > 0) {  // material_rise, solver.py:43-44,178-186
-              const double thr = __dadd_rn(__dmul_rn(prev, 1.0 + 1e-4), 1e-12);
-              if (e > thr) {
-                if (++rises >= 10) {
-                  err = ERR_RISES;
-                  s_cs[3] = k;
-                  stop = 1;
-                }
-              } else if (e <= prev) {
-                rises = 0;
-              }
-            }
-            if (!stop) {
-              s_cs[1] = k + 1;
-              s_hist[k % 6] = e;
-              if (k + 1 >= 6) {  // solver.py:192-195; trace[-6] == hist[(k+1)%6]
-                const double base = s_hist[(k + 1) % 6];
-                if (fabs(__dsub_rn(e, base)) <= __dmul_rn(tol, fmax(fabs(base), 1e-12)))
-                  stop = 2;  // take this step, then stop
-              }
-            }
-          }
-          if (rank == 0) d.trace[k] = e;
-          s_prev = e;
+          for (int row = 0; row < 4; ++row) ld_row4(w.base + size_t(row) * d.pitch, tap[row]);
+          const float2 s = combine(w, tap);
+          r[j] = s.x - s.y;
+          sm.xs[t + j * kClusterThreads] = s.x;
+          e2 = fma(double(r[j]), double(r[j]), e2);
         }
-        s_cs[0] = rises;
-        s_cs[2] = err;
-        s_ctl[0] = stop;
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) e2 += __shfl_down_sync(0xffffffffu, e2, o);
+      if (lane == 0) s_wpart[k & 1][warp] = e2;
     }
-    __syncthreads();
-    const int stop = s_ctl[0];
-    if (stop == 1) break;
+    PROF(k, 1)
+    cluster_sync_all();  // s_te, energy partials (and the k-1 decision) visible
+    PROF(k, 2)
+    if (s_stop) break;   // iteration k-1 was the last one (u untouched since)
+    for (int h = t; h < nhalo; h += kClusterThreads) {  // pull the s_te halo
+      const uint32_t c = sm.halo[h];
+      sm.xs[SLOTS + h] = ld_dsmem_f32(mapa_u32(xs_addr, c >> 16) + 4u * (c & 0xffffu));
+    }
+    PROF(k, 3)
+    __syncthreads();  // s_te halo complete
+    PROF(k, 4)
 
     // -------- phase B: gradient via the fused one-ring operator, descent
     bool bad = false;
-    if (own) {
-      const float si = s_ste[t];
-      float gx = gs.x * si, gy = gs.y * si;
-      for (int e = 0; e < deg; ++e) {
-        const uint32_t c = s_code[e * kClusterThreads + t];
-        const float2 ge = s_g[e * kClusterThreads + t];
-        const float sj = s_rste[c >> 12][c & 0xfff];
-        gx = fmaf(ge.x, sj, gx);
-        gy = fmaf(ge.y, sj, gy);
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+      if (OWN(j)) {
+        const int slot = t + j * kClusterThreads;
+        const uint32_t so = sm.soff[slot >> 5] + (slot & 31);
+        const float si = sm.xs[slot];
+        const float2 gs = sm.gs[slot];
+        float gx = gs.x * si, gy = gs.y * si;
+        ring_gather(sm, so, sm.deg[slot], [&](int e, uint32_t c) {
+          const float sj = sm.xs[c];
+          const float2 ge = sm.g[so + 32u * e];
+          gx = fmaf(ge.x, sj, gx);
+          gy = fmaf(ge.y, sj, gy);
+        });
+        const float dx = r[j] * gx, dy = r[j] * gy;  // solver.py:189
+        bad |= !isfinite(dx) || !isfinite(dy);
+        sm.xu0[slot] = make_float2(u[j].x - tau * dx, u[j].y - tau * dy);  // solver.py:133
       }
-      const float dx = r * gx, dy = r * gy;
-      bad = !isfinite(dx) || !isfinite(dy);
-      s_u0[t] = make_float2(u.x - tau * dx, u.y - tau * dy);
     }
+    PROF(k, 5)
     if (__syncthreads_or(bad) && t == 0) s_gradbad = 1;
-    cluster_sync_all();  // #2: u0 visible cluster-wide
+    PROF(k, 6)
 
     // -------- phase C: umbrella smoothing passes + domain clamp
     if (passes == 0) {
-      if (own) {
-        const float2 v = s_u0[t];
-        u.x = float(fmin(fmax(double(v.x), -V.x), (double(d.W) - 1.0) - V.x));
-        u.y = float(fmin(fmax(double(v.y), -V.y), (double(d.H) - 1.0) - V.y));
+      cluster_sync_all();  // gradbad flags visible; s_te halo reads of all CTAs done
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) {
+        if (OWN(j)) {
+          const int slot = t + j * kClusterThreads;
+          u[j] = clamp_dom(sm.xu0[slot], sm.V[slot], d.W, d.H);
+        }
       }
     }
     for (int q = 0; q < passes; ++q) {
-      const float2* const* src = (q & 1) ? s_ru1 : s_ru0;
-      float2 v = make_float2(0.f, 0.f);
-      if (own) {
-        float ax = 0.f, ay = 0.f;
-        for (int e = 0; e < deg; ++e) {
-          const uint32_t c = s_code[e * kClusterThreads + t];
-          const float2 uj = src[c >> 12][c & 0xfff];
-          ax = fmaf(iv, uj.x, ax);
-          ay = fmaf(iv, uj.y, ay);
+      float2* src = (q & 1) ? sm.xu1 : sm.xu0;
+      const uint32_t src_addr = (q & 1) ? xu1_addr : xu0_addr;
+      PROF(k, 7)
+      cluster_sync_all();  // src (and the gradbad flags) visible cluster-wide
+      PROF(k, 8)
+      for (int h = t; h < nhalo; h += kClusterThreads) {  // pull the halo of src
+        const uint32_t c = sm.halo[h];
+        src[SLOTS + h] = ld_dsmem_f32x2(mapa_u32(src_addr, c >> 16) + 8u * (c & 0xffffu));
+      }
+      PROF(k, 9)
+      __syncthreads();
+      PROF(k, 10)
+      float2 v[NPT];
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) {
+        v[j] = make_float2(0.f, 0.f);
+        if (OWN(j)) {
+          const int slot = t + j * kClusterThreads;
+          const uint32_t so = sm.soff[slot >> 5] + (slot & 31);
+          const float iv = sm.iv[slot];
+          float ax = 0.f, ay = 0.f;
+          ring_gather(sm, so, sm.deg[slot], [&](int, uint32_t c) {  // (L u)_i, L_ij = 1/val_i
+            const float2 uj = src[c];
+            ax = fmaf(iv, uj.x, ax);
+            ay = fmaf(iv, uj.y, ay);
+          });
+          const float2 si = src[slot];
+          const float om = 1.f - lam;  // (1 - lam) u + lam (L u), mesh.py:281
+          v[j] = make_float2(om * si.x + lam * ax, om * si.y + lam * ay);
         }
-        const float2 si = src[rank][t];
-        const float om = 1.f - lam;
-        v = make_float2(om * si.x + lam * ax, om * si.y + lam * ay);
       }
       if (q == passes - 1) {
-        if (own) {
-          u.x = float(fmin(fmax(double(v.x), -V.x), (double(d.W) - 1.0) - V.x));
-          u.y = float(fmin(fmax(double(v.y), -V.y), (double(d.H) - 1.0) - V.y));
-        }
+#pragma unroll
+        for (int j = 0; j < NPT; ++j)
+          if (OWN(j)) u[j] = clamp_dom(v[j], sm.V[t + j * kClusterThreads], d.W, d.H);
       } else {
-        if (own) ((q & 1) ? s_u0 : s_u1)[t] = v;
-        cluster_sync_all();
+        float2* dst = (q & 1) ? sm.xu0 : sm.xu1;
+#pragma unroll
+        for (int j = 0; j < NPT; ++j)
+          if (OWN(j)) dst[t + j * kClusterThreads] = v[j];
       }
     }
-    if (stop == 2) {
-      ++k;
-      break;
+    // -------- control of iteration k, off the critical path; its decision is
+    // read by every thread after the next cluster barrier
+    if (warp == kCtlWarp) control(k);
+    PROF(k, 11)
+  }
+#undef PROF
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) {
+    if (OWN(j)) {
+      const int nd = rank * d.chunk + t + j * kClusterThreads;
+      d.u[nd] = u[j];
+      d.u_out[d.perm[nd]] = make_double2(double(u[j].x), double(u[j].y));
     }
   }
-  // final gradient-finiteness check of the last step taken
-  cluster_sync_all();
-  if (t == 0 && s_cs[2] == ERR_NONE) {
-    int gb = 0;
-    for (int c = 0; c < CS; ++c) gb |= *cluster.map_shared_rank(&s_gradbad, c);
-    if (gb) {
-      s_cs[2] = ERR_NONFINITE_GRAD;
-      s_cs[3] = k - 1;
-    }
-  }
-  if (own) {
-    d.u[i] = u;
-    d.u_out[d.perm[i]] = make_double2(double(u.x), double(u.y));
-  }
+#undef OWN
+  __syncthreads();
   if (rank == 0 && t == 0) {
     PairStatus s{};
     s.stop_iter = k;

@@ -47,12 +47,16 @@ struct DeviceMesh {
   double* inv_val_d = nullptr;
   std::map<std::pair<int, int>, int*> pixel_maps;
   // cluster fast path: register topology packed for a given chunk size
-  struct Topo {
+  struct Topo {  // SELL-32 one-ring layout for one (cluster size, nodes/thread)
     uint16_t* codes = nullptr;
     float2* g = nullptr;
+    uint32_t* slice_off = nullptr;
+    uint32_t* halo = nullptr;
+    int* n_halo = nullptr;
     unsigned char* deg = nullptr;
+    int chunk = 0, topo_stride = 0, slices = 0, halo_stride = 0;
   };
-  std::map<int, Topo> topo;
+  std::map<int, Topo> topo;  // key: chunk size
   int max_deg = 0;
   ~DeviceMesh() {
     int cur = -1;
@@ -66,6 +70,9 @@ struct DeviceMesh {
     for (auto& kv : topo) {
       cudaFree(kv.second.codes);
       cudaFree(kv.second.g);
+      cudaFree(kv.second.slice_off);
+      cudaFree(kv.second.halo);
+      cudaFree(kv.second.n_halo);
       cudaFree(kv.second.deg);
     }
     if (cur >= 0) cudaSetDevice(cur);
@@ -205,32 +212,94 @@ void ensure_device_mesh(mrb_ctx* ctx, HostMesh& h) {
   ck(cudaStreamSynchronize(s));  // host vectors above go out of scope
 }
 
-// Register-resident topology of the cluster kernel for chunk size `chunk`:
-// entry-major [kMaxDeg][n] neighbour codes (owning CTA rank << 12 | local
-// index) and fused-gradient coefficients, plus the valence.
-const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int chunk) {
+// Shared-memory topology of the cluster kernel for `cs` CTAs of `chunk` nodes
+// and `npt` slots per thread:
+//  * SELL-32 one-rings — for every 32-slot slice of a CTA's chunk, entry e of
+//    slot s sits at slice_off[slice] + 32 e + s % 32, padded to the slice's
+//    largest one-ring; every CTA block is padded to the same stride;
+//  * codes are CTA-local indices into [own slots (SLOTS = 768*npt) | halo];
+//  * halo[r] lists (owner rank << 16 | owner slot) of every remote node CTA r's
+//    one-rings reference, in first-reference order.
+const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, int chunk,
+                                            int npt) {
   DeviceMesh& d = *h.dev;
-  auto it = d.topo.find(chunk);
+  const int key = chunk * 4 + npt;
+  auto it = d.topo.find(key);
   if (it != d.topo.end()) return it->second;
-  const size_t n = size_t(h.n);
-  std::vector<uint16_t> codes(kMaxDeg * n, 0);
-  std::vector<float2> g(kMaxDeg * n, make_float2(0.f, 0.f));
+  const int n = int(h.n);
+  const int SLOTS = kClusterThreads * npt;
+  const int slices = (chunk + 31) / 32;
+  std::vector<uint32_t> soff(size_t(cs) * slices, 0);
+  int stride = 0;
+  std::vector<std::vector<uint32_t>> halos(cs);
+  std::vector<std::map<int, int>> halo_index(cs);
+  for (int r = 0; r < cs; ++r) {
+    int acc = 0;
+    for (int sl = 0; sl < slices; ++sl) {
+      soff[size_t(r) * slices + sl] = uint32_t(acc);
+      int mx = 0;
+      for (int s = sl * 32; s < std::min(chunk, sl * 32 + 32); ++s) {
+        const int i = r * chunk + s;
+        if (i >= n) continue;
+        mx = std::max(mx, h.nb_ptr[i + 1] - h.nb_ptr[i]);
+        for (int q = h.nb_ptr[i]; q < h.nb_ptr[i + 1]; ++q) {
+          const int j = h.nb_idx[q];
+          if (j / chunk != r && !halo_index[r].count(j)) {
+            halo_index[r][j] = int(halos[r].size());
+            halos[r].push_back(uint32_t((j / chunk) << 16 | (j % chunk)));
+          }
+        }
+      }
+      acc += 32 * mx;
+    }
+    stride = std::max(stride, acc);
+  }
+  stride = std::max((stride + 7) / 8 * 8, 8);
+  int hstride = 2;
+  for (auto& hl : halos) hstride = std::max<int>(hstride, int(hl.size()));
+  hstride = (hstride + 31) / 32 * 32;
+  std::vector<uint16_t> codes(size_t(cs) * stride, 0);
+  std::vector<float2> g(size_t(cs) * stride, make_float2(0.f, 0.f));
   std::vector<unsigned char> deg(n);
-  for (size_t i = 0; i < n; ++i) {
+  for (int i = 0; i < n; ++i) {
+    const int r = i / chunk, s = i % chunk;
     const int b = h.nb_ptr[i], e = h.nb_ptr[i + 1];
     deg[i] = (unsigned char)(e - b);
+    const size_t base = size_t(r) * stride + soff[size_t(r) * slices + s / 32] + (s % 32);
     for (int q = b; q < e; ++q) {
       const int j = h.nb_idx[q];
-      codes[size_t(q - b) * n + i] = uint16_t(((j / chunk) << 12) | (j % chunk));
-      g[size_t(q - b) * n + i] = make_float2(float(h.g_nb[2 * q]), float(h.g_nb[2 * q + 1]));
+      const int code = (j / chunk == r) ? (j % chunk) : SLOTS + halo_index[r][j];
+      codes[base + 32 * size_t(q - b)] = uint16_t(code);
+      g[base + 32 * size_t(q - b)] = make_float2(float(h.g_nb[2 * q]), float(h.g_nb[2 * q + 1]));
     }
   }
+  std::vector<uint32_t> hl(size_t(cs) * hstride, 0);
+  std::vector<int> nh(cs);
+  for (int r = 0; r < cs; ++r) {
+    nh[r] = int(halos[r].size());
+    std::copy(halos[r].begin(), halos[r].end(), hl.begin() + size_t(r) * hstride);
+  }
   DeviceMesh::Topo t;
+  t.chunk = chunk;
+  t.topo_stride = stride;
+  t.slices = slices;
+  t.halo_stride = hstride;
   t.codes = dupload(codes.data(), codes.size(), ctx->stream);
   t.g = dupload(g.data(), g.size(), ctx->stream);
+  t.slice_off = dupload(soff.data(), soff.size(), ctx->stream);
+  t.halo = dupload(hl.data(), hl.size(), ctx->stream);
+  t.n_halo = dupload(nh.data(), nh.size(), ctx->stream);
   t.deg = dupload(deg.data(), deg.size(), ctx->stream);
   ck(cudaStreamSynchronize(ctx->stream));
-  return d.topo[chunk] = t;
+  return d.topo[key] = t;
+}
+
+// bytes of dynamic shared memory of k_cluster_register (ClusterSmem carve)
+size_t cluster_dyn_smem(int npt, int topo_stride, int slices, int halo_stride, bool two_u) {
+  const size_t S = size_t(kClusterThreads) * npt, X = S + halo_stride;
+  return S * (sizeof(double2) + sizeof(float2) + sizeof(float) + 1) +
+         X * (sizeof(float2) * (two_u ? 2 : 1) + sizeof(float)) + size_t(halo_stride) * 4 +
+         size_t(topo_stride) * (sizeof(float2) + sizeof(uint16_t)) + size_t(slices) * 4;
 }
 
 // Pixel->triangle map for (W, H): GPU raster + host locate fallback.
@@ -323,8 +392,13 @@ struct mrb_batch {
   cudaGraphExec_t graph = nullptr;
   std::vector<const void*> graph_src;
   // cluster fast path (0 = generic three-kernel loop)
-  int cluster_cs = 0;
-  void* cpairs = nullptr;  // ClusterPair[n_pairs]
+  int cluster_cs = 0, cluster_npt = 1;
+  size_t cluster_smem = 0;
+  int pad_pitch = 0;
+  size_t pad_plane = 0;
+  void* cpairs = nullptr;     // ClusterPair[n_pairs]
+  long long* phase_prof = nullptr;  // MESHREG_B200_PROFILE_PHASES
+  float2* img_pad = nullptr;  // 4 shifted padded (H+2)x(W+2) (Te, Re) copies per pair
   int runs = 0;
   // host results
   std::vector<PairStatus> h_st;
@@ -333,7 +407,8 @@ struct mrb_batch {
   ~mrb_batch() {
     if (graph) cudaGraphExecDestroy(graph);
     void* ptrs[] = {pairs, st, blk_pair, pix_blk_pair, partials, pix_partials, state, traces,
-                    img, stage, src_ptrs, img_ptrs, dense, u_out, conv, cpairs};
+                    img, stage, src_ptrs, img_ptrs, dense, u_out, conv, cpairs, img_pad,
+                    phase_prof};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
@@ -449,12 +524,12 @@ struct KernelTimer {
   }
 };
 
-template <int CS>
+template <int CS, int NPT>
 void launch_cluster_t(mrb_batch* b) {
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(unsigned(b->n_pairs * CS));
   lc.blockDim = dim3(kClusterThreads);
-  lc.dynamicSmemBytes = kClusterDynSmem;
+  lc.dynamicSmemBytes = b->cluster_smem;
   lc.stream = b->ctx->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -463,21 +538,25 @@ void launch_cluster_t(mrb_batch* b) {
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  ck(cudaLaunchKernelEx(&lc, k_cluster_register<CS>,
+  ck(cudaLaunchKernelEx(&lc, k_cluster_register<CS, NPT>,
                         static_cast<const ClusterPair*>(b->cpairs), b->st,
                         int(b->cfg.max_iterations), double(b->cfg.energy_tolerance),
                         float(b->cfg.tau), float(b->cfg.lam), int(b->cfg.smoothing_passes)));
 }
 
-template <int CS>
-int cluster_occupancy() {
-  cudaFuncSetAttribute(k_cluster_register<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaFuncSetAttribute(k_cluster_register<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(kClusterDynSmem));
+template <int CS, int NPT>
+int cluster_occupancy(size_t smem) {
+  auto kern = k_cluster_register<CS, NPT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(unsigned(CS));
   lc.blockDim = dim3(kClusterThreads);
-  lc.dynamicSmemBytes = kClusterDynSmem;
+  lc.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CS;
@@ -486,32 +565,44 @@ int cluster_occupancy() {
   lc.attrs = attr;
   lc.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_cluster_register<CS>, &lc) != cudaSuccess) {
+  const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, kern, &lc);
+  if (e != cudaSuccess) {
+    if (std::getenv("MESHREG_B200_DEBUG"))
+      std::fprintf(stderr, "meshreg_b200: cudaOccupancyMaxActiveClusters(%d,%d): %s\n", CS, NPT,
+                   cudaGetErrorString(e));
     cudaGetLastError();
     return 0;
   }
   return n;
 }
 
-int cluster_occupancy_cs(int cs) {
-  switch (cs) {
-    case 1: return cluster_occupancy<1>();
-    case 2: return cluster_occupancy<2>();
-    case 4: return cluster_occupancy<4>();
-    case 8: return cluster_occupancy<8>();
-    case 16: return cluster_occupancy<16>();
+#define MRB_CLUSTER_SWITCH(CS_, NPT_, CALL)                      \
+  switch ((CS_) * 4 + (NPT_)) {                                  \
+    case 1 * 4 + 1: CALL(1, 1); break;                           \
+    case 2 * 4 + 1: CALL(2, 1); break;                           \
+    case 4 * 4 + 1: CALL(4, 1); break;                           \
+    case 8 * 4 + 1: CALL(8, 1); break;                           \
+    case 16 * 4 + 1: CALL(16, 1); break;                         \
+    case 1 * 4 + 2: CALL(1, 2); break;                           \
+    case 2 * 4 + 2: CALL(2, 2); break;                           \
+    case 4 * 4 + 2: CALL(4, 2); break;                           \
+    case 8 * 4 + 2: CALL(8, 2); break;                           \
+    case 16 * 4 + 2: CALL(16, 2); break;                         \
+    default: break;                                              \
   }
-  return 0;
+
+int cluster_occupancy_cs(int cs, int npt, size_t smem) {
+  int occ = 0;
+#define MRB_OCC(C, N) occ = cluster_occupancy<C, N>(smem)
+  MRB_CLUSTER_SWITCH(cs, npt, MRB_OCC)
+#undef MRB_OCC
+  return occ;
 }
 
 int64_t launch_cluster(mrb_batch* b) {
-  switch (b->cluster_cs) {
-    case 1: launch_cluster_t<1>(b); break;
-    case 2: launch_cluster_t<2>(b); break;
-    case 4: launch_cluster_t<4>(b); break;
-    case 8: launch_cluster_t<8>(b); break;
-    case 16: launch_cluster_t<16>(b); break;
-  }
+#define MRB_LAUNCH(C, N) launch_cluster_t<C, N>(b)
+  MRB_CLUSTER_SWITCH(b->cluster_cs, b->cluster_npt, MRB_LAUNCH)
+#undef MRB_LAUNCH
   return 1;
 }
 
@@ -534,6 +625,11 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
   const int nb = b->n_node_blocks;
   if (b->cluster_cs) {
     if constexpr (std::is_same<TapT, float>::value && std::is_same<Real, float>::value) {
+      const size_t npx = size_t(b->W) * b->H, npad = size_t(b->W + 2) * (b->H + 2);
+      k_pad_image4<<<dim3(unsigned(std::min<size_t>((npad + 255) / 256, 1024)), b->n_pairs), 256, 0,
+                     s>>>(static_cast<const float*>(b->img), 2 * npx, b->W, b->H, b->img_pad,
+                          b->pad_pitch, b->pad_plane, 4 * b->pad_plane);
+      ++launches;
       tm->mark(-1);
       launches += launch_cluster(b);
       tm->mark(0);
@@ -598,7 +694,7 @@ int64_t dispatch_enqueue(mrb_batch* b, KernelTimer* tm = nullptr) {
 }
 
 int64_t launches_per_run(const mrb_batch* b) {
-  if (b->cluster_cs) return 2 + 1 + 2;  // interleave, reset, cluster loop, dense, msd
+  if (b->cluster_cs) return 2 + 1 + 1 + 2;  // interleave, reset, pad, cluster loop, dense, msd
   return 2 + int64_t(b->cfg.max_iterations) * (2 + b->cfg.smoothing_passes) + 3;
 }
 
@@ -607,45 +703,94 @@ int64_t launches_per_run(const mrb_batch* b) {
 void setup_cluster_path(mrb_batch* b) {
   b->cluster_cs = 0;
   const char* env = std::getenv("MESHREG_B200_PATH");
-  if (env && std::string(env) == "generic") return;
-  if (b->real_d || b->tap_d) return;
+  const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
+  auto why = [&](const char* m) {
+    if (dbg) std::fprintf(stderr, "meshreg_b200: generic path (%s)\n", m);
+  };
+  if (env && std::string(env) == "generic") return why("MESHREG_B200_PATH=generic");
+  if (b->real_d || b->tap_d) return why("fp64 precision");
   int64_t nmax = 0;
   for (mrb_mesh* m : b->meshes) {
     nmax = std::max<int64_t>(nmax, m->h.n);
-    if (m->h.dev->max_deg > kMaxDeg) return;
+    if (m->h.dev->max_deg > kMaxDeg) return why("one-ring larger than kMaxDeg");
   }
-  int cs = 1;
-  while (cs < 16 && (nmax + cs - 1) / cs > kClusterThreads) cs *= 2;
-  if ((nmax + cs - 1) / cs > kClusterThreads) return;
-  if (cluster_occupancy_cs(cs) < 1) return;
-  std::vector<ClusterPair> cp(b->n_pairs);
+  // latency mode (few pairs): one node per thread, more CTAs per pair;
+  // throughput mode: two nodes per thread, fewer CTAs per pair
+  const char* npt_env = std::getenv("MESHREG_B200_NPT");
+  int npt = npt_env ? std::atoi(npt_env) : (b->n_pairs >= 4 ? 2 : 1);
+  for (; npt >= 1; --npt) {
+    const int cap = kClusterThreads * npt;
+    int cs = 1;
+    while (cs < 16 && (nmax + cs - 1) / cs > cap) cs *= 2;
+    if ((nmax + cs - 1) / cs > cap) continue;
+    size_t smem = 0;
+    for (mrb_mesh* m : b->meshes) {
+      const int chunk = int((m->h.n + cs - 1) / cs);
+      const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, m->h, cs, chunk, npt);
+      smem = std::max(smem, cluster_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride,
+                                             b->cfg.smoothing_passes >= 2));
+    }
+    const int occ = cluster_occupancy_cs(cs, npt, smem);
+    if (dbg)
+      std::fprintf(stderr,
+                   "meshreg_b200: cluster %d CTAs x %d nodes/thread, %zu B dynamic smem, "
+                   "max active clusters %d\n",
+                   cs, npt, smem, occ);
+    if (occ < 1) continue;
+    b->cluster_cs = cs;
+    b->cluster_npt = npt;
+    b->cluster_smem = smem;
+    break;
+  }
+  if (!b->cluster_cs) return why("no cluster configuration fits");
+  const int cs = b->cluster_cs;
+  b->pad_pitch = (b->W + 5 + 3) / 4 * 4;
+  b->pad_plane = size_t(b->H + 2) * b->pad_pitch;
+  b->img_pad = dalloc<float2>(4 * b->pad_plane * b->n_pairs);
+  ck(cudaMemset(b->img_pad, 0, 4 * b->pad_plane * b->n_pairs * sizeof(float2)));
   std::vector<PairDev<float, float>> host(b->n_pairs);
   ck(cudaMemcpy(host.data(), b->pairs, b->n_pairs * sizeof(PairDev<float, float>),
                 cudaMemcpyDeviceToHost));
+  std::vector<ClusterPair> cp(b->n_pairs);
   for (int p = 0; p < b->n_pairs; ++p) {
     HostMesh& h = b->meshes[p]->h;
     const int chunk = int((h.n + cs - 1) / cs);
-    const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, h, chunk);
+    const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, h, cs, chunk, b->cluster_npt);
     ClusterPair& c = cp[p];
     c.V = h.dev->V;
-    c.codes = t.codes;
-    c.g = t.g;
     c.g_self = h.dev->g_self_f;
     c.inv_val = h.dev->inv_val_f;
+    c.codes = t.codes;
+    c.g = t.g;
+    c.slice_off = t.slice_off;
+    c.halo = t.halo;
+    c.n_halo = t.n_halo;
+    c.halo_stride = t.halo_stride;
     c.deg = t.deg;
-    c.img = host[p].img;
+    c.img4 = b->img_pad + 4 * b->pad_plane * p;
     c.u = host[p].u;
     c.u_out = host[p].u_out;
     c.perm = h.dev->perm;
     c.trace = host[p].trace;
+    c.prof = nullptr;
+    if (std::getenv("MESHREG_B200_PROFILE_PHASES")) {
+      if (!b->phase_prof) {
+        b->phase_prof = dalloc<long long>(size_t(b->n_pairs) * cs * 8 * 16);
+        ck(cudaMemset(b->phase_prof, 0, size_t(b->n_pairs) * cs * 8 * 16 * sizeof(long long)));
+      }
+      c.prof = b->phase_prof + size_t(p) * cs * 8 * 16;
+    }
     c.n = int(h.n);
     c.chunk = chunk;
     c.W = b->W;
     c.H = b->H;
+    c.topo_stride = t.topo_stride;
+    c.slices = t.slices;
+    c.pitch = b->pad_pitch;
+    c.plane = int(b->pad_plane);
   }
   b->cpairs = dupload(cp.data(), cp.size(), b->ctx->stream);
   ck(cudaStreamSynchronize(b->ctx->stream));
-  b->cluster_cs = cs;
 }
 
 template <typename From, typename To>
@@ -1068,6 +1213,14 @@ int mrb_batch_pair_status(mrb_batch* b, int32_t p, int32_t* iters, double* msd_b
 int64_t mrb_batch_launches_per_run(const mrb_batch* b) { return launches_per_run(b); }
 
 int32_t mrb_batch_path(const mrb_batch* b) { return b->cluster_cs; }
+
+// debug: phase timestamps of the cluster kernel (MESHREG_B200_PROFILE_PHASES)
+int mrb_batch_phase_profile(mrb_batch* b, long long* out, int64_t n) {
+  if (!b->phase_prof) return MRB_E_VALUE;
+  const size_t cnt = std::min<size_t>(size_t(n), size_t(b->n_pairs) * b->cluster_cs * 8 * 16);
+  ck(cudaMemcpy(out, b->phase_prof, cnt * sizeof(long long), cudaMemcpyDeviceToHost));
+  return MRB_OK;
+}
 
 double mrb_batch_algorithmic_bytes(const mrb_batch* b) {
   // iterations*(184 n_V + 60 n_T + 8 n_E) + 128 W H per pair
