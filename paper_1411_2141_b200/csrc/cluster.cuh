@@ -58,6 +58,11 @@ struct ClusterPair {
   const int* perm;
   double* trace;
   long long* prof;            // optional phase timestamps (MESHREG_B200_PROFILE_PHASES)
+  // dense pass (k_dense_fast)
+  const int* tri_of;          // pixel -> triangle
+  const int4* tri;            // triangles (device node ids)
+  float *ux, *uy, *warped;
+  int pix_blk_begin;
   int n, chunk, W, H;
   int topo_stride, slices, halo_stride, pitch;
   int plane;
@@ -78,6 +83,25 @@ __global__ void k_pad_image4(const float* __restrict__ img, size_t img_stride, i
     const int r = q / Wp, c = q - r * Wp;
     const Px<float, double, 2> v = ext_tap<float, double, 2>(src, W, H, r, c);
     const float2 f = make_float2(float(v.v[0]), float(v.v[1]));
+#pragma unroll
+    for (int s = 0; s < 4; ++s) dst[s * plane + size_t(r) * pitch + c + s] = f;
+  }
+}
+
+// Same four padded copies built straight from the planar fp32 inputs
+// (reference / template stacks) — the fast path needs no other image layout.
+__global__ void k_pad_planar4(const float* const* __restrict__ re, const float* const* __restrict__ te,
+                              int W, int H, float2* __restrict__ out, int pitch, size_t plane,
+                              size_t out_stride) {
+  const int Wp = W + 2, Hp = H + 2;
+  const float* r_img = re[blockIdx.y];
+  const float* t_img = te[blockIdx.y];
+  float2* dst = out + blockIdx.y * out_stride;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Wp * Hp; q += gridDim.x * blockDim.x) {
+    const int r = q / Wp, c = q - r * Wp;
+    const double vt = ext_tap<float, double, 1>(t_img, W, H, r, c).v[0];
+    const double vr = ext_tap<float, double, 1>(r_img, W, H, r, c).v[0];
+    const float2 f = make_float2(float(vt), float(vr));
 #pragma unroll
     for (int s = 0; s < 4; ++s) dst[s * plane + size_t(r) * pitch + c + s] = f;
   }
@@ -227,13 +251,14 @@ __device__ __forceinline__ void ring_gather(const ClusterSmem& sm, uint32_t so, 
   }
 }
 
-template <int CS, int NPT>
+template <int NPT>
 __global__ void __launch_bounds__(kClusterThreads, 1)
     k_cluster_register(const ClusterPair* __restrict__ pairs, PairStatus* __restrict__ st,
                        int max_iter, double tol, float tau, float lam, int passes) {
   constexpr int SLOTS = kClusterThreads * NPT;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = int(cluster.block_rank());
+  const int CS = int(cluster.num_blocks());  // runtime cluster size (1..16)
   const int p = blockIdx.x / CS;
   const ClusterPair& d = pairs[p];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -492,6 +517,51 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     st[p] = s;
   }
   cluster_sync_all();  // keep every CTA's smem alive until all remote reads are done
+}
+
+// Dense pass of the fp32 fast path: densify (densefield.py:130-187; fp64
+// barycentric weights in numpy's operation order), backward warp
+// (densefield.py:190-199) from the aligned padded copies, and the fp64 MSD
+// partials of msd(Te, Re) and msd(warped, Re) (image.py:181-186), with the
+// same block partition as k_dense so k_msd_final reduces them unchanged.
+__global__ void __launch_bounds__(kPixBlock)
+    k_dense_fast(const ClusterPair* __restrict__ pairs, PairStatus* __restrict__ st,
+                 const int* __restrict__ blk_pair, double2* __restrict__ partials) {
+  __shared__ double sh[2 * kPixBlock / 32];
+  const int p = blk_pair[blockIdx.x];
+  const ClusterPair& d = pairs[p];
+  if (st[p].err) return;
+  const int q = (blockIdx.x - d.pix_blk_begin) * kPixBlock + threadIdx.x;
+  double2 acc = make_double2(0.0, 0.0);
+  if (q < d.W * d.H) {
+    const int y = q / d.W, x = q - y * d.W;
+    const int4 tv = __ldg(d.tri + __ldg(d.tri_of + q));
+    double w[3];
+    bary_rn(__ldg(d.V + tv.x), __ldg(d.V + tv.y), __ldg(d.V + tv.z), double(x), double(y), w);
+    const float2 ua = d.u[tv.x], ub = d.u[tv.y], uc = d.u[tv.z];
+    // (w * u[T]).sum(axis=2) = (w1 ua + w2 ub) + w3 uc, densefield.py:184-187
+    const float rx = float(__dadd_rn(__dadd_rn(__dmul_rn(w[0], double(ua.x)), __dmul_rn(w[1], double(ub.x))),
+                                     __dmul_rn(w[2], double(uc.x))));
+    const float ry = float(__dadd_rn(__dadd_rn(__dmul_rn(w[0], double(ua.y)), __dmul_rn(w[1], double(ub.y))),
+                                     __dmul_rn(w[2], double(uc.y))));
+    d.ux[q] = rx;
+    d.uy[q] = ry;
+    const Window win = locate(d, double(x) + double(rx), double(y) + double(ry));
+    float2 tap[4][4];
+#pragma unroll
+    for (int row = 0; row < 4; ++row) ld_row4(win.base + size_t(row) * d.pitch, tap[row]);
+    const float wv = combine(win, tap).x;
+    d.warped[q] = wv;
+    const float2 own = __ldg(d.img4 + size_t(y + 1) * d.pitch + (x + 1));  // (Te, Re) at p
+    const double d0 = double(own.x) - double(own.y);
+    const double d1 = double(wv) - double(own.y);
+    acc.x = d0 * d0;
+    acc.y = d1 * d1;
+    if (!isfinite(rx) || !isfinite(ry)) atomicOr(&st[p].dense_nonfinite, 1);
+    if (!isfinite(wv)) atomicOr(&st[p].dense_nonfinite, 2);
+  }
+  const double2 bs = block_sum2<kPixBlock>(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = bs;
 }
 
 }  // namespace mrb

@@ -484,7 +484,8 @@ __global__ void __launch_bounds__(kPixBlock)
     const double d1 = double(wv) - own.v[1];
     acc.x = d0 * d0;
     acc.y = d1 * d1;
-    if (!isfinite(rx) || !isfinite(ry) || !isfinite(wv)) st[p].dense_nonfinite = 1;
+    if (!isfinite(rx) || !isfinite(ry)) atomicOr(&st[p].dense_nonfinite, 1);
+    if (!isfinite(wv)) atomicOr(&st[p].dense_nonfinite, 2);
   }
   const double2 bs = block_sum2<kPixBlock>(acc, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = bs;

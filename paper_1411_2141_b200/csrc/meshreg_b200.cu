@@ -524,8 +524,9 @@ struct KernelTimer {
   }
 };
 
-template <int CS, int NPT>
+template <int NPT>
 void launch_cluster_t(mrb_batch* b) {
+  const int CS = b->cluster_cs;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(unsigned(b->n_pairs * CS));
   lc.blockDim = dim3(kClusterThreads);
@@ -538,15 +539,15 @@ void launch_cluster_t(mrb_batch* b) {
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  ck(cudaLaunchKernelEx(&lc, k_cluster_register<CS, NPT>,
+  ck(cudaLaunchKernelEx(&lc, k_cluster_register<NPT>,
                         static_cast<const ClusterPair*>(b->cpairs), b->st,
                         int(b->cfg.max_iterations), double(b->cfg.energy_tolerance),
                         float(b->cfg.tau), float(b->cfg.lam), int(b->cfg.smoothing_passes)));
 }
 
-template <int CS, int NPT>
-int cluster_occupancy(size_t smem) {
-  auto kern = k_cluster_register<CS, NPT>;
+template <int NPT>
+int cluster_occupancy(int CS, size_t smem) {
+  auto kern = k_cluster_register<NPT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
       cudaSuccess) {
@@ -576,33 +577,15 @@ int cluster_occupancy(size_t smem) {
   return n;
 }
 
-#define MRB_CLUSTER_SWITCH(CS_, NPT_, CALL)                      \
-  switch ((CS_) * 4 + (NPT_)) {                                  \
-    case 1 * 4 + 1: CALL(1, 1); break;                           \
-    case 2 * 4 + 1: CALL(2, 1); break;                           \
-    case 4 * 4 + 1: CALL(4, 1); break;                           \
-    case 8 * 4 + 1: CALL(8, 1); break;                           \
-    case 16 * 4 + 1: CALL(16, 1); break;                         \
-    case 1 * 4 + 2: CALL(1, 2); break;                           \
-    case 2 * 4 + 2: CALL(2, 2); break;                           \
-    case 4 * 4 + 2: CALL(4, 2); break;                           \
-    case 8 * 4 + 2: CALL(8, 2); break;                           \
-    case 16 * 4 + 2: CALL(16, 2); break;                         \
-    default: break;                                              \
-  }
-
 int cluster_occupancy_cs(int cs, int npt, size_t smem) {
-  int occ = 0;
-#define MRB_OCC(C, N) occ = cluster_occupancy<C, N>(smem)
-  MRB_CLUSTER_SWITCH(cs, npt, MRB_OCC)
-#undef MRB_OCC
-  return occ;
+  return npt == 2 ? cluster_occupancy<2>(cs, smem) : cluster_occupancy<1>(cs, smem);
 }
 
 int64_t launch_cluster(mrb_batch* b) {
-#define MRB_LAUNCH(C, N) launch_cluster_t<C, N>(b)
-  MRB_CLUSTER_SWITCH(b->cluster_cs, b->cluster_npt, MRB_LAUNCH)
-#undef MRB_LAUNCH
+  if (b->cluster_npt == 2)
+    launch_cluster_t<2>(b);
+  else
+    launch_cluster_t<1>(b);
   return 1;
 }
 
@@ -614,6 +597,30 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
   cudaStream_t s = b->ctx->stream;
   const PD* pairs = static_cast<const PD*>(b->pairs);
   int64_t launches = 0;
+  if (b->cluster_cs) {
+    if constexpr (std::is_same<TapT, float>::value && std::is_same<Real, float>::value) {
+      // fast path: padded aligned copies straight from the planar inputs,
+      // one persistent cluster launch for every iteration of every pair,
+      // then the fused dense pass
+      const size_t npad = size_t(b->W + 2) * (b->H + 2);
+      k_pad_planar4<<<dim3(unsigned(std::min<size_t>((npad + 255) / 256, 1024)), b->n_pairs), 256,
+                      0, s>>>(reinterpret_cast<const float* const*>(b->src_ptrs),
+                              reinterpret_cast<const float* const*>(b->src_ptrs + b->n_pairs),
+                              b->W, b->H, b->img_pad, b->pad_pitch, b->pad_plane,
+                              4 * b->pad_plane);
+      ++launches;
+      tm->mark(-1);
+      launches += launch_cluster(b);
+      tm->mark(0);
+      k_dense_fast<<<b->n_pix_blocks, kPixBlock, 0, s>>>(
+          static_cast<const ClusterPair*>(b->cpairs), b->st, b->pix_blk_pair, b->pix_partials);
+      tm->mark(3);
+      k_msd_final<TapT, Real><<<b->n_pairs, kPixBlock, 0, s>>>(pairs, b->st, b->pix_partials);
+      launches += 2;
+      ck(cudaGetLastError());
+      return launches;
+    }
+  }
   if (b->in_dtype == MRB_F64)
     launch_interleave<double, TapT>(b);
   else
@@ -623,25 +630,6 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
                                                          b->cfg.max_iterations);
   ++launches;
   const int nb = b->n_node_blocks;
-  if (b->cluster_cs) {
-    if constexpr (std::is_same<TapT, float>::value && std::is_same<Real, float>::value) {
-      const size_t npx = size_t(b->W) * b->H, npad = size_t(b->W + 2) * (b->H + 2);
-      k_pad_image4<<<dim3(unsigned(std::min<size_t>((npad + 255) / 256, 1024)), b->n_pairs), 256, 0,
-                     s>>>(static_cast<const float*>(b->img), 2 * npx, b->W, b->H, b->img_pad,
-                          b->pad_pitch, b->pad_plane, 4 * b->pad_plane);
-      ++launches;
-      tm->mark(-1);
-      launches += launch_cluster(b);
-      tm->mark(0);
-      k_dense<TapT, Real><<<b->n_pix_blocks, kPixBlock, 0, s>>>(pairs, b->st, b->pix_blk_pair,
-                                                                b->pix_partials);
-      tm->mark(3);
-      k_msd_final<TapT, Real><<<b->n_pairs, kPixBlock, 0, s>>>(pairs, b->st, b->pix_partials);
-      launches += 2;
-      ck(cudaGetLastError());
-      return launches;
-    }
-  }
   const double tol = b->cfg.energy_tolerance;
   const Real tau = Real(b->cfg.tau), lam = Real(b->cfg.lam);
   const int passes = b->cfg.smoothing_passes;
@@ -694,7 +682,7 @@ int64_t dispatch_enqueue(mrb_batch* b, KernelTimer* tm = nullptr) {
 }
 
 int64_t launches_per_run(const mrb_batch* b) {
-  if (b->cluster_cs) return 2 + 1 + 1 + 2;  // interleave, reset, pad, cluster loop, dense, msd
+  if (b->cluster_cs) return 4;  // pad, cluster loop, dense, msd
   return 2 + int64_t(b->cfg.max_iterations) * (2 + b->cfg.smoothing_passes) + 3;
 }
 
@@ -709,6 +697,7 @@ void setup_cluster_path(mrb_batch* b) {
   };
   if (env && std::string(env) == "generic") return why("MESHREG_B200_PATH=generic");
   if (b->real_d || b->tap_d) return why("fp64 precision");
+  if (b->in_dtype != MRB_F32) return why("fp64 image storage");
   int64_t nmax = 0;
   for (mrb_mesh* m : b->meshes) {
     nmax = std::max<int64_t>(nmax, m->h.n);
@@ -718,29 +707,55 @@ void setup_cluster_path(mrb_batch* b) {
   // throughput mode: two nodes per thread, fewer CTAs per pair
   const char* npt_env = std::getenv("MESHREG_B200_NPT");
   int npt = npt_env ? std::atoi(npt_env) : (b->n_pairs >= 4 ? 2 : 1);
-  for (; npt >= 1; --npt) {
+  // Cluster size: any CS in [ceil(n / (768*npt)), 16].  Cost model =
+  // waves x nodes per CTA = ceil(P / max active clusters(CS)) * ceil(n / CS);
+  // the occupancy API sees the GPC structure (e.g. clusters of 9 pack two per
+  // 18/19-SM GPC where clusters of 8 leave SMs idle).
+  const bool two_u = b->cfg.smoothing_passes >= 2;
+  mrb_mesh* big = *std::max_element(b->meshes.begin(), b->meshes.end(),
+                                    [](mrb_mesh* x, mrb_mesh* y) { return x->h.n < y->h.n; });
+  const char* cs_env = std::getenv("MESHREG_B200_CS");
+  for (; npt >= 1 && !b->cluster_cs; --npt) {
     const int cap = kClusterThreads * npt;
-    int cs = 1;
-    while (cs < 16 && (nmax + cs - 1) / cs > cap) cs *= 2;
-    if ((nmax + cs - 1) / cs > cap) continue;
+    const int cs_min = int((nmax + cap - 1) / cap);
+    if (cs_min > 16) continue;
+    double best = 1e300;
+    for (int cs = cs_min; cs <= 16; ++cs) {
+      if (cs_env && std::atoi(cs_env) != cs) continue;
+      const int chunk = int((big->h.n + cs - 1) / cs);
+      const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, big->h, cs, chunk, npt);
+      // estimate with the largest mesh; re-checked below with every mesh
+      const size_t smem =
+          cluster_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride, two_u) + 4096;
+      const int occ = cluster_occupancy_cs(cs, npt, smem);
+      if (occ < 1) continue;
+      const double cost = double((b->n_pairs + occ - 1) / occ) * double((nmax + cs - 1) / cs);
+      if (dbg)
+        std::fprintf(stderr,
+                     "meshreg_b200: candidate cluster %d x %d nodes/thread: %zu B smem, "
+                     "%d active clusters, cost %.0f\n",
+                     cs, npt, smem, occ, cost);
+      if (cost < best) {
+        best = cost;
+        b->cluster_cs = cs;
+        b->cluster_npt = npt;
+      }
+    }
+    if (!b->cluster_cs) continue;
     size_t smem = 0;
     for (mrb_mesh* m : b->meshes) {
-      const int chunk = int((m->h.n + cs - 1) / cs);
-      const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, m->h, cs, chunk, npt);
-      smem = std::max(smem, cluster_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride,
-                                             b->cfg.smoothing_passes >= 2));
+      const int chunk = int((m->h.n + b->cluster_cs - 1) / b->cluster_cs);
+      const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, m->h, b->cluster_cs, chunk, npt);
+      smem = std::max(smem, cluster_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride, two_u));
     }
-    const int occ = cluster_occupancy_cs(cs, npt, smem);
-    if (dbg)
-      std::fprintf(stderr,
-                   "meshreg_b200: cluster %d CTAs x %d nodes/thread, %zu B dynamic smem, "
-                   "max active clusters %d\n",
-                   cs, npt, smem, occ);
-    if (occ < 1) continue;
-    b->cluster_cs = cs;
-    b->cluster_npt = npt;
+    if (cluster_occupancy_cs(b->cluster_cs, npt, smem) < 1) {
+      b->cluster_cs = 0;
+      continue;
+    }
     b->cluster_smem = smem;
-    break;
+    if (dbg)
+      std::fprintf(stderr, "meshreg_b200: cluster %d CTAs x %d nodes/thread, %zu B smem\n",
+                   b->cluster_cs, b->cluster_npt, smem);
   }
   if (!b->cluster_cs) return why("no cluster configuration fits");
   const int cs = b->cluster_cs;
@@ -768,6 +783,12 @@ void setup_cluster_path(mrb_batch* b) {
     c.halo_stride = t.halo_stride;
     c.deg = t.deg;
     c.img4 = b->img_pad + 4 * b->pad_plane * p;
+    c.tri_of = host[p].tri_of;
+    c.tri = host[p].tri;
+    c.ux = host[p].ux;
+    c.uy = host[p].uy;
+    c.warped = host[p].warped;
+    c.pix_blk_begin = host[p].pix_blk_begin;
     c.u = host[p].u;
     c.u_out = host[p].u_out;
     c.perm = h.dev->perm;
