@@ -11,6 +11,11 @@
 #include <memory>
 #include <string>
 #include <type_traits>
+#include <atomic>
+#include <thread>
+#include <tuple>
+#include <mutex>
+#include <chrono>
 #include <vector>
 
 #include "../../include/meshreg_b200.h"
@@ -24,6 +29,9 @@ struct mrb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::string err;
+  void* pinned = nullptr;  // host staging buffer for mesh uploads (grows)
+  size_t pinned_cap = 0;
+  cudaEvent_t stage_done = nullptr;  // last async copy out of `pinned`
 };
 
 struct mrb_mesh {
@@ -32,8 +40,30 @@ struct mrb_mesh {
 
 namespace mrb {
 
+// Stream-ordered device memory from the pool allocator: allocations made
+// inside an API call are ordered on that call's context stream (AllocScope),
+// so building and tearing down batches costs no device synchronisation.
+inline thread_local cudaStream_t t_alloc_stream = nullptr;
+
+inline void dev_free(void* p, cudaStream_t s) {
+  if (!p) return;
+  if (s)
+    cudaFreeAsync(p, s);
+  else
+    cudaFree(p);
+}
+
+struct AllocScope {
+  cudaStream_t prev;
+  explicit AllocScope(cudaStream_t s) : prev(t_alloc_stream) { t_alloc_stream = s; }
+  ~AllocScope() { t_alloc_stream = prev; }
+};
+
 struct DeviceMesh {
   int device = -1;
+  cudaStream_t stream = nullptr;  // stream its memory is ordered on
+  unsigned char* slab = nullptr;
+  unsigned char* slab64 = nullptr;
   double2* V = nullptr;
   int* nb_ptr = nullptr;
   int* nb_idx = nullptr;
@@ -62,18 +92,16 @@ struct DeviceMesh {
     int cur = -1;
     cudaGetDevice(&cur);
     if (device >= 0) cudaSetDevice(device);
-    void* ptrs[] = {V, nb_ptr, nb_idx, tri, perm, g_self_f, g_nb_f, inv_val_f, g_self_d, g_nb_d,
-                    inv_val_d};
-    for (void* p : ptrs)
-      if (p) cudaFree(p);
-    for (auto& kv : pixel_maps) cudaFree(kv.second);
+    dev_free(slab, stream);  // every per-mesh array lives in the slabs
+    dev_free(slab64, stream);
+    for (auto& kv : pixel_maps) dev_free(kv.second, stream);
     for (auto& kv : topo) {
-      cudaFree(kv.second.codes);
-      cudaFree(kv.second.g);
-      cudaFree(kv.second.slice_off);
-      cudaFree(kv.second.halo);
-      cudaFree(kv.second.n_halo);
-      cudaFree(kv.second.deg);
+      dev_free(kv.second.codes, stream);
+      dev_free(kv.second.g, stream);
+      dev_free(kv.second.slice_off, stream);
+      dev_free(kv.second.halo, stream);
+      dev_free(kv.second.n_halo, stream);
+      dev_free(kv.second.deg, stream);
     }
     if (cur >= 0) cudaSetDevice(cur);
   }
@@ -99,7 +127,10 @@ template <typename T>
 T* dalloc(size_t n) {
   void* p = nullptr;
   if (n == 0) n = 1;
-  ck(cudaMalloc(&p, n * sizeof(T)));
+  if (t_alloc_stream)
+    ck(cudaMallocAsync(&p, n * sizeof(T), t_alloc_stream));
+  else
+    ck(cudaMalloc(&p, n * sizeof(T)));
   return static_cast<T*>(p);
 }
 
@@ -188,28 +219,133 @@ std::string py_repr(double v) {
   return neg ? "-" + out : out;
 }
 
-void ensure_device_mesh(mrb_ctx* ctx, HostMesh& h) {
-  if (h.dev && h.dev->device == ctx->device) return;
-  h.dev.reset(new DeviceMesh());
+// Host staging memory owned by the context (pinned, grows, reused once the
+// previous copy out of it has completed).
+void* pinned_stage(mrb_ctx* ctx, size_t bytes) {
+  if (ctx->stage_done) ck(cudaEventSynchronize(ctx->stage_done));
+  if (bytes > ctx->pinned_cap) {
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    ctx->pinned = nullptr;
+    ctx->pinned_cap = 0;
+    const size_t cap = std::max<size_t>(bytes + bytes / 4, size_t(16) << 20);
+    ck(cudaHostAlloc(&ctx->pinned, cap, cudaHostAllocDefault));
+    ctx->pinned_cap = cap;
+  }
+  return ctx->pinned;
+}
+
+// Run f(0..n-1) on up to 16 host threads.
+template <typename F>
+void parallel_for(size_t n, F&& f) {
+  const unsigned nt = unsigned(std::min<size_t>(
+      n, std::max(1u, std::min(16u, std::thread::hardware_concurrency()))));
+  if (nt <= 1) {
+    for (size_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::atomic<size_t> next{0};
+  auto work = [&]() {
+    for (size_t i; (i = next.fetch_add(1)) < n;) f(i);
+  };
+  std::vector<std::thread> pool;
+  for (unsigned k = 1; k < nt; ++k) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+}
+
+// Upload the per-mesh device arrays of every mesh in `meshes` that has none
+// yet.  Each mesh gets one device slab; the slabs are filled on a host thread
+// pool into a context-owned pinned staging buffer and copied asynchronously.
+// The fp64 operator arrays are uploaded only when an fp64 batch needs them
+// (ensure_device_mesh_f64).
+void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes) {
+  std::vector<HostMesh*> todo;
+  for (HostMesh* h : meshes)
+    if (!(h->dev && h->dev->device == ctx->device) &&
+        std::find(todo.begin(), todo.end(), h) == todo.end())
+      todo.push_back(h);
+  if (todo.empty()) return;
+  AllocScope scope(ctx->stream);
+  struct Plan {
+    size_t off[8], tot, base;
+  };
+  std::vector<Plan> plan(todo.size());
+  size_t total = 0;
+  for (size_t i = 0; i < todo.size(); ++i) {
+    const HostMesh& h = *todo[i];
+    const size_t n = size_t(h.n), m = size_t(h.m), ne2 = h.nb_idx.size();
+    const size_t sizes[8] = {n * 16, (n + 1) * 4, ne2 * 4, m * 16, n * 4, n * 8, ne2 * 8, n * 4};
+    Plan& pl = plan[i];
+    pl.tot = 0;
+    for (int k = 0; k < 8; ++k) {
+      pl.off[k] = pl.tot;
+      pl.tot += (sizes[k] + 255) / 256 * 256;
+    }
+    pl.base = total;
+    total += pl.tot;
+  }
+  unsigned char* stage = static_cast<unsigned char*>(pinned_stage(ctx, total));
+  auto fill = [&](size_t i) {
+    const HostMesh& h = *todo[i];
+    const Plan& pl = plan[i];
+    unsigned char* dst = stage + pl.base;
+    const size_t n = size_t(h.n), m = size_t(h.m), ne2 = h.nb_idx.size();
+    std::memcpy(dst + pl.off[0], h.Vn.data(), n * 16);
+    std::memcpy(dst + pl.off[1], h.nb_ptr.data(), (n + 1) * 4);
+    std::memcpy(dst + pl.off[2], h.nb_idx.data(), ne2 * 4);
+    std::memcpy(dst + pl.off[3], h.Tn.data(), m * 16);
+    std::memcpy(dst + pl.off[4], h.perm.data(), n * 4);
+    float* gs = reinterpret_cast<float*>(dst + pl.off[5]);
+    for (size_t k = 0; k < 2 * n; ++k) gs[k] = float(h.g_self[k]);
+    float* gn = reinterpret_cast<float*>(dst + pl.off[6]);
+    for (size_t k = 0; k < 2 * ne2; ++k) gn[k] = float(h.g_nb[k]);
+    float* iv = reinterpret_cast<float*>(dst + pl.off[7]);
+    for (size_t k = 0; k < n; ++k) iv[k] = float(h.inv_val[k]);
+  };
+  parallel_for(todo.size(), fill);
+  for (size_t i = 0; i < todo.size(); ++i) {
+    HostMesh& h = *todo[i];
+    const Plan& pl = plan[i];
+    h.dev.reset(new DeviceMesh());
+    DeviceMesh& d = *h.dev;
+    d.device = ctx->device;
+    d.stream = ctx->stream;
+    unsigned char* slab = dalloc<unsigned char>(pl.tot);
+    d.slab = slab;
+    ck(cudaMemcpyAsync(slab, stage + pl.base, pl.tot, cudaMemcpyHostToDevice, ctx->stream));
+    d.V = reinterpret_cast<double2*>(slab + pl.off[0]);
+    d.nb_ptr = reinterpret_cast<int*>(slab + pl.off[1]);
+    d.nb_idx = reinterpret_cast<int*>(slab + pl.off[2]);
+    d.tri = reinterpret_cast<int4*>(slab + pl.off[3]);
+    d.perm = reinterpret_cast<int*>(slab + pl.off[4]);
+    d.g_self_f = reinterpret_cast<float2*>(slab + pl.off[5]);
+    d.g_nb_f = reinterpret_cast<float2*>(slab + pl.off[6]);
+    d.inv_val_f = reinterpret_cast<float*>(slab + pl.off[7]);
+    for (int64_t k = 0; k < h.n; ++k)
+      d.max_deg = std::max(d.max_deg, h.nb_ptr[k + 1] - h.nb_ptr[k]);
+  }
+  ck(cudaEventRecord(ctx->stage_done, ctx->stream));  // staging buffer reusable after this
+}
+
+void ensure_device_mesh(mrb_ctx* ctx, HostMesh& h) { ensure_device_meshes(ctx, {&h}); }
+
+// fp64 operator arrays, uploaded on first use by an fp64 batch / single op
+void ensure_device_mesh_f64(mrb_ctx* ctx, HostMesh& h) {
+  ensure_device_mesh(ctx, h);
   DeviceMesh& d = *h.dev;
-  d.device = ctx->device;
-  cudaStream_t s = ctx->stream;
-  const size_t n = size_t(h.n), m = size_t(h.m), ne2 = h.nb_idx.size();
-  d.V = dupload(reinterpret_cast<const double2*>(h.Vn.data()), n, s);
-  d.nb_ptr = dupload(h.nb_ptr.data(), n + 1, s);
-  d.nb_idx = dupload(h.nb_idx.data(), ne2, s);
-  d.tri = dupload(reinterpret_cast<const int4*>(h.Tn.data()), m, s);
-  d.perm = dupload(h.perm.data(), n, s);
-  d.g_self_d = dupload(reinterpret_cast<const double2*>(h.g_self.data()), n, s);
-  d.g_nb_d = dupload(reinterpret_cast<const double2*>(h.g_nb.data()), ne2, s);
-  d.inv_val_d = dupload(h.inv_val.data(), n, s);
-  std::vector<float> gs(h.g_self.begin(), h.g_self.end()), gn(h.g_nb.begin(), h.g_nb.end()),
-      iv(h.inv_val.begin(), h.inv_val.end());
-  d.g_self_f = dupload(reinterpret_cast<const float2*>(gs.data()), n, s);
-  d.g_nb_f = dupload(reinterpret_cast<const float2*>(gn.data()), ne2, s);
-  d.inv_val_f = dupload(iv.data(), n, s);
-  for (int64_t k = 0; k < h.n; ++k) d.max_deg = std::max(d.max_deg, h.nb_ptr[k + 1] - h.nb_ptr[k]);
-  ck(cudaStreamSynchronize(s));  // host vectors above go out of scope
+  if (d.slab64) return;
+  AllocScope scope(ctx->stream);
+  const size_t n = size_t(h.n), ne2 = h.nb_idx.size();
+  const size_t o1 = (n * 16 + 255) / 256 * 256, o2 = o1 + (ne2 * 16 + 255) / 256 * 256;
+  std::vector<unsigned char> host(o2 + n * 8);
+  std::memcpy(host.data(), h.g_self.data(), n * 16);
+  std::memcpy(host.data() + o1, h.g_nb.data(), ne2 * 16);
+  std::memcpy(host.data() + o2, h.inv_val.data(), n * 8);
+  d.slab64 = dalloc<unsigned char>(host.size());
+  ck(cudaMemcpyAsync(d.slab64, host.data(), host.size(), cudaMemcpyHostToDevice, ctx->stream));
+  d.g_self_d = reinterpret_cast<double2*>(d.slab64);
+  d.g_nb_d = reinterpret_cast<double2*>(d.slab64 + o1);
+  d.inv_val_d = reinterpret_cast<double*>(d.slab64 + o2);
 }
 
 // Shared-memory topology of the cluster kernel for `cs` CTAs of `chunk` nodes
@@ -232,7 +368,7 @@ const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, i
   std::vector<uint32_t> soff(size_t(cs) * slices, 0);
   int stride = 0;
   std::vector<std::vector<uint32_t>> halos(cs);
-  std::vector<std::map<int, int>> halo_index(cs);
+  std::vector<std::vector<int>> halo_index(cs, std::vector<int>(size_t(n), -1));
   for (int r = 0; r < cs; ++r) {
     int acc = 0;
     for (int sl = 0; sl < slices; ++sl) {
@@ -244,7 +380,7 @@ const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, i
         mx = std::max(mx, h.nb_ptr[i + 1] - h.nb_ptr[i]);
         for (int q = h.nb_ptr[i]; q < h.nb_ptr[i + 1]; ++q) {
           const int j = h.nb_idx[q];
-          if (j / chunk != r && !halo_index[r].count(j)) {
+          if (j / chunk != r && halo_index[r][j] < 0) {
             halo_index[r][j] = int(halos[r].size());
             halos[r].push_back(uint32_t((j / chunk) << 16 | (j % chunk)));
           }
@@ -289,8 +425,7 @@ const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, i
   t.slice_off = dupload(soff.data(), soff.size(), ctx->stream);
   t.halo = dupload(hl.data(), hl.size(), ctx->stream);
   t.n_halo = dupload(nh.data(), nh.size(), ctx->stream);
-  t.deg = dupload(deg.data(), deg.size(), ctx->stream);
-  ck(cudaStreamSynchronize(ctx->stream));
+  t.deg = dupload(deg.data(), deg.size(), ctx->stream);  // pageable: staged on return
   return d.topo[key] = t;
 }
 
@@ -304,58 +439,74 @@ size_t cluster_dyn_smem(int npt, int topo_stride, int slices, int halo_stride, b
 
 // Pixel->triangle map for (W, H): GPU raster + host locate fallback.
 // Returns "" or the MeshCoverageError message.
-std::string ensure_pixel_map(mrb_ctx* ctx, HostMesh& h, int W, int H, int** out) {
-  ensure_device_mesh(ctx, h);
-  DeviceMesh& d = *h.dev;
-  auto key = std::make_pair(W, H);
-  auto it = d.pixel_maps.find(key);
-  if (it != d.pixel_maps.end()) {
-    *out = it->second;
-    return "";
+std::string ensure_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int W, int H) {
+  const auto key = std::make_pair(W, H);
+  std::vector<HostMesh*> todo;
+  for (HostMesh* h : meshes) {
+    ensure_device_mesh(ctx, *h);
+    if (!h->dev->pixel_maps.count(key) &&
+        std::find(todo.begin(), todo.end(), h) == todo.end())
+      todo.push_back(h);
   }
+  if (todo.empty()) return "";
   cudaStream_t s = ctx->stream;
   const size_t npx = size_t(W) * size_t(H);
-  int* tri_of = dalloc<int>(npx);
-  ck(cudaMemsetAsync(tri_of, 0x7f, npx * sizeof(int), s));
-  const int threads = 256;
-  const long long warps = h.m;
-  k_raster<<<unsigned((warps * 32 + threads - 1) / threads), threads, 0, s>>>(
-      d.V, d.tri, int(h.m), W, H, tri_of);
-  ck(cudaGetLastError());
   unsigned long long* cnt = nullptr;
-  ck(cudaMallocAsync(&cnt, sizeof(unsigned long long), s));
-  ck(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
-  k_count_uncovered<<<std::min<size_t>((npx + 255) / 256, 1184), 256, 0, s>>>(tri_of, int(npx),
-                                                                             cnt);
+  ck(cudaMallocAsync(&cnt, todo.size() * sizeof(unsigned long long), s));
+  ck(cudaMemsetAsync(cnt, 0, todo.size() * sizeof(unsigned long long), s));
+  std::vector<int*> maps(todo.size());
+  for (size_t i = 0; i < todo.size(); ++i) {  // every raster before one sync
+    const HostMesh& h = *todo[i];
+    maps[i] = dalloc<int>(npx);
+    ck(cudaMemsetAsync(maps[i], 0x7f, npx * sizeof(int), s));
+    k_raster<<<unsigned((h.m * 32 + 255) / 256), 256, 0, s>>>(h.dev->V, h.dev->tri, int(h.m), W, H,
+                                                          maps[i]);
+    k_count_uncovered<<<unsigned(std::min<size_t>((npx + 255) / 256, 1184)), 256, 0, s>>>(
+        maps[i], int(npx), cnt + i);
+  }
   ck(cudaGetLastError());
-  unsigned long long missing = 0;
-  ck(cudaMemcpyAsync(&missing, cnt, sizeof missing, cudaMemcpyDeviceToHost, s));
+  std::vector<unsigned long long> missing(todo.size());
+  ck(cudaMemcpyAsync(missing.data(), cnt, todo.size() * sizeof(unsigned long long),
+                     cudaMemcpyDeviceToHost, s));
   ck(cudaFreeAsync(cnt, s));
   ck(cudaStreamSynchronize(s));
-  if (missing) {
-    // densefield.py:176-182: binned locate for each unassigned pixel, row-major
-    std::vector<int> host(npx);
-    ck(cudaMemcpy(host.data(), tri_of, npx * sizeof(int), cudaMemcpyDeviceToHost));
-    Locator loc(h);
-    for (size_t q = 0; q < npx; ++q) {
-      if (host[q] != kUnassigned) continue;
-      const double px = double(q % W), py = double(q / W);
-      double w[3];
-      const int64_t t = loc.locate(h, px, py, w);
-      if (t < 0) {
-        cudaFree(tri_of);
-        char buf[128];
-        std::snprintf(buf, sizeof buf, "point (%s, %s) not covered by any triangle",
-                      py_repr(px).c_str(), py_repr(py).c_str());
-        return buf;
+  std::string err;
+  for (size_t i = 0; i < todo.size(); ++i) {
+    HostMesh& h = *todo[i];
+    if (missing[i] && err.empty()) {
+      // densefield.py:176-182: binned locate for each unassigned pixel, row-major
+      std::vector<int> host(npx);
+      ck(cudaMemcpy(host.data(), maps[i], npx * sizeof(int), cudaMemcpyDeviceToHost));
+      Locator loc(h);
+      for (size_t q = 0; q < npx && err.empty(); ++q) {
+        if (host[q] != kUnassigned) continue;
+        const double px = double(q % W), py = double(q / W);
+        double w[3];
+        const int64_t t = loc.locate(h, px, py, w);
+        if (t < 0) {
+          char buf[128];
+          std::snprintf(buf, sizeof buf, "point (%s, %s) not covered by any triangle",
+                        py_repr(px).c_str(), py_repr(py).c_str());
+          err = buf;
+        }
+        host[q] = int(t);
       }
-      host[q] = int(t);
+      if (err.empty())
+        ck(cudaMemcpy(maps[i], host.data(), npx * sizeof(int), cudaMemcpyHostToDevice));
     }
-    ck(cudaMemcpy(tri_of, host.data(), npx * sizeof(int), cudaMemcpyHostToDevice));
+    if (missing[i] && !err.empty()) {
+      dev_free(maps[i], ctx->stream);
+      continue;
+    }
+    h.dev->pixel_maps[key] = maps[i];
   }
-  d.pixel_maps[key] = tri_of;
-  *out = tri_of;
-  return "";
+  return err;
+}
+
+std::string ensure_pixel_map(mrb_ctx* ctx, HostMesh& h, int W, int H, int** out) {
+  const std::string err = ensure_pixel_maps(ctx, {&h}, W, H);
+  if (err.empty()) *out = h.dev->pixel_maps.at(std::make_pair(W, H));
+  return err;
 }
 
 }  // namespace
@@ -409,8 +560,7 @@ struct mrb_batch {
     void* ptrs[] = {pairs, st, blk_pair, pix_blk_pair, partials, pix_partials, state, traces,
                     img, stage, src_ptrs, img_ptrs, dense, u_out, conv, cpairs, img_pad,
                     phase_prof};
-    for (void* p : ptrs)
-      if (p) cudaFree(p);
+    for (void* p : ptrs) dev_free(p, ctx ? ctx->stream : nullptr);
   }
 };
 
@@ -715,6 +865,17 @@ void setup_cluster_path(mrb_batch* b) {
   mrb_mesh* big = *std::max_element(b->meshes.begin(), b->meshes.end(),
                                     [](mrb_mesh* x, mrb_mesh* y) { return x->h.n < y->h.n; });
   const char* cs_env = std::getenv("MESHREG_B200_CS");
+  // the shape decision is cached per (batch shape, device): later batches of
+  // the same shape evaluate only the chosen candidate
+  static std::mutex cache_mu;
+  static std::map<std::tuple<int, int, int64_t, bool, int>, std::pair<int, int>> cache;
+  const auto cache_key = std::make_tuple(npt, b->n_pairs, int64_t(nmax), two_u, b->ctx->device);
+  int cached_cs = 0, cached_npt = 0;
+  {
+    std::lock_guard<std::mutex> lock(cache_mu);
+    auto it = cache.find(cache_key);
+    if (it != cache.end()) std::tie(cached_cs, cached_npt) = it->second;
+  }
   for (; npt >= 1 && !b->cluster_cs; --npt) {
     const int cap = kClusterThreads * npt;
     const int cs_min = int((nmax + cap - 1) / cap);
@@ -722,6 +883,7 @@ void setup_cluster_path(mrb_batch* b) {
     double best = 1e300;
     for (int cs = cs_min; cs <= 16; ++cs) {
       if (cs_env && std::atoi(cs_env) != cs) continue;
+      if (cached_cs && (cs != cached_cs || npt != cached_npt)) continue;
       const int chunk = int((big->h.n + cs - 1) / cs);
       const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, big->h, cs, chunk, npt);
       // estimate with the largest mesh; re-checked below with every mesh
@@ -742,6 +904,35 @@ void setup_cluster_path(mrb_batch* b) {
       }
     }
     if (!b->cluster_cs) continue;
+    // per-mesh topologies on a host thread pool (distinct meshes only)
+    std::vector<mrb_mesh*> uniq(b->meshes);
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    {
+      const int cs_sel = b->cluster_cs, dev = b->ctx->device;
+      std::atomic<size_t> next{0};
+      std::atomic<bool> failed{false};
+      cudaStream_t st_alloc = b->ctx->stream;
+      auto worker = [&]() {
+        cudaSetDevice(dev);
+        AllocScope scope(st_alloc);
+        try {
+          for (size_t i; (i = next.fetch_add(1)) < uniq.size();) {
+            HostMesh& h = uniq[i]->h;
+            ensure_cluster_topo(b->ctx, h, cs_sel, int((h.n + cs_sel - 1) / cs_sel), npt);
+          }
+        } catch (const CudaError&) {
+          failed = true;
+        }
+      };
+      const unsigned nt = std::max(1u, std::min<unsigned>(
+          std::min<unsigned>(std::thread::hardware_concurrency(), 16u), unsigned(uniq.size())));
+      std::vector<std::thread> pool;
+      for (unsigned k = 1; k < nt; ++k) pool.emplace_back(worker);
+      worker();
+      for (auto& th : pool) th.join();
+      if (failed) throw CudaError{cudaErrorMemoryAllocation};
+    }
     size_t smem = 0;
     for (mrb_mesh* m : b->meshes) {
       const int chunk = int((m->h.n + b->cluster_cs - 1) / b->cluster_cs);
@@ -756,13 +947,15 @@ void setup_cluster_path(mrb_batch* b) {
     if (dbg)
       std::fprintf(stderr, "meshreg_b200: cluster %d CTAs x %d nodes/thread, %zu B smem\n",
                    b->cluster_cs, b->cluster_npt, smem);
+    std::lock_guard<std::mutex> lock(cache_mu);
+    cache[cache_key] = std::make_pair(b->cluster_cs, b->cluster_npt);
   }
   if (!b->cluster_cs) return why("no cluster configuration fits");
   const int cs = b->cluster_cs;
   b->pad_pitch = (b->W + 5 + 3) / 4 * 4;
   b->pad_plane = size_t(b->H + 2) * b->pad_pitch;
+  // columns of a copy that k_pad_planar4 does not write are never read
   b->img_pad = dalloc<float2>(4 * b->pad_plane * b->n_pairs);
-  ck(cudaMemset(b->img_pad, 0, 4 * b->pad_plane * b->n_pairs * sizeof(float2)));
   std::vector<PairDev<float, float>> host(b->n_pairs);
   ck(cudaMemcpy(host.data(), b->pairs, b->n_pairs * sizeof(PairDev<float, float>),
                 cudaMemcpyDeviceToHost));
@@ -881,6 +1074,14 @@ int mrb_ctx_create(int32_t device, mrb_ctx** out) {
   c->device = device;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming);
+  if (e == cudaSuccess) {  // keep freed pool memory for reuse by later batches
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   if (e != cudaSuccess) {
     delete c;
     return MRB_E_CUDA;
@@ -896,6 +1097,8 @@ int mrb_ctx_destroy(mrb_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     cudaStreamDestroy(ctx->stream);
   }
+  if (ctx->stage_done) cudaEventDestroy(ctx->stage_done);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
   return MRB_OK;
 }
@@ -995,6 +1198,7 @@ int mrb_mesh_export_geometry(const mrb_mesh* mesh, double* areas, double* coeffs
 int mrb_pixel_map(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int64_t* tri_of,
                   double* weights) {
   try {
+    AllocScope scope(ctx->stream);
     ck(cudaSetDevice(ctx->device));
     int* map = nullptr;
     const std::string msg = ensure_pixel_map(ctx, mesh->h, W, H, &map);
@@ -1044,16 +1248,33 @@ int mrb_batch_create(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int
   b->real_d = cfg->precision == MRB_PREC_F64;
   b->tap_d = img_dtype == MRB_F64 && b->real_d;
   b->meshes.assign(meshes, meshes + n_pairs);
+  AllocScope scope(ctx->stream);
   try {
     ck(cudaSetDevice(ctx->device));
     int64_t off = 0;
+    const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto tick = [&](const char* what) {
+      if (!dbg) return;
+      cudaStreamSynchronize(ctx->stream);
+      const auto t1 = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "meshreg_b200: batch_create %-22s %8.2f ms\n", what,
+                   std::chrono::duration<double, std::milli>(t1 - t0).count());
+      t0 = t1;
+    };
+    std::vector<HostMesh*> hm;
     for (int p = 0; p < n_pairs; ++p) {
       b->node_off.push_back(int(off));
       off += meshes[p]->h.n;
-      int* map = nullptr;
-      const std::string msg = ensure_pixel_map(ctx, meshes[p]->h, W, H, &map);
-      if (!msg.empty()) return fail(ctx, MRB_E_COVERAGE, msg);
+      hm.push_back(&meshes[p]->h);
     }
+    ensure_device_meshes(ctx, hm);
+    if (b->real_d)
+      for (HostMesh* h : hm) ensure_device_mesh_f64(ctx, *h);
+    tick("mesh upload");
+    const std::string msg = ensure_pixel_maps(ctx, hm, W, H);
+    if (!msg.empty()) return fail(ctx, MRB_E_COVERAGE, msg);
+    tick("pixel maps");
     b->total_nodes = off;
     const size_t npx = size_t(W) * H;
     b->st = dalloc<PairStatus>(n_pairs);
@@ -1072,7 +1293,9 @@ int mrb_batch_create(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int
       build_pairs<float, double>(b.get());
     else
       build_pairs<float, float>(b.get());
+    tick("buffers + descriptors");
     setup_cluster_path(b.get());
+    tick("cluster path setup");
   } catch (const CudaError& e) {
     return cuda_fail(ctx, e.e);
   }
@@ -1090,6 +1313,7 @@ int mrb_batch_destroy(mrb_batch* b) {
 
 int mrb_batch_set_images(mrb_batch* b, const void* re, const void* te, int32_t on_device) {
   mrb_ctx* ctx = b->ctx;
+  AllocScope scope(ctx->stream);
   try {
     ck(cudaSetDevice(ctx->device));
     const size_t npx = size_t(b->W) * b->H, es = in_size(b->in_dtype);
@@ -1151,6 +1375,7 @@ int mrb_batch_run(mrb_batch* b) {
 int mrb_batch_get_results(mrb_batch* b, int32_t out_dtype, double* u, void* ux, void* uy,
                           void* warped) {
   mrb_ctx* ctx = b->ctx;
+  AllocScope scope(ctx->stream);
   try {
     ck(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
@@ -1371,7 +1596,7 @@ int unit_eval(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int32_t dtype,
   try {
     ck(cudaSetDevice(ctx->device));
     HostMesh& h = mesh->h;
-    ensure_device_mesh(ctx, h);
+    ensure_device_mesh_f64(ctx, h);
     DeviceMesh& dm = *h.dev;
     cudaStream_t s = ctx->stream;
     Tmp t(s);
@@ -1548,6 +1773,7 @@ int mrb_step_csr(mrb_ctx* ctx, int64_t n, const int64_t* indptr, const int64_t* 
 int mrb_densify(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, const double* u, double* ux,
                 double* uy) {
   try {
+    AllocScope scope(ctx->stream);
     ck(cudaSetDevice(ctx->device));
     HostMesh& h = mesh->h;
     int* map = nullptr;
