@@ -37,6 +37,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_1411_2141_b200 import pairqueue  # noqa: E402
 from paper_1411_2141_b200.synthetic import CONFIGS, make_pair  # noqa: E402
 
 MESH_DIR = os.path.join(ROOT, "data", "meshes")
@@ -85,13 +86,20 @@ def workload_spec(name):
     return spec, mesh_cfg
 
 
-def load_pair(name, seed):
-    """(re, te, V, T, mesh_kind, seed_used) for one pair of the workload."""
+def cached_seeds(name):
     spec, mesh_cfg = workload_spec(name)
-    used = seed
-    if not os.path.exists(mesh_file(mesh_cfg, used)) and os.path.exists(
-            mesh_file(mesh_cfg, seed % 64)):
-        used = seed % 64  # replica of a cached pair
+    out = set()
+    if os.path.isdir(MESH_DIR):
+        for f in os.listdir(MESH_DIR):
+            pre = f"{mesh_cfg}_s"
+            if f.startswith(pre) and f.endswith(".npz") and f[len(pre):-4].isdigit():
+                out.add(int(f[len(pre):-4]))
+    return out
+
+
+def load_pair(name, used):
+    """(re, te, V, T, mesh_kind, seed) for one pair of the workload."""
+    spec, mesh_cfg = workload_spec(name)
     re, te = make_pair(spec, used)
     if os.path.exists(mesh_file(mesh_cfg, used)):
         d = np.load(mesh_file(mesh_cfg, used))
@@ -156,10 +164,8 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- dist
 def dist_setup():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    info = pairqueue.rank_info()
+    return info.rank, info.world, info.local
 
 
 def dist_init(backend, local):
@@ -171,17 +177,11 @@ def dist_init(backend, local):
 
 
 def reduce_max(value, world, dist, device):
-    if world == 1:
-        return value
-    import torch
-    t = torch.tensor([value], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return pairqueue.max_over_ranks(value, world, device)
 
 
 def barrier(world, dist):
-    if world > 1:
-        dist.barrier()
+    pairqueue.barrier(world)
 
 
 # --------------------------------------------------------------------------- ours
@@ -215,8 +215,9 @@ def run_ours(args, rank, world, local):
 
     spec, _ = workload_spec(args.workload)
     P = args.pairs or (64 if args.workload == "c4" else 1)
-    seeds = [rank * P + i for i in range(P)]
-    pairs = [load_pair(args.workload, s) for s in seeds]
+    avail = cached_seeds(args.workload)
+    seeds, used = pairqueue.shard_seeds(rank, P, avail or None)
+    pairs = [load_pair(args.workload, s) for s in used]
     W = H = spec.size
     iters = spec.iterations
     npx = W * H
@@ -271,7 +272,7 @@ def run_ours(args, rank, world, local):
         lib.mrb_batch_pair_status(batch, p, C.byref(it), None, None, None, None, 0)
         tot_iters += it.value
     work = float(npx) * tot_iters  # px*iter per step on this rank
-    value = world * work * args.steps / (t_ms / 1e3) / 1e6
+    value = pairqueue.job_throughput(work * args.steps, t_ms / 1e3, world)
     launches = int(lib.mrb_batch_launches_per_run(batch)) * args.steps
     path_cs = int(lib.mrb_batch_path(batch))
     alg_bytes = lib.mrb_batch_algorithmic_bytes(batch)
