@@ -64,6 +64,7 @@ struct DeviceMesh {
   cudaStream_t stream = nullptr;  // stream its memory is ordered on
   unsigned char* slab = nullptr;
   unsigned char* slab64 = nullptr;
+  unsigned char* slab_ring = nullptr;
   double2* V = nullptr;
   int* nb_ptr = nullptr;
   int* nb_idx = nullptr;
@@ -78,6 +79,7 @@ struct DeviceMesh {
   std::map<std::pair<int, int>, int*> pixel_maps;
   // cluster fast path: register topology packed for a given chunk size
   struct Topo {  // SELL-32 one-ring layout for one (cluster size, nodes/thread)
+    unsigned char* slab = nullptr;  // owns every array below
     uint16_t* codes = nullptr;
     float2* g = nullptr;
     uint32_t* slice_off = nullptr;
@@ -94,15 +96,9 @@ struct DeviceMesh {
     if (device >= 0) cudaSetDevice(device);
     dev_free(slab, stream);  // every per-mesh array lives in the slabs
     dev_free(slab64, stream);
+    dev_free(slab_ring, stream);
     for (auto& kv : pixel_maps) dev_free(kv.second, stream);
-    for (auto& kv : topo) {
-      dev_free(kv.second.codes, stream);
-      dev_free(kv.second.g, stream);
-      dev_free(kv.second.slice_off, stream);
-      dev_free(kv.second.halo, stream);
-      dev_free(kv.second.n_halo, stream);
-      dev_free(kv.second.deg, stream);
-    }
+    for (auto& kv : topo) dev_free(kv.second.slab, stream);
     if (cur >= 0) cudaSetDevice(cur);
   }
 };
@@ -258,7 +254,7 @@ void parallel_for(size_t n, F&& f) {
 // pool into a context-owned pinned staging buffer and copied asynchronously.
 // The fp64 operator arrays are uploaded only when an fp64 batch needs them
 // (ensure_device_mesh_f64).
-void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes) {
+void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, bool with_ring) {
   std::vector<HostMesh*> todo;
   for (HostMesh* h : meshes)
     if (!(h->dev && h->dev->device == ctx->device) &&
@@ -274,7 +270,10 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes) {
   for (size_t i = 0; i < todo.size(); ++i) {
     const HostMesh& h = *todo[i];
     const size_t n = size_t(h.n), m = size_t(h.m), ne2 = h.nb_idx.size();
-    const size_t sizes[8] = {n * 16, (n + 1) * 4, ne2 * 4, m * 16, n * 4, n * 8, ne2 * 8, n * 4};
+    // 1, 2, 6: one-ring CSR + fused operator of the generic path (optional)
+    const size_t r = with_ring ? 1 : 0;
+    const size_t sizes[8] = {n * 16, r * (n + 1) * 4, r * ne2 * 4, m * 16, n * 4, n * 8,
+                             r * ne2 * 8, n * 4};
     Plan& pl = plan[i];
     pl.tot = 0;
     for (int k = 0; k < 8; ++k) {
@@ -291,14 +290,16 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes) {
     unsigned char* dst = stage + pl.base;
     const size_t n = size_t(h.n), m = size_t(h.m), ne2 = h.nb_idx.size();
     std::memcpy(dst + pl.off[0], h.Vn.data(), n * 16);
-    std::memcpy(dst + pl.off[1], h.nb_ptr.data(), (n + 1) * 4);
-    std::memcpy(dst + pl.off[2], h.nb_idx.data(), ne2 * 4);
+    if (with_ring) {
+      std::memcpy(dst + pl.off[1], h.nb_ptr.data(), (n + 1) * 4);
+      std::memcpy(dst + pl.off[2], h.nb_idx.data(), ne2 * 4);
+      float* gn = reinterpret_cast<float*>(dst + pl.off[6]);
+      for (size_t k = 0; k < 2 * ne2; ++k) gn[k] = float(h.g_nb[k]);
+    }
     std::memcpy(dst + pl.off[3], h.Tn.data(), m * 16);
     std::memcpy(dst + pl.off[4], h.perm.data(), n * 4);
     float* gs = reinterpret_cast<float*>(dst + pl.off[5]);
     for (size_t k = 0; k < 2 * n; ++k) gs[k] = float(h.g_self[k]);
-    float* gn = reinterpret_cast<float*>(dst + pl.off[6]);
-    for (size_t k = 0; k < 2 * ne2; ++k) gn[k] = float(h.g_nb[k]);
     float* iv = reinterpret_cast<float*>(dst + pl.off[7]);
     for (size_t k = 0; k < n; ++k) iv[k] = float(h.inv_val[k]);
   };
@@ -314,12 +315,14 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes) {
     d.slab = slab;
     ck(cudaMemcpyAsync(slab, stage + pl.base, pl.tot, cudaMemcpyHostToDevice, ctx->stream));
     d.V = reinterpret_cast<double2*>(slab + pl.off[0]);
-    d.nb_ptr = reinterpret_cast<int*>(slab + pl.off[1]);
-    d.nb_idx = reinterpret_cast<int*>(slab + pl.off[2]);
+    if (with_ring) {
+      d.nb_ptr = reinterpret_cast<int*>(slab + pl.off[1]);
+      d.nb_idx = reinterpret_cast<int*>(slab + pl.off[2]);
+      d.g_nb_f = reinterpret_cast<float2*>(slab + pl.off[6]);
+    }
     d.tri = reinterpret_cast<int4*>(slab + pl.off[3]);
     d.perm = reinterpret_cast<int*>(slab + pl.off[4]);
     d.g_self_f = reinterpret_cast<float2*>(slab + pl.off[5]);
-    d.g_nb_f = reinterpret_cast<float2*>(slab + pl.off[6]);
     d.inv_val_f = reinterpret_cast<float*>(slab + pl.off[7]);
     for (int64_t k = 0; k < h.n; ++k)
       d.max_deg = std::max(d.max_deg, h.nb_ptr[k + 1] - h.nb_ptr[k]);
@@ -327,11 +330,34 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes) {
   ck(cudaEventRecord(ctx->stage_done, ctx->stream));  // staging buffer reusable after this
 }
 
-void ensure_device_mesh(mrb_ctx* ctx, HostMesh& h) { ensure_device_meshes(ctx, {&h}); }
+// one-ring CSR + fp32 operator of the generic path, when a mesh was uploaded
+// without them (cluster-path batches)
+void ensure_device_mesh_ring(mrb_ctx* ctx, HostMesh& h) {
+  DeviceMesh& d = *h.dev;
+  if (d.nb_ptr) return;
+  AllocScope scope(ctx->stream);
+  const size_t n = size_t(h.n), ne2 = h.nb_idx.size();
+  const size_t o1 = ((n + 1) * 4 + 255) / 256 * 256, o2 = o1 + (ne2 * 4 + 255) / 256 * 256;
+  std::vector<unsigned char> host(o2 + ne2 * 8);
+  std::memcpy(host.data(), h.nb_ptr.data(), (n + 1) * 4);
+  std::memcpy(host.data() + o1, h.nb_idx.data(), ne2 * 4);
+  float* gn = reinterpret_cast<float*>(host.data() + o2);
+  for (size_t k = 0; k < 2 * ne2; ++k) gn[k] = float(h.g_nb[k]);
+  d.slab_ring = dalloc<unsigned char>(host.size());
+  ck(cudaMemcpyAsync(d.slab_ring, host.data(), host.size(), cudaMemcpyHostToDevice, ctx->stream));
+  d.nb_ptr = reinterpret_cast<int*>(d.slab_ring);
+  d.nb_idx = reinterpret_cast<int*>(d.slab_ring + o1);
+  d.g_nb_f = reinterpret_cast<float2*>(d.slab_ring + o2);
+}
+
+void ensure_device_mesh(mrb_ctx* ctx, HostMesh& h) {
+  ensure_device_meshes(ctx, {&h}, true);
+  ensure_device_mesh_ring(ctx, h);
+}
 
 // fp64 operator arrays, uploaded on first use by an fp64 batch / single op
 void ensure_device_mesh_f64(mrb_ctx* ctx, HostMesh& h) {
-  ensure_device_mesh(ctx, h);
+  ensure_device_mesh(ctx, h);  // includes the one-ring arrays
   DeviceMesh& d = *h.dev;
   if (d.slab64) return;
   AllocScope scope(ctx->stream);
@@ -420,12 +446,26 @@ const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, i
   t.topo_stride = stride;
   t.slices = slices;
   t.halo_stride = hstride;
-  t.codes = dupload(codes.data(), codes.size(), ctx->stream);
-  t.g = dupload(g.data(), g.size(), ctx->stream);
-  t.slice_off = dupload(soff.data(), soff.size(), ctx->stream);
-  t.halo = dupload(hl.data(), hl.size(), ctx->stream);
-  t.n_halo = dupload(nh.data(), nh.size(), ctx->stream);
-  t.deg = dupload(deg.data(), deg.size(), ctx->stream);  // pageable: staged on return
+  // one device slab, one (pageable, staged-on-return) copy
+  const size_t bytes[6] = {codes.size() * 2, g.size() * 8, soff.size() * 4, hl.size() * 4,
+                           nh.size() * 4, deg.size()};
+  const void* src[6] = {codes.data(), g.data(), soff.data(), hl.data(), nh.data(), deg.data()};
+  size_t off[6], tot = 0;
+  for (int k = 0; k < 6; ++k) {
+    off[k] = tot;
+    tot += (bytes[k] + 255) / 256 * 256;
+  }
+  std::vector<unsigned char> host(tot);
+  for (int k = 0; k < 6; ++k) std::memcpy(host.data() + off[k], src[k], bytes[k]);
+  unsigned char* slab = dalloc<unsigned char>(tot);
+  ck(cudaMemcpyAsync(slab, host.data(), tot, cudaMemcpyHostToDevice, ctx->stream));
+  t.slab = slab;
+  t.codes = reinterpret_cast<uint16_t*>(slab + off[0]);
+  t.g = reinterpret_cast<float2*>(slab + off[1]);
+  t.slice_off = reinterpret_cast<uint32_t*>(slab + off[2]);
+  t.halo = reinterpret_cast<uint32_t*>(slab + off[3]);
+  t.n_halo = reinterpret_cast<int*>(slab + off[4]);
+  t.deg = slab + off[5];
   return d.topo[key] = t;
 }
 
@@ -441,9 +481,9 @@ size_t cluster_dyn_smem(int npt, int topo_stride, int slices, int halo_stride, b
 // Returns "" or the MeshCoverageError message.
 std::string ensure_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int W, int H) {
   const auto key = std::make_pair(W, H);
+  ensure_device_meshes(ctx, meshes, false);
   std::vector<HostMesh*> todo;
   for (HostMesh* h : meshes) {
-    ensure_device_mesh(ctx, *h);
     if (!h->dev->pixel_maps.count(key) &&
         std::find(todo.begin(), todo.end(), h) == todo.end())
       todo.push_back(h);
@@ -569,6 +609,17 @@ namespace {
 size_t tap_size(const mrb_batch* b) { return b->tap_d ? sizeof(double) : sizeof(float); }
 size_t real_size(const mrb_batch* b) { return b->real_d ? sizeof(double) : sizeof(float); }
 size_t in_size(int dtype) { return dtype == MRB_F64 ? sizeof(double) : sizeof(float); }
+
+void free_pairs(mrb_batch* b) {
+  void** ptrs[] = {&b->state, &b->dense, &b->pairs, reinterpret_cast<void**>(&b->blk_pair),
+                   reinterpret_cast<void**>(&b->pix_blk_pair),
+                   reinterpret_cast<void**>(&b->partials),
+                   reinterpret_cast<void**>(&b->pix_partials)};
+  for (void** p : ptrs) {
+    dev_free(*p, b->ctx->stream);
+    *p = nullptr;
+  }
+}
 
 template <typename TapT, typename Real>
 void build_pairs(mrb_batch* b) {
@@ -1268,7 +1319,19 @@ int mrb_batch_create(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int
       off += meshes[p]->h.n;
       hm.push_back(&meshes[p]->h);
     }
-    ensure_device_meshes(ctx, hm);
+    // the fast path never reads the generic one-ring arrays: upload them only
+    // when the batch is not eligible for it
+    const char* penv = std::getenv("MESHREG_B200_PATH");
+    bool eligible = !b->real_d && !b->tap_d && img_dtype == MRB_F32 &&
+                    !(penv && std::string(penv) == "generic");
+    for (HostMesh* h : hm) {
+      int md = 0;
+      for (int64_t k = 0; k < h->n; ++k) md = std::max(md, h->nb_ptr[k + 1] - h->nb_ptr[k]);
+      eligible = eligible && md <= kMaxDeg && h->n <= 16 * 2 * kClusterThreads;
+    }
+    ensure_device_meshes(ctx, hm, !eligible);
+    if (!eligible)  // meshes uploaded earlier by a fast-path batch lack them
+      for (HostMesh* h : hm) ensure_device_mesh_ring(ctx, *h);
     if (b->real_d)
       for (HostMesh* h : hm) ensure_device_mesh_f64(ctx, *h);
     tick("mesh upload");
@@ -1294,8 +1357,17 @@ int mrb_batch_create(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int
     else
       build_pairs<float, float>(b.get());
     tick("buffers + descriptors");
-    setup_cluster_path(b.get());
+    if (eligible) setup_cluster_path(b.get());
     tick("cluster path setup");
+    if (eligible && !b->cluster_cs) {
+      // predicted fast path did not fit after all: generic path needs the rings
+      for (HostMesh* h : hm) ensure_device_mesh_ring(ctx, *h);
+      free_pairs(b.get());
+      if (b->real_d)
+        build_pairs<float, double>(b.get());
+      else
+        build_pairs<float, float>(b.get());
+    }
   } catch (const CudaError& e) {
     return cuda_fail(ctx, e.e);
   }
