@@ -382,12 +382,13 @@ void ensure_device_mesh_f64(mrb_ctx* ctx, HostMesh& h) {
 //  * codes are CTA-local indices into [own slots (SLOTS = 768*npt) | halo];
 //  * halo[r] lists (owner rank << 16 | owner slot) of every remote node CTA r's
 //    one-rings reference, in first-reference order.
-const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, int chunk,
-                                            int npt) {
-  DeviceMesh& d = *h.dev;
-  const int key = chunk * 4 + npt;
-  auto it = d.topo.find(key);
-  if (it != d.topo.end()) return it->second;
+struct TopoHost {
+  int chunk = 0, stride = 0, slices = 0, hstride = 0;
+  size_t off[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<unsigned char> packed;  // codes | g | slice_off | halo | n_halo | deg
+};
+
+TopoHost build_topo_host(const HostMesh& h, int cs, int chunk, int npt) {
   const int n = int(h.n);
   const int SLOTS = kClusterThreads * npt;
   const int slices = (chunk + 31) / 32;
@@ -441,32 +442,101 @@ const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, i
     nh[r] = int(halos[r].size());
     std::copy(halos[r].begin(), halos[r].end(), hl.begin() + size_t(r) * hstride);
   }
-  DeviceMesh::Topo t;
+  TopoHost t;
   t.chunk = chunk;
-  t.topo_stride = stride;
+  t.stride = stride;
   t.slices = slices;
-  t.halo_stride = hstride;
-  // one device slab, one (pageable, staged-on-return) copy
+  t.hstride = hstride;
   const size_t bytes[6] = {codes.size() * 2, g.size() * 8, soff.size() * 4, hl.size() * 4,
                            nh.size() * 4, deg.size()};
   const void* src[6] = {codes.data(), g.data(), soff.data(), hl.data(), nh.data(), deg.data()};
-  size_t off[6], tot = 0;
+  size_t tot = 0;
   for (int k = 0; k < 6; ++k) {
-    off[k] = tot;
+    t.off[k] = tot;
     tot += (bytes[k] + 255) / 256 * 256;
   }
-  std::vector<unsigned char> host(tot);
-  for (int k = 0; k < 6; ++k) std::memcpy(host.data() + off[k], src[k], bytes[k]);
-  unsigned char* slab = dalloc<unsigned char>(tot);
-  ck(cudaMemcpyAsync(slab, host.data(), tot, cudaMemcpyHostToDevice, ctx->stream));
+  t.packed.resize(tot);
+  for (int k = 0; k < 6; ++k) std::memcpy(t.packed.data() + t.off[k], src[k], bytes[k]);
+  return t;
+}
+
+// device arrays of a packed topology, carved out of one slab
+const DeviceMesh::Topo& install_topo(HostMesh& h, int npt, const TopoHost& th,
+                                     unsigned char* slab) {
+  DeviceMesh::Topo t;
+  t.chunk = th.chunk;
+  t.topo_stride = th.stride;
+  t.slices = th.slices;
+  t.halo_stride = th.hstride;
   t.slab = slab;
-  t.codes = reinterpret_cast<uint16_t*>(slab + off[0]);
-  t.g = reinterpret_cast<float2*>(slab + off[1]);
-  t.slice_off = reinterpret_cast<uint32_t*>(slab + off[2]);
-  t.halo = reinterpret_cast<uint32_t*>(slab + off[3]);
-  t.n_halo = reinterpret_cast<int*>(slab + off[4]);
-  t.deg = slab + off[5];
-  return d.topo[key] = t;
+  t.codes = reinterpret_cast<uint16_t*>(slab + th.off[0]);
+  t.g = reinterpret_cast<float2*>(slab + th.off[1]);
+  t.slice_off = reinterpret_cast<uint32_t*>(slab + th.off[2]);
+  t.halo = reinterpret_cast<uint32_t*>(slab + th.off[3]);
+  t.n_halo = reinterpret_cast<int*>(slab + th.off[4]);
+  t.deg = slab + th.off[5];
+  return h.dev->topo[th.chunk * 4 + npt] = t;
+}
+
+const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, int chunk,
+                                            int npt) {
+  auto it = h.dev->topo.find(chunk * 4 + npt);
+  if (it != h.dev->topo.end()) return it->second;
+  AllocScope scope(ctx->stream);
+  const TopoHost th = build_topo_host(h, cs, chunk, npt);
+  unsigned char* slab = dalloc<unsigned char>(th.packed.size());
+  ck(cudaMemcpyAsync(slab, th.packed.data(), th.packed.size(), cudaMemcpyHostToDevice,
+                     ctx->stream));  // pageable: staged before return
+  return install_topo(h, npt, th, slab);
+}
+
+// topologies of many meshes: built on a host thread pool, uploaded through
+// the pinned staging buffer
+void ensure_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int cs, int npt) {
+  std::vector<HostMesh*> todo;
+  for (HostMesh* h : meshes) {
+    const int chunk = int((h->n + cs - 1) / cs);
+    if (!h->dev->topo.count(chunk * 4 + npt) &&
+        std::find(todo.begin(), todo.end(), h) == todo.end())
+      todo.push_back(h);
+  }
+  if (todo.empty()) return;
+  const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto tick = [&](const char* what) {
+    if (!dbg) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "meshreg_b200:   topologies %-14s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
+  std::vector<TopoHost> th(todo.size());
+  parallel_for(todo.size(), [&](size_t i) {
+    const HostMesh& h = *todo[i];
+    th[i] = build_topo_host(h, cs, int((h.n + cs - 1) / cs), npt);
+  });
+  tick("host build");
+  size_t total = 0;
+  std::vector<size_t> base(todo.size());
+  for (size_t i = 0; i < todo.size(); ++i) {
+    base[i] = total;
+    total += th[i].packed.size();
+  }
+  unsigned char* stage = static_cast<unsigned char*>(pinned_stage(ctx, total));
+  tick("stage wait");
+  parallel_for(todo.size(), [&](size_t i) {
+    std::memcpy(stage + base[i], th[i].packed.data(), th[i].packed.size());
+  });
+  tick("stage fill");
+  AllocScope scope(ctx->stream);
+  for (size_t i = 0; i < todo.size(); ++i) {
+    unsigned char* slab = dalloc<unsigned char>(th[i].packed.size());
+    ck(cudaMemcpyAsync(slab, stage + base[i], th[i].packed.size(), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    install_topo(*todo[i], npt, th[i], slab);
+  }
+  ck(cudaEventRecord(ctx->stage_done, ctx->stream));
+  tick("copies issued");
 }
 
 // bytes of dynamic shared memory of k_cluster_register (ClusterSmem carve)
@@ -955,34 +1025,10 @@ void setup_cluster_path(mrb_batch* b) {
       }
     }
     if (!b->cluster_cs) continue;
-    // per-mesh topologies on a host thread pool (distinct meshes only)
-    std::vector<mrb_mesh*> uniq(b->meshes);
-    std::sort(uniq.begin(), uniq.end());
-    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
-    {
-      const int cs_sel = b->cluster_cs, dev = b->ctx->device;
-      std::atomic<size_t> next{0};
-      std::atomic<bool> failed{false};
-      cudaStream_t st_alloc = b->ctx->stream;
-      auto worker = [&]() {
-        cudaSetDevice(dev);
-        AllocScope scope(st_alloc);
-        try {
-          for (size_t i; (i = next.fetch_add(1)) < uniq.size();) {
-            HostMesh& h = uniq[i]->h;
-            ensure_cluster_topo(b->ctx, h, cs_sel, int((h.n + cs_sel - 1) / cs_sel), npt);
-          }
-        } catch (const CudaError&) {
-          failed = true;
-        }
-      };
-      const unsigned nt = std::max(1u, std::min<unsigned>(
-          std::min<unsigned>(std::thread::hardware_concurrency(), 16u), unsigned(uniq.size())));
-      std::vector<std::thread> pool;
-      for (unsigned k = 1; k < nt; ++k) pool.emplace_back(worker);
-      worker();
-      for (auto& th : pool) th.join();
-      if (failed) throw CudaError{cudaErrorMemoryAllocation};
+    {  // per-mesh topologies: host thread pool + pinned staged upload
+      std::vector<HostMesh*> hm;
+      for (mrb_mesh* m : b->meshes) hm.push_back(&m->h);
+      ensure_cluster_topos(b->ctx, hm, b->cluster_cs, npt);
     }
     size_t smem = 0;
     for (mrb_mesh* m : b->meshes) {
