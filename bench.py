@@ -335,7 +335,11 @@ def run_ours(args, rank, world, local):
             "roofline": {"kernel": names[dom], "bound": "hbm", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
+                         "note": "achieved = SURVEY 8(d) algorithmic bytes per launch / CUDA-event "
+                                 "time; the fast path serves them from SMEM (topology, halo "
+                                 "exchange) and L2 (image taps); traffic = ncu DRAM bytes per "
+                                 "launch (profiles/ncu_traffic.json)"},
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
