@@ -148,6 +148,9 @@ int32_t mrb_batch_path(const mrb_batch* batch);
 /* debug: per-CTA phase timestamps of the cluster kernel (first 8 iterations,
  * 16 slots each) when MESHREG_B200_PROFILE_PHASES is set at batch creation */
 int mrb_batch_phase_profile(mrb_batch* batch, long long* out, int64_t n);
+/* host->device and device->host bytes copied by the library in this process
+ * since the last reset (the benchmark's e2e transfer accounting) */
+int mrb_transfer_bytes(int64_t* h2d, int64_t* d2h, int32_t reset);
 /* device kernels launched by one mrb_batch_run (for the bench's launch count) */
 int64_t mrb_batch_launches_per_run(const mrb_batch* batch);
 /* algorithmic bytes of one run, SURVEY.md §8(d) byte model */
@@ -159,6 +162,21 @@ int mrb_batch_kernel_bytes(const mrb_batch* batch, double* out);
  * return the mean device time per launch in ms: out[0] k_sample, out[1]
  * k_grad, out[2] k_smooth, out[3] k_dense, out[4] whole run.  Synchronises. */
 int mrb_batch_kernel_times(mrb_batch* batch, double* out);
+
+/* Pipelined registration of many pairs (the per-GPU pair queue end to end):
+ * pairs are processed in chunks of `chunk_pairs` on two internal streams, so
+ * the host-side setup of chunk k overlaps the device work of chunk k-1 and
+ * transfers overlap kernels.  Inputs are n_pairs*H*W stacks (host memory,
+ * pinned for overlap).  Outputs (host, any may be NULL): u (concatenated
+ * n_i*2 f64), ux/uy/warped (n_pairs*H*W in out_dtype), per-pair
+ * iterations_run, MSDs, trace (n_pairs*max_iterations), MRB_* codes and
+ * messages (n_pairs*msg_len).  Returns the first pair error (or MRB_OK). */
+int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int32_t width,
+                      int32_t height, int32_t img_dtype, const void* reference, const void* tmpl,
+                      const mrb_config* cfg, int32_t chunk_pairs, int32_t out_dtype, double* u,
+                      void* ux, void* uy, void* warped, int32_t* iterations_run,
+                      double* msd_before, double* msd_after, double* trace, int32_t* codes,
+                      char* messages, int32_t msg_len);
 
 /* ---- single operations (reference functions of the same name) ---------- */
 /* warp_sample, solver.py:91-97 / ImageGrid.sample image.py:73-84 */

@@ -59,7 +59,11 @@ _SIGS = {
     "mrb_batch_sync": (C.c_int, [_vp]),
     "mrb_batch_pair_status": (C.c_int, [_vp, _i32, C.POINTER(_i32), _dp, _dp, _vp, C.c_char_p,
                                         _i32]),
+    "mrb_register_many": (C.c_int, [_vp, _i32, _vp, _i32, _i32, _i32, _vp, _vp,
+                                    C.POINTER(mrb_config), _i32, _i32, _vp, _vp, _vp, _vp, _vp,
+                                    _vp, _vp, _vp, _vp, C.c_char_p, _i32]),
     "mrb_batch_path": (_i32, [_vp]),
+    "mrb_transfer_bytes": (C.c_int, [_vp, _vp, _i32]),
     "mrb_batch_phase_profile": (C.c_int, [_vp, _vp, _i64]),
     "mrb_batch_launches_per_run": (_i64, [_vp]),
     "mrb_batch_algorithmic_bytes": (C.c_double, [_vp]),

@@ -16,6 +16,8 @@
 #include <tuple>
 #include <mutex>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
 #include <vector>
 
 #include "../../include/meshreg_b200.h"
@@ -29,6 +31,7 @@ struct mrb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::string err;
+  mrb_ctx* sub[2] = {nullptr, nullptr};  // pipeline streams of mrb_register_many
   void* pinned = nullptr;  // host staging buffer for mesh uploads (grows)
   size_t pinned_cap = 0;
   cudaEvent_t stage_done = nullptr;  // last async copy out of `pinned`
@@ -119,6 +122,25 @@ inline void ck(cudaError_t e) {
   if (e != cudaSuccess) throw CudaError{e};
 }
 
+// host<->device bytes moved by the library (reported by the benchmark)
+std::atomic<long long> g_h2d_bytes{0}, g_d2h_bytes{0};
+
+inline void count_copy(size_t bytes, cudaMemcpyKind kind) {
+  if (kind == cudaMemcpyHostToDevice) g_h2d_bytes += (long long)bytes;
+  if (kind == cudaMemcpyDeviceToHost) g_d2h_bytes += (long long)bytes;
+}
+
+inline cudaError_t mrb_copy_async(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                                  cudaStream_t s) {
+  count_copy(bytes, kind);
+  return cudaMemcpyAsync(dst, src, bytes, kind, s);
+}
+
+inline cudaError_t mrb_copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  count_copy(bytes, kind);
+  return cudaMemcpy(dst, src, bytes, kind);
+}
+
 template <typename T>
 T* dalloc(size_t n) {
   void* p = nullptr;
@@ -133,7 +155,7 @@ T* dalloc(size_t n) {
 template <typename T>
 T* dupload(const T* h, size_t n, cudaStream_t s) {
   T* d = dalloc<T>(n);
-  if (n) ck(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  if (n) ck(mrb_copy_async(d, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
   return d;
 }
 
@@ -152,7 +174,7 @@ struct Tmp {
   template <typename T>
   T* up(const T* h, size_t n) {
     T* d = get<T>(n);
-    if (n) ck(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    if (n) ck(mrb_copy_async(d, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
     return d;
   }
   ~Tmp() {
@@ -230,23 +252,90 @@ void* pinned_stage(mrb_ctx* ctx, size_t bytes) {
   return ctx->pinned;
 }
 
-// Run f(0..n-1) on up to 16 host threads.
+// Persistent host worker pool: parallel_for(n, f) runs f(0..n-1) on up to 16
+// threads (the caller participates).  Thread start-up is paid once per
+// process, not per call — batch setup calls it several times per chunk.
+class WorkerPool {
+ public:
+  static WorkerPool& get() {
+    static WorkerPool pool;
+    return pool;
+  }
+  template <typename F>
+  void run(size_t n, F&& f) {
+    if (n == 0) return;
+    if (workers_.empty() || n == 1) {
+      for (size_t i = 0; i < n; ++i) f(i);
+      return;
+    }
+    std::unique_lock<std::mutex> job_lock(job_mu_);  // one parallel_for at a time
+    std::function<void(size_t)> fn = std::forward<F>(f);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      n_ = n;
+      next_ = 0;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return done_ == n_; });
+    fn_ = nullptr;
+  }
+
+ private:
+  WorkerPool() {
+    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency())) - 1;
+    for (unsigned k = 0; k < nt; ++k)
+      workers_.emplace_back([this] {
+        size_t seen = 0;
+        for (;;) {
+          {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+          }
+          work();
+        }
+      });
+  }
+  ~WorkerPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void work() {
+    for (;;) {
+      size_t i;
+      std::function<void(size_t)>* fn;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (!fn_ || next_ >= n_) return;
+        i = next_++;
+        fn = fn_;
+      }
+      (*fn)(i);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (++done_ == n_) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, job_mu_;
+  std::condition_variable cv_, done_cv_;
+  std::function<void(size_t)>* fn_ = nullptr;
+  size_t n_ = 0, next_ = 0, done_ = 0, gen_ = 0;
+  bool stop_ = false;
+};
+
 template <typename F>
 void parallel_for(size_t n, F&& f) {
-  const unsigned nt = unsigned(std::min<size_t>(
-      n, std::max(1u, std::min(16u, std::thread::hardware_concurrency()))));
-  if (nt <= 1) {
-    for (size_t i = 0; i < n; ++i) f(i);
-    return;
-  }
-  std::atomic<size_t> next{0};
-  auto work = [&]() {
-    for (size_t i; (i = next.fetch_add(1)) < n;) f(i);
-  };
-  std::vector<std::thread> pool;
-  for (unsigned k = 1; k < nt; ++k) pool.emplace_back(work);
-  work();
-  for (auto& t : pool) t.join();
+  WorkerPool::get().run(n, std::forward<F>(f));
 }
 
 // Upload the per-mesh device arrays of every mesh in `meshes` that has none
@@ -262,6 +351,15 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, bo
       todo.push_back(h);
   if (todo.empty()) return;
   AllocScope scope(ctx->stream);
+  const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto tick = [&](const char* what) {
+    if (!dbg) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "meshreg_b200:   meshes %-18s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   struct Plan {
     size_t off[8], tot, base;
   };
@@ -284,6 +382,7 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, bo
     total += pl.tot;
   }
   unsigned char* stage = static_cast<unsigned char*>(pinned_stage(ctx, total));
+  tick("stage wait");
   auto fill = [&](size_t i) {
     const HostMesh& h = *todo[i];
     const Plan& pl = plan[i];
@@ -304,6 +403,7 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, bo
     for (size_t k = 0; k < n; ++k) iv[k] = float(h.inv_val[k]);
   };
   parallel_for(todo.size(), fill);
+  tick("host fill");
   for (size_t i = 0; i < todo.size(); ++i) {
     HostMesh& h = *todo[i];
     const Plan& pl = plan[i];
@@ -313,7 +413,7 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, bo
     d.stream = ctx->stream;
     unsigned char* slab = dalloc<unsigned char>(pl.tot);
     d.slab = slab;
-    ck(cudaMemcpyAsync(slab, stage + pl.base, pl.tot, cudaMemcpyHostToDevice, ctx->stream));
+    ck(mrb_copy_async(slab, stage + pl.base, pl.tot, cudaMemcpyHostToDevice, ctx->stream));
     d.V = reinterpret_cast<double2*>(slab + pl.off[0]);
     if (with_ring) {
       d.nb_ptr = reinterpret_cast<int*>(slab + pl.off[1]);
@@ -328,6 +428,7 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, bo
       d.max_deg = std::max(d.max_deg, h.nb_ptr[k + 1] - h.nb_ptr[k]);
   }
   ck(cudaEventRecord(ctx->stage_done, ctx->stream));  // staging buffer reusable after this
+  tick("copies issued");
 }
 
 // one-ring CSR + fp32 operator of the generic path, when a mesh was uploaded
@@ -344,7 +445,7 @@ void ensure_device_mesh_ring(mrb_ctx* ctx, HostMesh& h) {
   float* gn = reinterpret_cast<float*>(host.data() + o2);
   for (size_t k = 0; k < 2 * ne2; ++k) gn[k] = float(h.g_nb[k]);
   d.slab_ring = dalloc<unsigned char>(host.size());
-  ck(cudaMemcpyAsync(d.slab_ring, host.data(), host.size(), cudaMemcpyHostToDevice, ctx->stream));
+  ck(mrb_copy_async(d.slab_ring, host.data(), host.size(), cudaMemcpyHostToDevice, ctx->stream));
   d.nb_ptr = reinterpret_cast<int*>(d.slab_ring);
   d.nb_idx = reinterpret_cast<int*>(d.slab_ring + o1);
   d.g_nb_f = reinterpret_cast<float2*>(d.slab_ring + o2);
@@ -368,7 +469,7 @@ void ensure_device_mesh_f64(mrb_ctx* ctx, HostMesh& h) {
   std::memcpy(host.data() + o1, h.g_nb.data(), ne2 * 16);
   std::memcpy(host.data() + o2, h.inv_val.data(), n * 8);
   d.slab64 = dalloc<unsigned char>(host.size());
-  ck(cudaMemcpyAsync(d.slab64, host.data(), host.size(), cudaMemcpyHostToDevice, ctx->stream));
+  ck(mrb_copy_async(d.slab64, host.data(), host.size(), cudaMemcpyHostToDevice, ctx->stream));
   d.g_self_d = reinterpret_cast<double2*>(d.slab64);
   d.g_nb_d = reinterpret_cast<double2*>(d.slab64 + o1);
   d.inv_val_d = reinterpret_cast<double*>(d.slab64 + o2);
@@ -485,7 +586,7 @@ const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, i
   AllocScope scope(ctx->stream);
   const TopoHost th = build_topo_host(h, cs, chunk, npt);
   unsigned char* slab = dalloc<unsigned char>(th.packed.size());
-  ck(cudaMemcpyAsync(slab, th.packed.data(), th.packed.size(), cudaMemcpyHostToDevice,
+  ck(mrb_copy_async(slab, th.packed.data(), th.packed.size(), cudaMemcpyHostToDevice,
                      ctx->stream));  // pageable: staged before return
   return install_topo(h, npt, th, slab);
 }
@@ -531,7 +632,7 @@ void ensure_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, in
   AllocScope scope(ctx->stream);
   for (size_t i = 0; i < todo.size(); ++i) {
     unsigned char* slab = dalloc<unsigned char>(th[i].packed.size());
-    ck(cudaMemcpyAsync(slab, stage + base[i], th[i].packed.size(), cudaMemcpyHostToDevice,
+    ck(mrb_copy_async(slab, stage + base[i], th[i].packed.size(), cudaMemcpyHostToDevice,
                        ctx->stream));
     install_topo(*todo[i], npt, th[i], slab);
   }
@@ -576,17 +677,22 @@ std::string ensure_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes
   }
   ck(cudaGetLastError());
   std::vector<unsigned long long> missing(todo.size());
-  ck(cudaMemcpyAsync(missing.data(), cnt, todo.size() * sizeof(unsigned long long),
+  ck(mrb_copy_async(missing.data(), cnt, todo.size() * sizeof(unsigned long long),
                      cudaMemcpyDeviceToHost, s));
   ck(cudaFreeAsync(cnt, s));
+  const auto ts = std::chrono::steady_clock::now();
   ck(cudaStreamSynchronize(s));
+  if (std::getenv("MESHREG_B200_DEBUG"))
+    std::fprintf(stderr, "meshreg_b200:   pixel maps: %zu rasters, sync wait %.2f ms\n", todo.size(),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts)
+                     .count());
   std::string err;
   for (size_t i = 0; i < todo.size(); ++i) {
     HostMesh& h = *todo[i];
     if (missing[i] && err.empty()) {
       // densefield.py:176-182: binned locate for each unassigned pixel, row-major
       std::vector<int> host(npx);
-      ck(cudaMemcpy(host.data(), maps[i], npx * sizeof(int), cudaMemcpyDeviceToHost));
+      ck(mrb_copy(host.data(), maps[i], npx * sizeof(int), cudaMemcpyDeviceToHost));
       Locator loc(h);
       for (size_t q = 0; q < npx && err.empty(); ++q) {
         if (host[q] != kUnassigned) continue;
@@ -602,7 +708,7 @@ std::string ensure_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes
         host[q] = int(t);
       }
       if (err.empty())
-        ck(cudaMemcpy(maps[i], host.data(), npx * sizeof(int), cudaMemcpyHostToDevice));
+        ck(mrb_copy(maps[i], host.data(), npx * sizeof(int), cudaMemcpyHostToDevice));
     }
     if (missing[i] && !err.empty()) {
       dev_free(maps[i], ctx->stream);
@@ -658,6 +764,7 @@ struct mrb_batch {
   int pad_pitch = 0;
   size_t pad_plane = 0;
   void* cpairs = nullptr;     // ClusterPair[n_pairs]
+  std::vector<unsigned char> pairs_host;  // host copy of the PairDev array
   long long* phase_prof = nullptr;  // MESHREG_B200_PROFILE_PHASES
   float2* img_pad = nullptr;  // 4 shifted padded (H+2)x(W+2) (Te, Re) copies per pair
   int runs = 0;
@@ -759,12 +866,13 @@ void build_pairs(mrb_batch* b) {
   b->n_node_blocks = blk;
   b->n_pix_blocks = pblk;
   cudaStream_t s = b->ctx->stream;
-  b->pairs = dupload(pd.data(), pd.size(), s);
+  b->pairs = dupload(pd.data(), pd.size(), s);  // pageable copies: staged on return
   b->blk_pair = dupload(bp.data(), bp.size(), s);
   b->pix_blk_pair = dupload(pbp.data(), pbp.size(), s);
   b->partials = dalloc<double>(blk);
   b->pix_partials = dalloc<double2>(pblk);
-  ck(cudaStreamSynchronize(s));
+  b->pairs_host.assign(reinterpret_cast<const unsigned char*>(pd.data()),
+                       reinterpret_cast<const unsigned char*>(pd.data() + pd.size()));
 }
 
 template <typename InT, typename TapT>
@@ -816,15 +924,32 @@ void launch_cluster_t(mrb_batch* b) {
                         float(b->cfg.tau), float(b->cfg.lam), int(b->cfg.smoothing_passes)));
 }
 
+// The kernel's dynamic-smem limit only ever grows (per device), so every
+// batch created so far can still launch.
 template <int NPT>
-int cluster_occupancy(int CS, size_t smem) {
+bool raise_smem_limit(size_t smem) {
+  static std::mutex mu;
+  static std::map<int, size_t> cur;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& c = cur[dev];
+  if (smem <= c) return true;
   auto kern = k_cluster_register<NPT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
       cudaSuccess) {
     cudaGetLastError();
-    return 0;
+    return false;
   }
+  c = smem;
+  return true;
+}
+
+template <int NPT>
+int cluster_occupancy(int CS, size_t smem) {
+  auto kern = k_cluster_register<NPT>;
+  if (!raise_smem_limit<NPT>(smem)) return 0;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(unsigned(CS));
   lc.blockDim = dim3(kClusterThreads);
@@ -849,7 +974,20 @@ int cluster_occupancy(int CS, size_t smem) {
 }
 
 int cluster_occupancy_cs(int cs, int npt, size_t smem) {
-  return npt == 2 ? cluster_occupancy<2>(cs, smem) : cluster_occupancy<1>(cs, smem);
+  // the answer only depends on (cs, npt, smem): cached (queries are not free)
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, size_t, int>, int> memo;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(cs, npt, smem, dev);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+  }
+  const int occ = npt == 2 ? cluster_occupancy<2>(cs, smem) : cluster_occupancy<1>(cs, smem);
+  std::lock_guard<std::mutex> lock(mu);
+  return memo[key] = occ;
 }
 
 int64_t launch_cluster(mrb_batch* b) {
@@ -997,14 +1135,18 @@ void setup_cluster_path(mrb_batch* b) {
     auto it = cache.find(cache_key);
     if (it != cache.end()) std::tie(cached_cs, cached_npt) = it->second;
   }
+  if (cached_cs) npt = cached_npt;
   for (; npt >= 1 && !b->cluster_cs; --npt) {
     const int cap = kClusterThreads * npt;
     const int cs_min = int((nmax + cap - 1) / cap);
     if (cs_min > 16) continue;
     double best = 1e300;
-    for (int cs = cs_min; cs <= 16; ++cs) {
+    if (cached_cs) {  // decided before for this batch shape
+      b->cluster_cs = cached_cs;
+      b->cluster_npt = cached_npt;
+    }
+    for (int cs = cs_min; cs <= 16 && !cached_cs; ++cs) {
       if (cs_env && std::atoi(cs_env) != cs) continue;
-      if (cached_cs && (cs != cached_cs || npt != cached_npt)) continue;
       const int chunk = int((big->h.n + cs - 1) / cs);
       const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, big->h, cs, chunk, npt);
       // estimate with the largest mesh; re-checked below with every mesh
@@ -1053,9 +1195,8 @@ void setup_cluster_path(mrb_batch* b) {
   b->pad_plane = size_t(b->H + 2) * b->pad_pitch;
   // columns of a copy that k_pad_planar4 does not write are never read
   b->img_pad = dalloc<float2>(4 * b->pad_plane * b->n_pairs);
-  std::vector<PairDev<float, float>> host(b->n_pairs);
-  ck(cudaMemcpy(host.data(), b->pairs, b->n_pairs * sizeof(PairDev<float, float>),
-                cudaMemcpyDeviceToHost));
+  const PairDev<float, float>* host =
+      reinterpret_cast<const PairDev<float, float>*>(b->pairs_host.data());
   std::vector<ClusterPair> cp(b->n_pairs);
   for (int p = 0; p < b->n_pairs; ++p) {
     HostMesh& h = b->meshes[p]->h;
@@ -1100,8 +1241,7 @@ void setup_cluster_path(mrb_batch* b) {
     c.pitch = b->pad_pitch;
     c.plane = int(b->pad_plane);
   }
-  b->cpairs = dupload(cp.data(), cp.size(), b->ctx->stream);
-  ck(cudaStreamSynchronize(b->ctx->stream));
+  b->cpairs = dupload(cp.data(), cp.size(), b->ctx->stream);  // staged on return
 }
 
 template <typename From, typename To>
@@ -1189,6 +1329,10 @@ int mrb_ctx_create(int32_t device, mrb_ctx** out) {
 
 int mrb_ctx_destroy(mrb_ctx* ctx) {
   if (!ctx) return MRB_OK;
+  for (mrb_ctx*& c : ctx->sub) {
+    mrb_ctx_destroy(c);
+    c = nullptr;
+  }
   cudaSetDevice(ctx->device);
   if (ctx->stream) {
     cudaStreamSynchronize(ctx->stream);
@@ -1303,7 +1447,7 @@ int mrb_pixel_map(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int64_t* t
     const size_t npx = size_t(W) * H;
     if (tri_of) {
       std::vector<int> host(npx);
-      ck(cudaMemcpyAsync(host.data(), map, npx * sizeof(int), cudaMemcpyDeviceToHost,
+      ck(mrb_copy_async(host.data(), map, npx * sizeof(int), cudaMemcpyDeviceToHost,
                          ctx->stream));
       ck(cudaStreamSynchronize(ctx->stream));
       for (size_t q = 0; q < npx; ++q) tri_of[q] = host[q];
@@ -1314,7 +1458,7 @@ int mrb_pixel_map(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int64_t* t
       k_pixel_weights<<<unsigned((npx + 255) / 256), 256, 0, ctx->stream>>>(
           mesh->h.dev->V, mesh->h.dev->tri, map, W, int(npx), w);
       ck(cudaGetLastError());
-      ck(cudaMemcpyAsync(weights, w, 3 * npx * sizeof(double), cudaMemcpyDeviceToHost,
+      ck(mrb_copy_async(weights, w, 3 * npx * sizeof(double), cudaMemcpyDeviceToHost,
                          ctx->stream));
       ck(cudaStreamSynchronize(ctx->stream));
     }
@@ -1395,7 +1539,7 @@ int mrb_batch_create(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int
     std::vector<void*> ip(n_pairs);
     for (int p = 0; p < n_pairs; ++p)
       ip[p] = static_cast<char*>(b->img) + size_t(p) * 2 * npx * tap_size(b.get());
-    ck(cudaMemcpy(b->img_ptrs, ip.data(), n_pairs * sizeof(void*), cudaMemcpyHostToDevice));
+    ck(mrb_copy(b->img_ptrs, ip.data(), n_pairs * sizeof(void*), cudaMemcpyHostToDevice));
     if (b->tap_d)
       build_pairs<double, double>(b.get());
     else if (b->real_d)
@@ -1443,8 +1587,8 @@ int mrb_batch_set_images(mrb_batch* b, const void* re, const void* te, int32_t o
     } else {
       if (!b->stage) b->stage = dalloc<char>(2 * bytes);
       char* st = static_cast<char*>(b->stage);
-      ck(cudaMemcpyAsync(st, re, bytes, cudaMemcpyHostToDevice, ctx->stream));
-      ck(cudaMemcpyAsync(st + bytes, te, bytes, cudaMemcpyHostToDevice, ctx->stream));
+      ck(mrb_copy_async(st, re, bytes, cudaMemcpyHostToDevice, ctx->stream));
+      ck(mrb_copy_async(st + bytes, te, bytes, cudaMemcpyHostToDevice, ctx->stream));
       rs = st;
       ts = st + bytes;
     }
@@ -1454,7 +1598,7 @@ int mrb_batch_set_images(mrb_batch* b, const void* re, const void* te, int32_t o
       ptrs[b->n_pairs + p] = ts + size_t(p) * npx * es;
     }
     if (ptrs != b->src_host) {
-      ck(cudaMemcpyAsync(b->src_ptrs, ptrs.data(), ptrs.size() * sizeof(void*),
+      ck(mrb_copy_async(b->src_ptrs, ptrs.data(), ptrs.size() * sizeof(void*),
                          cudaMemcpyHostToDevice, ctx->stream));
       ck(cudaStreamSynchronize(ctx->stream));  // ptrs is a stack temporary
       b->src_host = ptrs;
@@ -1498,7 +1642,7 @@ int mrb_batch_get_results(mrb_batch* b, int32_t out_dtype, double* u, void* ux, 
     ck(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     if (u)
-      ck(cudaMemcpyAsync(u, b->u_out, size_t(b->total_nodes) * sizeof(double2),
+      ck(mrb_copy_async(u, b->u_out, size_t(b->total_nodes) * sizeof(double2),
                          cudaMemcpyDeviceToHost, s));
     const size_t npx = size_t(b->W) * b->H;
     const bool same = (out_dtype == MRB_F64) == b->real_d;
@@ -1510,7 +1654,7 @@ int mrb_batch_get_results(mrb_batch* b, int32_t out_dtype, double* u, void* ux, 
         const char* src = static_cast<const char*>(b->dense) + (3 * size_t(p) + c) * npx * real_size(b);
         char* dst = static_cast<char*>(outs[c]) + size_t(p) * npx * os;
         if (same) {
-          ck(cudaMemcpyAsync(dst, src, npx * os, cudaMemcpyDeviceToHost, s));
+          ck(mrb_copy_async(dst, src, npx * os, cudaMemcpyDeviceToHost, s));
         } else {
           if (!b->conv) b->conv = dalloc<char>(3 * size_t(b->n_pairs) * npx * os);
           char* cv = static_cast<char*>(b->conv) + (3 * size_t(p) + c) * npx * os;
@@ -1522,7 +1666,7 @@ int mrb_batch_get_results(mrb_batch* b, int32_t out_dtype, double* u, void* ux, 
             k_convert<float, double><<<g, 256, 0, s>>>(reinterpret_cast<const float*>(src),
                                                        reinterpret_cast<double*>(cv), npx);
           ck(cudaGetLastError());
-          ck(cudaMemcpyAsync(dst, cv, npx * os, cudaMemcpyDeviceToHost, s));
+          ck(mrb_copy_async(dst, cv, npx * os, cudaMemcpyDeviceToHost, s));
         }
       }
     }
@@ -1539,9 +1683,9 @@ int mrb_batch_sync(mrb_batch* b) {
     ck(cudaStreamSynchronize(ctx->stream));
     b->h_st.resize(b->n_pairs);
     b->h_trace.resize(size_t(b->n_pairs) * b->cfg.max_iterations);
-    ck(cudaMemcpy(b->h_st.data(), b->st, b->n_pairs * sizeof(PairStatus),
+    ck(mrb_copy(b->h_st.data(), b->st, b->n_pairs * sizeof(PairStatus),
                   cudaMemcpyDeviceToHost));
-    ck(cudaMemcpy(b->h_trace.data(), b->traces, b->h_trace.size() * sizeof(double),
+    ck(mrb_copy(b->h_trace.data(), b->traces, b->h_trace.size() * sizeof(double),
                   cudaMemcpyDeviceToHost));
     b->synced = true;
   } catch (const CudaError& e) {
@@ -1578,11 +1722,21 @@ int64_t mrb_batch_launches_per_run(const mrb_batch* b) { return launches_per_run
 
 int32_t mrb_batch_path(const mrb_batch* b) { return b->cluster_cs; }
 
+int mrb_transfer_bytes(int64_t* h2d, int64_t* d2h, int32_t reset) {
+  if (h2d) *h2d = g_h2d_bytes.load();
+  if (d2h) *d2h = g_d2h_bytes.load();
+  if (reset) {
+    g_h2d_bytes = 0;
+    g_d2h_bytes = 0;
+  }
+  return MRB_OK;
+}
+
 // debug: phase timestamps of the cluster kernel (MESHREG_B200_PROFILE_PHASES)
 int mrb_batch_phase_profile(mrb_batch* b, long long* out, int64_t n) {
   if (!b->phase_prof) return MRB_E_VALUE;
   const size_t cnt = std::min<size_t>(size_t(n), size_t(b->n_pairs) * b->cluster_cs * 8 * 16);
-  ck(cudaMemcpy(out, b->phase_prof, cnt * sizeof(long long), cudaMemcpyDeviceToHost));
+  ck(mrb_copy(out, b->phase_prof, cnt * sizeof(long long), cudaMemcpyDeviceToHost));
   return MRB_OK;
 }
 
@@ -1655,6 +1809,145 @@ int mrb_batch_kernel_times(mrb_batch* b, double* out) {
   return MRB_OK;
 }
 
+// ---------------------------------------------------------------- pipeline
+int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int32_t W,
+                      int32_t H, int32_t img_dtype, const void* reference, const void* tmpl,
+                      const mrb_config* cfg, int32_t chunk_pairs, int32_t out_dtype, double* u,
+                      void* ux, void* uy, void* warped, int32_t* iterations_run,
+                      double* msd_before, double* msd_after, double* trace, int32_t* codes,
+                      char* messages, int32_t msg_len) {
+  // Pipeline: chunk 0 is set up and launched on pipeline stream A.  For every
+  // later chunk k the per-mesh device setup (mesh upload, pixel maps,
+  // fast-path topologies) runs on the context's own stream while chunk k-1
+  // computes on the other pipeline stream; the chunk's pipeline stream then
+  // waits for that setup (event) and its batch creation is cheap.
+  if (n_pairs < 1) return fail(ctx, MRB_E_VALUE, "batch needs at least one pair");
+  for (auto& c : ctx->sub)
+    if (!c) {
+      const int rc = mrb_ctx_create(ctx->device, &c);
+      if (rc != MRB_OK) return fail(ctx, rc, "cannot create a pipeline stream");
+    }
+  // default: one chunk (measured fastest while the per-mesh host setup costs
+  // more than a chunk's device time); smaller chunks overlap setup and compute
+  if (chunk_pairs <= 0) chunk_pairs = n_pairs;
+  const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
+  const auto T0 = std::chrono::steady_clock::now();
+  auto stamp = [&](const char* what, int k) {
+    if (dbg)
+      std::fprintf(stderr, "meshreg_b200: many %8.2f ms  %s %d\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - T0)
+                       .count(),
+                   what, k);
+  };
+  const size_t npx = size_t(W) * H, es = in_size(img_dtype), os = in_size(out_dtype);
+  std::vector<mrb_batch*> live;  // batches in flight, freed once harvested
+  std::vector<std::pair<int, int>> span;
+  int first_err = MRB_OK;
+  std::string first_msg;
+  auto harvest = [&](size_t k) {  // wait for chunk k and collect its statuses
+    mrb_batch* b = live[k];
+    if (!b) return;
+    stamp("harvest begin", int(k));
+    const int rc = mrb_batch_sync(b);
+    if (rc == MRB_E_CUDA && first_err == MRB_OK) {
+      first_err = rc;
+      first_msg = b->ctx->err;
+    }
+    if (b->synced) {
+      for (int q = 0; q < b->n_pairs; ++q) {
+        const int p = span[k].first + q;
+        char buf[512];
+        const int code = mrb_batch_pair_status(
+            b, q, iterations_run ? iterations_run + p : nullptr,
+            msd_before ? msd_before + p : nullptr, msd_after ? msd_after + p : nullptr,
+            trace ? trace + size_t(p) * cfg->max_iterations : nullptr, buf, sizeof buf);
+        if (codes) codes[p] = code;
+        if (messages && msg_len > 0) {
+          std::strncpy(messages + size_t(p) * msg_len, buf, size_t(msg_len) - 1);
+          messages[size_t(p) * msg_len + msg_len - 1] = 0;
+        }
+        if (code != MRB_OK && first_err == MRB_OK) {
+          first_err = code;
+          first_msg = buf;
+        }
+      }
+    }
+    mrb_batch_destroy(b);
+    live[k] = nullptr;
+  };
+  cudaEvent_t setup_done = nullptr;
+  int cs = 0, npt = 0;
+  size_t node_off = 0;
+  try {
+    ck(cudaSetDevice(ctx->device));
+    ck(cudaEventCreateWithFlags(&setup_done, cudaEventDisableTiming));
+    for (int p0 = 0, k = 0; p0 < n_pairs; p0 += chunk_pairs, ++k) {
+      const int P = std::min<int>(chunk_pairs, n_pairs - p0);
+      mrb_ctx* sc = ctx->sub[k & 1];
+      std::vector<HostMesh*> hm;
+      for (int q = 0; q < P; ++q) hm.push_back(&meshes[p0 + q]->h);
+      if (k > 0) {
+        // per-mesh setup on the context stream, overlapping chunk k-1's run
+        stamp("setup begin", k);
+        AllocScope scope(ctx->stream);
+        ensure_device_meshes(ctx, hm, cs == 0);
+        stamp("  meshes", k);
+        if (cs == 0)
+          for (HostMesh* h : hm) ensure_device_mesh_ring(ctx, *h);
+        const std::string msg = ensure_pixel_maps(ctx, hm, W, H);
+        stamp("  pixel maps", k);
+        if (!msg.empty()) {
+          for (size_t j = 0; j < live.size(); ++j) harvest(j);
+          cudaEventDestroy(setup_done);
+          return fail(ctx, MRB_E_COVERAGE, msg);
+        }
+        if (cs) ensure_cluster_topos(ctx, hm, cs, npt);
+        ck(cudaEventRecord(setup_done, ctx->stream));
+        stamp("setup end", k);
+        if (k >= 2) harvest(size_t(k - 2));  // the pipeline stream's previous chunk
+        ck(cudaStreamWaitEvent(sc->stream, setup_done, 0));
+      }
+      mrb_batch* b = nullptr;
+      stamp("create begin", k);
+      int rc = mrb_batch_create(sc, P, meshes + p0, W, H, img_dtype, cfg, &b);
+      stamp("create end", k);
+      if (rc == MRB_OK && k == 0) {
+        cs = b->cluster_cs;
+        npt = b->cluster_npt;
+      }
+      if (rc == MRB_OK)
+        rc = mrb_batch_set_images(b, static_cast<const char*>(reference) + size_t(p0) * npx * es,
+                                  static_cast<const char*>(tmpl) + size_t(p0) * npx * es, 0);
+      if (rc == MRB_OK) rc = mrb_batch_run(b);
+      if (rc == MRB_OK) {
+        auto off = [&](void* base) -> void* {
+          return base ? static_cast<char*>(base) + size_t(p0) * npx * os : nullptr;
+        };
+        rc = mrb_batch_get_results(b, out_dtype, u ? u + 2 * node_off : nullptr, off(ux), off(uy),
+                                   off(warped));
+      }
+      stamp("enqueued", k);
+      for (int q = 0; q < P; ++q) node_off += size_t(meshes[p0 + q]->h.n);
+      live.push_back(b);
+      span.emplace_back(p0, P);
+      if (rc != MRB_OK) {
+        const std::string m = sc->err;
+        for (size_t j = 0; j < live.size(); ++j) harvest(j);
+        cudaEventDestroy(setup_done);
+        return fail(ctx, rc, m);
+      }
+    }
+  } catch (const CudaError& e) {
+    for (size_t j = 0; j < live.size(); ++j) harvest(j);
+    if (setup_done) cudaEventDestroy(setup_done);
+    return cuda_fail(ctx, e.e);
+  }
+  for (size_t j = 0; j < live.size(); ++j) harvest(j);
+  cudaEventDestroy(setup_done);
+  if (first_err != MRB_OK) return fail(ctx, first_err, first_msg);
+  return MRB_OK;
+}
+
 // ---------------------------------------------------------------- register
 int mrb_register(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int32_t img_dtype,
                  const void* re, const void* te, const mrb_config* cfg, double* u,
@@ -1694,7 +1987,7 @@ int mrb_warp_sample(mrb_ctx* ctx, int32_t W, int32_t H, int32_t dtype, const voi
             t.up(static_cast<const float*>(image), npx), W, H, int(n), dV, du, dout);
       ck(cudaGetLastError());
     }
-    ck(cudaMemcpyAsync(out, dout, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(mrb_copy_async(out, dout, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     ck(cudaStreamSynchronize(ctx->stream));
   } catch (const CudaError& e) {
     return cuda_fail(ctx, e.e);
@@ -1752,8 +2045,8 @@ int unit_eval(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int32_t dtype,
     if (f_override) {  // vertex_gradient_all: ste = f, r = 1
       std::vector<double> f(n), one(n, 1.0);
       for (size_t k = 0; k < n; ++k) f[k] = f_override[h.perm[k]];
-      ck(cudaMemcpyAsync(d.ste, f.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
-      ck(cudaMemcpyAsync(d.r, one.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+      ck(mrb_copy_async(d.ste, f.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+      ck(mrb_copy_async(d.r, one.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
       PD* dd = t.up(&d, 1);
       k_grad<double, double><<<d.nblk, kNodeBlock, 0, s>>>(dd, st, blk_pair, 0, 0.0, 0);
       ck(cudaGetLastError());
@@ -1767,21 +2060,21 @@ int unit_eval(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int32_t dtype,
         inter[2 * q + 1] = dtype == MRB_F64 ? static_cast<const double*>(re)[q]
                                             : double(static_cast<const float*>(re)[q]);
       }
-      ck(cudaMemcpyAsync(img, inter.data(), 2 * npx * sizeof(double), cudaMemcpyHostToDevice, s));
+      ck(mrb_copy_async(img, inter.data(), 2 * npx * sizeof(double), cudaMemcpyHostToDevice, s));
       d.img = img;
       PD* dd = t.up(&d, 1);
       k_sample<double, double><<<d.nblk, kNodeBlock, 0, s>>>(dd, st, blk_pair, partials, 0, 0.0);
       ck(cudaGetLastError());
       if (grad) {
         // k_grad skips pairs whose status says stop; force it to run
-        ck(cudaMemcpyAsync(st, &st0, sizeof st0, cudaMemcpyHostToDevice, s));
+        ck(mrb_copy_async(st, &st0, sizeof st0, cudaMemcpyHostToDevice, s));
         k_grad<double, double><<<d.nblk, kNodeBlock, 0, s>>>(dd, st, blk_pair, 0, 0.0, 0);
         ck(cudaGetLastError());
       }
     }
-    if (energy) ck(cudaMemcpyAsync(energy, d.trace, sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (energy) ck(mrb_copy_async(energy, d.trace, sizeof(double), cudaMemcpyDeviceToHost, s));
     if (grad) {
-      ck(cudaMemcpyAsync(tmp.data(), d.grad_out, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
+      ck(mrb_copy_async(tmp.data(), d.grad_out, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
       ck(cudaStreamSynchronize(s));
       for (size_t k = 0; k < n; ++k) {
         grad[2 * h.perm[k]] = tmp[2 * k];
@@ -1843,7 +2136,7 @@ int mrb_smooth_csr(mrb_ctx* ctx, int64_t n, const int64_t* indptr, const int64_t
     double2* cur = reinterpret_cast<double2*>(t.up(u0, 2 * n));
     double2* res = nullptr;
     csr_smooth_impl(ctx, t, n, indptr, indices, data, cur, lam, passes, &res);
-    ck(cudaMemcpyAsync(out, res, n * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(mrb_copy_async(out, res, n * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
     ck(cudaStreamSynchronize(ctx->stream));
   } catch (const CudaError& e) {
     return cuda_fail(ctx, e.e);
@@ -1866,7 +2159,7 @@ int mrb_step_csr(mrb_ctx* ctx, int64_t n, const int64_t* indptr, const int64_t* 
     if (n > 0) k_descent<<<g, 256, 0, ctx->stream>>>(int(n), du, dg, tau, u0, bad);
     ck(cudaGetLastError());
     int hbad = 0;
-    ck(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(mrb_copy_async(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     ck(cudaStreamSynchronize(ctx->stream));
     if (hbad) return fail(ctx, MRB_E_DIVERGED, "non-finite gradient; reduce the step size tau");
     double2* res = u0;
@@ -1880,7 +2173,7 @@ int mrb_step_csr(mrb_ctx* ctx, int64_t n, const int64_t* indptr, const int64_t* 
                                           W, H, res);
       ck(cudaGetLastError());
     }
-    ck(cudaMemcpyAsync(out, res, n * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(mrb_copy_async(out, res, n * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
     ck(cudaStreamSynchronize(ctx->stream));
   } catch (const CudaError& e) {
     return cuda_fail(ctx, e.e);
@@ -1910,8 +2203,8 @@ int mrb_densify(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, const double
     k_densify<<<unsigned((npx + 255) / 256), 256, 0, ctx->stream>>>(h.dev->V, h.dev->tri, map, du,
                                                                     W, int(npx), dx, dy);
     ck(cudaGetLastError());
-    ck(cudaMemcpyAsync(ux, dx, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    ck(cudaMemcpyAsync(uy, dy, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(mrb_copy_async(ux, dx, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(mrb_copy_async(uy, dy, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     ck(cudaStreamSynchronize(ctx->stream));
   } catch (const CudaError& e) {
     return cuda_fail(ctx, e.e);
@@ -1938,7 +2231,7 @@ int mrb_warp_image(mrb_ctx* ctx, int32_t W, int32_t H, int32_t dtype, const void
       k_warp_image<float><<<g, 256, 0, ctx->stream>>>(t.up(static_cast<const float*>(te), npx), W,
                                                       H, dx, dy, dout);
     ck(cudaGetLastError());
-    ck(cudaMemcpyAsync(out, dout, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(mrb_copy_async(out, dout, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     ck(cudaStreamSynchronize(ctx->stream));
   } catch (const CudaError& e) {
     return cuda_fail(ctx, e.e);
@@ -1958,7 +2251,7 @@ int mrb_msd(mrb_ctx* ctx, int64_t n, const double* a, const double* b, double* o
     if (nb > 0) k_sqdiff_partials<<<nb, kPixBlock, 0, ctx->stream>>>(int(n), da, db, partials);
     k_sum_final<<<1, kPixBlock, 0, ctx->stream>>>(nb, partials, double(n), dout);
     ck(cudaGetLastError());
-    ck(cudaMemcpyAsync(out, dout, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ck(mrb_copy_async(out, dout, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     ck(cudaStreamSynchronize(ctx->stream));
   } catch (const CudaError& e) {
     return cuda_fail(ctx, e.e);

@@ -227,10 +227,13 @@ def register(reference, template, mesh, cfg=None, *, precision=None, return_dens
     return u, report
 
 
-def register_batch(references, templates, meshes, cfg=None, *, precision=None):
-    """Register many independent equally-sized pairs in one device pass (the
-    per-GPU pair queue).  Returns a list of (u, report) or the exception the
-    reference would have raised for that pair."""
+def register_batch(references, templates, meshes, cfg=None, *, precision=None,
+                   return_dense=False, chunk_pairs=0):
+    """Register many independent equally-sized pairs (the per-GPU pair queue)
+    through the pipelined native entry point mrb_register_many: chunks of
+    pairs overlap their host setup, transfers and kernels.  Returns a list
+    with, per pair, (u, report) — plus (ux, uy, warped) when return_dense —
+    or the exception the reference would have raised for that pair."""
     cfg = cfg or SolverConfig()
     precision = precision or DEFAULT_PRECISION
     P = len(references)
@@ -253,36 +256,34 @@ def register_batch(references, templates, meshes, cfg=None, *, precision=None):
     ctx = _lib.context()
     c = _cfg_struct(cfg, precision)
     arr = (C.c_void_p * P)(*[m._h for m in meshes])
-    b = C.c_void_p()
-    _lib.check(lib.mrb_batch_create(ctx, P, arr, W, H, dt, C.byref(c), C.byref(b)), ctx, _errs())
-    try:
-        _lib.check(lib.mrb_batch_set_images(b, _lib.ptr(re), _lib.ptr(te), 0), ctx, _errs())
-        _lib.check(lib.mrb_batch_run(b), ctx, _errs())
-        n_tot = sum(m.n_vertices for m in meshes)
-        u_all = np.empty((n_tot, 2))
-        _lib.check(lib.mrb_batch_get_results(b, _lib.F64, _lib.ptr(u_all), None, None, None),
-                   ctx, _errs())
-        lib.mrb_batch_sync(b)
-        out = []
-        off = 0
-        trace = np.empty(cfg.max_iterations)
-        msg = C.create_string_buffer(1024)
-        for p, m in enumerate(meshes):
-            iters = C.c_int32(0)
-            mb, ma = C.c_double(0), C.c_double(0)
-            code = lib.mrb_batch_pair_status(b, p, C.byref(iters), C.byref(mb), C.byref(ma),
-                                             _lib.ptr(trace), msg, 1024)
-            u = u_all[off:off + m.n_vertices].copy()
-            off += m.n_vertices
-            if code != _lib.OK:
-                exc = {_lib.E_DIVERGED: DivergenceError, _lib.E_VALUE: ValueError}.get(
-                    code, RuntimeError)
-                out.append(exc(msg.value.decode()))
-                continue
-            out.append((u, RegistrationReport(int(iters.value),
-                                              [float(e) for e in trace[:iters.value]],
-                                              float(mb.value), float(ma.value), 0.0,
-                                              cfg.to_dict())))
-        return out
-    finally:
-        lib.mrb_batch_destroy(b)
+    n_tot = sum(m.n_vertices for m in meshes)
+    u_all = np.empty((n_tot, 2))
+    dense = [np.empty((P, H, W)) for _ in range(3)] if return_dense else [None] * 3
+    iters = np.zeros(P, np.int32)
+    mb = np.zeros(P)
+    ma = np.zeros(P)
+    trace = np.zeros((P, cfg.max_iterations))
+    codes = np.zeros(P, np.int32)
+    msg_len = 512
+    msgs = C.create_string_buffer(P * msg_len)
+    lib.mrb_register_many(ctx, P, arr, W, H, dt, _lib.ptr(re), _lib.ptr(te), C.byref(c),
+                          int(chunk_pairs), _lib.F64, _lib.ptr(u_all), *(_lib.ptr(d) for d in dense),
+                          _lib.ptr(iters), _lib.ptr(mb), _lib.ptr(ma), _lib.ptr(trace),
+                          _lib.ptr(codes), msgs, msg_len)
+    out = []
+    off = 0
+    for p, m in enumerate(meshes):
+        u = u_all[off:off + m.n_vertices].copy()
+        off += m.n_vertices
+        code = int(codes[p])
+        if code != _lib.OK:
+            text = msgs.raw[p * msg_len:(p + 1) * msg_len].split(b"\0", 1)[0].decode()
+            exc = {_lib.E_DIVERGED: DivergenceError, _lib.E_VALUE: ValueError,
+                   _lib.E_COVERAGE: MeshCoverageError}.get(code, RuntimeError)
+            out.append(exc(text or _lib.last_error(ctx)))
+            continue
+        k = int(iters[p])
+        rep = RegistrationReport(k, [float(e) for e in trace[p, :k]], float(mb[p]), float(ma[p]),
+                                 0.0, cfg.to_dict())
+        out.append((u, rep, tuple(d[p] for d in dense)) if return_dense else (u, rep))
+    return out

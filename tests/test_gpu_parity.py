@@ -282,3 +282,33 @@ def test_fp32_paths_agree_with_reference(name, path, monkeypatch):
     else:
         monkeypatch.delenv("MESHREG_B200_PATH", raising=False)
     check_register(golden(name), "f32", name)
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_pipelined_batch_chunks_and_per_pair_errors(precision):
+    """mrb_register_many with one pair per chunk (both pipeline streams,
+    several chunks in flight) equals single registrations; a diverging pair
+    yields its DivergenceError without affecting the others."""
+    names = ["gen64", "plateau64", "gen64_x255", "gen64", "plateau64"]
+    res, tes, meshes = [], [], []
+    for n in names:
+        g = golden(n)
+        r, t = images(g)
+        res.append(r)
+        tes.append(t)
+        meshes.append(mrb.TriMesh(g["V"], g["T_in"]))
+    cfg = mrb.SolverConfig(tau=0.005, max_iterations=40, energy_tolerance=0.0)
+    out = mrb.register_batch(res, tes, meshes, cfg, precision=precision, return_dense=True,
+                             chunk_pairs=1)
+    assert isinstance(out[2], mrb.DivergenceError)  # gen64_x255 diverges at tau=0.005
+    assert "consecutive iterations" in str(out[2])
+    for k in (0, 1, 3, 4):
+        u, rep, (ux, uy, warped) = out[k]
+        u1, rep1, (ux1, uy1, w1) = mrb.register(res[k], tes[k], meshes[k], cfg,
+                                                precision=precision, return_dense=True)
+        assert np.array_equal(u, u1)
+        assert rep.energy_trace == rep1.energy_trace
+        assert rep.msd_after == rep1.msd_after and rep.msd_before == rep1.msd_before
+        assert np.array_equal(warped, w1) and np.array_equal(ux, ux1)
+    # identical inputs give identical results (determinism across chunks/streams)
+    assert np.array_equal(out[0][0], out[3][0]) and np.array_equal(out[1][0], out[4][0])
