@@ -53,6 +53,7 @@ extern "C" {
 typedef struct mrb_ctx mrb_ctx;
 typedef struct mrb_mesh mrb_mesh;
 typedef struct mrb_batch mrb_batch;
+typedef struct mrb_pixel_batch mrb_pixel_batch;
 
 /* SolverConfig, reference solver.py:47-68 (validated the same way). */
 typedef struct mrb_config {
@@ -64,6 +65,16 @@ typedef struct mrb_config {
   int32_t precision; /* MRB_PREC_* */
   int32_t reserved;
 } mrb_config;
+
+/* register_pixelwise keyword arguments, reference baseline.py:46-64 */
+typedef struct mrb_pixel_config {
+  double tau;
+  double lam;                /* [0, 1); 0 disables smoothing               */
+  int32_t iterations;
+  int32_t smoothing_passes;  /* grid_umbrella_smooth passes per iteration   */
+  int32_t precision;         /* MRB_PREC_*                                  */
+  int32_t reserved;
+} mrb_pixel_config;
 
 /* ---- library / context ------------------------------------------------ */
 const char* mrb_version(void);
@@ -210,6 +221,42 @@ int mrb_warp_image(mrb_ctx* ctx, int32_t width, int32_t height, int32_t img_dtyp
                    const void* tmpl, const double* ux, const double* uy, double* out);
 /* msd, image.py:181-186 */
 int mrb_msd(mrb_ctx* ctx, int64_t n, const double* a, const double* b, double* out);
+
+/* ---- pixel-grid engine (reference baseline.py) ---- */
+/* register_pixelwise, baseline.py:46-118, one pair.  Outputs are f64 host
+ * arrays (any may be NULL): ux/uy/warped H*W, trace[iterations].  Returns
+ * MRB_E_VALUE for the ValueErrors of baseline.py:57-64 / DenseField, and
+ * MRB_E_DIVERGED with the reference's DivergenceError message. */
+int mrb_register_pixelwise(mrb_ctx* ctx, int32_t width, int32_t height, int32_t img_dtype,
+                           const void* reference, const void* tmpl, const mrb_pixel_config* cfg,
+                           double* ux, double* uy, double* warped, double* trace,
+                           int32_t* iterations_run, double* msd_before, double* msd_after);
+/* A resident batch of equally sized pairs for the pixel engine (same life
+ * cycle as mrb_batch: set_images -> run -> get_results -> sync). */
+int mrb_pixel_batch_create(mrb_ctx* ctx, int32_t n_pairs, int32_t width, int32_t height,
+                           int32_t img_dtype, const mrb_pixel_config* cfg,
+                           mrb_pixel_batch** out);
+int mrb_pixel_batch_destroy(mrb_pixel_batch* batch);
+int mrb_pixel_batch_set_images(mrb_pixel_batch* batch, const void* reference, const void* tmpl,
+                               int32_t on_device);
+int mrb_pixel_batch_run(mrb_pixel_batch* batch);
+int mrb_pixel_batch_get_results(mrb_pixel_batch* batch, int32_t out_dtype, void* ux, void* uy,
+                                void* warped);
+int mrb_pixel_batch_sync(mrb_pixel_batch* batch);
+int mrb_pixel_batch_pair_status(mrb_pixel_batch* batch, int32_t pair, int32_t* iterations_run,
+                                double* msd_before, double* msd_after, double* trace, char* msg,
+                                int32_t msg_len);
+/* kernel launches per run; mean device ms: out[0] fused iteration kernel,
+ * out[1] whole run (synchronises) */
+int64_t mrb_pixel_batch_launches_per_run(const mrb_pixel_batch* batch);
+int mrb_pixel_batch_kernel_times(mrb_pixel_batch* batch, double* out);
+/* ImageGrid.sample_gradient, image.py:86-103: pts = n (x, y) pairs */
+int mrb_sample_gradient(mrb_ctx* ctx, int32_t width, int32_t height, int32_t img_dtype,
+                        const void* image, int64_t n, const double* pts, double* gx,
+                        double* gy);
+/* grid_umbrella_smooth, baseline.py:27-43 (one pass, f64 plane) */
+int mrb_grid_umbrella_smooth(mrb_ctx* ctx, int32_t width, int32_t height, const double* plane,
+                             double lam, double* out);
 
 #ifdef __cplusplus
 }

@@ -446,3 +446,103 @@ def warp_image(te, ux, uy):
     h, w = te.shape
     gx, gy = np.meshgrid(np.arange(w, dtype=np.float64), np.arange(h, dtype=np.float64))
     return sample(te, gx + ux, gy + uy)
+
+
+# --------------------------------------------------------------------------
+# pixel-grid engine (baseline.py) — SURVEY.md §8(f) row 1
+# --------------------------------------------------------------------------
+
+def cr_dweights(t):
+    """Derivative Catmull-Rom weights, image.py:167-178."""
+    t2 = t * t
+    return np.stack([0.5 * (-3.0 * t2 + 4.0 * t - 1.0),
+                     0.5 * (9.0 * t2 - 10.0 * t),
+                     0.5 * (-9.0 * t2 + 8.0 * t + 1.0),
+                     0.5 * (3.0 * t2 - 2.0 * t)], axis=-1)
+
+
+def sample_gradient(img, x, y, ext=None):
+    """Analytic (d/dx, d/dy) of the Catmull-Rom interpolant, image.py:86-103."""
+    img = np.asarray(img, np.float64)
+    h, w = img.shape
+    if ext is None:
+        ext = pad_ring(img)
+    x = np.atleast_1d(np.asarray(x, np.float64))
+    y = np.atleast_1d(np.asarray(y, np.float64))
+    x, y = np.broadcast_arrays(x, y)
+    xc = np.clip(x, 0.0, w - 1.0)
+    yc = np.clip(y, 0.0, h - 1.0)
+    cx = np.minimum(np.floor(xc), max(w - 2, 0)).astype(np.int64)
+    cy = np.minimum(np.floor(yc), max(h - 2, 0)).astype(np.int64)
+    k = np.arange(4)
+    taps = ext[cy[..., None, None] + k[:, None], cx[..., None, None] + k[None, :]]
+    tx, ty = xc - cx, yc - cy
+    wx, wy = cr_weights(tx), cr_weights(ty)
+    gx = np.einsum("...j,...i,...ji->...", wy, cr_dweights(tx), taps)
+    gy = np.einsum("...j,...i,...ji->...", cr_dweights(ty), wx, taps)
+    return gx, gy
+
+
+def grid_umbrella_smooth(plane, lam):
+    """4-neighbour mean blend with edge-aware counts, baseline.py:27-43."""
+    total = np.zeros_like(plane)
+    count = np.zeros_like(plane)
+    total[1:, :] += plane[:-1, :]
+    count[1:, :] += 1
+    total[:-1, :] += plane[1:, :]
+    count[:-1, :] += 1
+    total[:, 1:] += plane[:, :-1]
+    count[:, 1:] += 1
+    total[:, :-1] += plane[:, 1:]
+    count[:, :-1] += 1
+    return (1.0 - lam) * plane + lam * total / count
+
+
+def register_pixelwise(re, te, tau=0.005, lam=0.8, iterations=100, smoothing_passes=3):
+    """Dense per-pixel engine of baseline.py:46-118.  Returns
+    (ux, uy, info) with info = iterations_run, energy_trace, msd_before,
+    msd_after, warped."""
+    re = np.asarray(re, np.float64)
+    te = np.asarray(te, np.float64)
+    if re.shape != te.shape:
+        raise ValueError(f"image sizes differ: {re.shape} vs {te.shape}")
+    if tau <= 0:
+        raise ValueError(f"tau must be positive, got {tau}")
+    if not 0.0 <= lam < 1.0:
+        raise ValueError(f"lambda must be in [0, 1), got {lam}")
+    if iterations < 1:
+        raise ValueError("iterations must be >= 1")
+    h, w = re.shape
+    gx0, gy0 = np.meshgrid(np.arange(w, dtype=np.float64), np.arange(h, dtype=np.float64))
+    ext_te, ext_re = pad_ring(te), pad_ring(re)
+    ux = np.zeros((h, w))
+    uy = np.zeros((h, w))
+    trace = []
+    rises = 0
+    for _ in range(iterations):
+        px, py = gx0 + ux, gy0 + uy
+        r = sample(te, px, py, ext_te) - sample(re, px, py, ext_re)
+        e = 0.5 * float(np.sum(r * r))
+        if not np.isfinite(e):
+            raise OracleDivergence("energy became non-finite; reduce tau")
+        if trace and e > trace[-1] * (1.0 + RISE_THRESHOLD) + 1e-12:
+            rises += 1
+            if rises >= 10:
+                raise OracleDivergence(
+                    f"energy increased for {rises} consecutive iterations; reduce tau")
+        elif trace and e <= trace[-1]:
+            rises = 0
+        trace.append(e)
+        dx, dy = sample_gradient(te, px, py, ext_te)
+        ux = ux - tau * r * dx
+        uy = uy - tau * r * dy
+        if lam > 0.0:
+            for _ in range(smoothing_passes):
+                ux = grid_umbrella_smooth(ux, lam)
+                uy = grid_umbrella_smooth(uy, lam)
+        np.clip(ux, -gx0, (w - 1.0) - gx0, out=ux)
+        np.clip(uy, -gy0, (h - 1.0) - gy0, out=uy)
+    warped = warp_image(te, ux, uy)
+    info = dict(iterations_run=len(trace), energy_trace=trace, msd_before=msd(te, re),
+                msd_after=msd(warped, re), warped=warped)
+    return ux, uy, info

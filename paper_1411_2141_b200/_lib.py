@@ -21,6 +21,12 @@ PREC_F32, PREC_F64 = 0, 1
 CSR_LAPLACIAN, CSR_GRAD_X, CSR_GRAD_Y, CSR_VERTEX_AVG = range(4)
 
 
+class mrb_pixel_config(C.Structure):
+    _fields_ = [("tau", C.c_double), ("lam", C.c_double), ("iterations", C.c_int32),
+                ("smoothing_passes", C.c_int32), ("precision", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
 class mrb_config(C.Structure):
     _fields_ = [("tau", C.c_double), ("lam", C.c_double), ("energy_tolerance", C.c_double),
                 ("max_iterations", C.c_int32), ("smoothing_passes", C.c_int32),
@@ -79,6 +85,23 @@ _SIGS = {
     "mrb_densify": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp]),
     "mrb_warp_image": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "mrb_msd": (C.c_int, [_vp, _i64, _vp, _vp, _vp]),
+    # pixel-grid engine (baseline.py)
+    "mrb_register_pixelwise": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp,
+                                         C.POINTER(mrb_pixel_config), _vp, _vp, _vp, _vp,
+                                         C.POINTER(_i32), _dp, _dp]),
+    "mrb_pixel_batch_create": (C.c_int, [_vp, _i32, _i32, _i32, _i32,
+                                         C.POINTER(mrb_pixel_config), C.POINTER(_vp)]),
+    "mrb_pixel_batch_destroy": (C.c_int, [_vp]),
+    "mrb_pixel_batch_set_images": (C.c_int, [_vp, _vp, _vp, _i32]),
+    "mrb_pixel_batch_run": (C.c_int, [_vp]),
+    "mrb_pixel_batch_get_results": (C.c_int, [_vp, _i32, _vp, _vp, _vp]),
+    "mrb_pixel_batch_sync": (C.c_int, [_vp]),
+    "mrb_pixel_batch_pair_status": (C.c_int, [_vp, _i32, C.POINTER(_i32), _dp, _dp, _vp,
+                                              C.c_char_p, _i32]),
+    "mrb_pixel_batch_launches_per_run": (_i64, [_vp]),
+    "mrb_pixel_batch_kernel_times": (C.c_int, [_vp, _vp]),
+    "mrb_sample_gradient": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp]),
+    "mrb_grid_umbrella_smooth": (C.c_int, [_vp, _i32, _i32, _vp, C.c_double, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -22,6 +22,7 @@
 
 #include "../../include/meshreg_b200.h"
 #include "cluster.cuh"
+#include "pixel.cuh"
 #include "kernels.cuh"
 #include "mesh_host.h"
 
@@ -2260,3 +2261,6 @@ int mrb_msd(mrb_ctx* ctx, int64_t n, const double* a, const double* b, double* o
 }
 
 }  // extern "C"
+
+// pixel-grid engine (baseline.py)
+#include "pixel_api.cuh"

@@ -52,6 +52,26 @@ class ImageGrid:
         out = sample_points(self, pts)
         return float(out[0]) if scalar else out.reshape(xb.shape)
 
+    def sample_gradient(self, x, y):
+        """Analytic (d/dx, d/dy) of the bicubic interpolant (image.py:86-103),
+        one-sided at clamped out-of-domain points; fp64 on the GPU."""
+        x = np.asarray(x, dtype=np.float64)
+        y = np.asarray(y, dtype=np.float64)
+        scalar = x.ndim == 0 and y.ndim == 0
+        xb, yb = np.broadcast_arrays(x, y)
+        pts = np.ascontiguousarray(np.stack([xb.ravel(), yb.ravel()], axis=1))
+        lib = _lib.load()
+        ctx = _lib.context()
+        data, dt = _lib.image_payload(self.data)
+        gx = np.empty(pts.shape[0])
+        gy = np.empty(pts.shape[0])
+        rc = lib.mrb_sample_gradient(ctx, self.width, self.height, dt, _lib.ptr(data),
+                                     pts.shape[0], _lib.ptr(pts), _lib.ptr(gx), _lib.ptr(gy))
+        _lib.check(rc, ctx, (ValueError, RuntimeError, RuntimeError))
+        if scalar:
+            return float(gx[0]), float(gy[0])
+        return gx.reshape(xb.shape), gy.reshape(xb.shape)
+
     def __eq__(self, other):
         if not isinstance(other, ImageGrid):
             return NotImplemented

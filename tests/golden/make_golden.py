@@ -199,6 +199,41 @@ def main():
     save("diverge64", re=ref.data, te=te.data, **mesh_parts(mesh, with_ops=False),
          error=np.array(msg), cfg=np.array([0.1, 0.8, 100, 1, 1e-6]))
 
+    # pixel-grid engine (baseline.py)
+    from meshreg.baseline import register_pixelwise, grid_umbrella_smooth
+    for name, w, seed, shift, kw in (("pixel64", 64, 11, (1.5, 0.5), dict(iterations=30)),
+                                     ("pixel96_p1", 96, 5, (2.0, 0.0),
+                                      dict(iterations=40, smoothing_passes=1, tau=0.004)),
+                                     ("pixel48_lam0", 48, 9, (1.0, 0.0),
+                                      dict(iterations=15, lam=0.0))):
+        ref = synthetic.smooth_texture(w, w, seed=seed, low=100, high=156)
+        field = synthetic.plateau_shift_field(w, w, shift=shift)
+        _, te = synthetic.warped_pair(ref, field)
+        out, rep = register_pixelwise(ref, te, **kw)
+        kwv = dict(tau=0.005, lam=0.8, iterations=100, smoothing_passes=3)
+        kwv.update(kw)
+        save(name, re=ref.data, te=te.data, ux=out.ux, uy=out.uy,
+             warped=mr.warp_image(te, out).data, trace=np.array(rep.energy_trace),
+             iterations_run=rep.iterations_run, msd_before=rep.msd_before,
+             msd_after=rep.msd_after,
+             cfg=np.array([kwv["tau"], kwv["lam"], kwv["iterations"], kwv["smoothing_passes"]]))
+    rng = np.random.default_rng(5)
+    img = smooth_image(16, 13, seed=3)
+    pts = rng.uniform([-1.0, -1.0], [17.0, 14.0], (200, 2))
+    gx, gy = img.sample_gradient(pts[:, 0], pts[:, 1])
+    plane = rng.uniform(-5, 5, (11, 7))
+    save("pixel_units", img=img.data, pts=pts, gx=gx, gy=gy, plane=plane,
+         smooth=grid_umbrella_smooth(plane, 0.6))
+    ref = synthetic.smooth_texture(48, 48, seed=7, low=20, high=235)
+    field = synthetic.plateau_shift_field(48, 48, shift=(2.0, 0.0))
+    _, te = synthetic.warped_pair(ref, field)
+    try:
+        register_pixelwise(ref, te, tau=0.2)
+        msg = ""
+    except mr.DivergenceError as exc:
+        msg = str(exc)
+    save("pixel_diverge48", re=ref.data, te=te.data, error=np.array(msg))
+
     # full BASELINE config 1 pair (seed 0) on the cached reference mesh
     mpath = os.path.join(ROOT, "data", "meshes", "c1_s0.npz")
     if os.path.exists(mpath):

@@ -77,3 +77,45 @@ def test_oracle_divergence_message():
     with pytest.raises(O.OracleDivergence) as exc:
         O.register(g["re"], g["te"], m, tau=0.1)
     assert str(exc.value) == str(g["error"])
+
+
+# ---- pixel-grid engine (baseline.py) ----------------
+PIXEL_CASES = ["pixel64", "pixel96_p1", "pixel48_lam0"]
+
+
+@pytest.mark.parametrize("name", PIXEL_CASES)
+def test_oracle_register_pixelwise_bit_exact(name):
+    g = golden(name)
+    tau, lam, iters, passes = g["cfg"]
+    ux, uy, info = O.register_pixelwise(g["re"], g["te"], tau=tau, lam=lam,
+                                        iterations=int(iters), smoothing_passes=int(passes))
+    assert info["iterations_run"] == int(g["iterations_run"])
+    assert np.array_equal(np.array(info["energy_trace"]), g["trace"])
+    assert np.array_equal(ux, g["ux"]) and np.array_equal(uy, g["uy"])
+    assert np.array_equal(info["warped"], g["warped"])
+    assert info["msd_before"] == float(g["msd_before"])
+    assert info["msd_after"] == float(g["msd_after"])
+
+
+def test_oracle_pixel_units_bit_exact():
+    g = golden("pixel_units")
+    gx, gy = O.sample_gradient(g["img"], g["pts"][:, 0], g["pts"][:, 1])
+    assert np.array_equal(gx, g["gx"]) and np.array_equal(gy, g["gy"])
+    assert np.array_equal(O.grid_umbrella_smooth(g["plane"], 0.6), g["smooth"])
+
+
+def test_oracle_pixel_divergence_message():
+    g = golden("pixel_diverge48")
+    with pytest.raises(O.OracleDivergence) as e:
+        O.register_pixelwise(g["re"], g["te"], tau=0.2)
+    assert str(e.value) == str(g["error"])
+
+
+def test_oracle_pixel_validation():
+    z = np.zeros((8, 8))
+    for kw, msg in ((dict(tau=0.0), "tau must be positive"), (dict(lam=1.0), "lambda must be in [0, 1)"),
+                    (dict(iterations=0), "iterations must be >= 1")):
+        with pytest.raises(ValueError, match=msg.replace("[", r"\[").replace(")", r"\)")):
+            O.register_pixelwise(z, z, **kw)
+    with pytest.raises(ValueError, match="image sizes differ"):
+        O.register_pixelwise(z, np.zeros((8, 9)))
