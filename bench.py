@@ -18,8 +18,12 @@ own 64-pair batch).
   --impl reference   the reference algorithm (CPU oracle port of meshreg, one
           process per core, one pair each) on the same workload.
 
+  --workload pixel   the reference's dense comparator engine (baseline.py,
+          SURVEY.md §8(f) row 1) on the config-4 batch: 64 pairs of 512x512,
+          200 iterations, 3 smoothing passes, same metric.
+
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                       [--workload c4|c1|c2|c3] [--pairs P] [--precision f32|f64]
+                       [--workload c4|c1|c2|c3|pixel] [--pairs P] [--precision f32|f64]
 """
 from __future__ import annotations
 
@@ -51,7 +55,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "pixel"])
     ap.add_argument("--pairs", type=int, default=None)
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -81,7 +85,7 @@ def fallback_mesh(size, target):
 
 
 def workload_spec(name):
-    spec = CONFIGS["c2" if name == "c4" else name]
+    spec = CONFIGS["c2" if name in ("c4", "pixel") else name]
     mesh_cfg = spec.name
     return spec, mesh_cfg
 
@@ -438,13 +442,19 @@ def cpu_baseline(args, pairs, spec):
 
 def _ref_worker(conn, workload, seed, iters):
     os.environ["OMP_NUM_THREADS"] = "1"
-    re, te, V, T, kind, used = load_pair(workload, seed)
+    if workload == "pixel":
+        re, te = make_pair(CONFIGS["c2"], seed)
+    else:
+        re, te, V, T, kind, used = load_pair(workload, seed)
     conn.send("ready")
     while True:
         msg = conn.recv()
         if msg == "stop":
             break
-        conn.send(_oracle_register(re, te, V, T, iters))
+        if workload == "pixel":
+            conn.send(_oracle_pixelwise(re, te, iters))
+        else:
+            conn.send(_oracle_register(re, te, V, T, iters))
 
 
 def run_reference(args, rank, world):
@@ -452,7 +462,7 @@ def run_reference(args, rank, world):
         return  # rank 0 alone runs the CPU reference arm
     import multiprocessing as mp
     spec, _ = workload_spec(args.workload)
-    P = args.pairs or (64 if args.workload == "c4" else 1)
+    P = args.pairs or (64 if args.workload in ("c4", "pixel") else 1)
     cores = len(os.sched_getaffinity(0))
     nproc = max(1, min(P, cores))
     env_bak = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS",
@@ -460,10 +470,11 @@ def run_reference(args, rank, world):
     for k in env_bak:
         os.environ[k] = "1"
     ctx = mp.get_context("spawn")
+    it_ref = PIXEL_REF_ITERS if args.workload == "pixel" else spec.iterations
     procs, conns = [], []
     for i in range(nproc):
         a, b = ctx.Pipe()
-        p = ctx.Process(target=_ref_worker, args=(b, args.workload, i, spec.iterations))
+        p = ctx.Process(target=_ref_worker, args=(b, args.workload, i, it_ref))
         p.start()
         procs.append(p)
         conns.append(a)
@@ -492,16 +503,177 @@ def run_reference(args, rank, world):
         "data": "synthetic (seeded BASELINE generator; meshes from the reference mesher)",
         "config": {"workload": f"{args.workload}: bounded sample of {nproc} pairs per step "
                                f"(one per host core) of {spec.size}x{spec.size}, "
-                               f"{spec.iterations} iterations",
+                               f"{it_ref} iterations",
                    "pairs_per_step": nproc, "image": [spec.size, spec.size],
-                   "iterations": spec.iterations, "energy_tolerance": 0.0},
+                   "iterations": it_ref, "energy_tolerance": 0.0},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": nproc, "kind": "port",
                          "sample": f"{nproc} pairs per step, one process per core, oracle port "
-                                   "of meshreg register (numpy/scipy, float64)"},
+                                   "of meshreg " + ("register_pixelwise" if args.workload == "pixel"
+                                                    else "register") + " (numpy/scipy, float64)"},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
+
+
+# --------------------------------------------------------------------------- pixel engine
+PIXEL_ITERS, PIXEL_PASSES = 200, 3
+PIXEL_REF_ITERS = 20  # bounded CPU sample per pair (numpy: ~0.1 s per 512x512 iteration)
+
+
+def _oracle_pixelwise(re, te, iters):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import meshreg_oracle as O
+    t0 = time.perf_counter()
+    _, _, info = O.register_pixelwise(re.astype(np.float64), te.astype(np.float64), tau=0.005,
+                                      lam=0.8, iterations=iters, smoothing_passes=PIXEL_PASSES)
+    return time.perf_counter() - t0, info["iterations_run"]
+
+
+def run_pixel(args, rank, world, local):
+    """The dense per-pixel engine (reference baseline.py) on the config-4
+    batch through the C ABI (mrb_pixel_batch_*)."""
+    import torch
+    from paper_1411_2141_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dist = dist_init("nccl", local) if world > 1 else None
+    device = torch.device("cuda", local)
+    lib = _lib.load()
+    ctx = _lib.context(local)
+    stream = torch.cuda.ExternalStream(lib.mrb_ctx_stream(ctx), device=device)
+    spec = CONFIGS["c2"]
+    P = args.pairs or 64
+    seeds, used = pairqueue.shard_seeds(rank, P, None)
+    pairs = [make_pair(spec, s) for s in used]
+    W = H = spec.size
+    npx = W * H
+    prec = _lib.PREC_F32 if args.precision == "f32" else _lib.PREC_F64
+    pcfg = _lib.mrb_pixel_config(0.005, 0.8, PIXEL_ITERS, PIXEL_PASSES, prec, 0)
+    batch = C.c_void_p()
+    check(lib, ctx, lib.mrb_pixel_batch_create(ctx, P, W, H, _lib.F32, C.byref(pcfg),
+                                               C.byref(batch)), "pixel_batch_create")
+    re_d = torch.from_numpy(np.stack([p[0] for p in pairs])).to(device)
+    te_d = torch.from_numpy(np.stack([p[1] for p in pairs])).to(device)
+    torch.cuda.synchronize()
+    check(lib, ctx, lib.mrb_pixel_batch_set_images(batch, re_d.data_ptr(), te_d.data_ptr(), 1),
+          "set")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+    for _ in range(max(args.warmup, 3)):
+        check(lib, ctx, lib.mrb_pixel_batch_run(batch), "run")
+    check(lib, ctx, lib.mrb_pixel_batch_sync(batch), "warmup sync")
+    kt = np.zeros(2)
+    check(lib, ctx, lib.mrb_pixel_batch_kernel_times(batch, kt.ctypes.data), "kernel_times")
+
+    barrier(world, dist)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    evs = []
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            check(lib, ctx, lib.mrb_pixel_batch_run(batch), "run")
+            e1.record(stream)
+            evs.append((e0, e1))
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    barrier(world, dist)
+    t_ms = reduce_max(sum(a.elapsed_time(b) for a, b in evs), world, dist, device)
+    check(lib, ctx, lib.mrb_pixel_batch_sync(batch), "result status")
+    it = C.c_int32()
+    tot_iters = 0
+    for p in range(P):
+        lib.mrb_pixel_batch_pair_status(batch, p, C.byref(it), None, None, None, None, 0)
+        tot_iters += it.value
+    value = pairqueue.job_throughput(float(npx) * tot_iters * args.steps, t_ms / 1e3, world)
+    launches = int(lib.mrb_pixel_batch_launches_per_run(batch)) * args.steps
+
+    # e2e: pinned host stacks -> set_images (H2D) -> run -> get_results (D2H) -> sync
+    e2e = None
+    if not args.no_e2e:
+        re_h = torch.from_numpy(np.stack([p[0] for p in pairs])).pin_memory()
+        te_h = torch.from_numpy(np.stack([p[1] for p in pairs])).pin_memory()
+        outs = [torch.empty((P, H, W), dtype=torch.float32).pin_memory() for _ in range(3)]
+        cnt = np.zeros(2, np.int64)
+        times = []
+        steps = max(1, min(args.steps, 5))
+        for step in range(1 + steps):
+            torch.cuda.synchronize()
+            barrier(world, dist)
+            lib.mrb_transfer_bytes(None, None, 1)
+            t0 = time.perf_counter()
+            check(lib, ctx, lib.mrb_pixel_batch_set_images(batch, re_h.data_ptr(), te_h.data_ptr(),
+                                                           0), "e2e set")
+            check(lib, ctx, lib.mrb_pixel_batch_run(batch), "e2e run")
+            check(lib, ctx, lib.mrb_pixel_batch_get_results(batch, _lib.F32,
+                                                            *(o.data_ptr() for o in outs)), "get")
+            check(lib, ctx, lib.mrb_pixel_batch_sync(batch), "e2e sync")
+            dt = time.perf_counter() - t0
+            lib.mrb_transfer_bytes(cnt.ctypes.data, cnt[1:].ctypes.data, 1)
+            if step:
+                times.append(dt)
+        t = reduce_max(sum(times), world, dist, device)
+        e2e = {"value": round(pairqueue.job_throughput(float(npx) * tot_iters * steps, t, world), 3),
+               "unit": UNIT, "steps": steps, "ms_per_step": round(1e3 * t / steps, 3),
+               "h2d_bytes_per_step": int(cnt[0]), "d2h_bytes_per_step": int(cnt[1]),
+               "api": "mrb_pixel_batch_set_images(host) + run + get_results + sync",
+               "includes": "H2D images, full registration, D2H ux/uy/warped + statuses"}
+    lib.mrb_pixel_batch_destroy(batch)
+
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    es = 4 if args.precision == "f32" else 8
+    bytes_launch = float(P) * npx * 6 * es  # read u, write u, read (Te, Re): 3 pairs of Real
+    achieved = bytes_launch / (kt[0] / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("pixel", {}).get(args.precision, {}).get(
+            "k_pixel_iter")
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        tot, work = 0.0, 0.0
+        for re, te in pairs[:1]:
+            dt, its = _oracle_pixelwise(re, te, PIXEL_REF_ITERS)
+            tot += dt
+            work += float(npx) * its
+        cpu = {"value": round(work / tot / 1e6, 4), "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"1 pair (seed {used[0]}) 512x512, {PIXEL_REF_ITERS} iterations of the "
+                         f"oracle register_pixelwise (numpy float64), {tot:.1f} s"}
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": round(t_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
+            "data": "synthetic (seeded BASELINE generator, config-2 pairs)",
+            "config": {"workload": f"pixel: {P} pairs/GPU of {W}x{H}, {PIXEL_ITERS} iterations, "
+                                   f"{PIXEL_PASSES} smoothing passes (reference baseline.py engine)",
+                       "pairs_per_gpu": P, "global_pairs": P * world, "image": [W, H],
+                       "iterations": PIXEL_ITERS, "tau": 0.005, "lam": 0.8,
+                       "smoothing_passes": PIXEL_PASSES, "pair_seeds": f"{seeds[0]}..{seeds[-1]}",
+                       "l2": "flushed (256 MiB write) between timed steps, outside the events",
+                       "parallelism": f"pair-sharded dp{world} (no collective)",
+                       "precision": args.precision},
+            "gpu_launches": launches,
+            "kernel_ms": {"k_pixel_iter": round(float(kt[0]), 5), "run": round(float(kt[1]), 4)},
+            "roofline": {"kernel": "k_pixel_iter", "bound": "hbm", "achieved": round(achieved, 1),
+                         "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
+                         "note": "algorithmic bytes = read u + write u + read (Te, Re) per pixel "
+                                 "per iteration; the kernel is instruction-issue bound (bicubic "
+                                 "value + gradient per pixel, 3 smoothing passes in SMEM)"},
+            "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
@@ -509,6 +681,8 @@ def main():
     rank, world, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.workload == "pixel":
+        run_pixel(args, rank, world, local)
     else:
         run_ours(args, rank, world, local)
 

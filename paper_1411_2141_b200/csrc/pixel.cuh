@@ -15,11 +15,13 @@
 // exit, so the decisions only depend on the trace).
 #pragma once
 
+#include <cuda.h>
+
 #include "kernels.cuh"
 
 namespace mrb {
 
-constexpr int kPixThreads = 512, kPixMaxR = 4;
+constexpr int kPixThreads = 512, kPixMaxR = 3;
 // tile per CTA: 64x32 (fp32 state) / 32x32 (fp64 state); the (TX+2R)x(TY+2R)
 // ping-pong state tiles stay under the 48 KB static shared-memory limit
 template <typename Real> struct PixTile {
@@ -29,17 +31,42 @@ template <typename Real> struct PixTile {
 template <typename Real>
 struct PixelDev {
   using R2 = typename V2<Real>::type;
-  const R2* img;     // padded (H+2)x(W+2) interleaved (Te, Re), ring included
+  const R2* img;     // padded (H+2) rows x (W+2) of interleaved (Te, Re), ring
+                     // included, row pitch `pitch` elements (16-byte multiple)
+  const CUtensorMap* tmap;  // TMA descriptor of img (2-D, Real elements)
   R2* u[2];          // double-buffered (ux, uy) planes, H x W
   Real* warped;      // H x W
   double* partials;  // [iterations][tiles]
-  int W, H, tiles_x, tiles;
+  int W, H, pitch, tiles_x, tiles;
 };
+
+// Shared-memory patch of the padded image staged by TMA per tile: region
+// + Catmull-Rom footprint (3) + displacement margin kPixD on each side.
+constexpr int kPixD = 4;
+// The patch is sized for the largest halo (kPixMaxR) so one TMA descriptor
+// (box) per pair serves every R; its origin is (x0, y0) - kPixMaxR - kPixD.
+template <typename Real, int R> struct PixPatch {
+  static constexpr int RW = PixTile<Real>::TX + 2 * R, RH = PixTile<Real>::TY + 2 * R;
+  // margin left/top of the tile, even: a TMA box must start on a 16-byte
+  // boundary of the row (x0 is a multiple of TX)
+  static constexpr int M = (kPixMaxR + kPixD + 1) / 2 * 2;
+  static constexpr int PW0 = PixTile<Real>::TX + 2 * M + 3;
+  // inner box bytes a multiple of 16
+  static constexpr int PW = sizeof(Real) == 4 ? (PW0 + 1) / 2 * 2 : PW0;
+  static constexpr int PH = PixTile<Real>::TY + 2 * M + 3;
+  static constexpr size_t patch_bytes = size_t(PW) * PH * 2 * sizeof(Real);
+  static constexpr size_t buf_bytes = size_t(RW) * RH * 2 * sizeof(Real);
+  static constexpr size_t smem_bytes = patch_bytes + 2 * buf_bytes;
+};
+
+__device__ __forceinline__ unsigned pix_smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
 
 // padded (Te, Re) image in Real with the ring computed in fp64
 template <typename InT, typename Real>
 __global__ void k_pixel_pad(const InT* const* __restrict__ re, const InT* const* __restrict__ te,
-                            int W, int H, typename V2<Real>::type* __restrict__ out,
+                            int W, int H, int pitch, typename V2<Real>::type* __restrict__ out,
                             size_t out_stride) {
   const int Wp = W + 2, Hp = H + 2;
   const InT* r_img = re[blockIdx.y];
@@ -48,9 +75,10 @@ __global__ void k_pixel_pad(const InT* const* __restrict__ re, const InT* const*
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Wp * Hp; q += gridDim.x * blockDim.x) {
     const int r = q / Wp, c = q - r * Wp;
     typename V2<Real>::type f;
+    const size_t at = size_t(r) * pitch + c;
     f.x = Real(ext_tap<InT, double, 1>(t_img, W, H, r, c).v[0]);
     f.y = Real(ext_tap<InT, double, 1>(r_img, W, H, r, c).v[0]);
-    dst[q] = f;
+    dst[at] = f;
   }
 }
 
@@ -65,142 +93,313 @@ __device__ __forceinline__ void cr_dweights(Real t, Real w[4]) {
   w[3] = mul_rn(h, sub_rn(mul_rn(Real(3), t2), mul_rn(Real(2), t)));
 }
 
-// value of Te and Re and the analytic gradient of Te at (x, y), from the
-// padded image (no border branch): s = (Te, Re), g = (dTe/dx, dTe/dy)
+// Clamped cell + fraction of a displaced coordinate q + u (q integer): the
+// reference computes xc = clip(q + u, 0, n - 1), c = min(floor(xc), n - 2),
+// t = xc - c in fp64 (image.py:105-121).  q + u splits exactly into the
+// integer q + floor(u) and the fraction u - floor(u), so c and t come out
+// bit-identical without fp64 arithmetic.
 template <typename Real>
-__device__ __forceinline__ void sample_with_gradient(const typename V2<Real>::type* __restrict__ img,
-                                                     int W, int H, double x, double y,
-                                                     typename V2<Real>::type& s,
-                                                     typename V2<Real>::type& g) {
-  const double xc = fmin(fmax(x, 0.0), double(W) - 1.0);
-  const double yc = fmin(fmax(y, 0.0), double(H) - 1.0);
-  const int cx = min(int(xc), W - 2);
-  const int cy = min(int(yc), H - 2);
-  const Real tx = Real(xc - double(cx)), ty = Real(yc - double(cy));
-  Real wx[4], wy[4], dwx[4], dwy[4];
-  cr_weights<Real>(tx, wx);
-  cr_weights<Real>(ty, wy);
-  cr_dweights<Real>(tx, dwx);
-  cr_dweights<Real>(ty, dwy);
-  const auto* base = img + (size_t(cy) * (W + 2) + cx);
-  Real te = 0, re = 0, gx = 0, gy = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    Real rt = 0, rr = 0, rd = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const auto v = __ldg(base + size_t(j) * (W + 2) + i);
-      rt = fma(wx[i], v.x, rt);
-      rr = fma(wx[i], v.y, rr);
-      rd = fma(dwx[i], v.x, rd);
-    }
-    te = fma(wy[j], rt, te);
-    re = fma(wy[j], rr, re);
-    gx = fma(wy[j], rd, gx);
-    gy = fma(dwy[j], rt, gy);
+__device__ __forceinline__ void locate_axis(int q, Real u, int n, int& c, Real& t) {
+  const Real fl = floor(u);
+  t = u - fl;  // exact
+  c = q + int(fl);
+  if (c < 0) {
+    c = 0;
+    t = Real(0);
+  } else if (c >= n - 1) {
+    c = n - 2;
+    t = Real(1);
   }
-  s.x = te;
-  s.y = re;
-  g.x = gx;
-  g.y = gy;
 }
 
-template <typename Real>
-__global__ void __launch_bounds__(kPixThreads)
-    k_pixel_iter(const PixelDev<Real>* __restrict__ pairs, int k, int src, Real tau, Real lam,
-                 int R, int descend, int clamp) {
+// packed fp32x2 FMA (FFMA2 on sm_100a): r = a * b + c lane-wise
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long ra, rb, rc, rd;
+  memcpy(&ra, &a, 8);
+  memcpy(&rb, &b, 8);
+  memcpy(&rc, &c, 8);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
+  float2 r;
+  memcpy(&r, &rd, 8);
+  return r;
+}
+
+// (w_i, dw_i) Catmull-Rom weight / derivative pairs by Horner in FFMA2
+// (image.py:154-178 expanded: w_i = ((a3 t + a2) t + a1) t + a0,
+// dw_i = (b2 t + b1) t + b0)
+__device__ __forceinline__ void cr_weight_pairs(float t, float2 wd[4]) {
+  const float2 tt = make_float2(t, t);
+  const float2 A3[4] = {{-0.5f, 0.f}, {1.5f, 0.f}, {-1.5f, 0.f}, {0.5f, 0.f}};
+  const float2 A2[4] = {{1.0f, -1.5f}, {-2.5f, 4.5f}, {2.0f, -4.5f}, {-0.5f, 1.5f}};
+  const float2 A1[4] = {{-0.5f, 2.0f}, {0.0f, -5.0f}, {0.5f, 4.0f}, {0.0f, -1.0f}};
+  const float2 A0[4] = {{0.0f, -0.5f}, {1.0f, 0.0f}, {0.0f, 0.5f}, {0.0f, 0.0f}};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 h = ffma2(A3[i], tt, A2[i]);
+    h = ffma2(h, tt, A1[i]);
+    wd[i] = ffma2(h, tt, A0[i]);
+  }
+}
+
+// value of Te and Re and the analytic gradient of Te at cell (cx, cy) +
+// fraction (tx, ty), from the padded image (no border branch):
+// s = (Te, Re), g = (dTe/dx, dTe/dy)
+template <typename Real, bool SMEM = false>
+__device__ __forceinline__ void sample_with_gradient(const typename V2<Real>::type* __restrict__ img,
+                                                     int pitch, int cx, int cy, Real tx, Real ty,
+                                                     typename V2<Real>::type& s,
+                                                     typename V2<Real>::type& g) {
   using R2 = typename V2<Real>::type;
-  constexpr int kPixTX = PixTile<Real>::TX, kPixTY = PixTile<Real>::TY;
-  constexpr int RW = kPixTX + 2 * kPixMaxR, RH = kPixTY + 2 * kPixMaxR;
-  __shared__ R2 buf[2][RH * RW];
+  const R2* base = img + (size_t(cy) * pitch + cx);
+  auto tap = [&](int j, int i) -> R2 {
+    if constexpr (SMEM)
+      return base[j * pitch + i];
+    else
+      return __ldg(base + size_t(j) * pitch + i);
+  };
+  if constexpr (std::is_same<Real, float>::value) {
+    float2 wdx[4], wdy[4];
+    cr_weight_pairs(tx, wdx);
+    cr_weight_pairs(ty, wdy);
+    float2 acc = make_float2(0.f, 0.f);  // (Te, Re)
+    float gx = 0.f, gy = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 row = make_float2(0.f, 0.f);  // (Te, Re) along x
+      float rd = 0.f;                      // dTe/dx along x
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 v = tap(j, i);
+        row = ffma2(make_float2(wdx[i].x, wdx[i].x), v, row);
+        rd = fmaf(wdx[i].y, v.x, rd);
+      }
+      acc = ffma2(make_float2(wdy[j].x, wdy[j].x), row, acc);
+      gx = fmaf(wdy[j].x, rd, gx);
+      gy = fmaf(wdy[j].y, row.x, gy);
+    }
+    s = acc;
+    g = make_float2(gx, gy);
+  } else {
+    Real wx[4], wy[4], dwx[4], dwy[4];
+    cr_weights<Real>(tx, wx);
+    cr_weights<Real>(ty, wy);
+    cr_dweights<Real>(tx, dwx);
+    cr_dweights<Real>(ty, dwy);
+    Real te = 0, re = 0, gx = 0, gy = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      Real rt = 0, rr = 0, rd = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const auto v = tap(j, i);
+        rt = fma(wx[i], v.x, rt);
+        rr = fma(wx[i], v.y, rr);
+        rd = fma(dwx[i], v.x, rd);
+      }
+      te = fma(wy[j], rt, te);
+      re = fma(wy[j], rr, re);
+      gx = fma(wy[j], rd, gx);
+      gy = fma(dwy[j], rt, gy);
+    }
+    s.x = te;
+    s.y = re;
+    g.x = gx;
+    g.y = gy;
+  }
+}
+
+// Pair arithmetic on (x, y) state: packed f32x2 instructions for fp32 state
+// (FADD2/FMUL2/FFMA2, tolerance mode), exact-rounding scalar ops for fp64.
+__device__ __forceinline__ unsigned long long pk2(float2 a) {
+  unsigned long long r;
+  memcpy(&r, &a, 8);
+  return r;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long a) {
+  float2 r;
+  memcpy(&r, &a, 8);
+  return r;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(d);
+}
+__device__ __forceinline__ double2 add2(double2 a, double2 b) {
+  return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+// (1 - lam) * self + lq * tot, lq = lam / count (count 4 or 2: an exact
+// power-of-two scaling of lam * tot)
+__device__ __forceinline__ float2 blend2(float om, float2 self, float lq, float2 tot) {
+  unsigned long long d, m;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(m) : "l"(pk2(make_float2(om, om))), "l"(pk2(self)));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(make_float2(lq, lq))), "l"(pk2(tot)), "l"(m));
+  return upk2(d);
+}
+__device__ __forceinline__ double2 blend2(double om, double2 self, double lq, double2 tot) {
+  return make_double2(__dadd_rn(__dmul_rn(om, self.x), __dmul_rn(lq, tot.x)),
+                      __dadd_rn(__dmul_rn(om, self.y), __dmul_rn(lq, tot.y)));
+}
+
+// One grid_umbrella_smooth pass (baseline.py:27-43) over the cells of the
+// region at margin M (TX + 2(R-M)) x (TY + 2(R-M)).  INTERIOR: every such
+// cell and its four neighbours lie inside the image (count = 4).  Otherwise
+// out-of-image cells are skipped and hold zero, so a missing neighbour adds
+// +0 exactly like the reference's zero-initialised total.
+template <typename Real, int TX, int TY, int R, int M, bool INTERIOR>
+__device__ __forceinline__ void smooth_pass(const typename V2<Real>::type* __restrict__ b,
+                                            typename V2<Real>::type* __restrict__ o, int gx0,
+                                            int gy0, int W, int H, Real om, Real lam) {
+  using R2 = typename V2<Real>::type;
+  constexpr int RW = TX + 2 * R, w = RW - 2 * M, h = TY + 2 * R - 2 * M;
+  constexpr int n = w * h;
+  const Real lq4 = lam * Real(0.25);  // exact
+#pragma unroll 2
+  for (int c = threadIdx.x; c < n; c += kPixThreads) {
+    const int cy = c / w, cx = c - cy * w;  // constant divisor
+    const int rx = cx + M, ry = cy + M;
+    const int q = ry * RW + rx;
+    if (!INTERIOR) {
+      const int gx = gx0 + rx, gy = gy0 + ry;
+      if (gx < 0 || gx >= W || gy < 0 || gy >= H) continue;
+      const R2 tot = add2(add2(add2(b[q - RW], b[q + RW]), b[q - 1]), b[q + 1]);
+      const int cnt = (gy > 0) + (gy < H - 1) + (gx > 0) + (gx < W - 1);
+      R2 v;
+      if (cnt == 4) {
+        v = blend2(om, b[q], lq4, tot);
+      } else if (cnt == 2) {
+        v = blend2(om, b[q], lam * Real(0.5), tot);
+      } else {  // count 3 (or 0 for a 1-pixel plane: 0 / 0 like numpy)
+        const R2 self = b[q];
+        v.x = add_rn(mul_rn(om, self.x), div_rn(mul_rn(lam, tot.x), Real(cnt)));
+        v.y = add_rn(mul_rn(om, self.y), div_rn(mul_rn(lam, tot.y), Real(cnt)));
+      }
+      o[q] = v;
+    } else {
+      const R2 tot = add2(add2(add2(b[q - RW], b[q + RW]), b[q - 1]), b[q + 1]);
+      o[q] = blend2(om, b[q], lq4, tot);
+    }
+  }
+}
+
+template <typename Real, int TX, int TY, int R, int M, bool INTERIOR>
+__device__ __forceinline__ void smooth_passes(typename V2<Real>::type (*buf)[(TX + 2 * R) * (TY + 2 * R)],
+                                              int gx0, int gy0, int W, int H, Real om, Real lam) {
+  if constexpr (M <= R) {
+    smooth_pass<Real, TX, TY, R, M, INTERIOR>(buf[(M - 1) & 1], buf[M & 1], gx0, gy0, W, H, om,
+                                              lam);
+    __syncthreads();
+    smooth_passes<Real, TX, TY, R, M + 1, INTERIOR>(buf, gx0, gy0, W, H, om, lam);
+  }
+}
+
+// One pixel-engine iteration for a TX x TY tile with a halo of R passes
+// (baseline.py:74-101): sample + gradient + descent on the (TX+2R)x(TY+2R)
+// region, R smoothing passes in shared memory, clamp, store.  descend = 0:
+// smoothing-only launch (passes beyond kPixMaxR); clamp = 0: more passes
+// follow in another launch.
+template <typename Real, int R>
+__global__ void __launch_bounds__(kPixThreads, 2)
+    k_pixel_iter(const PixelDev<Real>* __restrict__ pairs, int k, int src, Real tau, Real lam,
+                 int descend, int clamp) {
+  using R2 = typename V2<Real>::type;
+  using PP = PixPatch<Real, R>;
+  constexpr int TX = PixTile<Real>::TX, TY = PixTile<Real>::TY;
+  constexpr int RW = PP::RW, RH = PP::RH, PW = PP::PW, PH = PP::PH;
+  extern __shared__ __align__(128) unsigned char pix_smem[];
+  R2* patch = reinterpret_cast<R2*>(pix_smem);
+  auto buf = reinterpret_cast<R2(*)[RW * RH]>(pix_smem + PP::patch_bytes);
   __shared__ double sh[2 * kPixThreads / 32];
+  __shared__ __align__(8) unsigned long long mbar;
   const PixelDev<Real>& d = pairs[blockIdx.y];
   const int tile = blockIdx.x;
-  const int x0 = (tile % d.tiles_x) * kPixTX, y0 = (tile / d.tiles_x) * kPixTY;
+  const int x0 = (tile % d.tiles_x) * TX, y0 = (tile / d.tiles_x) * TY;
   const R2* __restrict__ uin = d.u[src];
   R2* __restrict__ uout = d.u[src ^ 1];
   const int W = d.W, H = d.H;
-  // region cell (ry, rx) <-> pixel (y0 - R + ry, x0 - R + rx)
-  const int rw = kPixTX + 2 * R, rh = kPixTY + 2 * R;
+  const int gx0 = x0 - R, gy0 = y0 - R;  // pixel of region cell (0, 0)
+  // patch origin in padded-image coordinates (may be negative: TMA zero-fills)
+  const int px0 = x0 - PP::M, py0 = y0 - PP::M;
+  const bool use_tma = !(descend & 2);  // bit 1: debug switch, global taps only
+  descend &= 1;
+  if (descend && use_tma && threadIdx.x == 0) {
+    const unsigned mb = pix_smem_u32(&mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                 "r"(unsigned(PP::patch_bytes))
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(pix_smem_u32(patch)),
+        "l"(reinterpret_cast<unsigned long long>(d.tmap)), "r"(int(sizeof(R2) / 8) * px0), "r"(py0), "r"(mb)
+        : "memory");
+  }
+  __syncthreads();  // mbarrier initialised before anyone waits on it
+  bool patch_ready = false;
   double e2 = 0.0;
-  for (int c = threadIdx.x; c < rw * rh; c += kPixThreads) {
-    const int ry = c / rw, rx = c - ry * rw;
-    const int gy = y0 - R + ry, gx = x0 - R + rx;
-    if (gx < 0 || gx >= W || gy < 0 || gy >= H) continue;
-    const R2 u = uin[size_t(gy) * W + gx];
-    if (!descend) {  // smoothing-only launch (passes beyond kPixMaxR)
-      buf[0][ry * RW + rx] = u;
+#pragma unroll 1
+  for (int c = threadIdx.x; c < RW * RH; c += kPixThreads) {
+    const int ry = c / RW, rx = c - ry * RW;
+    const int gx = gx0 + rx, gy = gy0 + ry;
+    if (gx < 0 || gx >= W || gy < 0 || gy >= H) {
+      buf[0][c] = R2{Real(0), Real(0)};
+      buf[1][c] = R2{Real(0), Real(0)};
       continue;
     }
+    const R2 u = uin[size_t(gy) * W + gx];
+    if (!descend) {
+      buf[0][c] = u;
+      continue;
+    }
+    int cx, cy;
+    Real tx, ty;
+    locate_axis<Real>(gx, u.x, W, cx, tx);
+    locate_axis<Real>(gy, u.y, H, cy, ty);
+    if (!patch_ready && use_tma) {  // first sample of this thread: wait for the TMA patch
+      const unsigned mb = pix_smem_u32(&mbar);
+      asm volatile(
+          "{\n .reg .pred p;\n WAIT_%=:\n"
+          " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+          " @!p bra WAIT_%=;\n}" ::"r"(mb)
+          : "memory");
+      patch_ready = true;
+    }
     R2 s, g;
-    sample_with_gradient<Real>(d.img, W, H, double(gx) + double(u.x), double(gy) + double(u.y),
-                               s, g);
+    const int lx = cx - px0, ly = cy - py0;  // footprint inside the patch?
+    if (use_tma && lx >= 0 && lx <= PW - 4 && ly >= 0 && ly <= PH - 4)
+      sample_with_gradient<Real, true>(patch, PW, lx, ly, tx, ty, s, g);
+    else  // displaced beyond kPixD: read the padded image in global memory
+      sample_with_gradient<Real>(d.img, d.pitch, cx, cy, tx, ty, s, g);
     const Real r = sub_rn(s.x, s.y);
     const Real tr = mul_rn(tau, r);  // ux - tau * r * dTe/dx  (baseline.py:94-95)
     R2 o;
     o.x = sub_rn(u.x, mul_rn(tr, g.x));
     o.y = sub_rn(u.y, mul_rn(tr, g.y));
-    buf[0][ry * RW + rx] = o;
-    if (rx >= R && rx < R + kPixTX && ry >= R && ry < R + kPixTY) e2 += double(r) * double(r);
+    buf[0][c] = o;
+    if (rx >= R && rx < R + TX && ry >= R && ry < R + TY) e2 = fma(double(r), double(r), e2);
   }
   __syncthreads();
-  int cur = 0;
-  for (int p = 0; p < R; ++p) {  // smoothing passes on a shrinking region
-    const int m = p + 1;         // margin of still-valid cells
-    for (int c = threadIdx.x; c < rw * rh; c += kPixThreads) {
-      const int ry = c / rw, rx = c - ry * rw;
-      if (rx < m || rx >= rw - m || ry < m || ry >= rh - m) continue;
-      const int gy = y0 - R + ry, gx = x0 - R + rx;
-      if (gx < 0 || gx >= W || gy < 0 || gy >= H) continue;
-      const R2* b = buf[cur];
-      // baseline.py:33-43: above, below, left, right; edge-aware counts
-      R2 tot;
-      tot.x = Real(0);
-      tot.y = Real(0);
-      Real cnt = Real(0);
-      if (gy > 0) {
-        const R2 v = b[(ry - 1) * RW + rx];
-        tot.x = add_rn(tot.x, v.x);
-        tot.y = add_rn(tot.y, v.y);
-        cnt = cnt + Real(1);
-      }
-      if (gy < H - 1) {
-        const R2 v = b[(ry + 1) * RW + rx];
-        tot.x = add_rn(tot.x, v.x);
-        tot.y = add_rn(tot.y, v.y);
-        cnt = cnt + Real(1);
-      }
-      if (gx > 0) {
-        const R2 v = b[ry * RW + rx - 1];
-        tot.x = add_rn(tot.x, v.x);
-        tot.y = add_rn(tot.y, v.y);
-        cnt = cnt + Real(1);
-      }
-      if (gx < W - 1) {
-        const R2 v = b[ry * RW + rx + 1];
-        tot.x = add_rn(tot.x, v.x);
-        tot.y = add_rn(tot.y, v.y);
-        cnt = cnt + Real(1);
-      }
-      const R2 self = b[ry * RW + rx];
-      const Real om = sub_rn(Real(1), lam);
-      R2 o;  // (1 - lam) * plane + lam * total / count
-      o.x = add_rn(mul_rn(om, self.x), div_rn(mul_rn(lam, tot.x), cnt));
-      o.y = add_rn(mul_rn(om, self.y), div_rn(mul_rn(lam, tot.y), cnt));
-      buf[cur ^ 1][ry * RW + rx] = o;
-    }
-    __syncthreads();
-    cur ^= 1;
+  if constexpr (R > 0) {
+    const Real om = sub_rn(Real(1), lam);
+    // every smoothed cell and its neighbours inside the image?
+    const bool interior = x0 >= R && y0 >= R && x0 + TX + R <= W && y0 + TY + R <= H;
+    if (interior)
+      smooth_passes<Real, TX, TY, R, 1, true>(buf, gx0, gy0, W, H, om, lam);
+    else
+      smooth_passes<Real, TX, TY, R, 1, false>(buf, gx0, gy0, W, H, om, lam);
   }
-  for (int c = threadIdx.x; c < kPixTX * kPixTY; c += kPixThreads) {
-    const int ty = c / kPixTX, tx = c - ty * kPixTX;
+  const R2* __restrict__ fin = buf[R & 1];
+#pragma unroll 2
+  for (int c = threadIdx.x; c < TX * TY; c += kPixThreads) {
+    const int ty = c / TX, tx = c - ty * TX;
     const int gy = y0 + ty, gx = x0 + tx;
     if (gx >= W || gy >= H) continue;
-    R2 o = buf[cur][(ty + R) * RW + tx + R];
-    if (clamp) {  // np.clip(u, -x, (w - 1) - x), baseline.py:100-101
-      // (NaN propagates like np.clip; fmin/fmax alone would drop it)
-      if (o.x == o.x) o.x = Real(fmin(fmax(double(o.x), -double(gx)), (double(W) - 1.0) - double(gx)));
-      if (o.y == o.y) o.y = Real(fmin(fmax(double(o.y), -double(gy)), (double(H) - 1.0) - double(gy)));
+    R2 o = fin[(ty + R) * RW + tx + R];
+    if (clamp) {  // np.clip(u, -x, (w - 1) - x), baseline.py:100-101; the
+      // bounds are integers, exact in Real.  NaN propagates like np.clip.
+      if (o.x == o.x) o.x = fmin(fmax(o.x, Real(-gx)), Real(W - 1 - gx));
+      if (o.y == o.y) o.y = fmin(fmax(o.y, Real(-gy)), Real(H - 1 - gy));
     }
     uout[size_t(gy) * W + gx] = o;
   }
@@ -266,11 +465,14 @@ __global__ void __launch_bounds__(kPixBlock)
     const auto u = d.u[src][q];
     if (!isfinite(u.x) || !isfinite(u.y)) atomicOr(const_cast<int*>(&st[p].dense_nonfinite), 1);
     typename V2<Real>::type s, g;
-    sample_with_gradient<Real>(d.img, d.W, d.H, double(x) + double(u.x), double(y) + double(u.y),
-                               s, g);
+    int cx, cy;
+    Real tx, ty;
+    locate_axis<Real>(x, u.x, d.W, cx, tx);
+    locate_axis<Real>(y, u.y, d.H, cy, ty);
+    sample_with_gradient<Real>(d.img, d.pitch, cx, cy, tx, ty, s, g);
     d.warped[q] = s.x;
     if (!isfinite(s.x)) atomicOr(const_cast<int*>(&st[p].dense_nonfinite), 2);
-    const auto own = d.img[size_t(y + 1) * (d.W + 2) + (x + 1)];
+    const auto own = d.img[size_t(y + 1) * d.pitch + (x + 1)];
     const double d0 = double(own.x) - double(own.y);
     const double d1 = double(s.x) - double(own.y);
     acc.x = d0 * d0;

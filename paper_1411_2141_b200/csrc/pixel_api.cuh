@@ -15,6 +15,9 @@ struct mrb_pixel_batch {
   double2* msd_partials = nullptr;
   double* traces = nullptr;
   void* img = nullptr;         // padded (Te, Re) per pair
+  int pitch = 0;               // padded row pitch (R2 elements)
+  size_t img_stride = 0;       // R2 elements between pairs
+  CUtensorMap* tmaps = nullptr;  // device: TMA descriptor per pair
   void* u = nullptr;           // [2][pair][H*W] (ux, uy)
   void* warped = nullptr;      // [pair][H*W]
   void* stage = nullptr;
@@ -29,7 +32,7 @@ struct mrb_pixel_batch {
   ~mrb_pixel_batch() {
     if (graph) cudaGraphExecDestroy(graph);
     void* ptrs[] = {pairs, st, partials, msd_partials, traces, img, u, warped, stage, conv,
-                    const_cast<void**>(src_ptrs)};
+                    const_cast<void**>(src_ptrs), tmaps};
     for (void* p : ptrs) dev_free(p, ctx ? ctx->stream : nullptr);
   }
 };
@@ -62,6 +65,47 @@ size_t pixel_tile_counts(int W, int H, int* tiles_x) {
 }
 
 template <typename Real>
+void launch_pixel_iter(const mrb_pixel_batch* b, const PixelDev<Real>* pairs, int k, int src,
+                       Real tau, Real lam, int r, int descend, int clamp) {
+  const dim3 grid(b->tiles, b->n_pairs);
+  cudaStream_t s = b->ctx->stream;
+  static const int notma = std::getenv("MESHREG_B200_PIX_NOTMA") ? 2 : 0;  // debug switch
+#define MRB_PIX_LAUNCH(RR)                                                              \
+  k_pixel_iter<Real, RR><<<grid, kPixThreads, PixPatch<Real, RR>::smem_bytes, s>>>(     \
+      pairs, k, src, tau, lam, descend | notma, clamp)
+  switch (r) {
+    case 0: MRB_PIX_LAUNCH(0); break;
+    case 1: MRB_PIX_LAUNCH(1); break;
+    case 2: MRB_PIX_LAUNCH(2); break;
+    default: MRB_PIX_LAUNCH(3); break;
+  }
+#undef MRB_PIX_LAUNCH
+}
+
+template <typename Real, int RR>
+void pixel_smem_attr() {
+  ck(cudaFuncSetAttribute(k_pixel_iter<Real, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          int(PixPatch<Real, RR>::smem_bytes)));
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    ck(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw CudaError{cudaErrorNotSupported};
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+template <typename Real>
 void pixel_enqueue_t(mrb_pixel_batch* b, KernelTimer* tm) {
   using R2 = typename V2<Real>::type;
   cudaStream_t s = b->ctx->stream;
@@ -73,13 +117,13 @@ void pixel_enqueue_t(mrb_pixel_batch* b, KernelTimer* tm) {
     if (b->in_dtype == MRB_F64)
       k_pixel_pad<double, Real><<<dim3(g, n), 256, 0, s>>>(
           reinterpret_cast<const double* const*>(b->src_ptrs),
-          reinterpret_cast<const double* const*>(b->src_ptrs) + n, W, H,
-          static_cast<R2*>(b->img), npad);
+          reinterpret_cast<const double* const*>(b->src_ptrs) + n, W, H, b->pitch,
+          static_cast<R2*>(b->img), b->img_stride);
     else
       k_pixel_pad<float, Real><<<dim3(g, n), 256, 0, s>>>(
           reinterpret_cast<const float* const*>(b->src_ptrs),
-          reinterpret_cast<const float* const*>(b->src_ptrs) + n, W, H,
-          static_cast<R2*>(b->img), npad);
+          reinterpret_cast<const float* const*>(b->src_ptrs) + n, W, H, b->pitch,
+          static_cast<R2*>(b->img), b->img_stride);
     ck(cudaGetLastError());
   }
   ck(cudaMemsetAsync(b->u, 0, size_t(n) * npx * sizeof(R2), s));  // u0 = 0 (buffer 0)
@@ -89,15 +133,17 @@ void pixel_enqueue_t(mrb_pixel_batch* b, KernelTimer* tm) {
   for (int k = 0; k < b->cfg.iterations; ++k) {
     int r = std::min(passes, kPixMaxR), rem = passes - r;
     if (tm) tm->mark(0);
-    k_pixel_iter<Real><<<dim3(b->tiles, n), kPixThreads, 0, s>>>(pairs, k, src, tau, lam, r, 1,
-                                                                  rem == 0);
+    launch_pixel_iter<Real>(b, pairs, k, src, tau, lam, r, 1, rem == 0);
     if (tm) tm->mark(1);
+    if (std::getenv("MESHREG_B200_DEBUG")) {
+      ck(cudaStreamSynchronize(s));
+      ck(cudaGetLastError());
+    }
     src ^= 1;
     while (rem > 0) {
       r = std::min(rem, kPixMaxR);
       rem -= r;
-      k_pixel_iter<Real><<<dim3(b->tiles, n), kPixThreads, 0, s>>>(pairs, k, src, tau, lam, r, 0,
-                                                                    rem == 0);
+      launch_pixel_iter<Real>(b, pairs, k, src, tau, lam, r, 0, rem == 0);
       src ^= 1;
     }
   }
@@ -126,7 +172,15 @@ void pixel_setup_t(mrb_pixel_batch* b) {
   const size_t npx = size_t(b->W) * b->H, npad = size_t(b->W + 2) * (b->H + 2);
   b->tiles = int(pixel_tile_counts<Real>(b->W, b->H, &b->tiles_x));
   b->warp_blocks = int((npx + kPixBlock - 1) / kPixBlock);
-  b->img = dalloc<R2>(size_t(n) * npad);
+  // rows padded to a 16-byte multiple (TMA global stride rule)
+  b->pitch = sizeof(R2) == 8 ? (b->W + 2 + 1) / 2 * 2 : b->W + 2;
+  b->img_stride = size_t(b->pitch) * (b->H + 2);
+  b->img = dalloc<R2>(size_t(n) * b->img_stride);
+  ck(cudaMemsetAsync(b->img, 0, size_t(n) * b->img_stride * sizeof(R2), s));  // pitch pad
+  pixel_smem_attr<Real, 0>();
+  pixel_smem_attr<Real, 1>();
+  pixel_smem_attr<Real, 2>();
+  pixel_smem_attr<Real, 3>();
   b->u = dalloc<R2>(2 * size_t(n) * npx);
   b->warped = dalloc<Real>(size_t(n) * npx);
   b->partials = dalloc<double>(size_t(n) * b->cfg.iterations * b->tiles);
@@ -135,9 +189,28 @@ void pixel_setup_t(mrb_pixel_batch* b) {
   b->st = dalloc<PairStatus>(n);
   b->src_ptrs = dalloc<const void*>(2 * size_t(n));
   std::vector<PixelDev<Real>> h(n);
+  std::vector<CUtensorMap> maps(n);
+  b->tmaps = dalloc<CUtensorMap>(n);
   for (int p = 0; p < n; ++p) {
     PixelDev<Real>& d = h[p];
-    d.img = static_cast<const R2*>(b->img) + size_t(p) * npad;
+    d.img = static_cast<const R2*>(b->img) + size_t(p) * b->img_stride;
+    // 2-D view of the padded image in Real elements, (2 * pitch) x (H + 2);
+    // box = the k_pixel_iter patch (same for every halo R)
+    // (8-byte elements: one per float2, two per double2)
+    constexpr int epr = int(sizeof(R2) / 8);
+    const cuuint64_t gdim[2] = {cuuint64_t(epr) * b->pitch, cuuint64_t(b->H + 2)};
+    const cuuint64_t gstride[1] = {cuuint64_t(b->pitch) * sizeof(R2)};
+    const cuuint32_t box[2] = {cuuint32_t(epr * PixPatch<Real, kPixMaxR>::PW),
+                               cuuint32_t(PixPatch<Real, kPixMaxR>::PH)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult cr = encode_tiled()(
+        &maps[p], CU_TENSOR_MAP_DATA_TYPE_UINT64,
+        2, const_cast<R2*>(d.img), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) throw CudaError{cudaErrorInvalidValue};
+    d.tmap = b->tmaps + p;
+    d.pitch = b->pitch;
     d.u[0] = static_cast<R2*>(b->u) + size_t(p) * npx;
     d.u[1] = static_cast<R2*>(b->u) + (size_t(n) + p) * npx;
     d.warped = static_cast<Real*>(b->warped) + size_t(p) * npx;
@@ -149,6 +222,7 @@ void pixel_setup_t(mrb_pixel_batch* b) {
   }
   b->pairs = dalloc<PixelDev<Real>>(n);
   ck(mrb_copy_async(b->pairs, h.data(), n * sizeof(PixelDev<Real>), cudaMemcpyHostToDevice, s));
+  ck(mrb_copy_async(b->tmaps, maps.data(), n * sizeof(CUtensorMap), cudaMemcpyHostToDevice, s));
   ck(cudaStreamSynchronize(s));  // h is a stack temporary
 }
 

@@ -1,0 +1,3 @@
+timeout 300 python tools/pixel_bench.py 64 f32 20 1 > gpurun_out/pix_plain.log 2>&1 && cat gpurun_out/pix_plain.log && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pixel_iter -s 5 -c 1 -o gpurun_out/prof_pix python tools/pixel_bench.py 64 f32 20 1 > gpurun_out/ncu_pix.log 2>&1; echo ncu rc=$?
+tail -2 gpurun_out/ncu_pix.log
