@@ -526,12 +526,13 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
 // same block partition as k_dense so k_msd_final reduces them unchanged.
 __global__ void __launch_bounds__(kPixBlock)
     k_dense_fast(const ClusterPair* __restrict__ pairs, PairStatus* __restrict__ st,
-                 const int* __restrict__ blk_pair, double2* __restrict__ partials) {
+                 const int* __restrict__ blk_pair, double2* __restrict__ partials, int blk0) {
   __shared__ double sh[2 * kPixBlock / 32];
-  const int p = blk_pair[blockIdx.x];
+  const int blk = blk0 + int(blockIdx.x);  // launched per group of pairs
+  const int p = blk_pair[blk];
   const ClusterPair& d = pairs[p];
   if (st[p].err) return;
-  const int q = (blockIdx.x - d.pix_blk_begin) * kPixBlock + threadIdx.x;
+  const int q = (blk - d.pix_blk_begin) * kPixBlock + threadIdx.x;
   double2 acc = make_double2(0.0, 0.0);
   if (q < d.W * d.H) {
     const int y = q / d.W, x = q - y * d.W;
@@ -561,7 +562,7 @@ __global__ void __launch_bounds__(kPixBlock)
     if (!isfinite(wv)) atomicOr(&st[p].dense_nonfinite, 2);
   }
   const double2 bs = block_sum2<kPixBlock>(acc, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = bs;
+  if (threadIdx.x == 0) partials[blk] = bs;
 }
 
 }  // namespace mrb

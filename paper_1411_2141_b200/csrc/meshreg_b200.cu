@@ -36,6 +36,8 @@ struct mrb_ctx {
   void* pinned = nullptr;  // host staging buffer for mesh uploads (grows)
   size_t pinned_cap = 0;
   cudaEvent_t stage_done = nullptr;  // last async copy out of `pinned`
+  cudaStream_t copy = nullptr;       // input copies of mrb_register_many
+  cudaEvent_t copy_done = nullptr;
 };
 
 struct mrb_mesh {
@@ -484,82 +486,98 @@ void ensure_device_mesh_f64(mrb_ctx* ctx, HostMesh& h) {
 //  * codes are CTA-local indices into [own slots (SLOTS = 768*npt) | halo];
 //  * halo[r] lists (owner rank << 16 | owner slot) of every remote node CTA r's
 //    one-rings reference, in first-reference order.
+// Host plan of one fast-path topology (cluster of cs CTAs, `chunk` nodes per
+// CTA): SELL-32 slice offsets, halo lists and the code of every one-ring
+// entry.  write_topo() then packs it straight into (pinned) memory.
 struct TopoHost {
   int chunk = 0, stride = 0, slices = 0, hstride = 0;
   size_t off[6] = {0, 0, 0, 0, 0, 0};
-  std::vector<unsigned char> packed;  // codes | g | slice_off | halo | n_halo | deg
+  size_t total = 0;                  // packed bytes
+  std::vector<uint32_t> soff;        // [cs][slices]
+  std::vector<uint32_t> halo;        // [cs][hstride]
+  std::vector<int> n_halo;           // [cs]
+  std::vector<uint16_t> code;        // per one-ring entry (CSR order)
 };
 
-TopoHost build_topo_host(const HostMesh& h, int cs, int chunk, int npt) {
+TopoHost plan_topo(const HostMesh& h, int cs, int chunk, int npt) {
   const int n = int(h.n);
   const int SLOTS = kClusterThreads * npt;
-  const int slices = (chunk + 31) / 32;
-  std::vector<uint32_t> soff(size_t(cs) * slices, 0);
-  int stride = 0;
+  TopoHost t;
+  t.chunk = chunk;
+  t.slices = (chunk + 31) / 32;
+  t.soff.assign(size_t(cs) * t.slices, 0);
+  t.code.resize(size_t(h.nb_ptr[n]));
   std::vector<std::vector<uint32_t>> halos(cs);
-  std::vector<std::vector<int>> halo_index(cs, std::vector<int>(size_t(n), -1));
+  std::vector<int> stamp(static_cast<size_t>(n), -1), hidx(static_cast<size_t>(n), 0);
+  int stride = 0;
   for (int r = 0; r < cs; ++r) {
     int acc = 0;
-    for (int sl = 0; sl < slices; ++sl) {
-      soff[size_t(r) * slices + sl] = uint32_t(acc);
+    for (int sl = 0; sl < t.slices; ++sl) {
+      t.soff[size_t(r) * t.slices + sl] = uint32_t(acc);
       int mx = 0;
       for (int s = sl * 32; s < std::min(chunk, sl * 32 + 32); ++s) {
         const int i = r * chunk + s;
-        if (i >= n) continue;
+        if (i >= n) break;
         mx = std::max(mx, h.nb_ptr[i + 1] - h.nb_ptr[i]);
         for (int q = h.nb_ptr[i]; q < h.nb_ptr[i + 1]; ++q) {
           const int j = h.nb_idx[q];
-          if (j / chunk != r && halo_index[r][j] < 0) {
-            halo_index[r][j] = int(halos[r].size());
-            halos[r].push_back(uint32_t((j / chunk) << 16 | (j % chunk)));
+          const int rj = j / chunk;
+          if (rj == r) {
+            t.code[q] = uint16_t(j - rj * chunk);
+            continue;
           }
+          if (stamp[j] != r) {  // first reference of remote node j by CTA r
+            stamp[j] = r;
+            hidx[j] = int(halos[r].size());
+            halos[r].push_back(uint32_t(rj << 16 | (j - rj * chunk)));
+          }
+          t.code[q] = uint16_t(SLOTS + hidx[j]);
         }
       }
       acc += 32 * mx;
     }
     stride = std::max(stride, acc);
   }
-  stride = std::max((stride + 7) / 8 * 8, 8);
+  t.stride = std::max((stride + 7) / 8 * 8, 8);
   int hstride = 2;
   for (auto& hl : halos) hstride = std::max<int>(hstride, int(hl.size()));
-  hstride = (hstride + 31) / 32 * 32;
-  std::vector<uint16_t> codes(size_t(cs) * stride, 0);
-  std::vector<float2> g(size_t(cs) * stride, make_float2(0.f, 0.f));
-  std::vector<unsigned char> deg(n);
+  t.hstride = (hstride + 31) / 32 * 32;
+  t.halo.assign(size_t(cs) * t.hstride, 0);
+  t.n_halo.resize(cs);
+  for (int r = 0; r < cs; ++r) {
+    t.n_halo[r] = int(halos[r].size());
+    std::copy(halos[r].begin(), halos[r].end(), t.halo.begin() + size_t(r) * t.hstride);
+  }
+  const size_t bytes[6] = {size_t(cs) * t.stride * 2, size_t(cs) * t.stride * 8,
+                           t.soff.size() * 4, t.halo.size() * 4, size_t(cs) * 4, size_t(n)};
+  for (int k = 0; k < 6; ++k) {
+    t.off[k] = t.total;
+    t.total += (bytes[k] + 255) / 256 * 256;
+  }
+  return t;
+}
+
+// packed layout: codes | g | slice_off | halo | n_halo | deg
+void write_topo(const HostMesh& h, int cs, const TopoHost& t, unsigned char* dst) {
+  const int n = int(h.n), chunk = t.chunk;
+  uint16_t* codes = reinterpret_cast<uint16_t*>(dst + t.off[0]);
+  float2* g = reinterpret_cast<float2*>(dst + t.off[1]);
+  std::memset(codes, 0, size_t(cs) * t.stride * 2);  // SELL padding: code 0, g 0
+  std::memset(g, 0, size_t(cs) * t.stride * 8);
+  unsigned char* deg = dst + t.off[5];
   for (int i = 0; i < n; ++i) {
-    const int r = i / chunk, s = i % chunk;
+    const int r = i / chunk, s = i - r * chunk;
     const int b = h.nb_ptr[i], e = h.nb_ptr[i + 1];
     deg[i] = (unsigned char)(e - b);
-    const size_t base = size_t(r) * stride + soff[size_t(r) * slices + s / 32] + (s % 32);
+    const size_t base = size_t(r) * t.stride + t.soff[size_t(r) * t.slices + s / 32] + (s % 32);
     for (int q = b; q < e; ++q) {
-      const int j = h.nb_idx[q];
-      const int code = (j / chunk == r) ? (j % chunk) : SLOTS + halo_index[r][j];
-      codes[base + 32 * size_t(q - b)] = uint16_t(code);
+      codes[base + 32 * size_t(q - b)] = t.code[q];
       g[base + 32 * size_t(q - b)] = make_float2(float(h.g_nb[2 * q]), float(h.g_nb[2 * q + 1]));
     }
   }
-  std::vector<uint32_t> hl(size_t(cs) * hstride, 0);
-  std::vector<int> nh(cs);
-  for (int r = 0; r < cs; ++r) {
-    nh[r] = int(halos[r].size());
-    std::copy(halos[r].begin(), halos[r].end(), hl.begin() + size_t(r) * hstride);
-  }
-  TopoHost t;
-  t.chunk = chunk;
-  t.stride = stride;
-  t.slices = slices;
-  t.hstride = hstride;
-  const size_t bytes[6] = {codes.size() * 2, g.size() * 8, soff.size() * 4, hl.size() * 4,
-                           nh.size() * 4, deg.size()};
-  const void* src[6] = {codes.data(), g.data(), soff.data(), hl.data(), nh.data(), deg.data()};
-  size_t tot = 0;
-  for (int k = 0; k < 6; ++k) {
-    t.off[k] = tot;
-    tot += (bytes[k] + 255) / 256 * 256;
-  }
-  t.packed.resize(tot);
-  for (int k = 0; k < 6; ++k) std::memcpy(t.packed.data() + t.off[k], src[k], bytes[k]);
-  return t;
+  std::memcpy(dst + t.off[2], t.soff.data(), t.soff.size() * 4);
+  std::memcpy(dst + t.off[3], t.halo.data(), t.halo.size() * 4);
+  std::memcpy(dst + t.off[4], t.n_halo.data(), t.n_halo.size() * 4);
 }
 
 // device arrays of a packed topology, carved out of one slab
@@ -585,10 +603,12 @@ const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, i
   auto it = h.dev->topo.find(chunk * 4 + npt);
   if (it != h.dev->topo.end()) return it->second;
   AllocScope scope(ctx->stream);
-  const TopoHost th = build_topo_host(h, cs, chunk, npt);
-  unsigned char* slab = dalloc<unsigned char>(th.packed.size());
-  ck(mrb_copy_async(slab, th.packed.data(), th.packed.size(), cudaMemcpyHostToDevice,
-                     ctx->stream));  // pageable: staged before return
+  const TopoHost th = plan_topo(h, cs, chunk, npt);
+  std::vector<unsigned char> packed(th.total);
+  write_topo(h, cs, th, packed.data());
+  unsigned char* slab = dalloc<unsigned char>(th.total);
+  ck(mrb_copy_async(slab, packed.data(), th.total, cudaMemcpyHostToDevice,
+                    ctx->stream));  // pageable: staged before return
   return install_topo(h, npt, th, slab);
 }
 
@@ -615,26 +635,23 @@ void ensure_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, in
   std::vector<TopoHost> th(todo.size());
   parallel_for(todo.size(), [&](size_t i) {
     const HostMesh& h = *todo[i];
-    th[i] = build_topo_host(h, cs, int((h.n + cs - 1) / cs), npt);
+    th[i] = plan_topo(h, cs, int((h.n + cs - 1) / cs), npt);
   });
-  tick("host build");
+  tick("host plan");
   size_t total = 0;
   std::vector<size_t> base(todo.size());
   for (size_t i = 0; i < todo.size(); ++i) {
     base[i] = total;
-    total += th[i].packed.size();
+    total += th[i].total;
   }
   unsigned char* stage = static_cast<unsigned char*>(pinned_stage(ctx, total));
   tick("stage wait");
-  parallel_for(todo.size(), [&](size_t i) {
-    std::memcpy(stage + base[i], th[i].packed.data(), th[i].packed.size());
-  });
+  parallel_for(todo.size(), [&](size_t i) { write_topo(*todo[i], cs, th[i], stage + base[i]); });
   tick("stage fill");
   AllocScope scope(ctx->stream);
-  for (size_t i = 0; i < todo.size(); ++i) {
-    unsigned char* slab = dalloc<unsigned char>(th[i].packed.size());
-    ck(mrb_copy_async(slab, stage + base[i], th[i].packed.size(), cudaMemcpyHostToDevice,
-                       ctx->stream));
+  for (size_t i = 0; i < todo.size(); ++i) {  // one slab per mesh (owned by its DeviceMesh)
+    unsigned char* slab = dalloc<unsigned char>(th[i].total);
+    ck(mrb_copy_async(slab, stage + base[i], th[i].total, cudaMemcpyHostToDevice, ctx->stream));
     install_topo(*todo[i], npt, th[i], slab);
   }
   ck(cudaEventRecord(ctx->stage_done, ctx->stream));
@@ -761,6 +778,14 @@ struct mrb_batch {
   std::vector<const void*> graph_src;
   // cluster fast path (0 = generic three-kernel loop)
   int cluster_cs = 0, cluster_npt = 1;
+  int forced_cs = 0, forced_npt = 0;  // shape imposed by mrb_register_many
+  // wave groups (mrb_register_many): the first run launches the fast path per
+  // group of pairs and records group_ev[g]; get_results then copies group g
+  // back on copy_stream while later groups still compute
+  std::vector<int> groups;  // pair boundaries, size G + 1 (empty: one launch)
+  std::vector<cudaEvent_t> group_ev;
+  cudaStream_t copy_stream = nullptr;
+  bool groups_recorded = false;
   size_t cluster_smem = 0;
   int pad_pitch = 0;
   size_t pad_plane = 0;
@@ -775,6 +800,11 @@ struct mrb_batch {
   bool synced = false;
   ~mrb_batch() {
     if (graph) cudaGraphExecDestroy(graph);
+    for (cudaEvent_t e : group_ev) cudaEventDestroy(e);
+    if (copy_stream) {
+      cudaStreamSynchronize(copy_stream);
+      cudaStreamDestroy(copy_stream);
+    }
     void* ptrs[] = {pairs, st, blk_pair, pix_blk_pair, partials, pix_partials, state, traces,
                     img, stage, src_ptrs, img_ptrs, dense, u_out, conv, cpairs, img_pad,
                     phase_prof};
@@ -905,10 +935,10 @@ struct KernelTimer {
 };
 
 template <int NPT>
-void launch_cluster_t(mrb_batch* b) {
+void launch_cluster_t(mrb_batch* b, int p0, int np) {
   const int CS = b->cluster_cs;
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(unsigned(b->n_pairs * CS));
+  lc.gridDim = dim3(unsigned(np * CS));
   lc.blockDim = dim3(kClusterThreads);
   lc.dynamicSmemBytes = b->cluster_smem;
   lc.stream = b->ctx->stream;
@@ -920,7 +950,7 @@ void launch_cluster_t(mrb_batch* b) {
   lc.attrs = attr;
   lc.numAttrs = 1;
   ck(cudaLaunchKernelEx(&lc, k_cluster_register<NPT>,
-                        static_cast<const ClusterPair*>(b->cpairs), b->st,
+                        static_cast<const ClusterPair*>(b->cpairs) + p0, b->st + p0,
                         int(b->cfg.max_iterations), double(b->cfg.energy_tolerance),
                         float(b->cfg.tau), float(b->cfg.lam), int(b->cfg.smoothing_passes)));
 }
@@ -991,11 +1021,11 @@ int cluster_occupancy_cs(int cs, int npt, size_t smem) {
   return memo[key] = occ;
 }
 
-int64_t launch_cluster(mrb_batch* b) {
+int64_t launch_cluster(mrb_batch* b, int p0, int np) {
   if (b->cluster_npt == 2)
-    launch_cluster_t<2>(b);
+    launch_cluster_t<2>(b, p0, np);
   else
-    launch_cluster_t<1>(b);
+    launch_cluster_t<1>(b, p0, np);
   return 1;
 }
 
@@ -1019,11 +1049,32 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
                               b->W, b->H, b->img_pad, b->pad_pitch, b->pad_plane,
                               4 * b->pad_plane);
       ++launches;
+      if (b->groups.size() > 2 && tm == &dummy && b->runs == 0) {
+        // per wave group: loop + dense pass + MSD, then an event for the
+        // group's device-to-host copies (mrb_batch_get_results)
+        const PD* host = reinterpret_cast<const PD*>(b->pairs_host.data());
+        for (size_t g = 0; g + 1 < b->groups.size(); ++g) {
+          const int p0 = b->groups[g], p1 = b->groups[g + 1];
+          const int blk0 = host[p0].pix_blk_begin;
+          const int blk1 = p1 < b->n_pairs ? host[p1].pix_blk_begin : b->n_pix_blocks;
+          launches += launch_cluster(b, p0, p1 - p0);
+          k_dense_fast<<<blk1 - blk0, kPixBlock, 0, s>>>(static_cast<const ClusterPair*>(b->cpairs),
+                                                         b->st, b->pix_blk_pair, b->pix_partials,
+                                                         blk0);
+          k_msd_final<TapT, Real><<<p1 - p0, kPixBlock, 0, s>>>(pairs + p0, b->st + p0,
+                                                                b->pix_partials);
+          launches += 2;
+          ck(cudaEventRecord(b->group_ev[g], s));
+        }
+        b->groups_recorded = true;
+        ck(cudaGetLastError());
+        return launches;
+      }
       tm->mark(-1);
-      launches += launch_cluster(b);
+      launches += launch_cluster(b, 0, b->n_pairs);
       tm->mark(0);
       k_dense_fast<<<b->n_pix_blocks, kPixBlock, 0, s>>>(
-          static_cast<const ClusterPair*>(b->cpairs), b->st, b->pix_blk_pair, b->pix_partials);
+          static_cast<const ClusterPair*>(b->cpairs), b->st, b->pix_blk_pair, b->pix_partials, 0);
       tm->mark(3);
       k_msd_final<TapT, Real><<<b->n_pairs, kPixBlock, 0, s>>>(pairs, b->st, b->pix_partials);
       launches += 2;
@@ -1098,64 +1149,48 @@ int64_t launches_per_run(const mrb_batch* b) {
 
 // Choose the cluster fast path when it applies: fp32, every pair fits one
 // cluster of <= 16 CTAs x 768 nodes, one-rings of <= kMaxDeg entries.
-void setup_cluster_path(mrb_batch* b) {
-  b->cluster_cs = 0;
-  const char* env = std::getenv("MESHREG_B200_PATH");
+// Cluster shape (CS CTAs per pair, NPT nodes per thread) for a batch of
+// n_pairs pairs whose largest mesh is `big`.  Cost model = waves x nodes per
+// CTA = ceil(P / max active clusters(CS)) * ceil(n / CS), evaluated with the
+// largest mesh's topology; the occupancy API sees the GPC structure (e.g.
+// clusters of 9 pack two per 18/19-SM GPC where clusters of 8 leave SMs
+// idle).  The decision is cached per (shape, device).  Returns false when no
+// candidate fits; *occ = active clusters of the choice (pairs per wave).
+bool choose_cluster_shape(mrb_ctx* ctx, HostMesh& big, int n_pairs, bool two_u, int* cs_out,
+                          int* npt_out, int* occ_out) {
   const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
-  auto why = [&](const char* m) {
-    if (dbg) std::fprintf(stderr, "meshreg_b200: generic path (%s)\n", m);
-  };
-  if (env && std::string(env) == "generic") return why("MESHREG_B200_PATH=generic");
-  if (b->real_d || b->tap_d) return why("fp64 precision");
-  if (b->in_dtype != MRB_F32) return why("fp64 image storage");
-  int64_t nmax = 0;
-  for (mrb_mesh* m : b->meshes) {
-    nmax = std::max<int64_t>(nmax, m->h.n);
-    if (m->h.dev->max_deg > kMaxDeg) return why("one-ring larger than kMaxDeg");
-  }
+  const int64_t nmax = big.n;
   // latency mode (few pairs): one node per thread, more CTAs per pair;
   // throughput mode: two nodes per thread, fewer CTAs per pair
   const char* npt_env = std::getenv("MESHREG_B200_NPT");
-  int npt = npt_env ? std::atoi(npt_env) : (b->n_pairs >= 4 ? 2 : 1);
-  // Cluster size: any CS in [ceil(n / (768*npt)), 16].  Cost model =
-  // waves x nodes per CTA = ceil(P / max active clusters(CS)) * ceil(n / CS);
-  // the occupancy API sees the GPC structure (e.g. clusters of 9 pack two per
-  // 18/19-SM GPC where clusters of 8 leave SMs idle).
-  const bool two_u = b->cfg.smoothing_passes >= 2;
-  mrb_mesh* big = *std::max_element(b->meshes.begin(), b->meshes.end(),
-                                    [](mrb_mesh* x, mrb_mesh* y) { return x->h.n < y->h.n; });
+  int npt = npt_env ? std::atoi(npt_env) : (n_pairs >= 4 ? 2 : 1);
   const char* cs_env = std::getenv("MESHREG_B200_CS");
-  // the shape decision is cached per (batch shape, device): later batches of
-  // the same shape evaluate only the chosen candidate
   static std::mutex cache_mu;
-  static std::map<std::tuple<int, int, int64_t, bool, int>, std::pair<int, int>> cache;
-  const auto cache_key = std::make_tuple(npt, b->n_pairs, int64_t(nmax), two_u, b->ctx->device);
-  int cached_cs = 0, cached_npt = 0;
+  static std::map<std::tuple<int, int, int64_t, bool, int>, std::tuple<int, int, int>> cache;
+  const auto key = std::make_tuple(npt, n_pairs, int64_t(nmax), two_u, ctx->device);
   {
     std::lock_guard<std::mutex> lock(cache_mu);
-    auto it = cache.find(cache_key);
-    if (it != cache.end()) std::tie(cached_cs, cached_npt) = it->second;
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      std::tie(*cs_out, *npt_out, *occ_out) = it->second;
+      return true;
+    }
   }
-  if (cached_cs) npt = cached_npt;
-  for (; npt >= 1 && !b->cluster_cs; --npt) {
+  for (; npt >= 1; --npt) {
     const int cap = kClusterThreads * npt;
     const int cs_min = int((nmax + cap - 1) / cap);
     if (cs_min > 16) continue;
     double best = 1e300;
-    if (cached_cs) {  // decided before for this batch shape
-      b->cluster_cs = cached_cs;
-      b->cluster_npt = cached_npt;
-    }
-    for (int cs = cs_min; cs <= 16 && !cached_cs; ++cs) {
+    int best_cs = 0, best_occ = 0;
+    for (int cs = cs_min; cs <= 16; ++cs) {
       if (cs_env && std::atoi(cs_env) != cs) continue;
-      const int chunk = int((big->h.n + cs - 1) / cs);
-      const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, big->h, cs, chunk, npt);
-      // estimate with the largest mesh; re-checked below with every mesh
+      const int chunk = int((big.n + cs - 1) / cs);
+      const DeviceMesh::Topo& t = ensure_cluster_topo(ctx, big, cs, chunk, npt);
       const size_t smem =
           cluster_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride, two_u) + 4096;
       const int occ = cluster_occupancy_cs(cs, npt, smem);
       if (occ < 1) continue;
-      const double cost = double((b->n_pairs + occ - 1) / occ) * double((nmax + cs - 1) / cs);
+      const double cost = double((n_pairs + occ - 1) / occ) * double((nmax + cs - 1) / cs);
       if (dbg)
         std::fprintf(stderr,
                      "meshreg_b200: candidate cluster %d x %d nodes/thread: %zu B smem, "
@@ -1163,35 +1198,75 @@ void setup_cluster_path(mrb_batch* b) {
                      cs, npt, smem, occ, cost);
       if (cost < best) {
         best = cost;
-        b->cluster_cs = cs;
-        b->cluster_npt = npt;
+        best_cs = cs;
+        best_occ = occ;
       }
     }
-    if (!b->cluster_cs) continue;
-    {  // per-mesh topologies: host thread pool + pinned staged upload
-      std::vector<HostMesh*> hm;
-      for (mrb_mesh* m : b->meshes) hm.push_back(&m->h);
-      ensure_cluster_topos(b->ctx, hm, b->cluster_cs, npt);
+    if (best_cs) {
+      *cs_out = best_cs;
+      *npt_out = npt;
+      *occ_out = best_occ;
+      std::lock_guard<std::mutex> lock(cache_mu);
+      cache[key] = std::make_tuple(best_cs, npt, best_occ);
+      return true;
     }
-    size_t smem = 0;
-    for (mrb_mesh* m : b->meshes) {
-      const int chunk = int((m->h.n + b->cluster_cs - 1) / b->cluster_cs);
-      const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, m->h, b->cluster_cs, chunk, npt);
-      smem = std::max(smem, cluster_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride, two_u));
-    }
-    if (cluster_occupancy_cs(b->cluster_cs, npt, smem) < 1) {
-      b->cluster_cs = 0;
-      continue;
-    }
-    b->cluster_smem = smem;
-    if (dbg)
-      std::fprintf(stderr, "meshreg_b200: cluster %d CTAs x %d nodes/thread, %zu B smem\n",
-                   b->cluster_cs, b->cluster_npt, smem);
-    std::lock_guard<std::mutex> lock(cache_mu);
-    cache[cache_key] = std::make_pair(b->cluster_cs, b->cluster_npt);
   }
-  if (!b->cluster_cs) return why("no cluster configuration fits");
-  const int cs = b->cluster_cs;
+  return false;
+}
+
+// fast-path eligibility of a batch: fp32 state and images, one-rings within
+// kMaxDeg, at most 16 CTAs x 768 x 2 nodes per pair
+const char* cluster_ineligible(bool real_d, bool tap_d, int in_dtype,
+                               const std::vector<mrb_mesh*>& meshes) {
+  const char* env = std::getenv("MESHREG_B200_PATH");
+  if (env && std::string(env) == "generic") return "MESHREG_B200_PATH=generic";
+  if (real_d || tap_d) return "fp64 precision";
+  if (in_dtype != MRB_F32) return "fp64 image storage";
+  for (mrb_mesh* m : meshes) {
+    if (m->h.n > 16 * 2 * kClusterThreads) return "mesh larger than 16 CTAs x 1536 nodes";
+    int md = 0;
+    for (int64_t k = 0; k < m->h.n; ++k) md = std::max(md, m->h.nb_ptr[k + 1] - m->h.nb_ptr[k]);
+    if (md > kMaxDeg) return "one-ring larger than kMaxDeg";
+  }
+  return nullptr;
+}
+
+void setup_cluster_path(mrb_batch* b) {
+  b->cluster_cs = 0;
+  const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
+  auto why = [&](const char* m) {
+    if (dbg) std::fprintf(stderr, "meshreg_b200: generic path (%s)\n", m);
+  };
+  if (const char* m = cluster_ineligible(b->real_d, b->tap_d, b->in_dtype, b->meshes))
+    return why(m);
+  const bool two_u = b->cfg.smoothing_passes >= 2;
+  mrb_mesh* big = *std::max_element(b->meshes.begin(), b->meshes.end(),
+                                    [](mrb_mesh* x, mrb_mesh* y) { return x->h.n < y->h.n; });
+  int cs = 0, npt = 0, occ = 0;
+  if (b->forced_cs) {  // shape decided for the whole queue (mrb_register_many)
+    cs = b->forced_cs;
+    npt = b->forced_npt;
+  } else if (!choose_cluster_shape(b->ctx, big->h, b->n_pairs, two_u, &cs, &npt, &occ)) {
+    return why("no cluster configuration fits");
+  }
+  {  // per-mesh topologies: host thread pool + pinned staged upload
+    std::vector<HostMesh*> hm;
+    for (mrb_mesh* m : b->meshes) hm.push_back(&m->h);
+    ensure_cluster_topos(b->ctx, hm, cs, npt);
+  }
+  size_t smem = 0;
+  for (mrb_mesh* m : b->meshes) {
+    const int chunk = int((m->h.n + cs - 1) / cs);
+    const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, m->h, cs, chunk, npt);
+    smem = std::max(smem, cluster_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride, two_u));
+  }
+  if (cluster_occupancy_cs(cs, npt, smem) < 1) return why("no cluster configuration fits");
+  b->cluster_cs = cs;
+  b->cluster_npt = npt;
+  b->cluster_smem = smem;
+  if (dbg)
+    std::fprintf(stderr, "meshreg_b200: cluster %d CTAs x %d nodes/thread, %zu B smem\n", cs, npt,
+                 smem);
   b->pad_pitch = (b->W + 5 + 3) / 4 * 4;
   b->pad_plane = size_t(b->H + 2) * b->pad_pitch;
   // columns of a copy that k_pad_planar4 does not write are never read
@@ -1340,6 +1415,11 @@ int mrb_ctx_destroy(mrb_ctx* ctx) {
     cudaStreamDestroy(ctx->stream);
   }
   if (ctx->stage_done) cudaEventDestroy(ctx->stage_done);
+  if (ctx->copy) {
+    cudaStreamSynchronize(ctx->copy);
+    cudaStreamDestroy(ctx->copy);
+  }
+  if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
   return MRB_OK;
@@ -1470,8 +1550,13 @@ int mrb_pixel_map(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int64_t* t
 }
 
 // ---------------------------------------------------------------- batch
-int mrb_batch_create(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int32_t W,
-                     int32_t H, int32_t img_dtype, const mrb_config* cfg, mrb_batch** out) {
+}  // extern "C"
+
+namespace {
+// mrb_batch_create with an optional imposed cluster shape (forced_cs > 0)
+int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int32_t W,
+                      int32_t H, int32_t img_dtype, const mrb_config* cfg, int forced_cs,
+                      int forced_npt, mrb_batch** out) {
   *out = nullptr;
   const std::string ce = config_error(cfg);
   if (!ce.empty()) return fail(ctx, MRB_E_VALUE, ce);
@@ -1512,20 +1597,26 @@ int mrb_batch_create(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int
     }
     // the fast path never reads the generic one-ring arrays: upload them only
     // when the batch is not eligible for it
-    const char* penv = std::getenv("MESHREG_B200_PATH");
-    bool eligible = !b->real_d && !b->tap_d && img_dtype == MRB_F32 &&
-                    !(penv && std::string(penv) == "generic");
-    for (HostMesh* h : hm) {
-      int md = 0;
-      for (int64_t k = 0; k < h->n; ++k) md = std::max(md, h->nb_ptr[k + 1] - h->nb_ptr[k]);
-      eligible = eligible && md <= kMaxDeg && h->n <= 16 * 2 * kClusterThreads;
-    }
+    const bool eligible = !cluster_ineligible(b->real_d, b->tap_d, img_dtype, b->meshes);
+    b->forced_cs = forced_cs;
+    b->forced_npt = forced_npt;
     ensure_device_meshes(ctx, hm, !eligible);
     if (!eligible)  // meshes uploaded earlier by a fast-path batch lack them
       for (HostMesh* h : hm) ensure_device_mesh_ring(ctx, *h);
     if (b->real_d)
       for (HostMesh* h : hm) ensure_device_mesh_f64(ctx, *h);
     tick("mesh upload");
+    if (eligible) {
+      // fast-path topologies first: their host planning overlaps the mesh and
+      // image uploads still in flight (ensure_pixel_maps synchronises)
+      mrb_mesh* big = *std::max_element(b->meshes.begin(), b->meshes.end(),
+                                        [](mrb_mesh* x, mrb_mesh* y) { return x->h.n < y->h.n; });
+      int cs = forced_cs, npt = forced_npt, occ = 0;
+      if (cs || choose_cluster_shape(ctx, big->h, n_pairs, cfg->smoothing_passes >= 2, &cs, &npt,
+                                     &occ))
+        ensure_cluster_topos(ctx, hm, cs, npt);
+      tick("topologies");
+    }
     const std::string msg = ensure_pixel_maps(ctx, hm, W, H);
     if (!msg.empty()) return fail(ctx, MRB_E_COVERAGE, msg);
     tick("pixel maps");
@@ -1564,6 +1655,24 @@ int mrb_batch_create(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int
   }
   *out = b.release();
   return MRB_OK;
+}
+// Split a fast-path batch into wave groups of `per` pairs (see mrb_batch).
+void batch_set_groups(mrb_batch* b, int per) {
+  if (!b->cluster_cs || per <= 0 || per >= b->n_pairs) return;
+  b->groups.clear();
+  for (int p = 0; p < b->n_pairs; p += per) b->groups.push_back(p);
+  b->groups.push_back(b->n_pairs);
+  b->group_ev.resize(b->groups.size());
+  for (auto& e : b->group_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  ck(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking));
+}
+}  // namespace
+
+extern "C" {
+
+int mrb_batch_create(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int32_t W,
+                     int32_t H, int32_t img_dtype, const mrb_config* cfg, mrb_batch** out) {
+  return batch_create_impl(ctx, n_pairs, meshes, W, H, img_dtype, cfg, 0, 0, out);
 }
 
 int mrb_batch_destroy(mrb_batch* b) {
@@ -1642,6 +1751,33 @@ int mrb_batch_get_results(mrb_batch* b, int32_t out_dtype, double* u, void* ux, 
   try {
     ck(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
+    const bool same_dtype = (out_dtype == MRB_F64) == b->real_d;
+    if (b->groups_recorded && same_dtype) {
+      // wave groups: group g's results leave while later groups compute
+      b->groups_recorded = false;
+      const size_t npx = size_t(b->W) * b->H, os = in_size(out_dtype);
+      void* outs[3] = {ux, uy, warped};
+      for (size_t g = 0; g + 1 < b->groups.size(); ++g) {
+        const int p0 = b->groups[g], p1 = b->groups[g + 1];
+        ck(cudaStreamWaitEvent(b->copy_stream, b->group_ev[g], 0));
+        if (u) {
+          const size_t n0 = size_t(b->node_off[p0]);
+          const size_t n1 = p1 < b->n_pairs ? size_t(b->node_off[p1]) : size_t(b->total_nodes);
+          ck(mrb_copy_async(u + 2 * n0, b->u_out + n0, (n1 - n0) * sizeof(double2),
+                            cudaMemcpyDeviceToHost, b->copy_stream));
+        }
+        for (int c = 0; c < 3; ++c) {
+          if (!outs[c]) continue;
+          for (int p = p0; p < p1; ++p)
+            ck(mrb_copy_async(static_cast<char*>(outs[c]) + size_t(p) * npx * os,
+                              static_cast<const char*>(b->dense) + (3 * size_t(p) + c) * npx * os,
+                              npx * os, cudaMemcpyDeviceToHost, b->copy_stream));
+        }
+      }
+      ck(cudaEventRecord(b->group_ev.back(), b->copy_stream));
+      ck(cudaStreamWaitEvent(s, b->group_ev.back(), 0));  // sync on ctx->stream covers it
+      return MRB_OK;
+    }
     if (u)
       ck(mrb_copy_async(u, b->u_out, size_t(b->total_nodes) * sizeof(double2),
                          cudaMemcpyDeviceToHost, s));
@@ -1828,8 +1964,36 @@ int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
       const int rc = mrb_ctx_create(ctx->device, &c);
       if (rc != MRB_OK) return fail(ctx, rc, "cannot create a pipeline stream");
     }
-  // default: one chunk (measured fastest while the per-mesh host setup costs
-  // more than a chunk's device time); smaller chunks overlap setup and compute
+  // The fast-path cluster shape is decided once for the whole queue (cost
+  // model with P = n_pairs) and imposed on every chunk.  Default chunk = one
+  // wave of that shape (the pairs one launch keeps resident), so the chunks'
+  // runs add up to the single-launch time while chunk k's host setup and
+  // transfers overlap chunk k-1's run.
+  int forced_cs = 0, forced_npt = 0, wave = 0;
+  {
+    std::vector<mrb_mesh*> all(meshes, meshes + n_pairs);
+    const bool real_d = cfg->precision == MRB_PREC_F64;
+    if (config_error(cfg).empty() && !cluster_ineligible(real_d, img_dtype == MRB_F64 && real_d,
+                                                         img_dtype, all)) {
+      mrb_mesh* big = *std::max_element(all.begin(), all.end(), [](mrb_mesh* x, mrb_mesh* y) {
+        return x->h.n < y->h.n;
+      });
+      int occ = 0;
+      try {
+        AllocScope scope(ctx->stream);
+        ck(cudaSetDevice(ctx->device));
+        ensure_device_meshes(ctx, {&big->h}, false);
+        if (!choose_cluster_shape(ctx, big->h, n_pairs, cfg->smoothing_passes >= 2, &forced_cs,
+                                  &forced_npt, &occ))
+          forced_cs = forced_npt = occ = 0;
+      } catch (const CudaError& e) {
+        return cuda_fail(ctx, e.e);
+      }
+      wave = occ;
+    }
+  }
+  // default: one chunk (the per-chunk host setup costs more than a wave's
+  // device time); within it, wave groups overlap results D2H with compute
   if (chunk_pairs <= 0) chunk_pairs = n_pairs;
   const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
   const auto T0 = std::chrono::steady_clock::now();
@@ -1845,11 +2009,18 @@ int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
   std::vector<std::pair<int, int>> span;
   int first_err = MRB_OK;
   std::string first_msg;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> dbg_events;  // run of each chunk
   auto harvest = [&](size_t k) {  // wait for chunk k and collect its statuses
     mrb_batch* b = live[k];
     if (!b) return;
     stamp("harvest begin", int(k));
     const int rc = mrb_batch_sync(b);
+    if (dbg && k < dbg_events.size()) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, dbg_events[k].first, dbg_events[k].second);
+      std::fprintf(stderr, "meshreg_b200: many chunk %zu run %.2f ms (path %d x %d)\n", k, ms,
+                   b->cluster_cs, b->cluster_npt);
+    }
     if (rc == MRB_E_CUDA && first_err == MRB_OK) {
       first_err = rc;
       first_msg = b->ctx->err;
@@ -1908,18 +2079,55 @@ int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
         if (k >= 2) harvest(size_t(k - 2));  // the pipeline stream's previous chunk
         ck(cudaStreamWaitEvent(sc->stream, setup_done, 0));
       }
+      // images: their H2D starts on the context's copy stream before the
+      // (host-bound) batch setup, so the copy overlaps it; the pipeline
+      // stream waits for it just before the run
+      const size_t img_bytes = size_t(P) * npx * es;
+      char* dimg = nullptr;
+      {
+        if (!ctx->copy) {
+          ck(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+          ck(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
+        }
+        AllocScope scope(ctx->copy);
+        dimg = dalloc<char>(2 * img_bytes);
+        ck(mrb_copy_async(dimg, static_cast<const char*>(reference) + size_t(p0) * npx * es,
+                          img_bytes, cudaMemcpyHostToDevice, ctx->copy));
+        ck(mrb_copy_async(dimg + img_bytes, static_cast<const char*>(tmpl) + size_t(p0) * npx * es,
+                          img_bytes, cudaMemcpyHostToDevice, ctx->copy));
+        ck(cudaEventRecord(ctx->copy_done, ctx->copy));
+      }
       mrb_batch* b = nullptr;
       stamp("create begin", k);
-      int rc = mrb_batch_create(sc, P, meshes + p0, W, H, img_dtype, cfg, &b);
+      int rc = batch_create_impl(sc, P, meshes + p0, W, H, img_dtype, cfg, forced_cs, forced_npt,
+                                 &b);
       stamp("create end", k);
       if (rc == MRB_OK && k == 0) {
         cs = b->cluster_cs;
         npt = b->cluster_npt;
       }
-      if (rc == MRB_OK)
-        rc = mrb_batch_set_images(b, static_cast<const char*>(reference) + size_t(p0) * npx * es,
-                                  static_cast<const char*>(tmpl) + size_t(p0) * npx * es, 0);
+      if (rc == MRB_OK) {
+        cudaStreamWaitEvent(sc->stream, ctx->copy_done, 0);
+        rc = mrb_batch_set_images(b, dimg, dimg + img_bytes, 1);
+      }
+      if (rc == MRB_OK && wave > 0 && !std::getenv("MESHREG_B200_NO_GROUPS")) {
+        try {
+          batch_set_groups(b, wave);
+        } catch (const CudaError& e) {
+          rc = cuda_fail(sc, e.e);
+        }
+      }
+      cudaEvent_t ev_run[2] = {nullptr, nullptr};
+      if (dbg && rc == MRB_OK) {
+        for (auto& e : ev_run) cudaEventCreate(&e);
+        cudaEventRecord(ev_run[0], sc->stream);
+      }
       if (rc == MRB_OK) rc = mrb_batch_run(b);
+      if (dbg && ev_run[1]) {
+        cudaEventRecord(ev_run[1], sc->stream);
+        dbg_events.push_back({ev_run[0], ev_run[1]});
+      }
+      cudaFreeAsync(dimg, sc->stream);  // stream-ordered: after the run consumed it
       if (rc == MRB_OK) {
         auto off = [&](void* base) -> void* {
           return base ? static_cast<char*>(base) + size_t(p0) * npx * os : nullptr;
