@@ -296,7 +296,8 @@ def run_ours(args, rank, world, local):
     n_launch = {0: iters, 1: iters, 2: iters, 3: 1}
     share = {k: ktimes[k] * n_launch[k] for k in range(4)}
     dom = max(share, key=share.get)
-    names = {0: "k_cluster_register" if path_cs else "k_sample", 1: "k_grad", 2: "k_smooth",
+    fast_name = "k_grid_register" if path_cs < 0 else "k_cluster_register"
+    names = {0: fast_name if path_cs else "k_sample", 1: "k_grad", 2: "k_smooth",
              3: "k_dense"}
     if path_cs:
         n_launch = {0: 1, 1: 0, 2: 0, 3: 1}
@@ -336,7 +337,9 @@ def run_ours(args, rank, world, local):
                 "precision": args.precision,
             },
             "gpu_launches": launches,
-            "path": (f"persistent cluster kernel (cluster of {path_cs} CTAs per pair)" if path_cs
+            "path": (f"persistent cluster kernel (cluster of {path_cs} CTAs per pair)" if path_cs > 0
+                     else f"whole-GPU persistent grid kernel ({-path_cs} CTAs, one cooperative "
+                          "launch per pair)" if path_cs < 0
                      else "generic 3-kernel loop (CUDA graph)"),
             "kernel_ms": {names[k]: round(float(ktimes[k]), 5) for k in range(4)},
             "algorithmic_bytes_per_step": alg_bytes,

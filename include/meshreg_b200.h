@@ -153,8 +153,10 @@ int mrb_batch_sync(mrb_batch* batch);
 int mrb_batch_pair_status(mrb_batch* batch, int32_t pair, int32_t* iterations_run,
                           double* msd_before, double* msd_after, double* trace, char* msg,
                           int32_t msg_len);
-/* execution path chosen for the batch: 0 = generic three-kernel loop, else the
- * cluster size of the persistent cluster kernel (fp32, <= 16 x 768 nodes) */
+/* execution path chosen for the batch: 0 = generic three-kernel loop; > 0 =
+ * the cluster size of the persistent cluster kernel (fp32, <= 16 x 1536
+ * nodes); < 0 = minus the CTA count of the whole-GPU persistent grid kernel
+ * (fp32, larger meshes, one cooperative launch per pair) */
 int32_t mrb_batch_path(const mrb_batch* batch);
 /* debug: per-CTA phase timestamps of the cluster kernel (first 8 iterations,
  * 16 slots each) when MESHREG_B200_PROFILE_PHASES is set at batch creation */

@@ -66,6 +66,12 @@ struct ClusterPair {
   int n, chunk, W, H;
   int topo_stride, slices, halo_stride, pitch;
   int plane;
+  // grid path only (k_grid_register): global exchange buffers
+  float* xg_s;                // [CS][SLOTS] s_te of every slot
+  float2* xg_u;               // [2][CS][SLOTS] smoothing ping-pong
+  double* wpart;              // [2][CS][kWarps] energy partials by parity
+  int* gbad;                  // [CS] sticky non-finite gradient flags
+  unsigned* bar;              // grid barrier counter (zeroed before each launch)
 };
 
 // Four copies of the padded (H+2)x(W+2) (Te, Re) image; copy s holds padded

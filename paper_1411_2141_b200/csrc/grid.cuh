@@ -1,0 +1,300 @@
+// Whole-GPU persistent registration kernel for meshes larger than one
+// thread-block cluster holds (BASELINE configs 3 and 5; fp32 fast path).
+//
+// Same iteration as k_cluster_register (cluster.cuh) with the cluster swapped
+// for the whole grid: CTA r of CS co-resident CTAs (cooperative launch, one
+// per SM) owns the Morton chunk [r*chunk, (r+1)*chunk) of one pair.  Owners
+// publish s_te / u0 to global exchange arrays; after a grid barrier each CTA
+// pulls its halo (L2, bypassing L1) into shared memory, so the one-ring
+// gathers of the fused gradient operator and of the umbrella Laplacian stay
+// shared-memory loads.  The SELL-32 topology and the per-node constants are
+// read through the read-only path (L1/L2 resident across iterations), so the
+// kernel has no per-CTA topology size limit.  Every CTA reduces all energy
+// partials in one fixed order and runs the control logic itself (identical
+// decisions, no broadcast); the decision of iteration k is read after the
+// first barrier of iteration k+1, as in the cluster kernel.
+#pragma once
+
+#include "cluster.cuh"
+
+namespace mrb {
+
+// Sense-free grid barrier on a monotonic counter: the n-th barrier of a launch
+// waits until the counter reaches n * gridDim.x.  Release/acquire at gpu scope
+// order the exchange-array writes before the halo reads of other CTAs.
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+// one-ring gather over the global SELL-32 topology of this CTA
+template <typename F>
+__device__ __forceinline__ void ring_gather_g(const uint16_t* __restrict__ code,
+                                              const float2* __restrict__ g, uint32_t so, int deg,
+                                              F&& f) {
+#pragma unroll
+  for (int e0 = 0; e0 < kMaxDeg; e0 += 8) {
+    if (e0 < deg) {
+      uint32_t c[8];
+      float2 ge[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const bool in = e0 + e < deg;
+        c[e] = in ? __ldg(code + so + 32u * (e0 + e)) : 0u;
+        ge[e] = in ? __ldg(g + so + 32u * (e0 + e)) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (e0 + e < deg) f(c[e], ge[e]);
+    }
+  }
+}
+
+template <int NPT>
+__global__ void __launch_bounds__(kClusterThreads, 1)
+    k_grid_register(const ClusterPair* __restrict__ pairs, PairStatus* __restrict__ st,
+                    int max_iter, double tol, float tau, float lam, int passes) {
+  constexpr int SLOTS = kClusterThreads * NPT;
+  const int rank = blockIdx.x, CS = gridDim.x;
+  const ClusterPair& d = pairs[0];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  __shared__ int s_stop, s_nhalo;
+  __shared__ double s_hist[6];
+  __shared__ double s_prev;
+  __shared__ int s_cs[4];  // rises, iters, err, err_iter
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  const int X = SLOTS + d.halo_stride;
+  float* xs = reinterpret_cast<float*>(s_dyn);             // [X] s_te, own + halo
+  float2* xu0 = reinterpret_cast<float2*>(xs + X + (X & 1));
+  float2* xu1 = xu0 + X;                                   // [X] when passes >= 2
+  uint32_t* halo = reinterpret_cast<uint32_t*>(xu1 + (passes >= 2 ? X : 0));
+
+  if (t == 0) {
+    s_stop = 0;
+    s_prev = 0.0;
+    s_cs[0] = s_cs[1] = s_cs[2] = s_cs[3] = 0;
+    s_nhalo = d.n_halo[rank];
+  }
+  for (int q = t; q < d.halo_stride; q += kClusterThreads)
+    halo[q] = d.halo[size_t(rank) * d.halo_stride + q];
+  const uint16_t* code = d.codes + size_t(rank) * d.topo_stride;
+  const float2* gco = d.g + size_t(rank) * d.topo_stride;
+  const uint32_t* soff = d.slice_off + size_t(rank) * d.slices;
+  float* xg_s = d.xg_s;
+  float2* xg_u0 = d.xg_u;
+  float2* xg_u1 = d.xg_u + size_t(CS) * SLOTS;
+
+  float2 u[NPT];
+  float r[NPT];
+  unsigned own_mask = 0;
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) {
+    const int slot = t + j * kClusterThreads;
+    own_mask |= unsigned(slot < d.chunk && rank * d.chunk + slot < d.n) << j;
+    u[j] = make_float2(0.f, 0.f);
+    r[j] = 0.f;
+  }
+#define OWN(j) ((own_mask >> (j)) & 1u)
+  unsigned nbar = 0;
+  auto gsync = [&]() { grid_barrier(d.bar, ++nbar * unsigned(CS)); };
+  __syncthreads();
+  const int nhalo = s_nhalo;
+
+  // control step of iteration kk: all CS * kWarps partials in one fixed order
+  auto control = [&](int kk) {
+    double v = 0.0;
+    const double* wp = d.wpart + size_t(kk & 1) * CS * kWarps;
+    for (int idx = lane; idx < CS * kWarps; idx += 32) v += __ldcg(wp + idx);
+    int gb = 0;
+    for (int idx = lane; idx < CS; idx += 32) gb |= __ldcg(d.gbad + idx);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v += __shfl_down_sync(0xffffffffu, v, o);
+      gb |= __shfl_down_sync(0xffffffffu, gb, o);
+    }
+    if (lane == 0 && s_stop == 0) {
+      int stop = 0, rises = s_cs[0], err = ERR_NONE, err_iter = 0;
+      const double e = 0.5 * v;
+      const double prev = s_prev;
+      if (!isfinite(e)) {  // solver.py:176-177
+        err = ERR_NONFINITE_ENERGY;
+        err_iter = kk;
+        stop = 1;
+      } else if (kk > 0 && e > __dadd_rn(__dmul_rn(prev, 1.0 + 1e-4), 1e-12)) {
+        if (++rises >= 10) {  // material_rise, solver.py:43-44,178-184
+          err = ERR_RISES;
+          err_iter = kk;
+          stop = 1;
+        }
+      } else if (kk > 0 && e <= prev) {
+        rises = 0;  // solver.py:185-186
+      }
+      if (!stop && gb) {  // step(): non-finite gradient, solver.py:131-132
+        err = ERR_NONFINITE_GRAD;
+        err_iter = kk;
+        stop = 1;
+      }
+      if (!stop) {
+        s_cs[1] = kk + 1;
+        s_hist[kk % 6] = e;
+        if (kk + 1 >= 6) {  // solver.py:192-195
+          const double base = s_hist[(kk + 1) % 6];
+          if (fabs(__dsub_rn(e, base)) <= __dmul_rn(tol, fmax(fabs(base), 1e-12))) stop = 2;
+        }
+      }
+      if (rank == 0) d.trace[kk] = e;
+      s_prev = e;
+      s_cs[0] = rises;
+      s_cs[2] = err;
+      s_cs[3] = err_iter;
+      s_stop = stop;
+    }
+  };
+
+  int k = 0;
+  for (; k < max_iter; ++k) {
+    // -------- phase A: sample Te, Re at V + u; residual; energy partial
+    {
+      double e2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) {
+        if (OWN(j)) {
+          const int slot = t + j * kClusterThreads;
+          const int nd = rank * d.chunk + slot;
+          const double2 V = __ldg(d.V + nd);
+          const Window w = locate(d, V.x + double(u[j].x), V.y + double(u[j].y));
+          float2 tap[4][4];
+#pragma unroll
+          for (int row = 0; row < 4; ++row) ld_row4(w.base + size_t(row) * d.pitch, tap[row]);
+          const float2 s = combine(w, tap);
+          r[j] = s.x - s.y;
+          xs[slot] = s.x;
+          __stcg(xg_s + size_t(rank) * SLOTS + slot, s.x);
+          e2 = fma(double(r[j]), double(r[j]), e2);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) e2 += __shfl_down_sync(0xffffffffu, e2, o);
+      if (lane == 0) __stcg(d.wpart + (size_t(k & 1) * CS + rank) * kWarps + warp, e2);
+    }
+    gsync();            // s_te, energy partials (and the k-1 decision) visible
+    if (s_stop) break;  // iteration k-1 was the last one (u untouched since)
+    for (int h = t; h < nhalo; h += kClusterThreads) {  // pull the s_te halo
+      const uint32_t c = halo[h];
+      xs[SLOTS + h] = __ldcg(xg_s + size_t(c >> 16) * SLOTS + (c & 0xffffu));
+    }
+    __syncthreads();
+
+    // -------- phase B: gradient via the fused one-ring operator, descent
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+      if (OWN(j)) {
+        const int slot = t + j * kClusterThreads;
+        const int nd = rank * d.chunk + slot;
+        const uint32_t so = __ldg(soff + (slot >> 5)) + (slot & 31);
+        const float si = xs[slot];
+        const float2 gs = __ldg(d.g_self + nd);
+        float gx = gs.x * si, gy = gs.y * si;
+        ring_gather_g(code, gco, so, __ldg(d.deg + nd), [&](uint32_t c, float2 ge) {
+          const float sj = xs[c];
+          gx = fmaf(ge.x, sj, gx);
+          gy = fmaf(ge.y, sj, gy);
+        });
+        const float dx = r[j] * gx, dy = r[j] * gy;  // solver.py:189
+        bad |= !isfinite(dx) || !isfinite(dy);
+        const float2 v = make_float2(u[j].x - tau * dx, u[j].y - tau * dy);  // solver.py:133
+        xu0[slot] = v;
+        __stcg(xg_u0 + size_t(rank) * SLOTS + slot, v);
+      }
+    }
+    if (__syncthreads_or(bad) && t == 0) __stcg(d.gbad + rank, 1);
+
+    // -------- phase C: umbrella smoothing passes + domain clamp
+    if (passes == 0) {
+      gsync();  // gradbad flags visible
+#pragma unroll
+      for (int j = 0; j < NPT; ++j)
+        if (OWN(j)) {
+          const int slot = t + j * kClusterThreads;
+          u[j] = clamp_dom(xu0[slot], __ldg(d.V + rank * d.chunk + slot), d.W, d.H);
+        }
+    }
+    for (int q = 0; q < passes; ++q) {
+      float2* src = (q & 1) ? xu1 : xu0;
+      const float2* gsrc = (q & 1) ? xg_u1 : xg_u0;
+      gsync();  // src (and the gradbad flags) visible grid-wide
+      for (int h = t; h < nhalo; h += kClusterThreads) {  // pull the halo of src
+        const uint32_t c = halo[h];
+        src[SLOTS + h] = __ldcg(gsrc + size_t(c >> 16) * SLOTS + (c & 0xffffu));
+      }
+      __syncthreads();
+      float2 v[NPT];
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) {
+        v[j] = make_float2(0.f, 0.f);
+        if (OWN(j)) {
+          const int slot = t + j * kClusterThreads;
+          const int nd = rank * d.chunk + slot;
+          const uint32_t so = __ldg(soff + (slot >> 5)) + (slot & 31);
+          const float iv = __ldg(d.inv_val + nd);
+          float ax = 0.f, ay = 0.f;
+          ring_gather_g(code, gco, so, __ldg(d.deg + nd), [&](uint32_t c, float2) {
+            const float2 uj = src[c];  // (L u)_i, L_ij = 1/val_i
+            ax = fmaf(iv, uj.x, ax);
+            ay = fmaf(iv, uj.y, ay);
+          });
+          const float2 si = src[slot];
+          const float om = 1.f - lam;  // (1 - lam) u + lam (L u), mesh.py:281
+          v[j] = make_float2(om * si.x + lam * ax, om * si.y + lam * ay);
+        }
+      }
+      if (q == passes - 1) {
+#pragma unroll
+        for (int j = 0; j < NPT; ++j)
+          if (OWN(j))
+            u[j] = clamp_dom(v[j], __ldg(d.V + rank * d.chunk + t + j * kClusterThreads), d.W,
+                             d.H);
+      } else {
+        float2* dst = (q & 1) ? xu0 : xu1;
+        float2* gdst = (q & 1) ? xg_u0 : xg_u1;
+#pragma unroll
+        for (int j = 0; j < NPT; ++j)
+          if (OWN(j)) {
+            const int slot = t + j * kClusterThreads;
+            dst[slot] = v[j];
+            __stcg(gdst + size_t(rank) * SLOTS + slot, v[j]);
+          }
+      }
+    }
+    if (warp == kCtlWarp) control(k);
+  }
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) {
+    if (OWN(j)) {
+      const int nd = rank * d.chunk + t + j * kClusterThreads;
+      d.u[nd] = u[j];
+      d.u_out[d.perm[nd]] = make_double2(double(u[j].x), double(u[j].y));
+    }
+  }
+#undef OWN
+  __syncthreads();
+  if (rank == 0 && t == 0) {
+    PairStatus s{};
+    s.stop_iter = k;
+    s.err = s_cs[2];
+    s.err_iter = s_cs[3];
+    s.rises = s_cs[0];
+    s.iters = s_cs[1];
+    st[0] = s;
+  }
+}
+
+}  // namespace mrb

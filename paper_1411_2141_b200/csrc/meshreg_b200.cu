@@ -22,6 +22,7 @@
 
 #include "../../include/meshreg_b200.h"
 #include "cluster.cuh"
+#include "grid.cuh"
 #include "pixel.cuh"
 #include "kernels.cuh"
 #include "mesh_host.h"
@@ -595,12 +596,12 @@ const DeviceMesh::Topo& install_topo(HostMesh& h, int npt, const TopoHost& th,
   t.halo = reinterpret_cast<uint32_t*>(slab + th.off[3]);
   t.n_halo = reinterpret_cast<int*>(slab + th.off[4]);
   t.deg = slab + th.off[5];
-  return h.dev->topo[th.chunk * 4 + npt] = t;
+  return h.dev->topo[th.chunk * 16 + npt] = t;
 }
 
 const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, int chunk,
                                             int npt) {
-  auto it = h.dev->topo.find(chunk * 4 + npt);
+  auto it = h.dev->topo.find(chunk * 16 + npt);
   if (it != h.dev->topo.end()) return it->second;
   AllocScope scope(ctx->stream);
   const TopoHost th = plan_topo(h, cs, chunk, npt);
@@ -618,7 +619,7 @@ void ensure_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, in
   std::vector<HostMesh*> todo;
   for (HostMesh* h : meshes) {
     const int chunk = int((h->n + cs - 1) / cs);
-    if (!h->dev->topo.count(chunk * 4 + npt) &&
+    if (!h->dev->topo.count(chunk * 16 + npt) &&
         std::find(todo.begin(), todo.end(), h) == todo.end())
       todo.push_back(h);
   }
@@ -779,6 +780,9 @@ struct mrb_batch {
   // cluster fast path (0 = generic three-kernel loop)
   int cluster_cs = 0, cluster_npt = 1;
   int forced_cs = 0, forced_npt = 0;  // shape imposed by mrb_register_many
+  bool grid_mode = false;  // k_grid_register (cluster_cs = CTAs of the whole-GPU grid)
+  void* xbuf = nullptr;    // grid path exchange buffers (shared by the pairs, run in turn)
+  unsigned* xbar = nullptr;  // grid barrier counter + gbad flags [1 + CS]
   // wave groups (mrb_register_many): the first run launches the fast path per
   // group of pairs and records group_ev[g]; get_results then copies group g
   // back on copy_stream while later groups still compute
@@ -807,7 +811,7 @@ struct mrb_batch {
     }
     void* ptrs[] = {pairs, st, blk_pair, pix_blk_pair, partials, pix_partials, state, traces,
                     img, stage, src_ptrs, img_ptrs, dense, u_out, conv, cpairs, img_pad,
-                    phase_prof};
+                    phase_prof, xbuf, xbar};
     for (void* p : ptrs) dev_free(p, ctx ? ctx->stream : nullptr);
   }
 };
@@ -1021,7 +1025,40 @@ int cluster_occupancy_cs(int cs, int npt, size_t smem) {
   return memo[key] = occ;
 }
 
+template <int NPT>
+void launch_grid_t(mrb_batch* b, int p) {
+  cudaStream_t s = b->ctx->stream;
+  // barrier counter and sticky gradient flags start at zero for every pair
+  ck(cudaMemsetAsync(b->xbar, 0, size_t(1 + b->cluster_cs) * sizeof(unsigned), s));
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(unsigned(b->cluster_cs));
+  lc.blockDim = dim3(kClusterThreads);
+  lc.dynamicSmemBytes = b->cluster_smem;
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the grid barrier
+  attr[0].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  ck(cudaLaunchKernelEx(&lc, k_grid_register<NPT>, static_cast<const ClusterPair*>(b->cpairs) + p,
+                        b->st + p, int(b->cfg.max_iterations), double(b->cfg.energy_tolerance),
+                        float(b->cfg.tau), float(b->cfg.lam), int(b->cfg.smoothing_passes)));
+}
+
+int64_t launch_grid(mrb_batch* b, int p0, int np) {
+  for (int p = p0; p < p0 + np; ++p) {  // one whole-GPU launch per pair
+    switch (b->cluster_npt) {
+      case 1: launch_grid_t<1>(b, p); break;
+      case 2: launch_grid_t<2>(b, p); break;
+      case 4: launch_grid_t<4>(b, p); break;
+      default: launch_grid_t<8>(b, p); break;
+    }
+  }
+  return np;
+}
+
 int64_t launch_cluster(mrb_batch* b, int p0, int np) {
+  if (b->grid_mode) return launch_grid(b, p0, np);
   if (b->cluster_npt == 2)
     launch_cluster_t<2>(b, p0, np);
   else
@@ -1143,7 +1180,8 @@ int64_t dispatch_enqueue(mrb_batch* b, KernelTimer* tm = nullptr) {
 }
 
 int64_t launches_per_run(const mrb_batch* b) {
-  if (b->cluster_cs) return 4;  // pad, cluster loop, dense, msd
+  if (b->grid_mode) return 3 + b->n_pairs;  // pad, one grid loop per pair, dense, msd
+  if (b->cluster_cs) return 4;               // pad, cluster loop, dense, msd
   return 2 + int64_t(b->cfg.max_iterations) * (2 + b->cfg.smoothing_passes) + 3;
 }
 
@@ -1214,22 +1252,64 @@ bool choose_cluster_shape(mrb_ctx* ctx, HostMesh& big, int n_pairs, bool two_u, 
   return false;
 }
 
-// fast-path eligibility of a batch: fp32 state and images, one-rings within
-// kMaxDeg, at most 16 CTAs x 768 x 2 nodes per pair
-const char* cluster_ineligible(bool real_d, bool tap_d, int in_dtype,
-                               const std::vector<mrb_mesh*>& meshes) {
+// SMs of the current device (whole-GPU grid size of k_grid_register)
+int device_sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return std::max(n, 1);
+}
+
+constexpr int kGridMaxNpt = 8;
+
+// Fast-path mode of a batch: 1 = thread-block cluster per pair (every mesh
+// fits 16 CTAs x 768 x 2 nodes), 2 = whole-GPU grid per pair (larger meshes,
+// up to SMs x 768 x 8 nodes), 0 = generic path (*why says why).  Both fast
+// modes need fp32 state and images and one-rings within kMaxDeg.
+int fast_mode(bool real_d, bool tap_d, int in_dtype, const std::vector<mrb_mesh*>& meshes,
+              const char** why) {
   const char* env = std::getenv("MESHREG_B200_PATH");
-  if (env && std::string(env) == "generic") return "MESHREG_B200_PATH=generic";
-  if (real_d || tap_d) return "fp64 precision";
-  if (in_dtype != MRB_F32) return "fp64 image storage";
+  const std::string path = env ? env : "";
+  *why = nullptr;
+  if (path == "generic") return (*why = "MESHREG_B200_PATH=generic"), 0;
+  if (real_d || tap_d) return (*why = "fp64 precision"), 0;
+  if (in_dtype != MRB_F32) return (*why = "fp64 image storage"), 0;
+  int64_t nmax = 0;
   for (mrb_mesh* m : meshes) {
-    if (m->h.n > 16 * 2 * kClusterThreads) return "mesh larger than 16 CTAs x 1536 nodes";
+    nmax = std::max<int64_t>(nmax, m->h.n);
     int md = 0;
     for (int64_t k = 0; k < m->h.n; ++k) md = std::max(md, m->h.nb_ptr[k + 1] - m->h.nb_ptr[k]);
-    if (md > kMaxDeg) return "one-ring larger than kMaxDeg";
+    if (md > kMaxDeg) return (*why = "one-ring larger than kMaxDeg"), 0;
   }
-  return nullptr;
+  if (path != "grid" && nmax <= 16 * 2 * kClusterThreads) return 1;
+  if (nmax <= int64_t(device_sms()) * kClusterThreads * kGridMaxNpt) return 2;
+  return (*why = "mesh larger than the whole-GPU grid holds"), 0;
 }
+
+const char* cluster_ineligible(bool real_d, bool tap_d, int in_dtype,
+                               const std::vector<mrb_mesh*>& meshes) {
+  const char* why = nullptr;
+  return fast_mode(real_d, tap_d, in_dtype, meshes, &why) == 1
+             ? nullptr
+             : (why ? why : "mesh larger than one cluster");
+}
+
+// grid shape for the largest mesh: CS = SMs, NPT = smallest of 1/2/4/8 with
+// CS * 768 * NPT >= n
+void grid_shape(int64_t nmax, int* cs, int* npt) {
+  *cs = device_sms();
+  const int64_t per = (nmax + *cs - 1) / *cs;
+  *npt = 1;
+  while (int64_t(*npt) * kClusterThreads < per) *npt *= 2;
+}
+
+size_t grid_dyn_smem(int npt, int halo_stride, bool two_u) {
+  const size_t X = size_t(kClusterThreads) * npt + halo_stride;
+  return X * 4 + 8 + X * 8 * (two_u ? 2 : 1) + size_t(halo_stride) * 4 + 64;
+}
+
+void build_fast_descriptors(mrb_batch* b);
+void setup_grid_path(mrb_batch* b, int64_t nmax);
 
 void setup_cluster_path(mrb_batch* b) {
   b->cluster_cs = 0;
@@ -1237,12 +1317,18 @@ void setup_cluster_path(mrb_batch* b) {
   auto why = [&](const char* m) {
     if (dbg) std::fprintf(stderr, "meshreg_b200: generic path (%s)\n", m);
   };
-  if (const char* m = cluster_ineligible(b->real_d, b->tap_d, b->in_dtype, b->meshes))
-    return why(m);
+  const char* reason = nullptr;
+  const int mode = fast_mode(b->real_d, b->tap_d, b->in_dtype, b->meshes, &reason);
+  if (mode == 0) return why(reason);
   const bool two_u = b->cfg.smoothing_passes >= 2;
   mrb_mesh* big = *std::max_element(b->meshes.begin(), b->meshes.end(),
                                     [](mrb_mesh* x, mrb_mesh* y) { return x->h.n < y->h.n; });
   int cs = 0, npt = 0, occ = 0;
+  if (mode == 2) {
+    setup_grid_path(b, big->h.n);
+    if (!b->cluster_cs) return why("grid kernel does not fit");
+    return;
+  }
   if (b->forced_cs) {  // shape decided for the whole queue (mrb_register_many)
     cs = b->forced_cs;
     npt = b->forced_npt;
@@ -1267,6 +1353,12 @@ void setup_cluster_path(mrb_batch* b) {
   if (dbg)
     std::fprintf(stderr, "meshreg_b200: cluster %d CTAs x %d nodes/thread, %zu B smem\n", cs, npt,
                  smem);
+  build_fast_descriptors(b);
+}
+
+// ClusterPair descriptors + padded image copies of a fast-path batch
+void build_fast_descriptors(mrb_batch* b) {
+  const int cs = b->cluster_cs;
   b->pad_pitch = (b->W + 5 + 3) / 4 * 4;
   b->pad_plane = size_t(b->H + 2) * b->pad_pitch;
   // columns of a copy that k_pad_planar4 does not write are never read
@@ -1316,8 +1408,68 @@ void setup_cluster_path(mrb_batch* b) {
     c.slices = t.slices;
     c.pitch = b->pad_pitch;
     c.plane = int(b->pad_plane);
+    c.xg_s = nullptr;
+    c.xg_u = nullptr;
+    c.wpart = nullptr;
+    c.gbad = nullptr;
+    c.bar = nullptr;
+    if (b->grid_mode) {  // exchange buffers shared by the pairs (launched in turn)
+      const size_t slots = size_t(cs) * kClusterThreads * b->cluster_npt;
+      char* x = static_cast<char*>(b->xbuf);
+      c.xg_s = reinterpret_cast<float*>(x);
+      c.xg_u = reinterpret_cast<float2*>(x + (slots * 4 + 255) / 256 * 256);
+      c.wpart = reinterpret_cast<double*>(reinterpret_cast<char*>(c.xg_u) +
+                                          (2 * slots * 8 + 255) / 256 * 256);
+      c.bar = b->xbar;
+      c.gbad = reinterpret_cast<int*>(b->xbar + 1);
+    }
   }
   b->cpairs = dupload(cp.data(), cp.size(), b->ctx->stream);  // staged on return
+}
+
+// Whole-GPU grid path (meshes larger than one cluster): CS = SMs CTAs per
+// pair, NPT nodes per thread, topology read from global memory.
+void setup_grid_path(mrb_batch* b, int64_t nmax) {
+  int cs = 0, npt = 0;
+  grid_shape(nmax, &cs, &npt);
+  std::vector<HostMesh*> hm;
+  for (mrb_mesh* m : b->meshes) hm.push_back(&m->h);
+  ensure_cluster_topos(b->ctx, hm, cs, npt);
+  int hs = 0;
+  for (mrb_mesh* m : b->meshes) {
+    const int chunk = int((m->h.n + cs - 1) / cs);
+    hs = std::max(hs, ensure_cluster_topo(b->ctx, m->h, cs, chunk, npt).halo_stride);
+  }
+  const size_t smem = grid_dyn_smem(npt, hs, b->cfg.smoothing_passes >= 2);
+  auto fit = [&](auto kern) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kClusterThreads, smem) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return per_sm;
+  };
+  const int per_sm = npt == 1 ? fit(k_grid_register<1>) : npt == 2 ? fit(k_grid_register<2>)
+                     : npt == 4 ? fit(k_grid_register<4>) : fit(k_grid_register<8>);
+  if (per_sm < 1) return;
+  b->grid_mode = true;
+  b->cluster_cs = cs;
+  b->cluster_npt = npt;
+  b->cluster_smem = smem;
+  const size_t slots = size_t(cs) * kClusterThreads * npt;
+  b->xbuf = dalloc<char>((slots * 4 + 255) / 256 * 256 + (2 * slots * 8 + 255) / 256 * 256 +
+                         size_t(2) * cs * kWarps * 8);
+  b->xbar = dalloc<unsigned>(1 + size_t(cs));
+  if (std::getenv("MESHREG_B200_DEBUG"))
+    std::fprintf(stderr, "meshreg_b200: grid %d CTAs x %d nodes/thread, %zu B smem\n", cs, npt,
+                 smem);
+  build_fast_descriptors(b);
 }
 
 template <typename From, typename To>
@@ -1597,7 +1749,9 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
     }
     // the fast path never reads the generic one-ring arrays: upload them only
     // when the batch is not eligible for it
-    const bool eligible = !cluster_ineligible(b->real_d, b->tap_d, img_dtype, b->meshes);
+    const char* why_not = nullptr;
+    const int mode = fast_mode(b->real_d, b->tap_d, img_dtype, b->meshes, &why_not);
+    const bool eligible = mode != 0;
     b->forced_cs = forced_cs;
     b->forced_npt = forced_npt;
     ensure_device_meshes(ctx, hm, !eligible);
@@ -1612,6 +1766,8 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
       mrb_mesh* big = *std::max_element(b->meshes.begin(), b->meshes.end(),
                                         [](mrb_mesh* x, mrb_mesh* y) { return x->h.n < y->h.n; });
       int cs = forced_cs, npt = forced_npt, occ = 0;
+      if (mode == 2)
+        grid_shape(big->h.n, &cs, &npt);
       if (cs || choose_cluster_shape(ctx, big->h, n_pairs, cfg->smoothing_passes >= 2, &cs, &npt,
                                      &occ))
         ensure_cluster_topos(ctx, hm, cs, npt);
@@ -1857,7 +2013,9 @@ int mrb_batch_pair_status(mrb_batch* b, int32_t p, int32_t* iters, double* msd_b
 
 int64_t mrb_batch_launches_per_run(const mrb_batch* b) { return launches_per_run(b); }
 
-int32_t mrb_batch_path(const mrb_batch* b) { return b->cluster_cs; }
+int32_t mrb_batch_path(const mrb_batch* b) {
+  return b->grid_mode ? -b->cluster_cs : b->cluster_cs;
+}
 
 int mrb_transfer_bytes(int64_t* h2d, int64_t* d2h, int32_t reset) {
   if (h2d) *h2d = g_h2d_bytes.load();

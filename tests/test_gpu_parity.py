@@ -272,16 +272,40 @@ def test_rises_guard_fp32_and_message_format():
                        "non-finite gradient; reduce the step size tau"), msg
 
 
-@pytest.mark.parametrize("path", ["cluster", "generic"])
+@pytest.mark.parametrize("path", ["cluster", "grid", "generic"])
 @pytest.mark.parametrize("name", ["gen64", "gen64_x255", "gen64_p0", "gen64_p2", "c1", "accept_c3"])
 def test_fp32_paths_agree_with_reference(name, path, monkeypatch):
-    """The persistent cluster kernel and the generic three-kernel loop both
-    meet the fp32 tolerances."""
-    if path == "generic":
-        monkeypatch.setenv("MESHREG_B200_PATH", "generic")
+    """The persistent cluster kernel, the whole-GPU grid kernel (forced here on
+    small meshes; chosen by size for C3/C5) and the generic three-kernel loop
+    all meet the fp32 tolerances."""
+    if path in ("generic", "grid"):
+        monkeypatch.setenv("MESHREG_B200_PATH", path)
     else:
         monkeypatch.delenv("MESHREG_B200_PATH", raising=False)
     check_register(golden(name), "f32", name)
+
+
+def test_path_selection(monkeypatch):
+    """mrb_batch_path: cluster size > 0, minus the grid CTA count < 0, 0 generic."""
+    import ctypes as C
+    from paper_1411_2141_b200 import _lib
+    g = golden("gen64")
+    lib = _lib.load()
+    ctx = _lib.context()
+    mesh = mrb.TriMesh(g["V"], g["T_in"])
+    cfg = _lib.mrb_config(0.005, 0.8, 0.0, 10, 1, _lib.PREC_F32, 0)
+    seen = {}
+    for path in ("", "grid", "generic"):
+        if path:
+            monkeypatch.setenv("MESHREG_B200_PATH", path)
+        else:
+            monkeypatch.delenv("MESHREG_B200_PATH", raising=False)
+        arr = (C.c_void_p * 1)(mesh._h)
+        b = C.c_void_p()
+        assert lib.mrb_batch_create(ctx, 1, arr, 64, 64, _lib.F32, C.byref(cfg), C.byref(b)) == 0
+        seen[path] = lib.mrb_batch_path(b)
+        lib.mrb_batch_destroy(b)
+    assert seen[""] > 0 and seen["grid"] < 0 and seen["generic"] == 0
 
 
 @pytest.mark.parametrize("precision", ["f32", "f64"])
