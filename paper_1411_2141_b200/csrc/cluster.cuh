@@ -270,6 +270,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
 
   __shared__ double s_wpart[2][kWarps];  // per-warp energy partials, by iteration parity
+  __shared__ double s_cpart[2];          // CTA energy partial (fixed-order sum of s_wpart)
   __shared__ int s_gradbad;              // non-finite gradient seen in this CTA
   __shared__ int s_stop;                 // decision so far: 0 go, 1 error, 2 converged
   __shared__ int s_nhalo;
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     r[j] = 0.f;
   }
 #define OWN(j) ((own_mask >> (j)) & 1u)
-  const uint32_t wpart_addr = smem_u32(&s_wpart[0][0]), bad_addr = smem_u32(&s_gradbad);
+  const uint32_t cpart_addr = smem_u32(&s_cpart[0]), bad_addr = smem_u32(&s_gradbad);
   const uint32_t xs_addr = smem_u32(sm.xs), xu0_addr = smem_u32(sm.xu0),
                  xu1_addr = smem_u32(sm.xu1);
   cluster_sync_all();  // every CTA started and staged
@@ -333,10 +334,9 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   // solver.py:176-195 in the reference's order (energy checks, the step's
   // gradient check, tolerance).
   auto control = [&](int kk) {
-    double v = 0.0;
-    for (int idx = lane; idx < CS * kWarps; idx += 32)
-      v += ld_dsmem_f64(mapa_u32(wpart_addr, idx / kWarps) +
-                        8u * ((kk & 1) * kWarps + idx % kWarps));
+    // one DSMEM load per lane: the CTA partials of iteration kk (each CTA
+    // reduced its own warp partials after the first barrier of kk)
+    double v = lane < CS ? ld_dsmem_f64(mapa_u32(cpart_addr, lane) + 8u * (kk & 1)) : 0.0;
     int gb = lane < CS ? ld_dsmem_s32(mapa_u32(bad_addr, lane)) : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -416,6 +416,12 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     }
     PROF(k, 3)
     __syncthreads();  // s_te halo complete
+    if (warp == kCtlWarp) {  // CTA energy partial of iteration k, fixed order
+      double v = lane < kWarps ? s_wpart[k & 1][lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if (lane == 0) s_cpart[k & 1] = v;  // read remotely after the next cluster barrier
+    }
     PROF(k, 4)
 
     // -------- phase B: gradient via the fused one-ring operator, descent

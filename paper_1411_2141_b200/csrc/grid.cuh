@@ -107,11 +107,12 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   __syncthreads();
   const int nhalo = s_nhalo;
 
-  // control step of iteration kk: all CS * kWarps partials in one fixed order
+  __shared__ double s_wpart[kWarps];
+  // control step of iteration kk: the CS CTA partials in one fixed order
   auto control = [&](int kk) {
     double v = 0.0;
-    const double* wp = d.wpart + size_t(kk & 1) * CS * kWarps;
-    for (int idx = lane; idx < CS * kWarps; idx += 32) v += __ldcg(wp + idx);
+    const double* wp = d.wpart + size_t(kk & 1) * CS;
+    for (int idx = lane; idx < CS; idx += 32) v += __ldcg(wp + idx);
     int gb = 0;
     for (int idx = lane; idx < CS; idx += 32) gb |= __ldcg(d.gbad + idx);
 #pragma unroll
@@ -182,13 +183,20 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) e2 += __shfl_down_sync(0xffffffffu, e2, o);
-      if (lane == 0) __stcg(d.wpart + (size_t(k & 1) * CS + rank) * kWarps + warp, e2);
+      if (lane == 0) s_wpart[warp] = e2;
     }
     gsync();            // s_te, energy partials (and the k-1 decision) visible
     if (s_stop) break;  // iteration k-1 was the last one (u untouched since)
     for (int h = t; h < nhalo; h += kClusterThreads) {  // pull the s_te halo
       const uint32_t c = halo[h];
       xs[SLOTS + h] = __ldcg(xg_s + size_t(c >> 16) * SLOTS + (c & 0xffffu));
+    }
+    if (warp == kCtlWarp) {  // CTA energy partial of iteration k, fixed order; read by
+      // every CTA's control(k) after the next grid barrier
+      double v = lane < kWarps ? s_wpart[lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if (lane == 0) __stcg(d.wpart + size_t(k & 1) * CS + rank, v);
     }
     __syncthreads();
 
