@@ -171,7 +171,18 @@ struct Window {
   float wx[4], wy[4];
 };
 
-__device__ __forceinline__ Window locate(const ClusterPair& d, double x, double y) {
+// the image fields locate() needs, held in registers across the loop
+struct ImgView {
+  const float2* img4;
+  int W, H, pitch, plane;
+};
+
+__device__ __forceinline__ ImgView img_view(const ClusterPair& d) {
+  return ImgView{d.img4, d.W, d.H, d.pitch, d.plane};
+}
+
+template <typename D>
+__device__ __forceinline__ Window locate(const D& d, double x, double y) {
   const double xc = fmin(fmax(x, 0.0), double(d.W) - 1.0);
   const double yc = fmin(fmax(y, 0.0), double(d.H) - 1.0);
   const int cx = min(int(xc), d.W - 2);  // xc >= 0: truncation == floor
@@ -382,6 +393,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     }
   };
 
+  const ImgView img = img_view(d);
   int k = 0;
   for (; k < max_iter; ++k) {
     PROF(k, 0)
@@ -392,10 +404,10 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       for (int j = 0; j < NPT; ++j) {  // one node at a time: no register spills
         if (OWN(j)) {
           const double2 V = sm.V[t + j * kClusterThreads];
-          const Window w = locate(d, V.x + double(u[j].x), V.y + double(u[j].y));
+          const Window w = locate(img, V.x + double(u[j].x), V.y + double(u[j].y));
           float2 tap[4][4];
 #pragma unroll
-          for (int row = 0; row < 4; ++row) ld_row4(w.base + size_t(row) * d.pitch, tap[row]);
+          for (int row = 0; row < 4; ++row) ld_row4(w.base + size_t(row) * img.pitch, tap[row]);
           const float2 s = combine(w, tap);
           r[j] = s.x - s.y;
           sm.xs[t + j * kClusterThreads] = s.x;
@@ -456,7 +468,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       for (int j = 0; j < NPT; ++j) {
         if (OWN(j)) {
           const int slot = t + j * kClusterThreads;
-          u[j] = clamp_dom(sm.xu0[slot], sm.V[slot], d.W, d.H);
+          u[j] = clamp_dom(sm.xu0[slot], sm.V[slot], img.W, img.H);
         }
       }
     }
@@ -495,7 +507,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       if (q == passes - 1) {
 #pragma unroll
         for (int j = 0; j < NPT; ++j)
-          if (OWN(j)) u[j] = clamp_dom(v[j], sm.V[t + j * kClusterThreads], d.W, d.H);
+          if (OWN(j)) u[j] = clamp_dom(v[j], sm.V[t + j * kClusterThreads], img.W, img.H);
       } else {
         float2* dst = (q & 1) ? sm.xu0 : sm.xu1;
 #pragma unroll
