@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   const int nhalo = s_nhalo;
 
   long long* const prof =
-      (d.prof && t == 0) ? d.prof + (size_t(blockIdx.x) * 8) * 16 : nullptr;
+      (d.prof && t == 0) ? d.prof + (size_t(rank) * 8) * 16 : nullptr;  // d.prof: this pair's
 #define PROF(k, slot) \
   if (prof && (k) < 8) prof[(k) * 16 + (slot)] = clock64();
 

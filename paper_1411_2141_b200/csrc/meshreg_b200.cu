@@ -34,11 +34,21 @@ struct mrb_ctx {
   cudaStream_t stream = nullptr;
   std::string err;
   mrb_ctx* sub[2] = {nullptr, nullptr};  // pipeline streams of mrb_register_many
-  void* pinned = nullptr;  // host staging buffer for mesh uploads (grows)
-  size_t pinned_cap = 0;
-  cudaEvent_t stage_done = nullptr;  // last async copy out of `pinned`
+  // host staging buffers for uploads (grow): [0] meshes, [1] fast-path
+  // topologies, so planning the topologies never waits for the mesh copies
+  void* pinned[2] = {nullptr, nullptr};
+  size_t pinned_cap[2] = {0, 0};
+  cudaEvent_t stage_done[2] = {nullptr, nullptr};  // last async copy out of pinned[i]
   cudaStream_t copy = nullptr;       // input copies of mrb_register_many
   cudaEvent_t copy_done = nullptr;
+  unsigned long long* counts = nullptr;  // pinned uncovered-pixel counts
+  size_t counts_cap = 0;
+  // pinned arena for the small descriptor uploads of a batch creation: a
+  // pageable cudaMemcpyAsync synchronises the stream first, a pinned one not
+  unsigned char* arena = nullptr;
+  size_t arena_cap = 0, arena_off = 0;
+  cudaEvent_t arena_done = nullptr;
+  bool arena_used = false;
 };
 
 struct mrb_mesh {
@@ -70,6 +80,7 @@ struct DeviceMesh {
   int device = -1;
   cudaStream_t stream = nullptr;  // stream its memory is ordered on
   unsigned char* slab = nullptr;
+  std::shared_ptr<unsigned char> slab_hold;  // set when `slab` is a slice of a shared upload
   unsigned char* slab64 = nullptr;
   unsigned char* slab_ring = nullptr;
   double2* V = nullptr;
@@ -86,7 +97,8 @@ struct DeviceMesh {
   std::map<std::pair<int, int>, int*> pixel_maps;
   // cluster fast path: register topology packed for a given chunk size
   struct Topo {  // SELL-32 one-ring layout for one (cluster size, nodes/thread)
-    unsigned char* slab = nullptr;  // owns every array below
+    unsigned char* slab = nullptr;  // every array below lives in it
+    std::shared_ptr<unsigned char> hold;  // owner when the slab is a shared upload's slice
     uint16_t* codes = nullptr;
     float2* g = nullptr;
     uint32_t* slice_off = nullptr;
@@ -101,11 +113,19 @@ struct DeviceMesh {
     int cur = -1;
     cudaGetDevice(&cur);
     if (device >= 0) cudaSetDevice(device);
-    dev_free(slab, stream);  // every per-mesh array lives in the slabs
+    if (slab_hold)  // every per-mesh array lives in the slabs
+      slab_hold.reset();
+    else
+      dev_free(slab, stream);
     dev_free(slab64, stream);
     dev_free(slab_ring, stream);
     for (auto& kv : pixel_maps) dev_free(kv.second, stream);
-    for (auto& kv : topo) dev_free(kv.second.slab, stream);
+    for (auto& kv : topo) {
+      if (kv.second.hold)
+        kv.second.hold.reset();
+      else
+        dev_free(kv.second.slab, stream);
+    }
     if (cur >= 0) cudaSetDevice(cur);
   }
 };
@@ -140,6 +160,13 @@ inline cudaError_t mrb_copy_async(void* dst, const void* src, size_t bytes, cuda
   return cudaMemcpyAsync(dst, src, bytes, kind, s);
 }
 
+inline cudaError_t mrb_copy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch,
+                                    size_t width, size_t height, cudaMemcpyKind kind,
+                                    cudaStream_t s) {
+  count_copy(width * height, kind);
+  return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, kind, s);
+}
+
 inline cudaError_t mrb_copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
   count_copy(bytes, kind);
   return cudaMemcpy(dst, src, bytes, kind);
@@ -154,6 +181,48 @@ T* dalloc(size_t n) {
   else
     ck(cudaMalloc(&p, n * sizeof(T)));
   return static_cast<T*>(p);
+}
+
+// One device allocation shared by the meshes of an upload (freed, stream
+// ordered, with the last mesh that uses it).
+std::shared_ptr<unsigned char> shared_slab(size_t bytes, cudaStream_t s) {
+  unsigned char* p = dalloc<unsigned char>(bytes);
+  return std::shared_ptr<unsigned char>(p, [s](unsigned char* q) { dev_free(q, s); });
+}
+
+// Descriptor arena (mrb_ctx::arena): arena_begin waits until the previous
+// creation's copies left the arena, then hands out slices (each upload
+// records arena_done after its copy).
+void arena_begin(mrb_ctx* ctx, size_t need) {
+  if (ctx->arena_used) ck(cudaEventSynchronize(ctx->arena_done));
+  ctx->arena_used = false;
+  ctx->arena_off = 0;
+  if (need > ctx->arena_cap) {
+    if (ctx->arena) cudaFreeHost(ctx->arena);
+    ctx->arena = nullptr;
+    ctx->arena_cap = 0;
+    const size_t cap = std::max<size_t>(need + need / 2, size_t(1) << 20);
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->arena), cap, cudaHostAllocDefault));
+    ctx->arena_cap = cap;
+  }
+  if (!ctx->arena_done) ck(cudaEventCreateWithFlags(&ctx->arena_done, cudaEventDisableTiming));
+}
+
+template <typename T>
+T* dupload(const T* h, size_t n, cudaStream_t s);
+
+// device copy of h[0..n) through the arena (pageable fallback when full)
+template <typename T>
+T* aupload(mrb_ctx* ctx, const T* h, size_t n) {
+  const size_t bytes = n * sizeof(T), at = (ctx->arena_off + 255) / 256 * 256;
+  if (!ctx->arena || at + bytes > ctx->arena_cap) return dupload(h, n, ctx->stream);
+  std::memcpy(ctx->arena + at, h, bytes);
+  ctx->arena_off = at + bytes;
+  T* d = dalloc<T>(n);
+  if (n) ck(mrb_copy_async(d, ctx->arena + at, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ck(cudaEventRecord(ctx->arena_done, ctx->stream));  // arena slice free after this
+  ctx->arena_used = true;
+  return d;
 }
 
 template <typename T>
@@ -243,17 +312,17 @@ std::string py_repr(double v) {
 
 // Host staging memory owned by the context (pinned, grows, reused once the
 // previous copy out of it has completed).
-void* pinned_stage(mrb_ctx* ctx, size_t bytes) {
-  if (ctx->stage_done) ck(cudaEventSynchronize(ctx->stage_done));
-  if (bytes > ctx->pinned_cap) {
-    if (ctx->pinned) cudaFreeHost(ctx->pinned);
-    ctx->pinned = nullptr;
-    ctx->pinned_cap = 0;
+void* pinned_stage(mrb_ctx* ctx, size_t bytes, int which) {
+  if (ctx->stage_done[which]) ck(cudaEventSynchronize(ctx->stage_done[which]));
+  if (bytes > ctx->pinned_cap[which]) {
+    if (ctx->pinned[which]) cudaFreeHost(ctx->pinned[which]);
+    ctx->pinned[which] = nullptr;
+    ctx->pinned_cap[which] = 0;
     const size_t cap = std::max<size_t>(bytes + bytes / 4, size_t(16) << 20);
-    ck(cudaHostAlloc(&ctx->pinned, cap, cudaHostAllocDefault));
-    ctx->pinned_cap = cap;
+    ck(cudaHostAlloc(&ctx->pinned[which], cap, cudaHostAllocDefault));
+    ctx->pinned_cap[which] = cap;
   }
-  return ctx->pinned;
+  return ctx->pinned[which];
 }
 
 // Persistent host worker pool: parallel_for(n, f) runs f(0..n-1) on up to 16
@@ -385,7 +454,7 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, bo
     pl.base = total;
     total += pl.tot;
   }
-  unsigned char* stage = static_cast<unsigned char*>(pinned_stage(ctx, total));
+  unsigned char* stage = static_cast<unsigned char*>(pinned_stage(ctx, total, 0));
   tick("stage wait");
   auto fill = [&](size_t i) {
     const HostMesh& h = *todo[i];
@@ -408,6 +477,10 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, bo
   };
   parallel_for(todo.size(), fill);
   tick("host fill");
+  // one allocation and one large copy for every mesh of the upload (large
+  // copies run at full PCIe rate, ~1 MB ones at less than half of it)
+  const std::shared_ptr<unsigned char> all = shared_slab(total, ctx->stream);
+  ck(mrb_copy_async(all.get(), stage, total, cudaMemcpyHostToDevice, ctx->stream));
   for (size_t i = 0; i < todo.size(); ++i) {
     HostMesh& h = *todo[i];
     const Plan& pl = plan[i];
@@ -415,9 +488,9 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, bo
     DeviceMesh& d = *h.dev;
     d.device = ctx->device;
     d.stream = ctx->stream;
-    unsigned char* slab = dalloc<unsigned char>(pl.tot);
+    unsigned char* slab = all.get() + pl.base;
     d.slab = slab;
-    ck(mrb_copy_async(slab, stage + pl.base, pl.tot, cudaMemcpyHostToDevice, ctx->stream));
+    d.slab_hold = all;
     d.V = reinterpret_cast<double2*>(slab + pl.off[0]);
     if (with_ring) {
       d.nb_ptr = reinterpret_cast<int*>(slab + pl.off[1]);
@@ -431,7 +504,7 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, bo
     for (int64_t k = 0; k < h.n; ++k)
       d.max_deg = std::max(d.max_deg, h.nb_ptr[k + 1] - h.nb_ptr[k]);
   }
-  ck(cudaEventRecord(ctx->stage_done, ctx->stream));  // staging buffer reusable after this
+  ck(cudaEventRecord(ctx->stage_done[0], ctx->stream));  // staging buffer reusable after this
   tick("copies issued");
 }
 
@@ -582,7 +655,7 @@ void write_topo(const HostMesh& h, int cs, const TopoHost& t, unsigned char* dst
 }
 
 // device arrays of a packed topology, carved out of one slab
-const DeviceMesh::Topo& install_topo(HostMesh& h, int npt, const TopoHost& th,
+DeviceMesh::Topo& install_topo(HostMesh& h, int npt, const TopoHost& th,
                                      unsigned char* slab) {
   DeviceMesh::Topo t;
   t.chunk = th.chunk;
@@ -645,17 +718,17 @@ void ensure_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, in
     base[i] = total;
     total += th[i].total;
   }
-  unsigned char* stage = static_cast<unsigned char*>(pinned_stage(ctx, total));
+  unsigned char* stage = static_cast<unsigned char*>(pinned_stage(ctx, total, 1));
   tick("stage wait");
   parallel_for(todo.size(), [&](size_t i) { write_topo(*todo[i], cs, th[i], stage + base[i]); });
   tick("stage fill");
   AllocScope scope(ctx->stream);
-  for (size_t i = 0; i < todo.size(); ++i) {  // one slab per mesh (owned by its DeviceMesh)
-    unsigned char* slab = dalloc<unsigned char>(th[i].total);
-    ck(mrb_copy_async(slab, stage + base[i], th[i].total, cudaMemcpyHostToDevice, ctx->stream));
-    install_topo(*todo[i], npt, th[i], slab);
-  }
-  ck(cudaEventRecord(ctx->stage_done, ctx->stream));
+  // one allocation, one copy; each mesh's topology is a slice (shared owner)
+  const std::shared_ptr<unsigned char> all = shared_slab(total, ctx->stream);
+  ck(mrb_copy_async(all.get(), stage, total, cudaMemcpyHostToDevice, ctx->stream));
+  for (size_t i = 0; i < todo.size(); ++i)
+    install_topo(*todo[i], npt, th[i], all.get() + base[i]).hold = all;
+  ck(cudaEventRecord(ctx->stage_done[1], ctx->stream));
   tick("copies issued");
 }
 
@@ -667,51 +740,87 @@ size_t cluster_dyn_smem(int npt, int topo_stride, int slices, int halo_stride, b
          size_t(topo_stride) * (sizeof(float2) + sizeof(uint16_t)) + size_t(slices) * 4;
 }
 
-// Pixel->triangle map for (W, H): GPU raster + host locate fallback.
-// Returns "" or the MeshCoverageError message.
-std::string ensure_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int W, int H) {
+// Pixel->triangle map for (W, H): GPU raster + host locate fallback, in two
+// halves so host work can run while the rasters do: issue_pixel_maps enqueues
+// the rasters and the uncovered-pixel counts (into pinned memory) and records
+// an event; finish_pixel_maps waits for that event only and runs the
+// reference's binned locate for uncovered pixels.  Returns "" or the
+// MeshCoverageError message.
+struct PixelMapJob {
+  std::vector<HostMesh*> todo;
+  std::vector<int*> maps;
+  int W = 0, H = 0;
+  unsigned long long* missing = nullptr;  // pinned, one count per map
+  cudaEvent_t done = nullptr;
+};
+
+PixelMapJob issue_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int W, int H) {
+  PixelMapJob job;
+  job.W = W;
+  job.H = H;
   const auto key = std::make_pair(W, H);
   ensure_device_meshes(ctx, meshes, false);
-  std::vector<HostMesh*> todo;
   for (HostMesh* h : meshes) {
     if (!h->dev->pixel_maps.count(key) &&
-        std::find(todo.begin(), todo.end(), h) == todo.end())
-      todo.push_back(h);
+        std::find(job.todo.begin(), job.todo.end(), h) == job.todo.end())
+      job.todo.push_back(h);
   }
-  if (todo.empty()) return "";
+  if (job.todo.empty()) return job;
   cudaStream_t s = ctx->stream;
   const size_t npx = size_t(W) * size_t(H);
+  if (ctx->counts_cap < job.todo.size()) {  // pinned count slots (grow)
+    if (ctx->counts) cudaFreeHost(ctx->counts);
+    ctx->counts = nullptr;
+    ctx->counts_cap = 0;
+    const size_t cap = std::max<size_t>(job.todo.size(), 1024);
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->counts), cap * sizeof(unsigned long long),
+                     cudaHostAllocDefault));
+    ctx->counts_cap = cap;
+  }
+  job.missing = ctx->counts;
   unsigned long long* cnt = nullptr;
-  ck(cudaMallocAsync(&cnt, todo.size() * sizeof(unsigned long long), s));
-  ck(cudaMemsetAsync(cnt, 0, todo.size() * sizeof(unsigned long long), s));
-  std::vector<int*> maps(todo.size());
-  for (size_t i = 0; i < todo.size(); ++i) {  // every raster before one sync
-    const HostMesh& h = *todo[i];
-    maps[i] = dalloc<int>(npx);
-    ck(cudaMemsetAsync(maps[i], 0x7f, npx * sizeof(int), s));
+  ck(cudaMallocAsync(&cnt, job.todo.size() * sizeof(unsigned long long), s));
+  ck(cudaMemsetAsync(cnt, 0, job.todo.size() * sizeof(unsigned long long), s));
+  job.maps.resize(job.todo.size());
+  for (size_t i = 0; i < job.todo.size(); ++i) {  // every raster before one wait
+    const HostMesh& h = *job.todo[i];
+    job.maps[i] = dalloc<int>(npx);
+    ck(cudaMemsetAsync(job.maps[i], 0x7f, npx * sizeof(int), s));
     k_raster<<<unsigned((h.m * 32 + 255) / 256), 256, 0, s>>>(h.dev->V, h.dev->tri, int(h.m), W, H,
-                                                          maps[i]);
+                                                          job.maps[i]);
     k_count_uncovered<<<unsigned(std::min<size_t>((npx + 255) / 256, 1184)), 256, 0, s>>>(
-        maps[i], int(npx), cnt + i);
+        job.maps[i], int(npx), cnt + i);
   }
   ck(cudaGetLastError());
-  std::vector<unsigned long long> missing(todo.size());
-  ck(mrb_copy_async(missing.data(), cnt, todo.size() * sizeof(unsigned long long),
-                     cudaMemcpyDeviceToHost, s));
+  ck(mrb_copy_async(job.missing, cnt, job.todo.size() * sizeof(unsigned long long),
+                    cudaMemcpyDeviceToHost, s));
   ck(cudaFreeAsync(cnt, s));
+  ck(cudaEventCreateWithFlags(&job.done, cudaEventDisableTiming));
+  ck(cudaEventRecord(job.done, s));
+  return job;
+}
+
+std::string finish_pixel_maps(mrb_ctx* ctx, PixelMapJob& job) {
+  if (job.todo.empty()) return "";
+  const int W = job.W, H = job.H;
+  const size_t npx = size_t(W) * size_t(H);
   const auto ts = std::chrono::steady_clock::now();
-  ck(cudaStreamSynchronize(s));
+  ck(cudaEventSynchronize(job.done));
+  cudaEventDestroy(job.done);
+  job.done = nullptr;
   if (std::getenv("MESHREG_B200_DEBUG"))
-    std::fprintf(stderr, "meshreg_b200:   pixel maps: %zu rasters, sync wait %.2f ms\n", todo.size(),
+    std::fprintf(stderr, "meshreg_b200:   pixel maps: %zu rasters, wait %.2f ms\n",
+                 job.todo.size(),
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts)
                      .count());
   std::string err;
-  for (size_t i = 0; i < todo.size(); ++i) {
-    HostMesh& h = *todo[i];
-    if (missing[i] && err.empty()) {
+  for (size_t i = 0; i < job.todo.size(); ++i) {
+    HostMesh& h = *job.todo[i];
+    const unsigned long long missing = job.missing[i];
+    if (missing && err.empty()) {
       // densefield.py:176-182: binned locate for each unassigned pixel, row-major
       std::vector<int> host(npx);
-      ck(mrb_copy(host.data(), maps[i], npx * sizeof(int), cudaMemcpyDeviceToHost));
+      ck(mrb_copy(host.data(), job.maps[i], npx * sizeof(int), cudaMemcpyDeviceToHost));
       Locator loc(h);
       for (size_t q = 0; q < npx && err.empty(); ++q) {
         if (host[q] != kUnassigned) continue;
@@ -727,15 +836,20 @@ std::string ensure_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes
         host[q] = int(t);
       }
       if (err.empty())
-        ck(mrb_copy(maps[i], host.data(), npx * sizeof(int), cudaMemcpyHostToDevice));
+        ck(mrb_copy(job.maps[i], host.data(), npx * sizeof(int), cudaMemcpyHostToDevice));
     }
-    if (missing[i] && !err.empty()) {
-      dev_free(maps[i], ctx->stream);
+    if (missing && !err.empty()) {
+      dev_free(job.maps[i], ctx->stream);
       continue;
     }
-    h.dev->pixel_maps[key] = maps[i];
+    h.dev->pixel_maps[std::make_pair(W, H)] = job.maps[i];
   }
   return err;
+}
+
+std::string ensure_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int W, int H) {
+  PixelMapJob job = issue_pixel_maps(ctx, meshes, W, H);
+  return finish_pixel_maps(ctx, job);
 }
 
 std::string ensure_pixel_map(mrb_ctx* ctx, HostMesh& h, int W, int H, int** out) {
@@ -901,9 +1015,9 @@ void build_pairs(mrb_batch* b) {
   b->n_node_blocks = blk;
   b->n_pix_blocks = pblk;
   cudaStream_t s = b->ctx->stream;
-  b->pairs = dupload(pd.data(), pd.size(), s);  // pageable copies: staged on return
-  b->blk_pair = dupload(bp.data(), bp.size(), s);
-  b->pix_blk_pair = dupload(pbp.data(), pbp.size(), s);
+  b->pairs = aupload(b->ctx, pd.data(), pd.size());
+  b->blk_pair = aupload(b->ctx, bp.data(), bp.size());
+  b->pix_blk_pair = aupload(b->ctx, pbp.data(), pbp.size());
   b->partials = dalloc<double>(blk);
   b->pix_partials = dalloc<double2>(pblk);
   b->pairs_host.assign(reinterpret_cast<const unsigned char*>(pd.data()),
@@ -1424,7 +1538,7 @@ void build_fast_descriptors(mrb_batch* b) {
       c.gbad = reinterpret_cast<int*>(b->xbar + 1);
     }
   }
-  b->cpairs = dupload(cp.data(), cp.size(), b->ctx->stream);  // staged on return
+  b->cpairs = aupload(b->ctx, cp.data(), cp.size());
 }
 
 // Whole-GPU grid path (meshes larger than one cluster): CS = SMs CTAs per
@@ -1470,6 +1584,15 @@ void setup_grid_path(mrb_batch* b, int64_t nmax) {
     std::fprintf(stderr, "meshreg_b200: grid %d CTAs x %d nodes/thread, %zu B smem\n", cs, npt,
                  smem);
   build_fast_descriptors(b);
+}
+
+// src_ptrs[p] = re + p * stride, src_ptrs[n + p] = te + p * stride
+__global__ void k_fill_ptrs(void** __restrict__ out, const char* re, const char* te,
+                            size_t stride, int n) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  out[p] = const_cast<char*>(re + size_t(p) * stride);
+  out[n + p] = const_cast<char*>(te + size_t(p) * stride);
 }
 
 template <typename From, typename To>
@@ -1539,7 +1662,8 @@ int mrb_ctx_create(int32_t device, mrb_ctx** out) {
   c->device = device;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming);
+  for (auto& ev : c->stage_done)
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   if (e == cudaSuccess) {  // keep freed pool memory for reuse by later batches
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -1566,13 +1690,18 @@ int mrb_ctx_destroy(mrb_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     cudaStreamDestroy(ctx->stream);
   }
-  if (ctx->stage_done) cudaEventDestroy(ctx->stage_done);
+  for (cudaEvent_t ev : ctx->stage_done)
+    if (ev) cudaEventDestroy(ev);
   if (ctx->copy) {
     cudaStreamSynchronize(ctx->copy);
     cudaStreamDestroy(ctx->copy);
   }
   if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
-  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (void* pin : ctx->pinned)
+    if (pin) cudaFreeHost(pin);
+  if (ctx->counts) cudaFreeHost(ctx->counts);
+  if (ctx->arena) cudaFreeHost(ctx->arena);
+  if (ctx->arena_done) cudaEventDestroy(ctx->arena_done);
   delete ctx;
   return MRB_OK;
 }
@@ -1730,12 +1859,20 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
   AllocScope scope(ctx->stream);
   try {
     ck(cudaSetDevice(ctx->device));
+    {
+      size_t nodes = 0;
+      for (int p = 0; p < n_pairs; ++p) nodes += size_t(meshes[p]->h.n);
+      const size_t pix_blocks = size_t(n_pairs) * ((size_t(W) * H + kPixBlock - 1) / kPixBlock);
+      arena_begin(ctx, size_t(n_pairs) * 2048 + 4 * (pix_blocks + nodes / kNodeBlock + n_pairs) +
+                           (64 << 10));
+    }
     int64_t off = 0;
     const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
     auto t0 = std::chrono::steady_clock::now();
+    const bool dbg_sync = dbg && std::string(std::getenv("MESHREG_B200_DEBUG")) != "2";
     auto tick = [&](const char* what) {
       if (!dbg) return;
-      cudaStreamSynchronize(ctx->stream);
+      if (dbg_sync) cudaStreamSynchronize(ctx->stream);  // MESHREG_B200_DEBUG=2: host time only
       const auto t1 = std::chrono::steady_clock::now();
       std::fprintf(stderr, "meshreg_b200: batch_create %-22s %8.2f ms\n", what,
                    std::chrono::duration<double, std::milli>(t1 - t0).count());
@@ -1760,6 +1897,7 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
     if (b->real_d)
       for (HostMesh* h : hm) ensure_device_mesh_f64(ctx, *h);
     tick("mesh upload");
+    PixelMapJob pmj = issue_pixel_maps(ctx, hm, W, H);  // rasters run while the host plans
     if (eligible) {
       // fast-path topologies first: their host planning overlaps the mesh and
       // image uploads still in flight (ensure_pixel_maps synchronises)
@@ -1773,7 +1911,7 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
         ensure_cluster_topos(ctx, hm, cs, npt);
       tick("topologies");
     }
-    const std::string msg = ensure_pixel_maps(ctx, hm, W, H);
+    const std::string msg = finish_pixel_maps(ctx, pmj);
     if (!msg.empty()) return fail(ctx, MRB_E_COVERAGE, msg);
     tick("pixel maps");
     b->total_nodes = off;
@@ -1783,11 +1921,10 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
     b->img = dalloc<char>(size_t(n_pairs) * 2 * npx * tap_size(b.get()));
     b->u_out = dalloc<double2>(off);
     b->src_ptrs = dalloc<void*>(2 * n_pairs);
-    b->img_ptrs = dalloc<void*>(n_pairs);
     std::vector<void*> ip(n_pairs);
     for (int p = 0; p < n_pairs; ++p)
       ip[p] = static_cast<char*>(b->img) + size_t(p) * 2 * npx * tap_size(b.get());
-    ck(mrb_copy(b->img_ptrs, ip.data(), n_pairs * sizeof(void*), cudaMemcpyHostToDevice));
+    b->img_ptrs = aupload(ctx, ip.data(), ip.size());
     if (b->tap_d)
       build_pairs<double, double>(b.get());
     else if (b->real_d)
@@ -1863,11 +2000,11 @@ int mrb_batch_set_images(mrb_batch* b, const void* re, const void* te, int32_t o
       ptrs[p] = rs + size_t(p) * npx * es;
       ptrs[b->n_pairs + p] = ts + size_t(p) * npx * es;
     }
-    if (ptrs != b->src_host) {
-      ck(mrb_copy_async(b->src_ptrs, ptrs.data(), ptrs.size() * sizeof(void*),
-                         cudaMemcpyHostToDevice, ctx->stream));
-      ck(cudaStreamSynchronize(ctx->stream));  // ptrs is a stack temporary
+    if (ptrs != b->src_host) {  // filled on the device: no host buffer, no stream sync
       b->src_host = ptrs;
+      k_fill_ptrs<<<(b->n_pairs + 255) / 256, 256, 0, ctx->stream>>>(
+          b->src_ptrs, rs, ts, npx * es, b->n_pairs);
+      ck(cudaGetLastError());
     }
   } catch (const CudaError& e) {
     return cuda_fail(ctx, e.e);
@@ -1922,12 +2059,12 @@ int mrb_batch_get_results(mrb_batch* b, int32_t out_dtype, double* u, void* ux, 
           ck(mrb_copy_async(u + 2 * n0, b->u_out + n0, (n1 - n0) * sizeof(double2),
                             cudaMemcpyDeviceToHost, b->copy_stream));
         }
-        for (int c = 0; c < 3; ++c) {
+        for (int c = 0; c < 3; ++c) {  // one strided copy per plane and group
           if (!outs[c]) continue;
-          for (int p = p0; p < p1; ++p)
-            ck(mrb_copy_async(static_cast<char*>(outs[c]) + size_t(p) * npx * os,
-                              static_cast<const char*>(b->dense) + (3 * size_t(p) + c) * npx * os,
-                              npx * os, cudaMemcpyDeviceToHost, b->copy_stream));
+          ck(mrb_copy2d_async(static_cast<char*>(outs[c]) + size_t(p0) * npx * os, npx * os,
+                              static_cast<const char*>(b->dense) + (3 * size_t(p0) + c) * npx * os,
+                              3 * npx * os, npx * os, size_t(p1 - p0), cudaMemcpyDeviceToHost,
+                              b->copy_stream));
         }
       }
       ck(cudaEventRecord(b->group_ev.back(), b->copy_stream));
@@ -2031,7 +2168,11 @@ int mrb_transfer_bytes(int64_t* h2d, int64_t* d2h, int32_t reset) {
 int mrb_batch_phase_profile(mrb_batch* b, long long* out, int64_t n) {
   if (!b->phase_prof) return MRB_E_VALUE;
   const size_t cnt = std::min<size_t>(size_t(n), size_t(b->n_pairs) * b->cluster_cs * 8 * 16);
-  ck(mrb_copy(out, b->phase_prof, cnt * sizeof(long long), cudaMemcpyDeviceToHost));
+  try {
+    ck(mrb_copy(out, b->phase_prof, cnt * sizeof(long long), cudaMemcpyDeviceToHost));
+  } catch (const CudaError& e) {
+    return cuda_fail(b->ctx, e.e);
+  }
   return MRB_OK;
 }
 
@@ -2168,6 +2309,12 @@ int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
   int first_err = MRB_OK;
   std::string first_msg;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> dbg_events;  // run of each chunk
+  std::vector<cudaEvent_t> dbg_done;                             // results of each chunk
+  cudaEvent_t dbg_t0 = nullptr;
+  if (dbg) {
+    cudaEventCreate(&dbg_t0);
+    cudaEventRecord(dbg_t0, ctx->stream);
+  }
   auto harvest = [&](size_t k) {  // wait for chunk k and collect its statuses
     mrb_batch* b = live[k];
     if (!b) return;
@@ -2176,8 +2323,14 @@ int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
     if (dbg && k < dbg_events.size()) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, dbg_events[k].first, dbg_events[k].second);
-      std::fprintf(stderr, "meshreg_b200: many chunk %zu run %.2f ms (path %d x %d)\n", k, ms,
-                   b->cluster_cs, b->cluster_npt);
+      float t_start = 0.f, t_end = 0.f, t_done = 0.f;
+      cudaEventElapsedTime(&t_start, dbg_t0, dbg_events[k].first);
+      cudaEventElapsedTime(&t_end, dbg_t0, dbg_events[k].second);
+      if (k < dbg_done.size()) cudaEventElapsedTime(&t_done, dbg_t0, dbg_done[k]);
+      std::fprintf(stderr,
+                   "meshreg_b200: many chunk %zu run %.2f ms (path %d x %d); device timeline: "
+                   "run %.2f -> %.2f ms, results %.2f ms\n",
+                   k, ms, b->cluster_cs, b->cluster_npt, t_start, t_end, t_done);
     }
     if (rc == MRB_E_CUDA && first_err == MRB_OK) {
       first_err = rc;
@@ -2292,6 +2445,12 @@ int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
         };
         rc = mrb_batch_get_results(b, out_dtype, u ? u + 2 * node_off : nullptr, off(ux), off(uy),
                                    off(warped));
+        if (dbg) {
+          cudaEvent_t e;
+          cudaEventCreate(&e);
+          cudaEventRecord(e, sc->stream);
+          dbg_done.push_back(e);
+        }
       }
       stamp("enqueued", k);
       for (int q = 0; q < P; ++q) node_off += size_t(meshes[p0 + q]->h.n);

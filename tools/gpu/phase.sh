@@ -1,2 +1,1 @@
-timeout 300 python tools/phase_profile.py 8 c4
-timeout 300 python tools/phase_profile.py 1 c2
+MESHREG_B200_DEBUG=1 timeout 300 python tools/phase_profile.py 64 c4 2>&1 | grep -v candidate | tail -25
