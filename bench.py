@@ -349,9 +349,10 @@ def run_ours(args, rank, world, local):
                          "traffic": traffic,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
                          "note": "achieved = SURVEY 8(d) algorithmic bytes per launch / CUDA-event "
-                                 "time; the fast path serves them from SMEM (topology, halo "
-                                 "exchange) and L2 (image taps); traffic = ncu DRAM bytes per "
-                                 "launch (profiles/ncu_traffic.json)"},
+                                 "time; the persistent kernels serve them from SMEM (topology, "
+                                 "halo exchange) and L2 (image taps), so frac can exceed 1: the "
+                                 "DRAM bytes one launch really moves are `traffic` (ncu, "
+                                 "profiles/ncu_traffic.json)"},
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
