@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "pixel"])
+    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "c5", "pixel"])
     ap.add_argument("--pairs", type=int, default=None)
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -315,7 +315,8 @@ def run_ours(args, rank, world, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, pairs[:args.cpu_pairs], spec)
+        cpu = cpu_baseline(args, pairs[:args.cpu_pairs], spec,
+                           iters=CPU_ITERS_CAP.get(args.workload, spec.iterations))
 
     if rank == 0:
         out = {
@@ -441,8 +442,13 @@ def _oracle_register(re, te, V, T, iters):
     return time.perf_counter() - t0, info["iterations_run"]
 
 
-def cpu_baseline(args, pairs, spec):
+# bounded CPU samples: the oracle needs minutes per C5 iteration batch
+CPU_ITERS_CAP = {"c5": 3}
+
+
+def cpu_baseline(args, pairs, spec, iters=None):
     """Oracle port timed single-threaded on this host (rank 0, N=1)."""
+    iters = iters or spec.iterations
     try:
         from threadpoolctl import threadpool_limits
     except ImportError:  # pragma: no cover
@@ -451,7 +457,7 @@ def cpu_baseline(args, pairs, spec):
     ctxm = threadpool_limits(1) if threadpool_limits else None
     try:
         for re, te, V, T, kind, used in pairs:
-            dt, it = _oracle_register(re, te, V, T, spec.iterations)
+            dt, it = _oracle_register(re, te, V, T, iters)
             tot += dt
             work += float(spec.size) ** 2 * it
     finally:
@@ -459,7 +465,7 @@ def cpu_baseline(args, pairs, spec):
             ctxm.unregister() if hasattr(ctxm, "unregister") else None
     return {"value": round(work / tot / 1e6, 4), "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"{len(pairs)} of the workload's pairs (seeds {[p[5] for p in pairs]}), "
-                      f"{spec.size}x{spec.size}, {spec.iterations} iterations each, full register "
+                      f"{spec.size}x{spec.size}, {iters} iterations each, full register "
                       f"(loop + densify + warp + MSD), {tot:.1f} s"}
 
 
@@ -493,7 +499,8 @@ def run_reference(args, rank, world):
     for k in env_bak:
         os.environ[k] = "1"
     ctx = mp.get_context("spawn")
-    it_ref = PIXEL_REF_ITERS if args.workload == "pixel" else spec.iterations
+    it_ref = (PIXEL_REF_ITERS if args.workload == "pixel"
+              else CPU_ITERS_CAP.get(args.workload, spec.iterations))
     procs, conns = [], []
     for i in range(nproc):
         a, b = ctx.Pipe()

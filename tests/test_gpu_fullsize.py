@@ -100,3 +100,42 @@ def test_c4_batch_pairs_match_oracle():
         assert relinf(u, u_ref) < 1e-4
         assert relinf(warped, info["warped"]) < 1e-4
         assert abs(rep.msd_after / info["msd_after"] - 1) < 1e-5
+
+
+def _c5_scale_inputs():
+    """4096x4096 smooth pair with a sub-pixel-to-few-pixel motion and a
+    structured ~500k-node mesh (the C5 node count; the reference mesher needs
+    ~10 h at that size, SURVEY.md §8(f) #3)."""
+    from bench import fallback_mesh
+    S = 4096
+    y, x = np.mgrid[0:S, 0:S].astype(np.float64)
+    base = lambda xx, yy: (0.5 + 0.25 * np.sin(xx / 53.0) * np.cos(yy / 71.0)
+                           + 0.2 * np.exp(-((xx - 1500.0) ** 2 + (yy - 2600.0) ** 2) / 2e5))
+    re = base(x, y).astype(np.float32)
+    te = base(x - 1.7 + 0.5 * np.sin(y / 400.0), y + 1.1).astype(np.float32)
+    V, T = fallback_mesh(S, 500000)
+    return S, re, te, V, T
+
+
+def test_c5_scale_grid_kernel_matches_generic_path(monkeypatch):
+    """At C5 scale (500k nodes, 8 nodes per thread on the whole-GPU grid) the
+    persistent grid kernel and the generic three-kernel loop agree to the fp32
+    tolerance class; the run is deterministic."""
+    S, re32, te32, V, T = _c5_scale_inputs()
+    re = mrb.ImageGrid(S, S, re32.astype(np.float64))
+    te = mrb.ImageGrid(S, S, te32.astype(np.float64))
+    mesh = mrb.TriMesh(V, T)
+    assert mesh.n_vertices >= 490000
+    cfg = mrb.SolverConfig(max_iterations=20, energy_tolerance=0.0)
+    monkeypatch.delenv("MESHREG_B200_PATH", raising=False)
+    a = mrb.register(re, te, mesh, cfg, precision="f32", return_dense=True)
+    b = mrb.register(re, te, mesh, cfg, precision="f32", return_dense=True)
+    monkeypatch.setenv("MESHREG_B200_PATH", "generic")
+    g = mrb.register(re, te, mesh, cfg, precision="f32", return_dense=True)
+    assert np.array_equal(a[0], b[0]) and a[1].energy_trace == b[1].energy_trace
+    assert a[1].iterations_run == g[1].iterations_run == 20
+    assert relinf(a[1].energy_trace, g[1].energy_trace) < 1e-5
+    assert relinf(a[0], g[0]) < 1e-4
+    assert relinf(a[2][2], g[2][2]) < 1e-4  # warped image
+    assert abs(a[1].msd_after / g[1].msd_after - 1) < 1e-5
+    assert a[1].msd_after < a[1].msd_before
