@@ -66,6 +66,10 @@ struct ClusterPair {
   int n, chunk, W, H;
   int topo_stride, slices, halo_stride, pitch;
   int plane;
+  // push exchange (k_cluster_push): per CTA send list, slot << 20 | dst << 16 | halo idx
+  const uint32_t* send;       // [CS][send_stride]
+  const int* n_send;          // [CS]
+  int send_stride;
   // grid path only (k_grid_register): global exchange buffers
   float* xg_s;                // [CS][SLOTS] s_te of every slot
   float2* xg_u;               // [2][CS][SLOTS] smoothing ping-pong

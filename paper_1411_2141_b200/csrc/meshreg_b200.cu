@@ -23,6 +23,7 @@
 #include "../../include/meshreg_b200.h"
 #include "cluster.cuh"
 #include "grid.cuh"
+#include "push.cuh"
 #include "pixel.cuh"
 #include "kernels.cuh"
 #include "mesh_host.h"
@@ -105,7 +106,9 @@ struct DeviceMesh {
     uint32_t* halo = nullptr;
     int* n_halo = nullptr;
     unsigned char* deg = nullptr;
-    int chunk = 0, topo_stride = 0, slices = 0, halo_stride = 0;
+    uint32_t* send = nullptr;
+    int* n_send = nullptr;
+    int chunk = 0, topo_stride = 0, slices = 0, halo_stride = 0, send_stride = 0;
   };
   std::map<int, Topo> topo;  // key: chunk size
   int max_deg = 0;
@@ -564,13 +567,17 @@ void ensure_device_mesh_f64(mrb_ctx* ctx, HostMesh& h) {
 // CTA): SELL-32 slice offsets, halo lists and the code of every one-ring
 // entry.  write_topo() then packs it straight into (pinned) memory.
 struct TopoHost {
-  int chunk = 0, stride = 0, slices = 0, hstride = 0;
-  size_t off[6] = {0, 0, 0, 0, 0, 0};
+  int chunk = 0, stride = 0, slices = 0, hstride = 0, sstride = 0;
+  size_t off[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   size_t total = 0;                  // packed bytes
   std::vector<uint32_t> soff;        // [cs][slices]
   std::vector<uint32_t> halo;        // [cs][hstride]
   std::vector<int> n_halo;           // [cs]
   std::vector<uint16_t> code;        // per one-ring entry (CSR order)
+  // push exchange (cluster kernel): what CTA r sends where, the inverse of the
+  // halo lists: slot << 20 | dst CTA << 16 | dst halo index
+  std::vector<uint32_t> send;        // [cs][sstride]
+  std::vector<int> n_send;           // [cs]
 };
 
 TopoHost plan_topo(const HostMesh& h, int cs, int chunk, int npt) {
@@ -622,16 +629,34 @@ TopoHost plan_topo(const HostMesh& h, int cs, int chunk, int npt) {
     t.n_halo[r] = int(halos[r].size());
     std::copy(halos[r].begin(), halos[r].end(), t.halo.begin() + size_t(r) * t.hstride);
   }
-  const size_t bytes[6] = {size_t(cs) * t.stride * 2, size_t(cs) * t.stride * 8,
-                           t.soff.size() * 4, t.halo.size() * 4, size_t(cs) * 4, size_t(n)};
-  for (int k = 0; k < 6; ++k) {
+  t.n_send.assign(cs, 0);
+  if (cs <= 16 && SLOTS <= 4096) {  // cluster shapes only
+    std::vector<std::vector<uint32_t>> sends(cs);
+    for (int c = 0; c < cs; ++c)
+      for (size_t hh = 0; hh < halos[c].size(); ++hh) {
+        const uint32_t e = halos[c][hh];
+        sends[e >> 16].push_back((e & 0xffffu) << 20 | uint32_t(c) << 16 | uint32_t(hh));
+      }
+    int ss = 2;
+    for (auto& v : sends) ss = std::max<int>(ss, int(v.size()));
+    t.sstride = (ss + 31) / 32 * 32;
+    t.send.assign(size_t(cs) * t.sstride, 0);
+    for (int r = 0; r < cs; ++r) {
+      t.n_send[r] = int(sends[r].size());
+      std::copy(sends[r].begin(), sends[r].end(), t.send.begin() + size_t(r) * t.sstride);
+    }
+  }
+  const size_t bytes[8] = {size_t(cs) * t.stride * 2, size_t(cs) * t.stride * 8,
+                           t.soff.size() * 4, t.halo.size() * 4, size_t(cs) * 4, size_t(n),
+                           t.send.size() * 4, size_t(cs) * 4};
+  for (int k = 0; k < 8; ++k) {
     t.off[k] = t.total;
     t.total += (bytes[k] + 255) / 256 * 256;
   }
   return t;
 }
 
-// packed layout: codes | g | slice_off | halo | n_halo | deg
+// packed layout: codes | g | slice_off | halo | n_halo | deg | send | n_send
 void write_topo(const HostMesh& h, int cs, const TopoHost& t, unsigned char* dst) {
   const int n = int(h.n), chunk = t.chunk;
   uint16_t* codes = reinterpret_cast<uint16_t*>(dst + t.off[0]);
@@ -652,6 +677,8 @@ void write_topo(const HostMesh& h, int cs, const TopoHost& t, unsigned char* dst
   std::memcpy(dst + t.off[2], t.soff.data(), t.soff.size() * 4);
   std::memcpy(dst + t.off[3], t.halo.data(), t.halo.size() * 4);
   std::memcpy(dst + t.off[4], t.n_halo.data(), t.n_halo.size() * 4);
+  std::memcpy(dst + t.off[6], t.send.data(), t.send.size() * 4);
+  std::memcpy(dst + t.off[7], t.n_send.data(), t.n_send.size() * 4);
 }
 
 // device arrays of a packed topology, carved out of one slab
@@ -669,6 +696,9 @@ DeviceMesh::Topo& install_topo(HostMesh& h, int npt, const TopoHost& th,
   t.halo = reinterpret_cast<uint32_t*>(slab + th.off[3]);
   t.n_halo = reinterpret_cast<int*>(slab + th.off[4]);
   t.deg = slab + th.off[5];
+  t.send = reinterpret_cast<uint32_t*>(slab + th.off[6]);
+  t.n_send = reinterpret_cast<int*>(slab + th.off[7]);
+  t.send_stride = th.sstride;
   return h.dev->topo[th.chunk * 16 + npt] = t;
 }
 
@@ -737,6 +767,14 @@ size_t cluster_dyn_smem(int npt, int topo_stride, int slices, int halo_stride, b
   const size_t S = size_t(kClusterThreads) * npt, X = S + halo_stride;
   return S * (sizeof(double2) + sizeof(float2) + sizeof(float) + 1) +
          X * (sizeof(float2) * (two_u ? 2 : 1) + sizeof(float)) + size_t(halo_stride) * 4 +
+         size_t(topo_stride) * (sizeof(float2) + sizeof(uint16_t)) + size_t(slices) * 4;
+}
+
+// bytes of dynamic shared memory of k_cluster_push (PushSmem carve)
+size_t push_dyn_smem(int npt, int topo_stride, int slices, int halo_stride, int send_stride) {
+  const size_t S = size_t(kClusterThreads) * npt, X = S + halo_stride;
+  return S * (sizeof(double2) + sizeof(float2) + sizeof(float) + 1) +
+         2 * X * (sizeof(float2) + sizeof(float)) + size_t(send_stride) * 4 +
          size_t(topo_stride) * (sizeof(float2) + sizeof(uint16_t)) + size_t(slices) * 4;
 }
 
@@ -895,6 +933,8 @@ struct mrb_batch {
   int cluster_cs = 0, cluster_npt = 1;
   int forced_cs = 0, forced_npt = 0;  // shape imposed by mrb_register_many
   bool grid_mode = false;  // k_grid_register (cluster_cs = CTAs of the whole-GPU grid)
+  bool push_mode = false;  // k_cluster_push (smoothing_passes <= 1): push halo exchange
+  size_t push_smem = 0;
   void* xbuf = nullptr;    // grid path exchange buffers (shared by the pairs, run in turn)
   unsigned* xbar = nullptr;  // grid barrier counter + gbad flags [1 + CS]
   // wave groups (mrb_register_many): the first run launches the fast path per
@@ -910,6 +950,7 @@ struct mrb_batch {
   void* cpairs = nullptr;     // ClusterPair[n_pairs]
   std::vector<unsigned char> pairs_host;  // host copy of the PairDev array
   long long* phase_prof = nullptr;  // MESHREG_B200_PROFILE_PHASES
+  long long* prof_host = nullptr;   // ... = "mapped": host pointer of phase_prof
   float2* img_pad = nullptr;  // 4 shifted padded (H+2)x(W+2) (Te, Re) copies per pair
   int runs = 0;
   // host results
@@ -925,7 +966,8 @@ struct mrb_batch {
     }
     void* ptrs[] = {pairs, st, blk_pair, pix_blk_pair, partials, pix_partials, state, traces,
                     img, stage, src_ptrs, img_ptrs, dense, u_out, conv, cpairs, img_pad,
-                    phase_prof, xbuf, xbar};
+                    prof_host ? nullptr : phase_prof, xbuf, xbar};
+    if (prof_host) cudaFreeHost(prof_host);
     for (void* p : ptrs) dev_free(p, ctx ? ctx->stream : nullptr);
   }
 };
@@ -1171,8 +1213,68 @@ int64_t launch_grid(mrb_batch* b, int p0, int np) {
   return np;
 }
 
+template <int NPT>
+int push_occupancy_t(int CS, size_t smem) {
+  auto kern = k_cluster_push<NPT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(unsigned(CS));
+  lc.blockDim = dim3(kClusterThreads);
+  lc.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &lc) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int push_occupancy(int cs, int npt, size_t smem) {
+  return npt == 2 ? push_occupancy_t<2>(cs, smem) : push_occupancy_t<1>(cs, smem);
+}
+
+template <int NPT>
+void launch_push_t(mrb_batch* b, int p0, int np) {
+  const int CS = b->cluster_cs;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(unsigned(np * CS));
+  lc.blockDim = dim3(kClusterThreads);
+  lc.dynamicSmemBytes = b->push_smem;
+  lc.stream = b->ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  ck(cudaLaunchKernelEx(&lc, k_cluster_push<NPT>,
+                        static_cast<const ClusterPair*>(b->cpairs) + p0, b->st + p0,
+                        int(b->cfg.max_iterations), double(b->cfg.energy_tolerance),
+                        float(b->cfg.tau), float(b->cfg.lam), int(b->cfg.smoothing_passes)));
+}
+
 int64_t launch_cluster(mrb_batch* b, int p0, int np) {
   if (b->grid_mode) return launch_grid(b, p0, np);
+  if (b->push_mode) {
+    if (b->cluster_npt == 2)
+      launch_push_t<2>(b, p0, np);
+    else
+      launch_push_t<1>(b, p0, np);
+    return 1;
+  }
   if (b->cluster_npt == 2)
     launch_cluster_t<2>(b, p0, np);
   else
@@ -1464,9 +1566,31 @@ void setup_cluster_path(mrb_batch* b) {
   b->cluster_cs = cs;
   b->cluster_npt = npt;
   b->cluster_smem = smem;
+  // Push exchange in latency mode (one node per thread: few pairs, per-
+  // iteration latency dominates; measured C1 -25%, C2 -18% time).  In
+  // throughput mode (two nodes per thread, a full wave of clusters) the pull
+  // kernel measured faster (C4 8.4 vs 9.5 ms).  MESHREG_B200_EXCHANGE=push|pull
+  // overrides.
+  const char* xenv = std::getenv("MESHREG_B200_EXCHANGE");
+  const bool want_push = xenv ? std::string(xenv) == "push" : npt == 1;
+  if (b->cfg.smoothing_passes <= 1 && want_push) {
+    size_t ps = 0;
+    bool lists = true;
+    for (mrb_mesh* m : b->meshes) {
+      const int chunk = int((m->h.n + cs - 1) / cs);
+      const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, m->h, cs, chunk, npt);
+      lists = lists && t.send_stride > 0;
+      ps = std::max(ps, push_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride,
+                                      t.send_stride));
+    }
+    if (lists && push_occupancy(cs, npt, ps) >= cluster_occupancy_cs(cs, npt, smem)) {
+      b->push_mode = true;
+      b->push_smem = ps;
+    }
+  }
   if (dbg)
-    std::fprintf(stderr, "meshreg_b200: cluster %d CTAs x %d nodes/thread, %zu B smem\n", cs, npt,
-                 smem);
+    std::fprintf(stderr, "meshreg_b200: cluster %d CTAs x %d nodes/thread, %zu B smem, %s exchange\n",
+                 cs, npt, b->push_mode ? b->push_smem : smem, b->push_mode ? "push" : "pull");
   build_fast_descriptors(b);
 }
 
@@ -1495,6 +1619,9 @@ void build_fast_descriptors(mrb_batch* b) {
     c.n_halo = t.n_halo;
     c.halo_stride = t.halo_stride;
     c.deg = t.deg;
+    c.send = t.send;
+    c.n_send = t.n_send;
+    c.send_stride = t.send_stride;
     c.img4 = b->img_pad + 4 * b->pad_plane * p;
     c.tri_of = host[p].tri_of;
     c.tri = host[p].tri;
@@ -1509,8 +1636,17 @@ void build_fast_descriptors(mrb_batch* b) {
     c.prof = nullptr;
     if (std::getenv("MESHREG_B200_PROFILE_PHASES")) {
       if (!b->phase_prof) {
-        b->phase_prof = dalloc<long long>(size_t(b->n_pairs) * cs * 8 * 16);
-        ck(cudaMemset(b->phase_prof, 0, size_t(b->n_pairs) * cs * 8 * 16 * sizeof(long long)));
+        const size_t cnt = size_t(b->n_pairs) * cs * 8 * 16;
+        if (std::string(std::getenv("MESHREG_B200_PROFILE_PHASES")) == "mapped") {
+          // debug: host-mapped, readable while the kernel runs (progress of a hang)
+          ck(cudaHostAlloc(reinterpret_cast<void**>(&b->prof_host), cnt * sizeof(long long),
+                           cudaHostAllocMapped));
+          std::memset(b->prof_host, 0xff, cnt * sizeof(long long));
+          ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&b->phase_prof), b->prof_host, 0));
+        } else {
+          b->phase_prof = dalloc<long long>(cnt);
+          ck(cudaMemset(b->phase_prof, 0, cnt * sizeof(long long)));
+        }
       }
       c.prof = b->phase_prof + size_t(p) * cs * 8 * 16;
     }
@@ -2168,6 +2304,10 @@ int mrb_transfer_bytes(int64_t* h2d, int64_t* d2h, int32_t reset) {
 int mrb_batch_phase_profile(mrb_batch* b, long long* out, int64_t n) {
   if (!b->phase_prof) return MRB_E_VALUE;
   const size_t cnt = std::min<size_t>(size_t(n), size_t(b->n_pairs) * b->cluster_cs * 8 * 16);
+  if (b->prof_host) {  // mapped debug buffer: no CUDA call, usable during a hang
+    std::memcpy(out, const_cast<const long long*>(b->prof_host), cnt * sizeof(long long));
+    return MRB_OK;
+  }
   try {
     ck(mrb_copy(out, b->phase_prof, cnt * sizeof(long long), cudaMemcpyDeviceToHost));
   } catch (const CudaError& e) {

@@ -272,16 +272,20 @@ def test_rises_guard_fp32_and_message_format():
                        "non-finite gradient; reduce the step size tau"), msg
 
 
-@pytest.mark.parametrize("path", ["cluster", "grid", "generic"])
+@pytest.mark.parametrize("path", ["cluster", "push", "pull", "grid", "generic"])
 @pytest.mark.parametrize("name", ["gen64", "gen64_x255", "gen64_p0", "gen64_p2", "c1", "accept_c3"])
 def test_fp32_paths_agree_with_reference(name, path, monkeypatch):
-    """The persistent cluster kernel, the whole-GPU grid kernel (forced here on
-    small meshes; chosen by size for C3/C5) and the generic three-kernel loop
-    all meet the fp32 tolerances."""
+    """The persistent cluster kernel (default exchange, and push / pull halo
+    exchange forced), the whole-GPU grid kernel (forced here on small meshes;
+    chosen by size for C3/C5) and the generic three-kernel loop all meet the
+    fp32 tolerances."""
+    monkeypatch.delenv("MESHREG_B200_EXCHANGE", raising=False)
     if path in ("generic", "grid"):
         monkeypatch.setenv("MESHREG_B200_PATH", path)
     else:
         monkeypatch.delenv("MESHREG_B200_PATH", raising=False)
+        if path in ("push", "pull"):  # cluster kernel with a forced halo exchange
+            monkeypatch.setenv("MESHREG_B200_EXCHANGE", path)
     check_register(golden(name), "f32", name)
 
 
