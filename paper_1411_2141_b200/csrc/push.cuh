@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       for (int o = 16; o > 0; o >>= 1) e2 += __shfl_down_sync(0xffffffffu, e2, o);
       if (lane == 0) s_wpart[warp] = e2;
     }
+    TRACE(7)
     __syncthreads();     // own s_te, warp partials, the decision of k-1
     // Re-arm the u0 barrier of iteration k-1's parity (used again by k+1) only
     // now that every thread has passed its wait: with an empty halo the

@@ -35,7 +35,7 @@ n = P * cs * 8 * 16
 buf = np.zeros(n, np.int64)
 assert lib.mrb_batch_phase_profile(b, buf.ctypes.data, n) == 0
 buf = buf.reshape(P * cs, 8, 16).astype(np.float64)
-order = [(0, "iter start"), (6, "A + sync (incl. control k-1)"), (1, "push s_te"),
+order = [(0, "iter start"), (7, "A (thread 0)"), (6, "sync (all warps, control k-1)"), (1, "push s_te"),
          (2, "wait s_te"), (3, "B + msg + push u0"), (4, "wait u0"), (5, "C (thread 0)")]
 print(f"cluster size {cs}, {P} pairs; mean cycles per phase (iterations 2-6, all CTAs)")
 for (a, _), (b_, name) in zip(order[:-1], order[1:]):
