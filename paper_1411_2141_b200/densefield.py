@@ -9,13 +9,17 @@ and CSV file formats are not on the registration path (out of scope).
 
 from __future__ import annotations
 
+import struct
+
 import numpy as np
 
 from . import _lib
 from .image import ImageGrid
 from .mesh import as_mesh
 
-__all__ = ["DenseField", "MeshCoverageError", "densify", "warp_image", "pixel_map"]
+__all__ = ["DenseField", "MeshCoverageError", "densify", "warp_image", "pixel_map",
+           "FIELD_MAGIC", "FileFormatError", "difference_image", "save_field", "load_field",
+           "save_node_displacements_csv"]
 
 
 class DenseField:
@@ -105,3 +109,66 @@ def pixel_map(mesh, width, height):
     rc = lib.mrb_pixel_map(ctx, mesh._h, int(width), int(height), _lib.ptr(tri_of), _lib.ptr(w))
     _lib.check(rc, ctx, _errs())
     return tri_of, w
+
+
+# ---------------------------------------------------------------------------
+# Output formats beside the path (reference densefield.py:202-251, SURVEY
+# §8(f) row 2): the MRDF binary field and the node-displacement CSV.  Plain
+# host I/O of results the GPU already produced (fp32 planes are written as
+# they come back from the device).
+# ---------------------------------------------------------------------------
+
+FIELD_MAGIC = b"MRDF"
+_HEADER = struct.Struct("<4sIII")  # magic, version, width, height (little-endian)
+
+
+class FileFormatError(ValueError):
+    """Malformed image or field file (reference image.py FileFormatError)."""
+
+
+def difference_image(a, b):
+    """Per-pixel absolute difference image (densefield.py:202-206)."""
+    from .image import ImageGrid
+    if a.shape != b.shape:
+        raise ValueError(f"dimension mismatch: {a.shape} vs {b.shape}")
+    return ImageGrid(a.width, a.height, np.abs(a.data - b.data))
+
+
+def save_field(field, path):
+    """MRDF v1: 16-byte header then the ux and uy planes as row-major
+    little-endian float32 (densefield.py:215-222)."""
+    with open(path, "wb") as fh:
+        fh.write(_HEADER.pack(FIELD_MAGIC, 1, field.width, field.height))
+        fh.write(np.ascontiguousarray(field.ux).astype("<f4").tobytes())
+        fh.write(np.ascontiguousarray(field.uy).astype("<f4").tobytes())
+
+
+def load_field(path):
+    """Read an MRDF v1 file with the reference's checks (densefield.py:225-242)."""
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if len(blob) < _HEADER.size:
+        raise FileFormatError(f"truncated field file {path!r}")
+    magic, version, width, height = _HEADER.unpack_from(blob)
+    if magic != FIELD_MAGIC:
+        raise FileFormatError(f"bad field magic in {path!r}")
+    if version != 1:
+        raise FileFormatError(f"unsupported field version {version} in {path!r}")
+    n = width * height
+    expected = _HEADER.size + 2 * 4 * n
+    if len(blob) != expected:
+        raise FileFormatError(f"field file {path!r} has {len(blob)} bytes, expected {expected}")
+    planes = np.frombuffer(blob, dtype="<f4", offset=_HEADER.size)
+    ux = planes[:n].reshape(height, width).astype(np.float64)
+    uy = planes[n:].reshape(height, width).astype(np.float64)
+    return DenseField(ux, uy)
+
+
+def save_node_displacements_csv(mesh, u, path):
+    """One ``x,y,ux,uy`` row per mesh node, Python float repr
+    (densefield.py:245-251)."""
+    u = np.asarray(u, dtype=np.float64)
+    with open(path, "w", encoding="ascii") as fh:
+        fh.write("x,y,ux,uy\n")
+        for (x, y), (dx, dy) in zip(np.asarray(mesh.vertices, dtype=np.float64), u):
+            fh.write(f"{float(x)!r},{float(y)!r},{float(dx)!r},{float(dy)!r}\n")

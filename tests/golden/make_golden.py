@@ -234,6 +234,20 @@ def main():
         msg = str(exc)
     save("pixel_diverge48", re=ref.data, te=te.data, error=np.array(msg))
 
+    # output formats (densefield.py:215-251): the reference's own MRDF bytes
+    # and node CSV for a small registered field
+    import tempfile
+    from meshreg.densefield import save_field, save_node_displacements_csv
+    g64 = np.load(os.path.join(HERE, "gen64.npz"))
+    fld = mr.DenseField(g64["ux"], g64["uy"])
+    mesh64 = mr.TriMesh(g64["V"], g64["T_in"])
+    with tempfile.TemporaryDirectory() as td:
+        save_field(fld, os.path.join(td, "f.mrdf"))
+        save_node_displacements_csv(mesh64, g64["u"], os.path.join(td, "u.csv"))
+        mrdf = np.frombuffer(open(os.path.join(td, "f.mrdf"), "rb").read(), np.uint8)
+        csv_text = open(os.path.join(td, "u.csv"), encoding="ascii").read()
+    save("formats", mrdf=mrdf, csv=np.array(csv_text))
+
     # full BASELINE config 1 pair (seed 0) on the cached reference mesh
     mpath = os.path.join(ROOT, "data", "meshes", "c1_s0.npz")
     if os.path.exists(mpath):
