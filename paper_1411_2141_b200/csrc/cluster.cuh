@@ -70,6 +70,7 @@ struct ClusterPair {
   const uint32_t* send;       // [CS][send_stride]
   const int* n_send;          // [CS]
   int send_stride;
+  unsigned* flags;            // k_grid_flags: energy-partial counters (zeroed per launch)
   // grid path only (k_grid_register): global exchange buffers
   float* xg_s;                // [CS][SLOTS] s_te of every slot
   float2* xg_u;               // [2][CS][SLOTS] smoothing ping-pong

@@ -306,3 +306,316 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
 }
 
 }  // namespace mrb
+
+namespace mrb {
+
+constexpr int kFlagStride = 32;  // unsigned words between flags (one 128-byte line)
+
+// Epoch-tagged exchange words: a value and the epoch it belongs to in one
+// 8-byte word (single-copy atomic), so a consumer polls the data itself —
+// one L2 round trip instead of flag + data.
+__device__ __forceinline__ void put_tagged(uint2* p, float v, unsigned e) {
+  asm volatile("st.relaxed.gpu.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(__float_as_uint(v)),
+               "r"(e)
+               : "memory");
+}
+__device__ __forceinline__ float get_tagged(const uint2* p, unsigned e) {
+  unsigned v, ep;
+  do {
+    asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(v), "=r"(ep) : "l"(p)
+                 : "memory");
+  } while (ep != e);
+  return __uint_as_float(v);
+}
+
+// Release-store / acquire-load of an epoch flag at gpu scope.
+__device__ __forceinline__ void flag_release(unsigned* f, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned flag_acquire(const unsigned* f) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  return v;
+}
+
+// k_grid_register with the two grid barriers per iteration replaced by
+// epoch-tagged exchange words (smoothing_passes <= 1):
+//   * each published s_te / u0 value carries the epoch k+1 in the same 8-byte
+//     word; a consumer thread polls exactly the halo words it needs until
+//     their epoch matches — no flag, no barrier, one L2 round trip;
+//   * exchange arrays are double-buffered by iteration parity — the halo
+//     relation is symmetric, so no CTA runs more than one iteration ahead of
+//     a CTA that reads it;
+//   * the CTA energy partial + non-finite-gradient flag of iteration k are
+//     published after phase B into buffer k & 3 with a release-increment of
+//     that buffer's counter; the control of iteration k runs one iteration
+//     late (end of k+1), waits until the counter holds all CS contributions
+//     and reduces the CS partials in one fixed order (identical decisions in
+//     every CTA); the decision is read after phase A of k+2, before any CTA
+//     waits on a word of k+2, so all CTAs stop together, and the field is
+//     rolled back to the one the reference returns (u before step k+1).  Four
+//     buffers: a CTA writing buffer k & 3 again at k+4 has waited for all
+//     partials of k+2, so every CTA finished control(k).
+template <int NPT>
+__global__ void __launch_bounds__(kClusterThreads, 1)
+    k_grid_flags(const ClusterPair* __restrict__ pairs, PairStatus* __restrict__ st, int max_iter,
+                 double tol, float tau, float lam, int passes) {
+  constexpr int SLOTS = kClusterThreads * NPT;
+  const int rank = blockIdx.x, CS = gridDim.x;
+  const ClusterPair& d = pairs[0];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  __shared__ int s_stop, s_nhalo;
+  __shared__ double s_hist[6];
+  __shared__ double s_prev;
+  __shared__ double s_wpart[kWarps];
+  __shared__ int s_cs[4];  // rises, iters, err, err_iter
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  const int X = SLOTS + d.halo_stride;
+  float* xs = reinterpret_cast<float*>(s_dyn);
+  float2* xu0 = reinterpret_cast<float2*>(xs + X + (X & 1));
+  uint32_t* halo = reinterpret_cast<uint32_t*>(xu0 + X);
+
+  if (t == 0) {
+    s_stop = 0;
+    s_prev = 0.0;
+    s_cs[0] = s_cs[1] = s_cs[2] = s_cs[3] = 0;
+    s_nhalo = d.n_halo[rank];
+  }
+  for (int q = t; q < d.halo_stride; q += kClusterThreads)
+    halo[q] = d.halo[size_t(rank) * d.halo_stride + q];
+  const uint16_t* code = d.codes + size_t(rank) * d.topo_stride;
+  const float2* gco = d.g + size_t(rank) * d.topo_stride;
+  const uint32_t* soff = d.slice_off + size_t(rank) * d.slices;
+  // one 128-byte line per flag: polled lines are never shared by two flags
+  constexpr int FS = kFlagStride;
+  unsigned* const flag_p = d.flags;  // [4] energy-partial counters, one line each
+  double* const wpart = d.wpart;       // [4][CS] by iteration mod 4
+  int* const gbad = d.gbad;            // [4][CS]
+
+  float2 u[NPT];
+  float2 u_save[NPT];  // u at the start of the previous iteration (deferred control)
+  float r[NPT];
+  unsigned own_mask = 0;
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) {
+    const int slot = t + j * kClusterThreads;
+    own_mask |= unsigned(slot < d.chunk && rank * d.chunk + slot < d.n) << j;
+    u[j] = make_float2(0.f, 0.f);
+    u_save[j] = u[j];
+    r[j] = 0.f;
+  }
+#define OWN(j) ((own_mask >> (j)) & 1u)
+  __syncthreads();
+  const int nhalo = s_nhalo;
+  auto control = [&](int kk) {  // control warp, every CTA identically
+    const int par = kk & 3;
+    // all CS partials of iteration kk: the counter of buffer kk & 3 counts
+    // every CTA's release-increment, so one polled word replaces CS flags
+    const unsigned target = unsigned(CS) * (unsigned(kk >> 2) + 1u);
+    if (lane == 0)
+      while (flag_acquire(flag_p + size_t(par) * FS) < target) __nanosleep(20);
+    __syncwarp();
+    double v = 0.0;
+    int gb = 0;
+    for (int idx = lane; idx < CS; idx += 32) {
+      v += __ldcg(wpart + size_t(par) * CS + idx);
+      gb |= __ldcg(gbad + size_t(par) * CS + idx);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v += __shfl_down_sync(0xffffffffu, v, o);
+      gb |= __shfl_down_sync(0xffffffffu, gb, o);
+    }
+    if (lane == 0 && s_stop == 0) {
+      int stop = 0, rises = s_cs[0], err = ERR_NONE, err_iter = 0;
+      const double en = 0.5 * v;
+      const double prev = s_prev;
+      if (!isfinite(en)) {  // solver.py:176-177
+        err = ERR_NONFINITE_ENERGY;
+        err_iter = kk;
+        stop = 1;
+      } else if (kk > 0 && en > __dadd_rn(__dmul_rn(prev, 1.0 + 1e-4), 1e-12)) {
+        if (++rises >= 10) {  // material_rise, solver.py:43-44,178-184
+          err = ERR_RISES;
+          err_iter = kk;
+          stop = 1;
+        }
+      } else if (kk > 0 && en <= prev) {
+        rises = 0;  // solver.py:185-186
+      }
+      if (!stop && gb) {  // step(): non-finite gradient, solver.py:131-132
+        err = ERR_NONFINITE_GRAD;
+        err_iter = kk;
+        stop = 1;
+      }
+      if (!stop) {
+        s_cs[1] = kk + 1;
+        s_hist[kk % 6] = en;
+        if (kk + 1 >= 6) {  // solver.py:192-195
+          const double base = s_hist[(kk + 1) % 6];
+          if (fabs(__dsub_rn(en, base)) <= __dmul_rn(tol, fmax(fabs(base), 1e-12))) stop = 2;
+        }
+      }
+      if (rank == 0) d.trace[kk] = en;
+      s_prev = en;
+      s_cs[0] = rises;
+      s_cs[2] = err;
+      s_cs[3] = err_iter;
+      s_stop = stop;
+    }
+  };
+
+  int k = 0;
+  for (; k < max_iter; ++k) {
+    const int par = k & 1;
+    const unsigned e = unsigned(k) + 1u;
+    // tagged exchange words: s_te [2][CS][SLOTS], u0 [2][CS][SLOTS][2] (x, y)
+    uint2* xg_s = reinterpret_cast<uint2*>(d.xg_s) + size_t(par) * CS * SLOTS;
+    uint2* xg_u = reinterpret_cast<uint2*>(d.xg_u) + size_t(par) * CS * SLOTS * 2;
+    // -------- phase A: sample Te, Re at V + u; residual; energy partial
+    {
+      double e2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) {
+        if (OWN(j)) {
+          const int slot = t + j * kClusterThreads;
+          const int nd = rank * d.chunk + slot;
+          const double2 V = __ldg(d.V + nd);
+          const Window w = locate(d, V.x + double(u[j].x), V.y + double(u[j].y));
+          float2 tap[4][4];
+#pragma unroll
+          for (int row = 0; row < 4; ++row) ld_row4(w.base + size_t(row) * d.pitch, tap[row]);
+          const float2 s = combine(w, tap);
+          r[j] = s.x - s.y;
+          xs[slot] = s.x;
+          put_tagged(xg_s + size_t(rank) * SLOTS + slot, s.x, e);
+          e2 = fma(double(r[j]), double(r[j]), e2);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) e2 += __shfl_down_sync(0xffffffffu, e2, o);
+      if (lane == 0) s_wpart[warp] = e2;
+    }
+    __syncthreads();   // s_te published by all threads; decision of k-2
+    // Control runs one iteration late (its all-CTA wait is then almost never
+    // on the critical path).  If iteration k-2 ended the reference's loop, the
+    // field it returns is the one before step k-1: restore it.  Identical in
+    // every CTA, so no flag of iteration k is published.
+    if (s_stop) {
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) u[j] = u_save[j];
+      break;
+    }
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) u_save[j] = u[j];
+    for (int h = t; h < nhalo; h += kClusterThreads) {  // the s_te halo, as it arrives
+      const uint32_t c = halo[h];
+      xs[SLOTS + h] = get_tagged(xg_s + size_t(c >> 16) * SLOTS + (c & 0xffffu), e);
+    }
+    __syncthreads();
+    // -------- phase B: gradient via the fused one-ring operator, descent
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+      if (OWN(j)) {
+        const int slot = t + j * kClusterThreads;
+        const int nd = rank * d.chunk + slot;
+        const uint32_t so = __ldg(soff + (slot >> 5)) + (slot & 31);
+        const float si = xs[slot];
+        const float2 gs = __ldg(d.g_self + nd);
+        float gx = gs.x * si, gy = gs.y * si;
+        ring_gather_g(code, gco, so, __ldg(d.deg + nd), [&](uint32_t c, float2 ge) {
+          const float sj = xs[c];
+          gx = fmaf(ge.x, sj, gx);
+          gy = fmaf(ge.y, sj, gy);
+        });
+        const float dx = r[j] * gx, dy = r[j] * gy;  // solver.py:189
+        bad |= !isfinite(dx) || !isfinite(dy);
+        const float2 v = make_float2(u[j].x - tau * dx, u[j].y - tau * dy);  // solver.py:133
+        xu0[slot] = v;
+        uint2* w = xg_u + (size_t(rank) * SLOTS + slot) * 2;
+        put_tagged(w, v.x, e);
+        put_tagged(w + 1, v.y, e);
+      }
+    }
+    const int anybad = __syncthreads_or(bad);  // also: u0 published by all threads
+    if (warp == kCtlWarp) {  // CTA partial + flag of iteration k, then its epoch
+      double v = lane < kWarps ? s_wpart[lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if (lane == 0) {
+        const int q4 = k & 3;
+        __stcg(wpart + size_t(q4) * CS + rank, v);
+        __stcg(gbad + size_t(q4) * CS + rank, anybad);
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(flag_p + size_t(q4) * FS)
+                     : "memory");
+      }
+    }
+    // -------- phase C: umbrella smoothing (one pass) + domain clamp
+    if (passes == 0) {
+#pragma unroll
+      for (int j = 0; j < NPT; ++j)
+        if (OWN(j)) {
+          const int slot = t + j * kClusterThreads;
+          u[j] = clamp_dom(xu0[slot], __ldg(d.V + rank * d.chunk + slot), d.W, d.H);
+        }
+    } else {
+      for (int h = t; h < nhalo; h += kClusterThreads) {  // the u0 halo, as it arrives
+        const uint32_t c = halo[h];
+        const uint2* w = xg_u + (size_t(c >> 16) * SLOTS + (c & 0xffffu)) * 2;
+        xu0[SLOTS + h] = make_float2(get_tagged(w, e), get_tagged(w + 1, e));
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) {
+        if (OWN(j)) {
+          const int slot = t + j * kClusterThreads;
+          const int nd = rank * d.chunk + slot;
+          const uint32_t so = __ldg(soff + (slot >> 5)) + (slot & 31);
+          const float iv = __ldg(d.inv_val + nd);
+          float ax = 0.f, ay = 0.f;
+          ring_gather_g(code, gco, so, __ldg(d.deg + nd), [&](uint32_t c, float2) {
+            const float2 uj = xu0[c];  // (L u)_i, L_ij = 1/val_i
+            ax = fmaf(iv, uj.x, ax);
+            ay = fmaf(iv, uj.y, ay);
+          });
+          const float2 si = xu0[slot];
+          const float om = 1.f - lam;  // (1 - lam) u + lam (L u), mesh.py:281
+          u[j] = clamp_dom(make_float2(om * si.x + lam * ax, om * si.y + lam * ay),
+                           __ldg(d.V + nd), d.W, d.H);
+        }
+      }
+    }
+    if (warp == kCtlWarp && k > 0) control(k - 1);
+  }
+  __syncthreads();
+  if (k == max_iter) {  // the loop ran out: settle the last two decisions
+    if (s_stop) {       // control(max_iter - 2) stopped: undo step max_iter - 1
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) u[j] = u_save[j];
+    } else if (warp == kCtlWarp) {
+      control(k - 1);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) {
+    if (OWN(j)) {
+      const int nd = rank * d.chunk + t + j * kClusterThreads;
+      d.u[nd] = u[j];
+      d.u_out[d.perm[nd]] = make_double2(double(u[j].x), double(u[j].y));
+    }
+  }
+#undef OWN
+  __syncthreads();
+  if (rank == 0 && t == 0) {
+    PairStatus s{};
+    s.stop_iter = k;
+    s.err = s_cs[2];
+    s.err_iter = s_cs[3];
+    s.rises = s_cs[0];
+    s.iters = s_cs[1];
+    st[0] = s;
+  }
+}
+
+}  // namespace mrb

@@ -933,6 +933,8 @@ struct mrb_batch {
   int cluster_cs = 0, cluster_npt = 1;
   int forced_cs = 0, forced_npt = 0;  // shape imposed by mrb_register_many
   bool grid_mode = false;  // k_grid_register (cluster_cs = CTAs of the whole-GPU grid)
+  bool grid_flags = false; // ... with the epoch-tagged exchange (k_grid_flags)
+  size_t xbytes = 0;       // exchange-word bytes of xbuf (zeroed per grid launch)
   bool push_mode = false;  // k_cluster_push (smoothing_passes <= 1): push halo exchange
   size_t push_smem = 0;
   void* xbuf = nullptr;    // grid path exchange buffers (shared by the pairs, run in turn)
@@ -1184,8 +1186,12 @@ int cluster_occupancy_cs(int cs, int npt, size_t smem) {
 template <int NPT>
 void launch_grid_t(mrb_batch* b, int p) {
   cudaStream_t s = b->ctx->stream;
-  // barrier counter and sticky gradient flags start at zero for every pair
-  ck(cudaMemsetAsync(b->xbar, 0, size_t(1 + b->cluster_cs) * sizeof(unsigned), s));
+  // barrier counter, sticky gradient flags / partial counters start at zero
+  // per pair; epoch-tagged exchange words too (a stale word of an earlier
+  // launch must never carry a current epoch)
+  ck(cudaMemsetAsync(b->xbar, 0, (1 + 3 * size_t(b->cluster_cs) * kFlagStride) * sizeof(unsigned),
+                     s));
+  if (b->grid_flags) ck(cudaMemsetAsync(b->xbuf, 0, b->xbytes, s));
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(unsigned(b->cluster_cs));
   lc.blockDim = dim3(kClusterThreads);
@@ -1196,8 +1202,9 @@ void launch_grid_t(mrb_batch* b, int p) {
   attr[0].val.cooperative = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  ck(cudaLaunchKernelEx(&lc, k_grid_register<NPT>, static_cast<const ClusterPair*>(b->cpairs) + p,
-                        b->st + p, int(b->cfg.max_iterations), double(b->cfg.energy_tolerance),
+  ck(cudaLaunchKernelEx(&lc, b->grid_flags ? k_grid_flags<NPT> : k_grid_register<NPT>,
+                        static_cast<const ClusterPair*>(b->cpairs) + p, b->st + p,
+                        int(b->cfg.max_iterations), double(b->cfg.energy_tolerance),
                         float(b->cfg.tau), float(b->cfg.lam), int(b->cfg.smoothing_passes)));
 }
 
@@ -1663,15 +1670,21 @@ void build_fast_descriptors(mrb_batch* b) {
     c.wpart = nullptr;
     c.gbad = nullptr;
     c.bar = nullptr;
+    c.flags = nullptr;
     if (b->grid_mode) {  // exchange buffers shared by the pairs (launched in turn)
       const size_t slots = size_t(cs) * kClusterThreads * b->cluster_npt;
       char* x = static_cast<char*>(b->xbuf);
       c.xg_s = reinterpret_cast<float*>(x);
-      c.xg_u = reinterpret_cast<float2*>(x + (slots * 4 + 255) / 256 * 256);
+      c.xg_u = reinterpret_cast<float2*>(x + (2 * slots * 8 + 255) / 256 * 256);
       c.wpart = reinterpret_cast<double*>(reinterpret_cast<char*>(c.xg_u) +
-                                          (2 * slots * 8 + 255) / 256 * 256);
+                                          (2 * slots * 16 + 255) / 256 * 256);
       c.bar = b->xbar;
-      c.gbad = reinterpret_cast<int*>(b->xbar + 1);
+      if (b->grid_flags) {
+        c.flags = b->xbar + 1;
+        c.gbad = reinterpret_cast<int*>(b->xbar + 1 + 3 * size_t(cs) * kFlagStride);
+      } else {
+        c.gbad = reinterpret_cast<int*>(b->xbar + 1);
+      }
     }
   }
   b->cpairs = aupload(b->ctx, cp.data(), cp.size());
@@ -1705,20 +1718,36 @@ void setup_grid_path(mrb_batch* b, int64_t nmax) {
     }
     return per_sm;
   };
-  const int per_sm = npt == 1 ? fit(k_grid_register<1>) : npt == 2 ? fit(k_grid_register<2>)
-                     : npt == 4 ? fit(k_grid_register<4>) : fit(k_grid_register<8>);
+  // epoch-tagged exchange (no grid barrier) for at most one smoothing pass;
+  // MESHREG_B200_GRID_SYNC=barrier keeps the barrier kernel
+  const char* genv = std::getenv("MESHREG_B200_GRID_SYNC");
+  bool flags = b->cfg.smoothing_passes <= 1 && !(genv && std::string(genv) == "barrier");
+  int per_sm = 0;
+  if (flags)
+    per_sm = npt == 1 ? fit(k_grid_flags<1>) : npt == 2 ? fit(k_grid_flags<2>)
+             : npt == 4 ? fit(k_grid_flags<4>) : fit(k_grid_flags<8>);
+  if (per_sm < 1) {
+    flags = false;
+    per_sm = npt == 1 ? fit(k_grid_register<1>) : npt == 2 ? fit(k_grid_register<2>)
+             : npt == 4 ? fit(k_grid_register<4>) : fit(k_grid_register<8>);
+  }
   if (per_sm < 1) return;
   b->grid_mode = true;
+  b->grid_flags = flags;
   b->cluster_cs = cs;
   b->cluster_npt = npt;
   b->cluster_smem = smem;
+  // exchange arrays: s_te [2][slots] x 8 B (epoch-tagged words; the barrier
+  // kernel uses floats), u [2][slots] x 16 B (tagged x, y; barrier kernel:
+  // u0/u1 float2), energy partials [4][CS]; xbar: barrier counter, the
+  // partial counters (one line each) and gradient flags [4][CS]
   const size_t slots = size_t(cs) * kClusterThreads * npt;
-  b->xbuf = dalloc<char>((slots * 4 + 255) / 256 * 256 + (2 * slots * 8 + 255) / 256 * 256 +
-                         size_t(2) * cs * kWarps * 8);
-  b->xbar = dalloc<unsigned>(1 + size_t(cs));
+  b->xbytes = (2 * slots * 8 + 255) / 256 * 256 + (2 * slots * 16 + 255) / 256 * 256;
+  b->xbuf = dalloc<char>(b->xbytes + size_t(4) * cs * kWarps * 8);
+  b->xbar = dalloc<unsigned>(1 + 3 * size_t(cs) * kFlagStride + 4 * size_t(cs));
   if (std::getenv("MESHREG_B200_DEBUG"))
-    std::fprintf(stderr, "meshreg_b200: grid %d CTAs x %d nodes/thread, %zu B smem\n", cs, npt,
-                 smem);
+    std::fprintf(stderr, "meshreg_b200: grid %d CTAs x %d nodes/thread, %zu B smem, %s\n", cs,
+                 npt, smem, flags ? "epoch-tagged exchange" : "grid barriers");
   build_fast_descriptors(b);
 }
 
