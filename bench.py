@@ -284,6 +284,7 @@ def run_ours(args, rank, world, local):
     value = pairqueue.job_throughput(work * args.steps, t_ms / 1e3, world)
     launches = int(lib.mrb_batch_launches_per_run(batch)) * args.steps
     path_cs = int(lib.mrb_batch_path(batch))
+    loop_kernel = lib.mrb_batch_loop_kernel(batch).decode()
     alg_bytes = lib.mrb_batch_algorithmic_bytes(batch)
     lib.mrb_batch_destroy(batch)
 
@@ -296,8 +297,7 @@ def run_ours(args, rank, world, local):
     n_launch = {0: iters, 1: iters, 2: iters, 3: 1}
     share = {k: ktimes[k] * n_launch[k] for k in range(4)}
     dom = max(share, key=share.get)
-    fast_name = "k_grid_register" if path_cs < 0 else "k_cluster_register"
-    names = {0: fast_name if path_cs else "k_sample", 1: "k_grad", 2: "k_smooth",
+    names = {0: loop_kernel, 1: "k_grad", 2: "k_smooth",
              3: "k_dense"}
     if path_cs:
         n_launch = {0: 1, 1: 0, 2: 0, 3: 1}
@@ -338,9 +338,10 @@ def run_ours(args, rank, world, local):
                 "precision": args.precision,
             },
             "gpu_launches": launches,
-            "path": (f"persistent cluster kernel (cluster of {path_cs} CTAs per pair)" if path_cs > 0
-                     else f"whole-GPU persistent grid kernel ({-path_cs} CTAs, one cooperative "
-                          "launch per pair)" if path_cs < 0
+            "path": (f"persistent cluster kernel {loop_kernel} (cluster of {path_cs} CTAs per pair)"
+                     if path_cs > 0
+                     else f"whole-GPU persistent grid kernel {loop_kernel} ({-path_cs} CTAs, one "
+                          "cooperative launch per pair)" if path_cs < 0
                      else "generic 3-kernel loop (CUDA graph)"),
             "kernel_ms": {names[k]: round(float(ktimes[k]), 5) for k in range(4)},
             # device ms per descent iteration of the whole batch (loop only)

@@ -158,6 +158,10 @@ int mrb_batch_pair_status(mrb_batch* batch, int32_t pair, int32_t* iterations_ru
  * nodes); < 0 = minus the CTA count of the whole-GPU persistent grid kernel
  * (fp32, larger meshes, one cooperative launch per pair) */
 int32_t mrb_batch_path(const mrb_batch* batch);
+/* name of the kernel that runs the descent loop: "k_cluster_register" (pull
+ * halo exchange), "k_cluster_push" (push exchange), "k_grid_flags" /
+ * "k_grid_register" (whole-GPU grid), "k_sample" (generic three-kernel loop) */
+const char* mrb_batch_loop_kernel(const mrb_batch* batch);
 /* debug: per-CTA phase timestamps of the cluster kernel (first 8 iterations,
  * 16 slots each) when MESHREG_B200_PROFILE_PHASES is set at batch creation */
 int mrb_batch_phase_profile(mrb_batch* batch, long long* out, int64_t n);

@@ -69,6 +69,7 @@ _SIGS = {
                                     C.POINTER(mrb_config), _i32, _i32, _vp, _vp, _vp, _vp, _vp,
                                     _vp, _vp, _vp, _vp, C.c_char_p, _i32]),
     "mrb_batch_path": (_i32, [_vp]),
+    "mrb_batch_loop_kernel": (C.c_char_p, [_vp]),
     "mrb_transfer_bytes": (C.c_int, [_vp, _vp, _i32]),
     "mrb_batch_phase_profile": (C.c_int, [_vp, _vp, _i64]),
     "mrb_batch_launches_per_run": (_i64, [_vp]),

@@ -2315,6 +2315,12 @@ int mrb_batch_pair_status(mrb_batch* b, int32_t p, int32_t* iters, double* msd_b
 
 int64_t mrb_batch_launches_per_run(const mrb_batch* b) { return launches_per_run(b); }
 
+const char* mrb_batch_loop_kernel(const mrb_batch* b) {
+  if (!b->cluster_cs) return "k_sample";
+  if (b->grid_mode) return b->grid_flags ? "k_grid_flags" : "k_grid_register";
+  return b->push_mode ? "k_cluster_push" : "k_cluster_register";
+}
+
 int32_t mrb_batch_path(const mrb_batch* b) {
   return b->grid_mode ? -b->cluster_cs : b->cluster_cs;
 }
