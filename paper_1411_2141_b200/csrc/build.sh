@@ -6,7 +6,7 @@ set -e
 HERE=$(cd "$(dirname "$0")" && pwd)
 OUT=${1:-$HERE/../libmeshreg_b200.so}
 NVCC=${NVCC:-nvcc}
-$NVCC -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a \
+$NVCC -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a $MRB_NVCC_FLAGS \
   -Xcompiler -fPIC,-ffp-contract=off -Xptxas -v -shared \
   -I"$HERE/../../include" \
   "$HERE/meshreg_b200.cu" "$HERE/mesh_host.cpp" -o "$OUT.tmp" 2> "$HERE/../../build_ptxas.log" || {
