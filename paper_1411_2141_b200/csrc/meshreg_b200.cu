@@ -718,6 +718,59 @@ const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, i
 
 // topologies of many meshes: built on a host thread pool, uploaded through
 // the pinned staging buffer
+// Topologies of many meshes in two halves.  plan_cluster_topos plans them on
+// the host thread pool, allocates one shared device slab and installs every
+// topology's device pointers (so descriptors can be built at once); the data
+// is packed straight into the pinned staging buffer and copied by
+// upload_cluster_topos, all at once or (mrb_register_many) one wave group at
+// a time, ahead of that group's launch.
+struct TopoUpload {
+  std::vector<HostMesh*> meshes;
+  std::vector<TopoHost> th;
+  std::vector<size_t> base;
+  int cs = 0;
+  unsigned char* stage = nullptr;  // pinned, ctx->pinned[1]
+  unsigned char* dev = nullptr;    // shared slab
+};
+
+TopoUpload plan_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, int cs, int npt) {
+  TopoUpload up;
+  up.meshes = todo;
+  up.cs = cs;
+  up.th.resize(todo.size());
+  parallel_for(todo.size(), [&](size_t i) {
+    const HostMesh& h = *todo[i];
+    up.th[i] = plan_topo(h, cs, int((h.n + cs - 1) / cs), npt);
+  });
+  size_t total = 0;
+  up.base.resize(todo.size());
+  for (size_t i = 0; i < todo.size(); ++i) {
+    up.base[i] = total;
+    total += up.th[i].total;
+  }
+  up.stage = static_cast<unsigned char*>(pinned_stage(ctx, std::max<size_t>(total, 1), 1));
+  AllocScope scope(ctx->stream);
+  const std::shared_ptr<unsigned char> all = shared_slab(std::max<size_t>(total, 1), ctx->stream);
+  up.dev = all.get();
+  for (size_t i = 0; i < todo.size(); ++i)
+    install_topo(*todo[i], npt, up.th[i], all.get() + up.base[i]).hold = all;
+  return up;
+}
+
+// pack meshes [i0, i1) of an upload and copy them on `stream` (one copy)
+void upload_cluster_topos(mrb_ctx* ctx, const TopoUpload& up, size_t i0, size_t i1,
+                          cudaStream_t stream) {
+  if (i0 >= i1) return;
+  parallel_for(i1 - i0, [&](size_t k) {
+    const size_t i = i0 + k;
+    write_topo(*up.meshes[i], up.cs, up.th[i], up.stage + up.base[i]);
+  });
+  const size_t b0 = up.base[i0];
+  const size_t b1 = i1 < up.meshes.size() ? up.base[i1] : up.base.back() + up.th.back().total;
+  ck(mrb_copy_async(up.dev + b0, up.stage + b0, b1 - b0, cudaMemcpyHostToDevice, stream));
+  ck(cudaEventRecord(ctx->stage_done[1], stream));  // staging reusable after this
+}
+
 void ensure_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int cs, int npt) {
   std::vector<HostMesh*> todo;
   for (HostMesh* h : meshes) {
@@ -736,30 +789,10 @@ void ensure_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, in
                  std::chrono::duration<double, std::milli>(t1 - t0).count());
     t0 = t1;
   };
-  std::vector<TopoHost> th(todo.size());
-  parallel_for(todo.size(), [&](size_t i) {
-    const HostMesh& h = *todo[i];
-    th[i] = plan_topo(h, cs, int((h.n + cs - 1) / cs), npt);
-  });
+  TopoUpload up = plan_cluster_topos(ctx, todo, cs, npt);
   tick("host plan");
-  size_t total = 0;
-  std::vector<size_t> base(todo.size());
-  for (size_t i = 0; i < todo.size(); ++i) {
-    base[i] = total;
-    total += th[i].total;
-  }
-  unsigned char* stage = static_cast<unsigned char*>(pinned_stage(ctx, total, 1));
-  tick("stage wait");
-  parallel_for(todo.size(), [&](size_t i) { write_topo(*todo[i], cs, th[i], stage + base[i]); });
-  tick("stage fill");
-  AllocScope scope(ctx->stream);
-  // one allocation, one copy; each mesh's topology is a slice (shared owner)
-  const std::shared_ptr<unsigned char> all = shared_slab(total, ctx->stream);
-  ck(mrb_copy_async(all.get(), stage, total, cudaMemcpyHostToDevice, ctx->stream));
-  for (size_t i = 0; i < todo.size(); ++i)
-    install_topo(*todo[i], npt, th[i], all.get() + base[i]).hold = all;
-  ck(cudaEventRecord(ctx->stage_done[1], ctx->stream));
-  tick("copies issued");
+  upload_cluster_topos(ctx, up, 0, up.meshes.size(), ctx->stream);
+  tick("fill + copy");
 }
 
 // bytes of dynamic shared memory of k_cluster_register (ClusterSmem carve)
@@ -943,6 +976,13 @@ struct mrb_batch {
   // group of pairs and records group_ev[g]; get_results then copies group g
   // back on copy_stream while later groups still compute
   std::vector<int> groups;  // pair boundaries, size G + 1 (empty: one launch)
+  // deferred topology upload (mrb_register_many): planned at creation, data
+  // packed and copied one wave group at a time ahead of that group's launch
+  std::unique_ptr<TopoUpload> topo_up;
+  std::map<const HostMesh*, size_t> topo_index;  // mesh -> position in topo_up
+  size_t topo_done = 0;                           // meshes of topo_up uploaded
+  cudaEvent_t topo_ev = nullptr;
+  std::vector<cudaEvent_t> dbg_group_ev;  // MESHREG_B200_DEBUG: start of each group launch
   std::vector<cudaEvent_t> group_ev;
   cudaStream_t copy_stream = nullptr;
   bool groups_recorded = false;
@@ -962,6 +1002,7 @@ struct mrb_batch {
   ~mrb_batch() {
     if (graph) cudaGraphExecDestroy(graph);
     for (cudaEvent_t e : group_ev) cudaEventDestroy(e);
+    if (topo_ev) cudaEventDestroy(topo_ev);
     if (copy_stream) {
       cudaStreamSynchronize(copy_stream);
       cudaStreamDestroy(copy_stream);
@@ -1289,6 +1330,25 @@ int64_t launch_cluster(mrb_batch* b, int p0, int np) {
   return 1;
 }
 
+// Deferred topologies (mrb_register_many): pack and copy, on `copy`, the
+// meshes pairs [0, p1) need and make `s` wait for them.
+void flush_topo(mrb_batch* b, int p1, cudaStream_t copy, cudaStream_t s) {
+  if (!b->topo_up) return;
+  size_t need = b->topo_done;
+  for (int p = 0; p < p1; ++p) {
+    auto it = b->topo_index.find(&b->meshes[p]->h);
+    if (it != b->topo_index.end()) need = std::max(need, it->second + 1);
+  }
+  if (need <= b->topo_done) return;
+  upload_cluster_topos(b->ctx, *b->topo_up, b->topo_done, need, copy);
+  b->topo_done = need;
+  if (copy != s) {
+    if (!b->topo_ev) ck(cudaEventCreateWithFlags(&b->topo_ev, cudaEventDisableTiming));
+    ck(cudaEventRecord(b->topo_ev, copy));
+    ck(cudaStreamWaitEvent(s, b->topo_ev, 0));
+  }
+}
+
 template <typename TapT, typename Real>
 int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
   KernelTimer dummy;
@@ -1317,6 +1377,14 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
           const int p0 = b->groups[g], p1 = b->groups[g + 1];
           const int blk0 = host[p0].pix_blk_begin;
           const int blk1 = p1 < b->n_pairs ? host[p1].pix_blk_begin : b->n_pix_blocks;
+          // this group's topologies (host packing overlaps the previous group)
+          flush_topo(b, p1, b->copy_stream, s);
+          if (std::getenv("MESHREG_B200_DEBUG")) {  // device timeline of the groups
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            cudaEventRecord(e, s);
+            b->dbg_group_ev.push_back(e);
+          }
           launches += launch_cluster(b, p0, p1 - p0);
           k_dense_fast<<<blk1 - blk0, kPixBlock, 0, s>>>(static_cast<const ClusterPair*>(b->cpairs),
                                                          b->st, b->pix_blk_pair, b->pix_partials,
@@ -1330,6 +1398,7 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
         ck(cudaGetLastError());
         return launches;
       }
+      flush_topo(b, b->n_pairs, s, s);  // deferred topologies not yet uploaded
       tm->mark(-1);
       launches += launch_cluster(b, 0, b->n_pairs);
       tm->mark(0);
@@ -2002,7 +2071,10 @@ namespace {
 // mrb_batch_create with an optional imposed cluster shape (forced_cs > 0)
 int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int32_t W,
                       int32_t H, int32_t img_dtype, const mrb_config* cfg, int forced_cs,
-                      int forced_npt, mrb_batch** out) {
+                      int forced_npt, mrb_batch** out, int defer_topo = 0) {
+  // defer_topo > 0: topologies are planned here, the first `defer_topo` pairs'
+  // data uploaded here too (they gate the first launch), the rest per wave
+  // group by the run (flush_topo)
   *out = nullptr;
   const std::string ce = config_error(cfg);
   if (!ce.empty()) return fail(ctx, MRB_E_VALUE, ce);
@@ -2072,8 +2144,24 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
       if (mode == 2)
         grid_shape(big->h.n, &cs, &npt);
       if (cs || choose_cluster_shape(ctx, big->h, n_pairs, cfg->smoothing_passes >= 2, &cs, &npt,
-                                     &occ))
-        ensure_cluster_topos(ctx, hm, cs, npt);
+                                     &occ)) {
+        if (defer_topo && mode == 1) {  // plan now, pack + copy per wave group in the run
+          std::vector<HostMesh*> todo;
+          for (HostMesh* h : hm) {
+            const int chunk = int((h->n + cs - 1) / cs);
+            if (!h->dev->topo.count(chunk * 16 + npt) &&
+                std::find(todo.begin(), todo.end(), h) == todo.end())
+              todo.push_back(h);
+          }
+          if (!todo.empty()) {
+            b->topo_up.reset(new TopoUpload(plan_cluster_topos(ctx, todo, cs, npt)));
+            for (size_t i = 0; i < todo.size(); ++i) b->topo_index[todo[i]] = i;
+            flush_topo(b.get(), std::min(defer_topo, n_pairs), ctx->stream, ctx->stream);
+          }
+        } else {
+          ensure_cluster_topos(ctx, hm, cs, npt);
+        }
+      }
       tick("topologies");
     }
     const std::string msg = finish_pixel_maps(ctx, pmj);
@@ -2506,6 +2594,11 @@ int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
                    "meshreg_b200: many chunk %zu run %.2f ms (path %d x %d); device timeline: "
                    "run %.2f -> %.2f ms, results %.2f ms\n",
                    k, ms, b->cluster_cs, b->cluster_npt, t_start, t_end, t_done);
+      for (size_t g = 0; g < b->dbg_group_ev.size(); ++g) {
+        float tg = 0.f;
+        cudaEventElapsedTime(&tg, dbg_t0, b->dbg_group_ev[g]);
+        std::fprintf(stderr, "meshreg_b200:   group %zu launch reached at %.2f ms\n", g, tg);
+      }
     }
     if (rc == MRB_E_CUDA && first_err == MRB_OK) {
       first_err = rc;
@@ -2585,8 +2678,9 @@ int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
       }
       mrb_batch* b = nullptr;
       stamp("create begin", k);
+      const bool grouped = wave > 0 && P > wave && !std::getenv("MESHREG_B200_NO_GROUPS");
       int rc = batch_create_impl(sc, P, meshes + p0, W, H, img_dtype, cfg, forced_cs, forced_npt,
-                                 &b);
+                                 &b, grouped && !std::getenv("MESHREG_B200_NO_DEFER") ? wave : 0);
       stamp("create end", k);
       if (rc == MRB_OK && k == 0) {
         cs = b->cluster_cs;
@@ -2596,7 +2690,7 @@ int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
         cudaStreamWaitEvent(sc->stream, ctx->copy_done, 0);
         rc = mrb_batch_set_images(b, dimg, dimg + img_bytes, 1);
       }
-      if (rc == MRB_OK && wave > 0 && !std::getenv("MESHREG_B200_NO_GROUPS")) {
+      if (rc == MRB_OK && grouped) {
         try {
           batch_set_groups(b, wave);
         } catch (const CudaError& e) {

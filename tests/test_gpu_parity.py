@@ -340,3 +340,35 @@ def test_pipelined_batch_chunks_and_per_pair_errors(precision):
         assert np.array_equal(warped, w1) and np.array_equal(ux, ux1)
     # identical inputs give identical results (determinism across chunks/streams)
     assert np.array_equal(out[0][0], out[3][0]) and np.array_equal(out[1][0], out[4][0])
+
+
+def test_register_batch_wave_groups_deferred_topologies(monkeypatch):
+    """More pairs than one wave of clusters: mrb_register_many launches per
+    wave group, uploads each group's topologies just ahead of its launch and
+    copies results back per group.  Bit-identical to one launch of the same
+    batch, and to the oracle within the fp32 tolerance."""
+    names = ["gen64", "gen64_x255", "plateau64"]
+    gs = [golden(n) for n in names]
+    P = 300  # small meshes: one wave holds ~150 clusters
+    res, tes, meshes, which = [], [], [], []
+    for i in range(P):
+        g = gs[i % 3]
+        r, t = images(g)
+        res.append(r)
+        tes.append(t)
+        meshes.append(mrb.TriMesh(g["V"], g["T_in"]))  # distinct mesh objects
+        which.append(i % 3)
+    cfg = mrb.SolverConfig(tau=0.001, max_iterations=20, energy_tolerance=0.0)
+    out = mrb.register_batch(res, tes, meshes, cfg, precision="f32", return_dense=True)
+    monkeypatch.setenv("MESHREG_B200_NO_GROUPS", "1")
+    meshes2 = [mrb.TriMesh(gs[k]["V"], gs[k]["T_in"]) for k in which]
+    ref = mrb.register_batch(res, tes, meshes2, cfg, precision="f32", return_dense=True)
+    for i, (o, r) in enumerate(zip(out, ref)):
+        assert np.array_equal(o[0], r[0]), i
+        assert o[1].energy_trace == r[1].energy_trace
+        assert all(np.array_equal(a, b) for a, b in zip(o[2], r[2]))
+    for k in range(3):  # and the oracle
+        g = gs[k]
+        u_ref, info = O.register(g["re"], g["te"], O.Mesh(g["V"], g["T_in"]), tau=0.001, lam=0.8,
+                                 max_iterations=20, smoothing_passes=1, energy_tolerance=0.0)
+        assert np.abs(out[k][0] - u_ref).max() <= 1e-4 * max(np.abs(u_ref).max(), 1e-30)
