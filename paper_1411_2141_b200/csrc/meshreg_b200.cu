@@ -1003,6 +1003,7 @@ struct mrb_batch {
     if (graph) cudaGraphExecDestroy(graph);
     for (cudaEvent_t e : group_ev) cudaEventDestroy(e);
     if (topo_ev) cudaEventDestroy(topo_ev);
+    for (cudaEvent_t e : dbg_group_ev) cudaEventDestroy(e);
     if (copy_stream) {
       cudaStreamSynchronize(copy_stream);
       cudaStreamDestroy(copy_stream);
@@ -2739,6 +2740,12 @@ int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
   }
   for (size_t j = 0; j < live.size(); ++j) harvest(j);
   cudaEventDestroy(setup_done);
+  for (auto& e : dbg_events) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  for (cudaEvent_t e : dbg_done) cudaEventDestroy(e);
+  if (dbg_t0) cudaEventDestroy(dbg_t0);
   if (first_err != MRB_OK) return fail(ctx, first_err, first_msg);
   return MRB_OK;
 }
