@@ -278,6 +278,7 @@ std::string build_mesh(int64_t n, const double* Vin, int64_t m, const int64_t* T
   for (int64_t k = 0; k < n; ++k) {
     const int64_t i = M.perm[k];
     M.nb_ptr[k + 1] = M.nb_ptr[k] + int32_t(M.valence[i]);
+    M.max_deg = std::max(M.max_deg, int32_t(M.valence[i]));
   }
   for (int64_t k = 0; k < n; ++k) {
     const int64_t i = M.perm[k];

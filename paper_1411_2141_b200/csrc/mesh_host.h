@@ -42,6 +42,7 @@ struct HostMesh {
   std::vector<double> inv_val; // n     1/valence (Laplacian row value)
   std::vector<double> Vn;      // n*2   vertices in new order
   std::vector<int32_t> Tn;     // m*4   triangles in new ids (+pad)
+  int32_t max_deg = 0;         // largest one-ring (fast-path eligibility)
 
   std::unique_ptr<DeviceMesh> dev;  // lazily created per device
   ~HostMesh();

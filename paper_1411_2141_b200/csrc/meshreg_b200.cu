@@ -504,8 +504,7 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, bo
     d.perm = reinterpret_cast<int*>(slab + pl.off[4]);
     d.g_self_f = reinterpret_cast<float2*>(slab + pl.off[5]);
     d.inv_val_f = reinterpret_cast<float*>(slab + pl.off[7]);
-    for (int64_t k = 0; k < h.n; ++k)
-      d.max_deg = std::max(d.max_deg, h.nb_ptr[k + 1] - h.nb_ptr[k]);
+    d.max_deg = h.max_deg;
   }
   ck(cudaEventRecord(ctx->stage_done[0], ctx->stream));  // staging buffer reusable after this
   tick("copies issued");
@@ -1570,9 +1569,7 @@ int fast_mode(bool real_d, bool tap_d, int in_dtype, const std::vector<mrb_mesh*
   int64_t nmax = 0;
   for (mrb_mesh* m : meshes) {
     nmax = std::max<int64_t>(nmax, m->h.n);
-    int md = 0;
-    for (int64_t k = 0; k < m->h.n; ++k) md = std::max(md, m->h.nb_ptr[k + 1] - m->h.nb_ptr[k]);
-    if (md > kMaxDeg) return (*why = "one-ring larger than kMaxDeg"), 0;
+    if (m->h.max_deg > kMaxDeg) return (*why = "one-ring larger than kMaxDeg"), 0;
   }
   if (path != "grid" && nmax <= 16 * 2 * kClusterThreads) return 1;
   if (nmax <= int64_t(device_sms()) * kClusterThreads * kGridMaxNpt) return 2;
