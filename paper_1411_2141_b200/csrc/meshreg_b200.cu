@@ -1553,11 +1553,17 @@ int device_sms() {
 }
 
 constexpr int kGridMaxNpt = 8;
+// A single pair with at least this many nodes runs faster on the whole-GPU
+// grid than on one 16-CTA cluster (measured: C2, 12k nodes, 0.79 vs 0.98 ms;
+// C1, 3k nodes, 0.43 vs 0.28 ms).
+constexpr int64_t kGridSinglePairNodes = 6000;
 
 // Fast-path mode of a batch: 1 = thread-block cluster per pair (every mesh
 // fits 16 CTAs x 768 x 2 nodes), 2 = whole-GPU grid per pair (larger meshes,
-// up to SMs x 768 x 8 nodes), 0 = generic path (*why says why).  Both fast
-// modes need fp32 state and images and one-rings within kMaxDeg.
+// up to SMs x 768 x 8 nodes, and a single pair of >= kGridSinglePairNodes),
+// 0 = generic path (*why says why).  Both fast modes need fp32 state and
+// images and one-rings within kMaxDeg.  MESHREG_B200_PATH=cluster|grid|generic
+// forces a mode.
 int fast_mode(bool real_d, bool tap_d, int in_dtype, const std::vector<mrb_mesh*>& meshes,
               const char** why) {
   const char* env = std::getenv("MESHREG_B200_PATH");
@@ -1571,7 +1577,9 @@ int fast_mode(bool real_d, bool tap_d, int in_dtype, const std::vector<mrb_mesh*
     nmax = std::max<int64_t>(nmax, m->h.n);
     if (m->h.max_deg > kMaxDeg) return (*why = "one-ring larger than kMaxDeg"), 0;
   }
-  if (path != "grid" && nmax <= 16 * 2 * kClusterThreads) return 1;
+  const bool single_big = meshes.size() == 1 && nmax >= kGridSinglePairNodes;
+  if (path == "cluster" || (path != "grid" && !single_big))
+    if (nmax <= 16 * 2 * kClusterThreads) return 1;
   if (nmax <= int64_t(device_sms()) * kClusterThreads * kGridMaxNpt) return 2;
   return (*why = "mesh larger than the whole-GPU grid holds"), 0;
 }

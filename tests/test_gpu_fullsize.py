@@ -33,8 +33,15 @@ def relinf(a, b):
     return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-30))
 
 
-@pytest.mark.parametrize("cfg,x255", [("c2", False), ("c2", True), ("c3", False)])
-def test_full_size_matches_oracle(cfg, x255):
+@pytest.mark.parametrize("cfg,x255,path", [("c2", False, ""), ("c2", True, ""), ("c3", False, ""),
+                                           ("c2", False, "cluster"), ("c2", True, "cluster")])
+def test_full_size_matches_oracle(cfg, x255, path, monkeypatch):
+    """Default path (a single C2/C3 pair runs on the whole-GPU grid kernel)
+    and the cluster kernel forced, against the live oracle."""
+    if path:
+        monkeypatch.setenv("MESHREG_B200_PATH", path)
+    else:
+        monkeypatch.delenv("MESHREG_B200_PATH", raising=False)
     spec, re32, te32, V, T = load(cfg, 0, x255)
     iters = spec.iterations if cfg != "c3" else 100
     u_ref, info = O.register(re32, te32, O.Mesh(V, T), tau=0.005, lam=0.8,
