@@ -112,6 +112,10 @@ int mrb_mesh_export_geometry(const mrb_mesh* mesh, double* areas, double* coeffs
 /* Pixel -> lowest-index containing triangle and barycentric weights
  * (densefield.py:148-182), rasterised on the GPU with fp64 predicates that
  * reproduce numpy's operation order; binned-locate fallback on the host. */
+/* PointLocator + locate, densefield.py:62-127 (host, binned): for n points
+ * (x, y) the lowest-index containing triangle (reference ids) or -1, and its
+ * barycentric weights (n*3, may be NULL) */
+int mrb_mesh_locate(mrb_mesh* mesh, int64_t n, const double* pts, int64_t* tri, double* w);
 int mrb_pixel_map(mrb_ctx* ctx, mrb_mesh* mesh, int32_t width, int32_t height,
                   int64_t* tri_of /* H*W */, double* weights /* H*W*3, may be NULL */);
 

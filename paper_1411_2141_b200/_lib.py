@@ -54,6 +54,7 @@ _SIGS = {
     "mrb_mesh_export_csr": (C.c_int, [_vp, _i32, _vp, _vp, _vp]),
     "mrb_mesh_export_geometry": (C.c_int, [_vp, _vp, _vp, _vp]),
     "mrb_pixel_map": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp]),
+    "mrb_mesh_locate": (C.c_int, [_vp, _i64, _vp, _vp, _vp]),
     "mrb_register": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _vp, C.POINTER(mrb_config),
                                _vp, _vp, C.POINTER(_i32), _dp, _dp, _vp, _vp, _vp]),
     "mrb_batch_create": (C.c_int, [_vp, _i32, _vp, _i32, _i32, _i32, C.POINTER(mrb_config),

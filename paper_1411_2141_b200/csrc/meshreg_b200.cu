@@ -54,6 +54,7 @@ struct mrb_ctx {
 
 struct mrb_mesh {
   HostMesh h;
+  std::unique_ptr<Locator> locator;  // built on first mrb_mesh_locate
 };
 
 namespace mrb {
@@ -2035,6 +2036,18 @@ int mrb_mesh_export_geometry(const mrb_mesh* mesh, double* areas, double* coeffs
   if (coeffs) std::memcpy(coeffs, h.coeffs.data(), h.coeffs.size() * sizeof(double));
   if (vertex_areas)
     std::memcpy(vertex_areas, h.vertex_areas.data(), h.vertex_areas.size() * sizeof(double));
+  return MRB_OK;
+}
+
+int mrb_mesh_locate(mrb_mesh* mesh, int64_t n, const double* pts, int64_t* tri, double* w) {
+  // PointLocator + locate, densefield.py:62-127: lowest-index containing
+  // triangle and its barycentric weights in numpy's order; -1 if uncovered
+  if (!mesh->locator) mesh->locator.reset(new Locator(mesh->h));
+  for (int64_t i = 0; i < n; ++i) {
+    double wi[3] = {0.0, 0.0, 0.0};
+    tri[i] = mesh->locator->locate(mesh->h, pts[2 * i], pts[2 * i + 1], wi);
+    if (w) std::memcpy(w + 3 * i, wi, sizeof wi);
+  }
   return MRB_OK;
 }
 

@@ -17,7 +17,8 @@ from . import _lib
 from .image import ImageGrid
 from .mesh import as_mesh
 
-__all__ = ["DenseField", "MeshCoverageError", "densify", "warp_image", "pixel_map",
+__all__ = ["DenseField", "MeshCoverageError", "PointLocator", "locate", "densify", "warp_image",
+           "pixel_map",
            "FIELD_MAGIC", "FileFormatError", "difference_image", "save_field", "load_field",
            "save_node_displacements_csv"]
 
@@ -49,6 +50,37 @@ class DenseField:
 
 class MeshCoverageError(RuntimeError):
     """An in-domain point was not covered by any mesh triangle."""
+
+
+class PointLocator:
+    """Uniform-bin point-in-triangle index (densefield.py:62-97), built on the
+    host by the native library on first use.  A triangle containing a point
+    always overlaps the point's bin, so ``cell_size`` does not change any
+    answer and is accepted for signature compatibility only."""
+
+    def __init__(self, mesh, cell_size=None):
+        self.mesh = as_mesh(mesh)
+        self.cell_size = cell_size
+
+    def find(self, pts):
+        """(triangle ids (n,), -1 when uncovered; weights (n, 3)) for pts (n, 2)."""
+        pts = np.ascontiguousarray(np.atleast_2d(pts), dtype=np.float64)
+        tri = np.empty(pts.shape[0], np.int64)
+        w = np.empty((pts.shape[0], 3))
+        _lib.load().mrb_mesh_locate(self.mesh._h, pts.shape[0], _lib.ptr(pts), _lib.ptr(tri),
+                                    _lib.ptr(w))
+        return tri, w
+
+
+def locate(locator, p):
+    """Containing triangle index and barycentric weights for point ``p``,
+    lowest index on shared edges (densefield.py:110-127); raises
+    MeshCoverageError when no triangle contains it."""
+    px, py = float(p[0]), float(p[1])
+    tri, w = locator.find(np.array([[px, py]]))
+    if tri[0] < 0:
+        raise MeshCoverageError(f"point ({px}, {py}) not covered by any triangle")
+    return int(tri[0]), w[0]
 
 
 def _errs():

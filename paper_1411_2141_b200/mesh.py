@@ -22,6 +22,9 @@ __all__ = [
     "TriangleGeometry",
     "build_adjacency",
     "vertex_gradient_all",
+    "triangle_gradient",
+    "vertex_gradient",
+    "umbrella",
     "build_laplacian",
     "smooth_displacement",
 ]
@@ -191,6 +194,36 @@ def smooth_displacement(L, u0, lam, iterations=1):
                             _lib.ptr(u2), float(lam), int(iterations), _lib.ptr(out))
     _lib.check(rc, ctx, (ValueError, RuntimeError, RuntimeError))
     return out[:, 0].copy() if squeeze else out
+
+
+def triangle_gradient(geom, tri, f):
+    """Gradient (gx, gy) of the linear interpolant of ``f`` on one triangle
+    (mesh.py:216-221).  A scalar host helper beside the path: the per-vertex
+    field on the path is vertex_gradient_all."""
+    f = np.asarray(f, dtype=np.float64)
+    g = f[geom.triangles[tri]] @ geom.coeffs[tri]
+    return float(g[0]), float(g[1])
+
+
+def vertex_gradient(mesh, geom, f, i):
+    """Area-weighted average of the incident-triangle gradients at vertex
+    ``i`` (mesh.py:224-233), the reference's operation order."""
+    tris = mesh.incident[i]
+    if tris.size == 0:
+        raise ValueError(f"vertex {i} has no incident triangle")
+    f = np.asarray(f, dtype=np.float64)
+    areas = geom.areas[tris]
+    grads = np.einsum("tc,tcd->td", f[geom.triangles[tris]], geom.coeffs[tris])
+    g = (areas[:, None] * grads).sum(axis=0) / areas.sum()
+    return float(g[0]), float(g[1])
+
+
+def umbrella(mesh, u, i):
+    """Mean of the one-ring values minus the center value at vertex ``i``
+    (mesh.py:244-251), per coordinate for (n,) or (n, d) ``u``."""
+    u = np.asarray(u, dtype=np.float64)
+    out = u[mesh.rings[i]].mean(axis=0) - u[i]
+    return float(out) if np.ndim(out) == 0 else out
 
 
 def vertex_gradient_all(mesh, geom, f):

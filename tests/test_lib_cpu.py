@@ -109,3 +109,35 @@ def test_no_cpu_fallback_without_gpu():
     img = mrb.ImageGrid(4, 4, np.arange(16.0))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         img.sample(1.5, 1.5)
+
+
+def test_locate_and_scalar_mesh_helpers():
+    """PointLocator/locate (densefield.py:62-127) through the native host
+    locator, and the scalar helpers triangle_gradient / vertex_gradient /
+    umbrella (mesh.py:216-251) — host-side, no GPU."""
+    import paper_1411_2141_b200 as mrb
+    g = golden("gen64")
+    mesh = mrb.TriMesh(g["V"], g["T_in"])
+    loc = mrb.PointLocator(mesh)
+    h, w = g["re"].shape
+    for q in (0, 17, 64 * 31 + 5, h * w - 1):  # pixel-map golden: tri + weights
+        x, y = q % w, q // w
+        t, wts = mrb.locate(loc, (x, y))
+        assert t == int(g["tri_of"].reshape(-1)[q])
+        if "pm_weights" in g.files:
+            assert np.array_equal(wts, g["pm_weights"].reshape(-1, 3)[q])
+    with pytest.raises(mrb.MeshCoverageError, match=r"point \(-5\.0, 3\.5\) not covered"):
+        mrb.locate(loc, (-5.0, 3.5))
+    import meshreg_oracle as O
+    m = O.Mesh(g["V"], g["T_in"])
+    geom = mrb.TriangleGeometry(mesh)
+    f = np.sin(g["V"][:, 0] / 7.0) + g["V"][:, 1] / 13.0
+    gt = mrb.triangle_gradient(geom, 5, f)
+    assert gt == tuple(float(v) for v in f[m.T[5]] @ m.coeffs[5])  # oracle geometry
+    gv = mrb.vertex_gradient(mesh, geom, f, 3)
+    a = geom.areas[mesh.incident[3]]
+    gr = np.einsum("tc,tcd->td", f[geom.triangles[mesh.incident[3]]], geom.coeffs[mesh.incident[3]])
+    assert gv == tuple(float(v) for v in (a[:, None] * gr).sum(axis=0) / a.sum())
+    u = np.stack([f, 2 * f], axis=1)
+    assert np.array_equal(mrb.umbrella(mesh, u, 3), u[mesh.rings[3]].mean(axis=0) - u[3])
+    assert mrb.umbrella(mesh, f, 3) == float(f[mesh.rings[3]].mean() - f[3])
