@@ -146,3 +146,30 @@ def test_c5_scale_grid_kernel_matches_generic_path(monkeypatch):
     assert relinf(a[2][2], g[2][2]) < 1e-4  # warped image
     assert abs(a[1].msd_after / g[1].msd_after - 1) < 1e-5
     assert a[1].msd_after < a[1].msd_before
+
+
+@pytest.mark.parametrize("path,exchange", [("grid", ""), ("cluster", "push"), ("cluster", "pull")])
+def test_repeatability_under_timing_variation(path, exchange, monkeypatch):
+    """The asynchronous exchanges (epoch-tagged grid words, st.async push,
+    DSMEM pull) must give bit-identical results run after run and across
+    batch sizes (different timing, co-running clusters)."""
+    monkeypatch.setenv("MESHREG_B200_PATH", path)
+    if exchange:
+        monkeypatch.setenv("MESHREG_B200_EXCHANGE", exchange)
+    spec, re32, te32, V, T = load("c2", 0, True)  # x255: real motion, cell crossings
+    S = spec.size
+    re = mrb.ImageGrid(S, S, re32.astype(np.float64))
+    te = mrb.ImageGrid(S, S, te32.astype(np.float64))
+    mesh = mrb.TriMesh(V, T)
+    cfg = mrb.SolverConfig(tau=0.001, max_iterations=60, energy_tolerance=0.0)
+    first = mrb.register(re, te, mesh, cfg, precision="f32", return_dense=True)
+    for _ in range(6):
+        again = mrb.register(re, te, mesh, cfg, precision="f32", return_dense=True)
+        assert np.array_equal(again[0], first[0])
+        assert again[1].energy_trace == first[1].energy_trace
+        assert np.array_equal(again[2][2], first[2][2])
+    if path == "cluster":  # the same pair inside a batch of 5 co-running clusters
+        out = mrb.register_batch([re] * 5, [te] * 5, [mrb.TriMesh(V, T) for _ in range(5)], cfg,
+                                 precision="f32")
+        for u, rep in out:
+            assert np.array_equal(u, out[0][0]) and rep.energy_trace == out[0][1].energy_trace
