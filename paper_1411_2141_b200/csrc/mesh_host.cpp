@@ -39,23 +39,35 @@ std::string fmt_g(double v) {
   return buf;
 }
 
-// Canonical CSR from duplicate-free triplets.
+// Canonical CSR (rows ascending, columns ascending within a row) from
+// duplicate-free triplets: a counting sort by row, then an insertion sort of
+// each (short) row by column — O(nnz) instead of a global comparison sort.
 void to_csr(int64_t nrows, const std::vector<int64_t>& rows, const std::vector<int64_t>& cols,
             const std::vector<double>& vals, Csr& out) {
   const size_t nnz = rows.size();
-  std::vector<int64_t> order(nnz);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) {
-    return rows[x] != rows[y] ? rows[x] < rows[y] : cols[x] < cols[y];
-  });
   out.indptr.assign(nrows + 1, 0);
   for (size_t k = 0; k < nnz; ++k) out.indptr[rows[k] + 1]++;
   for (int64_t i = 0; i < nrows; ++i) out.indptr[i + 1] += out.indptr[i];
   out.indices.resize(nnz);
   out.data.resize(nnz);
+  std::vector<int64_t> fill(out.indptr.begin(), out.indptr.end() - 1);
   for (size_t k = 0; k < nnz; ++k) {
-    out.indices[k] = cols[order[k]];
-    out.data[k] = vals[order[k]];
+    const int64_t at = fill[rows[k]]++;
+    out.indices[at] = cols[k];
+    out.data[at] = vals[k];
+  }
+  for (int64_t i = 0; i < nrows; ++i) {
+    for (int64_t a = out.indptr[i] + 1; a < out.indptr[i + 1]; ++a) {
+      const int64_t c = out.indices[a];
+      const double v = out.data[a];
+      int64_t b = a - 1;
+      for (; b >= out.indptr[i] && out.indices[b] > c; --b) {
+        out.indices[b + 1] = out.indices[b];
+        out.data[b + 1] = out.data[b];
+      }
+      out.indices[b + 1] = c;
+      out.data[b + 1] = v;
+    }
   }
 }
 
