@@ -970,6 +970,14 @@ struct mrb_batch {
   size_t xbytes = 0;       // exchange-word bytes of xbuf (zeroed per grid launch)
   bool push_mode = false;  // k_cluster_push (smoothing_passes <= 1): push halo exchange
   size_t push_smem = 0;
+  // Tail of a throughput-mode batch: the pairs of the last, partial wave
+  // [tail_p0, n_pairs) run in a second launch with the latency shape (more
+  // CTAs per pair, one node per thread), which finishes the partial wave
+  // sooner than the throughput shape would.
+  int tail_p0 = 1 << 30;
+  int tail_cs = 0, tail_npt = 0;
+  size_t tail_smem = 0;
+  bool tail_push = false;
   void* xbuf = nullptr;    // grid path exchange buffers (shared by the pairs, run in turn)
   unsigned* xbar = nullptr;  // grid barrier counter + gbad flags [1 + CS]
   // wave groups (mrb_register_many): the first run launches the fast path per
@@ -1139,12 +1147,11 @@ struct KernelTimer {
 };
 
 template <int NPT>
-void launch_cluster_t(mrb_batch* b, int p0, int np) {
-  const int CS = b->cluster_cs;
+void launch_cluster_t(mrb_batch* b, int p0, int np, int CS, size_t smem) {
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(unsigned(np * CS));
   lc.blockDim = dim3(kClusterThreads);
-  lc.dynamicSmemBytes = b->cluster_smem;
+  lc.dynamicSmemBytes = smem;
   lc.stream = b->ctx->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1295,12 +1302,11 @@ int push_occupancy(int cs, int npt, size_t smem) {
 }
 
 template <int NPT>
-void launch_push_t(mrb_batch* b, int p0, int np) {
-  const int CS = b->cluster_cs;
+void launch_push_t(mrb_batch* b, int p0, int np, int CS, size_t smem) {
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(unsigned(np * CS));
   lc.blockDim = dim3(kClusterThreads);
-  lc.dynamicSmemBytes = b->push_smem;
+  lc.dynamicSmemBytes = smem;
   lc.stream = b->ctx->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1315,20 +1321,29 @@ void launch_push_t(mrb_batch* b, int p0, int np) {
                         float(b->cfg.tau), float(b->cfg.lam), int(b->cfg.smoothing_passes)));
 }
 
+void launch_shape(mrb_batch* b, int p0, int np, int cs, int npt, bool push, size_t smem) {
+  if (np <= 0) return;
+  if (push) {
+    if (npt == 2)
+      launch_push_t<2>(b, p0, np, cs, smem);
+    else
+      launch_push_t<1>(b, p0, np, cs, smem);
+  } else {
+    if (npt == 2)
+      launch_cluster_t<2>(b, p0, np, cs, smem);
+    else
+      launch_cluster_t<1>(b, p0, np, cs, smem);
+  }
+}
+
+// pairs [p0, p0 + np): the batch shape, and the tail shape past tail_p0
 int64_t launch_cluster(mrb_batch* b, int p0, int np) {
   if (b->grid_mode) return launch_grid(b, p0, np);
-  if (b->push_mode) {
-    if (b->cluster_npt == 2)
-      launch_push_t<2>(b, p0, np);
-    else
-      launch_push_t<1>(b, p0, np);
-    return 1;
-  }
-  if (b->cluster_npt == 2)
-    launch_cluster_t<2>(b, p0, np);
-  else
-    launch_cluster_t<1>(b, p0, np);
-  return 1;
+  const int p1 = p0 + np, split = std::min(std::max(b->tail_p0, p0), p1);
+  launch_shape(b, p0, split - p0, b->cluster_cs, b->cluster_npt, b->push_mode,
+               b->push_mode ? b->push_smem : b->cluster_smem);
+  launch_shape(b, split, p1 - split, b->tail_cs, b->tail_npt, b->tail_push, b->tail_smem);
+  return (split > p0) + (p1 > split);
 }
 
 // Deferred topologies (mrb_register_many): pack and copy, on `copy`, the
@@ -1474,7 +1489,7 @@ int64_t dispatch_enqueue(mrb_batch* b, KernelTimer* tm = nullptr) {
 
 int64_t launches_per_run(const mrb_batch* b) {
   if (b->grid_mode) return 3 + b->n_pairs;  // pad, one grid loop per pair, dense, msd
-  if (b->cluster_cs) return 4;               // pad, cluster loop, dense, msd
+  if (b->cluster_cs) return 4 + (b->tail_p0 < b->n_pairs);  // pad, loop(s), dense, msd
   return 2 + int64_t(b->cfg.max_iterations) * (2 + b->cfg.smoothing_passes) + 3;
 }
 
@@ -1488,13 +1503,13 @@ int64_t launches_per_run(const mrb_batch* b) {
 // idle).  The decision is cached per (shape, device).  Returns false when no
 // candidate fits; *occ = active clusters of the choice (pairs per wave).
 bool choose_cluster_shape(mrb_ctx* ctx, HostMesh& big, int n_pairs, bool two_u, int* cs_out,
-                          int* npt_out, int* occ_out) {
+                          int* npt_out, int* occ_out, int npt_pref = 0) {
   const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
   const int64_t nmax = big.n;
   // latency mode (few pairs): one node per thread, more CTAs per pair;
   // throughput mode: two nodes per thread, fewer CTAs per pair
   const char* npt_env = std::getenv("MESHREG_B200_NPT");
-  int npt = npt_env ? std::atoi(npt_env) : (n_pairs >= 4 ? 2 : 1);
+  int npt = npt_pref ? npt_pref : npt_env ? std::atoi(npt_env) : (n_pairs >= 4 ? 2 : 1);
   const char* cs_env = std::getenv("MESHREG_B200_CS");
   static std::mutex cache_mu;
   static std::map<std::tuple<int, int, int64_t, bool, int>, std::tuple<int, int, int>> cache;
@@ -1609,6 +1624,7 @@ size_t grid_dyn_smem(int npt, int halo_stride, bool two_u) {
 
 void build_fast_descriptors(mrb_batch* b);
 void setup_grid_path(mrb_batch* b, int64_t nmax);
+void setup_tail(mrb_batch* b, size_t main_smem);
 
 void setup_cluster_path(mrb_batch* b) {
   b->cluster_cs = 0;
@@ -1674,7 +1690,51 @@ void setup_cluster_path(mrb_batch* b) {
   if (dbg)
     std::fprintf(stderr, "meshreg_b200: cluster %d CTAs x %d nodes/thread, %zu B smem, %s exchange\n",
                  cs, npt, b->push_mode ? b->push_smem : smem, b->push_mode ? "push" : "pull");
+  setup_tail(b, smem);
   build_fast_descriptors(b);
+}
+
+// Tail split of a throughput-mode batch (see mrb_batch::tail_p0): with W
+// clusters per wave and r = P mod W > 0 pairs left for the last wave, run
+// those r pairs in the latency shape when it holds all r in one wave
+// (measured C4: 60 pairs 6.93 ms + 4 pairs 1.07 ms vs 8.41 ms for 64).
+void setup_tail(mrb_batch* b, size_t main_smem) {
+  b->tail_p0 = 1 << 30;
+  if (b->cluster_npt != 2 || std::getenv("MESHREG_B200_NO_TAIL")) return;
+  const int W = cluster_occupancy_cs(b->cluster_cs, b->cluster_npt, main_smem);
+  const int P = b->n_pairs;
+  if (W < 1 || P <= W || P % W == 0) return;
+  const int r = P % W, p0 = P - r;
+  std::vector<mrb_mesh*> tm(b->meshes.begin() + p0, b->meshes.end());
+  mrb_mesh* big = *std::max_element(tm.begin(), tm.end(),
+                                    [](mrb_mesh* x, mrb_mesh* y) { return x->h.n < y->h.n; });
+  const bool two_u = b->cfg.smoothing_passes >= 2;
+  int cs = 0, npt = 0, occ = 0;
+  if (!choose_cluster_shape(b->ctx, big->h, r, two_u, &cs, &npt, &occ, 1) || npt != 1 || occ < r)
+    return;
+  std::vector<HostMesh*> hm;
+  for (mrb_mesh* m : tm) hm.push_back(&m->h);
+  ensure_cluster_topos(b->ctx, hm, cs, npt);
+  size_t smem = 0, ps = 0;
+  bool lists = true;
+  for (mrb_mesh* m : tm) {
+    const int chunk = int((m->h.n + cs - 1) / cs);
+    const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, m->h, cs, chunk, npt);
+    smem = std::max(smem, cluster_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride, two_u));
+    ps = std::max(ps, push_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride, t.send_stride));
+    lists = lists && t.send_stride > 0;
+  }
+  if (cluster_occupancy_cs(cs, npt, smem) < r) return;
+  const char* xenv = std::getenv("MESHREG_B200_EXCHANGE");
+  const bool want_push = !(xenv && std::string(xenv) == "pull") && b->cfg.smoothing_passes <= 1;
+  b->tail_push = want_push && lists && push_occupancy(cs, npt, ps) >= r;
+  b->tail_cs = cs;
+  b->tail_npt = npt;
+  b->tail_smem = b->tail_push ? ps : smem;
+  b->tail_p0 = p0;
+  if (std::getenv("MESHREG_B200_DEBUG"))
+    std::fprintf(stderr, "meshreg_b200: tail of %d pairs: cluster %d CTAs x %d nodes/thread, %s\n",
+                 r, cs, npt, b->tail_push ? "push" : "pull");
 }
 
 // ClusterPair descriptors + padded image copies of a fast-path batch
@@ -1689,8 +1749,10 @@ void build_fast_descriptors(mrb_batch* b) {
   std::vector<ClusterPair> cp(b->n_pairs);
   for (int p = 0; p < b->n_pairs; ++p) {
     HostMesh& h = b->meshes[p]->h;
-    const int chunk = int((h.n + cs - 1) / cs);
-    const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, h, cs, chunk, b->cluster_npt);
+    const bool tail = p >= b->tail_p0;
+    const int pcs = tail ? b->tail_cs : cs, pnpt = tail ? b->tail_npt : b->cluster_npt;
+    const int chunk = int((h.n + pcs - 1) / pcs);
+    const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, h, pcs, chunk, pnpt);
     ClusterPair& c = cp[p];
     c.V = h.dev->V;
     c.g_self = h.dev->g_self_f;

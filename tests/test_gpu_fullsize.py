@@ -173,3 +173,24 @@ def test_repeatability_under_timing_variation(path, exchange, monkeypatch):
                                  precision="f32")
         for u, rep in out:
             assert np.array_equal(u, out[0][0]) and rep.energy_trace == out[0][1].energy_trace
+
+
+def test_c4_tail_wave_in_latency_shape(monkeypatch):
+    """64 C4 pairs: the last partial wave runs in the latency shape (a second
+    launch).  Per-node arithmetic does not depend on the cluster shape, so the
+    fields are bit-identical to the single-shape run; energies agree to the
+    rounding of the (shape-dependent) fixed-order reduction."""
+    pairs = [load("c2", s) for s in range(64)]
+    S = pairs[0][0].size
+    res = [mrb.ImageGrid(S, S, p[1].astype(np.float64)) for p in pairs]
+    tes = [mrb.ImageGrid(S, S, p[2].astype(np.float64)) for p in pairs]
+    cfg = mrb.SolverConfig(max_iterations=50, energy_tolerance=0.0)
+    monkeypatch.setenv("MESHREG_B200_NO_GROUPS", "1")
+    tail = mrb.register_batch(res, tes, [mrb.TriMesh(p[3], p[4]) for p in pairs], cfg,
+                              precision="f32")
+    monkeypatch.setenv("MESHREG_B200_NO_TAIL", "1")
+    plain = mrb.register_batch(res, tes, [mrb.TriMesh(p[3], p[4]) for p in pairs], cfg,
+                               precision="f32")
+    for (u1, r1), (u2, r2) in zip(tail, plain):
+        assert np.array_equal(u1, u2)
+        assert relinf(r1.energy_trace, r2.energy_trace) < 1e-12
