@@ -95,6 +95,14 @@ int mrb_ctx_synchronize(mrb_ctx* ctx);
 int mrb_mesh_build(int64_t n_vertices, const double* vertices /* n*2 */,
                    int64_t n_triangles, const int64_t* triangles /* m*3 */,
                    mrb_mesh** out, char* err, int32_t err_len);
+/* mrb_mesh_build for `count` meshes at once on the library's host worker
+ * pool (no reference counterpart: the reference builds one TriMesh at a time,
+ * mesh.py:58).  All or nothing: on the first failing mesh (lowest index) every
+ * out[k] is NULL, *first_bad = its index and err holds its message. */
+int mrb_mesh_build_many(int32_t count, const int64_t* n_vertices,
+                        const double* const* vertices, const int64_t* n_triangles,
+                        const int64_t* const* triangles, mrb_mesh** out,
+                        int32_t* first_bad, char* err, int32_t err_len);
 int mrb_mesh_destroy(mrb_mesh* mesh);
 /* counts[0..5] = n_vertices, n_triangles, n_edges, nnz(L), nnz(grad), nnz(avg) */
 int mrb_mesh_counts(const mrb_mesh* mesh, int64_t* counts);

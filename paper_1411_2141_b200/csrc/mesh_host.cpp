@@ -39,38 +39,6 @@ std::string fmt_g(double v) {
   return buf;
 }
 
-// Canonical CSR (rows ascending, columns ascending within a row) from
-// duplicate-free triplets: a counting sort by row, then an insertion sort of
-// each (short) row by column — O(nnz) instead of a global comparison sort.
-void to_csr(int64_t nrows, const std::vector<int64_t>& rows, const std::vector<int64_t>& cols,
-            const std::vector<double>& vals, Csr& out) {
-  const size_t nnz = rows.size();
-  out.indptr.assign(nrows + 1, 0);
-  for (size_t k = 0; k < nnz; ++k) out.indptr[rows[k] + 1]++;
-  for (int64_t i = 0; i < nrows; ++i) out.indptr[i + 1] += out.indptr[i];
-  out.indices.resize(nnz);
-  out.data.resize(nnz);
-  std::vector<int64_t> fill(out.indptr.begin(), out.indptr.end() - 1);
-  for (size_t k = 0; k < nnz; ++k) {
-    const int64_t at = fill[rows[k]]++;
-    out.indices[at] = cols[k];
-    out.data[at] = vals[k];
-  }
-  for (int64_t i = 0; i < nrows; ++i) {
-    for (int64_t a = out.indptr[i] + 1; a < out.indptr[i + 1]; ++a) {
-      const int64_t c = out.indices[a];
-      const double v = out.data[a];
-      int64_t b = a - 1;
-      for (; b >= out.indptr[i] && out.indices[b] > c; --b) {
-        out.indices[b + 1] = out.indices[b];
-        out.data[b + 1] = out.data[b];
-      }
-      out.indices[b + 1] = c;
-      out.data[b + 1] = v;
-    }
-  }
-}
-
 uint32_t spread16(uint32_t x) {
   x &= 0xFFFF;
   x = (x | (x << 8)) & 0x00FF00FF;
@@ -132,23 +100,46 @@ std::string build_mesh(int64_t n, const double* Vin, int64_t m, const int64_t* T
   }
 
   // ---- connectivity, mesh.py:91-123 ----
-  std::vector<std::pair<int64_t, int64_t>> raw;
-  raw.reserve(3 * m);
-  for (int64_t t = 0; t < m; ++t) {
-    const int64_t* r = &M.T[3 * t];
-    const int64_t pr[3][2] = {{r[0], r[1]}, {r[1], r[2]}, {r[2], r[0]}};
-    for (auto& e : pr) raw.emplace_back(std::min(e[0], e[1]), std::max(e[0], e[1]));
-  }
-  std::sort(raw.begin(), raw.end());
+  // Unique undirected edges in np.unique's lexicographic (lo, hi) order with
+  // their use counts: a counting sort on lo, then an insertion sort of each
+  // (short) bucket on hi — O(m) instead of a comparison sort of 3m pairs.
   std::vector<int64_t> counts;
-  M.edges.clear();
-  for (size_t k = 0; k < raw.size();) {
-    size_t j = k;
-    while (j < raw.size() && raw[j] == raw[k]) ++j;
-    M.edges.push_back(raw[k].first);
-    M.edges.push_back(raw[k].second);
-    counts.push_back(int64_t(j - k));
-    k = j;
+  {
+    std::vector<int64_t> bptr(n + 1, 0), bhi(3 * m);
+    for (int64_t t = 0; t < m; ++t) {
+      const int64_t* r = &M.T[3 * t];
+      bptr[std::min(r[0], r[1]) + 1]++;
+      bptr[std::min(r[1], r[2]) + 1]++;
+      bptr[std::min(r[2], r[0]) + 1]++;
+    }
+    for (int64_t i = 0; i < n; ++i) bptr[i + 1] += bptr[i];
+    std::vector<int64_t> fill(bptr.begin(), bptr.end() - 1);
+    for (int64_t t = 0; t < m; ++t) {
+      const int64_t* r = &M.T[3 * t];
+      const int64_t pr[3][2] = {{r[0], r[1]}, {r[1], r[2]}, {r[2], r[0]}};
+      for (auto& e : pr) bhi[fill[std::min(e[0], e[1])]++] = std::max(e[0], e[1]);
+    }
+    M.edges.clear();
+    M.edges.reserve(3 * m);
+    counts.reserve(3 * m / 2 + n);
+    for (int64_t lo = 0; lo < n; ++lo) {
+      int64_t* b = bhi.data() + bptr[lo];
+      const int64_t len = bptr[lo + 1] - bptr[lo];
+      for (int64_t a = 1; a < len; ++a) {
+        const int64_t v = b[a];
+        int64_t c = a - 1;
+        for (; c >= 0 && b[c] > v; --c) b[c + 1] = b[c];
+        b[c + 1] = v;
+      }
+      for (int64_t k = 0; k < len;) {
+        int64_t j = k;
+        while (j < len && b[j] == b[k]) ++j;
+        M.edges.push_back(lo);
+        M.edges.push_back(b[k]);
+        counts.push_back(j - k);
+        k = j;
+      }
+    }
   }
   M.ne = int64_t(counts.size());
   for (int64_t c : counts)
@@ -169,8 +160,8 @@ std::string build_mesh(int64_t n, const double* Vin, int64_t m, const int64_t* T
       M.ring_idx[fill[a]++] = b;
       M.ring_idx[fill[b]++] = a;
     }
-    for (int64_t i = 0; i < n; ++i)
-      std::sort(M.ring_idx.begin() + M.ring_ptr[i], M.ring_idx.begin() + M.ring_ptr[i + 1]);
+    // Already ascending: edges arrive in (lo, hi) order, so a vertex first
+    // receives its lower neighbours (ascending lo), then its higher ones.
   }
   M.inc_ptr.assign(n + 1, 0);
   for (int64_t k = 0; k < 3 * m; ++k) M.inc_ptr[M.T[k] + 1]++;
@@ -229,32 +220,8 @@ std::string build_mesh(int64_t n, const double* Vin, int64_t m, const int64_t* T
       co[2 * 2 + d] = tk * inv4a2;
     }
   }
-  {
-    std::vector<int64_t> rows(3 * m), cols(3 * m);
-    std::vector<double> vx(3 * m), vy(3 * m);
-    for (int64_t t = 0; t < m; ++t)
-      for (int c = 0; c < 3; ++c) {
-        rows[3 * t + c] = t;
-        cols[3 * t + c] = M.T[3 * t + c];
-        vx[3 * t + c] = M.coeffs[6 * t + 2 * c];
-        vy[3 * t + c] = M.coeffs[6 * t + 2 * c + 1];
-      }
-    to_csr(m, rows, cols, vx, M.gx);
-    to_csr(m, rows, cols, vy, M.gy);
-    M.vertex_areas.assign(n, 0.0);
-    for (int64_t k = 0; k < 3 * m; ++k) M.vertex_areas[cols[k]] += M.areas[rows[k]];
-    std::vector<double> w(3 * m);
-    for (int64_t k = 0; k < 3 * m; ++k) w[k] = M.areas[rows[k]] / M.vertex_areas[cols[k]];
-    to_csr(n, cols, rows, w, M.avg);
-  }
-  // Laplacian (mesh.py:254-265)
-  M.lap.indptr = M.ring_ptr;
-  M.lap.indices = M.ring_idx;
-  M.lap.data.resize(M.ring_idx.size());
-  for (int64_t i = 0; i < n; ++i) {
-    const double v = 1.0 / double(M.valence[i]);
-    for (int64_t k = M.ring_ptr[i]; k < M.ring_ptr[i + 1]; ++k) M.lap.data[k] = v;
-  }
+  M.vertex_areas.assign(n, 0.0);  // np.add.at in (t, corner) order
+  for (int64_t k = 0; k < 3 * m; ++k) M.vertex_areas[M.T[k]] += M.areas[k / 3];
 
   // ---- device-facing layout ----
   // Morton (Z-order) relabelling so a warp's nodes gather nearby image taps.
@@ -301,6 +268,9 @@ std::string build_mesh(int64_t n, const double* Vin, int64_t m, const int64_t* T
     const int32_t base = M.nb_ptr[k];
     for (int64_t r = r0; r < r1; ++r) M.nb_idx[base + (r - r0)] = M.iperm[M.ring_idx[r]];
     // accumulate fused coefficients over incident triangles (ascending id)
+    const int64_t* ring = &M.ring_idx[r0];
+    double* g = &M.g_nb[2 * int64_t(base)];
+    double sx = 0.0, sy = 0.0;
     for (int64_t q = M.inc_ptr[i]; q < M.inc_ptr[i + 1]; ++q) {
       const int64_t t = M.inc_idx[q];
       const double w = M.areas[t] / M.vertex_areas[i];
@@ -309,16 +279,18 @@ std::string build_mesh(int64_t n, const double* Vin, int64_t m, const int64_t* T
         const double cx = w * M.coeffs[6 * t + 2 * c];
         const double cy = w * M.coeffs[6 * t + 2 * c + 1];
         if (j == i) {
-          M.g_self[2 * k] += cx;
-          M.g_self[2 * k + 1] += cy;
+          sx += cx;
+          sy += cy;
         } else {
-          const int64_t* b = &M.ring_idx[r0];
-          const int64_t pos = std::lower_bound(b, b + (r1 - r0), j) - b;
-          M.g_nb[2 * (base + pos)] += cx;
-          M.g_nb[2 * (base + pos) + 1] += cy;
+          int64_t pos = 0;
+          while (ring[pos] != j) ++pos;  // j is a one-ring neighbour of i
+          g[2 * pos] += cx;
+          g[2 * pos + 1] += cy;
         }
       }
     }
+    M.g_self[2 * k] = sx;
+    M.g_self[2 * k + 1] = sy;
   }
   M.Tn.resize(4 * m);
   for (int64_t t = 0; t < m; ++t) {
@@ -326,6 +298,48 @@ std::string build_mesh(int64_t n, const double* Vin, int64_t m, const int64_t* T
     M.Tn[4 * t + 3] = 0;
   }
   return "";
+}
+
+void ensure_reference_csr(HostMesh& M) {
+  std::call_once(M.csr_once, [&M] {
+    const int64_t n = M.n, m = M.m;
+    // Gx, Gy (m x n, one row per triangle, its 3 corners by ascending vertex id)
+    // and avg (n x m, row i = the incident triangles, ascending id: exactly
+    // inc_ptr / inc_idx) — the canonical CSR scipy builds from the triplets.
+    M.gx.indptr.resize(m + 1);
+    M.gy.indptr.resize(m + 1);
+    M.gx.indices.resize(3 * m);
+    M.gy.indices.resize(3 * m);
+    M.gx.data.resize(3 * m);
+    M.gy.data.resize(3 * m);
+    for (int64_t t = 0; t <= m; ++t) M.gx.indptr[t] = M.gy.indptr[t] = 3 * t;
+    for (int64_t t = 0; t < m; ++t) {
+      int o[3] = {0, 1, 2};
+      const int64_t* r = &M.T[3 * t];
+      if (r[o[1]] < r[o[0]]) std::swap(o[0], o[1]);
+      if (r[o[2]] < r[o[1]]) std::swap(o[1], o[2]);
+      if (r[o[1]] < r[o[0]]) std::swap(o[0], o[1]);
+      for (int c = 0; c < 3; ++c) {
+        M.gx.indices[3 * t + c] = M.gy.indices[3 * t + c] = r[o[c]];
+        M.gx.data[3 * t + c] = M.coeffs[6 * t + 2 * o[c]];
+        M.gy.data[3 * t + c] = M.coeffs[6 * t + 2 * o[c] + 1];
+      }
+    }
+    M.avg.indptr = M.inc_ptr;
+    M.avg.indices = M.inc_idx;
+    M.avg.data.resize(3 * m);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t q = M.inc_ptr[i]; q < M.inc_ptr[i + 1]; ++q)
+        M.avg.data[q] = M.areas[M.inc_idx[q]] / M.vertex_areas[i];
+    // Laplacian (mesh.py:254-265): rows = one-rings, values 1/valence
+    M.lap.indptr = M.ring_ptr;
+    M.lap.indices = M.ring_idx;
+    M.lap.data.resize(M.ring_idx.size());
+    for (int64_t i = 0; i < n; ++i) {
+      const double v = 1.0 / double(M.valence[i]);
+      for (int64_t k = M.ring_ptr[i]; k < M.ring_ptr[i + 1]; ++k) M.lap.data[k] = v;
+    }
+  });
 }
 
 // ---- PointLocator / locate (densefield.py:62-127) ----

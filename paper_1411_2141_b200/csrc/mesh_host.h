@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -30,7 +31,8 @@ struct HostMesh {
   std::vector<int64_t> ring_ptr, ring_idx;  // sorted one-rings
   std::vector<int64_t> inc_ptr, inc_idx;    // ascending incident triangles
   std::vector<double> areas, coeffs, vertex_areas;  // m, m*3*2, n
-  Csr lap, gx, gy, avg;
+  Csr lap, gx, gy, avg;          // built on first export (ensure_reference_csr)
+  std::once_flag csr_once;
 
   // device-facing layout (node relabelling by Morton order of V)
   std::vector<int32_t> perm;   // new -> old
@@ -50,6 +52,10 @@ struct HostMesh {
 
 // Build + validate; returns "" on success, else the reference's ValueError text.
 std::string build_mesh(int64_t n, const double* V, int64_t m, const int64_t* T, HostMesh& out);
+
+// The reference's CSR operators L, Gx, Gy, avg (mesh.py:199-213, 254-265):
+// only the export entry points need them, so they are built on first use.
+void ensure_reference_csr(HostMesh& M);
 
 // PointLocator + locate (densefield.py:62-127) for pixels the raster pass
 // left unassigned.  Returns triangle id or -1 (uncovered), fills w[3].

@@ -12,6 +12,7 @@
 #include <string>
 #include <type_traits>
 #include <atomic>
+#include <pthread.h>
 #include <thread>
 #include <tuple>
 #include <mutex>
@@ -332,16 +333,18 @@ void* pinned_stage(mrb_ctx* ctx, size_t bytes, int which) {
 // Persistent host worker pool: parallel_for(n, f) runs f(0..n-1) on up to 16
 // threads (the caller participates).  Thread start-up is paid once per
 // process, not per call — batch setup calls it several times per chunk.
+// The pool is never destroyed (its threads end with the process), and a
+// forked child, which inherits no threads, runs everything on the caller.
 class WorkerPool {
  public:
   static WorkerPool& get() {
-    static WorkerPool pool;
-    return pool;
+    static WorkerPool* pool = new WorkerPool();
+    return *pool;
   }
   template <typename F>
   void run(size_t n, F&& f) {
     if (n == 0) return;
-    if (workers_.empty() || n == 1) {
+    if (workers_.empty() || n == 1 || forked_) {
       for (size_t i = 0; i < n; ++i) f(i);
       return;
     }
@@ -364,6 +367,7 @@ class WorkerPool {
 
  private:
   WorkerPool() {
+    pthread_atfork(nullptr, nullptr, [] { get().forked_ = true; });
     const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency())) - 1;
     for (unsigned k = 0; k < nt; ++k)
       workers_.emplace_back([this] {
@@ -378,14 +382,6 @@ class WorkerPool {
           work();
         }
       });
-  }
-  ~WorkerPool() {
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
-    }
-    cv_.notify_all();
-    for (auto& t : workers_) t.join();
   }
   void work() {
     for (;;) {
@@ -408,6 +404,7 @@ class WorkerPool {
   std::function<void(size_t)>* fn_ = nullptr;
   size_t n_ = 0, next_ = 0, done_ = 0, gen_ = 0;
   bool stop_ = false;
+  volatile bool forked_ = false;
 };
 
 template <typename F>
@@ -2042,6 +2039,41 @@ int mrb_mesh_build(int64_t n, const double* V, int64_t m, const int64_t* T, mrb_
   return MRB_OK;
 }
 
+int mrb_mesh_build_many(int32_t count, const int64_t* n, const double* const* V, const int64_t* m,
+                        const int64_t* const* T, mrb_mesh** out, int32_t* first_bad, char* err,
+                        int32_t err_len) {
+  if (first_bad) *first_bad = -1;
+  if (count < 0 || (count > 0 && (!n || !V || !m || !T || !out))) return MRB_E_VALUE;
+  std::vector<std::string> msg(static_cast<size_t>(count));
+  for (int32_t k = 0; k < count; ++k) out[k] = nullptr;
+  WorkerPool::get().run(size_t(count), [&](size_t k) {
+    auto* mesh = new mrb_mesh();
+    try {
+      msg[k] = build_mesh(n[k], V[k], m[k], T[k], mesh->h);
+    } catch (const std::exception& ex) {
+      msg[k] = std::string("internal error: ") + ex.what();
+    }
+    if (msg[k].empty())
+      out[k] = mesh;
+    else
+      delete mesh;
+  });
+  for (int32_t k = 0; k < count; ++k)
+    if (!msg[k].empty()) {
+      if (first_bad) *first_bad = k;
+      if (err && err_len > 0) {
+        std::strncpy(err, msg[k].c_str(), size_t(err_len) - 1);
+        err[err_len - 1] = 0;
+      }
+      for (int32_t j = 0; j < count; ++j) {  // all or nothing
+        delete out[j];
+        out[j] = nullptr;
+      }
+      return MRB_E_VALUE;
+    }
+  return MRB_OK;
+}
+
 int mrb_mesh_destroy(mrb_mesh* mesh) {
   delete mesh;
   return MRB_OK;
@@ -2052,9 +2084,9 @@ int mrb_mesh_counts(const mrb_mesh* mesh, int64_t* c) {
   c[0] = h.n;
   c[1] = h.m;
   c[2] = h.ne;
-  c[3] = int64_t(h.lap.indices.size());
-  c[4] = int64_t(h.gx.indices.size());
-  c[5] = int64_t(h.avg.indices.size());
+  c[3] = int64_t(h.ring_idx.size());  // nnz(L) = 2 n_edges
+  c[4] = 3 * h.m;                      // nnz(Gx) = nnz(Gy)
+  c[5] = 3 * h.m;                      // nnz(avg)
   return MRB_OK;
 }
 
@@ -2078,7 +2110,8 @@ int mrb_mesh_export_connectivity(const mrb_mesh* mesh, int64_t* tri, int64_t* ed
 
 int mrb_mesh_export_csr(const mrb_mesh* mesh, int32_t which, int64_t* indptr, int64_t* indices,
                         double* data) {
-  const HostMesh& h = mesh->h;
+  HostMesh& h = const_cast<mrb_mesh*>(mesh)->h;  // the CSR cache is built on first use
+  ensure_reference_csr(h);
   const Csr* c = which == MRB_CSR_LAPLACIAN  ? &h.lap
                  : which == MRB_CSR_GRAD_X   ? &h.gx
                  : which == MRB_CSR_GRAD_Y   ? &h.gy

@@ -32,16 +32,21 @@ __all__ = [
 DEGENERATE_AREA = 1e-9
 
 
+def _mesh_arrays(vertices, triangles):
+    V = np.ascontiguousarray(np.asarray(vertices, dtype=np.float64))
+    T = np.ascontiguousarray(np.asarray(triangles, dtype=np.int64))
+    if V.ndim != 2 or V.shape[1] != 2:
+        raise ValueError(f"vertices must be (n, 2), got {V.shape}")
+    if T.ndim != 2 or T.shape[1] != 3 or T.shape[0] < 1:
+        raise ValueError(f"triangles must be (m, 3) with m >= 1, got {T.shape}")
+    return V, T
+
+
 class TriMesh:
     """Static 2-D triangulation with one-ring connectivity (mesh.py:31-145)."""
 
     def __init__(self, vertices, triangles):
-        V = np.ascontiguousarray(np.asarray(vertices, dtype=np.float64))
-        T = np.ascontiguousarray(np.asarray(triangles, dtype=np.int64))
-        if V.ndim != 2 or V.shape[1] != 2:
-            raise ValueError(f"vertices must be (n, 2), got {V.shape}")
-        if T.ndim != 2 or T.shape[1] != 3 or T.shape[0] < 1:
-            raise ValueError(f"triangles must be (m, 3) with m >= 1, got {T.shape}")
+        V, T = _mesh_arrays(vertices, triangles)
         lib = _lib.load()
         h = C.c_void_p()
         err = C.create_string_buffer(512)
@@ -49,7 +54,39 @@ class TriMesh:
                                 err, 512)
         if rc != _lib.OK:
             raise ValueError(err.value.decode())
-        self._h = h.value
+        self._adopt(h.value, V)
+
+    @classmethod
+    def build_many(cls, meshes):
+        """[(vertices, triangles), ...] -> [TriMesh], built in parallel on the
+        library's host worker pool (mrb_mesh_build_many).  Raises the
+        ValueError the first invalid mesh (lowest index) would raise alone."""
+        arrs = [_mesh_arrays(V, T) for V, T in meshes]
+        k = len(arrs)
+        if k == 0:
+            return []
+        lib = _lib.load()
+        n = np.array([V.shape[0] for V, _ in arrs], np.int64)
+        m = np.array([T.shape[0] for _, T in arrs], np.int64)
+        Vp = (C.c_void_p * k)(*(V.ctypes.data for V, _ in arrs))
+        Tp = (C.c_void_p * k)(*(T.ctypes.data for _, T in arrs))
+        out = (C.c_void_p * k)()
+        bad = C.c_int32(-1)
+        err = C.create_string_buffer(512)
+        rc = lib.mrb_mesh_build_many(k, _lib.ptr(n), Vp, _lib.ptr(m), Tp, out, C.byref(bad),
+                                     err, 512)
+        if rc != _lib.OK:
+            raise ValueError(err.value.decode())
+        meshes = []
+        for (V, _), h in zip(arrs, out):
+            obj = cls.__new__(cls)
+            obj._adopt(h, V)
+            meshes.append(obj)
+        return meshes
+
+    def _adopt(self, handle, V):
+        lib = _lib.load()
+        self._h = handle
         self._fin = weakref.finalize(self, lib.mrb_mesh_destroy, self._h)
         counts = np.zeros(6, dtype=np.int64)
         lib.mrb_mesh_counts(self._h, _lib.ptr(counts))
@@ -73,9 +110,24 @@ class TriMesh:
         self.edges = edges
         self.valence = valence
         self.boundary = boundary.astype(bool)
-        self.rings = np.split(ring_idx, ring_ptr[1:-1])
-        self.incident = np.split(inc_idx, inc_ptr[1:-1])
+        self._ring = (ring_ptr, ring_idx)
+        self._inc = (inc_ptr, inc_idx)
+        self._rings = self._incident = None
         self._geometry = None
+
+    @property
+    def rings(self):
+        """Sorted one-ring neighbour ids per vertex (mesh.py:107-113), split lazily."""
+        if self._rings is None:
+            self._rings = np.split(self._ring[1], self._ring[0][1:-1])
+        return self._rings
+
+    @property
+    def incident(self):
+        """Ascending incident triangle ids per vertex (mesh.py:114-117), split lazily."""
+        if self._incident is None:
+            self._incident = np.split(self._inc[1], self._inc[0][1:-1])
+        return self._incident
 
     @property
     def n_vertices(self):

@@ -58,6 +58,30 @@ def test_native_mesh_setup_bit_exact(name):
         assert np.array_equal(geom.vertex_areas, g["vertex_areas"])
 
 
+def test_build_many_matches_single_builds():
+    """mrb_mesh_build_many (host worker pool) gives the same meshes as one
+    mrb_mesh_build each, and reports the lowest-index invalid mesh."""
+    gs = [golden(n) for n in ("gen64", "c1", "plateau64", "accept_c3", "gen64_x255")]
+    many = mrb.TriMesh.build_many([(g["V"], g["T_in"]) for g in gs] * 3)
+    assert len(many) == 15
+    for k, mesh in enumerate(many):
+        g = gs[k % len(gs)]
+        one = mrb.TriMesh(g["V"], g["T_in"])
+        assert np.array_equal(mesh.triangles, one.triangles)
+        assert np.array_equal(mesh.edges, one.edges)
+        assert np.array_equal(np.concatenate(mesh.rings), np.concatenate(one.rings))
+        for a, b in ((mrb.build_laplacian(mesh), mrb.build_laplacian(one)),
+                     (mesh.geometry.vertex_average_op, one.geometry.vertex_average_op),
+                     (mesh.geometry.grad_x_op, one.geometry.grad_x_op)):
+            assert np.array_equal(a.indices, b.indices) and np.array_equal(a.data, b.data)
+    assert mrb.TriMesh.build_many([]) == []
+    bad = [(gs[0]["V"], gs[0]["T_in"]), ([(0, 0), (1, 0), (2, 0)], [(0, 1, 2)]),
+           ([(0, 0), (1, 0), (0, 1)], [(0, 1, 3)])]
+    with pytest.raises(ValueError) as e:
+        mrb.TriMesh.build_many(bad)
+    assert str(e.value) == "degenerate triangle 0 (area 0)"
+
+
 def test_mesh_validation_messages_match_reference():
     # texts of mesh.py:61-123
     with pytest.raises(ValueError, match=r"vertices must be \(n, 2\)"):

@@ -26,7 +26,7 @@ u_h = torch.empty((n_tot, 2), dtype=torch.float64).pin_memory()
 dense = [torch.empty((P, H, W), dtype=torch.float32).pin_memory() for _ in range(3)]
 for rep in range(3):
     t = [time.perf_counter()]
-    hs = [bench.mesh_handle(lib, p[2], p[3]) for p in pairs]
+    hs = bench.mesh_handles(lib, [(p[2], p[3]) for p in pairs])
     t.append(time.perf_counter())
     arr = (C.c_void_p * P)(*hs)
     b = C.c_void_p()

@@ -18,7 +18,7 @@ n_tot = sum(len(p[2]) for p in pairs)
 u_h = torch.empty((n_tot, 2), dtype=torch.float64).pin_memory()
 dense = [torch.empty((P, H, W), dtype=torch.float32).pin_memory() for _ in range(3)]
 for rep in range(3):
-    hs = [bench.mesh_handle(lib, p[2], p[3]) for p in pairs]
+    hs = bench.mesh_handles(lib, [(p[2], p[3]) for p in pairs])
     arr = (C.c_void_p * P)(*hs)
     pass
     t0 = time.perf_counter()

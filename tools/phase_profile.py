@@ -22,7 +22,7 @@ spec, _ = bench.workload_spec(wl)
 pairs = [bench.load_pair(wl, s) for s in range(P)]
 W = H = spec.size
 cfg = _lib.mrb_config(0.005, 0.8, 0.0, spec.iterations, 1, _lib.PREC_F32, 0)
-hs = [bench.mesh_handle(lib, p[2], p[3]) for p in pairs]
+hs = bench.mesh_handles(lib, [(p[2], p[3]) for p in pairs])
 arr = (C.c_void_p * P)(*hs)
 b = C.c_void_p()
 assert lib.mrb_batch_create(ctx, P, arr, W, H, _lib.F32, C.byref(cfg), C.byref(b)) == 0
