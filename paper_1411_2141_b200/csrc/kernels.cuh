@@ -564,12 +564,10 @@ __global__ void k_zero_state(typename V2<Real>::type* u, int n) {
 // one warp per triangle; lanes stride over the triangle's pixel bbox and keep
 // the lowest triangle id per pixel (atomicMin == ascending-order
 // assign-if-unassigned of the reference).
-__global__ void k_raster(const double2* __restrict__ V, const int4* __restrict__ tri, int m,
-                         int W, int H, int* __restrict__ tri_of) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= m) return;
-  const int4 tv = tri[warp];
+__device__ __forceinline__ void raster_triangle(const double2* __restrict__ V,
+                                                const int4* __restrict__ tri, int t, int lane,
+                                                int W, int H, int* __restrict__ tri_of) {
+  const int4 tv = tri[t];
   const double2 a = V[tv.x], b = V[tv.y], c = V[tv.z];
   const double mnx = fmin(fmin(a.x, b.x), c.x), mxx = fmax(fmax(a.x, b.x), c.x);
   const double mny = fmin(fmin(a.y, b.y), c.y), mxy = fmax(fmax(a.y, b.y), c.y);
@@ -584,8 +582,32 @@ __global__ void k_raster(const double2* __restrict__ V, const int4* __restrict__
     const long long py = y0 + q / bw, px = x0 + q % bw;
     double w[3];
     bary_rn(a, b, c, double(px), double(py), w);
-    if (fmin(fmin(w[0], w[1]), w[2]) >= -1e-9) atomicMin(tri_of + py * W + px, warp);
+    if (fmin(fmin(w[0], w[1]), w[2]) >= -1e-9) atomicMin(tri_of + py * W + px, t);
   }
+}
+
+__global__ void k_raster(const double2* __restrict__ V, const int4* __restrict__ tri, int m,
+                         int W, int H, int* __restrict__ tri_of) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (warp < m) raster_triangle(V, tri, warp, threadIdx.x & 31, W, H, tri_of);
+}
+
+// Many meshes in one launch (blockIdx.y = mesh): setup of a whole batch costs
+// three launches instead of three per mesh.  The job table travels in the
+// kernel parameters (kRasterJobs x 28 B).
+constexpr int kRasterJobs = 128;
+struct RasterJobs {
+  const double2* V[kRasterJobs];
+  const int4* tri[kRasterJobs];
+  int* map[kRasterJobs];
+  int m[kRasterJobs];
+};
+
+__global__ void k_raster_many(const RasterJobs jobs, int W, int H) {
+  const int j = blockIdx.y;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (warp < jobs.m[j]) raster_triangle(jobs.V[j], jobs.tri[j], warp, threadIdx.x & 31, W, H,
+                                        jobs.map[j]);
 }
 
 __global__ void k_count_uncovered(const int* __restrict__ tri_of, int npx,
@@ -595,6 +617,16 @@ __global__ void k_count_uncovered(const int* __restrict__ tri_of, int npx,
     local += (tri_of[q] == kUnassigned);
   for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, (unsigned long long)local);
+}
+
+__global__ void k_count_uncovered_many(const RasterJobs jobs, int npx,
+                                       unsigned long long* __restrict__ count) {
+  const int* tri_of = jobs.map[blockIdx.y];
+  int local = 0;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < npx; q += gridDim.x * blockDim.x)
+    local += (tri_of[q] == kUnassigned);
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(count + blockIdx.y, (unsigned long long)local);
 }
 
 __global__ void k_pixel_weights(const double2* __restrict__ V, const int4* __restrict__ tri,

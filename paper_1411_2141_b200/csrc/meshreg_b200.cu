@@ -38,9 +38,10 @@ struct mrb_ctx {
   mrb_ctx* sub[2] = {nullptr, nullptr};  // pipeline streams of mrb_register_many
   // host staging buffers for uploads (grow): [0] meshes, [1] fast-path
   // topologies, so planning the topologies never waits for the mesh copies
-  void* pinned[2] = {nullptr, nullptr};
-  size_t pinned_cap[2] = {0, 0};
-  cudaEvent_t stage_done[2] = {nullptr, nullptr};  // last async copy out of pinned[i]
+  // pinned staging: [0] meshes, [1] topologies, [2] tail-shape topologies
+  void* pinned[3] = {nullptr, nullptr, nullptr};
+  size_t pinned_cap[3] = {0, 0, 0};
+  cudaEvent_t stage_done[3] = {nullptr, nullptr, nullptr};  // last async copy out of pinned[i]
   cudaStream_t copy = nullptr;       // input copies of mrb_register_many
   cudaEvent_t copy_done = nullptr;
   unsigned long long* counts = nullptr;  // pinned uncovered-pixel counts
@@ -98,6 +99,8 @@ struct DeviceMesh {
   double2* g_nb_d = nullptr;
   double* inv_val_d = nullptr;
   std::map<std::pair<int, int>, int*> pixel_maps;
+  // owners of pixel maps that are slices of a batch's shared slab
+  std::map<std::pair<int, int>, std::shared_ptr<unsigned char>> pixel_map_hold;
   // cluster fast path: register topology packed for a given chunk size
   struct Topo {  // SELL-32 one-ring layout for one (cluster size, nodes/thread)
     unsigned char* slab = nullptr;  // every array below lives in it
@@ -124,7 +127,9 @@ struct DeviceMesh {
       dev_free(slab, stream);
     dev_free(slab64, stream);
     dev_free(slab_ring, stream);
-    for (auto& kv : pixel_maps) dev_free(kv.second, stream);
+    for (auto& kv : pixel_maps)
+      if (!pixel_map_hold.count(kv.first)) dev_free(kv.second, stream);
+    pixel_map_hold.clear();
     for (auto& kv : topo) {
       if (kv.second.hold)
         kv.second.hold.reset();
@@ -412,6 +417,21 @@ void parallel_for(size_t n, F&& f) {
   WorkerPool::get().run(n, std::forward<F>(f));
 }
 
+// MESHREG_B200_DEBUG: named device timestamps, printed (relative to the
+// call's start) by mrb_register_many
+std::vector<std::pair<std::string, cudaEvent_t>>& dev_marks() {
+  static std::vector<std::pair<std::string, cudaEvent_t>> v;
+  return v;
+}
+void dev_mark(cudaStream_t s, const char* what) {
+  static const bool on = std::getenv("MESHREG_B200_DEBUG") != nullptr;
+  if (!on) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+  dev_marks().emplace_back(what, e);
+}
+
 // Upload the per-mesh device arrays of every mesh in `meshes` that has none
 // yet.  Each mesh gets one device slab; the slabs are filled on a host thread
 // pool into a context-owned pinned staging buffer and copied asynchronously.
@@ -482,6 +502,7 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, bo
   // copies run at full PCIe rate, ~1 MB ones at less than half of it)
   const std::shared_ptr<unsigned char> all = shared_slab(total, ctx->stream);
   ck(mrb_copy_async(all.get(), stage, total, cudaMemcpyHostToDevice, ctx->stream));
+  dev_mark(ctx->stream, "mesh upload done");
   for (size_t i = 0; i < todo.size(); ++i) {
     HostMesh& h = *todo[i];
     const Plan& pl = plan[i];
@@ -726,14 +747,17 @@ struct TopoUpload {
   std::vector<TopoHost> th;
   std::vector<size_t> base;
   int cs = 0;
-  unsigned char* stage = nullptr;  // pinned, ctx->pinned[1]
+  int slot = 1;                    // pinned staging slot
+  unsigned char* stage = nullptr;  // pinned, ctx->pinned[slot]
   unsigned char* dev = nullptr;    // shared slab
 };
 
-TopoUpload plan_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, int cs, int npt) {
+TopoUpload plan_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, int cs, int npt,
+                              int slot = 1) {
   TopoUpload up;
   up.meshes = todo;
   up.cs = cs;
+  up.slot = slot;
   up.th.resize(todo.size());
   parallel_for(todo.size(), [&](size_t i) {
     const HostMesh& h = *todo[i];
@@ -745,7 +769,7 @@ TopoUpload plan_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, 
     up.base[i] = total;
     total += up.th[i].total;
   }
-  up.stage = static_cast<unsigned char*>(pinned_stage(ctx, std::max<size_t>(total, 1), 1));
+  up.stage = static_cast<unsigned char*>(pinned_stage(ctx, std::max<size_t>(total, 1), slot));
   AllocScope scope(ctx->stream);
   const std::shared_ptr<unsigned char> all = shared_slab(std::max<size_t>(total, 1), ctx->stream);
   up.dev = all.get();
@@ -764,11 +788,18 @@ void upload_cluster_topos(mrb_ctx* ctx, const TopoUpload& up, size_t i0, size_t 
   });
   const size_t b0 = up.base[i0];
   const size_t b1 = i1 < up.meshes.size() ? up.base[i1] : up.base.back() + up.th.back().total;
+  if (std::getenv("MESHREG_B200_DEBUG")) {
+    char what[64];
+    std::snprintf(what, sizeof what, "topology copy %.1f MB", (b1 - b0) / 1e6);
+    dev_mark(stream, what);
+  }
   ck(mrb_copy_async(up.dev + b0, up.stage + b0, b1 - b0, cudaMemcpyHostToDevice, stream));
-  ck(cudaEventRecord(ctx->stage_done[1], stream));  // staging reusable after this
+  dev_mark(stream, "topology copy done");
+  ck(cudaEventRecord(ctx->stage_done[up.slot], stream));  // staging reusable after this
 }
 
-void ensure_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int cs, int npt) {
+void ensure_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int cs, int npt,
+                          int slot = 1) {
   std::vector<HostMesh*> todo;
   for (HostMesh* h : meshes) {
     const int chunk = int((h->n + cs - 1) / cs);
@@ -786,7 +817,7 @@ void ensure_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, in
                  std::chrono::duration<double, std::milli>(t1 - t0).count());
     t0 = t1;
   };
-  TopoUpload up = plan_cluster_topos(ctx, todo, cs, npt);
+  TopoUpload up = plan_cluster_topos(ctx, todo, cs, npt, slot);
   tick("host plan");
   upload_cluster_topos(ctx, up, 0, up.meshes.size(), ctx->stream);
   tick("fill + copy");
@@ -820,6 +851,7 @@ struct PixelMapJob {
   int W = 0, H = 0;
   unsigned long long* missing = nullptr;  // pinned, one count per map
   cudaEvent_t done = nullptr;
+  std::shared_ptr<unsigned char> slab;    // the maps, when rasterised together
 };
 
 PixelMapJob issue_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int W, int H) {
@@ -850,19 +882,49 @@ PixelMapJob issue_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes,
   ck(cudaMallocAsync(&cnt, job.todo.size() * sizeof(unsigned long long), s));
   ck(cudaMemsetAsync(cnt, 0, job.todo.size() * sizeof(unsigned long long), s));
   job.maps.resize(job.todo.size());
-  for (size_t i = 0; i < job.todo.size(); ++i) {  // every raster before one wait
-    const HostMesh& h = *job.todo[i];
-    job.maps[i] = dalloc<int>(npx);
-    ck(cudaMemsetAsync(job.maps[i], 0x7f, npx * sizeof(int), s));
+  if (job.todo.size() == 1) {
+    const HostMesh& h = *job.todo[0];
+    job.maps[0] = dalloc<int>(npx);
+    ck(cudaMemsetAsync(job.maps[0], 0x7f, npx * sizeof(int), s));
     k_raster<<<unsigned((h.m * 32 + 255) / 256), 256, 0, s>>>(h.dev->V, h.dev->tri, int(h.m), W, H,
-                                                          job.maps[i]);
+                                                          job.maps[0]);
     k_count_uncovered<<<unsigned(std::min<size_t>((npx + 255) / 256, 1184)), 256, 0, s>>>(
-        job.maps[i], int(npx), cnt + i);
+        job.maps[0], int(npx), cnt);
+  } else {
+    // every map in one slab: one memset, then one raster and one count launch
+    // per kRasterJobs meshes
+    const size_t map_bytes = (npx * sizeof(int) + 255) / 256 * 256;
+    job.slab = shared_slab(map_bytes * job.todo.size(), s);
+    ck(cudaMemsetAsync(job.slab.get(), 0x7f, map_bytes * job.todo.size(), s));
+    for (size_t i0 = 0; i0 < job.todo.size(); i0 += kRasterJobs) {
+      const size_t nj = std::min<size_t>(kRasterJobs, job.todo.size() - i0);
+      RasterJobs rj{};
+      int64_t mmax = 0;
+      for (size_t j = 0; j < nj; ++j) {
+        const HostMesh& h = *job.todo[i0 + j];
+        job.maps[i0 + j] = reinterpret_cast<int*>(job.slab.get() + (i0 + j) * map_bytes);
+        rj.V[j] = h.dev->V;
+        rj.tri[j] = h.dev->tri;
+        rj.map[j] = job.maps[i0 + j];
+        rj.m[j] = int(h.m);
+        mmax = std::max(mmax, h.m);
+      }
+      k_raster_many<<<dim3(unsigned((mmax * 32 + 255) / 256), unsigned(nj)), 256, 0, s>>>(rj, W, H);
+      k_count_uncovered_many<<<dim3(unsigned(std::min<size_t>((npx + 255) / 256, 296)),
+                                    unsigned(nj)), 256, 0, s>>>(rj, int(npx), cnt + i0);
+    }
   }
   ck(cudaGetLastError());
+  // installed now so descriptors can be built while the rasters run;
+  // finish_pixel_maps removes the maps of meshes that fail the coverage check
+  for (size_t i = 0; i < job.todo.size(); ++i) {
+    job.todo[i]->dev->pixel_maps[key] = job.maps[i];
+    if (job.slab) job.todo[i]->dev->pixel_map_hold[key] = job.slab;
+  }
   ck(mrb_copy_async(job.missing, cnt, job.todo.size() * sizeof(unsigned long long),
                     cudaMemcpyDeviceToHost, s));
   ck(cudaFreeAsync(cnt, s));
+  dev_mark(s, "rasters done");
   ck(cudaEventCreateWithFlags(&job.done, cudaEventDisableTiming));
   ck(cudaEventRecord(job.done, s));
   return job;
@@ -907,10 +969,11 @@ std::string finish_pixel_maps(mrb_ctx* ctx, PixelMapJob& job) {
         ck(mrb_copy(job.maps[i], host.data(), npx * sizeof(int), cudaMemcpyHostToDevice));
     }
     if (missing && !err.empty()) {
-      dev_free(job.maps[i], ctx->stream);
+      h.dev->pixel_maps.erase(std::make_pair(W, H));
+      h.dev->pixel_map_hold.erase(std::make_pair(W, H));
+      if (!job.slab) dev_free(job.maps[i], ctx->stream);
       continue;
     }
-    h.dev->pixel_maps[std::make_pair(W, H)] = job.maps[i];
   }
   return err;
 }
@@ -987,6 +1050,9 @@ struct mrb_batch {
   std::map<const HostMesh*, size_t> topo_index;  // mesh -> position in topo_up
   size_t topo_done = 0;                           // meshes of topo_up uploaded
   cudaEvent_t topo_ev = nullptr;
+  std::unique_ptr<TopoUpload> tail_up;  // the tail pairs' latency-shape topologies
+  bool tail_done = false;
+  int planned_end = 1 << 30;  // pairs past this got no throughput-shape topology planned
   std::vector<cudaEvent_t> dbg_group_ev;  // MESHREG_B200_DEBUG: start of each group launch
   std::vector<cudaEvent_t> group_ev;
   cudaStream_t copy_stream = nullptr;
@@ -1005,6 +1071,13 @@ struct mrb_batch {
   std::vector<double> h_trace;
   bool synced = false;
   ~mrb_batch() {
+    try {  // topologies installed in the meshes' caches must hold data
+      if (topo_up && topo_done < topo_up->meshes.size())
+        upload_cluster_topos(ctx, *topo_up, topo_done, topo_up->meshes.size(), ctx->stream);
+      if (tail_up && !tail_done)
+        upload_cluster_topos(ctx, *tail_up, 0, tail_up->meshes.size(), ctx->stream);
+    } catch (const CudaError&) {
+    }
     if (graph) cudaGraphExecDestroy(graph);
     for (cudaEvent_t e : group_ev) cudaEventDestroy(e);
     if (topo_ev) cudaEventDestroy(topo_ev);
@@ -1362,6 +1435,19 @@ void flush_topo(mrb_batch* b, int p1, cudaStream_t copy, cudaStream_t s) {
   }
 }
 
+// Deferred tail-shape topologies: pack and copy on `copy` before the tail's
+// launch and make `s` wait for them.
+void flush_tail_topo(mrb_batch* b, cudaStream_t copy, cudaStream_t s) {
+  if (!b->tail_up || b->tail_done) return;
+  upload_cluster_topos(b->ctx, *b->tail_up, 0, b->tail_up->meshes.size(), copy);
+  b->tail_done = true;
+  if (copy != s) {
+    if (!b->topo_ev) ck(cudaEventCreateWithFlags(&b->topo_ev, cudaEventDisableTiming));
+    ck(cudaEventRecord(b->topo_ev, copy));
+    ck(cudaStreamWaitEvent(s, b->topo_ev, 0));
+  }
+}
+
 template <typename TapT, typename Real>
 int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
   KernelTimer dummy;
@@ -1392,6 +1478,7 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
           const int blk1 = p1 < b->n_pairs ? host[p1].pix_blk_begin : b->n_pix_blocks;
           // this group's topologies (host packing overlaps the previous group)
           flush_topo(b, p1, b->copy_stream, s);
+          if (p1 > b->tail_p0) flush_tail_topo(b, b->copy_stream, s);
           if (std::getenv("MESHREG_B200_DEBUG")) {  // device timeline of the groups
             cudaEvent_t e;
             cudaEventCreate(&e);
@@ -1412,6 +1499,7 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
         return launches;
       }
       flush_topo(b, b->n_pairs, s, s);  // deferred topologies not yet uploaded
+      flush_tail_topo(b, s, s);
       tm->mark(-1);
       launches += launch_cluster(b, 0, b->n_pairs);
       tm->mark(0);
@@ -1647,17 +1735,24 @@ void setup_cluster_path(mrb_batch* b) {
   } else if (!choose_cluster_shape(b->ctx, big->h, b->n_pairs, two_u, &cs, &npt, &occ)) {
     return why("no cluster configuration fits");
   }
+  // pairs past planned_end (the expected tail wave of a deferred batch) have
+  // no throughput-shape topology unless setup_tail turns the tail down
+  const int main_end = std::min(b->n_pairs, b->planned_end);
   {  // per-mesh topologies: host thread pool + pinned staged upload
     std::vector<HostMesh*> hm;
-    for (mrb_mesh* m : b->meshes) hm.push_back(&m->h);
+    for (int p = 0; p < main_end; ++p) hm.push_back(&b->meshes[p]->h);
     ensure_cluster_topos(b->ctx, hm, cs, npt);
   }
-  size_t smem = 0;
-  for (mrb_mesh* m : b->meshes) {
-    const int chunk = int((m->h.n + cs - 1) / cs);
-    const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, m->h, cs, chunk, npt);
-    smem = std::max(smem, cluster_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride, two_u));
-  }
+  auto main_smem = [&](int p0, int p1, size_t smem) {
+    for (int p = p0; p < p1; ++p) {
+      HostMesh& h = b->meshes[p]->h;
+      const int chunk = int((h.n + cs - 1) / cs);
+      const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, h, cs, chunk, npt);
+      smem = std::max(smem, cluster_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride, two_u));
+    }
+    return smem;
+  };
+  size_t smem = main_smem(0, main_end, 0);
   if (cluster_occupancy_cs(cs, npt, smem) < 1) return why("no cluster configuration fits");
   b->cluster_cs = cs;
   b->cluster_npt = npt;
@@ -1688,6 +1783,18 @@ void setup_cluster_path(mrb_batch* b) {
     std::fprintf(stderr, "meshreg_b200: cluster %d CTAs x %d nodes/thread, %zu B smem, %s exchange\n",
                  cs, npt, b->push_mode ? b->push_smem : smem, b->push_mode ? "push" : "pull");
   setup_tail(b, smem);
+  if (b->tail_p0 > main_end && main_end < b->n_pairs) {
+    // no tail after all: the remaining pairs need the main shape (staging
+    // slot 2, slot 1 still backs the deferred groups)
+    std::vector<HostMesh*> rest;
+    for (int p = main_end; p < b->n_pairs; ++p) rest.push_back(&b->meshes[p]->h);
+    ensure_cluster_topos(b->ctx, rest, cs, npt, 2);
+    b->cluster_smem = smem = main_smem(main_end, b->n_pairs, smem);
+    if (cluster_occupancy_cs(cs, npt, smem) < 1) {
+      b->cluster_cs = 0;
+      return why("no cluster configuration fits");
+    }
+  }
   build_fast_descriptors(b);
 }
 
@@ -1711,7 +1818,21 @@ void setup_tail(mrb_batch* b, size_t main_smem) {
     return;
   std::vector<HostMesh*> hm;
   for (mrb_mesh* m : tm) hm.push_back(&m->h);
-  ensure_cluster_topos(b->ctx, hm, cs, npt);
+  // own staging slot: slot 1 may still hold deferred wave-group topologies.
+  // With deferred topologies (mrb_register_many) only plan now; the data is
+  // packed and copied just before the tail's launch (flush_tail_topo).
+  if (b->topo_up) {
+    std::vector<HostMesh*> todo;
+    for (HostMesh* h : hm) {
+      const int chunk = int((h->n + cs - 1) / cs);
+      if (!h->dev->topo.count(chunk * 16 + npt) &&
+          std::find(todo.begin(), todo.end(), h) == todo.end())
+        todo.push_back(h);
+    }
+    if (!todo.empty()) b->tail_up.reset(new TopoUpload(plan_cluster_topos(b->ctx, todo, cs, npt, 2)));
+  } else {
+    ensure_cluster_topos(b->ctx, hm, cs, npt, 2);
+  }
   size_t smem = 0, ps = 0;
   bool lists = true;
   for (mrb_mesh* m : tm) {
@@ -2248,10 +2369,16 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
     if (b->real_d)
       for (HostMesh* h : hm) ensure_device_mesh_f64(ctx, *h);
     tick("mesh upload");
-    PixelMapJob pmj = issue_pixel_maps(ctx, hm, W, H);  // rasters run while the host plans
+    PixelMapJob pmj;
+    bool rasters_issued = false;
+    const bool defer = eligible && defer_topo && mode == 1;
+    if (!defer) {  // rasters run while the host plans the topologies
+      pmj = issue_pixel_maps(ctx, hm, W, H);
+      rasters_issued = true;
+    }
     if (eligible) {
-      // fast-path topologies first: their host planning overlaps the mesh and
-      // image uploads still in flight (ensure_pixel_maps synchronises)
+      // fast-path topologies: their host planning overlaps the mesh and image
+      // uploads still in flight (finish_pixel_maps synchronises)
       mrb_mesh* big = *std::max_element(b->meshes.begin(), b->meshes.end(),
                                         [](mrb_mesh* x, mrb_mesh* y) { return x->h.n < y->h.n; });
       int cs = forced_cs, npt = forced_npt, occ = 0;
@@ -2259,18 +2386,39 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
         grid_shape(big->h.n, &cs, &npt);
       if (cs || choose_cluster_shape(ctx, big->h, n_pairs, cfg->smoothing_passes >= 2, &cs, &npt,
                                      &occ)) {
-        if (defer_topo && mode == 1) {  // plan now, pack + copy per wave group in the run
+        if (defer) {  // plan now, pack + copy per wave group in the run
+          // pairs of the expected tail wave (setup_tail) run in the latency
+          // shape: no throughput-shape topology for them
+          int planned = n_pairs;
+          if (npt == 2 && n_pairs > defer_topo && n_pairs % defer_topo &&
+              !std::getenv("MESHREG_B200_NO_TAIL"))
+            planned = n_pairs - n_pairs % defer_topo;
+          b->planned_end = planned;
           std::vector<HostMesh*> todo;
-          for (HostMesh* h : hm) {
+          for (int p = 0; p < planned; ++p) {
+            HostMesh* h = hm[p];
             const int chunk = int((h->n + cs - 1) / cs);
             if (!h->dev->topo.count(chunk * 16 + npt) &&
                 std::find(todo.begin(), todo.end(), h) == todo.end())
               todo.push_back(h);
           }
+          cudaEvent_t slab_ev = nullptr;
           if (!todo.empty()) {
             b->topo_up.reset(new TopoUpload(plan_cluster_topos(ctx, todo, cs, npt)));
             for (size_t i = 0; i < todo.size(); ++i) b->topo_index[todo[i]] = i;
-            flush_topo(b.get(), std::min(defer_topo, n_pairs), ctx->stream, ctx->stream);
+            ck(cudaEventCreateWithFlags(&slab_ev, cudaEventDisableTiming));
+            ck(cudaEventRecord(slab_ev, ctx->stream));  // the slab exists from here on
+          }
+          // rasters after the slab allocation, so the first group's topology
+          // copy (on the batch's copy stream) need not wait for them
+          pmj = issue_pixel_maps(ctx, hm, W, H);
+          rasters_issued = true;
+          if (!todo.empty()) {
+            if (!b->copy_stream)
+              ck(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking));
+            ck(cudaStreamWaitEvent(b->copy_stream, slab_ev, 0));
+            cudaEventDestroy(slab_ev);
+            flush_topo(b.get(), std::min(defer_topo, n_pairs), b->copy_stream, ctx->stream);
           }
         } else {
           ensure_cluster_topos(ctx, hm, cs, npt);
@@ -2278,9 +2426,7 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
       }
       tick("topologies");
     }
-    const std::string msg = finish_pixel_maps(ctx, pmj);
-    if (!msg.empty()) return fail(ctx, MRB_E_COVERAGE, msg);
-    tick("pixel maps");
+    if (!rasters_issued) pmj = issue_pixel_maps(ctx, hm, W, H);
     b->total_nodes = off;
     const size_t npx = size_t(W) * H;
     b->st = dalloc<PairStatus>(n_pairs);
@@ -2310,6 +2456,10 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
       else
         build_pairs<float, float>(b.get());
     }
+    // coverage check last: the host work above overlapped the rasters
+    const std::string msg = finish_pixel_maps(ctx, pmj);
+    if (!msg.empty()) return fail(ctx, MRB_E_COVERAGE, msg);
+    tick("pixel maps");
   } catch (const CudaError& e) {
     return cuda_fail(ctx, e.e);
   }
@@ -2324,7 +2474,7 @@ void batch_set_groups(mrb_batch* b, int per) {
   b->groups.push_back(b->n_pairs);
   b->group_ev.resize(b->groups.size());
   for (auto& e : b->group_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  ck(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking));
+  if (!b->copy_stream) ck(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking));
 }
 }  // namespace
 
@@ -2713,6 +2863,13 @@ int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
         cudaEventElapsedTime(&tg, dbg_t0, b->dbg_group_ev[g]);
         std::fprintf(stderr, "meshreg_b200:   group %zu launch reached at %.2f ms\n", g, tg);
       }
+      for (auto& mk : dev_marks()) {
+        float tm = 0.f;
+        if (cudaEventElapsedTime(&tm, dbg_t0, mk.second) == cudaSuccess)
+          std::fprintf(stderr, "meshreg_b200:   device: %-20s at %.2f ms\n", mk.first.c_str(), tm);
+        cudaEventDestroy(mk.second);
+      }
+      dev_marks().clear();
     }
     if (rc == MRB_E_CUDA && first_err == MRB_OK) {
       first_err = rc;
@@ -2789,6 +2946,7 @@ int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
         ck(mrb_copy_async(dimg + img_bytes, static_cast<const char*>(tmpl) + size_t(p0) * npx * es,
                           img_bytes, cudaMemcpyHostToDevice, ctx->copy));
         ck(cudaEventRecord(ctx->copy_done, ctx->copy));
+        dev_mark(ctx->copy, "images H2D done");
       }
       mrb_batch* b = nullptr;
       stamp("create begin", k);
