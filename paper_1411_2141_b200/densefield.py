@@ -14,7 +14,7 @@ import struct
 import numpy as np
 
 from . import _lib
-from .image import ImageGrid
+from .image import FileFormatError, ImageGrid
 from .mesh import as_mesh
 
 __all__ = ["DenseField", "MeshCoverageError", "PointLocator", "locate", "densify", "warp_image",
@@ -152,10 +152,6 @@ def pixel_map(mesh, width, height):
 
 FIELD_MAGIC = b"MRDF"
 _HEADER = struct.Struct("<4sIII")  # magic, version, width, height (little-endian)
-
-
-class FileFormatError(ValueError):
-    """Malformed image or field file (reference image.py FileFormatError)."""
 
 
 def difference_image(a, b):

@@ -2,17 +2,26 @@
 
 `ImageGrid` keeps the reference's container semantics (image.py:25-131):
 row-major float64 (H, W), read-only, finite-checked.  Sampling and `msd` run
-on the GPU through libmeshreg_b200 (no CPU fallback).  File I/O
-(load_image/save_image) is not on the registration path and is out of scope.
+on the GPU through libmeshreg_b200 (no CPU fallback).  load_image /
+save_image read and write the reference's file formats (image.py:190-296:
+PGM P2/P5 up to 16 bit, PNG through Pillow, rescaled to [0, 255]); they feed
+the command-line front end (cli.py).
 """
 
 from __future__ import annotations
+
+import os
+import re
 
 import numpy as np
 
 from . import _lib
 
-__all__ = ["ImageGrid", "msd"]
+__all__ = ["ImageGrid", "msd", "load_image", "save_image", "FileFormatError"]
+
+
+class FileFormatError(ValueError):
+    """Malformed or unsupported image / field / mesh file (image.py:21-22)."""
 
 
 class ImageGrid:
@@ -108,3 +117,104 @@ def msd(a, b):
     rc = lib.mrb_msd(ctx, da.size, _lib.ptr(da), _lib.ptr(db), _lib.ptr(out))
     _lib.check(rc, ctx, (ValueError, RuntimeError, RuntimeError))
     return float(out[0])
+
+
+# ---- file formats (image.py:190-296) ----------------------------------------
+_PNG_SIGNATURE = b"\x89PNG\r\n\x1a\n"
+_LUMA = (0.299, 0.587, 0.114)  # Rec. 601, as the reference converts colour PNGs
+
+
+def load_image(path):
+    """PGM (P2 text / P5 binary, maxval <= 65535) or PNG -> ImageGrid with
+    intensities rescaled so that full scale is 255.0 (image.py:197-209)."""
+    with open(path, "rb") as fh:
+        head = fh.read(8)
+    if head[:2] in (b"P2", b"P5"):
+        return _read_pgm(path)
+    if head == _PNG_SIGNATURE:
+        return _read_png(path)
+    raise FileFormatError(f"unsupported image format: {path!r}")
+
+
+def save_image(img, path):
+    """8-bit binary PGM or grayscale PNG by extension; values rounded half to
+    even and clamped to [0, 255] (image.py:212-228)."""
+    pix = np.clip(np.rint(img.data), 0, 255).astype(np.uint8)
+    ext = os.path.splitext(str(path))[1].lower()
+    if ext == ".pgm":
+        with open(path, "wb") as fh:
+            fh.write(b"P5\n%d %d\n255\n" % (img.width, img.height))
+            fh.write(pix.tobytes())
+    elif ext == ".png":
+        from PIL import Image as _PIL
+
+        _PIL.fromarray(pix, mode="L").save(path, format="PNG")
+    else:
+        raise ValueError(f"unsupported output extension: {ext!r} (use .pgm or .png)")
+
+
+def _pgm_header(blob):
+    """Width, height and maxval tokens after the magic (comments allowed
+    between tokens), and the offset of the pixel data: one whitespace byte
+    after the last token (image.py:258-276)."""
+    tokens = []
+    pos = 2
+    number = re.compile(rb"[0-9]+")
+    while len(tokens) < 3 and pos < len(blob):
+        c = blob[pos:pos + 1]
+        if c == b"#":
+            end = blob.find(b"\n", pos)
+            pos = len(blob) if end < 0 else end + 1
+        elif c.isspace():
+            pos += 1
+        else:
+            m = number.match(blob, pos)
+            if m is None:
+                raise FileFormatError("malformed PGM header")
+            tokens.append(int(m.group(0)))
+            pos = m.end()
+    return tokens, pos + 1
+
+
+def _read_pgm(path):
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    tokens, body = _pgm_header(blob)
+    if len(tokens) < 3:
+        raise FileFormatError(f"truncated PGM header in {path!r}")
+    width, height, maxval = tokens
+    if width < 1 or height < 1:
+        raise FileFormatError(f"zero-dimension PGM image in {path!r}")
+    if not 0 < maxval <= 65535:
+        raise FileFormatError(f"PGM maxval {maxval} out of range in {path!r}")
+    count = width * height
+    if blob[:2] == b"P2":
+        vals = np.array(blob[body:].split()[:count], dtype=np.float64)
+    else:
+        dt = np.dtype(">u2" if maxval > 255 else "u1")
+        vals = np.frombuffer(blob[body:body + count * dt.itemsize], dtype=dt).astype(np.float64)
+    if vals.size != count:
+        raise FileFormatError(f"PGM pixel data truncated in {path!r}")
+    return ImageGrid(width, height, vals * (255.0 / maxval))
+
+
+def _read_png(path):
+    from PIL import Image as _PIL
+
+    with _PIL.open(path) as im:
+        im.load()
+        if im.width < 1 or im.height < 1:
+            raise FileFormatError(f"zero-dimension PNG image in {path!r}")
+        mode = im.mode
+        if mode == "L":
+            arr = np.asarray(im, dtype=np.float64)
+        elif mode == "LA":
+            arr = np.asarray(im.convert("L"), dtype=np.float64)
+        elif mode in ("I", "I;16", "I;16B", "I;16L"):
+            arr = np.asarray(im, dtype=np.float64) * (255.0 / 65535.0)
+        elif mode in ("RGB", "RGBA", "P"):
+            rgb = np.asarray(im.convert("RGB"), dtype=np.float64)
+            arr = _LUMA[0] * rgb[..., 0] + _LUMA[1] * rgb[..., 1] + _LUMA[2] * rgb[..., 2]
+        else:
+            raise FileFormatError(f"unsupported PNG mode {mode!r} in {path!r}")
+    return ImageGrid(arr.shape[1], arr.shape[0], arr)

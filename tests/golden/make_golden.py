@@ -275,5 +275,117 @@ def main():
                  T=mesh.triangles.copy(), **out, **extra)
 
 
+def _bytes(path):
+    with open(path, "rb") as fh:
+        return np.frombuffer(fh.read(), np.uint8)
+
+
+def _text(path):
+    with open(path, "r", encoding="utf-8") as fh:
+        return np.array(fh.read())
+
+
+def cli_goldens():
+    """The reference CLI itself (cli.py) on small pairs: its input files, the
+    meshes its `mesh` command makes, every file `register` / `bench` /
+    `metrics` write, their exit codes and stdout; plus the reference's image
+    readers on PGM/PNG variants (image.py:190-296)."""
+    import contextlib
+    import io
+    import tempfile
+    from meshreg.cli import main as ref_main
+
+    def run(argv):
+        out, err = io.StringIO(), io.StringIO()
+        with contextlib.redirect_stdout(out), contextlib.redirect_stderr(err):
+            rc = ref_main([str(a) for a in argv])
+        return rc, out.getvalue(), err.getvalue()
+
+    with tempfile.TemporaryDirectory() as td:
+        d = lambda *p: os.path.join(td, *p)  # noqa: E731
+        # the reference's CLI test pair (test_cli.py:13-22)
+        ref = synthetic.smooth_texture(96, 96, seed=5, low=100, high=156)
+        field = synthetic.plateau_shift_field(96, 96, shift=(2.0, 0.0))
+        _, te = synthetic.warped_pair(ref, field)
+        mr.save_image(ref, d("ref.png"))
+        mr.save_image(te, d("template.pgm"))
+        rc_m, out_m, _ = run(["mesh", "--template", d("template.pgm"), "--nodes", 400,
+                              "--seed", 3, "--out", d("m")])
+        assert rc_m == 0
+        rc, out, err = run(["register", "--ref", d("ref.png"), "--template", d("template.pgm"),
+                            "--mesh", d("m", "mesh.json"), "--iters", 40, "--out", d("r")])
+        assert rc == 0, err
+        rec = dict(ref_png=_bytes(d("ref.png")), te_pgm=_bytes(d("template.pgm")),
+                   mesh_json=_text(d("m", "mesh.json")), mesh_node=_text(d("m", "mesh.node")),
+                   mesh_ele=_text(d("m", "mesh.ele")), stdout=np.array(out))
+        for name in ("field.bin", "warped.png", "difference.png"):
+            rec[name.replace(".", "_")] = _bytes(d("r", name))
+        for name in ("mesh.json", "nodes.csv", "report.json", "manifest.json"):
+            rec["out_" + name.replace(".", "_")] = _text(d("r", name))
+        rec["warped"] = mr.load_image(d("r", "warped.png")).data
+        rec["difference"] = mr.load_image(d("r", "difference.png")).data
+        rec["ref"] = mr.load_image(d("ref.png")).data
+        rec["te"] = mr.load_image(d("template.pgm")).data
+
+        # divergence exit code 4 (test_cli.py:165-180) on a reference mesh
+        r2 = synthetic.smooth_texture(96, 96, seed=7, low=40, high=220)
+        bump = synthetic.random_bump_field(96, 96, seed=42, n_bumps=2, max_amplitude=4.0,
+                                           sigma_range=(20, 35))
+        _, t2 = synthetic.warped_pair(r2, bump)
+        mr.save_image(r2, d("r2.pgm"))
+        mr.save_image(t2, d("t2.pgm"))
+        assert run(["mesh", "--template", d("t2.pgm"), "--nodes", 500, "--out", d("m2")])[0] == 0
+        rc4, _, err4 = run(["register", "--ref", d("r2.pgm"), "--template", d("t2.pgm"),
+                            "--mesh", d("m2", "mesh.json"), "--tau", 0.01, "--out", d("o2")])
+        assert rc4 == 4, (rc4, err4)
+        rec.update(div_ref_pgm=_bytes(d("r2.pgm")), div_te_pgm=_bytes(d("t2.pgm")),
+                   div_mesh_json=_text(d("m2", "mesh.json")), div_stderr=np.array(err4))
+
+        # bench over a 3-slice stack, meshes from the reference's `mesh` with the
+        # bench's own budget and seed (test_cli.py:255-268)
+        os.makedirs(d("s"))
+        for i, sl in enumerate(synthetic.slice_stack(48, 48, 3, seed=4, max_shift=1.0)):
+            mr.save_image(sl, d("s", f"s{i}.pgm"))
+            rec[f"slice{i}_pgm"] = _bytes(d("s", f"s{i}.pgm"))
+        for i in range(2):
+            assert run(["mesh", "--template", d("s", f"s{i}.pgm"), "--nodes", 150,
+                        "--out", d("bm", f"s{i}")])[0] == 0
+            rec[f"bench_mesh{i}_json"] = _text(d("bm", f"s{i}", "mesh.json"))
+        rcb, outb, errb = run(["bench", "--dir", d("s"), "--nodes", 150, "--iters", 15,
+                               "--out", d("b")])
+        assert rcb == 0, errb
+        rec["bench_json"] = _text(d("b", "bench.json"))
+
+        rcx, outx, _ = run(["metrics", "--ref", d("ref.png"), "--template", d("template.pgm"),
+                            "--out", d("x")])
+        assert rcx == 0
+        rec["metrics_stdout"] = np.array(outx)
+
+        # image readers: P2 with comments, 16-bit P5, RGB / 16-bit / LA PNGs
+        from PIL import Image as PILImage
+        rng = np.random.default_rng(11)
+        a8 = rng.integers(0, 256, (7, 9)).astype(np.uint8)
+        a16 = rng.integers(0, 65536, (5, 6)).astype(np.uint16)
+        rgb = rng.integers(0, 256, (4, 5, 3)).astype(np.uint8)
+        with open(d("p2.pgm"), "w") as fh:
+            fh.write("P2\n# a comment\n9 7\n# another\n200\n")
+            fh.write(" ".join(str(int(v) * 200 // 255) for v in a8.ravel()) + "\n")
+        with open(d("p5_16.pgm"), "wb") as fh:
+            fh.write(b"P5 6 5 65535\n" + a16.astype(">u2").tobytes())
+        PILImage.fromarray(rgb, mode="RGB").save(d("rgb.png"))
+        PILImage.fromarray(a16.astype(np.int32), mode="I").save(d("i16.png"))
+        PILImage.fromarray(np.dstack([a8, 255 - a8]), mode="LA").save(d("la.png"))
+        for name in ("p2.pgm", "p5_16.pgm", "rgb.png", "i16.png", "la.png"):
+            key = name.replace(".", "_")
+            rec["io_" + key] = _bytes(d(name))
+            rec["io_" + key + "_data"] = mr.load_image(d(name)).data
+        mr.save_image(mr.ImageGrid(9, 7, a8.astype(np.float64) + 0.5), d("w.pgm"))
+        rec["io_saved_pgm"] = _bytes(d("w.pgm"))
+        rec["io_saved_src"] = a8.astype(np.float64) + 0.5
+    save("cli", **rec)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] != ["cli"]:
+        main()
+    cli_goldens()
