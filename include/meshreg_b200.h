@@ -276,6 +276,66 @@ int mrb_sample_gradient(mrb_ctx* ctx, int32_t width, int32_t height, int32_t img
 int mrb_grid_umbrella_smooth(mrb_ctx* ctx, int32_t width, int32_t height, const double* plane,
                              double lam, double* out);
 
+/* ---- content-adaptive mesher (meshgen.py, delaunay.py) -----------------
+ * SURVEY.md §8(f) rows 3-4.  Images are (height, width) row-major float64.
+ * `taps` is the full 2*radius+1 Gaussian kernel the reference's
+ * scipy.ndimage.gaussian_filter builds (_gaussian_kernel1d: np.exp taps
+ * normalised by their sum, radius = int(4*sigma + 0.5)); the Python layer
+ * computes it with numpy so it is bit-identical.  Outputs match the
+ * reference bit for bit. */
+typedef struct mrb_tris mrb_tris;  /* a (V, T) triangulation + TriMesh connectivity */
+
+/* _gradient_magnitude, meshgen.py:99-102 (GPU): hypot of np.gradient of the
+ * Gaussian-smoothed image */
+int mrb_gradient_magnitude(mrb_ctx* ctx, int32_t width, int32_t height, const double* image,
+                           int32_t radius, const double* taps, double* mag);
+/* _canny_edges, meshgen.py:105-132 (GPU): edges = H*W bytes (0/1); mag
+ * (optional) = the gradient magnitude it thresholds */
+int mrb_canny_edges(mrb_ctx* ctx, int32_t width, int32_t height, const double* image,
+                    int32_t radius, const double* taps, double low, double high, uint8_t* edges,
+                    double* mag);
+/* canny_sample, meshgen.py:135-154: up to budget edge points (x, y),
+ * strongest first, thinned to `spacing` (points: budget*2) */
+int mrb_canny_sample(mrb_ctx* ctx, int32_t width, int32_t height, const double* image,
+                     int32_t radius, const double* taps, double low, double high, double spacing,
+                     int64_t budget, double* points, int64_t* count);
+/* halftone_sample's dot mask, meshgen.py:157-203 (host): total = numpy's
+ * pairwise mag.sum(); dots = Floyd-Steinberg of mag*budget/total (all zero
+ * when total <= 1e-12) */
+int mrb_halftone_dots(int32_t width, int32_t height, const double* mag, int64_t budget,
+                      int32_t serpentine_start, uint8_t* dots, double* total);
+/* _SpacingGrid thinning, meshgen.py:80-96 (host): points xy (n*2) visited in
+ * `order` (NULL = 0..n-1), kept while count < budget; out: budget*2 */
+int mrb_spacing_thin(int64_t n, const double* xy, const int64_t* order, double spacing,
+                     int64_t budget, double* out, int64_t* count);
+/* uniform_sample, meshgen.py:219-248 (host); out capacity `cap` points */
+int mrb_uniform_sample(int32_t width, int32_t height, int64_t budget, double* out, int64_t cap,
+                       int64_t* count, char* err, int32_t err_len);
+/* dedupe_points, delaunay.py:30-51 (host); out capacity n points */
+int mrb_dedupe_points(int64_t n, const double* points, double tol, double* out, int64_t* count,
+                      char* err, int32_t err_len);
+/* TriMesh(V, T), mesh.py:59-123: validate + orient (host) */
+int mrb_tris_create(int64_t n_vertices, const double* vertices, int64_t n_triangles,
+                    const int64_t* triangles, mrb_tris** out, char* err, int32_t err_len);
+/* delaunay, delaunay.py:75-91 (host): dedupe, Bowyer-Watson (same triangle
+ * ids as the reference), flip_edges(passes=100).  MRB_E_VALUE = ValueError,
+ * MRB_E_INTERNAL = RuntimeError (insertion point not covered) */
+int mrb_delaunay(int64_t n, const double* points, mrb_tris** out, char* err, int32_t err_len);
+/* flip_edges, delaunay.py:181-199 (host, in place); *changed = sweeps that flipped */
+int mrb_flip_edges(mrb_tris* mesh, int32_t passes, int32_t* changed, char* err, int32_t err_len);
+/* smooth_mesh, meshgen.py:269-327 (host, in place); mag = gradient magnitude
+ * at sigma 1.5 (mrb_gradient_magnitude) */
+int mrb_smooth_mesh(mrb_tris* mesh, int32_t width, int32_t height, const double* mag,
+                    int32_t cvt_iterations, int32_t odt_iterations, char* err, int32_t err_len);
+int mrb_tris_counts(const mrb_tris* mesh, int64_t* n_vertices, int64_t* n_triangles);
+int mrb_tris_export(const mrb_tris* mesh, double* vertices, int64_t* triangles);
+int mrb_tris_destroy(mrb_tris* mesh);
+/* delaunay_violations, delaunay.py:290-309 (GPU): (triangle, vertex) pairs
+ * with the vertex deeper than `margin` inside the circumcircle */
+int mrb_delaunay_violations(mrb_ctx* ctx, int64_t n_vertices, const double* vertices,
+                            int64_t n_triangles, const int64_t* triangles, double margin,
+                            int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -106,6 +106,24 @@ _SIGS = {
     "mrb_pixel_batch_kernel_times": (C.c_int, [_vp, _vp]),
     "mrb_sample_gradient": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp]),
     "mrb_grid_umbrella_smooth": (C.c_int, [_vp, _i32, _i32, _vp, C.c_double, _vp]),
+    # content-adaptive mesher (meshgen.py, delaunay.py)
+    "mrb_gradient_magnitude": (C.c_int, [_vp, _i32, _i32, _vp, _i32, _vp, _vp]),
+    "mrb_canny_edges": (C.c_int, [_vp, _i32, _i32, _vp, _i32, _vp, C.c_double, C.c_double, _vp,
+                                  _vp]),
+    "mrb_canny_sample": (C.c_int, [_vp, _i32, _i32, _vp, _i32, _vp, C.c_double, C.c_double,
+                                   C.c_double, _i64, _vp, _i64p]),
+    "mrb_halftone_dots": (C.c_int, [_i32, _i32, _vp, _i64, _i32, _vp, _dp]),
+    "mrb_spacing_thin": (C.c_int, [_i64, _vp, _vp, C.c_double, _i64, _vp, _i64p]),
+    "mrb_uniform_sample": (C.c_int, [_i32, _i32, _i64, _vp, _i64, _i64p, C.c_char_p, _i32]),
+    "mrb_dedupe_points": (C.c_int, [_i64, _vp, C.c_double, _vp, _i64p, C.c_char_p, _i32]),
+    "mrb_tris_create": (C.c_int, [_i64, _vp, _i64, _vp, C.POINTER(_vp), C.c_char_p, _i32]),
+    "mrb_delaunay": (C.c_int, [_i64, _vp, C.POINTER(_vp), C.c_char_p, _i32]),
+    "mrb_flip_edges": (C.c_int, [_vp, _i32, C.POINTER(_i32), C.c_char_p, _i32]),
+    "mrb_smooth_mesh": (C.c_int, [_vp, _i32, _i32, _vp, _i32, _i32, C.c_char_p, _i32]),
+    "mrb_tris_counts": (C.c_int, [_vp, _i64p, _i64p]),
+    "mrb_tris_export": (C.c_int, [_vp, _vp, _vp]),
+    "mrb_tris_destroy": (C.c_int, [_vp]),
+    "mrb_delaunay_violations": (C.c_int, [_vp, _i64, _vp, _i64, _vp, C.c_double, _i64p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -9,7 +9,7 @@ NVCC=${NVCC:-nvcc}
 $NVCC -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a $MRB_NVCC_FLAGS \
   -Xcompiler -fPIC,-ffp-contract=off -Xptxas -v -shared \
   -I"$HERE/../../include" \
-  "$HERE/meshreg_b200.cu" "$HERE/mesh_host.cpp" -o "$OUT.tmp" 2> "$HERE/../../build_ptxas.log" || {
+  "$HERE/meshreg_b200.cu" "$HERE/mesh_host.cpp" "$HERE/mesher_host.cpp" -o "$OUT.tmp" 2> "$HERE/../../build_ptxas.log" || {
     grep -v "^ptxas info\|^    [0-9]* bytes stack" "$HERE/../../build_ptxas.log" | head -40; exit 1; }
 mv "$OUT.tmp" "$OUT"
 echo "built $OUT"

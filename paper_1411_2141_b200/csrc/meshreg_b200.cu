@@ -3336,3 +3336,6 @@ int mrb_msd(mrb_ctx* ctx, int64_t n, const double* a, const double* b, double* o
 
 // pixel-grid engine (baseline.py)
 #include "pixel_api.cuh"
+
+// content-adaptive mesher (meshgen.py, delaunay.py)
+#include "mesher.cuh"
