@@ -304,6 +304,9 @@ int mrb_canny_sample(mrb_ctx* ctx, int32_t width, int32_t height, const double* 
  * when total <= 1e-12) */
 int mrb_halftone_dots(int32_t width, int32_t height, const double* mag, int64_t budget,
                       int32_t serpentine_start, uint8_t* dots, double* total);
+/* _floyd_steinberg, meshgen.py:157-185 (host): dots of a density map */
+int mrb_floyd_steinberg(int32_t width, int32_t height, const double* density,
+                        int32_t serpentine_start, uint8_t* dots);
 /* _SpacingGrid thinning, meshgen.py:80-96 (host): points xy (n*2) visited in
  * `order` (NULL = 0..n-1), kept while count < budget; out: budget*2 */
 int mrb_spacing_thin(int64_t n, const double* xy, const int64_t* order, double spacing,

@@ -113,6 +113,7 @@ _SIGS = {
     "mrb_canny_sample": (C.c_int, [_vp, _i32, _i32, _vp, _i32, _vp, C.c_double, C.c_double,
                                    C.c_double, _i64, _vp, _i64p]),
     "mrb_halftone_dots": (C.c_int, [_i32, _i32, _vp, _i64, _i32, _vp, _dp]),
+    "mrb_floyd_steinberg": (C.c_int, [_i32, _i32, _vp, _i32, _vp]),
     "mrb_spacing_thin": (C.c_int, [_i64, _vp, _vp, C.c_double, _i64, _vp, _i64p]),
     "mrb_uniform_sample": (C.c_int, [_i32, _i32, _i64, _vp, _i64, _i64p, C.c_char_p, _i32]),
     "mrb_dedupe_points": (C.c_int, [_i64, _vp, C.c_double, _vp, _i64p, C.c_char_p, _i32]),

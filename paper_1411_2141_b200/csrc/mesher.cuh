@@ -406,6 +406,13 @@ int mrb_halftone_dots(int32_t width, int32_t height, const double* mag, int64_t 
   return MRB_OK;
 }
 
+int mrb_floyd_steinberg(int32_t width, int32_t height, const double* density,
+                        int32_t serpentine_start, uint8_t* dots) {
+  if (!density || !dots || width < 1 || height < 1) return MRB_E_VALUE;
+  mrb::floyd_steinberg(density, 1.0, width, height, serpentine_start, dots);
+  return MRB_OK;
+}
+
 int mrb_spacing_thin(int64_t n, const double* xy, const int64_t* order, double spacing,
                      int64_t budget, double* out, int64_t* count) {
   if (!count || (n > 0 && !xy) || (budget > 0 && !out)) return MRB_E_VALUE;

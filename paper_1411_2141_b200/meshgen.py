@@ -161,6 +161,18 @@ def canny_sample(img, cfg, budget):
     return out[: cnt.value].copy()
 
 
+def _floyd_steinberg(density, serpentine_start=0):
+    """Binary dot mask from serpentine Floyd-Steinberg error diffusion of a
+    non-negative density map (meshgen.py:157-185), in native code."""
+    d = np.ascontiguousarray(np.asarray(density, dtype=np.float64))
+    h, w = d.shape
+    dots = np.empty((h, w), np.uint8)
+    rc = _lib.load().mrb_floyd_steinberg(w, h, _lib.ptr(d), int(serpentine_start), _lib.ptr(dots))
+    if rc != _lib.OK:
+        raise ValueError("density must be a non-empty 2-D array")
+    return dots.astype(bool)
+
+
 def _thin(xy, order, spacing, budget):
     xy = np.ascontiguousarray(xy, dtype=np.float64)
     order = None if order is None else np.ascontiguousarray(order, dtype=np.int64)
@@ -182,14 +194,20 @@ def halftone_sample(img, budget, spacing, seed=0):
     budget = int(budget)
     if budget <= 0:
         return np.empty((0, 2))
-    mag = gradient_magnitude(img.data, 1.0)
+    return _halftone_from_mag(gradient_magnitude(img.data, 1.0), budget, spacing, seed)
+
+
+def _halftone_from_mag(mag, budget, spacing, seed):
+    """Host half of halftone_sample: pairwise mass, error diffusion, the
+    seeded permutation and spacing thinning (meshgen.py:196-216)."""
+    mag = np.ascontiguousarray(mag, dtype=np.float64)
     h, w = mag.shape
     rng = np.random.default_rng(seed)
     serpentine = int(rng.integers(2))
     dots = np.empty((h, w), np.uint8)
     total = C.c_double()
-    rc = _lib.load().mrb_halftone_dots(w, h, _lib.ptr(mag), budget, serpentine, _lib.ptr(dots),
-                                       C.byref(total))
+    rc = _lib.load().mrb_halftone_dots(w, h, _lib.ptr(mag), int(budget), serpentine,
+                                       _lib.ptr(dots), C.byref(total))
     if rc != _lib.OK:
         raise ValueError("halftoning failed")
     if total.value <= 1e-12:

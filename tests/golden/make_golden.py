@@ -317,7 +317,15 @@ def cli_goldens():
         assert rc == 0, err
         rec = dict(ref_png=_bytes(d("ref.png")), te_pgm=_bytes(d("template.pgm")),
                    mesh_json=_text(d("m", "mesh.json")), mesh_node=_text(d("m", "mesh.node")),
-                   mesh_ele=_text(d("m", "mesh.ele")), stdout=np.array(out))
+                   mesh_ele=_text(d("m", "mesh.ele")), stdout=np.array(out),
+                   mesh_quality_json=_text(d("m", "quality.json")),
+                   mesh_stdout=np.array(out_m))
+        # register without --mesh: the CLI meshes the template itself
+        rc, out_g, err = run(["register", "--ref", d("ref.png"), "--template", d("template.pgm"),
+                              "--nodes", 300, "--seed", 2, "--iters", 30, "--out", d("g")])
+        assert rc == 0, err
+        rec.update(gen_stdout=np.array(out_g), gen_mesh_json=_text(d("g", "mesh.json")),
+                   gen_report_json=_text(d("g", "report.json")))
         for name in ("field.bin", "warped.png", "difference.png"):
             rec[name.replace(".", "_")] = _bytes(d("r", name))
         for name in ("mesh.json", "nodes.csv", "report.json", "manifest.json"):

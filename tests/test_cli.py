@@ -140,9 +140,9 @@ def test_exit_codes_before_the_gpu(tmp_path, pair, capsys):
     assert cli.main(["register", "--ref", ref, "--template", te, "--config", str(cfg),
                      "--out", o]) == 2
     capsys.readouterr()
-    assert cli.main(["register", "--ref", ref, "--template", te, "--out", o]) == 2
-    assert "pass it with --mesh" in capsys.readouterr().err
-    assert cli.main(["mesh", "--template", te, "--nodes", "25", "--out", o]) == 2
+    assert cli.main(["mesh", "--template", te, "--nodes", "3", "--out", o]) == 2
+    assert "nodes must be an integer >= 4" in capsys.readouterr().err
+    assert cli.main(["mesh", "--out", o]) == 2
     assert cli.main(["mesh", "--template", str(tmp_path / "nope.pgm"), "--out", o]) == 3
     assert not os.path.exists(o)  # nothing written on failure
     one = tmp_path / "one"
@@ -297,3 +297,55 @@ def test_metrics_and_warp_roundtrip(tmp_path, pair, capsys):
     a = mrb.load_image(tmp_path / "r" / "warped.png").data
     b = mrb.load_image(tmp_path / "w" / "warped.png").data
     assert np.abs(a - b).max() <= 1.0 and np.mean(a != b) < 1e-3
+
+
+# ---- the mesher through the CLI (GPU; meshgen.py, cli.py:202-223) --------------
+@pytest.mark.gpu
+def test_mesh_command_matches_reference_cli(tmp_path, pair, capsys):
+    """`mesh --nodes 400 --seed 3`: mesh.node / mesh.ele / mesh.json /
+    quality.json byte-identical to the reference CLI's files."""
+    _, te, _ = pair
+    out = tmp_path / "m"
+    assert cli.main(["mesh", "--template", te, "--nodes", "400", "--seed", "3",
+                     "--out", str(out)]) == 0
+    assert json.loads(capsys.readouterr().out) == json.loads(text("mesh_stdout"))
+    for name in ("mesh.json", "mesh.node", "mesh.ele", "quality.json"):
+        key = {"quality.json": "mesh_quality_json"}.get(name, name.replace(".", "_"))
+        assert (out / name).read_text(encoding="ascii") == text(key), name
+    man = read_json(out / "manifest.json")
+    assert man["command"] == "mesh" and man["seed"] == 3
+    assert man["outputs"] == sorted(["mesh.node", "mesh.ele", "mesh.json", "quality.json"])
+
+
+@pytest.mark.gpu
+def test_register_without_mesh_meshes_the_template(tmp_path, pair, capsys):
+    """`register` with no --mesh meshes the template itself (cli.py:250-258)."""
+    ref, te, _ = pair
+    out = tmp_path / "g"
+    assert cli.main(["register", "--ref", ref, "--template", te, "--nodes", "300", "--seed", "2",
+                     "--iters", "30", "--out", str(out)]) == 0
+    got, want = json.loads(capsys.readouterr().out), json.loads(text("gen_stdout"))
+    assert got["iterations_run"] == want["iterations_run"]
+    assert got["msd_after"] == pytest.approx(want["msd_after"], rel=1e-10)
+    assert (out / "mesh.json").read_text(encoding="ascii") == text("gen_mesh_json")
+    rep, ref_rep = read_json(out / "report.json"), json.loads(text("gen_report_json"))
+    assert relinf(rep["energy_trace"], ref_rep["energy_trace"]) < 1e-12
+
+
+@pytest.mark.gpu
+def test_bench_meshes_each_template_like_the_reference(tmp_path, capsys):
+    """`bench` with no mesh arguments meshes every template with the bench's
+    own budget and seed (cli.py:330-336): same node counts and MSDs."""
+    s = tmp_path / "s"
+    s.mkdir()
+    for i in range(3):
+        put(s / f"s{i}.pgm", G[f"slice{i}_pgm"])
+    out = tmp_path / "b"
+    assert cli.main(["bench", "--dir", str(s), "--nodes", "150", "--iters", "15",
+                     "--out", str(out)]) == 0
+    capsys.readouterr()
+    got, want = read_json(out / "bench.json"), json.loads(text("bench_json"))
+    for p, q in zip(got["pairs"], want["pairs"]):
+        assert p["mesh_nodes"] == q["mesh_nodes"]
+        for key in ("mesh_msd", "pixel_msd", "msd_before"):
+            assert p[key] == pytest.approx(q[key], rel=1e-9), key
