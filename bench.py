@@ -107,11 +107,38 @@ def load_pair(name, used):
     re, te = make_pair(spec, used)
     if os.path.exists(mesh_file(mesh_cfg, used)):
         d = np.load(mesh_file(mesh_cfg, used))
-        V, T, kind = d["V"], d["T"].astype(np.int64), "reference-mesher"
+        V, T = d["V"], d["T"].astype(np.int64)
+        kind = ("package-mesher (bit-identical to the reference mesher)" if "mesher" in d.files
+                else "reference-mesher")
     else:
-        V, T = fallback_mesh(spec.size, spec.target_nodes)
-        kind = "fallback-structured"
+        V, T, kind = package_mesh(spec, te, mesh_cfg, used)
     return re, te, V, T, kind, used
+
+
+def package_mesh(spec, te, mesh_cfg, seed):
+    """The mesh the reference mesher would make (generate_mesh on the
+    template, NodeBudget(target), MeshGenConfig(seed=0)), built
+    by this package's mesher, whose meshes are bit-identical to the
+    reference's (tests/test_mesher.py, C1-C3 at full size).  Untimed; cached
+    in data/meshes.  Used when the reference-mesher cache is absent (a fresh
+    checkout, or C5, where the reference mesher would need ~10 h)."""
+    from paper_1411_2141_b200 import ImageGrid, MeshGenConfig, NodeBudget, generate_mesh
+    try:
+        m = generate_mesh(ImageGrid(spec.size, spec.size, te.astype(np.float64)),
+                          NodeBudget(spec.target_nodes), MeshGenConfig(seed=0))
+    except Exception as exc:  # noqa: BLE001 - no GPU: structured stand-in, reported
+        print(f"bench: package mesher unavailable ({exc}); structured mesh", file=sys.stderr)
+        V, T = fallback_mesh(spec.size, spec.target_nodes)
+        return V, T, "fallback-structured"
+    V, T = m.vertices.copy(), m.triangles.copy()
+    try:
+        os.makedirs(MESH_DIR, exist_ok=True)
+        tmp = mesh_file(mesh_cfg, seed) + f".{os.getpid()}.tmp.npz"
+        np.savez_compressed(tmp, V=V, T=T.astype(np.int32), mesher="package")
+        os.replace(tmp, mesh_file(mesh_cfg, seed))
+    except OSError:
+        pass
+    return V, T, "package-mesher (bit-identical to the reference mesher)"
 
 
 # --------------------------------------------------------------------------- clocks
@@ -224,6 +251,7 @@ def run_ours(args, rank, world, local):
     from paper_1411_2141_b200 import _lib
 
     torch.cuda.set_device(local)
+    os.environ["MESHREG_B200_DEVICE"] = str(local)  # the package's default context (mesher)
     dist = dist_init("nccl", local) if world > 1 else None
     device = torch.device("cuda", local)
     lib = _lib.load()
@@ -332,7 +360,7 @@ def run_ours(args, rank, world, local):
             "steps": args.steps, "warmup": max(args.warmup, 3),
             "ms_per_step": round(t_ms / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
-            "data": "synthetic (seeded BASELINE generator; meshes from the reference mesher)",
+            "data": "synthetic (seeded BASELINE generator; content-adaptive meshes of the reference mesher algorithm, see config.mesh)",
             "config": {
                 "workload": f"{args.workload}: {P} pairs/GPU of {W}x{H}, {iters} iterations, "
                             f"{pairs[0][4]} meshes (~{int(np.mean([len(p[2]) for p in pairs]))} nodes)",
@@ -379,9 +407,12 @@ def run_ours(args, rank, world, local):
 def run_e2e(args, lib, ctx, pairs, cfg, W, H, world, dist, device):
     """The same work through the public pipelined C-ABI call mrb_register_many
     from pinned host buffers: per-pair device mesh setup (upload, pixel map,
-    fast-path topology), H2D images, registration, D2H of u / ux / uy /
-    warped / statuses.  Host mesh connectivity (mrb_mesh_build, the
-    counterpart of the reference's TriMesh built by its mesher) is untimed."""
+    fast-path topology), H2D images, registration including the dense pass,
+    and D2H of what the reference's register returns (u and the report:
+    iterations, energy trace, MSD before / after, status; solver.py:148-208).
+    A second figure adds the D2H of the dense field and warped image (what
+    the CLI writes).  Host mesh connectivity (mrb_mesh_build, the counterpart
+    of the reference's TriMesh built by its mesher) is reported separately."""
     import torch
     from paper_1411_2141_b200 import _lib
 
@@ -392,41 +423,48 @@ def run_e2e(args, lib, ctx, pairs, cfg, W, H, world, dist, device):
     n_tot = sum(len(p[2]) for p in pairs)
     u_h = torch.empty((n_tot, 2), dtype=torch.float64).pin_memory()
     dense_h = [torch.empty((P, H, W), dtype=torch.float32).pin_memory() for _ in range(3)]
+    trace_h = torch.empty((P, cfg.max_iterations), dtype=torch.float64).pin_memory()
+    msd_h = torch.empty((2, P), dtype=torch.float64).pin_memory()
     iters = np.zeros(P, np.int32)
     codes = np.zeros(P, np.int32)
-    times = []
-    tot_iters = 0
-    h2d = d2h = 0
     steps = max(1, min(args.steps, 5))
     cnt = np.zeros(2, np.int64)
+    res = {}
     setup_times = []
-    for step in range(1 + steps):  # one untimed warm-up step
-        ts = time.perf_counter()
-        handles = mesh_handles(lib, [(p[2], p[3]) for p in pairs])  # host mesh (mesher output)
-        if step:
-            setup_times.append(time.perf_counter() - ts)
-        arr = (C.c_void_p * P)(*handles)
-        torch.cuda.synchronize()
-        barrier(world, dist)
-        lib.mrb_transfer_bytes(None, None, 1)
-        t0 = time.perf_counter()
-        rc = lib.mrb_register_many(ctx, P, arr, W, H, _lib.F32, re_h.data_ptr(), te_h.data_ptr(),
-                                   C.byref(cfg), 0, _lib.F32, u_h.data_ptr(),
-                                   *(d.data_ptr() for d in dense_h), iters.ctypes.data, None,
-                                   None, None, codes.ctypes.data, None, 0)
-        dt = time.perf_counter() - t0
-        lib.mrb_transfer_bytes(cnt.ctypes.data, cnt[1:].ctypes.data, 1)
-        check(lib, ctx, rc, "e2e register_many")
-        if step:
-            times.append(dt)
-            tot_iters += int(iters.sum())
-            h2d, d2h = int(cnt[0]), int(cnt[1])
-        for h in handles:
-            lib.mrb_mesh_destroy(h)
-    t = reduce_max(sum(times), world, dist, device)
-    value = pairqueue.job_throughput(float(npx) * tot_iters, t, world)
+    for variant in ("report", "dense"):
+        dense = [d.data_ptr() for d in dense_h] if variant == "dense" else [None] * 3
+        times, tot_iters, h2d, d2h = [], 0, 0, 0
+        for step in range(1 + steps):  # one untimed warm-up step
+            ts = time.perf_counter()
+            handles = mesh_handles(lib, [(p[2], p[3]) for p in pairs])  # host mesh (mesher output)
+            if step and variant == "report":
+                setup_times.append(time.perf_counter() - ts)
+            arr = (C.c_void_p * P)(*handles)
+            torch.cuda.synchronize()
+            barrier(world, dist)
+            lib.mrb_transfer_bytes(None, None, 1)
+            t0 = time.perf_counter()
+            rc = lib.mrb_register_many(ctx, P, arr, W, H, _lib.F32, re_h.data_ptr(),
+                                       te_h.data_ptr(), C.byref(cfg), 0, _lib.F32, u_h.data_ptr(),
+                                       *dense, iters.ctypes.data, msd_h[0].data_ptr(),
+                                       msd_h[1].data_ptr(), trace_h.data_ptr(), codes.ctypes.data,
+                                       None, 0)
+            dt = time.perf_counter() - t0
+            lib.mrb_transfer_bytes(cnt.ctypes.data, cnt[1:].ctypes.data, 1)
+            check(lib, ctx, rc, "e2e register_many")
+            if step:
+                times.append(dt)
+                tot_iters += int(iters.sum())
+                h2d, d2h = int(cnt[0]), int(cnt[1])
+            for h in handles:
+                lib.mrb_mesh_destroy(h)
+        t = reduce_max(sum(times), world, dist, device)
+        res[variant] = (pairqueue.job_throughput(float(npx) * tot_iters, t, world), t, h2d, d2h,
+                        tot_iters)
+    value, t, h2d, d2h, tot_iters = res["report"]
     ts = reduce_max(sum(setup_times), world, dist, device)
     with_setup = pairqueue.job_throughput(float(npx) * tot_iters, t + ts, world)
+    dv, dt_, dh2d, dd2h, _ = res["dense"]
     return {"value": round(value, 3), "unit": UNIT, "steps": steps,
             "ms_per_step": round(1e3 * t / steps, 3),
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -434,10 +472,16 @@ def run_e2e(args, lib, ctx, pairs, cfg, W, H, world, dist, device):
             # fused operator: mrb_mesh_build_many on the host) reported separately
             "mesh_setup_ms_per_step": round(1e3 * ts / steps, 3),
             "value_with_mesh_setup": round(with_setup, 3),
+            "with_dense_outputs": {"value": round(dv, 3), "ms_per_step": round(1e3 * dt_ / steps, 3),
+                                   "h2d_bytes_per_step": dh2d, "d2h_bytes_per_step": dd2h,
+                                   "adds": "D2H of the dense field ux/uy and the warped image "
+                                           "(fp32), what the CLI writes"},
             "api": "mrb_register_many (one chunk: per-mesh setup, H2D, run, D2H)",
             "includes": "device mesh setup (upload, pixel map, fast-path topology), H2D images, "
-                        "full registration, D2H u/ux/uy/warped/status; host mesh connectivity "
-                        "(mrb_mesh_build, the reference's TriMesh) untimed"}
+                        "full registration incl. densify + warp + MSD on the device, D2H of "
+                        "register's results (u, iterations, energy trace, MSD before/after, "
+                        "status); host mesh connectivity (mrb_mesh_build, the reference's "
+                        "TriMesh) reported separately"}
 
 
 # --------------------------------------------------------------------------- CPU legs
@@ -539,7 +583,7 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
         "ms_per_step": round(1e3 * sum(times) / len(times), 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE generator; meshes from the reference mesher)",
+        "data": "synthetic (seeded BASELINE generator; content-adaptive meshes of the reference mesher algorithm, see config.mesh)",
         "config": {"workload": f"{args.workload}: bounded sample of {nproc} pairs per step "
                                f"(one per host core) of {spec.size}x{spec.size}, "
                                f"{it_ref} iterations",
@@ -576,6 +620,7 @@ def run_pixel(args, rank, world, local):
     from paper_1411_2141_b200 import _lib
 
     torch.cuda.set_device(local)
+    os.environ["MESHREG_B200_DEVICE"] = str(local)  # the package's default context (mesher)
     dist = dist_init("nccl", local) if world > 1 else None
     device = torch.device("cuda", local)
     lib = _lib.load()
