@@ -77,6 +77,10 @@ struct ClusterPair {
   double* wpart;              // [2][CS][kWarps] energy partials by parity
   int* gbad;                  // [CS] sticky non-finite gradient flags
   unsigned* bar;              // grid barrier counter (zeroed before each launch)
+  // k_grid_flags: [CS][SLOTS/32] bit per slot read by another CTA's halo
+  // (only those slots publish exchange words); null = publish every slot
+  const uint32_t* exports;
+  int tap_evict_first;        // k_grid_flags: L2 policy of the tap loads (see ld_row4_pol)
 };
 
 // Four copies of the padded (H+2)x(W+2) (Te, Re) image; copy s holds padded
@@ -167,6 +171,16 @@ __device__ __forceinline__ void ld_row4(const float2* p, float2 (&t)[4]) {
                : "=f"(t[0].x), "=f"(t[0].y), "=f"(t[1].x), "=f"(t[1].y), "=f"(t[2].x),
                  "=f"(t[2].y), "=f"(t[3].x), "=f"(t[3].y)
                : "l"(p));
+}
+
+// ld_row4 with an L2 cache-eviction policy (createpolicy): the whole-GPU
+// kernel marks the taps evict_first when the image copies exceed L2, so the
+// per-iteration constants (topology, coordinates) stay resident instead.
+__device__ __forceinline__ void ld_row4_pol(const float2* p, float2 (&t)[4], uint64_t pol) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=f"(t[0].x), "=f"(t[0].y), "=f"(t[1].x), "=f"(t[1].y), "=f"(t[2].x),
+                 "=f"(t[2].y), "=f"(t[3].x), "=f"(t[3].y)
+               : "l"(p), "l"(pol));
 }
 
 // Catmull-Rom window of (Te, Re) at (x, y) (ImageGrid.sample, image.py:73-84,

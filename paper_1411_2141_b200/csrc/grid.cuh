@@ -374,6 +374,11 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   float* xs = reinterpret_cast<float*>(s_dyn);
   float2* xu0 = reinterpret_cast<float2*>(xs + X + (X & 1));
   uint32_t* halo = reinterpret_cast<uint32_t*>(xu0 + X);
+  // per-slot state kept in SMEM, not registers (NPT = 8 spilled it to local
+  // memory, whose traffic competed with the taps for L2): u at the start of
+  // the previous iteration (deferred control) and the residual
+  float2* xsave = reinterpret_cast<float2*>(halo + d.halo_stride + (d.halo_stride & 1));
+  float* xr = reinterpret_cast<float*>(xsave + SLOTS);
 
   if (t == 0) {
     s_stop = 0;
@@ -393,18 +398,44 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   int* const gbad = d.gbad;            // [4][CS]
 
   float2 u[NPT];
-  float2 u_save[NPT];  // u at the start of the previous iteration (deferred control)
-  float r[NPT];
-  unsigned own_mask = 0;
+  // NPT = 8 keeps u_save / r in SMEM (in registers they spill); smaller NPT
+  // keeps them in registers
+  constexpr bool kSmemState = NPT >= 8;  // NPT = 8: u_save / r in SMEM (registers spill)
+  float2 u_save[kSmemState ? 1 : NPT];
+  float r_reg[kSmemState ? 1 : NPT];
+  auto save_u = [&](int j, float2 v) {
+    if constexpr (kSmemState) xsave[t + j * kClusterThreads] = v; else u_save[j] = v;
+  };
+  auto saved_u = [&](int j) {
+    if constexpr (kSmemState) return xsave[t + j * kClusterThreads]; else return u_save[j];
+  };
+  auto set_r = [&](int j, float v) {
+    if constexpr (kSmemState) xr[t + j * kClusterThreads] = v; else r_reg[j] = v;
+  };
+  auto get_r = [&](int j) {
+    if constexpr (kSmemState) return xr[t + j * kClusterThreads]; else return r_reg[j];
+  };
+  uint64_t tap_pol;
+  if (d.tap_evict_first)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(tap_pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(tap_pol));
+  unsigned own_mask = 0, exp_mask = 0;
+  constexpr int WORDS = SLOTS / 32;
 #pragma unroll
   for (int j = 0; j < NPT; ++j) {
     const int slot = t + j * kClusterThreads;
     own_mask |= unsigned(slot < d.chunk && rank * d.chunk + slot < d.n) << j;
+    const unsigned ex =
+        d.exports ? (__ldg(d.exports + size_t(rank) * WORDS + (slot >> 5)) >> (slot & 31)) & 1u
+                  : 1u;
+    exp_mask |= ex << j;
     u[j] = make_float2(0.f, 0.f);
-    u_save[j] = u[j];
-    r[j] = 0.f;
+    save_u(j, u[j]);
+    set_r(j, 0.f);
   }
 #define OWN(j) ((own_mask >> (j)) & 1u)
+#define EXPORTED(j) ((exp_mask >> (j)) & 1u)
   __syncthreads();
   const int nhalo = s_nhalo;
   auto control = [&](int kk) {  // control warp, every CTA identically
@@ -484,12 +515,14 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
           const Window w = locate(d, V.x + double(u[j].x), V.y + double(u[j].y));
           float2 tap[4][4];
 #pragma unroll
-          for (int row = 0; row < 4; ++row) ld_row4(w.base + size_t(row) * d.pitch, tap[row]);
+          for (int row = 0; row < 4; ++row)
+            ld_row4_pol(w.base + size_t(row) * d.pitch, tap[row], tap_pol);
           const float2 s = combine(w, tap);
-          r[j] = s.x - s.y;
+          const float rj = s.x - s.y;
+          set_r(j, rj);
           xs[slot] = s.x;
-          put_tagged(xg_s + size_t(rank) * SLOTS + slot, s.x, e);
-          e2 = fma(double(r[j]), double(r[j]), e2);
+          if (EXPORTED(j)) put_tagged(xg_s + size_t(rank) * SLOTS + slot, s.x, e);
+          e2 = fma(double(rj), double(rj), e2);
         }
       }
 #pragma unroll
@@ -503,11 +536,11 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     // every CTA, so no flag of iteration k is published.
     if (s_stop) {
 #pragma unroll
-      for (int j = 0; j < NPT; ++j) u[j] = u_save[j];
+      for (int j = 0; j < NPT; ++j) u[j] = saved_u(j);
       break;
     }
 #pragma unroll
-    for (int j = 0; j < NPT; ++j) u_save[j] = u[j];
+    for (int j = 0; j < NPT; ++j) save_u(j, u[j]);
     for (int h = t; h < nhalo; h += kClusterThreads) {  // the s_te halo, as it arrives
       const uint32_t c = halo[h];
       xs[SLOTS + h] = get_tagged(xg_s + size_t(c >> 16) * SLOTS + (c & 0xffffu), e);
@@ -529,13 +562,16 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
           gx = fmaf(ge.x, sj, gx);
           gy = fmaf(ge.y, sj, gy);
         });
-        const float dx = r[j] * gx, dy = r[j] * gy;  // solver.py:189
+        const float rj = get_r(j);
+        const float dx = rj * gx, dy = rj * gy;  // solver.py:189
         bad |= !isfinite(dx) || !isfinite(dy);
         const float2 v = make_float2(u[j].x - tau * dx, u[j].y - tau * dy);  // solver.py:133
         xu0[slot] = v;
-        uint2* w = xg_u + (size_t(rank) * SLOTS + slot) * 2;
-        put_tagged(w, v.x, e);
-        put_tagged(w + 1, v.y, e);
+        if (passes > 0 && EXPORTED(j)) {
+          uint2* w = xg_u + (size_t(rank) * SLOTS + slot) * 2;
+          put_tagged(w, v.x, e);
+          put_tagged(w + 1, v.y, e);
+        }
       }
     }
     const int anybad = __syncthreads_or(bad);  // also: u0 published by all threads
@@ -592,7 +628,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   if (k == max_iter) {  // the loop ran out: settle the last two decisions
     if (s_stop) {       // control(max_iter - 2) stopped: undo step max_iter - 1
 #pragma unroll
-      for (int j = 0; j < NPT; ++j) u[j] = u_save[j];
+      for (int j = 0; j < NPT; ++j) u[j] = saved_u(j);
     } else if (warp == kCtlWarp) {
       control(k - 1);
     }
@@ -606,6 +642,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     }
   }
 #undef OWN
+#undef EXPORTED
   __syncthreads();
   if (rank == 0 && t == 0) {
     PairStatus s{};

@@ -1039,6 +1039,7 @@ struct mrb_batch {
   size_t tail_smem = 0;
   bool tail_push = false;
   void* xbuf = nullptr;    // grid path exchange buffers (shared by the pairs, run in turn)
+  uint32_t* xexports = nullptr;  // grid path: per pair [CS][SLOTS/32] export bitmaps
   unsigned* xbar = nullptr;  // grid barrier counter + gbad flags [1 + CS]
   // wave groups (mrb_register_many): the first run launches the fast path per
   // group of pairs and records group_ev[g]; get_results then copies group g
@@ -1088,7 +1089,7 @@ struct mrb_batch {
     }
     void* ptrs[] = {pairs, st, blk_pair, pix_blk_pair, partials, pix_partials, state, traces,
                     img, stage, src_ptrs, img_ptrs, dense, u_out, conv, cpairs, img_pad,
-                    prof_host ? nullptr : phase_prof, xbuf, xbar};
+                    prof_host ? nullptr : phase_prof, xbuf, xbar, xexports};
     if (prof_host) cudaFreeHost(prof_host);
     for (void* p : ptrs) dev_free(p, ctx ? ctx->stream : nullptr);
   }
@@ -1653,6 +1654,13 @@ int device_sms() {
   return std::max(n, 1);
 }
 
+size_t device_l2_bytes() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrL2CacheSize, dev);
+  return size_t(std::max(n, 1));
+}
+
 constexpr int kGridMaxNpt = 8;
 // A single pair with at least this many nodes runs faster on the whole-GPU
 // grid than on one 16-CTA cluster (measured: C2, 12k nodes, 0.79 vs 0.98 ms;
@@ -1702,9 +1710,23 @@ void grid_shape(int64_t nmax, int* cs, int* npt) {
   while (int64_t(*npt) * kClusterThreads < per) *npt *= 2;
 }
 
-size_t grid_dyn_smem(int npt, int halo_stride, bool two_u) {
-  const size_t X = size_t(kClusterThreads) * npt + halo_stride;
-  return X * 4 + 8 + X * 8 * (two_u ? 2 : 1) + size_t(halo_stride) * 4 + 64;
+size_t grid_dyn_smem(int npt, int halo_stride, bool two_u, bool flags = false) {
+  const size_t slots = size_t(kClusterThreads) * npt, X = slots + halo_stride;
+  // k_grid_flags adds u_save (float2) + residual (float) per slot
+  return X * 4 + 8 + X * 8 * (two_u ? 2 : 1) + size_t(halo_stride) * 4 + 64 +
+         (flags && npt >= 8 ? slots * 12 + 8 : 0);
+}
+
+// exports[src][slot >> 5] |= bit: slots some other CTA's halo reads
+__global__ void k_mark_exports(const uint32_t* __restrict__ halo, const int* __restrict__ n_halo,
+                               int hs, int cs, int words, uint32_t* __restrict__ exports) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cs * hs; i += gridDim.x * blockDim.x) {
+    const int r = i / hs, h = i - r * hs;
+    if (h >= __ldg(n_halo + r)) continue;
+    const uint32_t c = __ldg(halo + i);
+    const uint32_t slot = c & 0xffffu;
+    atomicOr(exports + size_t(c >> 16) * words + (slot >> 5), 1u << (slot & 31));
+  }
 }
 
 void build_fast_descriptors(mrb_batch* b);
@@ -1927,6 +1949,26 @@ void build_fast_descriptors(mrb_batch* b) {
     c.gbad = nullptr;
     c.bar = nullptr;
     c.flags = nullptr;
+    c.exports = nullptr;
+    {
+      // taps evict_first when the four image copies exceed half of L2 (C5)
+      const size_t img_bytes = 4 * b->pad_plane * sizeof(float2);
+      const char* te = std::getenv("MESHREG_B200_TAP_EVICT");  // "first" / "normal"
+      c.tap_evict_first = te ? std::string(te) == "first" : img_bytes > device_l2_bytes() / 2;
+    }
+    if (b->grid_mode && b->grid_flags && !b->xexports) {
+      const int words = kClusterThreads * b->cluster_npt / 32;
+      b->xexports = dalloc<uint32_t>(size_t(b->n_pairs) * cs * words);
+      ck(cudaMemsetAsync(b->xexports, 0, sizeof(uint32_t) * b->n_pairs * cs * words,
+                         b->ctx->stream));
+    }
+    if (b->grid_mode && b->grid_flags) {
+      const int words = kClusterThreads * b->cluster_npt / 32;
+      k_mark_exports<<<std::max(1, std::min(1024, (cs * t.halo_stride + 255) / 256)), 256, 0,
+                       b->ctx->stream>>>(t.halo, t.n_halo, t.halo_stride, cs, words,
+                                         b->xexports + size_t(p) * cs * words);
+      ck(cudaGetLastError());
+    }
     if (b->grid_mode) {  // exchange buffers shared by the pairs (launched in turn)
       const size_t slots = size_t(cs) * kClusterThreads * b->cluster_npt;
       char* x = static_cast<char*>(b->xbuf);
@@ -1936,6 +1978,13 @@ void build_fast_descriptors(mrb_batch* b) {
                                           (2 * slots * 16 + 255) / 256 * 256);
       c.bar = b->xbar;
       if (b->grid_flags) {
+        // export bitmap of this pair's topology (built below, once per batch)
+        const int words = kClusterThreads * b->cluster_npt / 32;
+        // publish only exported slots at NPT = 8 (C5: 2% faster); smaller
+        // NPT publishes every slot (measured faster, C2/C3)
+        const char* xe = std::getenv("MESHREG_B200_GRID_EXPORTS");  // "all" / "sel"
+        const bool sel = xe ? std::string(xe) == "sel" : b->cluster_npt >= 8;
+        c.exports = sel ? b->xexports + size_t(p) * cs * words : nullptr;
         c.flags = b->xbar + 1;
         c.gbad = reinterpret_cast<int*>(b->xbar + 1 + 3 * size_t(cs) * kFlagStride);
       } else {
@@ -1959,7 +2008,7 @@ void setup_grid_path(mrb_batch* b, int64_t nmax) {
     const int chunk = int((m->h.n + cs - 1) / cs);
     hs = std::max(hs, ensure_cluster_topo(b->ctx, m->h, cs, chunk, npt).halo_stride);
   }
-  const size_t smem = grid_dyn_smem(npt, hs, b->cfg.smoothing_passes >= 2);
+  size_t smem = grid_dyn_smem(npt, hs, b->cfg.smoothing_passes >= 2, true);
   auto fit = [&](auto kern) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
         cudaSuccess) {
@@ -1984,6 +2033,7 @@ void setup_grid_path(mrb_batch* b, int64_t nmax) {
              : npt == 4 ? fit(k_grid_flags<4>) : fit(k_grid_flags<8>);
   if (per_sm < 1) {
     flags = false;
+    smem = grid_dyn_smem(npt, hs, b->cfg.smoothing_passes >= 2, false);
     per_sm = npt == 1 ? fit(k_grid_register<1>) : npt == 2 ? fit(k_grid_register<2>)
              : npt == 4 ? fit(k_grid_register<4>) : fit(k_grid_register<8>);
   }
