@@ -18,6 +18,7 @@
 #include "mesher_host.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -406,6 +407,7 @@ struct BowyerWatson {
   std::vector<uint32_t> stamp;
   uint32_t epoch = 0;
   bool check_full = false;    // MESHREG_B200_BW_CHECK: compare with the full scan
+  mutable int64_t st_steps = 0, st_walk_fail = 0, st_scan = 0, st_cavity = 0;
 
   int64_t count() const { return int64_t(alive.size()); }
 
@@ -441,6 +443,7 @@ struct BowyerWatson {
   int64_t walk(int64_t t, const double* p) const {
     const int64_t limit = count() + 16;
     for (int64_t s = 0; s < limit && t >= 0; ++s) {
+      ++st_steps;
       if (!alive[t]) return -1;
       int64_t next = -2;
       for (int k = 0; k < 3; ++k) {
@@ -494,12 +497,41 @@ struct BowyerWatson {
     PySet2 set;
     std::vector<int64_t> scan_bad;
     int64_t last = 0;
+    // Walk start (jump-and-walk): a coarse grid over the points remembers a
+    // triangle made by the latest insertion in each cell.  The points come in
+    // lexicographic (x, y) order, so `last` alone can be a whole column away.
+    // The start does not change the result, only the walk length.
+    const int64_t G = std::max<int64_t>(1, int64_t(std::sqrt(double(n) / 2.0)));
+    const double gw = std::max(hi[0] - lo[0], 1e-300), gh = std::max(hi[1] - lo[1], 1e-300);
+    std::vector<int64_t> cell_tri(size_t(G * G), -1);
+    auto cell_of = [&](const double* q) {
+      int64_t cx = int64_t((q[0] - lo[0]) / gw * double(G));
+      int64_t cy = int64_t((q[1] - lo[1]) / gh * double(G));
+      cx = std::min(std::max<int64_t>(cx, 0), G - 1);
+      cy = std::min(std::max<int64_t>(cy, 0), G - 1);
+      return cy * G + cx;
+    };
+    auto start_for = [&](const double* q) {
+      const int64_t c = cell_of(q), cx = c % G, cy = c / G;
+      for (int64_t r = 0; r <= 2; ++r)
+        for (int64_t dy = -r; dy <= r; ++dy)
+          for (int64_t dx = -r; dx <= r; ++dx) {
+            if (std::max(std::llabs(dx), std::llabs(dy)) != r) continue;
+            const int64_t x = cx + dx, y = cy + dy;
+            if (x < 0 || y < 0 || x >= G || y >= G) continue;
+            const int64_t t = cell_tri[size_t(y * G + x)];
+            if (t >= 0 && alive[t]) return t;
+          }
+      return last;
+    };
     for (int64_t idx = 0; idx < n; ++idx) {
       const double* p = &X[2 * idx];
       const double px = p[0], py = p[1];
       cavity.clear();
       ++epoch;
-      int64_t t0 = walk(last, p);
+      int64_t t0 = walk(start_for(p), p);
+      if (t0 < 0 && alive[last]) t0 = walk(last, p);
+      if (t0 < 0) ++st_walk_fail;
       if (t0 < 0) {
         for (int64_t t = 0; t < count(); ++t)
           if (alive[t] && contains_tol(t, p)) {
@@ -528,6 +560,7 @@ struct BowyerWatson {
       if (queue.empty()) {
         // the reference's full scan decides (and its containing-triangle fallback)
         scanned = true;
+        ++st_scan;
         for (int64_t t = 0; t < count(); ++t)
           if (bad(t, px, py)) cavity.push_back(t);
         if (cavity.empty()) {
@@ -613,8 +646,15 @@ struct BowyerWatson {
           if (i2 != by_end.end()) nbr[3 * a + 2] = i2->second;
         }
       }
-      if (k_new > 0) last = count() - 1;
+      if (k_new > 0) {
+        last = count() - 1;
+        cell_tri[size_t(cell_of(p))] = last;
+      }
     }
+    if (std::getenv("MESHREG_B200_DEBUG"))
+      std::fprintf(stderr, "meshreg_b200: bowyer-watson walk steps %lld, walk fallbacks %lld, "
+                   "full scans %lld\n", (long long)st_steps, (long long)st_walk_fail,
+                   (long long)st_scan);
     T_out.clear();
     for (int64_t t = 0; t < count(); ++t) {
       if (!alive[t]) continue;
@@ -734,8 +774,18 @@ std::string delaunay(const double* points, int64_t n, Tris& out, int& err_kind) 
   BowyerWatson bw;
   const char* chk = std::getenv("MESHREG_B200_BW_CHECK");
   bw.check_full = chk && chk[0] == '1';
+  const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto tick = [&](const char* what) {
+    if (!dbg) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "meshreg_b200: delaunay %-14s %8.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   std::vector<int64_t> T;
   e = bw.run(P, T);
+  tick("bowyer-watson");
   if (!e.empty()) {
     err_kind = e.rfind("insertion", 0) == 0 ? 2 : 1;
     return e;
@@ -743,8 +793,11 @@ std::string delaunay(const double* points, int64_t n, Tris& out, int& err_kind) 
   out.V = std::move(P);
   out.T = std::move(T);
   e = trimesh_init(out);
+  tick("trimesh");
   if (!e.empty()) return e;
-  flip_edges(out, 100, e);
+  const int sweeps = flip_edges(out, 100, e);
+  if (dbg) std::fprintf(stderr, "meshreg_b200: delaunay %d flip sweeps\n", sweeps);
+  tick("flips");
   return e;
 }
 
