@@ -674,29 +674,65 @@ int64_t flip_sweep(const std::vector<double>& V, std::vector<int64_t>& T) {
     int64_t t[2], w[2];
     int cnt;
   };
+  // The reference's edge_map is an insertion-ordered dict keyed by (min, max)
+  // over the half-edges h = 3t + j in order.  Here: bucket the half-edges by
+  // their low vertex (counting sort), pair equal keys inside each bucket, and
+  // order the edges by their first half-edge.
+  const int64_t nv = m > 0 ? *std::max_element(T.begin(), T.end()) + 1 : 0;
+  std::vector<int64_t> start(size_t(nv) + 1, 0), hv(size_t(3 * m)), hid(size_t(3 * m));
+  auto half = [&](int64_t h, int64_t& u, int64_t& v, int64_t& w) {
+    const int64_t t = h / 3, j = h - 3 * t;
+    const int64_t a = T[3 * t + j], b = T[3 * t + (j + 1) % 3];
+    w = T[3 * t + (j + 2) % 3];
+    u = std::min(a, b);
+    v = std::max(a, b);
+  };
+  for (int64_t h = 0; h < 3 * m; ++h) {
+    int64_t u, v, w;
+    half(h, u, v, w);
+    start[size_t(u) + 1]++;
+  }
+  for (int64_t i = 0; i < nv; ++i) start[size_t(i) + 1] += start[size_t(i)];
+  {
+    std::vector<int64_t> fillp(start.begin(), start.end() - 1);
+    for (int64_t h = 0; h < 3 * m; ++h) {
+      int64_t u, v, w;
+      half(h, u, v, w);
+      const int64_t k = fillp[size_t(u)]++;
+      hv[size_t(k)] = v;
+      hid[size_t(k)] = h;  // ascending within a bucket
+    }
+  }
+  std::vector<int64_t> first_of(size_t(3 * m), -1);  // first half-edge -> edge slot
   std::vector<Ent> ents;
   ents.reserve(size_t(1.6 * double(m)) + 8);
-  std::unordered_map<uint64_t, int64_t> where;
-  where.reserve(size_t(3 * m));
-  for (int64_t t = 0; t < m; ++t) {
-    const int64_t a = T[3 * t], b = T[3 * t + 1], c = T[3 * t + 2];
-    const int64_t trip[3][3] = {{a, b, c}, {b, c, a}, {c, a, b}};
-    for (const auto& r : trip) {
-      const int64_t u = std::min(r[0], r[1]), v = std::max(r[0], r[1]);
-      const uint64_t key = (uint64_t(u) << 32) | uint64_t(v);
-      auto it = where.find(key);
-      if (it == where.end()) {
-        where.emplace(key, int64_t(ents.size()));
-        ents.push_back(Ent{u, v, {t, -1}, {r[2], -1}, 1});
-      } else {
-        Ent& e = ents[it->second];
+  for (int64_t u = 0; u < nv; ++u) {
+    const int64_t b0 = start[size_t(u)], b1 = start[size_t(u) + 1];
+    for (int64_t k = b0; k < b1; ++k) {
+      if (hv[size_t(k)] < 0) continue;  // consumed by an earlier half-edge
+      const int64_t v = hv[size_t(k)];
+      Ent e{u, v, {-1, -1}, {-1, -1}, 0};
+      for (int64_t q = k; q < b1; ++q) {
+        if (hv[size_t(q)] != v) continue;
+        int64_t uu, vv, w;
+        half(hid[size_t(q)], uu, vv, w);
         if (e.cnt < 2) {
-          e.t[e.cnt] = t;
-          e.w[e.cnt] = r[2];
+          e.t[e.cnt] = hid[size_t(q)] / 3;
+          e.w[e.cnt] = w;
         }
         e.cnt++;
+        if (q != k) hv[size_t(q)] = -1;
       }
+      first_of[size_t(hid[size_t(k)])] = int64_t(ents.size());
+      ents.push_back(e);
     }
+  }
+  {  // insertion order of the reference's dict: by first half-edge
+    std::vector<Ent> ordered;
+    ordered.reserve(ents.size());
+    for (int64_t h = 0; h < 3 * m; ++h)
+      if (first_of[size_t(h)] >= 0) ordered.push_back(ents[size_t(first_of[size_t(h)])]);
+    ents.swap(ordered);
   }
   struct Cand {
     int64_t u, v, c, q, t1, t2;
