@@ -1057,6 +1057,11 @@ struct mrb_batch {
   std::vector<cudaEvent_t> dbg_group_ev;  // MESHREG_B200_DEBUG: start of each group launch
   std::vector<cudaEvent_t> group_ev;
   cudaStream_t copy_stream = nullptr;
+  // tail wave + its dense pass on a side stream, concurrent with the main
+  // launch's dense pass (enqueue_run)
+  cudaStream_t tail_stream = nullptr;
+  cudaEvent_t tail_fork = nullptr, tail_join = nullptr;
+  cudaStream_t lstream = nullptr;  // launch stream override (nullptr: ctx->stream)
   bool groups_recorded = false;
   size_t cluster_smem = 0;
   int pad_pitch = 0;
@@ -1087,6 +1092,12 @@ struct mrb_batch {
       cudaStreamSynchronize(copy_stream);
       cudaStreamDestroy(copy_stream);
     }
+    if (tail_stream) {
+      cudaStreamSynchronize(tail_stream);
+      cudaStreamDestroy(tail_stream);
+    }
+    if (tail_fork) cudaEventDestroy(tail_fork);
+    if (tail_join) cudaEventDestroy(tail_join);
     void* ptrs[] = {pairs, st, blk_pair, pix_blk_pair, partials, pix_partials, state, traces,
                     img, stage, src_ptrs, img_ptrs, dense, u_out, conv, cpairs, img_pad,
                     prof_host ? nullptr : phase_prof, xbuf, xbar, xexports};
@@ -1223,7 +1234,7 @@ void launch_cluster_t(mrb_batch* b, int p0, int np, int CS, size_t smem) {
   lc.gridDim = dim3(unsigned(np * CS));
   lc.blockDim = dim3(kClusterThreads);
   lc.dynamicSmemBytes = smem;
-  lc.stream = b->ctx->stream;
+  lc.stream = b->lstream ? b->lstream : b->ctx->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CS;
@@ -1378,7 +1389,7 @@ void launch_push_t(mrb_batch* b, int p0, int np, int CS, size_t smem) {
   lc.gridDim = dim3(unsigned(np * CS));
   lc.blockDim = dim3(kClusterThreads);
   lc.dynamicSmemBytes = smem;
-  lc.stream = b->ctx->stream;
+  lc.stream = b->lstream ? b->lstream : b->ctx->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CS;
@@ -1473,10 +1484,35 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
         // per wave group: loop + dense pass + MSD, then an event for the
         // group's device-to-host copies (mrb_batch_get_results)
         const PD* host = reinterpret_cast<const PD*>(b->pairs_host.data());
-        for (size_t g = 0; g + 1 < b->groups.size(); ++g) {
-          const int p0 = b->groups[g], p1 = b->groups[g + 1];
+        static const bool tail_serial = std::getenv("MESHREG_B200_TAIL_SERIAL") != nullptr;
+        const size_t ng = b->groups.size() - 1;
+        // the last group is the tail wave (latency shape, a third of the
+        // SMs): it runs on a side stream from the end of the previous group's
+        // loop, beside that group's dense pass
+        const bool tail_side = !tail_serial && !b->grid_mode && ng >= 2 &&
+                               b->groups[ng - 1] >= b->tail_p0 && b->tail_p0 < b->n_pairs;
+        if (tail_side && !b->tail_stream) {
+          ck(cudaStreamCreateWithFlags(&b->tail_stream, cudaStreamNonBlocking));
+          ck(cudaEventCreateWithFlags(&b->tail_fork, cudaEventDisableTiming));
+          ck(cudaEventCreateWithFlags(&b->tail_join, cudaEventDisableTiming));
+        }
+        auto dense_msd = [&](int p0, int p1, cudaStream_t st_) {
           const int blk0 = host[p0].pix_blk_begin;
           const int blk1 = p1 < b->n_pairs ? host[p1].pix_blk_begin : b->n_pix_blocks;
+          k_dense_fast<<<blk1 - blk0, kPixBlock, 0, st_>>>(
+              static_cast<const ClusterPair*>(b->cpairs), b->st, b->pix_blk_pair, b->pix_partials,
+              blk0);
+          k_msd_final<TapT, Real><<<p1 - p0, kPixBlock, 0, st_>>>(pairs + p0, b->st + p0,
+                                                                 b->pix_partials);
+          launches += 2;
+        };
+        for (size_t g = 0; g < ng; ++g) {
+          const int p0 = b->groups[g], p1 = b->groups[g + 1];
+          if (tail_side && g == ng - 1) {  // launched beside group ng - 2's dense pass
+            ck(cudaStreamWaitEvent(s, b->tail_join, 0));
+            ck(cudaEventRecord(b->group_ev[g], s));
+            continue;
+          }
           // this group's topologies (host packing overlaps the previous group)
           flush_topo(b, p1, b->copy_stream, s);
           if (p1 > b->tail_p0) flush_tail_topo(b, b->copy_stream, s);
@@ -1487,12 +1523,19 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
             b->dbg_group_ev.push_back(e);
           }
           launches += launch_cluster(b, p0, p1 - p0);
-          k_dense_fast<<<blk1 - blk0, kPixBlock, 0, s>>>(static_cast<const ClusterPair*>(b->cpairs),
-                                                         b->st, b->pix_blk_pair, b->pix_partials,
-                                                         blk0);
-          k_msd_final<TapT, Real><<<p1 - p0, kPixBlock, 0, s>>>(pairs + p0, b->st + p0,
-                                                                b->pix_partials);
-          launches += 2;
+          if (tail_side && g == ng - 2) {
+            const int t0 = b->groups[ng - 1], t1 = b->groups[ng];
+            ck(cudaEventRecord(b->tail_fork, s));
+            ck(cudaStreamWaitEvent(b->tail_stream, b->tail_fork, 0));
+            flush_topo(b, t1, b->copy_stream, b->tail_stream);
+            flush_tail_topo(b, b->copy_stream, b->tail_stream);
+            b->lstream = b->tail_stream;
+            launches += launch_cluster(b, t0, t1 - t0);
+            b->lstream = nullptr;
+            dense_msd(t0, t1, b->tail_stream);
+            ck(cudaEventRecord(b->tail_join, b->tail_stream));
+          }
+          dense_msd(p0, p1, s);
           ck(cudaEventRecord(b->group_ev[g], s));
         }
         b->groups_recorded = true;
@@ -1501,6 +1544,38 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
       }
       flush_topo(b, b->n_pairs, s, s);  // deferred topologies not yet uploaded
       flush_tail_topo(b, s, s);
+      static const bool serial = std::getenv("MESHREG_B200_TAIL_SERIAL") != nullptr;
+      if (tm == &dummy && !b->grid_mode && b->tail_p0 > 0 && b->tail_p0 < b->n_pairs && !serial) {
+        // the tail wave holds a third of the SMs for ~1 ms after the main
+        // launch: run it, and then its pairs' dense pass, on a side stream
+        // while the main pairs' dense pass fills the idle SMs
+        const PD* host = reinterpret_cast<const PD*>(b->pairs_host.data());
+        const int tb = host[b->tail_p0].pix_blk_begin;
+        if (!b->tail_stream) {
+          ck(cudaStreamCreateWithFlags(&b->tail_stream, cudaStreamNonBlocking));
+          ck(cudaEventCreateWithFlags(&b->tail_fork, cudaEventDisableTiming));
+          ck(cudaEventCreateWithFlags(&b->tail_join, cudaEventDisableTiming));
+        }
+        launch_shape(b, 0, b->tail_p0, b->cluster_cs, b->cluster_npt, b->push_mode,
+                     b->push_mode ? b->push_smem : b->cluster_smem);
+        ck(cudaEventRecord(b->tail_fork, s));
+        ck(cudaStreamWaitEvent(b->tail_stream, b->tail_fork, 0));
+        b->lstream = b->tail_stream;
+        launch_shape(b, b->tail_p0, b->n_pairs - b->tail_p0, b->tail_cs, b->tail_npt,
+                     b->tail_push, b->tail_smem);
+        b->lstream = nullptr;
+        k_dense_fast<<<b->n_pix_blocks - tb, kPixBlock, 0, b->tail_stream>>>(
+            static_cast<const ClusterPair*>(b->cpairs), b->st, b->pix_blk_pair, b->pix_partials,
+            tb);
+        ck(cudaEventRecord(b->tail_join, b->tail_stream));
+        k_dense_fast<<<tb, kPixBlock, 0, s>>>(static_cast<const ClusterPair*>(b->cpairs), b->st,
+                                             b->pix_blk_pair, b->pix_partials, 0);
+        ck(cudaStreamWaitEvent(s, b->tail_join, 0));
+        k_msd_final<TapT, Real><<<b->n_pairs, kPixBlock, 0, s>>>(pairs, b->st, b->pix_partials);
+        launches += 5;
+        ck(cudaGetLastError());
+        return launches;
+      }
       tm->mark(-1);
       launches += launch_cluster(b, 0, b->n_pairs);
       tm->mark(0);
