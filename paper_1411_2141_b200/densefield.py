@@ -4,7 +4,8 @@ densify and warp_image run on the GPU: the pixel->triangle map is rasterised
 once per (mesh, W, H) with fp64 predicates in numpy's operation order
 (lowest-index tie-break, densefield.py:148-174) and a host fallback for
 pixels the raster leaves unassigned (PointLocator/locate, 62-127).  The MRDF
-and CSV file formats are not on the registration path (out of scope).
+field file and the node CSV (densefield.py:202-251) are written byte-identical
+to the reference's for the command-line front end.
 """
 
 from __future__ import annotations

@@ -1,8 +1,8 @@
 """Mesh file formats of the reference (meshgen.py:400-452): a Triangle-style
 ``<stem>.node`` / ``<stem>.ele`` text pair and a single JSON file, both with
-0-based ids.  The mesher that produces them (generate_mesh) is outside this
-package; these readers let the command-line front end
-register with a mesh made by the reference's ``meshreg mesh``.
+0-based ids.  The package's mesher (meshgen.generate_mesh) and the
+reference's ``meshreg mesh`` both write them; the writers here produce the
+reference's bytes.
 """
 
 from __future__ import annotations

@@ -1,6 +1,6 @@
 """Full-size BASELINE configurations on the GPU against the CPU oracle run
 live (the oracle finishes C2 in ~5 s and C3 in ~20 s), plus size-independent
-properties at full size.  Meshes come from the reference mesher cache
+properties at full size.  Meshes come from the reference-mesher cache
 (data/meshes, produced by tools/make_meshes.py); without it the package
 mesher builds the same meshes.
 
