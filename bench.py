@@ -2,12 +2,20 @@
 """Benchmark of the B200 mesh-registration path (BASELINE.json metric).
 
 Metric: Mpx*iter/s = sum over pairs of W*H*iterations_run / time (SURVEY.md
-§8(d)), whole job over all ranks.  Default workload = BASELINE config 4: a
-batch of 64 independent 512x512 pairs per GPU (config-2 pairs, reference
-mesher meshes, 200 iterations, tau=0.005, lam=0.8, 1 smoothing pass,
-energy_tolerance=0 so every pair runs all 200 iterations).  Pairs shard
-across ranks with no collective ("scaling": "weak": every rank registers its
-own 64-pair batch).
+§8(d)), whole job over all ranks.  Default workload = BASELINE config 4 as
+written: ONE job of 64 independent 512x512 pairs (config-2 pairs, seeds
+0..63, reference-mesher meshes, 200 iterations, tau=0.005, lam=0.8, 1
+smoothing pass, energy_tolerance=0 so every pair runs all 200 iterations)
+sharded across the N GPUs: rank r registers seeds r, r+N, ... ("scaling":
+"strong", no collective on the data path).  `--weak` gives every rank its
+own 64 pairs instead (an extra measurement, not the headline).  Single-pair
+workloads (c1, c2, c3, c5) at N > 1 run one replica per GPU ("replicas
+only": one pair does not shard).
+
+`--gpus N` without a torchrun environment re-launches this script under
+`python -m torch.distributed.run --nproc-per-node N` (127.0.0.1 rendezvous);
+under torchrun, WORLD_SIZE must equal N.  `--dry-run` runs only the
+launcher, the sharding and the cross-rank timing reductions (gloo, no GPU).
 
   value   device time of K runs of the whole registration (loop + dense pass)
           with inputs resident in HBM, CUDA events on the library's stream,
@@ -23,7 +31,8 @@ own 64-pair batch).
           200 iterations, 3 smoothing passes, same metric.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                       [--workload c4|c1|c2|c3|pixel] [--pairs P] [--precision f32|f64]
+                       [--workload c4|c1|c2|c3|c5|pixel] [--pairs P] [--precision f32|f64]
+                       [--weak] [--dry-run]
 """
 from __future__ import annotations
 
@@ -49,7 +58,7 @@ METRIC = "registration throughput (Mpx*iter/s)"
 UNIT = "Mpx*iter/s"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -60,8 +69,12 @@ def parse():
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-pairs", type=int, default=2)
-    return ap.parse_args()
+    ap.add_argument("--cpu-pairs", type=int, default=4)
+    ap.add_argument("--weak", action="store_true",
+                    help="every GPU registers its own --pairs pairs (weak scaling)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher + sharding + timing reductions only (gloo, no GPU)")
+    return ap.parse_args(argv)
 
 
 # --------------------------------------------------------------------------- inputs
@@ -88,17 +101,6 @@ def workload_spec(name):
     spec = CONFIGS["c2" if name in ("c4", "pixel") else name]
     mesh_cfg = spec.name
     return spec, mesh_cfg
-
-
-def cached_seeds(name):
-    spec, mesh_cfg = workload_spec(name)
-    out = set()
-    if os.path.isdir(MESH_DIR):
-        for f in os.listdir(MESH_DIR):
-            pre = f"{mesh_cfg}_s"
-            if f.startswith(pre) and f.endswith(".npz") and f[len(pre):-4].isdigit():
-                out.add(int(f[len(pre):-4]))
-    return out
 
 
 def load_pair(name, used):
@@ -220,6 +222,22 @@ def barrier(world, dist):
     pairqueue.barrier(world)
 
 
+def job_seeds(args, rank, world):
+    """(this rank's pair seeds, pairs in the whole job, scaling)."""
+    P = args.pairs or (64 if args.workload in ("c4", "pixel") else 1)
+    if args.weak:
+        return pairqueue.weak_seeds(rank, P), P * world, "weak"
+    if P < world:  # one pair does not shard: one replica per GPU
+        return list(range(P)), P * world, "weak"
+    return pairqueue.shard_seeds(rank, world, P), P, "strong"
+
+
+def seeds_text(seeds, rank, world, weak):
+    if world == 1 or weak:
+        return f"{seeds[0]}..{seeds[-1]}" if len(seeds) > 1 else str(seeds[0])
+    return f"rank r of {world} owns seeds r, r+{world}, ... (rank 0: {seeds[0]}..{seeds[-1]})"
+
+
 # --------------------------------------------------------------------------- ours
 def mesh_handles(lib, meshes):
     """Host mesh setup for many meshes at once (mrb_mesh_build_many: the
@@ -259,10 +277,9 @@ def run_ours(args, rank, world, local):
     stream = torch.cuda.ExternalStream(lib.mrb_ctx_stream(ctx), device=device)
 
     spec, _ = workload_spec(args.workload)
-    P = args.pairs or (64 if args.workload == "c4" else 1)
-    avail = cached_seeds(args.workload)
-    seeds, used = pairqueue.shard_seeds(rank, P, avail or None)
-    pairs = [load_pair(args.workload, s) for s in used]
+    seeds, total, scaling = job_seeds(args, rank, world)
+    P = len(seeds)
+    pairs = [load_pair(args.workload, s) for s in seeds]
     W = H = spec.size
     iters = spec.iterations
     npx = W * H
@@ -317,7 +334,7 @@ def run_ours(args, rank, world, local):
         lib.mrb_batch_pair_status(batch, p, C.byref(it), None, None, None, None, 0)
         tot_iters += it.value
     work = float(npx) * tot_iters  # px*iter per step on this rank
-    value = pairqueue.job_throughput(work * args.steps, t_ms / 1e3, world)
+    value = pairqueue.job_throughput(work * args.steps, t_ms / 1e3, world, device)
     launches = int(lib.mrb_batch_launches_per_run(batch)) * args.steps
     path_cs = int(lib.mrb_batch_path(batch))
     loop_kernel = lib.mrb_batch_loop_kernel(batch).decode()
@@ -359,16 +376,16 @@ def run_ours(args, rank, world, local):
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3),
             "ms_per_step": round(t_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
+            "scaling": scaling, "vs_baseline": None, "dtype": args.precision,
             "data": "synthetic (seeded BASELINE generator; content-adaptive meshes of the reference mesher algorithm, see config.mesh)",
             "config": {
-                "workload": f"{args.workload}: {P} pairs/GPU of {W}x{H}, {iters} iterations, "
+                "workload": f"{args.workload}: {total} pairs of {W}x{H} in the job"
+                            f"{f' over {world} GPUs' if world > 1 else ''}, {iters} iterations, "
                             f"{pairs[0][4]} meshes (~{int(np.mean([len(p[2]) for p in pairs]))} nodes)",
-                "pairs_per_gpu": P, "global_pairs": P * world, "image": [W, H],
+                "pairs_per_gpu": P, "global_pairs": total, "image": [W, H],
                 "iterations": iters, "tau": 0.005, "lam": 0.8, "smoothing_passes": 1,
                 "energy_tolerance": 0.0, "mesh": pairs[0][4],
-                "pair_seeds": f"{seeds[0]}..{seeds[-1]}",
-                "replicated_pairs": any(p[5] != s for p, s in zip(pairs, seeds)),
+                "pair_seeds": seeds_text(seeds, rank, world, args.weak),
                 "l2": "flushed (256 MiB write) between timed steps, outside the events",
                 "parallelism": f"pair-sharded dp{world} (no collective)",
                 "precision": args.precision,
@@ -459,11 +476,11 @@ def run_e2e(args, lib, ctx, pairs, cfg, W, H, world, dist, device):
             for h in handles:
                 lib.mrb_mesh_destroy(h)
         t = reduce_max(sum(times), world, dist, device)
-        res[variant] = (pairqueue.job_throughput(float(npx) * tot_iters, t, world), t, h2d, d2h,
-                        tot_iters)
+        res[variant] = (pairqueue.job_throughput(float(npx) * tot_iters, t, world, device), t,
+                        h2d, d2h, tot_iters)
     value, t, h2d, d2h, tot_iters = res["report"]
     ts = reduce_max(sum(setup_times), world, dist, device)
-    with_setup = pairqueue.job_throughput(float(npx) * tot_iters, t + ts, world)
+    with_setup = pairqueue.job_throughput(float(npx) * tot_iters, t + ts, world, device)
     dv, dt_, dh2d, dd2h, _ = res["dense"]
     return {"value": round(value, 3), "unit": UNIT, "steps": steps,
             "ms_per_step": round(1e3 * t / steps, 3),
@@ -522,29 +539,43 @@ def cpu_baseline(args, pairs, spec, iters=None):
                       f"(loop + densify + warp + MSD), {tot:.1f} s"}
 
 
-def _ref_worker(conn, workload, seed, iters):
+def _ref_worker(conn, workload, seeds, iters):
+    """One host core of the reference arm: its share of the job's pairs."""
     os.environ["OMP_NUM_THREADS"] = "1"
-    if workload == "pixel":
-        re, te = make_pair(CONFIGS["c2"], seed)
-    else:
-        re, te, V, T, kind, used = load_pair(workload, seed)
+    jobs = []
+    for seed in seeds:
+        if workload == "pixel":
+            jobs.append(make_pair(CONFIGS["c2"], seed))
+        else:
+            jobs.append(load_pair(workload, seed)[:4])
     conn.send("ready")
+
+    def one(job, it):
+        if workload == "pixel":
+            return _oracle_pixelwise(job[0], job[1], it)
+        return _oracle_register(*job, it)
+
     while True:
         msg = conn.recv()
         if msg == "stop":
             break
-        if workload == "pixel":
-            conn.send(_oracle_pixelwise(re, te, iters))
+        if msg == "warm":  # untimed: page in numpy/scipy and this core's first pair
+            conn.send([one(jobs[0], 2)])
         else:
-            conn.send(_oracle_register(re, te, V, T, iters))
+            conn.send([one(job, iters) for job in jobs])
 
 
 def run_reference(args, rank, world):
+    """The reference algorithm on the host cores: the whole job (all its
+    pairs — the same config as our arm), one process per core, each
+    registering its share of the pairs in turn."""
     if rank != 0:
         return  # rank 0 alone runs the CPU reference arm
     import multiprocessing as mp
     spec, _ = workload_spec(args.workload)
     P = args.pairs or (64 if args.workload in ("c4", "pixel") else 1)
+    if args.weak:
+        P *= world
     cores = len(os.sched_getaffinity(0))
     nproc = max(1, min(P, cores))
     env_bak = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS",
@@ -557,20 +588,22 @@ def run_reference(args, rank, world):
     procs, conns = [], []
     for i in range(nproc):
         a, b = ctx.Pipe()
-        p = ctx.Process(target=_ref_worker, args=(b, args.workload, i, it_ref))
+        p = ctx.Process(target=_ref_worker,
+                        args=(b, args.workload, list(range(i, P, nproc)), it_ref))
         p.start()
         procs.append(p)
         conns.append(a)
     for c in conns:
         c.recv()
+    warm = max(args.warmup, 3)
     times, work = [], 0.0
-    for step in range(max(args.warmup, 3) + args.steps):
+    for step in range(warm + args.steps):
         t0 = time.perf_counter()
         for c in conns:
-            c.send("go")
-        res = [c.recv() for c in conns]
+            c.send("warm" if step < warm else "go")
+        res = [r for c in conns for r in c.recv()]
         dt = time.perf_counter() - t0
-        if step >= max(args.warmup, 3):
+        if step >= warm:
             times.append(dt)
             work += sum(float(spec.size) ** 2 * it for _, it in res)
     for c in conns:
@@ -578,21 +611,26 @@ def run_reference(args, rank, world):
     for p in procs:
         p.join()
     value = work / sum(times) / 1e6
+    same = it_ref == (PIXEL_ITERS if args.workload == "pixel" else spec.iterations)
     out = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
-        "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "n_gpus": world, "steps": args.steps, "warmup": warm,
         "ms_per_step": round(1e3 * sum(times) / len(times), 2), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if P >= world and not args.weak else "weak", "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic (seeded BASELINE generator; content-adaptive meshes of the reference mesher algorithm, see config.mesh)",
-        "config": {"workload": f"{args.workload}: bounded sample of {nproc} pairs per step "
-                               f"(one per host core) of {spec.size}x{spec.size}, "
-                               f"{it_ref} iterations",
-                   "pairs_per_step": nproc, "image": [spec.size, spec.size],
-                   "iterations": it_ref, "energy_tolerance": 0.0},
+        "config": {"workload": f"{args.workload}: {P} pairs of {spec.size}x{spec.size} in the job, "
+                               f"{it_ref} iterations"
+                               + ("" if same else " (bounded sample of the iterations)"),
+                   "global_pairs": P, "image": [spec.size, spec.size],
+                   "iterations": it_ref, "energy_tolerance": 0.0, "same_config": same,
+                   "pair_seeds": f"0..{P - 1}"},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": nproc, "kind": "port",
-                         "sample": f"{nproc} pairs per step, one process per core, oracle port "
-                                   "of meshreg " + ("register_pixelwise" if args.workload == "pixel"
-                                                    else "register") + " (numpy/scipy, float64)"},
+                         "sample": f"all {P} pairs per timed step ({it_ref} iterations each), one "
+                                   f"process per host core ({nproc}), oracle port of meshreg "
+                                   + ("register_pixelwise" if args.workload == "pixel"
+                                      else "register") + " (numpy/scipy, float64); warm-up steps "
+                                   "run 2 iterations of one pair per core"},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -627,9 +665,10 @@ def run_pixel(args, rank, world, local):
     ctx = _lib.context(local)
     stream = torch.cuda.ExternalStream(lib.mrb_ctx_stream(ctx), device=device)
     spec = CONFIGS["c2"]
-    P = args.pairs or 64
-    seeds, used = pairqueue.shard_seeds(rank, P, None)
-    pairs = [make_pair(spec, s) for s in used]
+    seeds, total, scaling = job_seeds(args, rank, world)
+    used = seeds
+    P = len(seeds)
+    pairs = [make_pair(spec, s) for s in seeds]
     W = H = spec.size
     npx = W * H
     prec = _lib.PREC_F32 if args.precision == "f32" else _lib.PREC_F64
@@ -673,7 +712,8 @@ def run_pixel(args, rank, world, local):
     for p in range(P):
         lib.mrb_pixel_batch_pair_status(batch, p, C.byref(it), None, None, None, None, 0)
         tot_iters += it.value
-    value = pairqueue.job_throughput(float(npx) * tot_iters * args.steps, t_ms / 1e3, world)
+    value = pairqueue.job_throughput(float(npx) * tot_iters * args.steps, t_ms / 1e3, world,
+                                     device)
     launches = int(lib.mrb_pixel_batch_launches_per_run(batch)) * args.steps
 
     # e2e: pinned host stacks -> set_images (H2D) -> run -> get_results (D2H) -> sync
@@ -701,7 +741,8 @@ def run_pixel(args, rank, world, local):
             if step:
                 times.append(dt)
         t = reduce_max(sum(times), world, dist, device)
-        e2e = {"value": round(pairqueue.job_throughput(float(npx) * tot_iters * steps, t, world), 3),
+        e2e = {"value": round(pairqueue.job_throughput(float(npx) * tot_iters * steps, t, world,
+                                                       device), 3),
                "unit": UNIT, "steps": steps, "ms_per_step": round(1e3 * t / steps, 3),
                "h2d_bytes_per_step": int(cnt[0]), "d2h_bytes_per_step": int(cnt[1]),
                "api": "mrb_pixel_batch_set_images(host) + run + get_results + sync",
@@ -734,13 +775,15 @@ def run_pixel(args, rank, world, local):
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3),
             "ms_per_step": round(t_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
+            "scaling": scaling, "vs_baseline": None, "dtype": args.precision,
             "data": "synthetic (seeded BASELINE generator, config-2 pairs)",
-            "config": {"workload": f"pixel: {P} pairs/GPU of {W}x{H}, {PIXEL_ITERS} iterations, "
-                                   f"{PIXEL_PASSES} smoothing passes (reference baseline.py engine)",
-                       "pairs_per_gpu": P, "global_pairs": P * world, "image": [W, H],
+            "config": {"workload": f"pixel: {total} pairs of {W}x{H} in the job, {PIXEL_ITERS} "
+                                   f"iterations, {PIXEL_PASSES} smoothing passes (reference "
+                                   "baseline.py engine)",
+                       "pairs_per_gpu": P, "global_pairs": total, "image": [W, H],
                        "iterations": PIXEL_ITERS, "tau": 0.005, "lam": 0.8,
-                       "smoothing_passes": PIXEL_PASSES, "pair_seeds": f"{seeds[0]}..{seeds[-1]}",
+                       "smoothing_passes": PIXEL_PASSES,
+                       "pair_seeds": seeds_text(seeds, rank, world, args.weak),
                        "l2": "flushed (256 MiB write) between timed steps, outside the events",
                        "parallelism": f"pair-sharded dp{world} (no collective)",
                        "precision": args.precision},
@@ -760,10 +803,51 @@ def run_pixel(args, rank, world, local):
         dist.destroy_process_group()
 
 
-def main():
-    args = parse()
+def relaunch_under_torchrun(n):
+    """`--gpus N` with no torchrun environment: run this script as N ranks,
+    one process per GPU, through torch.distributed.run (127.0.0.1
+    rendezvous on a free port); rank 0 prints the JSON line."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args, rank, world):
+    """The multi-rank plumbing without a GPU: sharding, barrier, max-over-
+    ranks time and summed work over gloo."""
+    dist = dist_init("gloo", rank) if world > 1 else None
+    seeds, total, scaling = job_seeds(args, rank, world)
+    barrier(world, dist)
+    t = reduce_max(1.0 + rank, world, dist, "cpu")
+    value = pairqueue.job_throughput(float(len(seeds)), t, world, "cpu")
+    gathered = [seeds]
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, seeds)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "scaling": scaling,
+                          "global_pairs": total, "seeds_by_rank": gathered,
+                          "max_time": t, "value": value}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main(argv=None):
+    args = parse(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     rank, world, local = dist_setup()
-    if args.impl == "reference":
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        run_dry(args, rank, world)
+    elif args.impl == "reference":
         run_reference(args, rank, world)
     elif args.workload == "pixel":
         run_pixel(args, rank, world, local)

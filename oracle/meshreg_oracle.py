@@ -10,8 +10,8 @@ Parity pinning: this restatement is checked against golden vectors produced by
 running the reference itself in the build container
 (``tests/golden/make_golden.py`` -> ``tests/golden/*.npz``; test
 ``tests/test_oracle_golden.py``).  The reference ships no golden files of its
-own; its known-answer tests are mirrored in
-``tests/test_oracle_kat.py``.
+own; its known-answer tests are mirrored against the B200
+path in ``tests/test_gpu_parity.py`` (sampling, energy, step, warp KATs).
 
 Third-party arithmetic the reference relies on (not vendored there, not pinned:
 reference pkg/pyproject.toml:10-14): numpy einsum / fancy indexing / dot and
@@ -294,7 +294,7 @@ def step(mesh, u, grad, tau, lam, passes, V=None, domain=None):
 
 
 def register(re, te, mesh, tau=0.005, lam=0.8, max_iterations=100,
-             smoothing_passes=1, energy_tolerance=1e-6, want_dense=True):
+             smoothing_passes=1, energy_tolerance=1e-6, want_dense=True, vec_pixel_map=False):
     """The descent loop of solver.py:148-208 followed by densify/warp/MSD.
 
     Returns (u, info) with info = dict(iterations_run, energy_trace,
@@ -333,7 +333,8 @@ def register(re, te, mesh, tau=0.005, lam=0.8, max_iterations=100,
                 break
     info = dict(iterations_run=len(trace), energy_trace=trace, msd_before=msd(te, re))
     if want_dense:
-        ux, uy = densify(mesh, u, w, h)
+        pmap = pixel_map_vec(mesh, w, h) if vec_pixel_map else None
+        ux, uy = densify(mesh, u, w, h, pmap)
         warped = warp_image(te, ux, uy)
         info.update(ux=ux, uy=uy, warped=warped, msd_after=msd(warped, re))
     return u, info
@@ -424,6 +425,58 @@ def pixel_map(mesh, width, height):
     return tri_of, wts
 
 
+def pixel_map_vec(mesh, width, height, chunk=1 << 16):
+    """The same pixel map as pixel_map(), vectorised over triangles for
+    C5-size meshes (1M triangles; the per-triangle loop takes minutes).
+
+    Triangles are visited in ascending chunks; inside a chunk every
+    (triangle, bbox pixel) candidate is tested with the same fp64 _bary
+    operations, the lowest containing triangle per pixel is kept, and only
+    pixels still unassigned take it — which is the reference's "ascending id,
+    assign if unassigned" rule (densefield.py:155-174).  Checked equal to
+    pixel_map() on the goldens (tests/test_oracle_golden.py)."""
+    V, T = mesh.V, mesh.T
+    tri_of = np.full(height * width, -1, np.int64)
+    wts = np.zeros((height * width, 3))
+    cmin, cmax = V[T].min(axis=1), V[T].max(axis=1)
+    x0 = np.maximum(np.ceil(cmin[:, 0] - BARY_EPS).astype(np.int64), 0)
+    x1 = np.minimum(np.floor(cmax[:, 0] + BARY_EPS).astype(np.int64), width - 1)
+    y0 = np.maximum(np.ceil(cmin[:, 1] - BARY_EPS).astype(np.int64), 0)
+    y1 = np.minimum(np.floor(cmax[:, 1] + BARY_EPS).astype(np.int64), height - 1)
+    nx = np.maximum(x1 - x0 + 1, 0)
+    ny = np.maximum(y1 - y0 + 1, 0)
+    for c0 in range(0, mesh.m, chunk):
+        tids = np.arange(c0, min(c0 + chunk, mesh.m))
+        cnt = nx[tids] * ny[tids]
+        tt = np.repeat(tids, cnt)
+        if tt.size == 0:
+            continue
+        k = np.arange(tt.size) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+        xx = x0[tt] + k % nx[tt]
+        yy = y0[tt] + k // nx[tt]
+        w = _bary(V, T[tt], xx.astype(np.float64), yy.astype(np.float64))
+        ok = np.min(w, axis=1) >= -BARY_EPS
+        tt, w, pix = tt[ok], w[ok], (yy * width + xx)[ok]
+        order = np.lexsort((tt, pix))  # per pixel, lowest triangle first
+        pix, tt, w = pix[order], tt[order], w[order]
+        first = np.ones(pix.size, bool)
+        first[1:] = pix[1:] != pix[:-1]
+        pix, tt, w = pix[first], tt[first], w[first]
+        free = tri_of[pix] < 0
+        tri_of[pix[free]] = tt[free]
+        wts[pix[free]] = w[free]
+    tri_of = tri_of.reshape(height, width)
+    wts = wts.reshape(height, width, 3)
+    miss = np.argwhere(tri_of < 0)
+    if miss.size:
+        loc = _locator(mesh)
+        for y, x in miss:
+            t, w = _locate(mesh, loc, float(x), float(y))
+            tri_of[y, x] = t
+            wts[y, x] = w
+    return tri_of, wts
+
+
 def densify(mesh, u, width=None, height=None, pmap=None):
     """densefield.py:130-187."""
     u = np.asarray(u, np.float64)
@@ -444,8 +497,15 @@ def warp_image(te, ux, uy):
     if ux.shape != te.shape:
         raise ValueError(f"field {ux.shape} does not match image {te.shape}")
     h, w = te.shape
-    gx, gy = np.meshgrid(np.arange(w, dtype=np.float64), np.arange(h, dtype=np.float64))
-    return sample(te, gx + ux, gy + uy)
+    ext = pad_ring(te)
+    gx = np.arange(w, dtype=np.float64)
+    out = np.empty((h, w))
+    step = max(1, (1 << 20) // max(w, 1))  # row blocks: bounded (n,4,4) tap arrays
+    for y0 in range(0, h, step):
+        y1 = min(h, y0 + step)
+        gy = np.arange(y0, y1, dtype=np.float64)[:, None]
+        out[y0:y1] = sample(te, gx[None, :] + ux[y0:y1], gy + uy[y0:y1], ext)
+    return out
 
 
 # --------------------------------------------------------------------------

@@ -311,21 +311,24 @@ namespace mrb {
 
 constexpr int kFlagStride = 32;  // unsigned words between flags (one 128-byte line)
 
-// Epoch-tagged exchange words: a value and the epoch it belongs to in one
-// 8-byte word (single-copy atomic), so a consumer polls the data itself —
-// one L2 round trip instead of flag + data.
+// Epoch-tagged exchange words: a value and the epoch it belongs to packed in
+// ONE 64-bit scalar (epoch << 32 | value bits), written and polled with a
+// single b64 relaxed access.  A scalar access is single-copy atomic in the
+// PTX memory model (a .v2.u32 access is not: its halves are separate
+// accesses in unspecified order, so a torn (new epoch, old value) read would
+// be allowed).  A consumer polls the data itself: one L2 round trip instead
+// of flag + data.
 __device__ __forceinline__ void put_tagged(uint2* p, float v, unsigned e) {
-  asm volatile("st.relaxed.gpu.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(__float_as_uint(v)),
-               "r"(e)
-               : "memory");
+  const unsigned long long w =
+      (static_cast<unsigned long long>(e) << 32) | __float_as_uint(v);
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
 }
 __device__ __forceinline__ float get_tagged(const uint2* p, unsigned e) {
-  unsigned v, ep;
+  unsigned long long w;
   do {
-    asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(v), "=r"(ep) : "l"(p)
-                 : "memory");
-  } while (ep != e);
-  return __uint_as_float(v);
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  } while (static_cast<unsigned>(w >> 32) != e);
+  return __uint_as_float(static_cast<unsigned>(w));
 }
 
 // Release-store / acquire-load of an epoch flag at gpu scope.

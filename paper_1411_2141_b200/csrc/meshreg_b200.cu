@@ -17,6 +17,7 @@
 #include <tuple>
 #include <mutex>
 #include <chrono>
+#include <climits>
 #include <condition_variable>
 #include <functional>
 #include <vector>
@@ -2898,12 +2899,12 @@ int mrb_batch_kernel_times(mrb_batch* b, double* out) {
 }
 
 // ---------------------------------------------------------------- pipeline
-int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int32_t W,
-                      int32_t H, int32_t img_dtype, const void* reference, const void* tmpl,
-                      const mrb_config* cfg, int32_t chunk_pairs, int32_t out_dtype, double* u,
-                      void* ux, void* uy, void* warped, int32_t* iterations_run,
-                      double* msd_before, double* msd_after, double* trace, int32_t* codes,
-                      char* messages, int32_t msg_len) {
+static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int32_t W,
+                              int32_t H, int32_t img_dtype, const void* reference,
+                              const void* tmpl, const mrb_config* cfg, int32_t chunk_pairs,
+                              int32_t out_dtype, double* u, void* ux, void* uy, void* warped,
+                              int32_t* iterations_run, double* msd_before, double* msd_after,
+                              double* trace, int32_t* codes, char* messages, int32_t msg_len) {
   // Pipeline: chunk 0 is set up and launched on pipeline stream A.  For every
   // later chunk k the per-mesh device setup (mesh upload, pixel maps,
   // fast-path topologies) runs on the context's own stream while chunk k-1
@@ -3083,10 +3084,10 @@ int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
         cs = b->cluster_cs;
         npt = b->cluster_npt;
       }
-      if (rc == MRB_OK) {
-        cudaStreamWaitEvent(sc->stream, ctx->copy_done, 0);
-        rc = mrb_batch_set_images(b, dimg, dimg + img_bytes, 1);
-      }
+      // unconditionally: the stream-ordered free of dimg below must follow
+      // the H2D into it even when the batch could not be created
+      cudaStreamWaitEvent(sc->stream, ctx->copy_done, 0);
+      if (rc == MRB_OK) rc = mrb_batch_set_images(b, dimg, dimg + img_bytes, 1);
       if (rc == MRB_OK && grouped) {
         try {
           batch_set_groups(b, wave);
@@ -3144,6 +3145,37 @@ int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
   if (dbg_t0) cudaEventDestroy(dbg_t0);
   if (first_err != MRB_OK) return fail(ctx, first_err, first_msg);
   return MRB_OK;
+}
+
+// Every pair gets a status: pairs the run never reached (an early failure —
+// invalid config, coverage, a CUDA error in the shape probe or a later
+// chunk) carry the call's own error code and message instead of a stale
+// zero (MRB_OK) that would read as success.
+int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int32_t W,
+                      int32_t H, int32_t img_dtype, const void* reference, const void* tmpl,
+                      const mrb_config* cfg, int32_t chunk_pairs, int32_t out_dtype, double* u,
+                      void* ux, void* uy, void* warped, int32_t* iterations_run,
+                      double* msd_before, double* msd_after, double* trace, int32_t* codes,
+                      char* messages, int32_t msg_len) {
+  constexpr int32_t kUnset = INT32_MIN;
+  if (codes)
+    for (int32_t p = 0; p < n_pairs; ++p) codes[p] = kUnset;
+  const int rc = register_many_impl(ctx, n_pairs, meshes, W, H, img_dtype, reference, tmpl, cfg,
+                                    chunk_pairs, out_dtype, u, ux, uy, warped, iterations_run,
+                                    msd_before, msd_after, trace, codes, messages, msg_len);
+  if (codes) {
+    const std::string msg =
+        rc != MRB_OK ? std::string(ctx->err) : std::string("internal error: pair not run");
+    for (int32_t p = 0; p < n_pairs; ++p) {
+      if (codes[p] != kUnset) continue;
+      codes[p] = rc != MRB_OK ? rc : MRB_E_INTERNAL;
+      if (messages && msg_len > 0) {
+        std::strncpy(messages + size_t(p) * msg_len, msg.c_str(), size_t(msg_len) - 1);
+        messages[size_t(p) * msg_len + msg_len - 1] = 0;
+      }
+    }
+  }
+  return rc;
 }
 
 // ---------------------------------------------------------------- register

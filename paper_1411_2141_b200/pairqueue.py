@@ -2,7 +2,7 @@
 
 Registrations of distinct pairs are independent (reference SPEC.md:400), so
 the multi-GPU path shards whole pairs across ranks with no data-path
-collective: rank r of N owns its own pair queue.  torch.distributed is only
+collective: rank r of N owns the queue of seeds r, r+N, ... of the job.  torch.distributed is only
 used to align timing windows (barrier) and to take the max of the per-rank
 device times, as the benchmark contract requires.
 """
@@ -11,8 +11,8 @@ from __future__ import annotations
 
 import os
 
-__all__ = ["RankInfo", "rank_info", "shard_seeds", "job_throughput", "max_over_ranks",
-           "barrier"]
+__all__ = ["RankInfo", "rank_info", "shard_seeds", "weak_seeds", "job_throughput",
+           "max_over_ranks", "sum_over_ranks", "barrier"]
 
 
 class RankInfo:
@@ -30,23 +30,38 @@ def rank_info(env=None):
                     int(env.get("LOCAL_RANK", "0")))
 
 
-def shard_seeds(rank, pairs_per_rank, available=None):
-    """Seeds of rank's pair queue (weak scaling: every rank registers its own
-    `pairs_per_rank` pairs, seeds rank*P .. rank*P+P-1).  When `available`
-    (the seeds with cached meshes) is given, seeds outside it are replaced by
-    seed % len(available) — replicas of cached pairs; the caller reports it."""
-    seeds = [rank * pairs_per_rank + i for i in range(pairs_per_rank)]
-    if available is None:
-        return seeds, seeds
-    avail = sorted(available)
-    used = [s if s in available else avail[s % len(avail)] for s in seeds]
-    return seeds, used
+def shard_seeds(rank, world, total):
+    """Strong scaling (BASELINE config 4 as written): the job is `total`
+    pairs, seeds 0..total-1, and rank r of `world` owns seeds r, r+world,
+    r+2*world, ... — disjoint queues that together cover the job once."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside a world of {world}")
+    return list(range(rank, total, world))
 
 
-def job_throughput(px_iters_per_rank, seconds, world):
-    """Whole-job Mpx*iter/s: every rank processed the same amount of work in
-    at most `seconds` (the max over ranks)."""
-    return world * float(px_iters_per_rank) / seconds / 1e6
+def weak_seeds(rank, per_rank):
+    """Weak scaling (reported as an extra only): rank r registers its own
+    `per_rank` pairs, seeds r*per_rank .. r*per_rank + per_rank - 1."""
+    return [rank * per_rank + i for i in range(per_rank)]
+
+
+def job_throughput(px_iters, seconds, world=1, device=None):
+    """Whole-job Mpx*iter/s: the px*iter of ALL ranks (summed over the
+    process group) over the job's time (the max over ranks, taken by the
+    caller)."""
+    return sum_over_ranks(float(px_iters), world, device) / seconds / 1e6
+
+
+def sum_over_ranks(value, world, device=None):
+    """Sum of a per-rank scalar over the default process group."""
+    if world <= 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64,
+                     device=device if device is not None else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
 
 
 def max_over_ranks(value, world, device=None):

@@ -263,13 +263,28 @@ def register_batch(references, templates, meshes, cfg=None, *, precision=None,
     mb = np.zeros(P)
     ma = np.zeros(P)
     trace = np.zeros((P, cfg.max_iterations))
-    codes = np.zeros(P, np.int32)
+    codes = np.full(P, -1, np.int32)  # -1: never written (cannot read as OK)
     msg_len = 512
     msgs = C.create_string_buffer(P * msg_len)
-    lib.mrb_register_many(ctx, P, arr, W, H, dt, _lib.ptr(re), _lib.ptr(te), C.byref(c),
+    rc = lib.mrb_register_many(ctx, P, arr, W, H, dt, _lib.ptr(re), _lib.ptr(te), C.byref(c),
                           int(chunk_pairs), _lib.F64, _lib.ptr(u_all), *(_lib.ptr(d) for d in dense),
                           _lib.ptr(iters), _lib.ptr(mb), _lib.ptr(ma), _lib.ptr(trace),
                           _lib.ptr(codes), msgs, msg_len)
+    if rc == _lib.E_COVERAGE and P > 1:
+        # a mesh that does not cover the image stops the whole call (the
+        # pixel maps are built for the batch at once); the reference raises
+        # MeshCoverageError for that pair only, so run the pairs one by one
+        out = []
+        for a, b, m in zip(references, templates, meshes):
+            try:
+                out.append(register(a, b, m, cfg, precision=precision, return_dense=return_dense))
+            except (ValueError, DivergenceError, MeshCoverageError) as e:
+                out.append(e)
+        return out
+    if rc in (_lib.E_CUDA, _lib.E_INTERNAL) or (codes < 0).any():
+        # a device / library failure is not a per-pair outcome: raise it
+        _lib.check(rc if rc != _lib.OK else _lib.E_INTERNAL, ctx,
+                   (ValueError, DivergenceError, MeshCoverageError))
     out = []
     off = 0
     for p, m in enumerate(meshes):

@@ -41,24 +41,29 @@ def check_register(g, precision, name):
     cfg = cfg_of(g)
     u, rep, (ux, uy, warped) = mrb.register(re, te, mesh, cfg, precision=precision,
                                             return_dense=True)
-    tol = TOL[precision]
-    if name == "c1_x255" and precision == "f32":
-        # 34 px of motion over 100 iterations: fp32 drift is amplified
-        tol = dict(u=3e-3, dense=3e-3, msd=3e-3, trace=1e-4)
-    assert rep.iterations_run == int(g["iterations_run"])
-    assert relinf(rep.energy_trace, g["trace"]) <= tol["trace"], name
+    tol = TOL[precision]  # the same tolerances for every case, large motion included
+    err = dict(trace=relinf(rep.energy_trace, g["trace"]))
     if np.abs(g["u"]).max() > 0:
-        assert relinf(u, g["u"]) <= tol["u"], (name, relinf(u, g["u"]))
+        err["u"] = relinf(u, g["u"])
+    if "ux" in g.files:
+        if np.abs(g["ux"]).max() > 0:
+            err["ux"], err["uy"] = relinf(ux, g["ux"]), relinf(uy, g["uy"])
+        err["warped"] = relinf(warped, g["warped"])
+        ref = float(g["msd_after"])
+        err["msd_after"] = abs(rep.msd_after - ref) / max(ref, 1e-300)
+    print(f"\n{name} {precision}: " + " ".join(f"{k} {v:.2e}" for k, v in err.items()))
+    assert rep.iterations_run == int(g["iterations_run"])
+    assert err["trace"] <= tol["trace"], (name, err)
+    if "u" in err:
+        assert err["u"] <= tol["u"], (name, err)
     else:
         assert np.abs(u).max() < 1e-12
     assert abs(rep.msd_before - float(g["msd_before"])) <= tol["msd"] * max(float(g["msd_before"]), 1e-300)
-    if "ux" in g.files:
-        if np.abs(g["ux"]).max() > 0:
-            assert relinf(ux, g["ux"]) <= tol["dense"], name
-            assert relinf(uy, g["uy"]) <= tol["dense"], name
-        assert relinf(warped, g["warped"]) <= tol["dense"], name
-        ref = float(g["msd_after"])
-        assert abs(rep.msd_after - ref) <= tol["msd"] * max(ref, 1e-300), (rep.msd_after, ref)
+    for k in ("ux", "uy", "warped"):
+        if k in err:
+            assert err[k] <= tol["dense"], (name, err)
+    if "msd_after" in err:
+        assert err["msd_after"] <= tol["msd"], (name, err)
 
 
 @pytest.mark.parametrize("precision", ["f64", "f32"])
@@ -372,3 +377,37 @@ def test_register_batch_wave_groups_deferred_topologies(monkeypatch):
         u_ref, info = O.register(g["re"], g["te"], O.Mesh(g["V"], g["T_in"]), tau=0.001, lam=0.8,
                                  max_iterations=20, smoothing_passes=1, energy_tolerance=0.0)
         assert np.abs(out[k][0] - u_ref).max() <= 1e-4 * max(np.abs(u_ref).max(), 1e-30)
+
+
+def test_register_batch_reports_call_level_failures():
+    """A failure that stops mrb_register_many before any pair ran (here: one
+    mesh does not cover the image, found while the batch's pixel maps are
+    built) never reads as success: the uncovered pair gets the reference's
+    MeshCoverageError, the others their results; an invalid configuration
+    makes every pair carry the ValueError."""
+    g = golden("gen64")
+    re, te = images(g)
+    good = mrb.TriMesh(g["V"], g["T_in"])
+    small = mrb.TriMesh([(0, 0), (40, 0), (0, 40), (40, 40)], [(0, 1, 2), (1, 3, 2)])
+    cfg = mrb.SolverConfig(tau=0.001, max_iterations=10, energy_tolerance=0.0)
+    for precision in ("f32", "f64"):
+        out = mrb.register_batch([re, re], [te, te], [good, small], cfg, precision=precision)
+        assert isinstance(out[1], mrb.MeshCoverageError), out[1]
+        u1, rep1 = mrb.register(re, te, good, cfg, precision=precision)
+        assert np.array_equal(out[0][0], u1) and out[0][1].energy_trace == rep1.energy_trace
+    import ctypes as C
+    from paper_1411_2141_b200 import _lib
+    lib = _lib.load()
+    bad = _lib.mrb_config(-1.0, 0.8, 0.0, 10, 1, _lib.PREC_F32, 0)  # tau <= 0
+    arr = (C.c_void_p * 2)(good._h, good._h)
+    P, n = 2, good.n_vertices
+    img = np.ascontiguousarray(np.stack([g["re"], g["re"]]).astype(np.float32))
+    u = np.zeros((P * n, 2))
+    codes = np.zeros(P, np.int32)  # zeros == OK: the library must overwrite them
+    msgs = C.create_string_buffer(P * 256)
+    rc = lib.mrb_register_many(_lib.context(), P, arr, 64, 64, _lib.F32, _lib.ptr(img),
+                               _lib.ptr(img), C.byref(bad), 0, _lib.F64, _lib.ptr(u), None, None,
+                               None, None, None, None, None, _lib.ptr(codes), msgs, 256)
+    assert rc == _lib.E_VALUE
+    assert list(codes) == [_lib.E_VALUE, _lib.E_VALUE]
+    assert b"tau" in msgs.raw[:256]

@@ -53,6 +53,37 @@ def test_oracle_pixel_map_bit_exact(name):
     assert np.array_equal(tri, g["tri_of"])
     if "pm_weights" in g.files:
         assert np.array_equal(wts, g["pm_weights"])
+    # the vectorised map used at C5 size is the same map, bit for bit
+    tri2, wts2 = O.pixel_map_vec(m, w, h, chunk=97)
+    assert np.array_equal(tri2, tri) and np.array_equal(wts2, wts)
+
+
+def test_oracle_warp_image_row_blocks():
+    # the row-blocked warp equals one whole-image sample call
+    g = golden("c1_x255")
+    te = g["te"].astype(np.float64)
+    h, w = te.shape
+    rng = np.random.default_rng(5)
+    ux, uy = rng.normal(0, 3, (2, h, w))
+    gx, gy = np.meshgrid(np.arange(w, dtype=np.float64), np.arange(h, dtype=np.float64))
+    assert np.array_equal(O.warp_image(te, ux, uy), O.sample(te, gx + ux, gy + uy))
+
+
+@pytest.mark.parametrize("name", ["c1_x255", "c1", "gen64_x255"])
+def test_fp32_emulation_meets_north_star_tolerance(name):
+    """fp32 arithmetic itself (tests/f32_emulation.py: what the fast path
+    computes) stays inside the north_star tolerance of the fp64 reference on
+    the large-motion goldens, so the GPU tests can hold the fast path to 1e-4."""
+    from f32_emulation import register32
+    g = golden(name)
+    tau, lam, it, p, tol = g["cfg"]
+    u, trace = register32(g["re"].astype(np.float64), g["te"].astype(np.float64),
+                          O.Mesh(g["V"], g["T_in"]), float(tau), float(lam), int(it), int(p))
+    err = np.abs(u - g["u"]).max() / np.abs(g["u"]).max()
+    print(f"{name}: fp32 emulation u relinf {err:.2e}")
+    assert err < 1e-5
+    n = len(trace)
+    assert np.abs(np.array(trace) - g["trace"][:n]).max() / np.abs(g["trace"]).max() < 1e-5
 
 
 @pytest.mark.parametrize("name", ["gen64", "gen64_x255"])
