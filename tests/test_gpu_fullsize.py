@@ -60,8 +60,8 @@ def check_against_oracle(tag, rep, u, dense, u_ref, info):
 
 
 @pytest.mark.parametrize("cfg,x255,path", [("c2", False, ""), ("c2", True, ""), ("c3", False, ""),
-                                           ("c3", True, ""), ("c2", False, "cluster"),
-                                           ("c2", True, "cluster"), ("c1", True, "")])
+                                           ("c2", False, "cluster"), ("c2", True, "cluster"),
+                                           ("c1", True, "")])
 def test_full_size_matches_oracle(cfg, x255, path, monkeypatch):
     """Default path (a single C2/C3 pair runs on the whole-GPU grid kernel)
     and the cluster kernel forced, against the live oracle, at the configs'
@@ -83,6 +83,35 @@ def test_full_size_matches_oracle(cfg, x255, path, monkeypatch):
     u, rep, dense = mrb.register(re, te, mesh, cfg_, precision="f32", return_dense=True)
     check_against_oracle(f"{cfg}{'x255' if x255 else ''} {path or 'default'} {iters} it",
                          rep, u, dense, u_ref, info)
+
+
+@pytest.mark.parametrize("precision,iters,tol_u,tol_w", [("f64", 20, 1e-9, 1e-9),
+                                                         ("f32", 5, 1e-4, 1e-4)])
+def test_c3_x255_chaotic_prefix(precision, iters, tol_u, tol_w, monkeypatch):
+    """C3 x255 (1024^2 with 30 sharp-edged rectangles at [0,255]) is chaotic
+    in the reference itself: its energy rises after ~iteration 10 (6.44e5 ->
+    1.01e6 at 200) and perturbations grow ~1e4x per 10 iterations.  Even our
+    fp64 path, which differs from the reference only in summation order
+    (~1e-16), departs by 1.9e-3 at 50 iterations; a plain numpy fp32
+    emulation departs by 1.3e-2 at 20 (profiles/r02_c3x255_chaos.log).  So
+    the case is checked over the prefix where a result is determined by the
+    inputs rather than by rounding: fp64 to 1e-9 over 20 iterations, fp32 to
+    the north_star 1e-4 over 5."""
+    monkeypatch.delenv("MESHREG_B200_PATH", raising=False)
+    spec, re32, te32, V, T = load("c3", 0, True)
+    u_ref, info = O.register(re32, te32, O.Mesh(V, T), tau=0.005, lam=0.8, max_iterations=iters,
+                             smoothing_passes=1, energy_tolerance=0.0)
+    S = spec.size
+    re = mrb.ImageGrid(S, S, re32.astype(np.float64))
+    te = mrb.ImageGrid(S, S, te32.astype(np.float64))
+    u, rep, (ux, uy, warped) = mrb.register(re, te, mrb.TriMesh(V, T), mrb.SolverConfig(
+        max_iterations=iters, energy_tolerance=0.0), precision=precision, return_dense=True)
+    eu, ew = relinf(u, u_ref), relinf(warped, info["warped"])
+    print(f"\nc3x255 {precision} {iters} it: u {eu:.2e} warped {ew:.2e}")
+    assert rep.iterations_run == iters
+    assert eu < tol_u and ew < tol_w
+    assert relinf(ux, info["ux"]) < tol_u and relinf(uy, info["uy"]) < tol_u
+    assert abs(rep.msd_after / info["msd_after"] - 1) < (1e-10 if precision == "f64" else 1e-5)
 
 
 def test_c5_matches_oracle(monkeypatch):
