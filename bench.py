@@ -360,11 +360,7 @@ def run_ours(args, rank, world, local):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = kbytes[dom] / (ktimes[dom] / 1e3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        tj = json.load(open(tpath))
-        traffic = tj.get(args.workload, {}).get(args.precision, {}).get(names[dom])
+    ncu = ncu_record(args.workload, args.precision, names[dom])
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -402,16 +398,14 @@ def run_ours(args, rank, world, local):
                                                  else ktimes[0] + ktimes[1] + ktimes[2]), 6),
             "algorithmic_bytes_per_step": alg_bytes,
             "hbm_frac_whole_run": round(alg_bytes / (t_ms / args.steps / 1e3) / 1e9 / peak, 4),
-            "roofline": {"kernel": names[dom], "bound": "hbm", "achieved": round(achieved, 1),
-                         "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
-                         "frac_of_8tbs_nominal": round(achieved / 8000.0, 4),
-                         "note": "achieved = SURVEY 8(d) algorithmic bytes per launch / CUDA-event "
-                                 "time; the persistent kernels serve them from SMEM (topology, "
-                                 "halo exchange) and L2 (image taps), so frac can exceed 1: the "
-                                 "DRAM bytes one launch really moves are `traffic` (ncu, "
-                                 "profiles/ncu_traffic.json)"},
+            "roofline": roofline_block(names[dom], achieved, peak, ncu, ktimes[dom],
+                                       "achieved = SURVEY 8(d) algorithmic bytes per launch / "
+                                       "CUDA-event time (a MODEL rate: the persistent kernels "
+                                       "serve those bytes from SMEM — topology, halo exchange — "
+                                       "and L2 — image taps — so it can exceed the HBM peak); "
+                                       "dram_frac = the DRAM bytes ncu measured per launch "
+                                       "(`traffic`) over the same time; `limiter` = what ncu "
+                                       "shows bounds the kernel"),
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -499,6 +493,37 @@ def run_e2e(args, lib, ctx, pairs, cfg, W, H, world, dist, device):
                         "register's results (u, iterations, energy trace, MSD before/after, "
                         "status); host mesh connectivity (mrb_mesh_build, the reference's "
                         "TriMesh) reported separately"}
+
+
+def ncu_record(workload, precision, kernel):
+    """The ncu capture of this kernel (profiles/ncu_traffic.json): DRAM bytes
+    per launch and the limiter counters."""
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(tpath):
+        return {}
+    rec = json.load(open(tpath)).get(workload, {}).get(precision, {}).get(kernel)
+    if rec is None:
+        return {}
+    return rec if isinstance(rec, dict) else {"dram_bytes": rec}
+
+
+def roofline_block(kernel, achieved, peak, ncu, kernel_ms, note):
+    traffic = ncu.get("dram_bytes")
+    out = {"kernel": kernel, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+           "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+           "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
+           "frac_of_8tbs_nominal": round(achieved / 8000.0, 4)}
+    if traffic:
+        dram = traffic / (kernel_ms / 1e3) / 1e9
+        out["dram_gbs"] = round(dram, 1)
+        out["dram_frac"] = round(dram / peak, 4)
+    if ncu.get("limiter"):
+        out["limiter"] = ncu["limiter"]
+        out["ncu"] = {k: ncu[k] for k in ("issue_active_pct", "l1tex_pct", "lts_pct",
+                                         "dram_pct", "warps_active_pct", "l2_hit_pct",
+                                         "source") if k in ncu}
+    out["note"] = note
+    return out
 
 
 # --------------------------------------------------------------------------- CPU legs
@@ -755,11 +780,7 @@ def run_pixel(args, rank, world, local):
     es = 4 if args.precision == "f32" else 8
     bytes_launch = float(P) * npx * 6 * es  # read u, write u, read (Te, Re): 3 pairs of Real
     achieved = bytes_launch / (kt[0] / 1e3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("pixel", {}).get(args.precision, {}).get(
-            "k_pixel_iter")
+    ncu = ncu_record("pixel", args.precision, "k_pixel_iter")
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tot, work = 0.0, 0.0
@@ -789,13 +810,9 @@ def run_pixel(args, rank, world, local):
                        "precision": args.precision},
             "gpu_launches": launches,
             "kernel_ms": {"k_pixel_iter": round(float(kt[0]), 5), "run": round(float(kt[1]), 4)},
-            "roofline": {"kernel": "k_pixel_iter", "bound": "hbm", "achieved": round(achieved, 1),
-                         "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
-                         "note": "algorithmic bytes = read u + write u + read (Te, Re) per pixel "
-                                 "per iteration; the kernel is instruction-issue bound (bicubic "
-                                 "value + gradient per pixel, 3 smoothing passes in SMEM)"},
+            "roofline": roofline_block("k_pixel_iter", achieved, peak, ncu, kt[0],
+                                       "algorithmic bytes = read u + write u + read (Te, Re) per "
+                                       "pixel per iteration"),
             "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
         }
         print(json.dumps(out), flush=True)

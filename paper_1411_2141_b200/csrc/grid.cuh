@@ -34,31 +34,23 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned target) {
   __syncthreads();
 }
 
-// one-ring gather over the global SELL-32 topology of this CTA
+// one-ring gather over this CTA's paired SELL topology in global memory
+// (read through L1; layout in write_topo): f(codes of entries 2p | 2p+1 <<
+// 16, row index) for the slice's warp-uniform pair-row count
 template <typename F>
-__device__ __forceinline__ void ring_gather_g(const uint16_t* __restrict__ code,
-                                              const float2* __restrict__ g, uint32_t so, int deg,
-                                              F&& f) {
-#pragma unroll
-  for (int e0 = 0; e0 < kMaxDeg; e0 += 8) {
-    if (e0 < deg) {
-      uint32_t c[8];
-      float2 ge[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const bool in = e0 + e < deg;
-        c[e] = in ? __ldg(code + so + 32u * (e0 + e)) : 0u;
-        ge[e] = in ? __ldg(g + so + 32u * (e0 + e)) : make_float2(0.f, 0.f);
-      }
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (e0 + e < deg) f(c[e], ge[e]);
-    }
+__device__ __forceinline__ void ring_pairs_g(const uint32_t* __restrict__ code2, uint32_t sw,
+                                             int lane, F&& f) {
+  const uint32_t base = (sw & 0xffffffu) + uint32_t(lane);
+  const int np = int(sw >> 24);
+#pragma unroll 2
+  for (int q = 0; q < np; ++q) {
+    const uint32_t at = base + 32u * uint32_t(q);
+    f(__ldg(code2 + at), at);
   }
 }
 
 template <int NPT>
-__global__ void __launch_bounds__(kClusterThreads, 1)
+__global__ void __launch_bounds__(kClusterThreads, kClusterMinBlocks)
     k_grid_register(const ClusterPair* __restrict__ pairs, PairStatus* __restrict__ st,
                     int max_iter, double tol, float tau, float lam, int passes) {
   constexpr int SLOTS = kClusterThreads * NPT;
@@ -84,8 +76,13 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   }
   for (int q = t; q < d.halo_stride; q += kClusterThreads)
     halo[q] = d.halo[size_t(rank) * d.halo_stride + q];
-  const uint16_t* code = d.codes + size_t(rank) * d.topo_stride;
-  const float2* gco = d.g + size_t(rank) * d.topo_stride;
+  const uint32_t* code2 = reinterpret_cast<const uint32_t*>(d.codes + size_t(rank) * d.topo_stride);
+  const float4* g4 = reinterpret_cast<const float4*>(d.g + size_t(rank) * d.topo_stride);
+  if (t == 0) {  // ZERO slot of the padding entries
+    xs[X - 1] = 0.f;
+    xu0[X - 1] = make_float2(0.f, 0.f);
+    if (passes >= 2) xu1[X - 1] = make_float2(0.f, 0.f);
+  }
   const uint32_t* soff = d.slice_off + size_t(rank) * d.slices;
   float* xg_s = d.xg_s;
   float2* xg_u0 = d.xg_u;
@@ -207,14 +204,16 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       if (OWN(j)) {
         const int slot = t + j * kClusterThreads;
         const int nd = rank * d.chunk + slot;
-        const uint32_t so = __ldg(soff + (slot >> 5)) + (slot & 31);
         const float si = xs[slot];
         const float2 gs = __ldg(d.g_self + nd);
         float gx = gs.x * si, gy = gs.y * si;
-        ring_gather_g(code, gco, so, __ldg(d.deg + nd), [&](uint32_t c, float2 ge) {
-          const float sj = xs[c];
-          gx = fmaf(ge.x, sj, gx);
-          gy = fmaf(ge.y, sj, gy);
+        ring_pairs_g(code2, __ldg(soff + (slot >> 5)), lane, [&](uint32_t cc, uint32_t at) {
+          const float s0 = xs[cc & 0xffffu], s1 = xs[cc >> 16];
+          const float4 ge = __ldg(g4 + at);
+          gx = fmaf(ge.x, s0, gx);
+          gy = fmaf(ge.y, s0, gy);
+          gx = fmaf(ge.z, s1, gx);
+          gy = fmaf(ge.w, s1, gy);
         });
         const float dx = r[j] * gx, dy = r[j] * gy;  // solver.py:189
         bad |= !isfinite(dx) || !isfinite(dy);
@@ -251,13 +250,14 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
         if (OWN(j)) {
           const int slot = t + j * kClusterThreads;
           const int nd = rank * d.chunk + slot;
-          const uint32_t so = __ldg(soff + (slot >> 5)) + (slot & 31);
           const float iv = __ldg(d.inv_val + nd);
           float ax = 0.f, ay = 0.f;
-          ring_gather_g(code, gco, so, __ldg(d.deg + nd), [&](uint32_t c, float2) {
-            const float2 uj = src[c];  // (L u)_i, L_ij = 1/val_i
-            ax = fmaf(iv, uj.x, ax);
-            ay = fmaf(iv, uj.y, ay);
+          ring_pairs_g(code2, __ldg(soff + (slot >> 5)), lane, [&](uint32_t cc, uint32_t) {
+            const float2 u0 = src[cc & 0xffffu], u1 = src[cc >> 16];  // (L u)_i, L_ij = 1/val_i
+            ax = fmaf(iv, u0.x, ax);
+            ay = fmaf(iv, u0.y, ay);
+            ax = fmaf(iv, u1.x, ax);
+            ay = fmaf(iv, u1.y, ay);
           });
           const float2 si = src[slot];
           const float om = 1.f - lam;  // (1 - lam) u + lam (L u), mesh.py:281
@@ -360,7 +360,7 @@ __device__ __forceinline__ unsigned flag_acquire(const unsigned* f) {
 //     buffers: a CTA writing buffer k & 3 again at k+4 has waited for all
 //     partials of k+2, so every CTA finished control(k).
 template <int NPT>
-__global__ void __launch_bounds__(kClusterThreads, 1)
+__global__ void __launch_bounds__(kClusterThreads, kClusterMinBlocks)
     k_grid_flags(const ClusterPair* __restrict__ pairs, PairStatus* __restrict__ st, int max_iter,
                  double tol, float tau, float lam, int passes) {
   constexpr int SLOTS = kClusterThreads * NPT;
@@ -391,8 +391,12 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   }
   for (int q = t; q < d.halo_stride; q += kClusterThreads)
     halo[q] = d.halo[size_t(rank) * d.halo_stride + q];
-  const uint16_t* code = d.codes + size_t(rank) * d.topo_stride;
-  const float2* gco = d.g + size_t(rank) * d.topo_stride;
+  const uint32_t* code2 = reinterpret_cast<const uint32_t*>(d.codes + size_t(rank) * d.topo_stride);
+  const float4* g4 = reinterpret_cast<const float4*>(d.g + size_t(rank) * d.topo_stride);
+  if (t == 0) {  // ZERO slot of the padding entries
+    xs[X - 1] = 0.f;
+    xu0[X - 1] = make_float2(0.f, 0.f);
+  }
   const uint32_t* soff = d.slice_off + size_t(rank) * d.slices;
   // one 128-byte line per flag: polled lines are never shared by two flags
   constexpr int FS = kFlagStride;
@@ -556,14 +560,16 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       if (OWN(j)) {
         const int slot = t + j * kClusterThreads;
         const int nd = rank * d.chunk + slot;
-        const uint32_t so = __ldg(soff + (slot >> 5)) + (slot & 31);
         const float si = xs[slot];
         const float2 gs = __ldg(d.g_self + nd);
         float gx = gs.x * si, gy = gs.y * si;
-        ring_gather_g(code, gco, so, __ldg(d.deg + nd), [&](uint32_t c, float2 ge) {
-          const float sj = xs[c];
-          gx = fmaf(ge.x, sj, gx);
-          gy = fmaf(ge.y, sj, gy);
+        ring_pairs_g(code2, __ldg(soff + (slot >> 5)), lane, [&](uint32_t cc, uint32_t at) {
+          const float s0 = xs[cc & 0xffffu], s1 = xs[cc >> 16];
+          const float4 ge = __ldg(g4 + at);
+          gx = fmaf(ge.x, s0, gx);
+          gy = fmaf(ge.y, s0, gy);
+          gx = fmaf(ge.z, s1, gx);
+          gy = fmaf(ge.w, s1, gy);
         });
         const float rj = get_r(j);
         const float dx = rj * gx, dy = rj * gy;  // solver.py:189
@@ -610,13 +616,14 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
         if (OWN(j)) {
           const int slot = t + j * kClusterThreads;
           const int nd = rank * d.chunk + slot;
-          const uint32_t so = __ldg(soff + (slot >> 5)) + (slot & 31);
           const float iv = __ldg(d.inv_val + nd);
           float ax = 0.f, ay = 0.f;
-          ring_gather_g(code, gco, so, __ldg(d.deg + nd), [&](uint32_t c, float2) {
-            const float2 uj = xu0[c];  // (L u)_i, L_ij = 1/val_i
-            ax = fmaf(iv, uj.x, ax);
-            ay = fmaf(iv, uj.y, ay);
+          ring_pairs_g(code2, __ldg(soff + (slot >> 5)), lane, [&](uint32_t cc, uint32_t) {
+            const float2 u0 = xu0[cc & 0xffffu], u1 = xu0[cc >> 16];  // (L u)_i, L_ij = 1/val_i
+            ax = fmaf(iv, u0.x, ax);
+            ay = fmaf(iv, u0.y, ay);
+            ax = fmaf(iv, u1.x, ax);
+            ay = fmaf(iv, u1.y, ay);
           });
           const float2 si = xu0[slot];
           const float om = 1.f - lam;  // (1 - lam) u + lam (L u), mesh.py:281

@@ -611,9 +611,9 @@ TopoHost plan_topo(const HostMesh& h, int cs, int chunk, int npt) {
   std::vector<int> stamp(static_cast<size_t>(n), -1), hidx(static_cast<size_t>(n), 0);
   int stride = 0;
   for (int r = 0; r < cs; ++r) {
-    int acc = 0;
+    int acc = 0;  // pair rows x 32 so far in this CTA's block
     for (int sl = 0; sl < t.slices; ++sl) {
-      t.soff[size_t(r) * t.slices + sl] = uint32_t(acc);
+      const size_t si = size_t(r) * t.slices + sl;
       int mx = 0;
       for (int s = sl * 32; s < std::min(chunk, sl * 32 + 32); ++s) {
         const int i = r * chunk + s;
@@ -634,13 +634,17 @@ TopoHost plan_topo(const HostMesh& h, int cs, int chunk, int npt) {
           t.code[q] = uint16_t(SLOTS + hidx[j]);
         }
       }
-      acc += 32 * mx;
+      const int pairs = (mx + 1) / 2;  // warp-uniform trip count of the gathers
+      t.soff[si] = uint32_t(pairs) << 24 | uint32_t(acc);
+      acc += 32 * pairs;
     }
-    stride = std::max(stride, acc);
+    stride = std::max(stride, 2 * acc);  // entries (uint16 codes / float2 coefficients)
   }
   t.stride = std::max((stride + 7) / 8 * 8, 8);
+  // halo slots, plus one: the last slot of the halo region is the ZERO slot
+  // (always 0) every padding entry of the SELL layout points at
   int hstride = 2;
-  for (auto& hl : halos) hstride = std::max<int>(hstride, int(hl.size()));
+  for (auto& hl : halos) hstride = std::max<int>(hstride, int(hl.size()) + 1);
   t.hstride = (hstride + 31) / 32 * 32;
   t.halo.assign(size_t(cs) * t.hstride, 0);
   t.n_halo.resize(cs);
@@ -676,21 +680,37 @@ TopoHost plan_topo(const HostMesh& h, int cs, int chunk, int npt) {
 }
 
 // packed layout: codes | g | slice_off | halo | n_halo | deg | send | n_send
-void write_topo(const HostMesh& h, int cs, const TopoHost& t, unsigned char* dst) {
+//
+// Paired SELL-32: the one-ring entries of a 32-slot slice (one warp) are
+// stored in pair rows; entry e of slot s sits at entry index
+//   2 * (pair_off(slice) + 32 * (e / 2) + s % 32) + e % 2
+// so one 32-bit load fetches the codes of entries (2p, 2p+1) and one 128-bit
+// load their two coefficient pairs.  slice_off = pair rows << 24 | pair_off;
+// the pair-row count is the slice's largest one-ring, rounded up, so every
+// gather loop is warp-uniform.  Padding entries point at the ZERO slot
+// (halo_stride - 1 past the own slots) with coefficient 0.
+inline uint16_t zero_slot(int npt, int hstride) {
+  return uint16_t(kClusterThreads * npt + hstride - 1);
+}
+
+void write_topo(const HostMesh& h, int cs, const TopoHost& t, unsigned char* dst, int npt) {
   const int n = int(h.n), chunk = t.chunk;
   uint16_t* codes = reinterpret_cast<uint16_t*>(dst + t.off[0]);
   float2* g = reinterpret_cast<float2*>(dst + t.off[1]);
-  std::memset(codes, 0, size_t(cs) * t.stride * 2);  // SELL padding: code 0, g 0
+  std::fill(codes, codes + size_t(cs) * t.stride, zero_slot(npt, t.hstride));
   std::memset(g, 0, size_t(cs) * t.stride * 8);
   unsigned char* deg = dst + t.off[5];
   for (int i = 0; i < n; ++i) {
     const int r = i / chunk, s = i - r * chunk;
     const int b = h.nb_ptr[i], e = h.nb_ptr[i + 1];
     deg[i] = (unsigned char)(e - b);
-    const size_t base = size_t(r) * t.stride + t.soff[size_t(r) * t.slices + s / 32] + (s % 32);
+    const size_t base =
+        size_t(r) * t.stride + 2 * size_t((t.soff[size_t(r) * t.slices + s / 32] & 0xffffffu) + (s % 32));
     for (int q = b; q < e; ++q) {
-      codes[base + 32 * size_t(q - b)] = t.code[q];
-      g[base + 32 * size_t(q - b)] = make_float2(float(h.g_nb[2 * q]), float(h.g_nb[2 * q + 1]));
+      const int k = q - b;
+      const size_t at = base + 64 * size_t(k >> 1) + (k & 1);
+      codes[at] = t.code[q];
+      g[at] = make_float2(float(h.g_nb[2 * q]), float(h.g_nb[2 * q + 1]));
     }
   }
   std::memcpy(dst + t.off[2], t.soff.data(), t.soff.size() * 4);
@@ -728,7 +748,7 @@ const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, i
   AllocScope scope(ctx->stream);
   const TopoHost th = plan_topo(h, cs, chunk, npt);
   std::vector<unsigned char> packed(th.total);
-  write_topo(h, cs, th, packed.data());
+  write_topo(h, cs, th, packed.data(), npt);
   unsigned char* slab = dalloc<unsigned char>(th.total);
   ck(mrb_copy_async(slab, packed.data(), th.total, cudaMemcpyHostToDevice,
                     ctx->stream));  // pageable: staged before return
@@ -747,7 +767,7 @@ struct TopoUpload {
   std::vector<HostMesh*> meshes;
   std::vector<TopoHost> th;
   std::vector<size_t> base;
-  int cs = 0;
+  int cs = 0, npt = 1;
   int slot = 1;                    // pinned staging slot
   unsigned char* stage = nullptr;  // pinned, ctx->pinned[slot]
   unsigned char* dev = nullptr;    // shared slab
@@ -758,6 +778,7 @@ TopoUpload plan_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, 
   TopoUpload up;
   up.meshes = todo;
   up.cs = cs;
+  up.npt = npt;
   up.slot = slot;
   up.th.resize(todo.size());
   parallel_for(todo.size(), [&](size_t i) {
@@ -785,7 +806,7 @@ void upload_cluster_topos(mrb_ctx* ctx, const TopoUpload& up, size_t i0, size_t 
   if (i0 >= i1) return;
   parallel_for(i1 - i0, [&](size_t k) {
     const size_t i = i0 + k;
-    write_topo(*up.meshes[i], up.cs, up.th[i], up.stage + up.base[i]);
+    write_topo(*up.meshes[i], up.cs, up.th[i], up.stage + up.base[i], up.npt);
   });
   const size_t b0 = up.base[i0];
   const size_t b1 = i1 < up.meshes.size() ? up.base[i1] : up.base.back() + up.th.back().total;

@@ -66,14 +66,14 @@ __device__ __forceinline__ void st_async_v4(uint32_t addr, uint4 v, uint32_t mb)
 }
 
 // Dynamic shared memory of k_cluster_push (host: push_dyn_smem).
+// The paired SELL coefficients (float4) come first: 16-byte aligned.
 struct PushSmem {
+  float4* g4;
   double2* V;
   float2 *gs, *xu[2];  // xu[p]: u0 of iteration parity p, own slots then halo
   float *iv, *xs[2];   // xs[p]: s_te of iteration parity p, own slots then halo
-  unsigned char* deg;
   uint32_t* send;
-  float2* g;
-  uint16_t* code;
+  uint32_t* code2;
   uint32_t* soff;
 };
 
@@ -82,7 +82,8 @@ __device__ __forceinline__ PushSmem push_carve(unsigned char* p, const ClusterPa
   constexpr int SLOTS = kClusterThreads * NPT;
   const int X = SLOTS + d.halo_stride;
   PushSmem s;
-  s.V = reinterpret_cast<double2*>(p);
+  s.g4 = reinterpret_cast<float4*>(p);
+  s.V = reinterpret_cast<double2*>(s.g4 + d.topo_stride / 2);  // topo_stride % 8 == 0
   s.gs = reinterpret_cast<float2*>(s.V + SLOTS);
   s.xu[0] = s.gs + SLOTS;
   s.xu[1] = s.xu[0] + X;
@@ -90,31 +91,13 @@ __device__ __forceinline__ PushSmem push_carve(unsigned char* p, const ClusterPa
   s.xs[0] = s.iv + SLOTS;
   s.xs[1] = s.xs[0] + X;
   s.send = reinterpret_cast<uint32_t*>(s.xs[1] + X);
-  s.g = reinterpret_cast<float2*>(s.send + d.send_stride);  // send_stride % 32 == 0
-  s.code = reinterpret_cast<uint16_t*>(s.g + d.topo_stride);
-  s.soff = reinterpret_cast<uint32_t*>(s.code + d.topo_stride);  // topo_stride % 2 == 0
-  s.deg = reinterpret_cast<unsigned char*>(s.soff + d.slices);
+  s.code2 = s.send + d.send_stride;
+  s.soff = s.code2 + d.topo_stride / 2;
   return s;
 }
 
-// SELL one-ring gather over a push-kernel layout (same batching as ring_gather)
-template <typename F>
-__device__ __forceinline__ void ring_gather_p(const PushSmem& sm, uint32_t so, int deg, F&& f) {
-#pragma unroll
-  for (int e0 = 0; e0 < kMaxDeg; e0 += 8) {
-    if (e0 < deg) {
-      uint32_t c[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) c[e] = (e0 + e < deg) ? sm.code[so + 32u * (e0 + e)] : 0u;
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (e0 + e < deg) f(e0 + e, c[e]);
-    }
-  }
-}
-
 template <int NPT>
-__global__ void __launch_bounds__(kClusterThreads, 1)
+__global__ void __launch_bounds__(kClusterThreads, kClusterMinBlocks)
     k_cluster_push(const ClusterPair* __restrict__ pairs, PairStatus* __restrict__ st,
                    int max_iter, double tol, float tau, float lam, int passes) {
   constexpr int SLOTS = kClusterThreads * NPT;
@@ -150,9 +133,16 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   }
   {  // this CTA's topology and send list
     const size_t tb = size_t(rank) * d.topo_stride;
-    for (int q = t; q < d.topo_stride; q += kClusterThreads) {
-      sm.g[q] = d.g[tb + q];
-      sm.code[q] = d.codes[tb + q];
+    const float4* g4 = reinterpret_cast<const float4*>(d.g + tb);
+    const uint32_t* c2 = reinterpret_cast<const uint32_t*>(d.codes + tb);
+    for (int q = t; q < d.topo_stride / 2; q += kClusterThreads) {
+      sm.g4[q] = g4[q];
+      sm.code2[q] = c2[q];
+    }
+    if (t == 0) {  // the ZERO slot of the padding entries, both parities
+      const int zero = SLOTS + d.halo_stride - 1;
+      sm.xs[0][zero] = sm.xs[1][zero] = 0.f;
+      sm.xu[0][zero] = sm.xu[1][zero] = make_float2(0.f, 0.f);
     }
     for (int q = t; q < d.slices; q += kClusterThreads)
       sm.soff[q] = d.slice_off[size_t(rank) * d.slices + q];
@@ -171,7 +161,6 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     sm.V[slot] = o ? d.V[nd] : make_double2(0.0, 0.0);
     sm.gs[slot] = o ? d.g_self[nd] : make_float2(0.f, 0.f);
     sm.iv[slot] = o ? d.inv_val[nd] : 0.f;
-    sm.deg[slot] = o ? d.deg[nd] : 0;
     u[j] = make_float2(0.f, 0.f);
     r[j] = 0.f;
   }
@@ -311,15 +300,16 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     for (int j = 0; j < NPT; ++j) {
       if (OWN(j)) {
         const int slot = t + j * kClusterThreads;
-        const uint32_t so = sm.soff[slot >> 5] + (slot & 31);
         const float si = xs[slot];
         const float2 gs = sm.gs[slot];
         float gx = gs.x * si, gy = gs.y * si;
-        ring_gather_p(sm, so, sm.deg[slot], [&](int e, uint32_t c) {
-          const float sj = xs[c];
-          const float2 ge = sm.g[so + 32u * e];
-          gx = fmaf(ge.x, sj, gx);
-          gy = fmaf(ge.y, sj, gy);
+        ring_pairs(sm.code2, sm.soff[slot >> 5], lane, [&](uint32_t cc, uint32_t at) {
+          const float s0 = xs[cc & 0xffffu], s1 = xs[cc >> 16];
+          const float4 ge = sm.g4[at];
+          gx = fmaf(ge.x, s0, gx);
+          gy = fmaf(ge.y, s0, gy);
+          gx = fmaf(ge.z, s1, gx);
+          gy = fmaf(ge.w, s1, gy);
         });
         const float dx = r[j] * gx, dy = r[j] * gy;  // solver.py:189
         bad |= !isfinite(dx) || !isfinite(dy);
@@ -363,13 +353,15 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       for (int j = 0; j < NPT; ++j) {
         if (OWN(j)) {
           const int slot = t + j * kClusterThreads;
-          const uint32_t so = sm.soff[slot >> 5] + (slot & 31);
           const float ivs = sm.iv[slot];
           float ax = 0.f, ay = 0.f;
-          ring_gather_p(sm, so, sm.deg[slot], [&](int, uint32_t c) {  // (L u)_i, L_ij = 1/val_i
-            const float2 uj = xu[c];
-            ax = fmaf(ivs, uj.x, ax);
-            ay = fmaf(ivs, uj.y, ay);
+          // (L u)_i, L_ij = 1/val_i
+          ring_pairs(sm.code2, sm.soff[slot >> 5], lane, [&](uint32_t cc, uint32_t) {
+            const float2 u0 = xu[cc & 0xffffu], u1 = xu[cc >> 16];
+            ax = fmaf(ivs, u0.x, ax);
+            ay = fmaf(ivs, u0.y, ay);
+            ax = fmaf(ivs, u1.x, ax);
+            ay = fmaf(ivs, u1.y, ay);
           });
           const float2 si = xu[slot];
           const float om = 1.f - lam;  // (1 - lam) u + lam (L u), mesh.py:281
