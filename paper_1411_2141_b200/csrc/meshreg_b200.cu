@@ -1876,13 +1876,13 @@ void setup_cluster_path(mrb_batch* b) {
   b->cluster_cs = cs;
   b->cluster_npt = npt;
   b->cluster_smem = smem;
-  // Push exchange in latency mode (one node per thread: few pairs, per-
-  // iteration latency dominates; measured C1 -25%, C2 -18% time).  In
-  // throughput mode (two nodes per thread, a full wave of clusters) the pull
-  // kernel measured faster (C4 8.4 vs 9.5 ms).  MESHREG_B200_EXCHANGE=push|pull
-  // overrides.
+  // Push exchange whenever it fits (smoothing_passes <= 1, send lists, no
+  // occupancy loss): no cluster barrier inside the loop.  Latency mode
+  // measured C1 -25%, C2 -18% time; throughput mode with the paired SELL
+  // gathers C4 6.90 -> 6.27 ms (before them the pull kernel was faster there:
+  // 8.4 vs 9.5 ms).  MESHREG_B200_EXCHANGE=push|pull overrides.
   const char* xenv = std::getenv("MESHREG_B200_EXCHANGE");
-  const bool want_push = xenv ? std::string(xenv) == "push" : npt == 1;
+  const bool want_push = xenv ? std::string(xenv) == "push" : true;
   if (b->cfg.smoothing_passes <= 1 && want_push) {
     size_t ps = 0;
     bool lists = true;
