@@ -1083,6 +1083,11 @@ struct mrb_batch {
   // launch's dense pass (enqueue_run)
   cudaStream_t tail_stream = nullptr;
   cudaEvent_t tail_fork = nullptr, tail_join = nullptr;
+  // wave groups alternate between ctx->stream and grp_stream, so group g+1's
+  // clusters fill the SMs group g's retiring clusters free (one launch per
+  // group on one stream would drain the GPU between groups)
+  cudaStream_t grp_stream = nullptr;
+  cudaEvent_t grp_fork = nullptr, grp_join = nullptr;
   cudaStream_t lstream = nullptr;  // launch stream override (nullptr: ctx->stream)
   bool groups_recorded = false;
   size_t cluster_smem = 0;
@@ -1120,6 +1125,12 @@ struct mrb_batch {
     }
     if (tail_fork) cudaEventDestroy(tail_fork);
     if (tail_join) cudaEventDestroy(tail_join);
+    if (grp_stream) {
+      cudaStreamSynchronize(grp_stream);
+      cudaStreamDestroy(grp_stream);
+    }
+    if (grp_fork) cudaEventDestroy(grp_fork);
+    if (grp_join) cudaEventDestroy(grp_join);
     void* ptrs[] = {pairs, st, blk_pair, pix_blk_pair, partials, pix_partials, state, traces,
                     img, stage, src_ptrs, img_ptrs, dense, u_out, conv, cpairs, img_pad,
                     prof_host ? nullptr : phase_prof, xbuf, xbar, xexports};
@@ -1528,26 +1539,38 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
                                                                  b->pix_partials);
           launches += 2;
         };
+        if (!b->grp_stream) {
+          ck(cudaStreamCreateWithFlags(&b->grp_stream, cudaStreamNonBlocking));
+          ck(cudaEventCreateWithFlags(&b->grp_fork, cudaEventDisableTiming));
+          ck(cudaEventCreateWithFlags(&b->grp_join, cudaEventDisableTiming));
+        }
+        ck(cudaEventRecord(b->grp_fork, s));  // padded images ready
+        ck(cudaStreamWaitEvent(b->grp_stream, b->grp_fork, 0));
+        const cudaStream_t gst[2] = {s, b->grp_stream};
         for (size_t g = 0; g < ng; ++g) {
           const int p0 = b->groups[g], p1 = b->groups[g + 1];
           if (tail_side && g == ng - 1) {  // launched beside group ng - 2's dense pass
-            ck(cudaStreamWaitEvent(s, b->tail_join, 0));
-            ck(cudaEventRecord(b->group_ev[g], s));
+            ck(cudaEventRecord(b->group_ev[g], b->tail_stream));
             continue;
           }
+          // (grid mode: whole-GPU cooperative launches sharing one exchange
+          // buffer must stay serial on one stream)
+          const cudaStream_t gs = b->grid_mode ? s : gst[g & 1];
           // this group's topologies (host packing overlaps the previous group)
-          flush_topo(b, p1, b->copy_stream, s);
-          if (p1 > b->tail_p0) flush_tail_topo(b, b->copy_stream, s);
+          flush_topo(b, p1, b->copy_stream, gs);
+          if (p1 > b->tail_p0) flush_tail_topo(b, b->copy_stream, gs);
           if (std::getenv("MESHREG_B200_DEBUG")) {  // device timeline of the groups
             cudaEvent_t e;
             cudaEventCreate(&e);
-            cudaEventRecord(e, s);
+            cudaEventRecord(e, gs);
             b->dbg_group_ev.push_back(e);
           }
+          b->lstream = gs;
           launches += launch_cluster(b, p0, p1 - p0);
+          b->lstream = nullptr;
           if (tail_side && g == ng - 2) {
             const int t0 = b->groups[ng - 1], t1 = b->groups[ng];
-            ck(cudaEventRecord(b->tail_fork, s));
+            ck(cudaEventRecord(b->tail_fork, gs));
             ck(cudaStreamWaitEvent(b->tail_stream, b->tail_fork, 0));
             flush_topo(b, t1, b->copy_stream, b->tail_stream);
             flush_tail_topo(b, b->copy_stream, b->tail_stream);
@@ -1557,9 +1580,13 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
             dense_msd(t0, t1, b->tail_stream);
             ck(cudaEventRecord(b->tail_join, b->tail_stream));
           }
-          dense_msd(p0, p1, s);
-          ck(cudaEventRecord(b->group_ev[g], s));
+          dense_msd(p0, p1, gs);
+          ck(cudaEventRecord(b->group_ev[g], gs));
         }
+        // everything later on ctx->stream (results, sync) follows every group
+        ck(cudaEventRecord(b->grp_join, b->grp_stream));
+        ck(cudaStreamWaitEvent(s, b->grp_join, 0));
+        if (tail_side) ck(cudaStreamWaitEvent(s, b->tail_join, 0));
         b->groups_recorded = true;
         ck(cudaGetLastError());
         return launches;
@@ -1886,9 +1913,13 @@ void setup_cluster_path(mrb_batch* b) {
   if (b->cfg.smoothing_passes <= 1 && want_push) {
     size_t ps = 0;
     bool lists = true;
-    for (mrb_mesh* m : b->meshes) {
-      const int chunk = int((m->h.n + cs - 1) / cs);
-      const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, m->h, cs, chunk, npt);
+    // the main shape's pairs only: the expected tail's pairs have no topology
+    // of this shape (setup_tail decides them; planning one here would cost a
+    // synchronous host plan + upload per tail mesh)
+    for (int p = 0; p < main_end; ++p) {
+      HostMesh& h = b->meshes[p]->h;
+      const int chunk = int((h.n + cs - 1) / cs);
+      const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, h, cs, chunk, npt);
       lists = lists && t.send_stride > 0;
       ps = std::max(ps, push_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride,
                                       t.send_stride));
