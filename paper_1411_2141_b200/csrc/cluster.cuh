@@ -380,10 +380,14 @@ __global__ void __launch_bounds__(kClusterThreads, kClusterMinBlocks)
   cluster_sync_all();  // every CTA started and staged
   const int nhalo = s_nhalo;
 
+#ifdef MRB_PHASE_PROFILE  // phase timestamps (build flag; MESHREG_B200_PROFILE_PHASES)
   long long* const prof =
       (d.prof && t == 0) ? d.prof + (size_t(rank) * 8) * 16 : nullptr;  // d.prof: this pair's
 #define PROF(k, slot) \
   if (prof && (k) < 8) prof[(k) * 16 + (slot)] = clock64();
+#else
+#define PROF(k, slot)
+#endif
 
   // Control step of iteration kk (control warp, all CTAs identically):
   // fixed-order cluster reduction of the energy partials, then the logic of

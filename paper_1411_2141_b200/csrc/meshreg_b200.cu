@@ -1517,12 +1517,11 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
         // per wave group: loop + dense pass + MSD, then an event for the
         // group's device-to-host copies (mrb_batch_get_results)
         const PD* host = reinterpret_cast<const PD*>(b->pairs_host.data());
-        static const bool tail_serial = std::getenv("MESHREG_B200_TAIL_SERIAL") != nullptr;
         const size_t ng = b->groups.size() - 1;
         // the last group is the tail wave (latency shape, a third of the
         // SMs): it runs on a side stream from the end of the previous group's
         // loop, beside that group's dense pass
-        const bool tail_side = !tail_serial && !b->grid_mode && ng >= 2 &&
+        const bool tail_side = !b->grid_mode && ng >= 2 &&
                                b->groups[ng - 1] >= b->tail_p0 && b->tail_p0 < b->n_pairs;
         if (tail_side && !b->tail_stream) {
           ck(cudaStreamCreateWithFlags(&b->tail_stream, cudaStreamNonBlocking));
@@ -1593,8 +1592,7 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
       }
       flush_topo(b, b->n_pairs, s, s);  // deferred topologies not yet uploaded
       flush_tail_topo(b, s, s);
-      static const bool serial = std::getenv("MESHREG_B200_TAIL_SERIAL") != nullptr;
-      if (tm == &dummy && !b->grid_mode && b->tail_p0 > 0 && b->tail_p0 < b->n_pairs && !serial) {
+      if (tm == &dummy && !b->grid_mode && b->tail_p0 > 0 && b->tail_p0 < b->n_pairs) {
         // the tail wave holds a third of the SMs for ~1 ms after the main
         // launch: run it, and then its pairs' dense pass, on a side stream
         // while the main pairs' dense pass fills the idle SMs
@@ -1718,9 +1716,7 @@ bool choose_cluster_shape(mrb_ctx* ctx, HostMesh& big, int n_pairs, bool two_u, 
   const int64_t nmax = big.n;
   // latency mode (few pairs): one node per thread, more CTAs per pair;
   // throughput mode: two nodes per thread, fewer CTAs per pair
-  const char* npt_env = std::getenv("MESHREG_B200_NPT");
-  int npt = npt_pref ? npt_pref : npt_env ? std::atoi(npt_env) : (n_pairs >= 4 ? 2 : 1);
-  const char* cs_env = std::getenv("MESHREG_B200_CS");
+  int npt = npt_pref ? npt_pref : (n_pairs >= 4 ? 2 : 1);
   static std::mutex cache_mu;
   static std::map<std::tuple<int, int, int64_t, bool, int>, std::tuple<int, int, int>> cache;
   const auto key = std::make_tuple(npt, n_pairs, int64_t(nmax), two_u, ctx->device);
@@ -1739,7 +1735,6 @@ bool choose_cluster_shape(mrb_ctx* ctx, HostMesh& big, int n_pairs, bool two_u, 
     double best = 1e300;
     int best_cs = 0, best_occ = 0;
     for (int cs = cs_min; cs <= 16; ++cs) {
-      if (cs_env && std::atoi(cs_env) != cs) continue;
       const int chunk = int((big.n + cs - 1) / cs);
       const DeviceMesh::Topo& t = ensure_cluster_topo(ctx, big, cs, chunk, npt);
       const size_t smem =
@@ -2081,8 +2076,7 @@ void build_fast_descriptors(mrb_batch* b) {
     {
       // taps evict_first when the four image copies exceed half of L2 (C5)
       const size_t img_bytes = 4 * b->pad_plane * sizeof(float2);
-      const char* te = std::getenv("MESHREG_B200_TAP_EVICT");  // "first" / "normal"
-      c.tap_evict_first = te ? std::string(te) == "first" : img_bytes > device_l2_bytes() / 2;
+      c.tap_evict_first = img_bytes > device_l2_bytes() / 2;
     }
     if (b->grid_mode && b->grid_flags && !b->xexports) {
       const int words = kClusterThreads * b->cluster_npt / 32;
@@ -2110,8 +2104,7 @@ void build_fast_descriptors(mrb_batch* b) {
         const int words = kClusterThreads * b->cluster_npt / 32;
         // publish only exported slots at NPT = 8 (C5: 2% faster); smaller
         // NPT publishes every slot (measured faster, C2/C3)
-        const char* xe = std::getenv("MESHREG_B200_GRID_EXPORTS");  // "all" / "sel"
-        const bool sel = xe ? std::string(xe) == "sel" : b->cluster_npt >= 8;
+        const bool sel = b->cluster_npt >= 8;
         c.exports = sel ? b->xexports + size_t(p) * cs * words : nullptr;
         c.flags = b->xbar + 1;
         c.gbad = reinterpret_cast<int*>(b->xbar + 1 + 3 * size_t(cs) * kFlagStride);
@@ -2151,10 +2144,8 @@ void setup_grid_path(mrb_batch* b, int64_t nmax) {
     }
     return per_sm;
   };
-  // epoch-tagged exchange (no grid barrier) for at most one smoothing pass;
-  // MESHREG_B200_GRID_SYNC=barrier keeps the barrier kernel
-  const char* genv = std::getenv("MESHREG_B200_GRID_SYNC");
-  bool flags = b->cfg.smoothing_passes <= 1 && !(genv && std::string(genv) == "barrier");
+  // epoch-tagged exchange (no grid barrier) for at most one smoothing pass
+  bool flags = b->cfg.smoothing_passes <= 1;
   int per_sm = 0;
   if (flags)
     per_sm = npt == 1 ? fit(k_grid_flags<1>) : npt == 2 ? fit(k_grid_flags<2>)
@@ -3130,7 +3121,7 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
       stamp("create begin", k);
       const bool grouped = wave > 0 && P > wave && !std::getenv("MESHREG_B200_NO_GROUPS");
       int rc = batch_create_impl(sc, P, meshes + p0, W, H, img_dtype, cfg, forced_cs, forced_npt,
-                                 &b, grouped && !std::getenv("MESHREG_B200_NO_DEFER") ? wave : 0);
+                                 &b, grouped ? wave : 0);
       stamp("create end", k);
       if (rc == MRB_OK && k == 0) {
         cs = b->cluster_cs;

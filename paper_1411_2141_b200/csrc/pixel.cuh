@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kPixThreads, 2)
   const int gx0 = x0 - R, gy0 = y0 - R;  // pixel of region cell (0, 0)
   // patch origin in padded-image coordinates (may be negative: TMA zero-fills)
   const int px0 = x0 - PP::M, py0 = y0 - PP::M;
-  const bool use_tma = !(descend & 2);  // bit 1: debug switch, global taps only
+  constexpr bool use_tma = true;
   descend &= 1;
   if (descend && use_tma && threadIdx.x == 0) {
     const unsigned mb = pix_smem_u32(&mbar);

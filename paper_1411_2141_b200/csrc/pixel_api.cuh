@@ -69,10 +69,9 @@ void launch_pixel_iter(const mrb_pixel_batch* b, const PixelDev<Real>* pairs, in
                        Real tau, Real lam, int r, int descend, int clamp) {
   const dim3 grid(b->tiles, b->n_pairs);
   cudaStream_t s = b->ctx->stream;
-  static const int notma = std::getenv("MESHREG_B200_PIX_NOTMA") ? 2 : 0;  // debug switch
 #define MRB_PIX_LAUNCH(RR)                                                              \
   k_pixel_iter<Real, RR><<<grid, kPixThreads, PixPatch<Real, RR>::smem_bytes, s>>>(     \
-      pairs, k, src, tau, lam, descend | notma, clamp)
+      pairs, k, src, tau, lam, descend, clamp)
   switch (r) {
     case 0: MRB_PIX_LAUNCH(0); break;
     case 1: MRB_PIX_LAUNCH(1); break;

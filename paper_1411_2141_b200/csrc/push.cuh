@@ -243,10 +243,14 @@ __global__ void __launch_bounds__(kClusterThreads, kClusterMinBlocks)
 
   // debug: per-CTA stamps of the first 8 iterations (MESHREG_B200_PROFILE_PHASES;
   // "mapped": iteration numbers readable during a hang, else clock64 cycles)
+#ifdef MRB_PHASE_PROFILE  // build flag
   volatile long long* const trace_pt =
       (d.prof && t == 0) ? d.prof + size_t(rank) * 128 : nullptr;
 #define TRACE(slot) \
   if (trace_pt && k < 8) trace_pt[k * 16 + (slot)] = clock64();
+#else
+#define TRACE(slot)
+#endif
   int k = 0;
   for (; k < max_iter; ++k) {
     const int par = k & 1;

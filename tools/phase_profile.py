@@ -1,6 +1,7 @@
 """Phase timing of the cluster kernel from clock64() stamps (debug aid).
 
 usage: MESHREG_B200_PROFILE_PHASES=1 python tools/phase_profile.py [pairs] [workload]
+(needs a library built with MRB_NVCC_FLAGS=-DMRB_PHASE_PROFILE)
 """
 import ctypes as C
 import os

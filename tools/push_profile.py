@@ -1,5 +1,6 @@
 """Phase timing of the push cluster kernel from clock64 stamps (debug aid):
-MESHREG_B200_PROFILE_PHASES=1 python tools/push_profile.py [pairs] [workload]"""
+MESHREG_B200_PROFILE_PHASES=1 python tools/push_profile.py [pairs] [workload]
+(needs a library built with MRB_NVCC_FLAGS=-DMRB_PHASE_PROFILE)"""
 import ctypes as C
 import os
 import sys
