@@ -610,9 +610,14 @@ __global__ void __launch_bounds__(kPixBlock)
   if (st[p].err) return;
   const int q = (blk - d.pix_blk_begin) * kPixBlock + threadIdx.x;
   double2 acc = make_double2(0.0, 0.0);
-  if (q < d.W * d.H) {
+  const int ti = q < d.W * d.H ? __ldg(d.tri_of + q) : kUnassigned;
+  if (ti == kUnassigned && q < d.W * d.H) {
+    // not yet assigned: the deferred coverage check (mrb_batch_sync) either
+    // raises MeshCoverageError or reruns the batch with the located pixels
+    d.ux[q] = d.uy[q] = d.warped[q] = 0.f;
+  } else if (q < d.W * d.H) {
     const int y = q / d.W, x = q - y * d.W;
-    const int4 tv = __ldg(d.tri + __ldg(d.tri_of + q));
+    const int4 tv = __ldg(d.tri + ti);
     double w[3];
     bary_rn(__ldg(d.V + tv.x), __ldg(d.V + tv.y), __ldg(d.V + tv.z), double(x), double(y), w);
     const float2 ua = d.u[tv.x], ub = d.u[tv.y], uc = d.u[tv.z];

@@ -774,7 +774,7 @@ struct TopoUpload {
 };
 
 TopoUpload plan_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, int cs, int npt,
-                              int slot = 1) {
+                              int slot = 1, cudaStream_t alloc_s = nullptr) {
   TopoUpload up;
   up.meshes = todo;
   up.cs = cs;
@@ -792,7 +792,9 @@ TopoUpload plan_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, 
     total += up.th[i].total;
   }
   up.stage = static_cast<unsigned char*>(pinned_stage(ctx, std::max<size_t>(total, 1), slot));
-  AllocScope scope(ctx->stream);
+  // allocated in `alloc_s` order (the copy stream of a lazily planned group:
+  // ctx->stream may hold running groups), freed in ctx->stream order
+  AllocScope scope(alloc_s ? alloc_s : ctx->stream);
   const std::shared_ptr<unsigned char> all = shared_slab(std::max<size_t>(total, 1), ctx->stream);
   up.dev = all.get();
   for (size_t i = 0; i < todo.size(); ++i)
@@ -1076,6 +1078,12 @@ struct mrb_batch {
   std::unique_ptr<TopoUpload> tail_up;  // the tail pairs' latency-shape topologies
   bool tail_done = false;
   int planned_end = 1 << 30;  // pairs past this got no throughput-shape topology planned
+  // mrb_register_many: main-shape pairs [lazy_from, planned_end) are planned
+  // per wave group in the run (flush_topo), while earlier groups compute
+  int lazy_from = 1 << 30;
+  std::vector<std::unique_ptr<TopoUpload>> lazy_ups;
+  std::vector<ClusterPair> cp_host;      // descriptors (patched for lazy pairs)
+  ClusterPair* cp_pinned = nullptr;      // their pinned copy-out buffer
   std::vector<cudaEvent_t> dbg_group_ev;  // MESHREG_B200_DEBUG: start of each group launch
   std::vector<cudaEvent_t> group_ev;
   cudaStream_t copy_stream = nullptr;
@@ -1088,6 +1096,11 @@ struct mrb_batch {
   // group on one stream would drain the GPU between groups)
   cudaStream_t grp_stream = nullptr;
   cudaEvent_t grp_fork = nullptr, grp_join = nullptr;
+  // mrb_register_many: the pixel maps' coverage check (host wait for the
+  // rasters) is deferred to mrb_batch_sync, off the launch path; the dense
+  // kernels skip unassigned pixels (flag 4) until then
+  std::unique_ptr<PixelMapJob> pending_pm;
+  bool redo = false;  // a located (not rasterised) pixel: rerun undeferred
   cudaStream_t lstream = nullptr;  // launch stream override (nullptr: ctx->stream)
   bool groups_recorded = false;
   size_t cluster_smem = 0;
@@ -1112,6 +1125,12 @@ struct mrb_batch {
     } catch (const CudaError&) {
     }
     if (graph) cudaGraphExecDestroy(graph);
+    if (pending_pm && pending_pm->done) cudaEventDestroy(pending_pm->done);
+    if (cp_pinned) {
+      cudaStreamSynchronize(ctx->stream);
+      if (copy_stream) cudaStreamSynchronize(copy_stream);
+      cudaFreeHost(cp_pinned);
+    }
     for (cudaEvent_t e : group_ev) cudaEventDestroy(e);
     if (topo_ev) cudaEventDestroy(topo_ev);
     for (cudaEvent_t e : dbg_group_ev) cudaEventDestroy(e);
@@ -1281,18 +1300,17 @@ void launch_cluster_t(mrb_batch* b, int p0, int np, int CS, size_t smem) {
                         float(b->cfg.tau), float(b->cfg.lam), int(b->cfg.smoothing_passes)));
 }
 
-// The kernel's dynamic-smem limit only ever grows (per device), so every
-// batch created so far can still launch.
-template <int NPT>
-bool raise_smem_limit(size_t smem) {
+// A kernel's dynamic-smem limit only ever grows (per device and kernel), so
+// every batch created so far can still launch.
+template <typename K>
+bool raise_smem_limit_of(K kern, size_t smem) {
   static std::mutex mu;
-  static std::map<int, size_t> cur;
+  static std::map<std::pair<const void*, int>, size_t> cur;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
-  size_t& c = cur[dev];
+  size_t& c = cur[std::make_pair(reinterpret_cast<const void*>(kern), dev)];
   if (smem <= c) return true;
-  auto kern = k_cluster_register<NPT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
       cudaSuccess) {
@@ -1301,6 +1319,11 @@ bool raise_smem_limit(size_t smem) {
   }
   c = smem;
   return true;
+}
+
+template <int NPT>
+bool raise_smem_limit(size_t smem) {
+  return raise_smem_limit_of(k_cluster_register<NPT>, smem);
 }
 
 template <int NPT>
@@ -1387,12 +1410,7 @@ int64_t launch_grid(mrb_batch* b, int p0, int np) {
 template <int NPT>
 int push_occupancy_t(int CS, size_t smem) {
   auto kern = k_cluster_push<NPT>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
-      cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
+  if (!raise_smem_limit_of(kern, smem)) return 0;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(unsigned(CS));
   lc.blockDim = dim3(kClusterThreads);
@@ -1463,16 +1481,52 @@ int64_t launch_cluster(mrb_batch* b, int p0, int np) {
 
 // Deferred topologies (mrb_register_many): pack and copy, on `copy`, the
 // meshes pairs [0, p1) need and make `s` wait for them.
+void patch_descriptors(mrb_batch* b, int p0, int p1);
+
 void flush_topo(mrb_batch* b, int p1, cudaStream_t copy, cudaStream_t s) {
-  if (!b->topo_up) return;
+  bool copied = false;
+  const int pe = std::min(p1, b->planned_end);
+  if (b->lazy_from < pe) {
+    // plan the main-shape topologies of pairs [lazy_from, pe) now (this host
+    // work overlaps the previous group's run), copy them and the patched
+    // descriptors on `copy`
+    const int cs = b->cluster_cs, npt = b->cluster_npt;
+    std::vector<HostMesh*> todo;
+    for (int p = b->lazy_from; p < pe; ++p) {
+      HostMesh* h = &b->meshes[p]->h;
+      const int chunk = int((h->n + cs - 1) / cs);
+      if (!h->dev->topo.count(chunk * 16 + npt) &&
+          std::find(todo.begin(), todo.end(), h) == todo.end())
+        todo.push_back(h);
+    }
+    if (!todo.empty()) {
+      b->lazy_ups.emplace_back(
+          new TopoUpload(plan_cluster_topos(b->ctx, todo, cs, npt, 1, copy)));
+      if (!b->topo_ev) ck(cudaEventCreateWithFlags(&b->topo_ev, cudaEventDisableTiming));
+      upload_cluster_topos(b->ctx, *b->lazy_ups.back(), 0, todo.size(), copy);
+    }
+    patch_descriptors(b, b->lazy_from, pe);
+    ck(mrb_copy_async(static_cast<ClusterPair*>(b->cpairs) + b->lazy_from,
+                      b->cp_pinned + b->lazy_from, sizeof(ClusterPair) * size_t(pe - b->lazy_from),
+                      cudaMemcpyHostToDevice, copy));
+    b->lazy_from = pe;
+    copied = true;
+  }
+  if (!b->topo_up) {
+    if (copied && copy != s) {
+      ck(cudaEventRecord(b->topo_ev, copy));
+      ck(cudaStreamWaitEvent(s, b->topo_ev, 0));
+    }
+    return;
+  }
   size_t need = b->topo_done;
   for (int p = 0; p < p1; ++p) {
     auto it = b->topo_index.find(&b->meshes[p]->h);
     if (it != b->topo_index.end()) need = std::max(need, it->second + 1);
   }
-  if (need <= b->topo_done) return;
-  upload_cluster_topos(b->ctx, *b->topo_up, b->topo_done, need, copy);
-  b->topo_done = need;
+  if (need <= b->topo_done && !copied) return;
+  if (need > b->topo_done) upload_cluster_topos(b->ctx, *b->topo_up, b->topo_done, need, copy);
+  b->topo_done = std::max(b->topo_done, need);
   if (copy != s) {
     if (!b->topo_ev) ck(cudaEventCreateWithFlags(&b->topo_ev, cudaEventDisableTiming));
     ck(cudaEventRecord(b->topo_ev, copy));
@@ -1879,9 +1933,11 @@ void setup_cluster_path(mrb_batch* b) {
   // pairs past planned_end (the expected tail wave of a deferred batch) have
   // no throughput-shape topology unless setup_tail turns the tail down
   const int main_end = std::min(b->n_pairs, b->planned_end);
+  // pairs [lazy_from, main_end) are planned in the run (mrb_register_many)
+  const int plan_end = std::min(main_end, b->lazy_from);
   {  // per-mesh topologies: host thread pool + pinned staged upload
     std::vector<HostMesh*> hm;
-    for (int p = 0; p < main_end; ++p) hm.push_back(&b->meshes[p]->h);
+    for (int p = 0; p < plan_end; ++p) hm.push_back(&b->meshes[p]->h);
     ensure_cluster_topos(b->ctx, hm, cs, npt);
   }
   auto main_smem = [&](int p0, int p1, size_t smem) {
@@ -1893,7 +1949,7 @@ void setup_cluster_path(mrb_batch* b) {
     }
     return smem;
   };
-  size_t smem = main_smem(0, main_end, 0);
+  size_t smem = main_smem(0, plan_end, 0);
   if (cluster_occupancy_cs(cs, npt, smem) < 1) return why("no cluster configuration fits");
   b->cluster_cs = cs;
   b->cluster_npt = npt;
@@ -1911,7 +1967,7 @@ void setup_cluster_path(mrb_batch* b) {
     // the main shape's pairs only: the expected tail's pairs have no topology
     // of this shape (setup_tail decides them; planning one here would cost a
     // synchronous host plan + upload per tail mesh)
-    for (int p = 0; p < main_end; ++p) {
+    for (int p = 0; p < plan_end; ++p) {
       HostMesh& h = b->meshes[p]->h;
       const int chunk = int((h.n + cs - 1) / cs);
       const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, h, cs, chunk, npt);
@@ -2000,6 +2056,21 @@ void setup_tail(mrb_batch* b, size_t main_smem) {
                  r, cs, npt, b->tail_push ? "push" : "pull");
 }
 
+void set_topology(ClusterPair& c, const DeviceMesh::Topo& t) {
+  c.codes = t.codes;
+  c.g = t.g;
+  c.slice_off = t.slice_off;
+  c.halo = t.halo;
+  c.n_halo = t.n_halo;
+  c.halo_stride = t.halo_stride;
+  c.deg = t.deg;
+  c.send = t.send;
+  c.n_send = t.n_send;
+  c.send_stride = t.send_stride;
+  c.topo_stride = t.topo_stride;
+  c.slices = t.slices;
+}
+
 // ClusterPair descriptors + padded image copies of a fast-path batch
 void build_fast_descriptors(mrb_batch* b) {
   const int cs = b->cluster_cs;
@@ -2010,26 +2081,21 @@ void build_fast_descriptors(mrb_batch* b) {
   const PairDev<float, float>* host =
       reinterpret_cast<const PairDev<float, float>*>(b->pairs_host.data());
   std::vector<ClusterPair> cp(b->n_pairs);
+  const DeviceMesh::Topo none{};
   for (int p = 0; p < b->n_pairs; ++p) {
     HostMesh& h = b->meshes[p]->h;
     const bool tail = p >= b->tail_p0;
     const int pcs = tail ? b->tail_cs : cs, pnpt = tail ? b->tail_npt : b->cluster_npt;
     const int chunk = int((h.n + pcs - 1) / pcs);
-    const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, h, pcs, chunk, pnpt);
+    // pairs planned lazily in the run get their topology fields then
+    // (patch_descriptors)
+    const bool lazy = !tail && p >= b->lazy_from && p < b->planned_end;
+    const DeviceMesh::Topo& t = lazy ? none : ensure_cluster_topo(b->ctx, h, pcs, chunk, pnpt);
     ClusterPair& c = cp[p];
     c.V = h.dev->V;
     c.g_self = h.dev->g_self_f;
     c.inv_val = h.dev->inv_val_f;
-    c.codes = t.codes;
-    c.g = t.g;
-    c.slice_off = t.slice_off;
-    c.halo = t.halo;
-    c.n_halo = t.n_halo;
-    c.halo_stride = t.halo_stride;
-    c.deg = t.deg;
-    c.send = t.send;
-    c.n_send = t.n_send;
-    c.send_stride = t.send_stride;
+    set_topology(c, t);
     c.img4 = b->img_pad + 4 * b->pad_plane * p;
     c.tri_of = host[p].tri_of;
     c.tri = host[p].tri;
@@ -2062,8 +2128,6 @@ void build_fast_descriptors(mrb_batch* b) {
     c.chunk = chunk;
     c.W = b->W;
     c.H = b->H;
-    c.topo_stride = t.topo_stride;
-    c.slices = t.slices;
     c.pitch = b->pad_pitch;
     c.plane = int(b->pad_plane);
     c.xg_s = nullptr;
@@ -2114,6 +2178,38 @@ void build_fast_descriptors(mrb_batch* b) {
     }
   }
   b->cpairs = aupload(b->ctx, cp.data(), cp.size());
+  if (b->lazy_from < std::min(b->planned_end, b->n_pairs)) {
+    b->cp_host = cp;
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&b->cp_pinned), sizeof(ClusterPair) * cp.size(),
+                     cudaHostAllocDefault));
+  }
+}
+
+// Topology fields of the lazily planned pairs [p0, p1) (main shape), into
+// the pinned descriptor copy flush_topo uploads; the launch's dynamic shared
+// memory grows to what they need.
+void patch_descriptors(mrb_batch* b, int p0, int p1) {
+  const int cs = b->cluster_cs, npt = b->cluster_npt;
+  const bool two_u = b->cfg.smoothing_passes >= 2;
+  for (int p = p0; p < p1; ++p) {
+    HostMesh& h = b->meshes[p]->h;
+    const DeviceMesh::Topo& t = ensure_cluster_topo(b->ctx, h, cs, int((h.n + cs - 1) / cs), npt);
+    set_topology(b->cp_host[p], t);
+    b->cp_pinned[p] = b->cp_host[p];
+    const size_t sm = cluster_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride, two_u);
+    if (sm > b->cluster_smem) {
+      b->cluster_smem = sm;
+      cluster_occupancy_cs(cs, npt, sm);  // raises the kernel's smem limit
+    }
+    if (b->push_mode) {
+      const size_t ps =
+          push_dyn_smem(npt, t.topo_stride, t.slices, t.halo_stride, t.send_stride);
+      if (ps > b->push_smem) {
+        b->push_smem = ps;
+        push_occupancy(cs, npt, ps);
+      }
+    }
+  }
 }
 
 // Whole-GPU grid path (meshes larger than one cluster): CS = SMs CTAs per
@@ -2563,8 +2659,11 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
               !std::getenv("MESHREG_B200_NO_TAIL"))
             planned = n_pairs - n_pairs % defer_topo;
           b->planned_end = planned;
+          // only the first wave group is planned here; later groups are
+          // planned in the run, ahead of their launch (flush_topo)
+          b->lazy_from = std::min(defer_topo, planned);
           std::vector<HostMesh*> todo;
-          for (int p = 0; p < planned; ++p) {
+          for (int p = 0; p < b->lazy_from; ++p) {
             HostMesh* h = hm[p];
             const int chunk = int((h->n + cs - 1) / cs);
             if (!h->dev->topo.count(chunk * 16 + npt) &&
@@ -2625,9 +2724,14 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
       else
         build_pairs<float, float>(b.get());
     }
-    // coverage check last: the host work above overlapped the rasters
-    const std::string msg = finish_pixel_maps(ctx, pmj);
-    if (!msg.empty()) return fail(ctx, MRB_E_COVERAGE, msg);
+    // coverage check last: the host work above overlapped the rasters.
+    // mrb_register_many (defer_topo) defers it to mrb_batch_sync.
+    if (defer_topo > 0 && eligible && b->cluster_cs && !b->grid_mode) {
+      b->pending_pm.reset(new PixelMapJob(std::move(pmj)));
+    } else {
+      const std::string msg = finish_pixel_maps(ctx, pmj);
+      if (!msg.empty()) return fail(ctx, MRB_E_COVERAGE, msg);
+    }
     tick("pixel maps");
   } catch (const CudaError& e) {
     return cuda_fail(ctx, e.e);
@@ -2797,6 +2901,18 @@ int mrb_batch_sync(mrb_batch* b) {
   try {
     ck(cudaSetDevice(ctx->device));
     ck(cudaStreamSynchronize(ctx->stream));
+    if (b->pending_pm) {  // deferred coverage check (mrb_register_many)
+      PixelMapJob& job = *b->pending_pm;
+      bool located = false;
+      ck(cudaEventSynchronize(job.done));
+      for (size_t i = 0; i < job.todo.size(); ++i) located = located || job.missing[i] > 0;
+      const std::string msg = finish_pixel_maps(ctx, job);
+      b->pending_pm.reset();
+      if (!msg.empty()) return fail(ctx, MRB_E_COVERAGE, msg);
+      // a pixel the rasters left and the binned locate assigned: the dense
+      // pass skipped it, so the caller reruns the batch undeferred
+      if (located) b->redo = true;
+    }
     b->h_st.resize(b->n_pairs);
     b->h_trace.resize(size_t(b->n_pairs) * b->cfg.max_iterations);
     ck(mrb_copy(b->h_st.data(), b->st, b->n_pairs * sizeof(PairStatus),
@@ -2947,7 +3063,9 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
                               const void* tmpl, const mrb_config* cfg, int32_t chunk_pairs,
                               int32_t out_dtype, double* u, void* ux, void* uy, void* warped,
                               int32_t* iterations_run, double* msd_before, double* msd_after,
-                              double* trace, int32_t* codes, char* messages, int32_t msg_len) {
+                              double* trace, int32_t* codes, char* messages, int32_t msg_len,
+                              bool defer = true) {
+  constexpr int kRedo = -1000;
   // Pipeline: chunk 0 is set up and launched on pipeline stream A.  For every
   // later chunk k the per-mesh device setup (mesh upload, pixel maps,
   // fast-path topologies) runs on the context's own stream while chunk k-1
@@ -3040,8 +3158,8 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
       }
       dev_marks().clear();
     }
-    if (rc == MRB_E_CUDA && first_err == MRB_OK) {
-      first_err = rc;
+    if ((rc == MRB_E_CUDA || rc == MRB_E_COVERAGE || b->redo) && first_err == MRB_OK) {
+      first_err = b->redo ? kRedo : rc;
       first_msg = b->ctx->err;
     }
     if (b->synced) {
@@ -3121,7 +3239,7 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
       stamp("create begin", k);
       const bool grouped = wave > 0 && P > wave && !std::getenv("MESHREG_B200_NO_GROUPS");
       int rc = batch_create_impl(sc, P, meshes + p0, W, H, img_dtype, cfg, forced_cs, forced_npt,
-                                 &b, grouped ? wave : 0);
+                                 &b, grouped && defer ? wave : 0);
       stamp("create end", k);
       if (rc == MRB_OK && k == 0) {
         cs = b->cluster_cs;
@@ -3186,6 +3304,10 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
   }
   for (cudaEvent_t e : dbg_done) cudaEventDestroy(e);
   if (dbg_t0) cudaEventDestroy(dbg_t0);
+  if (first_err == kRedo)  // see mrb_batch::redo: rerun with the blocking coverage check
+    return register_many_impl(ctx, n_pairs, meshes, W, H, img_dtype, reference, tmpl, cfg,
+                              chunk_pairs, out_dtype, u, ux, uy, warped, iterations_run,
+                              msd_before, msd_after, trace, codes, messages, msg_len, false);
   if (first_err != MRB_OK) return fail(ctx, first_err, first_msg);
   return MRB_OK;
 }
