@@ -45,6 +45,8 @@ struct mrb_ctx {
   cudaEvent_t stage_done[3] = {nullptr, nullptr, nullptr};  // last async copy out of pinned[i]
   cudaStream_t copy = nullptr;       // input copies of mrb_register_many
   cudaEvent_t copy_done = nullptr;
+  cudaStream_t aux = nullptr;        // rasters of mrb_register_many (beside the run)
+  cudaEvent_t aux_ev = nullptr;
   unsigned long long* counts = nullptr;  // pinned uncovered-pixel counts
   size_t counts_cap = 0;
   // pinned arena for the small descriptor uploads of a batch creation: a
@@ -878,19 +880,33 @@ struct PixelMapJob {
   std::shared_ptr<unsigned char> slab;    // the maps, when rasterised together
 };
 
-PixelMapJob issue_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int W, int H) {
+// side = true: the rasters run on ctx->aux after the mesh uploads on
+// ctx->stream, so a run enqueued on ctx->stream need not wait for them (its
+// dense passes wait for job.done instead)
+PixelMapJob issue_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int W, int H,
+                             bool side = false) {
   PixelMapJob job;
   job.W = W;
   job.H = H;
   const auto key = std::make_pair(W, H);
   ensure_device_meshes(ctx, meshes, false);
+  cudaStream_t s = ctx->stream;
+  if (side) {
+    if (!ctx->aux) {
+      ck(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+      ck(cudaEventCreateWithFlags(&ctx->aux_ev, cudaEventDisableTiming));
+    }
+    ck(cudaEventRecord(ctx->aux_ev, ctx->stream));  // meshes uploaded
+    ck(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev, 0));
+    s = ctx->aux;
+  }
+  AllocScope scope(s);
   for (HostMesh* h : meshes) {
     if (!h->dev->pixel_maps.count(key) &&
         std::find(job.todo.begin(), job.todo.end(), h) == job.todo.end())
       job.todo.push_back(h);
   }
   if (job.todo.empty()) return job;
-  cudaStream_t s = ctx->stream;
   const size_t npx = size_t(W) * size_t(H);
   if (ctx->counts_cap < job.todo.size()) {  // pinned count slots (grow)
     if (ctx->counts) cudaFreeHost(ctx->counts);
@@ -918,7 +934,7 @@ PixelMapJob issue_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes,
     // every map in one slab: one memset, then one raster and one count launch
     // per kRasterJobs meshes
     const size_t map_bytes = (npx * sizeof(int) + 255) / 256 * 256;
-    job.slab = shared_slab(map_bytes * job.todo.size(), s);
+    job.slab = shared_slab(map_bytes * job.todo.size(), ctx->stream);
     ck(cudaMemsetAsync(job.slab.get(), 0x7f, map_bytes * job.todo.size(), s));
     for (size_t i0 = 0; i0 < job.todo.size(); i0 += kRasterJobs) {
       const size_t nj = std::min<size_t>(kRasterJobs, job.todo.size() - i0);
@@ -1583,6 +1599,8 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
           ck(cudaEventCreateWithFlags(&b->tail_join, cudaEventDisableTiming));
         }
         auto dense_msd = [&](int p0, int p1, cudaStream_t st_) {
+          if (b->pending_pm && b->pending_pm->done)  // rasters on the side stream
+            ck(cudaStreamWaitEvent(st_, b->pending_pm->done, 0));
           const int blk0 = host[p0].pix_blk_begin;
           const int blk1 = p1 < b->n_pairs ? host[p1].pix_blk_begin : b->n_pix_blocks;
           k_dense_fast<<<blk1 - blk0, kPixBlock, 0, st_>>>(
@@ -1644,6 +1662,8 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
         ck(cudaGetLastError());
         return launches;
       }
+      if (b->pending_pm && b->pending_pm->done)  // side-stream rasters (pixel maps)
+        ck(cudaStreamWaitEvent(s, b->pending_pm->done, 0));
       flush_topo(b, b->n_pairs, s, s);  // deferred topologies not yet uploaded
       flush_tail_topo(b, s, s);
       if (tm == &dummy && !b->grid_mode && b->tail_p0 > 0 && b->tail_p0 < b->n_pairs) {
@@ -2383,6 +2403,11 @@ int mrb_ctx_destroy(mrb_ctx* ctx) {
     cudaStreamDestroy(ctx->copy);
   }
   if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
+  if (ctx->aux) {
+    cudaStreamSynchronize(ctx->aux);
+    cudaStreamDestroy(ctx->aux);
+  }
+  if (ctx->aux_ev) cudaEventDestroy(ctx->aux_ev);
   for (void* pin : ctx->pinned)
     if (pin) cudaFreeHost(pin);
   if (ctx->counts) cudaFreeHost(ctx->counts);
@@ -2677,9 +2702,9 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
             ck(cudaEventCreateWithFlags(&slab_ev, cudaEventDisableTiming));
             ck(cudaEventRecord(slab_ev, ctx->stream));  // the slab exists from here on
           }
-          // rasters after the slab allocation, so the first group's topology
-          // copy (on the batch's copy stream) need not wait for them
-          pmj = issue_pixel_maps(ctx, hm, W, H);
+          // rasters on the side stream: the first group's loop and topology
+          // copy need not wait for them (its dense pass does)
+          pmj = issue_pixel_maps(ctx, hm, W, H, true);
           rasters_issued = true;
           if (!todo.empty()) {
             if (!b->copy_stream)
