@@ -26,6 +26,7 @@
 #include "cluster.cuh"
 #include "grid.cuh"
 #include "push.cuh"
+#include "cluster64.cuh"
 #include "pixel.cuh"
 #include "kernels.cuh"
 #include "mesh_host.h"
@@ -110,6 +111,7 @@ struct DeviceMesh {
     std::shared_ptr<unsigned char> hold;  // owner when the slab is a shared upload's slice
     uint16_t* codes = nullptr;
     float2* g = nullptr;
+    double2* g64 = nullptr;  // fp64 coefficients (k_cluster64 topologies)
     uint32_t* slice_off = nullptr;
     uint32_t* halo = nullptr;
     int* n_halo = nullptr;
@@ -601,7 +603,8 @@ struct TopoHost {
   std::vector<int> n_send;           // [cs]
 };
 
-TopoHost plan_topo(const HostMesh& h, int cs, int chunk, int npt) {
+// gbytes: bytes per SELL coefficient entry (float2 8, double2 16 for k_cluster64)
+TopoHost plan_topo(const HostMesh& h, int cs, int chunk, int npt, int gbytes = 8) {
   const int n = int(h.n);
   const int SLOTS = kClusterThreads * npt;
   TopoHost t;
@@ -671,7 +674,7 @@ TopoHost plan_topo(const HostMesh& h, int cs, int chunk, int npt) {
       std::copy(sends[r].begin(), sends[r].end(), t.send.begin() + size_t(r) * t.sstride);
     }
   }
-  const size_t bytes[8] = {size_t(cs) * t.stride * 2, size_t(cs) * t.stride * 8,
+  const size_t bytes[8] = {size_t(cs) * t.stride * 2, size_t(cs) * t.stride * gbytes,
                            t.soff.size() * 4, t.halo.size() * 4, size_t(cs) * 4, size_t(n),
                            t.send.size() * 4, size_t(cs) * 4};
   for (int k = 0; k < 8; ++k) {
@@ -695,12 +698,14 @@ inline uint16_t zero_slot(int npt, int hstride) {
   return uint16_t(kClusterThreads * npt + hstride - 1);
 }
 
-void write_topo(const HostMesh& h, int cs, const TopoHost& t, unsigned char* dst, int npt) {
+void write_topo(const HostMesh& h, int cs, const TopoHost& t, unsigned char* dst, int npt,
+                bool f64 = false) {
   const int n = int(h.n), chunk = t.chunk;
   uint16_t* codes = reinterpret_cast<uint16_t*>(dst + t.off[0]);
   float2* g = reinterpret_cast<float2*>(dst + t.off[1]);
+  double2* g64 = reinterpret_cast<double2*>(dst + t.off[1]);
   std::fill(codes, codes + size_t(cs) * t.stride, zero_slot(npt, t.hstride));
-  std::memset(g, 0, size_t(cs) * t.stride * 8);
+  std::memset(g, 0, size_t(cs) * t.stride * (f64 ? 16 : 8));
   unsigned char* deg = dst + t.off[5];
   for (int i = 0; i < n; ++i) {
     const int r = i / chunk, s = i - r * chunk;
@@ -712,7 +717,10 @@ void write_topo(const HostMesh& h, int cs, const TopoHost& t, unsigned char* dst
       const int k = q - b;
       const size_t at = base + 64 * size_t(k >> 1) + (k & 1);
       codes[at] = t.code[q];
-      g[at] = make_float2(float(h.g_nb[2 * q]), float(h.g_nb[2 * q + 1]));
+      if (f64)
+        g64[at] = make_double2(h.g_nb[2 * q], h.g_nb[2 * q + 1]);
+      else
+        g[at] = make_float2(float(h.g_nb[2 * q]), float(h.g_nb[2 * q + 1]));
     }
   }
   std::memcpy(dst + t.off[2], t.soff.data(), t.soff.size() * 4);
@@ -847,6 +855,67 @@ void ensure_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, in
   tick("host plan");
   upload_cluster_topos(ctx, up, 0, up.meshes.size(), ctx->stream);
   tick("fill + copy");
+}
+
+// fp64 topologies of k_cluster64 (one node per thread): the same paired
+// SELL layout with double2 coefficients, cached under their own key; planned
+// and packed on the worker pool, uploaded as one copy
+int topo64_key(int chunk) { return -(chunk * 16 + 1); }
+
+void ensure_cluster_topos64(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int cs) {
+  std::vector<HostMesh*> todo;
+  for (HostMesh* h : meshes) {
+    const int chunk = int((h->n + cs - 1) / cs);
+    if (!h->dev->topo.count(topo64_key(chunk)) &&
+        std::find(todo.begin(), todo.end(), h) == todo.end())
+      todo.push_back(h);
+  }
+  if (todo.empty()) return;
+  std::vector<TopoHost> th(todo.size());
+  parallel_for(todo.size(), [&](size_t i) {
+    th[i] = plan_topo(*todo[i], cs, int((todo[i]->n + cs - 1) / cs), 1, 16);
+  });
+  std::vector<size_t> base(todo.size());
+  size_t total = 0;
+  for (size_t i = 0; i < todo.size(); ++i) {
+    base[i] = total;
+    total += th[i].total;
+  }
+  // packed straight into the pinned staging buffer (a pageable copy of the
+  // ~2 MB per C2-size mesh would stage synchronously)
+  unsigned char* packed =
+      static_cast<unsigned char*>(pinned_stage(ctx, std::max<size_t>(total, 1), 1));
+  parallel_for(todo.size(), [&](size_t i) {
+    write_topo(*todo[i], cs, th[i], packed + base[i], 1, true);
+  });
+  AllocScope scope(ctx->stream);
+  const std::shared_ptr<unsigned char> all = shared_slab(std::max<size_t>(total, 1), ctx->stream);
+  ck(mrb_copy_async(all.get(), packed, total, cudaMemcpyHostToDevice, ctx->stream));
+  ck(cudaEventRecord(ctx->stage_done[1], ctx->stream));  // staging reusable after this
+  for (size_t i = 0; i < todo.size(); ++i) {
+    DeviceMesh::Topo t;
+    unsigned char* slab = all.get() + base[i];
+    t.chunk = th[i].chunk;
+    t.topo_stride = th[i].stride;
+    t.slices = th[i].slices;
+    t.halo_stride = th[i].hstride;
+    t.slab = slab;
+    t.hold = all;
+    t.codes = reinterpret_cast<uint16_t*>(slab + th[i].off[0]);
+    t.g64 = reinterpret_cast<double2*>(slab + th[i].off[1]);
+    t.slice_off = reinterpret_cast<uint32_t*>(slab + th[i].off[2]);
+    t.halo = reinterpret_cast<uint32_t*>(slab + th[i].off[3]);
+    t.n_halo = reinterpret_cast<int*>(slab + th[i].off[4]);
+    t.deg = slab + th[i].off[5];
+    todo[i]->dev->topo[topo64_key(t.chunk)] = t;
+  }
+}
+
+// bytes of dynamic shared memory of k_cluster64 (Cluster64Smem carve)
+size_t cluster64_dyn_smem(int topo_stride, int slices, int halo_stride, bool two_u) {
+  const size_t S = size_t(kClusterThreads), X = S + halo_stride;
+  return size_t(topo_stride) * (16 + 2) + S * (16 + 16 + 8) + X * (16 * (two_u ? 2 : 1) + 8) +
+         size_t(halo_stride) * 4 + size_t(slices) * 4;
 }
 
 // bytes of dynamic shared memory of k_cluster_register (ClusterSmem carve)
@@ -1094,6 +1163,12 @@ struct mrb_batch {
   std::unique_ptr<TopoUpload> tail_up;  // the tail pairs' latency-shape topologies
   bool tail_done = false;
   int planned_end = 1 << 30;  // pairs past this got no throughput-shape topology planned
+  // fp64 batches: the generic path's state, image and dense pass, with the
+  // descent loop in one persistent k_cluster64 launch (c64_cs CTAs per pair)
+  int c64_cs = 0;
+  size_t c64_smem = 0;
+  void* c64_pairs = nullptr;  // ClusterPair64[n_pairs]
+  double2* pad64 = nullptr;   // padded fp64 images [pair][(H+2) x (W+2)]
   // mrb_register_many: main-shape pairs [lazy_from, planned_end) are planned
   // per wave group in the run (flush_topo), while earlier groups compute
   int lazy_from = 1 << 30;
@@ -1167,7 +1242,7 @@ struct mrb_batch {
     if (grp_fork) cudaEventDestroy(grp_fork);
     if (grp_join) cudaEventDestroy(grp_join);
     void* ptrs[] = {pairs, st, blk_pair, pix_blk_pair, partials, pix_partials, state, traces,
-                    img, stage, src_ptrs, img_ptrs, dense, u_out, conv, cpairs, img_pad,
+                    img, stage, src_ptrs, img_ptrs, dense, u_out, conv, cpairs, img_pad, c64_pairs, pad64,
                     prof_host ? nullptr : phase_prof, xbuf, xbar, xexports};
     if (prof_host) cudaFreeHost(prof_host);
     for (void* p : ptrs) dev_free(p, ctx ? ctx->stream : nullptr);
@@ -1563,6 +1638,9 @@ void flush_tail_topo(mrb_batch* b, cudaStream_t copy, cudaStream_t s) {
   }
 }
 
+void setup_cluster64(mrb_batch* b);
+void launch_cluster64(mrb_batch* b);
+
 template <typename TapT, typename Real>
 int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
   KernelTimer dummy;
@@ -1722,7 +1800,19 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
   const Real tau = Real(b->cfg.tau), lam = Real(b->cfg.lam);
   const int passes = b->cfg.smoothing_passes;
   tm->mark(-1);
-  for (int k = 0; k < b->cfg.max_iterations; ++k) {
+  if (b->c64_cs) {  // fp64: the whole descent loop in one persistent cluster launch
+    const size_t padn = size_t(b->W + 2) * (b->H + 2);
+    const dim3 pg(unsigned(std::min<size_t>((padn + 255) / 256, 1024)), b->n_pairs);
+    if (b->tap_d)
+      k_pad_pair64<double><<<pg, 256, 0, s>>>(static_cast<const ClusterPair64*>(b->c64_pairs));
+    else
+      k_pad_pair64<float><<<pg, 256, 0, s>>>(static_cast<const ClusterPair64*>(b->c64_pairs));
+    ++launches;
+    launch_cluster64(b);
+    tm->mark(0);
+    ++launches;
+  }
+  for (int k = 0; k < (b->c64_cs ? 0 : b->cfg.max_iterations); ++k) {
     k_sample<TapT, Real><<<nb, kNodeBlock, 0, s>>>(pairs, b->st, b->blk_pair, b->partials, k, tol);
     tm->mark(0);
     k_grad<TapT, Real><<<nb, kNodeBlock, 0, s>>>(pairs, b->st, b->blk_pair, k, tau, passes);
@@ -1772,6 +1862,7 @@ int64_t dispatch_enqueue(mrb_batch* b, KernelTimer* tm = nullptr) {
 int64_t launches_per_run(const mrb_batch* b) {
   if (b->grid_mode) return 3 + b->n_pairs;  // pad, one grid loop per pair, dense, msd
   if (b->cluster_cs) return 4 + (b->tail_p0 < b->n_pairs);  // pad, loop(s), dense, msd
+  if (b->c64_cs) return 7;  // interleave, reset, pad, loop, dense, msd, unpermute
   return 2 + int64_t(b->cfg.max_iterations) * (2 + b->cfg.smoothing_passes) + 3;
 }
 
@@ -2739,6 +2830,7 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
       build_pairs<float, float>(b.get());
     tick("buffers + descriptors");
     if (eligible) setup_cluster_path(b.get());
+    if (b->real_d) setup_cluster64(b.get());
     tick("cluster path setup");
     if (eligible && !b->cluster_cs) {
       // predicted fast path did not fit after all: generic path needs the rings
@@ -2764,6 +2856,133 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
   *out = b.release();
   return MRB_OK;
 }
+// fp64 persistent cluster loop (k_cluster64) for a batch on the generic path
+// (fp64 state, fp32-exact images): every mesh fits 16 CTAs x 768 nodes with
+// one-rings of <= kMaxDeg.  Cluster size by the cost model of
+// choose_cluster_shape (waves x nodes per CTA).  MESHREG_B200_PATH=generic
+// keeps the three-kernel loop.
+template <int NPT>
+int cluster64_occupancy(int CS, size_t smem) {
+  auto kern = k_cluster64<NPT>;
+  if (!raise_smem_limit_of(kern, smem)) return 0;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(unsigned(CS));
+  lc.blockDim = dim3(kClusterThreads);
+  lc.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &lc) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+void setup_cluster64(mrb_batch* b) {
+  const char* env = std::getenv("MESHREG_B200_PATH");
+  const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
+  if (env && std::string(env) == "generic") return;
+  int64_t nmax = 0;
+  for (mrb_mesh* m : b->meshes) {
+    nmax = std::max<int64_t>(nmax, m->h.n);
+    if (m->h.max_deg > kMaxDeg) return;
+  }
+  const int cs_min = int((nmax + kClusterThreads - 1) / kClusterThreads);
+  if (cs_min > 16) return;
+  const bool two_u = b->cfg.smoothing_passes >= 2;
+  std::vector<HostMesh*> hm;
+  for (mrb_mesh* m : b->meshes) hm.push_back(&m->h);
+  double best = 1e300;
+  int best_cs = 0;
+  size_t best_smem = 0;
+  for (int cs = cs_min; cs <= 16; ++cs) {
+    ensure_cluster_topos64(b->ctx, hm, cs);
+    size_t smem = 0;
+    for (HostMesh* h : hm) {
+      const DeviceMesh::Topo& t = h->dev->topo.at(topo64_key(int((h->n + cs - 1) / cs)));
+      smem = std::max(smem, cluster64_dyn_smem(t.topo_stride, t.slices, t.halo_stride, two_u));
+    }
+    const int occ = cluster64_occupancy<1>(cs, smem);
+    if (occ < 1) continue;
+    const double cost = double((b->n_pairs + occ - 1) / occ) * double((nmax + cs - 1) / cs);
+    if (cost < best) {
+      best = cost;
+      best_cs = cs;
+      best_smem = smem;
+    }
+  }
+  if (!best_cs) {
+    if (dbg) std::fprintf(stderr, "meshreg_b200: fp64 generic loop (no cluster shape fits)\n");
+    return;
+  }
+  // the generic path's descriptors: PairDev<float, double> or, with fp64
+  // image storage, PairDev<double, double> (same fields, taps differ)
+  const PairDev<float, double>* host32 =
+      reinterpret_cast<const PairDev<float, double>*>(b->pairs_host.data());
+  const PairDev<double, double>* host64 =
+      reinterpret_cast<const PairDev<double, double>*>(b->pairs_host.data());
+  std::vector<ClusterPair64> cp(b->n_pairs);
+  const size_t padn = size_t(b->W + 2) * (b->H + 2);
+  b->pad64 = dalloc<double2>(padn * b->n_pairs);
+  for (int p = 0; p < b->n_pairs; ++p) {
+    HostMesh& h = b->meshes[p]->h;
+    const int chunk = int((h.n + best_cs - 1) / best_cs);
+    const DeviceMesh::Topo& t = h.dev->topo.at(topo64_key(chunk));
+    ClusterPair64& c = cp[p];
+    c.tap_d = b->tap_d ? 1 : 0;
+    c.pad = b->pad64 + padn * p;
+    c.V = b->tap_d ? host64[p].V : host32[p].V;
+    c.g_self = b->tap_d ? host64[p].g_self : host32[p].g_self;
+    c.inv_val = b->tap_d ? host64[p].inv_val : host32[p].inv_val;
+    c.codes = t.codes;
+    c.g = t.g64;
+    c.slice_off = t.slice_off;
+    c.halo = t.halo;
+    c.n_halo = t.n_halo;
+    c.img = b->tap_d ? static_cast<const void*>(host64[p].img)
+                     : static_cast<const void*>(host32[p].img);
+    c.u = b->tap_d ? host64[p].u : host32[p].u;
+    c.trace = b->tap_d ? host64[p].trace : host32[p].trace;
+    c.n = int(h.n);
+    c.chunk = chunk;
+    c.W = b->W;
+    c.H = b->H;
+    c.topo_stride = t.topo_stride;
+    c.slices = t.slices;
+    c.halo_stride = t.halo_stride;
+  }
+  b->c64_pairs = aupload(b->ctx, cp.data(), cp.size());
+  b->c64_cs = best_cs;
+  b->c64_smem = best_smem;
+  if (std::getenv("MESHREG_B200_DEBUG"))
+    std::fprintf(stderr, "meshreg_b200: fp64 cluster %d CTAs x 1 node/thread, %zu B smem\n",
+                 best_cs, best_smem);
+}
+
+void launch_cluster64(mrb_batch* b) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(unsigned(b->n_pairs * b->c64_cs));
+  lc.blockDim = dim3(kClusterThreads);
+  lc.dynamicSmemBytes = b->c64_smem;
+  lc.stream = b->ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = b->c64_cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  ck(cudaLaunchKernelEx(&lc, k_cluster64<1>, static_cast<const ClusterPair64*>(b->c64_pairs),
+                        b->st, int(b->cfg.max_iterations), double(b->cfg.energy_tolerance),
+                        double(b->cfg.tau), double(b->cfg.lam), int(b->cfg.smoothing_passes)));
+}
+
 // Split a fast-path batch into wave groups of `per` pairs (see mrb_batch).
 void batch_set_groups(mrb_batch* b, int per) {
   if (!b->cluster_cs || per <= 0 || per >= b->n_pairs) return;
@@ -2978,12 +3197,14 @@ int mrb_batch_pair_status(mrb_batch* b, int32_t p, int32_t* iters, double* msd_b
 int64_t mrb_batch_launches_per_run(const mrb_batch* b) { return launches_per_run(b); }
 
 const char* mrb_batch_loop_kernel(const mrb_batch* b) {
+  if (b->c64_cs) return "k_cluster64";
   if (!b->cluster_cs) return "k_sample";
   if (b->grid_mode) return b->grid_flags ? "k_grid_flags" : "k_grid_register";
   return b->push_mode ? "k_cluster_push" : "k_cluster_register";
 }
 
 int32_t mrb_batch_path(const mrb_batch* b) {
+  if (b->c64_cs) return b->c64_cs;
   return b->grid_mode ? -b->cluster_cs : b->cluster_cs;
 }
 
@@ -3040,7 +3261,7 @@ int mrb_batch_kernel_bytes(const mrb_batch* b, double* out) {
   out[1] = 16.0 * nv + 60.0 * nt;
   out[2] = 20.0 * nv + 8.0 * ne;
   out[3] = 128.0 * double(b->W) * b->H * b->n_pairs;
-  if (b->cluster_cs) {  // one launch runs every iteration of every pair
+  if (b->cluster_cs || b->c64_cs) {  // one launch runs every iteration of every pair
     out[0] = double(b->cfg.max_iterations) * (184.0 * nv + 60.0 * nt + 8.0 * ne);
     out[1] = out[2] = 0.0;
   }

@@ -114,6 +114,35 @@ def test_c3_x255_chaotic_prefix(precision, iters, tol_u, tol_w, monkeypatch):
     assert abs(rep.msd_after / info["msd_after"] - 1) < (1e-10 if precision == "f64" else 1e-5)
 
 
+@pytest.mark.parametrize("x255", [False, True])
+def test_fp64_cluster_loop_matches_oracle(x255, monkeypatch):
+    """precision="f64" (the reference's width, the API default): a C2 pair
+    on the persistent fp64 cluster kernel (k_cluster64, 16 CTAs x 768 nodes)
+    against the live oracle at 1e-9, and the same run through the generic
+    three-kernel loop (MESHREG_B200_PATH=generic) agrees with it."""
+    monkeypatch.delenv("MESHREG_B200_PATH", raising=False)
+    spec, re32, te32, V, T = load("c2", 0, x255)
+    iters = 200 if not x255 else 40
+    u_ref, info = O.register(re32, te32, O.Mesh(V, T), tau=0.005, lam=0.8, max_iterations=iters,
+                             smoothing_passes=1, energy_tolerance=0.0)
+    S = spec.size
+    re = mrb.ImageGrid(S, S, re32.astype(np.float64))
+    te = mrb.ImageGrid(S, S, te32.astype(np.float64))
+    cfg = mrb.SolverConfig(max_iterations=iters, energy_tolerance=0.0)
+    u, rep, (ux, uy, warped) = mrb.register(re, te, mrb.TriMesh(V, T), cfg, precision="f64",
+                                            return_dense=True)
+    eu, ew = relinf(u, u_ref), relinf(warped, info["warped"])
+    print(f"\nc2{'x255' if x255 else ''} f64 cluster {iters} it: u {eu:.2e} warped {ew:.2e}")
+    assert rep.iterations_run == iters
+    assert eu < 1e-9 and ew < 1e-9
+    assert relinf(ux, info["ux"]) < 1e-9 and relinf(uy, info["uy"]) < 1e-9
+    assert relinf(rep.energy_trace, info["energy_trace"]) < 1e-10
+    assert abs(rep.msd_after / info["msd_after"] - 1) < 1e-10
+    monkeypatch.setenv("MESHREG_B200_PATH", "generic")
+    u2, rep2 = mrb.register(re, te, mrb.TriMesh(V, T), cfg, precision="f64")
+    assert relinf(u2, u) < 1e-9
+
+
 def test_c5_matches_oracle(monkeypatch):
     """BASELINE config 5 as specified: the 4096^2 pair (300 blobs + 100
     rectangles, 24 px peak warp), its ~500k-node content-adaptive mesh from the
