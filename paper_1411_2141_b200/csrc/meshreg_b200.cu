@@ -90,6 +90,7 @@ struct DeviceMesh {
   unsigned char* slab = nullptr;
   std::shared_ptr<unsigned char> slab_hold;  // set when `slab` is a slice of a shared upload
   unsigned char* slab64 = nullptr;
+  std::shared_ptr<unsigned char> slab64_hold;  // set when slab64 is a shared upload's slice
   unsigned char* slab_ring = nullptr;
   double2* V = nullptr;
   int* nb_ptr = nullptr;
@@ -120,7 +121,7 @@ struct DeviceMesh {
     int* n_send = nullptr;
     int chunk = 0, topo_stride = 0, slices = 0, halo_stride = 0, send_stride = 0;
   };
-  std::map<int, Topo> topo;  // key: chunk size
+  std::map<int64_t, Topo> topo;  // key: topo_key(cluster size, chunk, nodes/thread, fp64)
   int max_deg = 0;
   ~DeviceMesh() {
     int cur = -1;
@@ -130,7 +131,10 @@ struct DeviceMesh {
       slab_hold.reset();
     else
       dev_free(slab, stream);
-    dev_free(slab64, stream);
+    if (slab64_hold)
+      slab64_hold.reset();
+    else
+      dev_free(slab64, stream);
     dev_free(slab_ring, stream);
     for (auto& kv : pixel_maps)
       if (!pixel_map_hold.count(kv.first)) dev_free(kv.second, stream);
@@ -563,7 +567,9 @@ void ensure_device_mesh(mrb_ctx* ctx, HostMesh& h) {
 void ensure_device_mesh_f64(mrb_ctx* ctx, HostMesh& h) {
   ensure_device_mesh(ctx, h);  // includes the one-ring arrays
   DeviceMesh& d = *h.dev;
-  if (d.slab64) return;
+  if (d.slab64 && d.g_nb_d) return;
+  if (d.slab64_hold) d.slab64_hold.reset();  // the self-term-only slice
+  else if (d.slab64) dev_free(d.slab64, ctx->stream);
   AllocScope scope(ctx->stream);
   const size_t n = size_t(h.n), ne2 = h.nb_idx.size();
   const size_t o1 = (n * 16 + 255) / 256 * 256, o2 = o1 + (ne2 * 16 + 255) / 256 * 256;
@@ -578,6 +584,41 @@ void ensure_device_mesh_f64(mrb_ctx* ctx, HostMesh& h) {
   d.inv_val_d = reinterpret_cast<double*>(d.slab64 + o2);
 }
 
+// fp64 self terms and 1/valence only (what k_cluster64 reads besides its
+// topology), for many meshes: one pinned-staged copy
+void ensure_device_meshes_f64_self(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes) {
+  std::vector<HostMesh*> todo;
+  for (HostMesh* h : meshes)
+    if (!h->dev->g_self_d && std::find(todo.begin(), todo.end(), h) == todo.end())
+      todo.push_back(h);
+  if (todo.empty()) return;
+  std::vector<size_t> base(todo.size());
+  size_t total = 0;
+  for (size_t i = 0; i < todo.size(); ++i) {
+    base[i] = total;
+    total += (size_t(todo[i]->n) * 16 + 255) / 256 * 256 + (size_t(todo[i]->n) * 8 + 255) / 256 * 256;
+  }
+  unsigned char* stage = static_cast<unsigned char*>(pinned_stage(ctx, total, 0));
+  parallel_for(todo.size(), [&](size_t i) {
+    const HostMesh& h = *todo[i];
+    const size_t n = size_t(h.n), o = (n * 16 + 255) / 256 * 256;
+    std::memcpy(stage + base[i], h.g_self.data(), n * 16);
+    std::memcpy(stage + base[i] + o, h.inv_val.data(), n * 8);
+  });
+  AllocScope scope(ctx->stream);
+  const std::shared_ptr<unsigned char> all = shared_slab(total, ctx->stream);
+  ck(mrb_copy_async(all.get(), stage, total, cudaMemcpyHostToDevice, ctx->stream));
+  ck(cudaEventRecord(ctx->stage_done[0], ctx->stream));
+  for (size_t i = 0; i < todo.size(); ++i) {
+    DeviceMesh& d = *todo[i]->dev;
+    const size_t o = (size_t(todo[i]->n) * 16 + 255) / 256 * 256;
+    d.slab64 = all.get() + base[i];
+    d.slab64_hold = all;
+    d.g_self_d = reinterpret_cast<double2*>(d.slab64);
+    d.inv_val_d = reinterpret_cast<double*>(d.slab64 + o);
+  }
+}
+
 // Shared-memory topology of the cluster kernel for `cs` CTAs of `chunk` nodes
 // and `npt` slots per thread:
 //  * SELL-32 one-rings — for every 32-slot slice of a CTA's chunk, entry e of
@@ -589,7 +630,14 @@ void ensure_device_mesh_f64(mrb_ctx* ctx, HostMesh& h) {
 // Host plan of one fast-path topology (cluster of cs CTAs, `chunk` nodes per
 // CTA): SELL-32 slice offsets, halo lists and the code of every one-ring
 // entry.  write_topo() then packs it straight into (pinned) memory.
+// A topology's arrays depend on the cluster size as well as the chunk (two
+// sizes can give the same chunk for a small mesh), so both are in the key.
+inline int64_t topo_key(int cs, int chunk, int npt, bool f64 = false) {
+  return (int64_t(cs) << 40) | (int64_t(chunk) << 8) | (int64_t(npt) << 1) | int64_t(f64);
+}
+
 struct TopoHost {
+  int cs = 0;
   int chunk = 0, stride = 0, slices = 0, hstride = 0, sstride = 0;
   size_t off[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   size_t total = 0;                  // packed bytes
@@ -608,6 +656,7 @@ TopoHost plan_topo(const HostMesh& h, int cs, int chunk, int npt, int gbytes = 8
   const int n = int(h.n);
   const int SLOTS = kClusterThreads * npt;
   TopoHost t;
+  t.cs = cs;
   t.chunk = chunk;
   t.slices = (chunk + 31) / 32;
   t.soff.assign(size_t(cs) * t.slices, 0);
@@ -748,12 +797,12 @@ DeviceMesh::Topo& install_topo(HostMesh& h, int npt, const TopoHost& th,
   t.send = reinterpret_cast<uint32_t*>(slab + th.off[6]);
   t.n_send = reinterpret_cast<int*>(slab + th.off[7]);
   t.send_stride = th.sstride;
-  return h.dev->topo[th.chunk * 16 + npt] = t;
+  return h.dev->topo[topo_key(th.cs, th.chunk, npt)] = t;
 }
 
 const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, int chunk,
                                             int npt) {
-  auto it = h.dev->topo.find(chunk * 16 + npt);
+  auto it = h.dev->topo.find(topo_key(cs, chunk, npt));
   if (it != h.dev->topo.end()) return it->second;
   AllocScope scope(ctx->stream);
   const TopoHost th = plan_topo(h, cs, chunk, npt);
@@ -837,7 +886,7 @@ void ensure_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, in
   std::vector<HostMesh*> todo;
   for (HostMesh* h : meshes) {
     const int chunk = int((h->n + cs - 1) / cs);
-    if (!h->dev->topo.count(chunk * 16 + npt) &&
+    if (!h->dev->topo.count(topo_key(cs, chunk, npt)) &&
         std::find(todo.begin(), todo.end(), h) == todo.end())
       todo.push_back(h);
   }
@@ -860,13 +909,13 @@ void ensure_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, in
 // fp64 topologies of k_cluster64 (one node per thread): the same paired
 // SELL layout with double2 coefficients, cached under their own key; planned
 // and packed on the worker pool, uploaded as one copy
-int topo64_key(int chunk) { return -(chunk * 16 + 1); }
+int64_t topo64_key(int cs, int chunk) { return topo_key(cs, chunk, 1, true); }
 
 void ensure_cluster_topos64(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int cs) {
   std::vector<HostMesh*> todo;
   for (HostMesh* h : meshes) {
     const int chunk = int((h->n + cs - 1) / cs);
-    if (!h->dev->topo.count(topo64_key(chunk)) &&
+    if (!h->dev->topo.count(topo64_key(cs, chunk)) &&
         std::find(todo.begin(), todo.end(), h) == todo.end())
       todo.push_back(h);
   }
@@ -907,7 +956,7 @@ void ensure_cluster_topos64(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, 
     t.halo = reinterpret_cast<uint32_t*>(slab + th[i].off[3]);
     t.n_halo = reinterpret_cast<int*>(slab + th[i].off[4]);
     t.deg = slab + th[i].off[5];
-    todo[i]->dev->topo[topo64_key(t.chunk)] = t;
+    todo[i]->dev->topo[topo64_key(cs, t.chunk)] = t;
   }
 }
 
@@ -1586,7 +1635,7 @@ void flush_topo(mrb_batch* b, int p1, cudaStream_t copy, cudaStream_t s) {
     for (int p = b->lazy_from; p < pe; ++p) {
       HostMesh* h = &b->meshes[p]->h;
       const int chunk = int((h->n + cs - 1) / cs);
-      if (!h->dev->topo.count(chunk * 16 + npt) &&
+      if (!h->dev->topo.count(topo_key(cs, chunk, npt)) &&
           std::find(todo.begin(), todo.end(), h) == todo.end())
         todo.push_back(h);
     }
@@ -1640,6 +1689,16 @@ void flush_tail_topo(mrb_batch* b, cudaStream_t copy, cudaStream_t s) {
 
 void setup_cluster64(mrb_batch* b);
 void launch_cluster64(mrb_batch* b);
+
+// fp64 batch k_cluster64 can run: every mesh fits 16 CTAs x 768 nodes with
+// one-rings of <= kMaxDeg (MESHREG_B200_PATH=generic keeps the 3-kernel loop)
+bool cluster64_candidate(const mrb_batch* b) {
+  const char* env = std::getenv("MESHREG_B200_PATH");
+  if (env && std::string(env) == "generic") return false;
+  for (const mrb_mesh* m : b->meshes)
+    if (m->h.n > 16 * kClusterThreads || m->h.max_deg > kMaxDeg) return false;
+  return true;
+}
 
 template <typename TapT, typename Real>
 int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
@@ -2137,7 +2196,7 @@ void setup_tail(mrb_batch* b, size_t main_smem) {
     std::vector<HostMesh*> todo;
     for (HostMesh* h : hm) {
       const int chunk = int((h->n + cs - 1) / cs);
-      if (!h->dev->topo.count(chunk * 16 + npt) &&
+      if (!h->dev->topo.count(topo_key(cs, chunk, npt)) &&
           std::find(todo.begin(), todo.end(), h) == todo.end())
         todo.push_back(h);
     }
@@ -2744,11 +2803,18 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
     const bool eligible = mode != 0;
     b->forced_cs = forced_cs;
     b->forced_npt = forced_npt;
-    ensure_device_meshes(ctx, hm, !eligible);
-    if (!eligible)  // meshes uploaded earlier by a fast-path batch lack them
+    // fp64 batches that k_cluster64 can run need neither the generic path's
+    // one-ring arrays nor its fp64 ring operator (setup_cluster64 falls back)
+    const bool c64 = b->real_d && cluster64_candidate(b.get());
+    ensure_device_meshes(ctx, hm, !eligible && !c64);
+    if (!eligible && !c64)  // meshes uploaded earlier by a fast-path batch lack them
       for (HostMesh* h : hm) ensure_device_mesh_ring(ctx, *h);
-    if (b->real_d)
-      for (HostMesh* h : hm) ensure_device_mesh_f64(ctx, *h);
+    if (b->real_d) {
+      if (c64)
+        ensure_device_meshes_f64_self(ctx, hm);
+      else
+        for (HostMesh* h : hm) ensure_device_mesh_f64(ctx, *h);
+    }
     tick("mesh upload");
     PixelMapJob pmj;
     bool rasters_issued = false;
@@ -2782,7 +2848,7 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
           for (int p = 0; p < b->lazy_from; ++p) {
             HostMesh* h = hm[p];
             const int chunk = int((h->n + cs - 1) / cs);
-            if (!h->dev->topo.count(chunk * 16 + npt) &&
+            if (!h->dev->topo.count(topo_key(cs, chunk, npt)) &&
                 std::find(todo.begin(), todo.end(), h) == todo.end())
               todo.push_back(h);
           }
@@ -2831,6 +2897,17 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
     tick("buffers + descriptors");
     if (eligible) setup_cluster_path(b.get());
     if (b->real_d) setup_cluster64(b.get());
+    if (c64 && !b->c64_cs) {  // no cluster shape after all: the generic loop's arrays
+      for (HostMesh* h : hm) {
+        ensure_device_mesh_ring(ctx, *h);
+        ensure_device_mesh_f64(ctx, *h);
+      }
+      free_pairs(b.get());
+      if (b->tap_d)
+        build_pairs<double, double>(b.get());
+      else
+        build_pairs<float, double>(b.get());
+    }
     tick("cluster path setup");
     if (eligible && !b->cluster_cs) {
       // predicted fast path did not fit after all: generic path needs the rings
@@ -2905,7 +2982,7 @@ void setup_cluster64(mrb_batch* b) {
     ensure_cluster_topos64(b->ctx, hm, cs);
     size_t smem = 0;
     for (HostMesh* h : hm) {
-      const DeviceMesh::Topo& t = h->dev->topo.at(topo64_key(int((h->n + cs - 1) / cs)));
+      const DeviceMesh::Topo& t = h->dev->topo.at(topo64_key(cs, int((h->n + cs - 1) / cs)));
       smem = std::max(smem, cluster64_dyn_smem(t.topo_stride, t.slices, t.halo_stride, two_u));
     }
     const int occ = cluster64_occupancy<1>(cs, smem);
@@ -2933,7 +3010,7 @@ void setup_cluster64(mrb_batch* b) {
   for (int p = 0; p < b->n_pairs; ++p) {
     HostMesh& h = b->meshes[p]->h;
     const int chunk = int((h.n + best_cs - 1) / best_cs);
-    const DeviceMesh::Topo& t = h.dev->topo.at(topo64_key(chunk));
+    const DeviceMesh::Topo& t = h.dev->topo.at(topo64_key(best_cs, chunk));
     ClusterPair64& c = cp[p];
     c.tap_d = b->tap_d ? 1 : 0;
     c.pad = b->pad64 + padn * p;
