@@ -221,7 +221,7 @@ void arena_begin(mrb_ctx* ctx, size_t need) {
     ctx->arena = nullptr;
     ctx->arena_cap = 0;
     const size_t cap = std::max<size_t>(need + need / 2, size_t(1) << 20);
-    ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->arena), cap, cudaHostAllocDefault));
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->arena), cap, cudaHostAllocMapped));
     ctx->arena_cap = cap;
   }
   if (!ctx->arena_done) ck(cudaEventCreateWithFlags(&ctx->arena_done, cudaEventDisableTiming));
@@ -230,6 +230,18 @@ void arena_begin(mrb_ctx* ctx, size_t need) {
 template <typename T>
 T* dupload(const T* h, size_t n, cudaStream_t s);
 
+// Zero-copy read of pinned host memory by a kernel: the descriptor uploads
+// of a batch are small, and as DMA copies they would queue behind the bulk
+// image / mesh copies of mrb_register_many on the copy engine.
+__global__ void k_copy_from_host(unsigned char* __restrict__ dst,
+                                 const unsigned char* __restrict__ src, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n / 16;
+       i += size_t(gridDim.x) * blockDim.x)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  const size_t tail = n & ~size_t(15);
+  if (blockIdx.x == 0 && threadIdx.x < n - tail) dst[tail + threadIdx.x] = src[tail + threadIdx.x];
+}
+
 // device copy of h[0..n) through the arena (pageable fallback when full)
 template <typename T>
 T* aupload(mrb_ctx* ctx, const T* h, size_t n) {
@@ -237,8 +249,15 @@ T* aupload(mrb_ctx* ctx, const T* h, size_t n) {
   if (!ctx->arena || at + bytes > ctx->arena_cap) return dupload(h, n, ctx->stream);
   std::memcpy(ctx->arena + at, h, bytes);
   ctx->arena_off = at + bytes;
-  T* d = dalloc<T>(n);
-  if (n) ck(mrb_copy_async(d, ctx->arena + at, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  T* d = dalloc<T>(n);  // 256-byte aligned, as is the arena slice
+  if (n) {
+    unsigned char* src = nullptr;
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&src), ctx->arena + at, 0));
+    const unsigned blocks = unsigned(std::min<size_t>((bytes / 16 + 255) / 256 + 1, 64));
+    k_copy_from_host<<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<unsigned char*>(d), src,
+                                                     bytes);
+    ck(cudaGetLastError());
+  }
   ck(cudaEventRecord(ctx->arena_done, ctx->stream));  // arena slice free after this
   ctx->arena_used = true;
   return d;
