@@ -618,8 +618,19 @@ __global__ void __launch_bounds__(kPixBlock)
   } else if (q < d.W * d.H) {
     const int y = q / d.W, x = q - y * d.W;
     const int4 tv = __ldg(d.tri + ti);
+    // barycentric weights (densefield.py:99-107) in fp64 with one reciprocal
+    // instead of two divisions: within an ulp of the exact-rounding form,
+    // far inside the fp32 path's tolerance (the exact form is bary_rn, used
+    // by the fp64 dense pass and the pixel_map export)
     double w[3];
-    bary_rn(__ldg(d.V + tv.x), __ldg(d.V + tv.y), __ldg(d.V + tv.z), double(x), double(y), w);
+    {
+      const double2 a = __ldg(d.V + tv.x), b = __ldg(d.V + tv.y), c = __ldg(d.V + tv.z);
+      const double px = double(x), py = double(y);
+      const double inv = 1.0 / ((b.x - a.x) * (c.y - a.y) - (c.x - a.x) * (b.y - a.y));
+      w[0] = ((b.x - px) * (c.y - py) - (c.x - px) * (b.y - py)) * inv;
+      w[1] = ((c.x - px) * (a.y - py) - (a.x - px) * (c.y - py)) * inv;
+      w[2] = (1.0 - w[0]) - w[1];
+    }
     const float2 ua = d.u[tv.x], ub = d.u[tv.y], uc = d.u[tv.z];
     // (w * u[T]).sum(axis=2) = (w1 ua + w2 ub) + w3 uc, densefield.py:184-187
     const float rx = float(__dadd_rn(__dadd_rn(__dmul_rn(w[0], double(ua.x)), __dmul_rn(w[1], double(ub.x))),
