@@ -31,6 +31,8 @@ struct ClusterPair64 {
   const int* n_halo;          // [CS]
   const void* img;            // interleaved (Te, Re), H x W: float, or double (tap_d)
   const double2* pad;         // padded (H+2) x (W+2) (Te, Re), exact fp64 ring
+  const float2* img4;         // fp32-exact inputs: the fp32 path's 4 shifted padded copies
+  int pitch, plane;           //   (interior windows only: their ring is rounded)
   double2* u;                 // [n] final displacement, device order
   double* trace;
   int n, chunk, W, H, tap_d;
@@ -76,6 +78,38 @@ __device__ __forceinline__ double2 sample_pad64(const double2* __restrict__ pad,
     for (int i = 1; i < 4; ++i) {
       rt = fma(wx[i], tp[i].x, rt);
       rr = fma(wx[i], tp[i].y, rr);
+    }
+    te = fma(wy[j], rt, te);
+    re = fma(wy[j], rr, re);
+  }
+  return make_double2(te, re);
+}
+
+// fp32-exact inputs: an interior window (no ring tap) reads the fp32 path's
+// aligned shifted copies — 4 x 32-byte rows instead of 16 x 16-byte taps —
+// with the same fp64 weights and accumulation as sample_pad64; a window
+// touching the ring reads the exact fp64 padded image
+__device__ __forceinline__ double2 sample_int64(const ClusterPair64& d, double x, double y) {
+  const double xc = fmin(fmax(x, 0.0), double(d.W) - 1.0);
+  const double yc = fmin(fmax(y, 0.0), double(d.H) - 1.0);
+  const int cx = min(int(xc), d.W - 2);
+  const int cy = min(int(yc), d.H - 2);
+  if (cx < 1 || cx > d.W - 3 || cy < 1 || cy > d.H - 3) return sample_pad64(d.pad, d.W, d.H, x, y);
+  double wx[4], wy[4];
+  cr_weights<double>(xc - double(cx), wx);
+  cr_weights<double>(yc - double(cy), wy);
+  const int s = (4 - (cx & 3)) & 3;
+  const float2* base = d.img4 + size_t(s) * d.plane + size_t(cy) * d.pitch + cx + s;
+  double te = 0.0, re = 0.0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float2 tp[4];
+    ld_row4(base + size_t(j) * d.pitch, tp);
+    double rt = wx[0] * double(tp[0].x), rr = wx[0] * double(tp[0].y);
+#pragma unroll
+    for (int i = 1; i < 4; ++i) {
+      rt = fma(wx[i], double(tp[i].x), rt);
+      rr = fma(wx[i], double(tp[i].y), rr);
     }
     te = fma(wy[j], rt, te);
     re = fma(wy[j], rr, re);
@@ -251,7 +285,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       for (int j = 0; j < NPT; ++j) {
         if (OWN(j)) {
           const double2 V = sm.V[t + j * kClusterThreads];
-          const double2 s = sample_pad64(d.pad, d.W, d.H, V.x + u[j].x, V.y + u[j].y);
+          const double2 s = d.img4 ? sample_int64(d, V.x + u[j].x, V.y + u[j].y)
+                                   : sample_pad64(d.pad, d.W, d.H, V.x + u[j].x, V.y + u[j].y);
           r[j] = s.x - s.y;
           sm.xs[t + j * kClusterThreads] = s.x;
           e2 = fma(r[j], r[j], e2);

@@ -1886,6 +1886,14 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
     else
       k_pad_pair64<float><<<pg, 256, 0, s>>>(static_cast<const ClusterPair64*>(b->c64_pairs));
     ++launches;
+    if (b->img_pad) {  // the fp32 shifted copies for interior windows
+      k_pad_planar4<<<pg, 256, 0, s>>>(reinterpret_cast<const float* const*>(b->src_ptrs),
+                                       reinterpret_cast<const float* const*>(b->src_ptrs +
+                                                                             b->n_pairs),
+                                       b->W, b->H, b->img_pad, b->pad_pitch, b->pad_plane,
+                                       4 * b->pad_plane);
+      ++launches;
+    }
     launch_cluster64(b);
     tm->mark(0);
     ++launches;
@@ -1940,7 +1948,7 @@ int64_t dispatch_enqueue(mrb_batch* b, KernelTimer* tm = nullptr) {
 int64_t launches_per_run(const mrb_batch* b) {
   if (b->grid_mode) return 3 + b->n_pairs;  // pad, one grid loop per pair, dense, msd
   if (b->cluster_cs) return 4 + (b->tail_p0 < b->n_pairs);  // pad, loop(s), dense, msd
-  if (b->c64_cs) return 7;  // interleave, reset, pad, loop, dense, msd, unpermute
+  if (b->c64_cs) return b->img_pad ? 8 : 7;  // interleave, reset, pad(s), loop, dense, msd, unpermute
   return 2 + int64_t(b->cfg.max_iterations) * (2 + b->cfg.smoothing_passes) + 3;
 }
 
@@ -3026,6 +3034,11 @@ void setup_cluster64(mrb_batch* b) {
   std::vector<ClusterPair64> cp(b->n_pairs);
   const size_t padn = size_t(b->W + 2) * (b->H + 2);
   b->pad64 = dalloc<double2>(padn * b->n_pairs);
+  if (!b->tap_d && b->in_dtype == MRB_F32) {  // fp32-exact inputs: the shifted fp32 copies too
+    b->pad_pitch = (b->W + 5 + 3) / 4 * 4;
+    b->pad_plane = size_t(b->H + 2) * b->pad_pitch;
+    b->img_pad = dalloc<float2>(4 * b->pad_plane * b->n_pairs);
+  }
   for (int p = 0; p < b->n_pairs; ++p) {
     HostMesh& h = b->meshes[p]->h;
     const int chunk = int((h.n + best_cs - 1) / best_cs);
@@ -3033,6 +3046,9 @@ void setup_cluster64(mrb_batch* b) {
     ClusterPair64& c = cp[p];
     c.tap_d = b->tap_d ? 1 : 0;
     c.pad = b->pad64 + padn * p;
+    c.img4 = b->img_pad ? b->img_pad + 4 * b->pad_plane * p : nullptr;
+    c.pitch = b->pad_pitch;
+    c.plane = int(b->pad_plane);
     c.V = b->tap_d ? host64[p].V : host32[p].V;
     c.g_self = b->tap_d ? host64[p].g_self : host32[p].g_self;
     c.inv_val = b->tap_d ? host64[p].inv_val : host32[p].inv_val;
