@@ -29,6 +29,9 @@ struct ClusterPair64 {
   const uint32_t* slice_off;  // [CS][slices]
   const uint32_t* halo;       // [CS][halo_stride]: rank << 16 | slot
   const int* n_halo;          // [CS]
+  const uint32_t* send;       // push exchange: [CS][send_stride] slot << 20 | dst << 16 | halo idx
+  const int* n_send;          // [CS]
+  int send_stride;
   const void* img;            // interleaved (Te, Re), H x W: float, or double (tap_d)
   const double2* pad;         // padded (H+2) x (W+2) (Te, Re), exact fp64 ring
   const float2* img4;         // fp32-exact inputs: the fp32 path's 4 shifted padded copies

@@ -27,6 +27,7 @@
 #include "grid.cuh"
 #include "push.cuh"
 #include "cluster64.cuh"
+#include "push64.cuh"
 #include "pixel.cuh"
 #include "kernels.cuh"
 #include "mesh_host.h"
@@ -975,8 +976,18 @@ void ensure_cluster_topos64(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, 
     t.halo = reinterpret_cast<uint32_t*>(slab + th[i].off[3]);
     t.n_halo = reinterpret_cast<int*>(slab + th[i].off[4]);
     t.deg = slab + th[i].off[5];
+    t.send = reinterpret_cast<uint32_t*>(slab + th[i].off[6]);
+    t.n_send = reinterpret_cast<int*>(slab + th[i].off[7]);
+    t.send_stride = th[i].sstride;
     todo[i]->dev->topo[topo64_key(cs, t.chunk)] = t;
   }
+}
+
+// bytes of dynamic shared memory of k_cluster64_push (Push64Smem carve)
+size_t push64_dyn_smem(int topo_stride, int slices, int halo_stride, int send_stride) {
+  const size_t S = size_t(kClusterThreads), X = S + halo_stride;
+  return size_t(topo_stride) * (16 + 2) + S * (16 + 16 + 8) + X * (2 * 16 + 2 * 8) +
+         size_t(send_stride) * 4 + size_t(slices) * 4;
 }
 
 // bytes of dynamic shared memory of k_cluster64 (Cluster64Smem carve)
@@ -1235,6 +1246,7 @@ struct mrb_batch {
   // descent loop in one persistent k_cluster64 launch (c64_cs CTAs per pair)
   int c64_cs = 0;
   size_t c64_smem = 0;
+  bool c64_push = false;  // k_cluster64_push (smoothing_passes <= 1, fits)
   void* c64_pairs = nullptr;  // ClusterPair64[n_pairs]
   double2* pad64 = nullptr;   // padded fp64 images [pair][(H+2) x (W+2)]
   // mrb_register_many: main-shape pairs [lazy_from, planned_end) are planned
@@ -2988,6 +3000,33 @@ int cluster64_occupancy(int CS, size_t smem) {
   return n;
 }
 
+std::string env_exchange() {
+  const char* x = std::getenv("MESHREG_B200_EXCHANGE");
+  return x ? std::string(x) : std::string();
+}
+
+int cluster64_push_occupancy(int CS, size_t smem) {
+  auto kern = k_cluster64_push;
+  if (!raise_smem_limit_of(kern, smem)) return 0;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(unsigned(CS));
+  lc.blockDim = dim3(kClusterThreads);
+  lc.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &lc) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 void setup_cluster64(mrb_batch* b) {
   const char* env = std::getenv("MESHREG_B200_PATH");
   const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
@@ -3057,6 +3096,9 @@ void setup_cluster64(mrb_batch* b) {
     c.slice_off = t.slice_off;
     c.halo = t.halo;
     c.n_halo = t.n_halo;
+    c.send = t.send;
+    c.n_send = t.n_send;
+    c.send_stride = t.send_stride;
     c.img = b->tap_d ? static_cast<const void*>(host64[p].img)
                      : static_cast<const void*>(host32[p].img);
     c.u = b->tap_d ? host64[p].u : host32[p].u;
@@ -3072,9 +3114,24 @@ void setup_cluster64(mrb_batch* b) {
   b->c64_pairs = aupload(b->ctx, cp.data(), cp.size());
   b->c64_cs = best_cs;
   b->c64_smem = best_smem;
+  // push exchange when it fits without losing resident clusters (no cluster
+  // barrier in the loop; the pull kernel measured barrier-bound)
+  if (b->cfg.smoothing_passes <= 1 && env_exchange() != "pull") {
+    size_t ps = 0;
+    bool lists = true;
+    for (HostMesh* h : hm) {
+      const DeviceMesh::Topo& t = h->dev->topo.at(topo64_key(best_cs, int((h->n + best_cs - 1) / best_cs)));
+      lists = lists && t.send_stride > 0;
+      ps = std::max(ps, push64_dyn_smem(t.topo_stride, t.slices, t.halo_stride, t.send_stride));
+    }
+    if (lists && cluster64_push_occupancy(best_cs, ps) >= cluster64_occupancy<1>(best_cs, best_smem)) {
+      b->c64_push = true;
+      b->c64_smem = ps;
+    }
+  }
   if (std::getenv("MESHREG_B200_DEBUG"))
-    std::fprintf(stderr, "meshreg_b200: fp64 cluster %d CTAs x 1 node/thread, %zu B smem\n",
-                 best_cs, best_smem);
+    std::fprintf(stderr, "meshreg_b200: fp64 cluster %d CTAs x 1 node/thread, %zu B smem, %s\n",
+                 best_cs, b->c64_smem, b->c64_push ? "push" : "pull");
 }
 
 void launch_cluster64(mrb_batch* b) {
@@ -3090,8 +3147,9 @@ void launch_cluster64(mrb_batch* b) {
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  ck(cudaLaunchKernelEx(&lc, k_cluster64<1>, static_cast<const ClusterPair64*>(b->c64_pairs),
-                        b->st, int(b->cfg.max_iterations), double(b->cfg.energy_tolerance),
+  ck(cudaLaunchKernelEx(&lc, b->c64_push ? k_cluster64_push : k_cluster64<1>,
+                        static_cast<const ClusterPair64*>(b->c64_pairs), b->st,
+                        int(b->cfg.max_iterations), double(b->cfg.energy_tolerance),
                         double(b->cfg.tau), double(b->cfg.lam), int(b->cfg.smoothing_passes)));
 }
 
@@ -3309,7 +3367,7 @@ int mrb_batch_pair_status(mrb_batch* b, int32_t p, int32_t* iters, double* msd_b
 int64_t mrb_batch_launches_per_run(const mrb_batch* b) { return launches_per_run(b); }
 
 const char* mrb_batch_loop_kernel(const mrb_batch* b) {
-  if (b->c64_cs) return "k_cluster64";
+  if (b->c64_cs) return b->c64_push ? "k_cluster64_push" : "k_cluster64";
   if (!b->cluster_cs) return "k_sample";
   if (b->grid_mode) return b->grid_flags ? "k_grid_flags" : "k_grid_register";
   return b->push_mode ? "k_cluster_push" : "k_cluster_register";

@@ -138,6 +138,12 @@ def test_fp64_cluster_loop_matches_oracle(x255, monkeypatch):
     assert relinf(ux, info["ux"]) < 1e-9 and relinf(uy, info["uy"]) < 1e-9
     assert relinf(rep.energy_trace, info["energy_trace"]) < 1e-10
     assert abs(rep.msd_after / info["msd_after"] - 1) < 1e-10
+    # the pull exchange (cluster barriers) gives bit-identical fields and
+    # energies to the default push exchange; the generic loop agrees to 1e-9
+    monkeypatch.setenv("MESHREG_B200_EXCHANGE", "pull")
+    u3, rep3 = mrb.register(re, te, mrb.TriMesh(V, T), cfg, precision="f64")
+    assert np.array_equal(u3, u) and rep3.energy_trace == rep.energy_trace
+    monkeypatch.delenv("MESHREG_B200_EXCHANGE")
     monkeypatch.setenv("MESHREG_B200_PATH", "generic")
     u2, rep2 = mrb.register(re, te, mrb.TriMesh(V, T), cfg, precision="f64")
     assert relinf(u2, u) < 1e-9
