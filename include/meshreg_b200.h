@@ -199,7 +199,12 @@ int mrb_batch_kernel_times(mrb_batch* batch, double* out);
  * pinned for overlap).  Outputs (host, any may be NULL): u (concatenated
  * n_i*2 f64), ux/uy/warped (n_pairs*H*W in out_dtype), per-pair
  * iterations_run, MSDs, trace (n_pairs*max_iterations), MRB_* codes and
- * messages (n_pairs*msg_len).  Returns the first pair error (or MRB_OK). */
+ * messages (n_pairs*msg_len).  Returns the first pair error (or MRB_OK).
+ * Every pair's code is written: a pair the call never reached (an early
+ * failure — invalid configuration, a mesh that does not cover the image, a
+ * CUDA error) carries the call's own code and mrb_last_error message, never
+ * a stale MRB_OK.  When one mesh fails the coverage check the call returns
+ * MRB_E_COVERAGE for the whole batch (the caller may retry pair by pair). */
 int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int32_t width,
                       int32_t height, int32_t img_dtype, const void* reference, const void* tmpl,
                       const mrb_config* cfg, int32_t chunk_pairs, int32_t out_dtype, double* u,
