@@ -104,6 +104,29 @@ int mrb_mesh_build_many(int32_t count, const int64_t* n_vertices,
                         const int64_t* const* triangles, mrb_mesh** out,
                         int32_t* first_bad, char* err, int32_t err_len);
 int mrb_mesh_destroy(mrb_mesh* mesh);
+/* Deferred mesh handles (no reference counterpart: the reference builds a
+ * TriMesh per mesh on the host, mesh.py:58-123).  Only the checks that need no
+ * connectivity run here (mesh.py:61-86: finite coordinates, index range,
+ * repeated indices, degenerate area; same messages), plus the CCW
+ * reorientation.  The connectivity, geometry, node order, fused operator and
+ * fast-path topology are built on the GPU by the first mrb_register_many that
+ * runs the handle on the fp32 cluster fast path (bit-identical to
+ * mrb_mesh_build's); every other consumer (exports, single operations,
+ * mrb_batch_create, other paths) runs the host build first, and a mesh the
+ * reference would reject (non-manifold edge, valence < 2) fails there with the
+ * reference's message.  All or nothing, like mrb_mesh_build_many. */
+int mrb_mesh_create_many(int32_t count, const int64_t* n_vertices,
+                         const double* const* vertices, const int64_t* n_triangles,
+                         const int64_t* const* triangles, mrb_mesh** out,
+                         int32_t* first_bad, char* err, int32_t err_len);
+/* Test hook: builds a deferred mesh and its (cs, npt) cluster topology on the
+ * GPU and compares them with the host build.  out[0..9] = mismatching
+ * elements of: device-order vertices, triangles, node order, fp32 G self
+ * terms, fp32 1/valence, (max valence, edge count), one-ring CSR row
+ * pointers, one-ring CSR indices, fp64 G ring terms, topology bytes (-1 if
+ * the layout sizes differ). */
+int mrb_mesh_device_check(mrb_ctx* ctx, mrb_mesh* mesh, int32_t cluster_size,
+                          int32_t nodes_per_thread, int64_t* out);
 /* counts[0..5] = n_vertices, n_triangles, n_edges, nnz(L), nnz(grad), nnz(avg) */
 int mrb_mesh_counts(const mrb_mesh* mesh, int64_t* counts);
 /* oriented triangles (m*3), edges (e*2), valence (n), boundary (n bytes),

@@ -50,6 +50,9 @@ _SIGS = {
     "mrb_mesh_build": (C.c_int, [_i64, _vp, _i64, _vp, C.POINTER(_vp), C.c_char_p, _i32]),
     "mrb_mesh_build_many": (C.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i32), C.c_char_p,
                                       _i32]),
+    "mrb_mesh_create_many": (C.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i32), C.c_char_p,
+                                       _i32]),
+    "mrb_mesh_device_check": (C.c_int, [_vp, _vp, _i32, _i32, _vp]),
     "mrb_mesh_destroy": (C.c_int, [_vp]),
     "mrb_mesh_counts": (C.c_int, [_vp, _vp]),
     "mrb_mesh_export_connectivity": (C.c_int, [_vp] + [_vp] * 8),

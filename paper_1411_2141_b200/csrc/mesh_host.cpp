@@ -14,7 +14,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <numeric>
+#ifdef __SSE2__
+#include <immintrin.h>
+#endif
 
 namespace mrb {
 
@@ -60,43 +64,130 @@ void barycentric(const double* a, const double* b, const double* c, double px, d
   w[2] = 1.0 - w1 - w2;
 }
 
-std::string build_mesh(int64_t n, const double* Vin, int64_t m, const int64_t* Tin,
-                       HostMesh& M) {
-  // ---- validation, mesh.py:61-78 (shape checks happen in the binding) ----
+namespace {
+
+// mesh.py:61-86: validation that needs no connectivity (shape checks happen
+// in the binding) and the CCW reorientation into Tout (rows [0, 2, 1] where
+// the signed area is negative)
+// Deferred meshes are written once here and then only read by the GPU's DMA:
+// non-temporal stores keep them out of the CPU caches (the upload then reads
+// DRAM instead of snooping freshly written cache lines)
+inline void store_nt(double* p, double v) {
+#ifdef __SSE2__
+  _mm_stream_si64(reinterpret_cast<long long*>(p), __builtin_bit_cast(long long, v));
+#else
+  *p = v;
+#endif
+}
+inline void store_nt(int32_t* p, int32_t v) {
+#ifdef __SSE2__
+  _mm_stream_si32(reinterpret_cast<int*>(p), v);
+#else
+  *p = v;
+#endif
+}
+inline void store_nt(int64_t* p, int64_t v) { *p = v; }  // host build: stays cached
+inline void store_fence() {
+#ifdef __SSE2__
+  _mm_sfence();
+#endif
+}
+
+template <typename TI>
+std::string validate_core(int64_t n, const double* Vin, int64_t m, const int64_t* Tin, TI* Tout,
+                          double* Vout = nullptr, int32_t* max_inc = nullptr) {
+  // one pass over V (copied to Vout if given) and one over T; the errors are
+  // reported in the reference's order whatever triangle trips them
   if (m < 1) return "triangles must be (m, 3) with m >= 1, got (0, 3)";
-  for (int64_t i = 0; i < 2 * n; ++i)
-    if (!std::isfinite(Vin[i])) return "vertex coordinates must be finite";
-  int64_t tmin = Tin[0], tmax = Tin[0];
-  for (int64_t k = 0; k < 3 * m; ++k) {
-    tmin = std::min(tmin, Tin[k]);
-    tmax = std::max(tmax, Tin[k]);
+  bool finite = true;
+  for (int64_t i = 0; i < 2 * n; ++i) {
+    finite = finite && std::isfinite(Vin[i]);
+    if (Vout) store_nt(Vout + i, Vin[i]);
   }
-  if (tmin < 0 || tmax >= n) return "triangle index out of range";
+  if (!finite) return "vertex coordinates must be finite";
+  std::vector<int32_t> inc(max_inc ? static_cast<size_t>(n) : 0, 0);
+  bool range = false, repeated = false, bad = false;
+  int64_t worst = 0;
+  double worst_abs = INFINITY;
+  int32_t mx = 0;
   for (int64_t t = 0; t < m; ++t) {
     const int64_t* r = Tin + 3 * t;
-    if (r[0] == r[1] || r[1] == r[2] || r[0] == r[2]) return "triangle with repeated vertex index";
+    if (uint64_t(r[0]) >= uint64_t(n) || uint64_t(r[1]) >= uint64_t(n) ||
+        uint64_t(r[2]) >= uint64_t(n)) {
+      range = true;
+      continue;
+    }
+    repeated = repeated || r[0] == r[1] || r[1] == r[2] || r[0] == r[2];
+    const double a2 = area2(Vin, r[0], r[1], r[2]);
+    const double ab = std::fabs(a2);
+    if (ab <= 2.0 * kDegenerateArea) bad = true;
+    if (ab < worst_abs) {  // np.argmin: first minimum
+      worst_abs = ab;
+      worst = t;
+    }
+    const bool flip = a2 < 0;  // [0, 2, 1]
+    store_nt(Tout + 3 * t, TI(r[0]));
+    store_nt(Tout + 3 * t + 1, TI(flip ? r[2] : r[1]));
+    store_nt(Tout + 3 * t + 2, TI(flip ? r[1] : r[2]));
+    if (max_inc)
+      for (int c = 0; c < 3; ++c) mx = std::max(mx, ++inc[size_t(r[c])]);
   }
+  store_fence();
+  if (range) return "triangle index out of range";
+  if (repeated) return "triangle with repeated vertex index";
+  if (bad)
+    return "degenerate triangle " + std::to_string(worst) + " (area " + fmt_g(worst_abs / 2.0) +
+           ")";
+  if (max_inc) *max_inc = mx;
+  return "";
+}
+
+// validate_core into the host mesh (M.n, M.m, M.V, M.T)
+std::string validate_orient(int64_t n, const double* Vin, int64_t m, const int64_t* Tin,
+                            HostMesh& M) {
+  M.T.resize(size_t(std::max<int64_t>(m, 0)) * 3);
+  const std::string e = validate_core(n, Vin, m, Tin, M.T.data());
+  if (!e.empty()) return e;
   M.n = n;
   M.m = m;
   M.V.assign(Vin, Vin + 2 * n);
-  M.T.assign(Tin, Tin + 3 * m);
+  return "";
+}
+
+}  // namespace
+
+std::string create_mesh(int64_t n, const double* Vin, int64_t m, const int64_t* Tin,
+                        double* Vout, int32_t* Tout, HostMesh& M) {
+  if (n >= (int64_t(1) << 31)) return "mesh too large for the device setup (n >= 2^31)";
+  int32_t mx = 0;
+  const std::string e = validate_core(n, Vin, m, Tin, Tout, Vout, &mx);
+  if (!e.empty()) return e;
+  M.n = n;
+  M.m = m;
+  M.dV = Vout;
+  M.dT = Tout;
+  M.deferred = true;
+  // fast-path eligibility estimate (valence = incident triangles, + 1 on the
+  // boundary); the device build reports the exact value
+  M.max_deg = mx + 1;
+  return "";
+}
+
+const std::string& ensure_host(HostMesh& M) {
+  std::call_once(M.host_once, [&M] {
+    if (!M.deferred) return;
+    const std::vector<int64_t> T(M.dT, M.dT + 3 * M.m);  // already oriented
+    M.host_err = build_mesh(M.n, M.dV, M.m, T.data(), M);
+    if (M.host_err.empty()) M.deferred = false;
+  });
+  return M.host_err;
+}
+
+std::string build_mesh(int64_t n, const double* Vin, int64_t m, const int64_t* Tin,
+                       HostMesh& M) {
   {
-    int64_t worst = 0;
-    double worst_abs = INFINITY;
-    bool bad = false;
-    for (int64_t t = 0; t < m; ++t) {
-      const double a2 = area2(M.V.data(), M.T[3 * t], M.T[3 * t + 1], M.T[3 * t + 2]);
-      const double ab = std::fabs(a2);
-      if (ab <= 2.0 * kDegenerateArea) bad = true;
-      if (ab < worst_abs) {  // np.argmin: first minimum
-        worst_abs = ab;
-        worst = t;
-      }
-      if (a2 < 0) std::swap(M.T[3 * t + 1], M.T[3 * t + 2]);  // [0, 2, 1]
-    }
-    if (bad)
-      return "degenerate triangle " + std::to_string(worst) + " (area " +
-             fmt_g(worst_abs / 2.0) + ")";
+    const std::string e = validate_orient(n, Vin, m, Tin, M);
+    if (!e.empty()) return e;
   }
 
   // ---- connectivity, mesh.py:91-123 ----

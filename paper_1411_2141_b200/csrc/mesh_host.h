@@ -46,12 +46,33 @@ struct HostMesh {
   std::vector<int32_t> Tn;     // m*4   triangles in new ids (+pad)
   int32_t max_deg = 0;         // largest one-ring (fast-path eligibility)
 
+  // Deferred handles (mrb_mesh_create_many): only V, T (oriented), n, m and
+  // an estimate of max_deg are set at creation; the rest is built on the GPU
+  // (meshbuild.cuh) or, for any host consumer, by ensure_host.
+  bool deferred = false;
+  const double* dV = nullptr;   // deferred storage: V (n*2) and the oriented
+  const int32_t* dT = nullptr;  // T (m*3) in the creation's block (pinned)
+  std::shared_ptr<unsigned char> def_hold;
+  std::once_flag host_once;
+  std::string host_err;        // ensure_host's build_mesh message ("" = ok)
+
   std::unique_ptr<DeviceMesh> dev;  // lazily created per device
   ~HostMesh();
 };
 
 // Build + validate; returns "" on success, else the reference's ValueError text.
 std::string build_mesh(int64_t n, const double* V, int64_t m, const int64_t* T, HostMesh& out);
+
+// Validation that needs no connectivity (mesh.py:61-86: shapes, finite
+// coordinates, index range, repeated indices, degenerate area) and the CCW
+// orientation; writes V and the oriented T into Vout / Tout (the creation's
+// block, the device build's upload source) and marks the mesh deferred.
+// Returns "" or the reference's ValueError text.
+std::string create_mesh(int64_t n, const double* V, int64_t m, const int64_t* T, double* Vout,
+                        int32_t* Tout, HostMesh& out);
+
+// Full host build of a deferred mesh (no-op otherwise); returns its error.
+const std::string& ensure_host(HostMesh& M);
 
 // The reference's CSR operators L, Gx, Gy, avg (mesh.py:199-213, 254-265):
 // only the export entry points need them, so they are built on first use.

@@ -30,7 +30,10 @@
 #include "push64.cuh"
 #include "pixel.cuh"
 #include "kernels.cuh"
+#include "meshbuild.cuh"
 #include "mesh_host.h"
+
+#include <cub/device/device_radix_sort.cuh>
 
 using namespace mrb;
 
@@ -57,7 +60,26 @@ struct mrb_ctx {
   size_t arena_cap = 0, arena_off = 0;
   cudaEvent_t arena_done = nullptr;
   bool arena_used = false;
+  // device-side mesh setup (meshbuild.cuh): small pinned scratch for job
+  // descriptors and stats, and the builds whose stats are not yet checked
+  void* small_pin = nullptr;
+  size_t small_cap = 0;
+  cudaEvent_t small_ev = nullptr;
+  std::vector<HostMesh*> build_pending;
+  int* build_stats = nullptr;  // pinned, [mesh][4]
+  size_t build_stats_cap = 0;
+  cudaEvent_t build_ev = nullptr;
+  cudaEvent_t build_in = nullptr;  // V / T of the pending build uploaded
+  // Large per-call buffers of mrb_register_many kept on the context (its
+  // batches on one context run in turn): a fresh stream-ordered allocation
+  // of a few hundred MB maps new pool memory, ~1 ms of host time each.
+  struct Kept {
+    void* p = nullptr;
+    size_t cap = 0;
+  } kept[5];  // see KeptSlot
 };
+
+enum KeptSlot { kKeptPad, kKeptDense, kKeptState, kKeptImages, kKeptVT };
 
 struct mrb_mesh {
   HostMesh h;
@@ -104,6 +126,12 @@ struct DeviceMesh {
   double2* g_self_d = nullptr;
   double2* g_nb_d = nullptr;
   double* inv_val_d = nullptr;
+  // device-built meshes (meshbuild.cuh): the one-ring CSR in device ids and
+  // the fp64 fused operator, kept for topology builds of any cluster shape
+  const int* b_nb_ptr = nullptr;
+  const int* b_nb_idx = nullptr;
+  const double2* b_g_nb = nullptr;
+  std::shared_ptr<unsigned char> build_hold;
   std::map<std::pair<int, int>, int*> pixel_maps;
   // owners of pixel maps that are slices of a batch's shared slab
   std::map<std::pair<int, int>, std::shared_ptr<unsigned char>> pixel_map_hold;
@@ -137,6 +165,7 @@ struct DeviceMesh {
     else
       dev_free(slab64, stream);
     dev_free(slab_ring, stream);
+    build_hold.reset();
     for (auto& kv : pixel_maps)
       if (!pixel_map_hold.count(kv.first)) dev_free(kv.second, stream);
     pixel_map_hold.clear();
@@ -158,13 +187,17 @@ namespace {
 
 const char* kVersion = "meshreg_b200 0.1.0 (sm_100a)";
 
+inline size_t al256(size_t b) { return (b + 255) / 256 * 256; }
+
 struct CudaError {
   cudaError_t e;
+  int line = 0;  // source line of the failing call (reported under MESHREG_B200_DEBUG)
 };
 
-inline void ck(cudaError_t e) {
-  if (e != cudaSuccess) throw CudaError{e};
+inline void ck_at(cudaError_t e, int line) {
+  if (e != cudaSuccess) throw CudaError{e, line};
 }
+#define ck(e) ck_at((e), __LINE__)
 
 // host<->device bytes moved by the library (reported by the benchmark)
 std::atomic<long long> g_h2d_bytes{0}, g_d2h_bytes{0};
@@ -201,6 +234,18 @@ T* dalloc(size_t n) {
   else
     ck(cudaMalloc(&p, n * sizeof(T)));
   return static_cast<T*>(p);
+}
+
+// A kept buffer of the context (grows; stream-ordered on ctx->stream, or
+// the AllocScope's stream)
+void* kept_buffer(mrb_ctx* ctx, int slot, size_t bytes) {
+  mrb_ctx::Kept& k = ctx->kept[slot];
+  if (k.cap < bytes) {
+    dev_free(k.p, ctx->stream);
+    k.p = dalloc<unsigned char>(bytes);
+    k.cap = bytes;
+  }
+  return k.p;
 }
 
 // One device allocation shared by the meshes of an upload (freed, stream
@@ -299,7 +344,10 @@ int fail(mrb_ctx* ctx, int code, const std::string& msg) {
   return code;
 }
 
-int cuda_fail(mrb_ctx* ctx, cudaError_t e) {
+int cuda_fail(mrb_ctx* ctx, cudaError_t e, int line = 0) {
+  if (line && std::getenv("MESHREG_B200_DEBUG"))
+    std::fprintf(stderr, "meshreg_b200: CUDA error %s at meshreg_b200.cu:%d\n",
+                 cudaGetErrorString(e), line);
   return fail(ctx, MRB_E_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
 }
 
@@ -473,6 +521,7 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, bo
         std::find(todo.begin(), todo.end(), h) == todo.end())
       todo.push_back(h);
   if (todo.empty()) return;
+  parallel_for(todo.size(), [&](size_t i) { ensure_host(*todo[i]); });
   AllocScope scope(ctx->stream);
   const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
   auto t0 = std::chrono::steady_clock::now();
@@ -563,6 +612,7 @@ void ensure_device_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, bo
 void ensure_device_mesh_ring(mrb_ctx* ctx, HostMesh& h) {
   DeviceMesh& d = *h.dev;
   if (d.nb_ptr) return;
+  ensure_host(h);
   AllocScope scope(ctx->stream);
   const size_t n = size_t(h.n), ne2 = h.nb_idx.size();
   const size_t o1 = ((n + 1) * 4 + 255) / 256 * 256, o2 = o1 + (ne2 * 4 + 255) / 256 * 256;
@@ -586,6 +636,7 @@ void ensure_device_mesh(mrb_ctx* ctx, HostMesh& h) {
 // fp64 operator arrays, uploaded on first use by an fp64 batch / single op
 void ensure_device_mesh_f64(mrb_ctx* ctx, HostMesh& h) {
   ensure_device_mesh(ctx, h);  // includes the one-ring arrays
+  ensure_host(h);
   DeviceMesh& d = *h.dev;
   if (d.slab64 && d.g_nb_d) return;
   if (d.slab64_hold) d.slab64_hold.reset();  // the self-term-only slice
@@ -612,6 +663,7 @@ void ensure_device_meshes_f64_self(mrb_ctx* ctx, const std::vector<HostMesh*>& m
     if (!h->dev->g_self_d && std::find(todo.begin(), todo.end(), h) == todo.end())
       todo.push_back(h);
   if (todo.empty()) return;
+  parallel_for(todo.size(), [&](size_t i) { ensure_host(*todo[i]); });
   std::vector<size_t> base(todo.size());
   size_t total = 0;
   for (size_t i = 0; i < todo.size(); ++i) {
@@ -673,6 +725,7 @@ struct TopoHost {
 
 // gbytes: bytes per SELL coefficient entry (float2 8, double2 16 for k_cluster64)
 TopoHost plan_topo(const HostMesh& h, int cs, int chunk, int npt, int gbytes = 8) {
+  ensure_host(const_cast<HostMesh&>(h));  // deferred handles: host arrays first
   const int n = int(h.n);
   const int SLOTS = kClusterThreads * npt;
   TopoHost t;
@@ -820,10 +873,448 @@ DeviceMesh::Topo& install_topo(HostMesh& h, int npt, const TopoHost& th,
   return h.dev->topo[topo_key(th.cs, th.chunk, npt)] = t;
 }
 
+// ---- device-side mesh setup (deferred handles, meshbuild.cuh) --------------
+//
+// Deferred handles (mrb_mesh_create_many) carry only V and the oriented T.
+// device_build_meshes stages them through pinned memory, copies them on the
+// given stream and runs the connectivity / geometry / node-order / fused
+// operator build on ctx->stream; device_cluster_topos plans and writes the
+// fast-path topology of any cluster shape on the GPU.  Both produce the bytes
+// the host build (build_mesh, plan_topo + write_topo) produces.
+
+// Process-wide cache of host blocks for deferred mesh handles: pinned when
+// the driver allows it (else plain memory, e.g. without a GPU), recycled when
+// the last mesh of a creation is destroyed.
+struct BlockCache {
+  std::mutex mu;
+  std::multimap<size_t, std::pair<void*, bool>> free;  // size -> (ptr, pinned)
+  size_t cached = 0;
+  static BlockCache& get() {
+    static BlockCache* c = new BlockCache();
+    return *c;
+  }
+};
+
+std::shared_ptr<unsigned char> pinned_block(size_t bytes) {
+  BlockCache& c = BlockCache::get();
+  void* p = nullptr;
+  bool pinned = false;
+  size_t size = bytes;
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.free.lower_bound(bytes);
+    if (it != c.free.end() && it->first <= 2 * bytes) {
+      size = it->first;
+      p = it->second.first;
+      pinned = it->second.second;
+      c.cached -= size;
+      c.free.erase(it);
+    }
+  }
+  if (!p) {
+    size = al256(bytes);
+    pinned = cudaHostAlloc(&p, size, cudaHostAllocDefault) == cudaSuccess;
+    if (!pinned) {
+      cudaGetLastError();  // no device: plain host memory
+      p = std::malloc(size);
+      if (!p) throw std::bad_alloc();
+    }
+  }
+  return std::shared_ptr<unsigned char>(static_cast<unsigned char*>(p), [size, pinned](unsigned char* q) {
+    BlockCache& cc = BlockCache::get();
+    std::lock_guard<std::mutex> lk(cc.mu);
+    if (cc.cached + size <= (size_t(1) << 30)) {
+      cc.free.emplace(size, std::make_pair(static_cast<void*>(q), pinned));
+      cc.cached += size;
+    } else if (pinned) {
+      cudaFreeHost(q);
+    } else {
+      std::free(q);
+    }
+  });
+}
+
+// MESHREG_B200_DEBUG: host time since the previous call (what: label)
+void host_tick(const char* what) {
+  static const bool on = std::getenv("MESHREG_B200_DEBUG") != nullptr;
+  if (!on) return;
+  static thread_local auto last = std::chrono::steady_clock::now();
+  const auto now = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "meshreg_b200:     host %-28s %8.3f ms\n", what,
+               std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
+}
+
+// pinned scratch for descriptors and stats (the previous use must be done)
+unsigned char* small_pinned(mrb_ctx* ctx, size_t bytes) {
+  if (ctx->small_ev) ck(cudaEventSynchronize(ctx->small_ev));
+  if (bytes > ctx->small_cap) {
+    if (ctx->small_pin) cudaFreeHost(ctx->small_pin);
+    ctx->small_pin = nullptr;
+    ctx->small_cap = 0;
+    const size_t cap = std::max<size_t>(2 * bytes, size_t(1) << 16);
+    ck(cudaHostAlloc(&ctx->small_pin, cap, cudaHostAllocMapped));
+    ctx->small_cap = cap;
+  }
+  if (!ctx->small_ev) ck(cudaEventCreateWithFlags(&ctx->small_ev, cudaEventDisableTiming));
+  return static_cast<unsigned char*>(ctx->small_pin);
+}
+
+// device copy of `bytes` of mapped pinned memory by a kernel: as a DMA copy a
+// descriptor upload would queue behind the bulk image copies on the engine
+void upload_zero_copy(void* dst, const unsigned char* pinned, size_t bytes, cudaStream_t s) {
+  count_copy(bytes, cudaMemcpyHostToDevice);
+  unsigned char* src = nullptr;
+  ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&src), const_cast<unsigned char*>(pinned),
+                              0));
+  const unsigned blocks = unsigned(std::min<size_t>((bytes / 16 + 255) / 256 + 1, 64));
+  k_copy_from_host<<<blocks, 256, 0, s>>>(static_cast<unsigned char*>(dst), src, bytes);
+  ck(cudaGetLastError());
+}
+
+// a deferred mesh the device build takes (cluster-sized, not yet on a device)
+bool device_buildable(const HostMesh& h) {
+  return h.deferred && h.dV && !h.dev && h.n >= 3 && h.n <= 16 * 2 * kClusterThreads;
+}
+
+void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, cudaStream_t copy) {
+  if (todo.empty()) return;
+  const size_t K = todo.size();
+  // inputs: V (double2) and T (int3) per mesh, one pinned stage, one copy
+  std::vector<size_t> in_off(K), out_off(K), b_off(K), key_off(K);
+  size_t in_tot = 0, out_tot = 0, b_tot = 0, keys = 0;
+  for (size_t i = 0; i < K; ++i) {
+    const size_t n = size_t(todo[i]->n), m = size_t(todo[i]->m);
+    in_off[i] = in_tot;
+    in_tot += al256(n * 16) + al256(m * 12);
+    out_off[i] = out_tot;  // DeviceMesh slab: V, tri, perm, g_self_f, inv_val_f
+    out_tot += al256(n * 16) + al256(m * 16) + al256(n * 4) + al256(n * 8) + al256(n * 4);
+    b_off[i] = b_tot;  // build slab (kept: nb_ptr, nb_idx, g_nb)
+    const size_t e2 = 3 * m + n;  // one-ring entries of a manifold mesh (2e <= 3m + n)
+    b_tot += al256(m * 8) + al256(m * 48) + 3 * al256(n * 4) + 2 * al256((n + 1) * 4) +
+             al256(3 * m * 4) + 2 * al256(e2 * 4) + al256(n * 8) + al256((n + 1) * 4) +
+             al256(e2 * 16);
+    key_off[i] = keys;
+    keys += n;
+  }
+  // V / T straight from the creation blocks (same layout): one copy per run
+  // of meshes adjacent in their block
+  unsigned char* din = nullptr;
+  {
+    AllocScope scope(copy);
+    if (ctx->kept[kKeptVT].cap >= in_tot && ctx->build_ev)
+      ck(cudaStreamWaitEvent(copy, ctx->build_ev, 0));  // the previous build read it
+    din = static_cast<unsigned char*>(kept_buffer(ctx, kKeptVT, in_tot));
+    dev_mark(copy, "mesh V/T upload start");
+    {
+      cudaPointerAttributes pa{};
+      if (std::getenv("MESHREG_B200_DEBUG") && cudaPointerGetAttributes(&pa, todo[0]->dV) == cudaSuccess)
+        std::fprintf(stderr, "meshreg_b200:   V/T source memory type %d (host pinned = %d)\n",
+                     int(pa.type), int(cudaMemoryTypeHost));
+    }
+    auto region = [&](size_t i) { return (i + 1 < K ? in_off[i + 1] : in_tot) - in_off[i]; };
+    for (size_t i = 0; i < K;) {
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(todo[i]->dV);
+      size_t j = i + 1, bytes = region(i);
+      while (j < K && reinterpret_cast<const unsigned char*>(todo[j]->dV) == src + bytes &&
+             todo[j]->def_hold == todo[i]->def_hold)
+        bytes += region(j++);
+      ck(mrb_copy_async(din + in_off[i], src, bytes, cudaMemcpyHostToDevice, copy));
+      if (std::getenv("MESHREG_B200_DEBUG"))
+        std::fprintf(stderr, "meshreg_b200:   V/T copy of meshes [%zu, %zu): %.1f MB\n", i, j,
+                     bytes / 1e6);
+      i = j;
+    }
+    if (!ctx->build_in) ck(cudaEventCreateWithFlags(&ctx->build_in, cudaEventDisableTiming));
+    ck(cudaEventRecord(ctx->build_in, copy));
+    dev_mark(copy, "mesh V/T upload done");
+  }
+  cudaStream_t s = ctx->stream;
+  ck(cudaStreamWaitEvent(s, ctx->build_in, 0));
+  AllocScope scope(s);
+  const std::shared_ptr<unsigned char> out = shared_slab(out_tot, s);
+  const std::shared_ptr<unsigned char> bld = shared_slab(b_tot + al256(K * 16), s);
+  int* dstats = reinterpret_cast<int*>(bld.get() + b_tot);
+  unsigned long long* kin = dalloc<unsigned long long>(2 * keys);
+  int* vin = dalloc<int>(2 * keys);
+  std::vector<BuildJob> jobs(K);
+  for (size_t i = 0; i < K; ++i) {
+    HostMesh& h = *todo[i];
+    const size_t n = size_t(h.n), m = size_t(h.m);
+    BuildJob& J = jobs[i];
+    J.n = int(n);
+    J.m = int(m);
+    J.mesh = int(i);
+    unsigned char* p = din + in_off[i];
+    J.V = reinterpret_cast<const double2*>(p);
+    J.T = reinterpret_cast<const int*>(p + al256(n * 16));
+    unsigned char* b = bld.get() + b_off[i];
+    auto take = [&](size_t bytes) {
+      unsigned char* q = b;
+      b += al256(bytes);
+      return q;
+    };
+    J.areas = reinterpret_cast<double*>(take(m * 8));
+    J.coeffs = reinterpret_cast<double*>(take(m * 48));
+    J.cnt = reinterpret_cast<int*>(take(n * 4));
+    J.valence = reinterpret_cast<int*>(take(n * 4));
+    J.iperm = reinterpret_cast<int*>(take(n * 4));
+    J.inc_ptr = reinterpret_cast<int*>(take((n + 1) * 4));
+    J.ring_ptr = reinterpret_cast<int*>(take((n + 1) * 4));
+    J.inc_idx = reinterpret_cast<int*>(take(3 * m * 4));
+    J.ring_cap = int(3 * m + n);
+    J.ring_idx = reinterpret_cast<int*>(take(size_t(J.ring_cap) * 4));
+    J.nb_idx = reinterpret_cast<int*>(take(size_t(J.ring_cap) * 4));
+    J.varea = reinterpret_cast<double*>(take(n * 8));
+    J.nb_ptr = reinterpret_cast<int*>(take((n + 1) * 4));
+    J.g_nb = reinterpret_cast<double2*>(take(size_t(J.ring_cap) * 16));
+    J.key = kin + key_off[i];
+    J.val = vin + key_off[i];
+    J.sorted = vin + keys + key_off[i];
+    unsigned char* o = out.get() + out_off[i];
+    J.Vn = reinterpret_cast<double2*>(o);
+    J.tri = reinterpret_cast<int4*>(o + al256(n * 16));
+    J.perm = reinterpret_cast<int*>(o + al256(n * 16) + al256(m * 16));
+    J.g_self_f = reinterpret_cast<float2*>(o + al256(n * 16) + al256(m * 16) + al256(n * 4));
+    J.inv_val_f = reinterpret_cast<float*>(o + al256(n * 16) + al256(m * 16) + al256(n * 4) +
+                                           al256(n * 8));
+    J.stats = dstats + 4 * i;
+  }
+  unsigned char* pin = small_pinned(ctx, K * sizeof(BuildJob));
+  std::memcpy(pin, jobs.data(), K * sizeof(BuildJob));
+  BuildJob* djobs = dalloc<BuildJob>(K);
+  upload_zero_copy(djobs, pin, K * sizeof(BuildJob), s);
+  ck(cudaEventRecord(ctx->small_ev, s));
+  ck(cudaMemsetAsync(dstats, 0, K * 16, s));
+  k_mesh_build_a<<<unsigned(K * kBuildCluster), kBuildThreads, 0, s>>>(djobs);
+  dev_mark(s, "  build pass A done");
+  // the node order: a stable sort of (mesh << 32 | Morton key) = the host's
+  // std::stable_sort of each mesh's keys
+  int end_bit = 32;
+  while ((size_t(1) << (end_bit - 32)) < K) ++end_bit;
+  size_t temp = 0;
+  ck(cub::DeviceRadixSort::SortPairs(nullptr, temp, kin, kin + keys, vin, vin + keys, int(keys),
+                                     0, end_bit, s));
+  void* dtemp = dalloc<unsigned char>(temp);
+  ck(cub::DeviceRadixSort::SortPairs(dtemp, temp, kin, kin + keys, vin, vin + keys, int(keys), 0,
+                                     end_bit, s));
+  dev_mark(s, "  node order sorted");
+  k_mesh_build_b<<<unsigned(K * kBuildCluster), kBuildThreads, 0, s>>>(djobs);
+  ck(cudaGetLastError());
+  dev_free(dtemp, s);
+  dev_free(kin, s);
+  dev_free(vin, s);
+  dev_free(djobs, s);
+  if (ctx->build_stats_cap < K) {
+    if (ctx->build_stats) cudaFreeHost(ctx->build_stats);
+    ctx->build_stats = nullptr;
+    ctx->build_stats_cap = 0;
+    const size_t cap = std::max<size_t>(K, 256);
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->build_stats), cap * 16, cudaHostAllocDefault));
+    ctx->build_stats_cap = cap;
+  }
+  ck(mrb_copy_async(ctx->build_stats, dstats, K * 16, cudaMemcpyDeviceToHost, s));
+  if (!ctx->build_ev) ck(cudaEventCreateWithFlags(&ctx->build_ev, cudaEventDisableTiming));
+  ck(cudaEventRecord(ctx->build_ev, s));
+  dev_mark(s, "mesh build done");
+  for (size_t i = 0; i < K; ++i) {
+    HostMesh& h = *todo[i];
+    const BuildJob& J = jobs[i];
+    h.dev.reset(new DeviceMesh());
+    DeviceMesh& d = *h.dev;
+    d.device = ctx->device;
+    d.stream = s;
+    d.slab = out.get() + out_off[i];
+    d.slab_hold = out;
+    d.V = J.Vn;
+    d.tri = J.tri;
+    d.perm = J.perm;
+    d.g_self_f = J.g_self_f;
+    d.inv_val_f = J.inv_val_f;
+    d.max_deg = h.max_deg;
+    d.b_nb_ptr = J.nb_ptr;
+    d.b_nb_idx = J.nb_idx;
+    d.b_g_nb = J.g_nb;
+    d.build_hold = bld;
+  }
+  ctx->build_pending = todo;
+}
+
+// Check the pending device builds (waits for them): exact max_deg and edge
+// counts; a mesh the build flagged loses its device arrays and gets the host
+// build.  Returns "" or the first failing mesh's ValueError text.
+std::string device_build_finish(mrb_ctx* ctx) {
+  if (ctx->build_pending.empty()) return "";
+  ck(cudaEventSynchronize(ctx->build_ev));
+  std::vector<HostMesh*> todo;
+  todo.swap(ctx->build_pending);
+  std::string err;
+  for (size_t i = 0; i < todo.size(); ++i) {
+    HostMesh& h = *todo[i];
+    const int* st = ctx->build_stats + 4 * i;
+    if (st[0] == 0) {
+      h.max_deg = st[1];
+      h.ne = st[2] / 2;
+      if (h.dev) h.dev->max_deg = st[1];
+      continue;
+    }
+    h.dev.reset();  // stream-ordered frees
+    const std::string& e = ensure_host(h);
+    if (!e.empty() && err.empty()) err = e;
+  }
+  return err;
+}
+
+// Fast-path topologies of device-built meshes for the requested (mesh,
+// cluster size, nodes/thread) shapes, planned and written on stream s
+// (k_topo_count, one sync for the sizes, k_topo_write, k_topo_send).
+// Returns false, installing nothing, when a mesh needs the host planner.
+bool device_cluster_topos(mrb_ctx* ctx, const std::vector<std::tuple<HostMesh*, int, int>>& req,
+                          cudaStream_t s) {
+  struct Item {
+    HostMesh* h;
+    int npt;
+    TopoHost th;
+    size_t base;
+  };
+  std::vector<Item> items;
+  for (const auto& r : req) {
+    HostMesh* h = std::get<0>(r);
+    const int cs = std::get<1>(r), npt = std::get<2>(r);
+    if (!h->dev || !h->dev->b_nb_ptr || cs < 1 || cs > 16 || kClusterThreads * npt > 4096)
+      return false;
+    const int chunk = int((h->n + cs - 1) / cs);
+    if (h->dev->topo.count(topo_key(cs, chunk, npt))) continue;
+    bool dup = false;
+    for (const Item& it : items)
+      dup = dup || (it.h == h && it.th.cs == cs && it.npt == npt);
+    if (dup) continue;
+    Item it;
+    it.h = h;
+    it.npt = npt;
+    it.th.cs = cs;
+    it.th.chunk = chunk;
+    it.th.slices = (chunk + 31) / 32;
+    if (it.th.slices > kTopoMaxSlices) return false;
+    items.push_back(std::move(it));
+  }
+  if (items.empty()) return true;
+  const size_t K = items.size();
+  AllocScope scope(s);
+  std::vector<size_t> soff(K);
+  size_t stat_ints = 0;
+  for (size_t k = 0; k < K; ++k) {
+    soff[k] = stat_ints;
+    stat_ints += 4 * size_t(items[k].th.cs);
+  }
+  int* dstat = dalloc<int>(stat_ints);
+  ck(cudaMemsetAsync(dstat, 0, stat_ints * 4, s));
+  std::vector<TopoJob> jobs(K);
+  for (size_t k = 0; k < K; ++k) {
+    const Item& it = items[k];
+    TopoJob& J = jobs[k];
+    J = TopoJob{};
+    J.n = int(it.h->n);
+    J.cs = it.th.cs;
+    J.chunk = it.th.chunk;
+    J.slices = it.th.slices;
+    J.slots = kClusterThreads * it.npt;
+    J.nb_ptr = it.h->dev->b_nb_ptr;
+    J.nb_idx = it.h->dev->b_nb_idx;
+    J.g_nb = it.h->dev->b_g_nb;
+    J.stat = dstat + soff[k];
+  }
+  const size_t jb = al256(K * sizeof(TopoJob));
+  unsigned char* pin = small_pinned(ctx, 2 * jb + stat_ints * 4);
+  std::memcpy(pin, jobs.data(), K * sizeof(TopoJob));
+  TopoJob* djobs = dalloc<TopoJob>(K);
+  upload_zero_copy(djobs, pin, K * sizeof(TopoJob), s);
+  k_topo_count<<<dim3(16, unsigned(K)), kTopoThreads, 0, s>>>(djobs);
+  int* hstat = reinterpret_cast<int*>(pin + 2 * jb);
+  ck(mrb_copy_async(hstat, dstat, stat_ints * 4, cudaMemcpyDeviceToHost, s));
+  dev_mark(s, "  topology sizes");
+  host_tick("topo: count enqueued");
+  ck(cudaStreamSynchronize(s));
+  host_tick("topo: sizes synced");
+  size_t total = 0;
+  bool ok = true;
+  for (size_t k = 0; k < K && ok; ++k) {
+    TopoHost& t = items[k].th;
+    const int cs = t.cs;
+    const int* st = hstat + soff[k];
+    int stride = 0, hs = 2, ss = 2;
+    for (int r = 0; r < cs; ++r) {
+      ok = ok && st[3 * r + 2] == 0;
+      stride = std::max(stride, st[3 * r]);
+      hs = std::max(hs, st[3 * r + 1] + 1);
+      ss = std::max(ss, st[3 * cs + r]);
+    }
+    t.stride = std::max((stride + 7) / 8 * 8, 8);
+    t.hstride = (hs + 31) / 32 * 32;
+    t.sstride = (ss + 31) / 32 * 32;
+    const size_t n = size_t(items[k].h->n);
+    const size_t bytes[8] = {size_t(cs) * t.stride * 2, size_t(cs) * t.stride * 8,
+                             size_t(cs) * t.slices * 4, size_t(cs) * t.hstride * 4,
+                             size_t(cs) * 4,           n,
+                             size_t(cs) * t.sstride * 4, size_t(cs) * 4};
+    t.total = 0;
+    for (int q = 0; q < 8; ++q) {
+      t.off[q] = t.total;
+      t.total += al256(bytes[q]);
+    }
+    items[k].base = total;
+    total += t.total;
+  }
+  if (!ok) {
+    ck(cudaEventRecord(ctx->small_ev, s));
+    dev_free(djobs, s);
+    dev_free(dstat, s);
+    return false;
+  }
+  const std::shared_ptr<unsigned char> all = shared_slab(total, ctx->stream);
+  ck(cudaMemsetAsync(all.get(), 0, total, s));
+  host_tick("topo: slab");
+  for (size_t k = 0; k < K; ++k) {
+    const TopoHost& t = items[k].th;
+    unsigned char* slab = all.get() + items[k].base;
+    TopoJob& J = jobs[k];
+    J.codes = reinterpret_cast<uint16_t*>(slab + t.off[0]);
+    J.g = reinterpret_cast<float2*>(slab + t.off[1]);
+    J.soff = reinterpret_cast<uint32_t*>(slab + t.off[2]);
+    J.halo = reinterpret_cast<uint32_t*>(slab + t.off[3]);
+    J.n_halo = reinterpret_cast<int*>(slab + t.off[4]);
+    J.deg = slab + t.off[5];
+    J.send = reinterpret_cast<uint32_t*>(slab + t.off[6]);
+    J.n_send = reinterpret_cast<int*>(slab + t.off[7]);
+    J.stride = t.stride;
+    J.hstride = t.hstride;
+    J.sstride = t.sstride;
+  }
+  std::memcpy(pin + jb, jobs.data(), K * sizeof(TopoJob));
+  dev_mark(s, "  topology slab zeroed");
+  upload_zero_copy(djobs, pin + jb, K * sizeof(TopoJob), s);
+  dev_mark(s, "  topology jobs uploaded");
+  ck(cudaEventRecord(ctx->small_ev, s));
+  k_topo_write<<<dim3(16, unsigned(K)), kTopoThreads, 0, s>>>(djobs);
+  dev_mark(s, "  topology written");
+  k_topo_send<<<dim3(16, unsigned(K)), 256, 0, s>>>(djobs);
+  ck(cudaGetLastError());
+  dev_mark(s, "device topologies done");
+  dev_free(djobs, s);
+  dev_free(dstat, s);
+  host_tick("topo: write enqueued");
+  for (size_t k = 0; k < K; ++k)
+    install_topo(*items[k].h, items[k].npt, items[k].th, all.get() + items[k].base).hold = all;
+  host_tick("topo: installed");
+  return true;
+}
+
 const DeviceMesh::Topo& ensure_cluster_topo(mrb_ctx* ctx, HostMesh& h, int cs, int chunk,
                                             int npt) {
   auto it = h.dev->topo.find(topo_key(cs, chunk, npt));
   if (it != h.dev->topo.end()) return it->second;
+  if (h.dev->b_nb_ptr && device_cluster_topos(ctx, {std::make_tuple(&h, cs, npt)}, ctx->stream))
+    return h.dev->topo.at(topo_key(cs, chunk, npt));
   AllocScope scope(ctx->stream);
   const TopoHost th = plan_topo(h, cs, chunk, npt);
   std::vector<unsigned char> packed(th.total);
@@ -850,6 +1341,7 @@ struct TopoUpload {
   int slot = 1;                    // pinned staging slot
   unsigned char* stage = nullptr;  // pinned, ctx->pinned[slot]
   unsigned char* dev = nullptr;    // shared slab
+  bool device = false;             // planned + written on the GPU (device_cluster_topos)
 };
 
 TopoUpload plan_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, int cs, int npt,
@@ -859,6 +1351,18 @@ TopoUpload plan_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, 
   up.cs = cs;
   up.npt = npt;
   up.slot = slot;
+  {  // device-built meshes: planned and written on the GPU
+    bool dev = !todo.empty();
+    std::vector<std::tuple<HostMesh*, int, int>> req;
+    for (HostMesh* h : todo) {
+      dev = dev && h->dev && h->dev->b_nb_ptr;
+      req.emplace_back(h, cs, npt);
+    }
+    if (dev && device_cluster_topos(ctx, req, alloc_s ? alloc_s : ctx->stream)) {
+      up.device = true;
+      return up;
+    }
+  }
   up.th.resize(todo.size());
   parallel_for(todo.size(), [&](size_t i) {
     const HostMesh& h = *todo[i];
@@ -884,7 +1388,7 @@ TopoUpload plan_cluster_topos(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, 
 // pack meshes [i0, i1) of an upload and copy them on `stream` (one copy)
 void upload_cluster_topos(mrb_ctx* ctx, const TopoUpload& up, size_t i0, size_t i1,
                           cudaStream_t stream) {
-  if (i0 >= i1) return;
+  if (i0 >= i1 || up.device) return;
   parallel_for(i1 - i0, [&](size_t k) {
     const size_t i = i0 + k;
     write_topo(*up.meshes[i], up.cs, up.th[i], up.stage + up.base[i], up.npt);
@@ -1137,6 +1641,7 @@ std::string finish_pixel_maps(mrb_ctx* ctx, PixelMapJob& job) {
     const unsigned long long missing = job.missing[i];
     if (missing && err.empty()) {
       // densefield.py:176-182: binned locate for each unassigned pixel, row-major
+      ensure_host(h);
       std::vector<int> host(npx);
       ck(mrb_copy(host.data(), job.maps[i], npx * sizeof(int), cudaMemcpyDeviceToHost));
       Locator loc(h);
@@ -1257,6 +1762,9 @@ struct mrb_batch {
   ClusterPair* cp_pinned = nullptr;      // their pinned copy-out buffer
   std::vector<cudaEvent_t> dbg_group_ev;  // MESHREG_B200_DEBUG: start of each group launch
   std::vector<cudaEvent_t> group_ev;
+  // per wave group: its images arrived (mrb_register_many; not owned).  The
+  // group's padded copies are then made on the group's stream after it.
+  std::vector<cudaEvent_t> img_ev;
   cudaStream_t copy_stream = nullptr;
   // tail wave + its dense pass on a side stream, concurrent with the main
   // launch's dense pass (enqueue_run)
@@ -1282,6 +1790,8 @@ struct mrb_batch {
   long long* phase_prof = nullptr;  // MESHREG_B200_PROFILE_PHASES
   long long* prof_host = nullptr;   // ... = "mapped": host pointer of phase_prof
   float2* img_pad = nullptr;  // 4 shifted padded (H+2)x(W+2) (Te, Re) copies per pair
+  bool img_pad_borrowed = false;  // ctx kept buffers (mrb_register_many batches)
+  bool pairs_borrowed = false;    // state + dense from the ctx kept buffers
   int runs = 0;
   // host results
   std::vector<PairStatus> h_st;
@@ -1321,8 +1831,10 @@ struct mrb_batch {
     }
     if (grp_fork) cudaEventDestroy(grp_fork);
     if (grp_join) cudaEventDestroy(grp_join);
-    void* ptrs[] = {pairs, st, blk_pair, pix_blk_pair, partials, pix_partials, state, traces,
-                    img, stage, src_ptrs, img_ptrs, dense, u_out, conv, cpairs, img_pad, c64_pairs, pad64,
+    void* ptrs[] = {pairs, st, blk_pair, pix_blk_pair, partials, pix_partials,
+                    pairs_borrowed ? nullptr : state, traces, img, stage, src_ptrs, img_ptrs,
+                    pairs_borrowed ? nullptr : dense, u_out, conv, cpairs,
+                    img_pad_borrowed ? nullptr : img_pad, c64_pairs, pad64,
                     prof_host ? nullptr : phase_prof, xbuf, xbar, xexports};
     if (prof_host) cudaFreeHost(prof_host);
     for (void* p : ptrs) dev_free(p, ctx ? ctx->stream : nullptr);
@@ -1336,6 +1848,7 @@ size_t real_size(const mrb_batch* b) { return b->real_d ? sizeof(double) : sizeo
 size_t in_size(int dtype) { return dtype == MRB_F64 ? sizeof(double) : sizeof(float); }
 
 void free_pairs(mrb_batch* b) {
+  if (b->pairs_borrowed) b->state = b->dense = nullptr;
   void** ptrs[] = {&b->state, &b->dense, &b->pairs, reinterpret_cast<void**>(&b->blk_pair),
                    reinterpret_cast<void**>(&b->pix_blk_pair),
                    reinterpret_cast<void**>(&b->partials),
@@ -1360,8 +1873,15 @@ void build_pairs(mrb_batch* b) {
     const size_t n = size_t(b->meshes[p]->h.n);
     state_bytes += (3 * n * sizeof(R2) + 2 * n * sizeof(Real) + 255) / 256 * 256;
   }
-  b->state = dalloc<char>(state_bytes);
-  b->dense = dalloc<Real>(3 * npx * b->n_pairs);
+  if (b->forced_cs) {  // mrb_register_many
+    b->state = kept_buffer(b->ctx, kKeptState, state_bytes);
+    b->dense = kept_buffer(b->ctx, kKeptDense, 3 * npx * b->n_pairs * sizeof(Real));
+    b->pairs_borrowed = true;
+  } else {
+    b->state = dalloc<char>(state_bytes);
+    b->dense = dalloc<Real>(3 * npx * b->n_pairs);
+  }
+  host_tick("pairs: state + dense");
   int blk = 0, pblk = 0;
   std::vector<int> bp, pbp;
   const int pix_nblk = int((npx + kPixBlock - 1) / kPixBlock);
@@ -1414,11 +1934,13 @@ void build_pairs(mrb_batch* b) {
   b->n_node_blocks = blk;
   b->n_pix_blocks = pblk;
   cudaStream_t s = b->ctx->stream;
+  host_tick("pairs: filled");
   b->pairs = aupload(b->ctx, pd.data(), pd.size());
   b->blk_pair = aupload(b->ctx, bp.data(), bp.size());
   b->pix_blk_pair = aupload(b->ctx, pbp.data(), pbp.size());
   b->partials = dalloc<double>(blk);
   b->pix_partials = dalloc<double2>(pblk);
+  host_tick("pairs: uploaded");
   b->pairs_host.assign(reinterpret_cast<const unsigned char*>(pd.data()),
                        reinterpret_cast<const unsigned char*>(pd.data() + pd.size()));
 }
@@ -1670,10 +2192,10 @@ void flush_topo(mrb_batch* b, int p1, cudaStream_t copy, cudaStream_t s) {
           std::find(todo.begin(), todo.end(), h) == todo.end())
         todo.push_back(h);
     }
+    if (!b->topo_ev) ck(cudaEventCreateWithFlags(&b->topo_ev, cudaEventDisableTiming));
     if (!todo.empty()) {
       b->lazy_ups.emplace_back(
           new TopoUpload(plan_cluster_topos(b->ctx, todo, cs, npt, 1, copy)));
-      if (!b->topo_ev) ck(cudaEventCreateWithFlags(&b->topo_ev, cudaEventDisableTiming));
       upload_cluster_topos(b->ctx, *b->lazy_ups.back(), 0, todo.size(), copy);
     }
     patch_descriptors(b, b->lazy_from, pe);
@@ -1745,13 +2267,24 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
       // one persistent cluster launch for every iteration of every pair,
       // then the fused dense pass
       const size_t npad = size_t(b->W + 2) * (b->H + 2);
-      k_pad_planar4<<<dim3(unsigned(std::min<size_t>((npad + 255) / 256, 1024)), b->n_pairs), 256,
-                      0, s>>>(reinterpret_cast<const float* const*>(b->src_ptrs),
-                              reinterpret_cast<const float* const*>(b->src_ptrs + b->n_pairs),
-                              b->W, b->H, b->img_pad, b->pad_pitch, b->pad_plane,
-                              4 * b->pad_plane);
-      ++launches;
-      if (b->groups.size() > 2 && tm == &dummy && b->runs == 0) {
+      auto pad = [&](int p0, int p1, cudaStream_t st_) {
+        k_pad_planar4<<<dim3(unsigned(std::min<size_t>((npad + 255) / 256, 1024)), p1 - p0), 256,
+                        0, st_>>>(reinterpret_cast<const float* const*>(b->src_ptrs) + p0,
+                                  reinterpret_cast<const float* const*>(b->src_ptrs + b->n_pairs) +
+                                      p0,
+                                  b->W, b->H, b->img_pad + size_t(p0) * 4 * b->pad_plane,
+                                  b->pad_pitch, b->pad_plane, 4 * b->pad_plane);
+        ++launches;
+      };
+      const bool grouped_run = b->groups.size() > 2 && tm == &dummy && b->runs == 0;
+      // images per wave group (mrb_register_many): each group pads its own
+      // pairs once their copy landed, so group 0 need not wait for the rest
+      const bool group_pads = grouped_run && b->img_ev.size() + 1 == b->groups.size();
+      if (!group_pads) {
+        for (cudaEvent_t e : b->img_ev) ck(cudaStreamWaitEvent(s, e, 0));
+        pad(0, b->n_pairs, s);
+      }
+      if (grouped_run) {
         // per wave group: loop + dense pass + MSD, then an event for the
         // group's device-to-host copies (mrb_batch_get_results)
         const PD* host = reinterpret_cast<const PD*>(b->pairs_host.data());
@@ -1783,7 +2316,7 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
           ck(cudaEventCreateWithFlags(&b->grp_fork, cudaEventDisableTiming));
           ck(cudaEventCreateWithFlags(&b->grp_join, cudaEventDisableTiming));
         }
-        ck(cudaEventRecord(b->grp_fork, s));  // padded images ready
+        ck(cudaEventRecord(b->grp_fork, s));  // descriptors (and unless group_pads, images) ready
         ck(cudaStreamWaitEvent(b->grp_stream, b->grp_fork, 0));
         const cudaStream_t gst[2] = {s, b->grp_stream};
         for (size_t g = 0; g < ng; ++g) {
@@ -1795,6 +2328,10 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
           // (grid mode: whole-GPU cooperative launches sharing one exchange
           // buffer must stay serial on one stream)
           const cudaStream_t gs = b->grid_mode ? s : gst[g & 1];
+          if (group_pads) {
+            ck(cudaStreamWaitEvent(gs, b->img_ev[g], 0));
+            pad(p0, p1, gs);
+          }
           // this group's topologies (host packing overlaps the previous group)
           flush_topo(b, p1, b->copy_stream, gs);
           if (p1 > b->tail_p0) flush_tail_topo(b, b->copy_stream, gs);
@@ -1811,6 +2348,10 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
             const int t0 = b->groups[ng - 1], t1 = b->groups[ng];
             ck(cudaEventRecord(b->tail_fork, gs));
             ck(cudaStreamWaitEvent(b->tail_stream, b->tail_fork, 0));
+            if (group_pads) {
+              ck(cudaStreamWaitEvent(b->tail_stream, b->img_ev[ng - 1], 0));
+              pad(t0, t1, b->tail_stream);
+            }
             flush_topo(b, t1, b->copy_stream, b->tail_stream);
             flush_tail_topo(b, b->copy_stream, b->tail_stream);
             b->lstream = b->tail_stream;
@@ -2121,6 +2662,14 @@ void setup_cluster_path(mrb_batch* b) {
   auto why = [&](const char* m) {
     if (dbg) std::fprintf(stderr, "meshreg_b200: generic path (%s)\n", m);
   };
+  auto t0 = std::chrono::steady_clock::now();
+  auto tick = [&](const char* what) {
+    if (!dbg) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "meshreg_b200:   cluster setup %-18s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   const char* reason = nullptr;
   const int mode = fast_mode(b->real_d, b->tap_d, b->in_dtype, b->meshes, &reason);
   if (mode == 0) return why(reason);
@@ -2149,6 +2698,7 @@ void setup_cluster_path(mrb_batch* b) {
     for (int p = 0; p < plan_end; ++p) hm.push_back(&b->meshes[p]->h);
     ensure_cluster_topos(b->ctx, hm, cs, npt);
   }
+  tick("topologies");
   auto main_smem = [&](int p0, int p1, size_t smem) {
     for (int p = p0; p < p1; ++p) {
       HostMesh& h = b->meshes[p]->h;
@@ -2189,10 +2739,12 @@ void setup_cluster_path(mrb_batch* b) {
       b->push_smem = ps;
     }
   }
+  tick("shape + exchange");
   if (dbg)
     std::fprintf(stderr, "meshreg_b200: cluster %d CTAs x %d nodes/thread, %zu B smem, %s exchange\n",
                  cs, npt, b->push_mode ? b->push_smem : smem, b->push_mode ? "push" : "pull");
   setup_tail(b, smem);
+  tick("tail");
   if (b->tail_p0 > main_end && main_end < b->n_pairs) {
     // no tail after all: the remaining pairs need the main shape (staging
     // slot 2, slot 1 still backs the deferred groups)
@@ -2206,6 +2758,7 @@ void setup_cluster_path(mrb_batch* b) {
     }
   }
   build_fast_descriptors(b);
+  tick("descriptors");
 }
 
 // Tail split of a throughput-mode batch (see mrb_batch::tail_p0): with W
@@ -2286,7 +2839,15 @@ void build_fast_descriptors(mrb_batch* b) {
   b->pad_pitch = (b->W + 5 + 3) / 4 * 4;
   b->pad_plane = size_t(b->H + 2) * b->pad_pitch;
   // columns of a copy that k_pad_planar4 does not write are never read
-  b->img_pad = dalloc<float2>(4 * b->pad_plane * b->n_pairs);
+  {
+    const size_t need = 4 * b->pad_plane * b->n_pairs;
+    if (b->forced_cs) {  // mrb_register_many: its batches on a context run in turn
+      b->img_pad = static_cast<float2*>(kept_buffer(b->ctx, kKeptPad, need * sizeof(float2)));
+      b->img_pad_borrowed = true;
+    } else {
+      b->img_pad = dalloc<float2>(need);
+    }
+  }
   const PairDev<float, float>* host =
       reinterpret_cast<const PairDev<float, float>*>(b->pairs_host.data());
   std::vector<ClusterPair> cp(b->n_pairs);
@@ -2386,7 +2947,9 @@ void build_fast_descriptors(mrb_batch* b) {
       }
     }
   }
+  host_tick("descriptors: filled");
   b->cpairs = aupload(b->ctx, cp.data(), cp.size());
+  host_tick("descriptors: uploaded");
   if (b->lazy_from < std::min(b->planned_end, b->n_pairs)) {
     b->cp_host = cp;
     ck(cudaHostAlloc(reinterpret_cast<void**>(&b->cp_pinned), sizeof(ClusterPair) * cp.size(),
@@ -2541,6 +3104,16 @@ std::string pair_message(const mrb_batch* b, int p, int* code) {
   return "";
 }
 
+// deferred handles reaching a host-side consumer: the full host build first
+// (the reference validates the whole mesh in TriMesh.__init__, mesh.py:58-123)
+int host_ready(mrb_ctx* ctx, mrb_mesh* const* meshes, int64_t count) {
+  for (int64_t k = 0; k < count; ++k) {
+    const std::string& e = ensure_host(meshes[k]->h);
+    if (!e.empty()) return fail(ctx, MRB_E_VALUE, e);
+  }
+  return MRB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -2602,6 +3175,13 @@ int mrb_ctx_destroy(mrb_ctx* ctx) {
   if (ctx->counts) cudaFreeHost(ctx->counts);
   if (ctx->arena) cudaFreeHost(ctx->arena);
   if (ctx->arena_done) cudaEventDestroy(ctx->arena_done);
+  if (ctx->small_pin) cudaFreeHost(ctx->small_pin);
+  if (ctx->small_ev) cudaEventDestroy(ctx->small_ev);
+  if (ctx->build_stats) cudaFreeHost(ctx->build_stats);
+  if (ctx->build_ev) cudaEventDestroy(ctx->build_ev);
+  if (ctx->build_in) cudaEventDestroy(ctx->build_in);
+  for (auto& k : ctx->kept)
+    if (k.p) cudaFree(k.p);
   delete ctx;
   return MRB_OK;
 }
@@ -2674,12 +3254,130 @@ int mrb_mesh_build_many(int32_t count, const int64_t* n, const double* const* V,
   return MRB_OK;
 }
 
+int mrb_mesh_create_many(int32_t count, const int64_t* n, const double* const* V, const int64_t* m,
+                         const int64_t* const* T, mrb_mesh** out, int32_t* first_bad, char* err,
+                         int32_t err_len) {
+  if (first_bad) *first_bad = -1;
+  if (count < 0 || (count > 0 && (!n || !V || !m || !T || !out))) return MRB_E_VALUE;
+  for (int32_t k = 0; k < count; ++k) out[k] = nullptr;
+  if (count == 0) return MRB_OK;
+  // one block for every mesh of the call, laid out as the device build
+  // uploads it (V, then the oriented int32 T, 256-byte aligned): pinned and
+  // recycled, so neither page faults nor a staging copy
+  std::vector<size_t> off(static_cast<size_t>(count) + 1, 0);
+  for (int32_t k = 0; k < count; ++k)
+    off[k + 1] = off[k] + al256(size_t(std::max<int64_t>(n[k], 0)) * 16) +
+                 al256(size_t(std::max<int64_t>(m[k], 0)) * 12);
+  const std::shared_ptr<unsigned char> block = pinned_block(std::max<size_t>(off[count], 256));
+  std::vector<std::string> msg(static_cast<size_t>(count));
+  WorkerPool::get().run(size_t(count), [&](size_t k) {
+    auto* mesh = new mrb_mesh();
+    unsigned char* at = block.get() + off[k];
+    try {
+      msg[k] = create_mesh(n[k], V[k], m[k], T[k], reinterpret_cast<double*>(at),
+                           reinterpret_cast<int32_t*>(at + al256(size_t(n[k]) * 16)), mesh->h);
+    } catch (const std::exception& ex) {
+      msg[k] = std::string("internal error: ") + ex.what();
+    }
+    if (msg[k].empty()) {
+      mesh->h.def_hold = block;
+      out[k] = mesh;
+    } else {
+      delete mesh;
+    }
+  });
+  for (int32_t k = 0; k < count; ++k)
+    if (!msg[k].empty()) {
+      if (first_bad) *first_bad = k;
+      if (err && err_len > 0) {
+        std::strncpy(err, msg[k].c_str(), size_t(err_len) - 1);
+        err[err_len - 1] = 0;
+      }
+      for (int32_t j = 0; j < count; ++j) {  // all or nothing
+        delete out[j];
+        out[j] = nullptr;
+      }
+      return MRB_E_VALUE;
+    }
+  return MRB_OK;
+}
+
 int mrb_mesh_destroy(mrb_mesh* mesh) {
   delete mesh;
   return MRB_OK;
 }
 
+int mrb_mesh_device_check(mrb_ctx* ctx, mrb_mesh* mesh, int32_t cs, int32_t npt, int64_t* out) {
+  // test hook: the device build of a deferred mesh against the host build
+  // (element mismatches per array; see the header)
+  if (!ctx || !mesh || !out) return MRB_E_VALUE;
+  HostMesh& h = mesh->h;
+  if (!h.deferred || !(h.dev ? h.dev->b_nb_ptr != nullptr : device_buildable(h)))
+    return fail(ctx, MRB_E_VALUE, "not a device-buildable deferred mesh");
+  try {
+    ck(cudaSetDevice(ctx->device));
+    AllocScope scope(ctx->stream);
+    if (!h.dev) device_build_meshes(ctx, {&h}, ctx->stream);
+    {
+      const std::string e = device_build_finish(ctx);
+      if (!e.empty()) return fail(ctx, MRB_E_VALUE, e);
+    }
+    if (!h.dev || !h.dev->b_nb_ptr) return fail(ctx, MRB_E_INTERNAL, "device build flagged");
+    const int chunk = int((h.n + cs - 1) / cs);
+    if (!device_cluster_topos(ctx, {std::make_tuple(&h, int(cs), int(npt))}, ctx->stream))
+      return fail(ctx, MRB_E_INTERNAL, "device topology needs the host planner");
+    ck(cudaStreamSynchronize(ctx->stream));
+    // the host build of the same mesh (a copy: h keeps its device arrays)
+    HostMesh H;
+    {
+      const std::vector<int64_t> T64(h.dT, h.dT + 3 * h.m);
+      const std::string e = build_mesh(h.n, h.dV, h.m, T64.data(), H);
+      if (!e.empty()) return fail(ctx, MRB_E_VALUE, e);
+    }
+    const size_t n = size_t(h.n), m = size_t(h.m), e2 = H.nb_idx.size();
+    const DeviceMesh& d = *h.dev;
+    auto fetch = [&](const void* src, size_t bytes) {
+      std::vector<unsigned char> v(bytes);
+      ck(cudaMemcpy(v.data(), src, bytes, cudaMemcpyDeviceToHost));
+      return v;
+    };
+    auto diff = [](const void* a, const void* b, size_t count, size_t size) {
+      int64_t c = 0;
+      for (size_t i = 0; i < count; ++i)
+        c += std::memcmp(static_cast<const char*>(a) + i * size,
+                         static_cast<const char*>(b) + i * size, size) != 0;
+      return c;
+    };
+    std::vector<float> gs(2 * n), iv(n);
+    for (size_t k = 0; k < 2 * n; ++k) gs[k] = float(H.g_self[k]);
+    for (size_t k = 0; k < n; ++k) iv[k] = float(H.inv_val[k]);
+    out[0] = diff(fetch(d.V, n * 16).data(), H.Vn.data(), n, 16);
+    out[1] = diff(fetch(d.tri, m * 16).data(), H.Tn.data(), m, 16);
+    out[2] = diff(fetch(d.perm, n * 4).data(), H.perm.data(), n, 4);
+    out[3] = diff(fetch(d.g_self_f, n * 8).data(), gs.data(), n, 8);
+    out[4] = diff(fetch(d.inv_val_f, n * 4).data(), iv.data(), n, 4);
+    out[5] = int64_t(h.max_deg != H.max_deg) + int64_t(h.ne != H.ne);
+    out[6] = diff(fetch(d.b_nb_ptr, (n + 1) * 4).data(), H.nb_ptr.data(), n + 1, 4);
+    out[7] = diff(fetch(d.b_nb_idx, e2 * 4).data(), H.nb_idx.data(), e2, 4);
+    out[8] = diff(fetch(d.b_g_nb, e2 * 16).data(), H.g_nb.data(), e2, 16);
+    const DeviceMesh::Topo& t = d.topo.at(topo_key(cs, chunk, npt));
+    const TopoHost th = plan_topo(H, cs, chunk, npt);
+    std::vector<unsigned char> packed(th.total, 0);
+    write_topo(H, cs, th, packed.data(), npt);
+    if (t.topo_stride != th.stride || t.halo_stride != th.hstride ||
+        t.send_stride != th.sstride || t.slices != th.slices) {
+      out[9] = -1;
+    } else {
+      out[9] = diff(fetch(t.slab, th.total).data(), packed.data(), th.total, 1);
+    }
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e, e.line);
+  }
+  return MRB_OK;
+}
+
 int mrb_mesh_counts(const mrb_mesh* mesh, int64_t* c) {
+  if (!ensure_host(const_cast<mrb_mesh*>(mesh)->h).empty()) return MRB_E_VALUE;
   const HostMesh& h = mesh->h;
   c[0] = h.n;
   c[1] = h.m;
@@ -2693,6 +3391,7 @@ int mrb_mesh_counts(const mrb_mesh* mesh, int64_t* c) {
 int mrb_mesh_export_connectivity(const mrb_mesh* mesh, int64_t* tri, int64_t* edges,
                                  int64_t* valence, uint8_t* boundary, int64_t* ring_ptr,
                                  int64_t* ring_idx, int64_t* inc_ptr, int64_t* inc_idx) {
+  if (!ensure_host(const_cast<mrb_mesh*>(mesh)->h).empty()) return MRB_E_VALUE;
   const HostMesh& h = mesh->h;
   auto cp = [](int64_t* dst, const std::vector<int64_t>& v) {
     if (dst) std::memcpy(dst, v.data(), v.size() * sizeof(int64_t));
@@ -2711,6 +3410,7 @@ int mrb_mesh_export_connectivity(const mrb_mesh* mesh, int64_t* tri, int64_t* ed
 int mrb_mesh_export_csr(const mrb_mesh* mesh, int32_t which, int64_t* indptr, int64_t* indices,
                         double* data) {
   HostMesh& h = const_cast<mrb_mesh*>(mesh)->h;  // the CSR cache is built on first use
+  if (!ensure_host(h).empty()) return MRB_E_VALUE;
   ensure_reference_csr(h);
   const Csr* c = which == MRB_CSR_LAPLACIAN  ? &h.lap
                  : which == MRB_CSR_GRAD_X   ? &h.gx
@@ -2726,6 +3426,7 @@ int mrb_mesh_export_csr(const mrb_mesh* mesh, int32_t which, int64_t* indptr, in
 
 int mrb_mesh_export_geometry(const mrb_mesh* mesh, double* areas, double* coeffs,
                              double* vertex_areas) {
+  if (!ensure_host(const_cast<mrb_mesh*>(mesh)->h).empty()) return MRB_E_VALUE;
   const HostMesh& h = mesh->h;
   if (areas) std::memcpy(areas, h.areas.data(), h.areas.size() * sizeof(double));
   if (coeffs) std::memcpy(coeffs, h.coeffs.data(), h.coeffs.size() * sizeof(double));
@@ -2737,6 +3438,7 @@ int mrb_mesh_export_geometry(const mrb_mesh* mesh, double* areas, double* coeffs
 int mrb_mesh_locate(mrb_mesh* mesh, int64_t n, const double* pts, int64_t* tri, double* w) {
   // PointLocator + locate, densefield.py:62-127: lowest-index containing
   // triangle and its barycentric weights in numpy's order; -1 if uncovered
+  if (!ensure_host(mesh->h).empty()) return MRB_E_VALUE;
   if (!mesh->locator) mesh->locator.reset(new Locator(mesh->h));
   for (int64_t i = 0; i < n; ++i) {
     double wi[3] = {0.0, 0.0, 0.0};
@@ -2748,6 +3450,7 @@ int mrb_mesh_locate(mrb_mesh* mesh, int64_t n, const double* pts, int64_t* tri, 
 
 int mrb_pixel_map(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int64_t* tri_of,
                   double* weights) {
+  if (const int rc = host_ready(ctx, &mesh, 1)) return rc;
   try {
     AllocScope scope(ctx->stream);
     ck(cudaSetDevice(ctx->device));
@@ -2774,7 +3477,7 @@ int mrb_pixel_map(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int64_t* t
     }
     return MRB_OK;
   } catch (const CudaError& e) {
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
 }
 
@@ -2881,8 +3584,17 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
             planned = n_pairs - n_pairs % defer_topo;
           b->planned_end = planned;
           // only the first wave group is planned here; later groups are
-          // planned in the run, ahead of their launch (flush_topo)
+          // planned in the run, ahead of their launch (flush_topo) — unless
+          // every topology exists already (device-built meshes)
           b->lazy_from = std::min(defer_topo, planned);
+          {
+            bool all = true;
+            for (int p = b->lazy_from; p < planned && all; ++p) {
+              HostMesh* h = hm[p];
+              all = h->dev->topo.count(topo_key(cs, int((h->n + cs - 1) / cs), npt)) > 0;
+            }
+            if (all) b->lazy_from = planned;
+          }
           std::vector<HostMesh*> todo;
           for (int p = 0; p < b->lazy_from; ++p) {
             HostMesh* h = hm[p];
@@ -2918,15 +3630,22 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
     if (!rasters_issued) pmj = issue_pixel_maps(ctx, hm, W, H);
     b->total_nodes = off;
     const size_t npx = size_t(W) * H;
+    host_tick("batch: before buffers");
     b->st = dalloc<PairStatus>(n_pairs);
     b->traces = dalloc<double>(size_t(n_pairs) * cfg->max_iterations);
-    b->img = dalloc<char>(size_t(n_pairs) * 2 * npx * tap_size(b.get()));
     b->u_out = dalloc<double2>(off);
     b->src_ptrs = dalloc<void*>(2 * n_pairs);
-    std::vector<void*> ip(n_pairs);
-    for (int p = 0; p < n_pairs; ++p)
-      ip[p] = static_cast<char*>(b->img) + size_t(p) * 2 * npx * tap_size(b.get());
-    b->img_ptrs = aupload(ctx, ip.data(), ip.size());
+    // the interleaved image copy of the generic / fp64 loops (the fp32
+    // cluster path reads the planar inputs): allocated when a path needs it
+    auto alloc_img = [&](mrb_batch* bb) {
+      bb->img = dalloc<char>(size_t(n_pairs) * 2 * npx * tap_size(bb));
+      std::vector<void*> ip(n_pairs);
+      for (int p = 0; p < n_pairs; ++p)
+        ip[p] = static_cast<char*>(bb->img) + size_t(p) * 2 * npx * tap_size(bb);
+      bb->img_ptrs = aupload(ctx, ip.data(), ip.size());
+    };
+    if (!(eligible && mode == 1 && !b->real_d)) alloc_img(b.get());
+    host_tick("batch: small buffers");
     if (b->tap_d)
       build_pairs<double, double>(b.get());
     else if (b->real_d)
@@ -2951,6 +3670,7 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
     if (eligible && !b->cluster_cs) {
       // predicted fast path did not fit after all: generic path needs the rings
       for (HostMesh* h : hm) ensure_device_mesh_ring(ctx, *h);
+      if (!b->img) alloc_img(b.get());
       free_pairs(b.get());
       if (b->real_d)
         build_pairs<float, double>(b.get());
@@ -2967,7 +3687,7 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
     }
     tick("pixel maps");
   } catch (const CudaError& e) {
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
   *out = b.release();
   return MRB_OK;
@@ -3169,6 +3889,8 @@ extern "C" {
 
 int mrb_batch_create(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int32_t W,
                      int32_t H, int32_t img_dtype, const mrb_config* cfg, mrb_batch** out) {
+  if (n_pairs > 0 && meshes)
+    if (const int rc = host_ready(ctx, meshes, n_pairs)) return rc;
   return batch_create_impl(ctx, n_pairs, meshes, W, H, img_dtype, cfg, 0, 0, out);
 }
 
@@ -3211,7 +3933,7 @@ int mrb_batch_set_images(mrb_batch* b, const void* re, const void* te, int32_t o
       ck(cudaGetLastError());
     }
   } catch (const CudaError& e) {
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
   return MRB_OK;
 }
@@ -3236,7 +3958,7 @@ int mrb_batch_run(mrb_batch* b) {
     }
     b->runs++;
   } catch (const CudaError& e) {
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
   return MRB_OK;
 }
@@ -3305,7 +4027,7 @@ int mrb_batch_get_results(mrb_batch* b, int32_t out_dtype, double* u, void* ux, 
       }
     }
   } catch (const CudaError& e) {
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
   return MRB_OK;
 }
@@ -3335,7 +4057,7 @@ int mrb_batch_sync(mrb_batch* b) {
                   cudaMemcpyDeviceToHost));
     b->synced = true;
   } catch (const CudaError& e) {
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
   for (int p = 0; p < b->n_pairs; ++p) {
     int code;
@@ -3399,7 +4121,7 @@ int mrb_batch_phase_profile(mrb_batch* b, long long* out, int64_t n) {
   try {
     ck(mrb_copy(out, b->phase_prof, cnt * sizeof(long long), cudaMemcpyDeviceToHost));
   } catch (const CudaError& e) {
-    return cuda_fail(b->ctx, e.e);
+    return cuda_fail(b->ctx, e.e, e.line);
   }
   return MRB_OK;
 }
@@ -3468,7 +4190,7 @@ int mrb_batch_kernel_times(mrb_batch* b, double* out) {
     cudaEventDestroy(e1);
     b->synced = false;
   } catch (const CudaError& e) {
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
   return MRB_OK;
 }
@@ -3488,11 +4210,67 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
   // computes on the other pipeline stream; the chunk's pipeline stream then
   // waits for that setup (event) and its batch creation is cheap.
   if (n_pairs < 1) return fail(ctx, MRB_E_VALUE, "batch needs at least one pair");
+  const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
+  const auto T0 = std::chrono::steady_clock::now();
+  auto stamp = [&](const char* what, int k) {
+    if (dbg)
+      std::fprintf(stderr, "meshreg_b200: many %8.2f ms  %s %d\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - T0)
+                       .count(),
+                   what, k);
+  };
+  cudaEvent_t dbg_t0 = nullptr;  // device timeline origin (MESHREG_B200_DEBUG)
+  if (dbg) {
+    cudaSetDevice(ctx->device);
+    cudaEventCreate(&dbg_t0);
+    cudaEventRecord(dbg_t0, ctx->stream);
+  }
   for (auto& c : ctx->sub)
     if (!c) {
       const int rc = mrb_ctx_create(ctx->device, &c);
       if (rc != MRB_OK) return fail(ctx, rc, "cannot create a pipeline stream");
     }
+  // Deferred handles (mrb_mesh_create_many): the per-mesh setup runs on the
+  // GPU (meshbuild.cuh) when the batch takes the fp32 cluster fast path; any
+  // other batch gets the host build first.
+  bool dev_setup = false;
+  {
+    bool any = false, fits = true;
+    for (int p = 0; p < n_pairs; ++p) {
+      const HostMesh& h = meshes[p]->h;
+      if (!h.deferred) continue;
+      any = true;
+      fits = fits && (h.dev ? h.dev->b_nb_ptr != nullptr : device_buildable(h));
+    }
+    if (any) {
+      std::vector<mrb_mesh*> all(meshes, meshes + n_pairs);
+      dev_setup = fits && !std::getenv("MESHREG_B200_HOST_SETUP") && config_error(cfg).empty() &&
+                  cfg->precision == MRB_PREC_F32 && img_dtype == MRB_F32 &&
+                  !cluster_ineligible(false, false, img_dtype, all);
+      if (!dev_setup) {
+        if (const int rc = host_ready(ctx, meshes, n_pairs)) return rc;
+      } else {
+        std::vector<HostMesh*> todo;
+        for (int p = 0; p < n_pairs; ++p) {
+          HostMesh* h = &meshes[p]->h;
+          if (device_buildable(*h) && std::find(todo.begin(), todo.end(), h) == todo.end())
+            todo.push_back(h);
+        }
+        try {
+          ck(cudaSetDevice(ctx->device));
+          if (!ctx->copy) {
+            ck(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+            ck(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
+          }
+          // V / T go first on the copy stream, ahead of the images
+          device_build_meshes(ctx, todo, ctx->copy);
+          stamp("device mesh build enqueued", 0);
+        } catch (const CudaError& e) {
+          return cuda_fail(ctx, e.e, e.line);
+        }
+      }
+    }
+  }
   // The fast-path cluster shape is decided once for the whole queue (cost
   // model with P = n_pairs) and imposed on every chunk.  Default chunk = one
   // wave of that shape (the pairs one launch keeps resident), so the chunks'
@@ -3516,7 +4294,7 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
                                   &forced_npt, &occ))
           forced_cs = forced_npt = occ = 0;
       } catch (const CudaError& e) {
-        return cuda_fail(ctx, e.e);
+        return cuda_fail(ctx, e.e, e.line);
       }
       wave = occ;
     }
@@ -3524,27 +4302,99 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
   // default: one chunk (the per-chunk host setup costs more than a wave's
   // device time); within it, wave groups overlap results D2H with compute
   if (chunk_pairs <= 0) chunk_pairs = n_pairs;
-  const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
-  const auto T0 = std::chrono::steady_clock::now();
-  auto stamp = [&](const char* what, int k) {
-    if (dbg)
-      std::fprintf(stderr, "meshreg_b200: many %8.2f ms  %s %d\n",
-                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - T0)
-                       .count(),
-                   what, k);
-  };
   const size_t npx = size_t(W) * H, es = in_size(img_dtype), os = in_size(out_dtype);
+  // Chunk 0's images: H2D issued now on the copy stream (behind the meshes'
+  // V / T), one copy pair per wave group with an event each, so the device
+  // setup overlaps them and group g's loop waits only for its own images.
+  struct EarlyImages {
+    char* dimg = nullptr;
+    std::vector<cudaEvent_t> ev;
+    ~EarlyImages() {
+      for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    }
+  } early;
+  const bool no_groups = std::getenv("MESHREG_B200_NO_GROUPS") != nullptr;
+  try {
+    ck(cudaSetDevice(ctx->device));
+    if (!ctx->copy) {
+      ck(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+      ck(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
+    }
+    const int P0 = std::min<int>(chunk_pairs, n_pairs);
+    const size_t img_bytes = size_t(P0) * npx * es;
+    const int per = wave > 0 && P0 > wave && !no_groups ? wave : P0;
+    AllocScope scope(ctx->copy);
+    early.dimg = static_cast<char*>(kept_buffer(ctx, kKeptImages, 2 * img_bytes));
+    for (int a = 0; a < P0; a += per) {
+      const int e = std::min(P0, a + per);
+      const size_t o = size_t(a) * npx * es, len = size_t(e - a) * npx * es;
+      ck(mrb_copy_async(early.dimg + o, static_cast<const char*>(reference) + o, len,
+                        cudaMemcpyHostToDevice, ctx->copy));
+      ck(mrb_copy_async(early.dimg + img_bytes + o, static_cast<const char*>(tmpl) + o, len,
+                        cudaMemcpyHostToDevice, ctx->copy));
+      cudaEvent_t ev;
+      ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      early.ev.push_back(ev);
+      ck(cudaEventRecord(ev, ctx->copy));
+    }
+    ck(cudaEventRecord(ctx->copy_done, ctx->copy));
+    dev_mark(ctx->copy, "images H2D done");
+    stamp("images enqueued", 0);
+  } catch (const CudaError& e) {
+    return cuda_fail(ctx, e.e, e.line);
+  }
+  if (dev_setup) {
+    // every fast-path topology the run uses, planned and written on the GPU
+    // now: the main shape for the pairs of full waves, the latency shape of
+    // the tail wave (setup_tail) for the rest
+    try {
+      AllocScope scope(ctx->stream);
+      if (forced_cs) {
+        int planned = n_pairs;
+        if (chunk_pairs >= n_pairs && forced_npt == 2 && wave > 0 && n_pairs > wave &&
+            n_pairs % wave && !std::getenv("MESHREG_B200_NO_TAIL"))
+          planned = n_pairs - n_pairs % wave;
+        std::vector<std::tuple<HostMesh*, int, int>> req;
+        for (int p = 0; p < planned; ++p) req.emplace_back(&meshes[p]->h, forced_cs, forced_npt);
+        if (planned < n_pairs) {
+          mrb_mesh* big = *std::max_element(
+              meshes + planned, meshes + n_pairs,
+              [](mrb_mesh* x, mrb_mesh* y) { return x->h.n < y->h.n; });
+          int tcs = 0, tnpt = 0, tocc = 0;
+          const bool tail = choose_cluster_shape(ctx, big->h, n_pairs - planned,
+                                                 cfg->smoothing_passes >= 2, &tcs, &tnpt, &tocc,
+                                                 1) &&
+                            tnpt == 1;
+          for (int p = planned; p < n_pairs; ++p)
+            req.emplace_back(&meshes[p]->h, tail ? tcs : forced_cs, tail ? 1 : forced_npt);
+        }
+        device_cluster_topos(ctx, req, ctx->stream);  // false: planned later (host)
+        stamp("device topologies", 0);
+      }
+      const std::string e = device_build_finish(ctx);
+      if (!e.empty()) return fail(ctx, MRB_E_VALUE, e);
+      // the build arrays go back to the pool now (stream-ordered) for this
+      // call's batch buffers; a later topology of another shape for these
+      // meshes is planned on the host
+      for (int p = 0; p < n_pairs; ++p) {
+        HostMesh& h = meshes[p]->h;
+        if (h.dev && h.dev->b_nb_ptr) {
+          h.dev->b_nb_ptr = nullptr;
+          h.dev->b_nb_idx = nullptr;
+          h.dev->b_g_nb = nullptr;
+          h.dev->build_hold.reset();
+        }
+      }
+    } catch (const CudaError& e) {
+      return cuda_fail(ctx, e.e, e.line);
+    }
+  }
   std::vector<mrb_batch*> live;  // batches in flight, freed once harvested
   std::vector<std::pair<int, int>> span;
   int first_err = MRB_OK;
   std::string first_msg;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> dbg_events;  // run of each chunk
   std::vector<cudaEvent_t> dbg_done;                             // results of each chunk
-  cudaEvent_t dbg_t0 = nullptr;
-  if (dbg) {
-    cudaEventCreate(&dbg_t0);
-    cudaEventRecord(dbg_t0, ctx->stream);
-  }
   auto harvest = [&](size_t k) {  // wait for chunk k and collect its statuses
     mrb_batch* b = live[k];
     if (!b) return;
@@ -3636,8 +4486,8 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
       // (host-bound) batch setup, so the copy overlaps it; the pipeline
       // stream waits for it just before the run
       const size_t img_bytes = size_t(P) * npx * es;
-      char* dimg = nullptr;
-      {
+      char* dimg = k == 0 ? early.dimg : nullptr;
+      if (!dimg) {
         if (!ctx->copy) {
           ck(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
           ck(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
@@ -3653,7 +4503,7 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
       }
       mrb_batch* b = nullptr;
       stamp("create begin", k);
-      const bool grouped = wave > 0 && P > wave && !std::getenv("MESHREG_B200_NO_GROUPS");
+      const bool grouped = wave > 0 && P > wave && !no_groups;
       int rc = batch_create_impl(sc, P, meshes + p0, W, H, img_dtype, cfg, forced_cs, forced_npt,
                                  &b, grouped && defer ? wave : 0);
       stamp("create end", k);
@@ -3661,16 +4511,23 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
         cs = b->cluster_cs;
         npt = b->cluster_npt;
       }
-      // unconditionally: the stream-ordered free of dimg below must follow
-      // the H2D into it even when the batch could not be created
-      cudaStreamWaitEvent(sc->stream, ctx->copy_done, 0);
+      // chunk 0's per-group image events go to the batch (its run waits for
+      // them); otherwise the run waits for all images
+      const bool group_images = k == 0 && early.ev.size() > 1;
+      if (!group_images) cudaStreamWaitEvent(sc->stream, ctx->copy_done, 0);
       if (rc == MRB_OK) rc = mrb_batch_set_images(b, dimg, dimg + img_bytes, 1);
       if (rc == MRB_OK && grouped) {
         try {
           batch_set_groups(b, wave);
         } catch (const CudaError& e) {
-          rc = cuda_fail(sc, e.e);
+          rc = cuda_fail(sc, e.e, e.line);
         }
+      }
+      if (group_images) {  // only the fp32 fast path pads per group (enqueue_run)
+        if (rc == MRB_OK && b->cluster_cs && !b->real_d && b->in_dtype == MRB_F32)
+          b->img_ev = early.ev;
+        else
+          cudaStreamWaitEvent(sc->stream, ctx->copy_done, 0);
       }
       cudaEvent_t ev_run[2] = {nullptr, nullptr};
       if (dbg && rc == MRB_OK) {
@@ -3682,7 +4539,10 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
         cudaEventRecord(ev_run[1], sc->stream);
         dbg_events.push_back({ev_run[0], ev_run[1]});
       }
-      cudaFreeAsync(dimg, sc->stream);  // stream-ordered: after the run consumed it
+      // stream-ordered free after the run consumed it; unconditionally after
+      // the H2D into it, even when the batch could not be created
+      if (group_images) cudaStreamWaitEvent(sc->stream, ctx->copy_done, 0);
+      if (dimg != early.dimg) cudaFreeAsync(dimg, sc->stream);  // chunk 0's are kept
       if (rc == MRB_OK) {
         auto off = [&](void* base) -> void* {
           return base ? static_cast<char*>(base) + size_t(p0) * npx * os : nullptr;
@@ -3710,7 +4570,7 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
   } catch (const CudaError& e) {
     for (size_t j = 0; j < live.size(); ++j) harvest(j);
     if (setup_done) cudaEventDestroy(setup_done);
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
   for (size_t j = 0; j < live.size(); ++j) harvest(j);
   cudaEventDestroy(setup_done);
@@ -3801,7 +4661,7 @@ int mrb_warp_sample(mrb_ctx* ctx, int32_t W, int32_t H, int32_t dtype, const voi
     ck(mrb_copy_async(out, dout, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     ck(cudaStreamSynchronize(ctx->stream));
   } catch (const CudaError& e) {
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
   return MRB_OK;
 }
@@ -3815,6 +4675,7 @@ int unit_eval(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int32_t dtype,
               double* grad) {
   if (W < 2 || H < 2)
     return fail(ctx, MRB_E_VALUE, "bicubic sampling needs an image of at least 2x2 pixels");
+  if (const int rc = host_ready(ctx, &mesh, 1)) return rc;
   try {
     ck(cudaSetDevice(ctx->device));
     HostMesh& h = mesh->h;
@@ -3894,7 +4755,7 @@ int unit_eval(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, int32_t dtype,
     }
     ck(cudaStreamSynchronize(s));
   } catch (const CudaError& e) {
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
   return MRB_OK;
 }
@@ -3950,7 +4811,7 @@ int mrb_smooth_csr(mrb_ctx* ctx, int64_t n, const int64_t* indptr, const int64_t
     ck(mrb_copy_async(out, res, n * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
     ck(cudaStreamSynchronize(ctx->stream));
   } catch (const CudaError& e) {
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
   return MRB_OK;
 }
@@ -3987,13 +4848,14 @@ int mrb_step_csr(mrb_ctx* ctx, int64_t n, const int64_t* indptr, const int64_t* 
     ck(mrb_copy_async(out, res, n * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
     ck(cudaStreamSynchronize(ctx->stream));
   } catch (const CudaError& e) {
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
   return MRB_OK;
 }
 
 int mrb_densify(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, const double* u, double* ux,
                 double* uy) {
+  if (const int rc = host_ready(ctx, &mesh, 1)) return rc;
   try {
     AllocScope scope(ctx->stream);
     ck(cudaSetDevice(ctx->device));
@@ -4018,7 +4880,7 @@ int mrb_densify(mrb_ctx* ctx, mrb_mesh* mesh, int32_t W, int32_t H, const double
     ck(mrb_copy_async(uy, dy, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     ck(cudaStreamSynchronize(ctx->stream));
   } catch (const CudaError& e) {
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
   return MRB_OK;
 }
@@ -4045,7 +4907,7 @@ int mrb_warp_image(mrb_ctx* ctx, int32_t W, int32_t H, int32_t dtype, const void
     ck(mrb_copy_async(out, dout, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     ck(cudaStreamSynchronize(ctx->stream));
   } catch (const CudaError& e) {
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
   return MRB_OK;
 }
@@ -4065,7 +4927,7 @@ int mrb_msd(mrb_ctx* ctx, int64_t n, const double* a, const double* b, double* o
     ck(mrb_copy_async(out, dout, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     ck(cudaStreamSynchronize(ctx->stream));
   } catch (const CudaError& e) {
-    return cuda_fail(ctx, e.e);
+    return cuda_fail(ctx, e.e, e.line);
   }
   return MRB_OK;
 }

@@ -19,6 +19,7 @@ from . import _lib
 
 __all__ = [
     "TriMesh",
+    "DeferredMesh",
     "TriangleGeometry",
     "build_adjacency",
     "vertex_gradient_all",
@@ -164,10 +165,79 @@ class TriMesh:
 _foreign = weakref.WeakKeyDictionary()
 
 
+class DeferredMesh:
+    """A mesh whose per-mesh setup runs on the GPU (no reference counterpart).
+
+    ``DeferredMesh.create_many([(V, T), ...])`` (mrb_mesh_create_many) runs
+    only the checks of TriMesh.__init__ that need no connectivity (mesh.py:61-
+    86: finite coordinates, index range, repeated indices, degenerate area,
+    with the reference's messages) and the CCW reorientation.  The first
+    ``register_batch`` that runs the meshes on the fp32 cluster path builds
+    their connectivity, geometry, fused operator and fast-path topology on the
+    GPU, bit-identical to TriMesh's host build; every other use builds on the
+    host first, and a mesh the reference would reject (non-manifold edge,
+    valence < 2) raises the reference's ValueError there."""
+
+    def __init__(self):
+        raise TypeError("use DeferredMesh.create_many")
+
+    @classmethod
+    def create_many(cls, meshes):
+        arrs = [_mesh_arrays(V, T) for V, T in meshes]
+        k = len(arrs)
+        if k == 0:
+            return []
+        lib = _lib.load()
+        n = np.array([V.shape[0] for V, _ in arrs], np.int64)
+        m = np.array([T.shape[0] for _, T in arrs], np.int64)
+        Vp = (C.c_void_p * k)(*(V.ctypes.data for V, _ in arrs))
+        Tp = (C.c_void_p * k)(*(T.ctypes.data for _, T in arrs))
+        out = (C.c_void_p * k)()
+        bad = C.c_int32(-1)
+        err = C.create_string_buffer(512)
+        rc = lib.mrb_mesh_create_many(k, _lib.ptr(n), Vp, _lib.ptr(m), Tp, out, C.byref(bad),
+                                      err, 512)
+        if rc != _lib.OK:
+            raise ValueError(err.value.decode())
+        res = []
+        for (V, T), h in zip(arrs, out):
+            obj = cls.__new__(cls)
+            obj._h = h
+            obj._fin = weakref.finalize(obj, lib.mrb_mesh_destroy, h)
+            obj.vertices = V
+            obj.vertices.setflags(write=False)
+            obj._n, obj._m = V.shape[0], T.shape[0]
+            res.append(obj)
+        return res
+
+    @property
+    def n_vertices(self):
+        return self._n
+
+    @property
+    def n_triangles(self):
+        return self._m
+
+    def device_check(self, cluster_size, nodes_per_thread):
+        """Test hook (mrb_mesh_device_check): mismatch counts of the GPU build
+        against the host build, all zero when they are bit-identical."""
+        out = np.zeros(10, np.int64)
+        lib = _lib.load()
+        ctx = _lib.context()
+        rc = lib.mrb_mesh_device_check(ctx, self._h, int(cluster_size), int(nodes_per_thread),
+                                       _lib.ptr(out))
+        _lib.check(rc, ctx, (ValueError, RuntimeError, RuntimeError))
+        return out
+
+    def __repr__(self):
+        return f"DeferredMesh({self._n} vertices, {self._m} triangles)"
+
+
 def as_mesh(mesh):
-    """Accept this package's TriMesh or any object with .vertices/.triangles
-    (e.g. a reference meshreg.TriMesh); the native mesh is cached."""
-    if isinstance(mesh, TriMesh):
+    """Accept this package's TriMesh or DeferredMesh, or any object with
+    .vertices/.triangles (e.g. a reference meshreg.TriMesh); the native mesh
+    is cached."""
+    if isinstance(mesh, (TriMesh, DeferredMesh)):
         return mesh
     try:
         got = _foreign.get(mesh)
