@@ -236,9 +236,13 @@ def test_delaunay_violations_counts():
 def test_generate_mesh_full_size_matches_reference_mesher(cfg):
     """BASELINE configs 1-3: the mesh generate_mesh builds from the template
     equals, bit for bit, the one the reference mesher wrote (data/meshes,
-    tools/make_meshes.py; ~3k, 12k and 50k nodes)."""
+    tools/make_meshes.py; ~3k, 12k and 50k nodes).  The seed-0 meshes are
+    committed as tests/golden/refmesh_<cfg>_s0.npz (written by
+    tools/make_meshes.py with the reference package in the build container)."""
     from paper_1411_2141_b200.synthetic import CONFIGS, make_pair
-    path = os.path.join(ROOT, "data", "meshes", f"{cfg}_s0.npz")
+    path = os.path.join(ROOT, "tests", "golden", f"refmesh_{cfg}_s0.npz")
+    if not os.path.exists(path):
+        path = os.path.join(ROOT, "data", "meshes", f"{cfg}_s0.npz")
     if not os.path.exists(path):
         pytest.skip(f"{path} absent")
     ref = np.load(path)
