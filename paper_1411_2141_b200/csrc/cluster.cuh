@@ -88,6 +88,7 @@ struct ClusterPair {
   // (only those slots publish exchange words); null = publish every slot
   const uint32_t* exports;
   int tap_evict_first;        // k_grid_flags: L2 policy of the tap loads (see ld_row4_pol)
+  int rowpair;                // img4 in the row-pair layout (k_pad_planar_rp): grid path, images beyond L2
 };
 
 // Four copies of the padded (H+2)x(W+2) (Te, Re) image; copy s holds padded
@@ -126,6 +127,39 @@ __global__ void k_pad_planar4(const float* const* __restrict__ re, const float* 
     const float2 f = make_float2(float(vt), float(vr));
 #pragma unroll
     for (int s = 0; s < 4; ++s) dst[s * plane + size_t(r) * pitch + c + s] = f;
+  }
+}
+
+// Row-pair layout of the padded image for images that stream from DRAM (the
+// whole-GPU grid path beyond L2, C5): eight copies, x shift s = 0..3 and row
+// parity p = 0..1.  Padded element (r, c) of copy (s, p) sits at
+//   (2s + p) * plane + ((r + p) / 2) * 2 pitch + ((c + s) / 4) * 8 + ((r + p) % 2) * 4 + (c + s) % 4
+// so the 4-tap rows r and r+1 of a window (r + p even) fill one 64-byte
+// aligned block: a 4x4 window is exactly two 64-byte DRAM fetches (the four
+// 32-byte rows of the shifted layout cost four, half of each wasted).
+__device__ __forceinline__ size_t rp_index(int s, int p, int r, int c, int pitch, size_t plane) {
+  const int rr = r + p, cc = c + s;
+  return size_t(2 * s + p) * plane + size_t(rr >> 1) * (2 * size_t(pitch)) + size_t(cc >> 2) * 8 +
+         (rr & 1) * 4 + (cc & 3);
+}
+
+__global__ void k_pad_planar_rp(const float* const* __restrict__ re,
+                                const float* const* __restrict__ te, int W, int H,
+                                float2* __restrict__ out, int pitch, size_t plane,
+                                size_t out_stride) {
+  const int Wp = W + 2, Hp = H + 2;
+  const float* r_img = re[blockIdx.y];
+  const float* t_img = te[blockIdx.y];
+  float2* dst = out + blockIdx.y * out_stride;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Wp * Hp; q += gridDim.x * blockDim.x) {
+    const int r = q / Wp, c = q - r * Wp;
+    const double vt = ext_tap<float, double, 1>(t_img, W, H, r, c).v[0];
+    const double vr = ext_tap<float, double, 1>(r_img, W, H, r, c).v[0];
+    const float2 f = make_float2(float(vt), float(vr));
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+      for (int p = 0; p < 2; ++p) dst[rp_index(s, p, r, c, pitch, plane)] = f;
   }
 }
 
@@ -221,7 +255,7 @@ __device__ __forceinline__ void cr_weights_fma(float t, float w[4]) {
   w[3] = t2 * fmaf(0.5f, t, -0.5f);                // 0.5 (t^3 - t^2)
 }
 
-template <typename D>
+template <bool RP = false, typename D>
 __device__ __forceinline__ Window locate(const D& d, double x, double y) {
   const double xc = fmin(fmax(x, 0.0), double(d.W) - 1.0);
   const double yc = fmin(fmax(y, 0.0), double(d.H) - 1.0);
@@ -231,8 +265,17 @@ __device__ __forceinline__ Window locate(const D& d, double x, double y) {
   cr_weights_fma(float(xc - double(cx)), w.wx);
   cr_weights_fma(float(yc - double(cy)), w.wy);
   const int s = (4 - (cx & 3)) & 3;
-  w.base = d.img4 + size_t(s) * d.plane + size_t(cy) * d.pitch + cx + s;
+  if constexpr (RP)  // padded window rows cy..cy+3, columns cx..cx+3
+    w.base = d.img4 + rp_index(s, cy & 1, cy, cx, d.pitch, size_t(d.plane));
+  else
+    w.base = d.img4 + size_t(s) * d.plane + size_t(cy) * d.pitch + cx + s;
   return w;
+}
+
+// offset of window row j from Window::base
+template <bool RP>
+__device__ __forceinline__ size_t row_off(int pitch, int j) {
+  return RP ? size_t(j >> 1) * (2 * size_t(pitch)) + (j & 1) * 4 : size_t(j) * pitch;
 }
 
 __device__ __forceinline__ float2 combine(const Window& w, const float2 (&t)[4][4]) {
@@ -639,13 +682,22 @@ __global__ void __launch_bounds__(kPixBlock)
                                      __dmul_rn(w[2], double(uc.y))));
     d.ux[q] = rx;
     d.uy[q] = ry;
-    const Window win = locate(d, double(x) + double(rx), double(y) + double(ry));
     float2 tap[4][4];
+    Window win;
+    float2 own;  // (Te, Re) at the pixel: padded (y + 1, x + 1) of copy 0
+    if (d.rowpair) {
+      win = locate<true>(d, double(x) + double(rx), double(y) + double(ry));
 #pragma unroll
-    for (int row = 0; row < 4; ++row) ld_row4(win.base + size_t(row) * d.pitch, tap[row]);
+      for (int row = 0; row < 4; ++row) ld_row4(win.base + row_off<true>(d.pitch, row), tap[row]);
+      own = __ldg(d.img4 + rp_index(0, 0, y + 1, x + 1, d.pitch, size_t(d.plane)));
+    } else {
+      win = locate(d, double(x) + double(rx), double(y) + double(ry));
+#pragma unroll
+      for (int row = 0; row < 4; ++row) ld_row4(win.base + size_t(row) * d.pitch, tap[row]);
+      own = __ldg(d.img4 + size_t(y + 1) * d.pitch + (x + 1));
+    }
     const float wv = combine(win, tap).x;
     d.warped[q] = wv;
-    const float2 own = __ldg(d.img4 + size_t(y + 1) * d.pitch + (x + 1));  // (Te, Re) at p
     const double d0 = double(own.x) - double(own.y);
     const double d1 = double(wv) - double(own.y);
     acc.x = d0 * d0;

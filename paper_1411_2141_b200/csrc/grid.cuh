@@ -359,7 +359,7 @@ __device__ __forceinline__ unsigned flag_acquire(const unsigned* f) {
 //     rolled back to the one the reference returns (u before step k+1).  Four
 //     buffers: a CTA writing buffer k & 3 again at k+4 has waited for all
 //     partials of k+2, so every CTA finished control(k).
-template <int NPT>
+template <int NPT, bool RP = false>  // RP: taps in the row-pair layout (k_pad_planar_rp)
 __global__ void __launch_bounds__(kClusterThreads, kClusterMinBlocks)
     k_grid_flags(const ClusterPair* __restrict__ pairs, PairStatus* __restrict__ st, int max_iter,
                  double tol, float tau, float lam, int passes) {
@@ -519,11 +519,12 @@ __global__ void __launch_bounds__(kClusterThreads, kClusterMinBlocks)
           const int slot = t + j * kClusterThreads;
           const int nd = rank * d.chunk + slot;
           const double2 V = __ldg(d.V + nd);
-          const Window w = locate(d, V.x + double(u[j].x), V.y + double(u[j].y));
           float2 tap[4][4];
+          Window w;
+          w = locate<RP>(d, V.x + double(u[j].x), V.y + double(u[j].y));
 #pragma unroll
-          for (int row = 0; row < 4; ++row)
-            ld_row4_pol(w.base + size_t(row) * d.pitch, tap[row], tap_pol);
+          for (int row = 0; row < 4; ++row)  // row-pair layout: two 64-byte blocks per window
+            ld_row4_pol(w.base + row_off<RP>(d.pitch, row), tap[row], tap_pol);
           const float2 s = combine(w, tap);
           const float rj = s.x - s.y;
           set_r(j, rj);

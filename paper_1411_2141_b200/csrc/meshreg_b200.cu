@@ -1785,6 +1785,9 @@ struct mrb_batch {
   size_t cluster_smem = 0;
   int pad_pitch = 0;
   size_t pad_plane = 0;
+  int pad_copies = 4;       // 4 shifted copies, or 8 in the row-pair layout
+  bool pad_rowpair = false;  // k_pad_planar_rp layout (grid path, images beyond L2)
+  bool tap_evict_first = false;
   void* cpairs = nullptr;     // ClusterPair[n_pairs]
   std::vector<unsigned char> pairs_host;  // host copy of the PairDev array
   long long* phase_prof = nullptr;  // MESHREG_B200_PROFILE_PHASES
@@ -2082,7 +2085,10 @@ void launch_grid_t(mrb_batch* b, int p) {
   attr[0].val.cooperative = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  ck(cudaLaunchKernelEx(&lc, b->grid_flags ? k_grid_flags<NPT> : k_grid_register<NPT>,
+  ck(cudaLaunchKernelEx(&lc,
+                        !b->grid_flags   ? k_grid_register<NPT>
+                        : b->pad_rowpair ? k_grid_flags<NPT, true>
+                                         : k_grid_flags<NPT, false>,
                         static_cast<const ClusterPair*>(b->cpairs) + p, b->st + p,
                         int(b->cfg.max_iterations), double(b->cfg.energy_tolerance),
                         float(b->cfg.tau), float(b->cfg.lam), int(b->cfg.smoothing_passes)));
@@ -2268,12 +2274,17 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
       // then the fused dense pass
       const size_t npad = size_t(b->W + 2) * (b->H + 2);
       auto pad = [&](int p0, int p1, cudaStream_t st_) {
-        k_pad_planar4<<<dim3(unsigned(std::min<size_t>((npad + 255) / 256, 1024)), p1 - p0), 256,
-                        0, st_>>>(reinterpret_cast<const float* const*>(b->src_ptrs) + p0,
-                                  reinterpret_cast<const float* const*>(b->src_ptrs + b->n_pairs) +
-                                      p0,
-                                  b->W, b->H, b->img_pad + size_t(p0) * 4 * b->pad_plane,
-                                  b->pad_pitch, b->pad_plane, 4 * b->pad_plane);
+        const dim3 grid(unsigned(std::min<size_t>((npad + 255) / 256, 1024)), unsigned(p1 - p0));
+        const float* const* re = reinterpret_cast<const float* const*>(b->src_ptrs) + p0;
+        const float* const* te =
+            reinterpret_cast<const float* const*>(b->src_ptrs + b->n_pairs) + p0;
+        const size_t per = size_t(b->pad_copies) * b->pad_plane;
+        if (b->pad_rowpair)
+          k_pad_planar_rp<<<grid, 256, 0, st_>>>(re, te, b->W, b->H, b->img_pad + p0 * per,
+                                                 b->pad_pitch, b->pad_plane, per);
+        else
+          k_pad_planar4<<<grid, 256, 0, st_>>>(re, te, b->W, b->H, b->img_pad + p0 * per,
+                                               b->pad_pitch, b->pad_plane, per);
         ++launches;
       };
       const bool grouped_run = b->groups.size() > 2 && tm == &dummy && b->runs == 0;
@@ -2838,9 +2849,23 @@ void build_fast_descriptors(mrb_batch* b) {
   const int cs = b->cluster_cs;
   b->pad_pitch = (b->W + 5 + 3) / 4 * 4;
   b->pad_plane = size_t(b->H + 2) * b->pad_pitch;
-  // columns of a copy that k_pad_planar4 does not write are never read
+  // taps evict_first when the four image copies exceed half of L2 (C5); the
+  // whole-GPU grid path then streams the taps from DRAM and reads them in the
+  // row-pair layout (one 64-byte fetch per two tap rows instead of one per
+  // row; MESHREG_B200_TAP_LAYOUT=shifted keeps the four shifted copies)
+  b->tap_evict_first = 4 * b->pad_plane * sizeof(float2) > device_l2_bytes() / 2;
   {
-    const size_t need = 4 * b->pad_plane * b->n_pairs;
+    const char* lay = std::getenv("MESHREG_B200_TAP_LAYOUT");
+    b->pad_rowpair = b->grid_mode && b->grid_flags && b->tap_evict_first &&
+                     !(lay && std::string(lay) == "shifted");
+  }
+  if (b->pad_rowpair) {
+    b->pad_copies = 8;
+    b->pad_plane = size_t((b->H + 2) / 2 + 1) * 2 * b->pad_pitch;
+  }
+  // columns of a copy that the pad kernel does not write are never read
+  {
+    const size_t need = size_t(b->pad_copies) * b->pad_plane * b->n_pairs;
     if (b->forced_cs) {  // mrb_register_many: its batches on a context run in turn
       b->img_pad = static_cast<float2*>(kept_buffer(b->ctx, kKeptPad, need * sizeof(float2)));
       b->img_pad_borrowed = true;
@@ -2866,7 +2891,8 @@ void build_fast_descriptors(mrb_batch* b) {
     c.g_self = h.dev->g_self_f;
     c.inv_val = h.dev->inv_val_f;
     set_topology(c, t);
-    c.img4 = b->img_pad + 4 * b->pad_plane * p;
+    c.img4 = b->img_pad + size_t(b->pad_copies) * b->pad_plane * p;
+    c.rowpair = b->pad_rowpair;
     c.tri_of = host[p].tri_of;
     c.tri = host[p].tri;
     c.ux = host[p].ux;
@@ -2907,11 +2933,7 @@ void build_fast_descriptors(mrb_batch* b) {
     c.bar = nullptr;
     c.flags = nullptr;
     c.exports = nullptr;
-    {
-      // taps evict_first when the four image copies exceed half of L2 (C5)
-      const size_t img_bytes = 4 * b->pad_plane * sizeof(float2);
-      c.tap_evict_first = img_bytes > device_l2_bytes() / 2;
-    }
+    c.tap_evict_first = b->tap_evict_first;
     if (b->grid_mode && b->grid_flags && !b->xexports) {
       const int words = kClusterThreads * b->cluster_npt / 32;
       b->xexports = dalloc<uint32_t>(size_t(b->n_pairs) * cs * words);
@@ -3015,9 +3037,12 @@ void setup_grid_path(mrb_batch* b, int64_t nmax) {
   // epoch-tagged exchange (no grid barrier) for at most one smoothing pass
   bool flags = b->cfg.smoothing_passes <= 1;
   int per_sm = 0;
+  auto fit2 = [&](auto k1, auto k2) { return std::min(fit(k1), fit(k2)); };  // both tap layouts
   if (flags)
-    per_sm = npt == 1 ? fit(k_grid_flags<1>) : npt == 2 ? fit(k_grid_flags<2>)
-             : npt == 4 ? fit(k_grid_flags<4>) : fit(k_grid_flags<8>);
+    per_sm = npt == 1   ? fit2(k_grid_flags<1, false>, k_grid_flags<1, true>)
+             : npt == 2 ? fit2(k_grid_flags<2, false>, k_grid_flags<2, true>)
+             : npt == 4 ? fit2(k_grid_flags<4, false>, k_grid_flags<4, true>)
+                        : fit2(k_grid_flags<8, false>, k_grid_flags<8, true>);
   if (per_sm < 1) {
     flags = false;
     smem = grid_dyn_smem(npt, hs, b->cfg.smoothing_passes >= 2, false);
