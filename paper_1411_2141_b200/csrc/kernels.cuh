@@ -564,6 +564,12 @@ __global__ void k_zero_state(typename V2<Real>::type* u, int n) {
 // one warp per triangle; lanes stride over the triangle's pixel bbox and keep
 // the lowest triangle id per pixel (atomicMin == ascending-order
 // assign-if-unassigned of the reference).
+// kRasterLanes threads per triangle: four triangles per warp, so the
+// per-triangle setup is shared by a quarter of a warp (a whole warp per
+// triangle left most lanes idle: a mesher triangle covers ~20 candidate
+// pixels).
+constexpr int kRasterLanes = 8;
+
 __device__ __forceinline__ void raster_triangle(const double2* __restrict__ V,
                                                 const int4* __restrict__ tri, int t, int lane,
                                                 int W, int H, int* __restrict__ tri_of) {
@@ -576,20 +582,42 @@ __device__ __forceinline__ void raster_triangle(const double2* __restrict__ V,
   const long long y0 = max((long long)ceil(__dsub_rn(mny, 1e-9)), 0LL);
   const long long y1 = min((long long)floor(__dadd_rn(mxy, 1e-9)), (long long)H - 1);
   if (x1 < x0 || y1 < y0) return;
-  const long long bw = x1 - x0 + 1;
-  const long long cnt = bw * (y1 - y0 + 1);
-  for (long long q = lane; q < cnt; q += 32) {
-    const long long py = y0 + q / bw, px = x0 + q % bw;
-    double w[3];
-    bary_rn(a, b, c, double(px), double(py), w);
-    if (fmin(fmin(w[0], w[1]), w[2]) >= -1e-9) atomicMin(tri_of + py * W + px, t);
+  // 32-bit bounding-box arithmetic (a 64-bit division per candidate pixel
+  // dominated this kernel)
+  const int bw = int(x1 - x0 + 1);
+  const int cnt = bw * int(y1 - y0 + 1);
+  // Classification by weights from one reciprocal (within a few ulp of the
+  // exactly rounded quotients): a pixel clearly inside (all > 1e-7) or
+  // clearly outside (one < -1e-7) of the reference's predicate min(w) >=
+  // -1e-9 is decided without the two divisions; only the band in between
+  // gets the exactly rounded weights (bary_rn, numpy's operation order).
+  const double d = __dsub_rn(__dmul_rn(__dsub_rn(b.x, a.x), __dsub_rn(c.y, a.y)),
+                             __dmul_rn(__dsub_rn(c.x, a.x), __dsub_rn(b.y, a.y)));
+  const double inv = 1.0 / d;
+  for (int q = lane; q < cnt; q += kRasterLanes) {
+    const int qy = q / bw;
+    const int py = int(y0) + qy, px = int(x0) + (q - qy * bw);
+    const double fx = double(px), fy = double(py);
+    const double n1 = __dsub_rn(__dmul_rn(__dsub_rn(b.x, fx), __dsub_rn(c.y, fy)),
+                                __dmul_rn(__dsub_rn(c.x, fx), __dsub_rn(b.y, fy)));
+    const double n2 = __dsub_rn(__dmul_rn(__dsub_rn(c.x, fx), __dsub_rn(a.y, fy)),
+                                __dmul_rn(__dsub_rn(a.x, fx), __dsub_rn(c.y, fy)));
+    const double w1 = n1 * inv, w2 = n2 * inv;
+    const double mn = fmin(fmin(w1, w2), (1.0 - w1) - w2);
+    bool inside = mn > 1e-7;
+    if (!inside && mn >= -1e-7) {  // near an edge: the exact weights decide
+      double w[3];
+      bary_rn(a, b, c, fx, fy, w);
+      inside = fmin(fmin(w[0], w[1]), w[2]) >= -1e-9;
+    }
+    if (inside) atomicMin(tri_of + size_t(py) * W + px, t);
   }
 }
 
 __global__ void k_raster(const double2* __restrict__ V, const int4* __restrict__ tri, int m,
                          int W, int H, int* __restrict__ tri_of) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (warp < m) raster_triangle(V, tri, warp, threadIdx.x & 31, W, H, tri_of);
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) / kRasterLanes;
+  if (t < m) raster_triangle(V, tri, t, threadIdx.x % kRasterLanes, W, H, tri_of);
 }
 
 // Many meshes in one launch (blockIdx.y = mesh): setup of a whole batch costs
@@ -605,9 +633,9 @@ struct RasterJobs {
 
 __global__ void k_raster_many(const RasterJobs jobs, int W, int H) {
   const int j = blockIdx.y;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (warp < jobs.m[j]) raster_triangle(jobs.V[j], jobs.tri[j], warp, threadIdx.x & 31, W, H,
-                                        jobs.map[j]);
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) / kRasterLanes;
+  if (t < jobs.m[j])
+    raster_triangle(jobs.V[j], jobs.tri[j], t, threadIdx.x % kRasterLanes, W, H, jobs.map[j]);
 }
 
 __global__ void k_count_uncovered(const int* __restrict__ tri_of, int npx,

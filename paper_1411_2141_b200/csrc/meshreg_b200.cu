@@ -1578,7 +1578,7 @@ PixelMapJob issue_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes,
     const HostMesh& h = *job.todo[0];
     job.maps[0] = dalloc<int>(npx);
     ck(cudaMemsetAsync(job.maps[0], 0x7f, npx * sizeof(int), s));
-    k_raster<<<unsigned((h.m * 32 + 255) / 256), 256, 0, s>>>(h.dev->V, h.dev->tri, int(h.m), W, H,
+    k_raster<<<unsigned((h.m * kRasterLanes + 255) / 256), 256, 0, s>>>(h.dev->V, h.dev->tri, int(h.m), W, H,
                                                           job.maps[0]);
     k_count_uncovered<<<unsigned(std::min<size_t>((npx + 255) / 256, 1184)), 256, 0, s>>>(
         job.maps[0], int(npx), cnt);
@@ -1601,7 +1601,7 @@ PixelMapJob issue_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes,
         rj.m[j] = int(h.m);
         mmax = std::max(mmax, h.m);
       }
-      k_raster_many<<<dim3(unsigned((mmax * 32 + 255) / 256), unsigned(nj)), 256, 0, s>>>(rj, W, H);
+      k_raster_many<<<dim3(unsigned((mmax * kRasterLanes + 255) / 256), unsigned(nj)), 256, 0, s>>>(rj, W, H);
       k_count_uncovered_many<<<dim3(unsigned(std::min<size_t>((npx + 255) / 256, 296)),
                                     unsigned(nj)), 256, 0, s>>>(rj, int(npx), cnt + i0);
     }
@@ -2352,9 +2352,11 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
             cudaEventRecord(e, gs);
             b->dbg_group_ev.push_back(e);
           }
+          host_tick("run: group pads + topo");
           b->lstream = gs;
           launches += launch_cluster(b, p0, p1 - p0);
           b->lstream = nullptr;
+          host_tick("run: group launched");
           if (tail_side && g == ng - 2) {
             const int t0 = b->groups[ng - 1], t1 = b->groups[ng];
             ck(cudaEventRecord(b->tail_fork, gs));
@@ -4540,7 +4542,9 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
       // them); otherwise the run waits for all images
       const bool group_images = k == 0 && early.ev.size() > 1;
       if (!group_images) cudaStreamWaitEvent(sc->stream, ctx->copy_done, 0);
+      host_tick("many: create end");
       if (rc == MRB_OK) rc = mrb_batch_set_images(b, dimg, dimg + img_bytes, 1);
+      host_tick("many: set images");
       if (rc == MRB_OK && grouped) {
         try {
           batch_set_groups(b, wave);
@@ -4559,7 +4563,9 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
         for (auto& e : ev_run) cudaEventCreate(&e);
         cudaEventRecord(ev_run[0], sc->stream);
       }
+      host_tick("many: groups");
       if (rc == MRB_OK) rc = mrb_batch_run(b);
+      host_tick("many: run enqueued");
       if (dbg && ev_run[1]) {
         cudaEventRecord(ev_run[1], sc->stream);
         dbg_events.push_back({ev_run[0], ev_run[1]});
