@@ -77,6 +77,9 @@ struct mrb_ctx {
     void* p = nullptr;
     size_t cap = 0;
   } kept[5];  // see KeptSlot
+  // side streams of this context's batches (wave groups, tail wave, topology
+  // copies): created once; a stream creation costs ~0.1 ms of host time
+  cudaStream_t side[3] = {nullptr, nullptr, nullptr};
 };
 
 enum KeptSlot { kKeptPad, kKeptDense, kKeptState, kKeptImages, kKeptVT };
@@ -234,6 +237,12 @@ T* dalloc(size_t n) {
   else
     ck(cudaMalloc(&p, n * sizeof(T)));
   return static_cast<T*>(p);
+}
+
+// side stream `which` of the context (0 wave groups, 1 tail wave, 2 copies)
+cudaStream_t side_stream(mrb_ctx* ctx, int which) {
+  if (!ctx->side[which]) ck(cudaStreamCreateWithFlags(&ctx->side[which], cudaStreamNonBlocking));
+  return ctx->side[which];
 }
 
 // A kept buffer of the context (grows; stream-ordered on ctx->stream, or
@@ -1536,7 +1545,7 @@ struct PixelMapJob {
 // ctx->stream, so a run enqueued on ctx->stream need not wait for them (its
 // dense passes wait for job.done instead)
 PixelMapJob issue_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, int W, int H,
-                             bool side = false) {
+                             bool side = false, cudaEvent_t after = nullptr) {
   PixelMapJob job;
   job.W = W;
   job.H = H;
@@ -1548,8 +1557,12 @@ PixelMapJob issue_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes,
       ck(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
       ck(cudaEventCreateWithFlags(&ctx->aux_ev, cudaEventDisableTiming));
     }
-    ck(cudaEventRecord(ctx->aux_ev, ctx->stream));  // meshes uploaded
-    ck(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev, 0));
+    if (after) {  // the meshes are ready at `after` (device build)
+      ck(cudaStreamWaitEvent(ctx->aux, after, 0));
+    } else {
+      ck(cudaEventRecord(ctx->aux_ev, ctx->stream));  // meshes uploaded
+      ck(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev, 0));
+    }
     s = ctx->aux;
   }
   AllocScope scope(s);
@@ -1620,6 +1633,22 @@ PixelMapJob issue_pixel_maps(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes,
   ck(cudaEventCreateWithFlags(&job.done, cudaEventDisableTiming));
   ck(cudaEventRecord(job.done, s));
   return job;
+}
+
+// rasters issued early by mrb_register_many (its device setup), handed to
+// chunk 0's batch creation on this thread
+inline thread_local PixelMapJob* t_early_pm = nullptr;
+
+// a batch whose maps the early rasters already installed takes over their
+// job (event + uncovered counts): its dense passes wait for them and its
+// coverage check covers them
+void adopt_early_rasters(PixelMapJob& pmj, int W, int H) {
+  if (!pmj.todo.empty() || !t_early_pm || t_early_pm->todo.empty() || t_early_pm->W != W ||
+      t_early_pm->H != H)
+    return;
+  pmj = std::move(*t_early_pm);
+  t_early_pm->todo.clear();
+  t_early_pm->done = nullptr;
 }
 
 std::string finish_pixel_maps(mrb_ctx* ctx, PixelMapJob& job) {
@@ -1795,6 +1824,7 @@ struct mrb_batch {
   float2* img_pad = nullptr;  // 4 shifted padded (H+2)x(W+2) (Te, Re) copies per pair
   bool img_pad_borrowed = false;  // ctx kept buffers (mrb_register_many batches)
   bool pairs_borrowed = false;    // state + dense from the ctx kept buffers
+  size_t state_bytes = 0;
   int runs = 0;
   // host results
   std::vector<PairStatus> h_st;
@@ -1818,20 +1848,11 @@ struct mrb_batch {
     for (cudaEvent_t e : group_ev) cudaEventDestroy(e);
     if (topo_ev) cudaEventDestroy(topo_ev);
     for (cudaEvent_t e : dbg_group_ev) cudaEventDestroy(e);
-    if (copy_stream) {
-      cudaStreamSynchronize(copy_stream);
-      cudaStreamDestroy(copy_stream);
-    }
-    if (tail_stream) {
-      cudaStreamSynchronize(tail_stream);
-      cudaStreamDestroy(tail_stream);
-    }
+    if (copy_stream) cudaStreamSynchronize(copy_stream);  // context-owned streams
+    if (tail_stream) cudaStreamSynchronize(tail_stream);
     if (tail_fork) cudaEventDestroy(tail_fork);
     if (tail_join) cudaEventDestroy(tail_join);
-    if (grp_stream) {
-      cudaStreamSynchronize(grp_stream);
-      cudaStreamDestroy(grp_stream);
-    }
+    if (grp_stream) cudaStreamSynchronize(grp_stream);
     if (grp_fork) cudaEventDestroy(grp_fork);
     if (grp_join) cudaEventDestroy(grp_join);
     void* ptrs[] = {pairs, st, blk_pair, pix_blk_pair, partials, pix_partials,
@@ -1884,6 +1905,7 @@ void build_pairs(mrb_batch* b) {
     b->state = dalloc<char>(state_bytes);
     b->dense = dalloc<Real>(3 * npx * b->n_pairs);
   }
+  b->state_bytes = state_bytes;
   host_tick("pairs: state + dense");
   int blk = 0, pblk = 0;
   std::vector<int> bp, pbp;
@@ -2306,7 +2328,7 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
         const bool tail_side = !b->grid_mode && ng >= 2 &&
                                b->groups[ng - 1] >= b->tail_p0 && b->tail_p0 < b->n_pairs;
         if (tail_side && !b->tail_stream) {
-          ck(cudaStreamCreateWithFlags(&b->tail_stream, cudaStreamNonBlocking));
+          b->tail_stream = side_stream(b->ctx, 1);
           ck(cudaEventCreateWithFlags(&b->tail_fork, cudaEventDisableTiming));
           ck(cudaEventCreateWithFlags(&b->tail_join, cudaEventDisableTiming));
         }
@@ -2323,7 +2345,7 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
           launches += 2;
         };
         if (!b->grp_stream) {
-          ck(cudaStreamCreateWithFlags(&b->grp_stream, cudaStreamNonBlocking));
+          b->grp_stream = side_stream(b->ctx, 0);
           ck(cudaEventCreateWithFlags(&b->grp_fork, cudaEventDisableTiming));
           ck(cudaEventCreateWithFlags(&b->grp_join, cudaEventDisableTiming));
         }
@@ -2395,7 +2417,7 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
         const PD* host = reinterpret_cast<const PD*>(b->pairs_host.data());
         const int tb = host[b->tail_p0].pix_blk_begin;
         if (!b->tail_stream) {
-          ck(cudaStreamCreateWithFlags(&b->tail_stream, cudaStreamNonBlocking));
+          b->tail_stream = side_stream(b->ctx, 1);
           ck(cudaEventCreateWithFlags(&b->tail_fork, cudaEventDisableTiming));
           ck(cudaEventCreateWithFlags(&b->tail_join, cudaEventDisableTiming));
         }
@@ -2488,15 +2510,10 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
 
 template <typename TapT, typename Real>
 void enqueue_zero_u(mrb_batch* b) {
-  // u = 0 for every pair (solver.py:168); u is the first slab of each pair's
-  // state (layout of build_pairs), so this is one memset node per pair
-  using R2 = typename V2<Real>::type;
-  size_t off = 0;
-  for (int p = 0; p < b->n_pairs; ++p) {
-    const size_t n = size_t(b->meshes[p]->h.n);
-    ck(cudaMemsetAsync(static_cast<char*>(b->state) + off, 0, n * sizeof(R2), b->ctx->stream));
-    off += (3 * n * sizeof(R2) + 2 * n * sizeof(Real) + 255) / 256 * 256;
-  }
+  // u = 0 for every pair (solver.py:168): u is the first slab of each pair's
+  // state (layout of build_pairs); the rest is scratch, so one memset of the
+  // whole state (one API call instead of one per pair)
+  ck(cudaMemsetAsync(b->state, 0, b->state_bytes, b->ctx->stream));
 }
 
 template <typename TapT, typename Real>
@@ -3209,6 +3226,11 @@ int mrb_ctx_destroy(mrb_ctx* ctx) {
   if (ctx->build_in) cudaEventDestroy(ctx->build_in);
   for (auto& k : ctx->kept)
     if (k.p) cudaFree(k.p);
+  for (cudaStream_t st : ctx->side)
+    if (st) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
   delete ctx;
   return MRB_OK;
 }
@@ -3590,6 +3612,7 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
     const bool defer = eligible && defer_topo && mode == 1;
     if (!defer) {  // rasters run while the host plans the topologies
       pmj = issue_pixel_maps(ctx, hm, W, H);
+      adopt_early_rasters(pmj, W, H);
       rasters_issued = true;
     }
     if (eligible) {
@@ -3640,10 +3663,11 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
           // rasters on the side stream: the first group's loop and topology
           // copy need not wait for them (its dense pass does)
           pmj = issue_pixel_maps(ctx, hm, W, H, true);
+          adopt_early_rasters(pmj, W, H);
           rasters_issued = true;
           if (!todo.empty()) {
             if (!b->copy_stream)
-              ck(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking));
+              b->copy_stream = side_stream(ctx, 2);
             ck(cudaStreamWaitEvent(b->copy_stream, slab_ev, 0));
             cudaEventDestroy(slab_ev);
             flush_topo(b.get(), std::min(defer_topo, n_pairs), b->copy_stream, ctx->stream);
@@ -3654,7 +3678,10 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
       }
       tick("topologies");
     }
-    if (!rasters_issued) pmj = issue_pixel_maps(ctx, hm, W, H);
+    if (!rasters_issued) {
+      pmj = issue_pixel_maps(ctx, hm, W, H);
+      adopt_early_rasters(pmj, W, H);
+    }
     b->total_nodes = off;
     const size_t npx = size_t(W) * H;
     host_tick("batch: before buffers");
@@ -3908,7 +3935,7 @@ void batch_set_groups(mrb_batch* b, int per) {
   b->groups.push_back(b->n_pairs);
   b->group_ev.resize(b->groups.size());
   for (auto& e : b->group_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  if (!b->copy_stream) ck(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking));
+  if (!b->copy_stream) b->copy_stream = side_stream(b->ctx, 2);
 }
 }  // namespace
 
@@ -4261,6 +4288,16 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
   // GPU (meshbuild.cuh) when the batch takes the fp32 cluster fast path; any
   // other batch gets the host build first.
   bool dev_setup = false;
+  PixelMapJob early_pm;  // rasters of the device setup (chunk 0's batch adopts them)
+  struct EarlyPmScope {
+    PixelMapJob* prev;
+    PixelMapJob* job;
+    explicit EarlyPmScope(PixelMapJob* j) : prev(t_early_pm), job(j) { t_early_pm = j; }
+    ~EarlyPmScope() {
+      t_early_pm = prev;
+      if (job->done) cudaEventDestroy(job->done);  // neither adopted nor finished (error)
+    }
+  } early_pm_scope(&early_pm);
   {
     bool any = false, fits = true;
     for (int p = 0; p < n_pairs; ++p) {
@@ -4400,6 +4437,16 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
       }
       const std::string e = device_build_finish(ctx);
       if (!e.empty()) return fail(ctx, MRB_E_VALUE, e);
+      {  // pixel maps: rasters on the side stream now, beside the topology
+         // writes and the host's batch setup (chunk 0's batch adopts them)
+        std::vector<HostMesh*> all_h;
+        bool built = true;
+        for (int p = 0; p < n_pairs; ++p) {
+          all_h.push_back(&meshes[p]->h);
+          built = built && meshes[p]->h.dev;
+        }
+        if (built) early_pm = issue_pixel_maps(ctx, all_h, W, H, true, ctx->build_ev);
+      }
       // the build arrays go back to the pool now (stream-ordered) for this
       // call's batch buffers; a later topology of another shape for these
       // meshes is planned on the host
@@ -4605,6 +4652,17 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
   }
   for (size_t j = 0; j < live.size(); ++j) harvest(j);
   cudaEventDestroy(setup_done);
+  if (!early_pm.todo.empty()) {  // early rasters no batch took over: check them here
+    try {
+      const std::string m = finish_pixel_maps(ctx, early_pm);
+      if (!m.empty() && first_err == MRB_OK) {
+        first_err = MRB_E_COVERAGE;
+        first_msg = m;
+      }
+    } catch (const CudaError& e) {
+      return cuda_fail(ctx, e.e, e.line);
+    }
+  }
   for (auto& e : dbg_events) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);

@@ -121,3 +121,30 @@ def test_register_batch_deferred_invalid_meshes():
     out = mrb.register_batch([re], [te], mrb.DeferredMesh.create_many([(V3, T)]), cfg,
                              precision="f32")
     assert isinstance(out[0], ValueError) and str(out[0]) == str(want3.value)
+
+
+def test_register_batch_deferred_coverage_error():
+    """A deferred mesh that leaves pixels uncovered: its pair raises
+    MeshCoverageError with the reference's message (densefield.py:176-182),
+    the other pairs of the batch register normally (the early rasters of the
+    device setup carry the coverage check)."""
+    g = golden("gen64")
+    h, w = g["re"].shape
+    re, te = mrb.ImageGrid(w, h, g["re"]), mrb.ImageGrid(w, h, g["te"])
+    V, T = g["V"], g["T_in"].astype(np.int64)
+    # a mesh of the upper half only
+    keep = V[T].max(axis=1)[:, 1] <= (h - 1) / 2
+    used = np.unique(T[keep])
+    remap = -np.ones(len(V), np.int64)
+    remap[used] = np.arange(len(used))
+    Vh, Th = V[used], remap[T[keep]]
+    cfg = mrb.SolverConfig(max_iterations=10)
+    with pytest.raises(mrb.MeshCoverageError) as want:
+        mrb.register(re, te, mrb.TriMesh(Vh, Th), cfg, precision="f32")
+    out = mrb.register_batch([re, re, re], [te, te, te],
+                             mrb.DeferredMesh.create_many([(V, T), (Vh, Th), (V, T)]), cfg,
+                             precision="f32")
+    assert isinstance(out[1], mrb.MeshCoverageError) and str(out[1]) == str(want.value)
+    u0, rep0 = mrb.register(re, te, mrb.TriMesh(V, T), cfg, precision="f32")
+    for k in (0, 2):
+        assert np.array_equal(out[k][0], u0)
