@@ -60,6 +60,7 @@ struct BuildJob {
   int* cnt;          // n
   int* inc_ptr;      // n+1
   int* inc_idx;      // 3m
+  unsigned char* cpos;  // 6m: ring position of the two other corners of each incident triangle
   int* valence;      // n
   int* ring_ptr;     // n+1
   int* ring_idx;     // ring_cap
@@ -284,19 +285,27 @@ __global__ void __cluster_dims__(kBuildCluster, 1, 1) __launch_bounds__(kBuildTh
       va = __dadd_rn(va, J.areas[tl[q]]);
     }
     J.varea[v] = va;
+    // neighbour id << 6 | origin (2 q + s: the s-th other corner of the q-th
+    // incident triangle): sorted, equal ids adjacent; the ring position of
+    // every origin (cpos) spares pass B a search per corner
     int nb[2 * kBuildMaxInc];
     int c = 0;
-    for (int q = 0; q < k; ++q)
+    for (int q = 0; q < k; ++q) {
+      int sidx = 0;
 #pragma unroll
       for (int x = 0; x < 3; ++x) {
         const int j = J.T[3 * tl[q] + x];
-        if (j != v) nb[c++] = j;
+        if (j != v) nb[c++] = j << 6 | (2 * q + sidx++);
       }
+    }
     insertion_sort(nb, c);
     int val = 0;
     for (int x = 0; x < c;) {
       int y = x;
-      while (y < c && nb[y] == nb[x]) ++y;
+      while (y < c && (nb[y] >> 6) == (nb[x] >> 6)) {
+        J.cpos[2 * size_t(b0) + (nb[y] & 63)] = (unsigned char)val;
+        ++y;
+      }
       if (y - x > 2) atomicOr(&s_flags, kBuildNonManifold);
       ++val;
       x = y;
@@ -389,17 +398,18 @@ __global__ void __cluster_dims__(kBuildCluster, 1, 1) __launch_bounds__(kBuildTh
     for (int q = q0; q < q1 && q1 - q0 <= kBuildMaxInc; ++q) {
       const int t = J.inc_idx[q];
       const double w = __ddiv_rn(J.areas[t], va);
+      const double* co = J.coeffs + 6 * size_t(t);
+      int sidx = 0;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const int j = J.T[3 * t + c];
-        const double cx = __dmul_rn(w, J.coeffs[6 * size_t(t) + 2 * c]);
-        const double cy = __dmul_rn(w, J.coeffs[6 * size_t(t) + 2 * c + 1]);
+        const double cx = __dmul_rn(w, co[2 * c]);
+        const double cy = __dmul_rn(w, co[2 * c + 1]);
         if (j == i) {
           sx = __dadd_rn(sx, cx);
           sy = __dadd_rn(sy, cy);
         } else {
-          int pos = 0;
-          while (pos < deg - 1 && ring[pos] != j) ++pos;
+          const int pos = min(int(J.cpos[2 * size_t(q) + sidx++]), max(deg - 1, 0));
           gx[pos] = __dadd_rn(gx[pos], cx);
           gy[pos] = __dadd_rn(gy[pos], cy);
         }

@@ -1001,8 +1001,8 @@ void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, cudaS
     b_off[i] = b_tot;  // build slab (kept: nb_ptr, nb_idx, g_nb)
     const size_t e2 = 3 * m + n;  // one-ring entries of a manifold mesh (2e <= 3m + n)
     b_tot += al256(m * 8) + al256(m * 48) + 3 * al256(n * 4) + 2 * al256((n + 1) * 4) +
-             al256(3 * m * 4) + 2 * al256(e2 * 4) + al256(n * 8) + al256((n + 1) * 4) +
-             al256(e2 * 16);
+             al256(3 * m * 4) + al256(6 * m) + 2 * al256(e2 * 4) + al256(n * 8) +
+             al256((n + 1) * 4) + al256(e2 * 16);
     key_off[i] = keys;
     keys += n;
   }
@@ -1071,6 +1071,7 @@ void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, cudaS
     J.inc_ptr = reinterpret_cast<int*>(take((n + 1) * 4));
     J.ring_ptr = reinterpret_cast<int*>(take((n + 1) * 4));
     J.inc_idx = reinterpret_cast<int*>(take(3 * m * 4));
+    J.cpos = take(6 * m);
     J.ring_cap = int(3 * m + n);
     J.ring_idx = reinterpret_cast<int*>(take(size_t(J.ring_cap) * 4));
     J.nb_idx = reinterpret_cast<int*>(take(size_t(J.ring_cap) * 4));
