@@ -447,18 +447,20 @@ def run_e2e(args, lib, ctx, pairs, cfg, W, H, world, dist, device):
     cnt = np.zeros(2, np.int64)
     res = {}
     setup_times = []
+    step_ms = {}
     mesh_in = [(np.ascontiguousarray(p[2], np.float64), np.ascontiguousarray(p[3], np.int64))
                for p in pairs]  # the mesher's arrays, as the caller holds them
     for variant in ("report", "dense"):
         dense = [d.data_ptr() for d in dense_h] if variant == "dense" else [None] * 3
         times, tot_iters, h2d, d2h = [], 0, 0, 0
-        for step in range(1 + steps):  # one untimed warm-up step
+        nwarm = max(1, args.warmup)  # untimed warm-up steps (the pool and caches settle)
+        for step in range(nwarm + steps):
             torch.cuda.synchronize()
             barrier(world, dist)
             lib.mrb_transfer_bytes(None, None, 1)
             t0 = time.perf_counter()
             handles = mesh_handles(lib, mesh_in, deferred=True)
-            if step and variant == "report":
+            if step >= nwarm and variant == "report":
                 setup_times.append(time.perf_counter() - t0)
             arr = (C.c_void_p * P)(*handles)
             rc = lib.mrb_register_many(ctx, P, arr, W, H, _lib.F32, re_h.data_ptr(),
@@ -469,7 +471,7 @@ def run_e2e(args, lib, ctx, pairs, cfg, W, H, world, dist, device):
             dt = time.perf_counter() - t0
             lib.mrb_transfer_bytes(cnt.ctypes.data, cnt[1:].ctypes.data, 1)
             check(lib, ctx, rc, "e2e register_many")
-            if step:
+            if step >= nwarm:
                 times.append(dt)
                 tot_iters += int(iters.sum())
                 h2d, d2h = int(cnt[0]), int(cnt[1])
@@ -478,6 +480,7 @@ def run_e2e(args, lib, ctx, pairs, cfg, W, H, world, dist, device):
         t = reduce_max(sum(times), world, dist, device)
         res[variant] = (pairqueue.job_throughput(float(npx) * tot_iters, t, world, device), t,
                         h2d, d2h, tot_iters)
+        step_ms[variant] = [round(1e3 * x, 3) for x in times]
     value, t, h2d, d2h, tot_iters = res["report"]
     ts = reduce_max(sum(setup_times), world, dist, device)
     dv, dt_, dh2d, dd2h, _ = res["dense"]
@@ -489,6 +492,7 @@ def run_e2e(args, lib, ctx, pairs, cfg, W, H, world, dist, device):
             "mesh_setup": "included: mrb_mesh_create_many on the host + GPU build in "
                           "mrb_register_many",
             "mesh_create_ms_per_step": round(1e3 * ts / steps, 3),
+            "step_ms": step_ms["report"],
             "value_with_mesh_setup": round(value, 3),
             "with_dense_outputs": {"value": round(dv, 3), "ms_per_step": round(1e3 * dt_ / steps, 3),
                                    "h2d_bytes_per_step": dh2d, "d2h_bytes_per_step": dd2h,

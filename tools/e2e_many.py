@@ -8,6 +8,7 @@ from paper_1411_2141_b200 import _lib
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 chunk = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 deferred = len(sys.argv) > 3 and sys.argv[3] == "dev"  # device mesh setup, timed
+report_only = len(sys.argv) > 4 and sys.argv[4] == "report"  # no dense outputs
 lib = _lib.load(); ctx = _lib.context(0)
 spec, _ = bench.workload_spec("c4")
 pairs = [bench.load_pair("c4", s) for s in range(P)]
@@ -26,7 +27,7 @@ for rep in range(3):
     t_mesh = time.perf_counter() - t0
     arr = (C.c_void_p * P)(*hs)
     rc = lib.mrb_register_many(ctx, P, arr, W, H, _lib.F32, re_h.data_ptr(), te_h.data_ptr(), C.byref(cfg), chunk, _lib.F32,
-                               u_h.data_ptr(), *(d.data_ptr() for d in dense), None, None, None, None, None, None, 0)
+                               u_h.data_ptr(), *((None,) * 3 if report_only else (d.data_ptr() for d in dense)), None, None, None, None, None, None, 0)
     print(f"rep {rep}: rc {rc} {1e3*(time.perf_counter()-t0):.1f} ms (mesh handles {1e3*t_mesh:.1f} ms)"
           + (f" ({lib.mrb_last_error(ctx).decode()})" if rc else ""), flush=True)
     for h in hs: lib.mrb_mesh_destroy(h)
