@@ -79,6 +79,8 @@ struct BuildJob {
   int* perm;
   float2* g_self_f;
   float* inv_val_f;
+  double2* g_self_d;  // fp64 self terms and 1/valence (k_cluster64), or null
+  double* inv_val_d;
   int* stats;        // [0] flags, [1] max valence, [2] nnz one-ring (2e)
 };
 
@@ -417,7 +419,12 @@ __global__ void __cluster_dims__(kBuildCluster, 1, 1) __launch_bounds__(kBuildTh
     }
     for (int r = 0; r < deg; ++r) J.g_nb[base + r] = make_double2(gx[r], gy[r]);
     J.g_self_f[k] = make_float2(__double2float_rn(sx), __double2float_rn(sy));
-    J.inv_val_f[k] = __double2float_rn(__ddiv_rn(1.0, double(max(deg, 1))));
+    const double iv = __ddiv_rn(1.0, double(max(deg, 1)));
+    J.inv_val_f[k] = __double2float_rn(iv);
+    if (J.g_self_d) {
+      J.g_self_d[k] = make_double2(sx, sy);
+      J.inv_val_d[k] = iv;
+    }
     J.Vn[k] = J.V[i];
   }
   for (int t = tid; t < m; t += nt)
@@ -436,6 +443,7 @@ struct TopoJob {
   // write pass (slab zeroed beforehand)
   uint16_t* codes;
   float2* g;
+  double2* g64;      // fp64 coefficients instead (k_cluster64 topologies), or null
   uint32_t* soff;
   uint32_t* halo;
   int* n_halo;
@@ -614,7 +622,10 @@ __global__ void __launch_bounds__(kTopoThreads) k_topo_write(const TopoJob* __re
                                              : uint16_t(J.slots + s_pos[topo_find(s_key, j)]);
       J.codes[at] = code;
       const double2 gq = J.g_nb[q];
-      J.g[at] = make_float2(__double2float_rn(gq.x), __double2float_rn(gq.y));
+      if (J.g64)
+        J.g64[at] = gq;
+      else
+        J.g[at] = make_float2(__double2float_rn(gq.x), __double2float_rn(gq.y));
     }
   }
 }

@@ -862,8 +862,9 @@ void write_topo(const HostMesh& h, int cs, const TopoHost& t, unsigned char* dst
 }
 
 // device arrays of a packed topology, carved out of one slab
+// f64: a k_cluster64 topology (double2 coefficients, its own cache key)
 DeviceMesh::Topo& install_topo(HostMesh& h, int npt, const TopoHost& th,
-                                     unsigned char* slab) {
+                                     unsigned char* slab, bool f64 = false) {
   DeviceMesh::Topo t;
   t.chunk = th.chunk;
   t.topo_stride = th.stride;
@@ -879,6 +880,11 @@ DeviceMesh::Topo& install_topo(HostMesh& h, int npt, const TopoHost& th,
   t.send = reinterpret_cast<uint32_t*>(slab + th.off[6]);
   t.n_send = reinterpret_cast<int*>(slab + th.off[7]);
   t.send_stride = th.sstride;
+  if (f64) {
+    t.g64 = reinterpret_cast<double2*>(t.g);
+    t.g = nullptr;
+    return h.dev->topo[topo_key(th.cs, th.chunk, 1, true)] = t;
+  }
   return h.dev->topo[topo_key(th.cs, th.chunk, npt)] = t;
 }
 
@@ -986,7 +992,9 @@ bool device_buildable(const HostMesh& h) {
   return h.deferred && h.dV && !h.dev && h.n >= 3 && h.n <= 16 * 2 * kClusterThreads;
 }
 
-void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, cudaStream_t copy) {
+// with64: also the fp64 self terms and 1/valence (the fp64 cluster path)
+void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, cudaStream_t copy,
+                         bool with64 = false) {
   if (todo.empty()) return;
   const size_t K = todo.size();
   // inputs: V (double2) and T (int3) per mesh, one pinned stage, one copy
@@ -996,8 +1004,9 @@ void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, cudaS
     const size_t n = size_t(todo[i]->n), m = size_t(todo[i]->m);
     in_off[i] = in_tot;
     in_tot += al256(n * 16) + al256(m * 12);
-    out_off[i] = out_tot;  // DeviceMesh slab: V, tri, perm, g_self_f, inv_val_f
-    out_tot += al256(n * 16) + al256(m * 16) + al256(n * 4) + al256(n * 8) + al256(n * 4);
+    out_off[i] = out_tot;  // DeviceMesh slab: V, tri, perm, g_self_f, inv_val_f (+ fp64)
+    out_tot += al256(n * 16) + al256(m * 16) + al256(n * 4) + al256(n * 8) + al256(n * 4) +
+               (with64 ? al256(n * 16) + al256(n * 8) : 0);
     b_off[i] = b_tot;  // build slab (kept: nb_ptr, nb_idx, g_nb)
     const size_t e2 = 3 * m + n;  // one-ring entries of a manifold mesh (2e <= 3m + n)
     b_tot += al256(m * 8) + al256(m * 48) + 3 * al256(n * 4) + 2 * al256((n + 1) * 4) +
@@ -1088,6 +1097,14 @@ void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, cudaS
     J.g_self_f = reinterpret_cast<float2*>(o + al256(n * 16) + al256(m * 16) + al256(n * 4));
     J.inv_val_f = reinterpret_cast<float*>(o + al256(n * 16) + al256(m * 16) + al256(n * 4) +
                                            al256(n * 8));
+    J.g_self_d = nullptr;
+    J.inv_val_d = nullptr;
+    if (with64) {
+      unsigned char* o64 = o + al256(n * 16) + al256(m * 16) + al256(n * 4) + al256(n * 8) +
+                           al256(n * 4);
+      J.g_self_d = reinterpret_cast<double2*>(o64);
+      J.inv_val_d = reinterpret_cast<double*>(o64 + al256(n * 16));
+    }
     J.stats = dstats + 4 * i;
   }
   unsigned char* pin = small_pinned(ctx, K * sizeof(BuildJob));
@@ -1141,6 +1158,8 @@ void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, cudaS
     d.perm = J.perm;
     d.g_self_f = J.g_self_f;
     d.inv_val_f = J.inv_val_f;
+    d.g_self_d = J.g_self_d;  // slab64 stays null: these live in the shared slab
+    d.inv_val_d = J.inv_val_d;
     d.max_deg = h.max_deg;
     d.b_nb_ptr = J.nb_ptr;
     d.b_nb_idx = J.nb_idx;
@@ -1180,7 +1199,7 @@ std::string device_build_finish(mrb_ctx* ctx) {
 // (k_topo_count, one sync for the sizes, k_topo_write, k_topo_send).
 // Returns false, installing nothing, when a mesh needs the host planner.
 bool device_cluster_topos(mrb_ctx* ctx, const std::vector<std::tuple<HostMesh*, int, int>>& req,
-                          cudaStream_t s) {
+                          cudaStream_t s, bool f64 = false) {
   struct Item {
     HostMesh* h;
     int npt;
@@ -1194,7 +1213,7 @@ bool device_cluster_topos(mrb_ctx* ctx, const std::vector<std::tuple<HostMesh*, 
     if (!h->dev || !h->dev->b_nb_ptr || cs < 1 || cs > 16 || kClusterThreads * npt > 4096)
       return false;
     const int chunk = int((h->n + cs - 1) / cs);
-    if (h->dev->topo.count(topo_key(cs, chunk, npt))) continue;
+    if (h->dev->topo.count(topo_key(cs, chunk, f64 ? 1 : npt, f64))) continue;
     bool dup = false;
     for (const Item& it : items)
       dup = dup || (it.h == h && it.th.cs == cs && it.npt == npt);
@@ -1263,7 +1282,7 @@ bool device_cluster_topos(mrb_ctx* ctx, const std::vector<std::tuple<HostMesh*, 
     t.hstride = (hs + 31) / 32 * 32;
     t.sstride = (ss + 31) / 32 * 32;
     const size_t n = size_t(items[k].h->n);
-    const size_t bytes[8] = {size_t(cs) * t.stride * 2, size_t(cs) * t.stride * 8,
+    const size_t bytes[8] = {size_t(cs) * t.stride * 2, size_t(cs) * t.stride * (f64 ? 16 : 8),
                              size_t(cs) * t.slices * 4, size_t(cs) * t.hstride * 4,
                              size_t(cs) * 4,           n,
                              size_t(cs) * t.sstride * 4, size_t(cs) * 4};
@@ -1290,6 +1309,7 @@ bool device_cluster_topos(mrb_ctx* ctx, const std::vector<std::tuple<HostMesh*, 
     TopoJob& J = jobs[k];
     J.codes = reinterpret_cast<uint16_t*>(slab + t.off[0]);
     J.g = reinterpret_cast<float2*>(slab + t.off[1]);
+    J.g64 = f64 ? reinterpret_cast<double2*>(slab + t.off[1]) : nullptr;
     J.soff = reinterpret_cast<uint32_t*>(slab + t.off[2]);
     J.halo = reinterpret_cast<uint32_t*>(slab + t.off[3]);
     J.n_halo = reinterpret_cast<int*>(slab + t.off[4]);
@@ -1314,7 +1334,8 @@ bool device_cluster_topos(mrb_ctx* ctx, const std::vector<std::tuple<HostMesh*, 
   dev_free(dstat, s);
   host_tick("topo: write enqueued");
   for (size_t k = 0; k < K; ++k)
-    install_topo(*items[k].h, items[k].npt, items[k].th, all.get() + items[k].base).hold = all;
+    install_topo(*items[k].h, items[k].npt, items[k].th, all.get() + items[k].base, f64).hold =
+        all;
   host_tick("topo: installed");
   return true;
 }
@@ -1454,6 +1475,15 @@ void ensure_cluster_topos64(mrb_ctx* ctx, const std::vector<HostMesh*>& meshes, 
       todo.push_back(h);
   }
   if (todo.empty()) return;
+  {  // device-built meshes: planned and written on the GPU
+    bool dev = true;
+    std::vector<std::tuple<HostMesh*, int, int>> req;
+    for (HostMesh* h : todo) {
+      dev = dev && h->dev->b_nb_ptr;
+      req.emplace_back(h, cs, 1);
+    }
+    if (dev && device_cluster_topos(ctx, req, ctx->stream, true)) return;
+  }
   std::vector<TopoHost> th(todo.size());
   parallel_for(todo.size(), [&](size_t i) {
     th[i] = plan_topo(*todo[i], cs, int((todo[i]->n + cs - 1) / cs), 1, 16);
@@ -3152,8 +3182,9 @@ std::string pair_message(const mrb_batch* b, int p, int* code) {
 // deferred handles reaching a host-side consumer: the full host build first
 // (the reference validates the whole mesh in TriMesh.__init__, mesh.py:58-123)
 int host_ready(mrb_ctx* ctx, mrb_mesh* const* meshes, int64_t count) {
+  parallel_for(size_t(count), [&](size_t k) { ensure_host(meshes[k]->h); });  // worker pool
   for (int64_t k = 0; k < count; ++k) {
-    const std::string& e = ensure_host(meshes[k]->h);
+    const std::string& e = ensure_host(meshes[k]->h);  // first failing mesh, in order
     if (!e.empty()) return fail(ctx, MRB_E_VALUE, e);
   }
   return MRB_OK;
@@ -3819,7 +3850,10 @@ void setup_cluster64(mrb_batch* b) {
   double best = 1e300;
   int best_cs = 0;
   size_t best_smem = 0;
-  for (int cs = cs_min; cs <= 16; ++cs) {
+  // mrb_register_many's device setup decides the cluster size (forced_cs)
+  const int cs_lo = b->forced_cs ? std::max(cs_min, b->forced_cs) : cs_min;
+  const int cs_hi = b->forced_cs ? cs_lo : 16;
+  for (int cs = cs_lo; cs <= cs_hi; ++cs) {
     ensure_cluster_topos64(b->ctx, hm, cs);
     size_t smem = 0;
     for (HostMesh* h : hm) {
@@ -4288,7 +4322,7 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
   // Deferred handles (mrb_mesh_create_many): the per-mesh setup runs on the
   // GPU (meshbuild.cuh) when the batch takes the fp32 cluster fast path; any
   // other batch gets the host build first.
-  bool dev_setup = false;
+  bool dev_setup = false, dev64 = false;  // dev64: the fp64 cluster path (k_cluster64)
   PixelMapJob early_pm;  // rasters of the device setup (chunk 0's batch adopts them)
   struct EarlyPmScope {
     PixelMapJob* prev;
@@ -4309,9 +4343,15 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
     }
     if (any) {
       std::vector<mrb_mesh*> all(meshes, meshes + n_pairs);
+      const char* penv = std::getenv("MESHREG_B200_PATH");
+      bool f64_ok = cfg->precision == MRB_PREC_F64 && !(penv && std::string(penv) == "generic");
+      for (int p = 0; p < n_pairs && f64_ok; ++p)  // k_cluster64's limits (cluster64_candidate)
+        f64_ok = meshes[p]->h.n <= 16 * kClusterThreads && meshes[p]->h.max_deg <= kMaxDeg;
+      const bool f32_ok =
+          cfg->precision == MRB_PREC_F32 && !cluster_ineligible(false, false, img_dtype, all);
       dev_setup = fits && !std::getenv("MESHREG_B200_HOST_SETUP") && config_error(cfg).empty() &&
-                  cfg->precision == MRB_PREC_F32 && img_dtype == MRB_F32 &&
-                  !cluster_ineligible(false, false, img_dtype, all);
+                  img_dtype == MRB_F32 && (f32_ok || f64_ok);
+      dev64 = dev_setup && f64_ok;
       if (!dev_setup) {
         if (const int rc = host_ready(ctx, meshes, n_pairs)) return rc;
       } else {
@@ -4328,7 +4368,7 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
             ck(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
           }
           // V / T go first on the copy stream, ahead of the images
-          device_build_meshes(ctx, todo, ctx->copy);
+          device_build_meshes(ctx, todo, ctx->copy, dev64);
           stamp("device mesh build enqueued", 0);
         } catch (const CudaError& e) {
           return cuda_fail(ctx, e.e, e.line);
@@ -4435,6 +4475,40 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
         }
         device_cluster_topos(ctx, req, ctx->stream);  // false: planned later (host)
         stamp("device topologies", 0);
+      } else if (dev64) {
+        // fp64 cluster size by setup_cluster64's cost model on the largest
+        // mesh (waves x nodes per CTA), then every mesh's topology of it
+        mrb_mesh* big = *std::max_element(meshes, meshes + n_pairs,
+                                          [](mrb_mesh* x, mrb_mesh* y) { return x->h.n < y->h.n; });
+        const int64_t nmax = big->h.n;
+        const int cs_min = int((nmax + kClusterThreads - 1) / kClusterThreads);
+        std::vector<std::tuple<HostMesh*, int, int>> cand;
+        for (int cs = cs_min; cs <= 16; ++cs) cand.emplace_back(&big->h, cs, 1);
+        if (device_cluster_topos(ctx, cand, ctx->stream, true)) {
+          double best = 1e300;
+          int best_cs = 0;
+          const bool two_u = cfg->smoothing_passes >= 2;
+          for (int cs = cs_min; cs <= 16; ++cs) {
+            const DeviceMesh::Topo& t =
+                big->h.dev->topo.at(topo64_key(cs, int((nmax + cs - 1) / cs)));
+            const int occ = cluster64_occupancy<1>(
+                cs, cluster64_dyn_smem(t.topo_stride, t.slices, t.halo_stride, two_u));
+            if (occ < 1) continue;
+            const double cost = double((n_pairs + occ - 1) / occ) * double((nmax + cs - 1) / cs);
+            if (cost < best) {
+              best = cost;
+              best_cs = cs;
+            }
+          }
+          if (best_cs) {
+            std::vector<std::tuple<HostMesh*, int, int>> req;
+            for (int p = 0; p < n_pairs; ++p) req.emplace_back(&meshes[p]->h, best_cs, 1);
+            device_cluster_topos(ctx, req, ctx->stream, true);
+            forced_cs = best_cs;  // setup_cluster64 takes it
+            forced_npt = 1;
+          }
+        }
+        stamp("device fp64 topologies", 0);
       }
       const std::string e = device_build_finish(ctx);
       if (!e.empty()) return fail(ctx, MRB_E_VALUE, e);

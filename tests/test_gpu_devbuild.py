@@ -64,9 +64,11 @@ def test_mesher_meshes_device_build():
             assert not mism.any(), (seed, cs, npt, mism.tolist())
 
 
-def test_register_batch_deferred_equals_trimesh():
-    """The golden pairs through DeferredMesh handles (device setup) and
-    through TriMesh (host setup): identical fields, reports and dense outputs."""
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_register_batch_deferred_equals_trimesh(precision):
+    """The golden pairs through DeferredMesh handles (device setup; fp64: the
+    fp64 self terms and double2 cluster topologies too) and through TriMesh
+    (host setup): identical fields, reports and dense outputs."""
     names = ["gen64", "plateau64", "gen64_x255", "gen96_tol", "c1", "gen64", "accept_c3"]
     res, tes, VT = [], [], []
     for n in names:
@@ -82,9 +84,9 @@ def test_register_batch_deferred_equals_trimesh():
         rr = [mrb.ImageGrid(W, H, res[k]) for k in idx]
         tt = [mrb.ImageGrid(W, H, tes[k]) for k in idx]
         host = mrb.register_batch(rr, tt, [mrb.TriMesh(*VT[k]) for k in idx], cfg,
-                                  precision="f32", return_dense=True)
+                                  precision=precision, return_dense=True)
         dev = mrb.register_batch(rr, tt, mrb.DeferredMesh.create_many([VT[k] for k in idx]),
-                                 cfg, precision="f32", return_dense=True)
+                                 cfg, precision=precision, return_dense=True)
         for a, b in zip(host, dev):
             assert type(a) is type(b)
             if isinstance(a, Exception):
