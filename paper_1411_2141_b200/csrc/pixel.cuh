@@ -338,16 +338,26 @@ __global__ void __launch_bounds__(kPixThreads, 2)
   __syncthreads();  // mbarrier initialised before anyone waits on it
   bool patch_ready = false;
   double e2 = 0.0;
+  // u of a region cell (zero outside the image); the next cell's u is loaded
+  // before this cell's sample so its latency overlaps the arithmetic
+  auto load_u = [&](int c) {
+    const int ry = c / RW, rx = c - ry * RW;
+    const int gx = gx0 + rx, gy = gy0 + ry;
+    return (c < RW * RH && gx >= 0 && gx < W && gy >= 0 && gy < H) ? uin[size_t(gy) * W + gx]
+                                                                   : R2{Real(0), Real(0)};
+  };
+  R2 u_next = load_u(threadIdx.x);
 #pragma unroll 1
   for (int c = threadIdx.x; c < RW * RH; c += kPixThreads) {
     const int ry = c / RW, rx = c - ry * RW;
     const int gx = gx0 + rx, gy = gy0 + ry;
+    const R2 u = u_next;
+    u_next = load_u(c + kPixThreads);
     if (gx < 0 || gx >= W || gy < 0 || gy >= H) {
       buf[0][c] = R2{Real(0), Real(0)};
       buf[1][c] = R2{Real(0), Real(0)};
       continue;
     }
-    const R2 u = uin[size_t(gy) * W + gx];
     if (!descend) {
       buf[0][c] = u;
       continue;
