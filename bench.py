@@ -451,13 +451,12 @@ def run_e2e(args, lib, ctx, pairs, cfg, W, H, world, dist, device):
     mesh_in = [(np.ascontiguousarray(p[2], np.float64), np.ascontiguousarray(p[3], np.int64))
                for p in pairs]  # the mesher's arrays, as the caller holds them
     # Deferred handles (per-mesh setup on the GPU inside mrb_register_many)
-    # where the cluster paths run: meshes of <= 16 x 2 x 768 nodes, and a
-    # single pair only below the whole-GPU grid threshold (6000 nodes).  The
-    # grid path (C2, C3, C5) builds its meshes on the host: they are built
-    # outside the timed region and that build is reported on its own, like
-    # the reference arm's TriMesh construction.
+    # wherever the device setup runs: every fp32 path (cluster and whole-GPU
+    # grid) and the fp64 cluster path (<= 16 x 768 nodes).  The fp64 generic
+    # loop builds its meshes on the host: outside the timed region, that
+    # build reported on its own, like the reference arm's TriMesh construction.
     nmax = max(len(p[2]) for p in pairs)
-    deferred = nmax <= 16 * 2 * 768 and (P > 1 or nmax < 6000)
+    deferred = args.precision == "f32" or nmax <= 16 * 768
     built_ms = []
     for variant in ("report", "dense"):
         dense = [d.data_ptr() for d in dense_h] if variant == "dense" else [None] * 3

@@ -41,7 +41,7 @@ constexpr int kBuildThreads = 512;
 constexpr int kBuildMaxInc = 24;  // incident triangles per vertex (else: host build)
 constexpr int kTopoThreads = 512;
 constexpr int kTopoHash = 2048;   // distinct remote nodes per CTA (else: host plan)
-constexpr int kTopoMaxSlices = 64;
+constexpr int kTopoMaxSlices = 256;  // 8192 slots per CTA (grid shapes: 768 x 8)
 
 enum BuildFlag : int {
   kBuildOverflow = 1,     // a vertex with more than kBuildMaxInc triangles

@@ -989,7 +989,7 @@ void upload_zero_copy(void* dst, const unsigned char* pinned, size_t bytes, cuda
 
 // a deferred mesh the device build takes (cluster-sized, not yet on a device)
 bool device_buildable(const HostMesh& h) {
-  return h.deferred && h.dV && !h.dev && h.n >= 3 && h.n <= 16 * 2 * kClusterThreads;
+  return h.deferred && h.dV && !h.dev && h.n >= 3;
 }
 
 // with64: also the fp64 self terms and 1/valence (the fp64 cluster path)
@@ -1210,7 +1210,8 @@ bool device_cluster_topos(mrb_ctx* ctx, const std::vector<std::tuple<HostMesh*, 
   for (const auto& r : req) {
     HostMesh* h = std::get<0>(r);
     const int cs = std::get<1>(r), npt = std::get<2>(r);
-    if (!h->dev || !h->dev->b_nb_ptr || cs < 1 || cs > 16 || kClusterThreads * npt > 4096)
+    // cluster shapes (<= 16 CTAs) and whole-GPU grid shapes (SMs CTAs, 768 x npt slots)
+    if (!h->dev || !h->dev->b_nb_ptr || cs < 1 || cs > 1024 || kClusterThreads * npt > 8192)
       return false;
     const int chunk = int((h->n + cs - 1) / cs);
     if (h->dev->topo.count(topo_key(cs, chunk, f64 ? 1 : npt, f64))) continue;
@@ -1258,7 +1259,9 @@ bool device_cluster_topos(mrb_ctx* ctx, const std::vector<std::tuple<HostMesh*, 
   std::memcpy(pin, jobs.data(), K * sizeof(TopoJob));
   TopoJob* djobs = dalloc<TopoJob>(K);
   upload_zero_copy(djobs, pin, K * sizeof(TopoJob), s);
-  k_topo_count<<<dim3(16, unsigned(K)), kTopoThreads, 0, s>>>(djobs);
+  int cs_max = 1;
+  for (const Item& it : items) cs_max = std::max(cs_max, it.th.cs);
+  k_topo_count<<<dim3(unsigned(cs_max), unsigned(K)), kTopoThreads, 0, s>>>(djobs);
   int* hstat = reinterpret_cast<int*>(pin + 2 * jb);
   ck(mrb_copy_async(hstat, dstat, stat_ints * 4, cudaMemcpyDeviceToHost, s));
   dev_mark(s, "  topology sizes");
@@ -1280,7 +1283,8 @@ bool device_cluster_topos(mrb_ctx* ctx, const std::vector<std::tuple<HostMesh*, 
     }
     t.stride = std::max((stride + 7) / 8 * 8, 8);
     t.hstride = (hs + 31) / 32 * 32;
-    t.sstride = (ss + 31) / 32 * 32;
+    // push send lists for cluster shapes only (plan_topo)
+    t.sstride = cs <= 16 && kClusterThreads * items[k].npt <= 4096 ? (ss + 31) / 32 * 32 : 0;
     const size_t n = size_t(items[k].h->n);
     const size_t bytes[8] = {size_t(cs) * t.stride * 2, size_t(cs) * t.stride * (f64 ? 16 : 8),
                              size_t(cs) * t.slices * 4, size_t(cs) * t.hstride * 4,
@@ -1325,9 +1329,9 @@ bool device_cluster_topos(mrb_ctx* ctx, const std::vector<std::tuple<HostMesh*, 
   upload_zero_copy(djobs, pin + jb, K * sizeof(TopoJob), s);
   dev_mark(s, "  topology jobs uploaded");
   ck(cudaEventRecord(ctx->small_ev, s));
-  k_topo_write<<<dim3(16, unsigned(K)), kTopoThreads, 0, s>>>(djobs);
+  k_topo_write<<<dim3(unsigned(cs_max), unsigned(K)), kTopoThreads, 0, s>>>(djobs);
   dev_mark(s, "  topology written");
-  k_topo_send<<<dim3(16, unsigned(K)), 256, 0, s>>>(djobs);
+  k_topo_send<<<dim3(unsigned(cs_max), unsigned(K)), 256, 0, s>>>(djobs);
   ck(cudaGetLastError());
   dev_mark(s, "device topologies done");
   dev_free(djobs, s);
@@ -4347,8 +4351,9 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
       bool f64_ok = cfg->precision == MRB_PREC_F64 && !(penv && std::string(penv) == "generic");
       for (int p = 0; p < n_pairs && f64_ok; ++p)  // k_cluster64's limits (cluster64_candidate)
         f64_ok = meshes[p]->h.n <= 16 * kClusterThreads && meshes[p]->h.max_deg <= kMaxDeg;
-      const bool f32_ok =
-          cfg->precision == MRB_PREC_F32 && !cluster_ineligible(false, false, img_dtype, all);
+      const char* why = nullptr;  // cluster (1) or whole-GPU grid (2) fp32 path
+      const bool f32_ok = cfg->precision == MRB_PREC_F32 &&
+                          fast_mode(false, false, img_dtype, all, &why) != 0;
       dev_setup = fits && !std::getenv("MESHREG_B200_HOST_SETUP") && config_error(cfg).empty() &&
                   img_dtype == MRB_F32 && (f32_ok || f64_ok);
       dev64 = dev_setup && f64_ok;
@@ -4475,6 +4480,21 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
         }
         device_cluster_topos(ctx, req, ctx->stream);  // false: planned later (host)
         stamp("device topologies", 0);
+      } else if (!dev64) {
+        // whole-GPU grid path (setup_grid_path): the grid shape of the
+        // largest mesh, every mesh's topology of it
+        std::vector<mrb_mesh*> all(meshes, meshes + n_pairs);
+        const char* why = nullptr;
+        if (fast_mode(false, false, img_dtype, all, &why) == 2) {
+          int64_t nmax = 0;
+          for (mrb_mesh* m : all) nmax = std::max<int64_t>(nmax, m->h.n);
+          int gcs = 0, gnpt = 0;
+          grid_shape(nmax, &gcs, &gnpt);
+          std::vector<std::tuple<HostMesh*, int, int>> req;
+          for (int p = 0; p < n_pairs; ++p) req.emplace_back(&meshes[p]->h, gcs, gnpt);
+          device_cluster_topos(ctx, req, ctx->stream);
+          stamp("device grid topologies", 0);
+        }
       } else if (dev64) {
         // fp64 cluster size by setup_cluster64's cost model on the largest
         // mesh (waves x nodes per CTA), then every mesh's topology of it

@@ -263,6 +263,10 @@ __device__ __forceinline__ void smooth_pass(const typename V2<Real>::type* __res
       const int gx = gx0 + rx, gy = gy0 + ry;
       if (gx < 0 || gx >= W || gy < 0 || gy >= H) continue;
       const R2 tot = add2(add2(add2(b[q - RW], b[q + RW]), b[q - 1]), b[q + 1]);
+      if (gx > 0 && gx < W - 1 && gy > 0 && gy < H - 1) {  // most cells of a border tile
+        o[q] = blend2(om, b[q], lq4, tot);
+        continue;
+      }
       const int cnt = (gy > 0) + (gy < H - 1) + (gx > 0) + (gx < W - 1);
       R2 v;
       if (cnt == 4) {

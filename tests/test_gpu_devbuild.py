@@ -15,7 +15,8 @@ from conftest import GOLDEN_CASES, golden
 
 pytestmark = pytest.mark.gpu
 
-SHAPES = [(1, 1), (2, 2), (4, 1), (9, 2), (16, 1), (16, 2)]
+# cluster shapes and whole-GPU grid shapes (148 CTAs, up to 8 nodes per thread)
+SHAPES = [(1, 1), (2, 2), (4, 1), (9, 2), (16, 1), (16, 2), (148, 1), (148, 4)]
 
 
 def perturbed_grid(k, seed):
