@@ -173,6 +173,82 @@ std::string create_mesh(int64_t n, const double* Vin, int64_t m, const int64_t* 
   return "";
 }
 
+void validate_part(int64_t n, const double* Vin, int64_t v0, int64_t v1, int64_t m,
+                   const int64_t* Tin, int64_t t0, int64_t t1, double* Vout, int32_t* Tout,
+                   int32_t* inc, ValidatePart& out) {
+  (void)m;
+  // locals, written to `out` once (neighbouring parts share cache lines)
+  ValidatePart p;
+  for (int64_t i = 2 * v0; i < 2 * v1; ++i) {
+    p.finite = p.finite && std::isfinite(Vin[i]);
+    store_nt(Vout + i, Vin[i]);
+  }
+  for (int64_t t = t0; t < t1; ++t) {
+    const int64_t* r = Tin + 3 * t;
+    if (uint64_t(r[0]) >= uint64_t(n) || uint64_t(r[1]) >= uint64_t(n) ||
+        uint64_t(r[2]) >= uint64_t(n)) {
+      p.range = true;
+      continue;
+    }
+    p.repeated = p.repeated || r[0] == r[1] || r[1] == r[2] || r[0] == r[2];
+    const double a2 = area2(Vin, r[0], r[1], r[2]);
+    const double ab = std::fabs(a2);
+    if (ab <= 2.0 * kDegenerateArea) p.bad = true;
+    if (ab < p.worst_abs) {  // np.argmin: first minimum (parts merged in order)
+      p.worst_abs = ab;
+      p.worst = t;
+    }
+    const bool flip = a2 < 0;
+    store_nt(Tout + 3 * t, int32_t(r[0]));
+    store_nt(Tout + 3 * t + 1, int32_t(flip ? r[2] : r[1]));
+    store_nt(Tout + 3 * t + 2, int32_t(flip ? r[1] : r[2]));
+    // incidence counts for the fast-path eligibility estimate: relaxed
+    // load + store, not a locked RMW (those ran 40x slower here); a count two
+    // parts bump at once may come out low, harmless for an estimate the
+    // device build replaces with the exact valence
+    for (int c = 0; c < 3; ++c) {
+      const int32_t v = __atomic_load_n(inc + r[c], __ATOMIC_RELAXED) + 1;
+      __atomic_store_n(inc + r[c], v, __ATOMIC_RELAXED);
+      p.max_inc = std::max(p.max_inc, v);
+    }
+  }
+  store_fence();
+  out = p;
+}
+
+std::string finish_create(const std::vector<ValidatePart>& parts, int64_t n, int64_t m,
+                          double* Vout, int32_t* Tout, HostMesh& M) {
+  if (m < 1) return "triangles must be (m, 3) with m >= 1, got (0, 3)";
+  bool finite = true, range = false, repeated = false, bad = false;
+  int64_t worst = 0;
+  double worst_abs = INFINITY;
+  int32_t mx = 0;
+  for (const ValidatePart& p : parts) {  // in triangle order
+    finite = finite && p.finite;
+    range = range || p.range;
+    repeated = repeated || p.repeated;
+    bad = bad || p.bad;
+    if (p.worst_abs < worst_abs) {
+      worst_abs = p.worst_abs;
+      worst = p.worst;
+    }
+    mx = std::max(mx, p.max_inc);
+  }
+  if (!finite) return "vertex coordinates must be finite";
+  if (range) return "triangle index out of range";
+  if (repeated) return "triangle with repeated vertex index";
+  if (bad)
+    return "degenerate triangle " + std::to_string(worst) + " (area " + fmt_g(worst_abs / 2.0) +
+           ")";
+  M.n = n;
+  M.m = m;
+  M.dV = Vout;
+  M.dT = Tout;
+  M.deferred = true;
+  M.max_deg = mx + 1;
+  return "";
+}
+
 const std::string& ensure_host(HostMesh& M) {
   std::call_once(M.host_once, [&M] {
     if (!M.deferred) return;

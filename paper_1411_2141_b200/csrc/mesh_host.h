@@ -2,6 +2,7 @@
 // Internal header (not part of the public ABI in include/meshreg_b200.h).
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -70,6 +71,21 @@ std::string build_mesh(int64_t n, const double* V, int64_t m, const int64_t* T, 
 // Returns "" or the reference's ValueError text.
 std::string create_mesh(int64_t n, const double* V, int64_t m, const int64_t* T, double* Vout,
                         int32_t* Tout, HostMesh& out);
+
+// create_mesh of one large mesh in parts on several threads: validate_part
+// over vertex range [v0, v1) and triangle range [t0, t1) (incidence counts
+// into inc, atomically), finish_create merges the parts in order.
+struct ValidatePart {
+  bool finite = true, range = false, repeated = false, bad = false;
+  int64_t worst = 0;
+  double worst_abs = INFINITY;
+  int32_t max_inc = 0;
+};
+void validate_part(int64_t n, const double* V, int64_t v0, int64_t v1, int64_t m,
+                   const int64_t* T, int64_t t0, int64_t t1, double* Vout, int32_t* Tout,
+                   int32_t* inc, ValidatePart& out);
+std::string finish_create(const std::vector<ValidatePart>& parts, int64_t n, int64_t m,
+                          double* Vout, int32_t* Tout, HostMesh& out);
 
 // Full host build of a deferred mesh (no-op otherwise); returns its error.
 const std::string& ensure_host(HostMesh& M);

@@ -203,6 +203,188 @@ __device__ __forceinline__ int gather_ring(const BuildJob& J, int v, int b0, int
   return c;
 }
 
+// ---- per-element steps (shared by the cluster kernels and the grid kernels) ----
+
+// TriangleGeometry (mesh.py:173-197; host: mesh_host.cpp build_mesh) of
+// triangle t and its three incidence counts
+__device__ __forceinline__ void build_tri(const BuildJob& J, int t) {
+  const int ia = J.T[3 * t], ib = J.T[3 * t + 1], ic = J.T[3 * t + 2];
+  const double2 A = J.V[ia], B = J.V[ib], Cc = J.V[ic];
+  const double a[2] = {A.x, A.y}, b[2] = {B.x, B.y}, c[2] = {Cc.x, Cc.y};
+  const double a2 = __dsub_rn(__dmul_rn(__dsub_rn(b[0], a[0]), __dsub_rn(c[1], a[1])),
+                              __dmul_rn(__dsub_rn(c[0], a[0]), __dsub_rn(b[1], a[1])));
+  const double ar = __dmul_rn(0.5, a2);
+  J.areas[t] = ar;
+  const double vij[2] = {__dsub_rn(b[0], a[0]), __dsub_rn(b[1], a[1])};
+  const double vjk[2] = {__dsub_rn(c[0], b[0]), __dsub_rn(c[1], b[1])};
+  const double vik[2] = {__dsub_rn(c[0], a[0]), __dsub_rn(c[1], a[1])};
+  auto dot = [](const double* u, double w0, double w1) {
+    return __dadd_rn(__dmul_rn(u[0], w0), __dmul_rn(u[1], w1));
+  };
+  const double di1 = dot(vij, vjk[0], vjk[1]), di2 = dot(vik, -vjk[0], -vjk[1]);
+  const double nvij[2] = {-vij[0], -vij[1]}, nvjk[2] = {-vjk[0], -vjk[1]};
+  const double nvik[2] = {-vik[0], -vik[1]};
+  const double dj1 = dot(nvij, vik[0], vik[1]), dj2 = dot(vjk, -vik[0], -vik[1]);
+  const double dk1 = dot(nvjk, -vij[0], -vij[1]), dk2 = dot(nvik, vij[0], vij[1]);
+  const double inv4a2 = __ddiv_rn(1.0, __dmul_rn(4.0, __dmul_rn(ar, ar)));
+  double* co = J.coeffs + 6 * size_t(t);
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    const double ti = __dadd_rn(__dmul_rn(di1, __dsub_rn(c[d], a[d])),
+                                __dmul_rn(di2, __dsub_rn(b[d], a[d])));
+    const double tj = __dadd_rn(__dmul_rn(dj1, __dsub_rn(c[d], b[d])),
+                                __dmul_rn(dj2, __dsub_rn(a[d], b[d])));
+    const double tk = __dadd_rn(__dmul_rn(dk1, __dsub_rn(a[d], c[d])),
+                                __dmul_rn(dk2, __dsub_rn(b[d], c[d])));
+    co[0 * 2 + d] = __dmul_rn(ti, inv4a2);
+    co[1 * 2 + d] = __dmul_rn(tj, inv4a2);
+    co[2 * 2 + d] = __dmul_rn(tk, inv4a2);
+  }
+  atomicAdd(J.cnt + ia, 1);
+  atomicAdd(J.cnt + ib, 1);
+  atomicAdd(J.cnt + ic, 1);
+}
+
+__device__ __forceinline__ void build_fill(const BuildJob& J, int t) {
+#pragma unroll
+  for (int x = 0; x < 3; ++x) {
+    const int v = J.T[3 * t + x];
+    J.inc_idx[J.inc_ptr[v] + atomicAdd(J.cnt + v, 1)] = t;
+  }
+}
+
+// vertex v: incident list ascending (mesh.py:106-110), vertex area in
+// np.add.at's (triangle, corner) order (mesh.py:209-211), valence, edge use
+// counts, ring positions of the incident triangles' corners; returns flags
+__device__ __forceinline__ int build_vertex(const BuildJob& J, int v) {
+  const int b0 = J.inc_ptr[v], k = J.inc_ptr[v + 1] - b0;
+  if (k > kBuildMaxInc) {
+    J.valence[v] = 0;
+    J.varea[v] = 0.0;
+    return kBuildOverflow;
+  }
+  int flags = 0;
+  int tl[kBuildMaxInc];
+  for (int q = 0; q < k; ++q) tl[q] = J.inc_idx[b0 + q];
+  insertion_sort(tl, k);
+  double va = 0.0;
+  for (int q = 0; q < k; ++q) {
+    J.inc_idx[b0 + q] = tl[q];
+    va = __dadd_rn(va, J.areas[tl[q]]);
+  }
+  J.varea[v] = va;
+  // neighbour id << 6 | origin (2 q + s: the s-th other corner of the q-th
+  // incident triangle): sorted, equal ids adjacent; the ring position of
+  // every origin (cpos) spares pass B a search per corner
+  int nb[2 * kBuildMaxInc];
+  int c = 0;
+  for (int q = 0; q < k; ++q) {
+    int sidx = 0;
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+      const int j = J.T[3 * tl[q] + x];
+      if (j != v) nb[c++] = j << 6 | (2 * q + sidx++);
+    }
+  }
+  insertion_sort(nb, c);
+  int val = 0;
+  for (int x = 0; x < c;) {
+    int y = x;
+    while (y < c && (nb[y] >> 6) == (nb[x] >> 6)) {
+      J.cpos[2 * size_t(b0) + (nb[y] & 63)] = (unsigned char)val;
+      ++y;
+    }
+    if (y - x > 2) flags |= kBuildNonManifold;
+    ++val;
+    x = y;
+  }
+  J.valence[v] = val;
+  if (val < 2) flags |= kBuildLone;
+  return flags;
+}
+
+// sorted one-ring of v (mesh.py:101-104,116) at ring_ptr[v]
+__device__ __forceinline__ void build_ring(const BuildJob& J, int v) {
+  const int b0 = J.inc_ptr[v], k = J.inc_ptr[v + 1] - b0;
+  if (k > kBuildMaxInc) return;
+  int nb[2 * kBuildMaxInc];
+  const int c = gather_ring(J, v, b0, k, nb);
+  int* out = J.ring_idx + J.ring_ptr[v];
+  int w = 0;
+  for (int x = 0; x < c; ++x)
+    if (x == 0 || nb[x] != nb[x - 1]) out[w++] = nb[x];
+}
+
+// Morton (Z-order) key of v for the node relabelling (host: build_mesh)
+__device__ __forceinline__ void build_key(const BuildJob& J, int v, double lo0, double lo1,
+                                          double span) {
+  const double2 p = J.V[v];
+  const uint32_t qx = __double2uint_rz(
+      fmin(65535.0, __dmul_rn(__ddiv_rn(__dsub_rn(p.x, lo0), span), 65535.0)));
+  const uint32_t qy = __double2uint_rz(
+      fmin(65535.0, __dmul_rn(__ddiv_rn(__dsub_rn(p.y, lo1), span), 65535.0)));
+  J.key[v] = (static_cast<unsigned long long>(J.mesh) << 32) |
+             (spread16_d(qx) | (spread16_d(qy) << 1));
+  J.val[v] = v;
+}
+
+__device__ __forceinline__ void build_perm(const BuildJob& J, int k) {
+  const int i = J.sorted[k];
+  J.perm[k] = i;
+  J.iperm[i] = k;
+}
+
+// device id k: one-ring CSR row and the fused operator G = avg∘grad on
+// {self} ∪ one-ring (mesh.py:199-213,236-241), incident triangles ascending,
+// corners in order, as the host accumulates; returns the valence
+__device__ __forceinline__ int build_row(const BuildJob& J, int k) {
+  const int i = J.perm[k];
+  const int deg = J.valence[i], rb = J.ring_ptr[i], base = J.nb_ptr[k];
+  const int* ring = J.ring_idx + rb;
+  double gx[2 * kBuildMaxInc], gy[2 * kBuildMaxInc];
+  for (int r = 0; r < deg; ++r) {
+    J.nb_idx[base + r] = J.iperm[ring[r]];
+    gx[r] = gy[r] = 0.0;
+  }
+  double sx = 0.0, sy = 0.0;
+  const int q0 = J.inc_ptr[i], q1 = J.inc_ptr[i + 1];
+  const double va = J.varea[i];
+  for (int q = q0; q < q1 && q1 - q0 <= kBuildMaxInc; ++q) {
+    const int t = J.inc_idx[q];
+    const double w = __ddiv_rn(J.areas[t], va);
+    const double* co = J.coeffs + 6 * size_t(t);
+    int sidx = 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int j = J.T[3 * t + c];
+      const double cx = __dmul_rn(w, co[2 * c]);
+      const double cy = __dmul_rn(w, co[2 * c + 1]);
+      if (j == i) {
+        sx = __dadd_rn(sx, cx);
+        sy = __dadd_rn(sy, cy);
+      } else {
+        const int pos = min(int(J.cpos[2 * size_t(q) + sidx++]), max(deg - 1, 0));
+        gx[pos] = __dadd_rn(gx[pos], cx);
+        gy[pos] = __dadd_rn(gy[pos], cy);
+      }
+    }
+  }
+  for (int r = 0; r < deg; ++r) J.g_nb[base + r] = make_double2(gx[r], gy[r]);
+  J.g_self_f[k] = make_float2(__double2float_rn(sx), __double2float_rn(sy));
+  const double iv = __ddiv_rn(1.0, double(max(deg, 1)));
+  J.inv_val_f[k] = __double2float_rn(iv);
+  if (J.g_self_d) {
+    J.g_self_d[k] = make_double2(sx, sy);
+    J.inv_val_d[k] = iv;
+  }
+  J.Vn[k] = J.V[i];
+  return deg;
+}
+
+__device__ __forceinline__ void build_tri_out(const BuildJob& J, int t) {
+  J.tri[t] = make_int4(J.iperm[J.T[3 * t]], J.iperm[J.T[3 * t + 1]], J.iperm[J.T[3 * t + 2]], 0);
+}
+
 // ---- pass A: geometry, incidence, one-rings, Morton keys ---------------------
 __global__ void __cluster_dims__(kBuildCluster, 1, 1) __launch_bounds__(kBuildThreads)
     k_mesh_build_a(const BuildJob* __restrict__ jobs) {
@@ -219,117 +401,21 @@ __global__ void __cluster_dims__(kBuildCluster, 1, 1) __launch_bounds__(kBuildTh
   if (threadIdx.x == 0) s_flags = 0;
   for (int v = tid; v < n; v += nt) J.cnt[v] = 0;
   cluster.sync();
-  // TriangleGeometry (mesh.py:173-197; host: mesh_host.cpp build_mesh)
-  for (int t = tid; t < m; t += nt) {
-    const int ia = J.T[3 * t], ib = J.T[3 * t + 1], ic = J.T[3 * t + 2];
-    const double2 A = J.V[ia], B = J.V[ib], Cc = J.V[ic];
-    const double a[2] = {A.x, A.y}, b[2] = {B.x, B.y}, c[2] = {Cc.x, Cc.y};
-    const double a2 = __dsub_rn(__dmul_rn(__dsub_rn(b[0], a[0]), __dsub_rn(c[1], a[1])),
-                                __dmul_rn(__dsub_rn(c[0], a[0]), __dsub_rn(b[1], a[1])));
-    const double ar = __dmul_rn(0.5, a2);
-    J.areas[t] = ar;
-    const double vij[2] = {__dsub_rn(b[0], a[0]), __dsub_rn(b[1], a[1])};
-    const double vjk[2] = {__dsub_rn(c[0], b[0]), __dsub_rn(c[1], b[1])};
-    const double vik[2] = {__dsub_rn(c[0], a[0]), __dsub_rn(c[1], a[1])};
-    auto dot = [](const double* u, double w0, double w1) {
-      return __dadd_rn(__dmul_rn(u[0], w0), __dmul_rn(u[1], w1));
-    };
-    const double di1 = dot(vij, vjk[0], vjk[1]), di2 = dot(vik, -vjk[0], -vjk[1]);
-    const double nvij[2] = {-vij[0], -vij[1]}, nvjk[2] = {-vjk[0], -vjk[1]};
-    const double nvik[2] = {-vik[0], -vik[1]};
-    const double dj1 = dot(nvij, vik[0], vik[1]), dj2 = dot(vjk, -vik[0], -vik[1]);
-    const double dk1 = dot(nvjk, -vij[0], -vij[1]), dk2 = dot(nvik, vij[0], vij[1]);
-    const double inv4a2 = __ddiv_rn(1.0, __dmul_rn(4.0, __dmul_rn(ar, ar)));
-    double* co = J.coeffs + 6 * size_t(t);
-#pragma unroll
-    for (int d = 0; d < 2; ++d) {
-      const double ti = __dadd_rn(__dmul_rn(di1, __dsub_rn(c[d], a[d])),
-                                  __dmul_rn(di2, __dsub_rn(b[d], a[d])));
-      const double tj = __dadd_rn(__dmul_rn(dj1, __dsub_rn(c[d], b[d])),
-                                  __dmul_rn(dj2, __dsub_rn(a[d], b[d])));
-      const double tk = __dadd_rn(__dmul_rn(dk1, __dsub_rn(a[d], c[d])),
-                                  __dmul_rn(dk2, __dsub_rn(b[d], c[d])));
-      co[0 * 2 + d] = __dmul_rn(ti, inv4a2);
-      co[1 * 2 + d] = __dmul_rn(tj, inv4a2);
-      co[2 * 2 + d] = __dmul_rn(tk, inv4a2);
-    }
-    atomicAdd(J.cnt + ia, 1);
-    atomicAdd(J.cnt + ib, 1);
-    atomicAdd(J.cnt + ic, 1);
-  }
+  for (int t = tid; t < m; t += nt) build_tri(J, t);
   cluster.sync();
   cluster_exclusive_scan(n, [&](int v) { return J.cnt[v]; }, J.inc_ptr, s_tmp, &s_tot);
   for (int v = tid; v < n; v += nt) J.cnt[v] = 0;
   cluster.sync();
-  for (int t = tid; t < m; t += nt)
-#pragma unroll
-    for (int x = 0; x < 3; ++x) {
-      const int v = J.T[3 * t + x];
-      J.inc_idx[J.inc_ptr[v] + atomicAdd(J.cnt + v, 1)] = t;
-    }
+  for (int t = tid; t < m; t += nt) build_fill(J, t);
   cluster.sync();
-  // incident lists ascending (mesh.py:106-110), vertex areas in np.add.at's
-  // (triangle, corner) order (mesh.py:209-211), valence and edge use counts
-  for (int v = tid; v < n; v += nt) {
-    const int b0 = J.inc_ptr[v], k = J.inc_ptr[v + 1] - b0;
-    if (k > kBuildMaxInc) {
-      atomicOr(&s_flags, kBuildOverflow);
-      J.valence[v] = 0;
-      J.varea[v] = 0.0;
-      continue;
-    }
-    int tl[kBuildMaxInc];
-    for (int q = 0; q < k; ++q) tl[q] = J.inc_idx[b0 + q];
-    insertion_sort(tl, k);
-    double va = 0.0;
-    for (int q = 0; q < k; ++q) {
-      J.inc_idx[b0 + q] = tl[q];
-      va = __dadd_rn(va, J.areas[tl[q]]);
-    }
-    J.varea[v] = va;
-    // neighbour id << 6 | origin (2 q + s: the s-th other corner of the q-th
-    // incident triangle): sorted, equal ids adjacent; the ring position of
-    // every origin (cpos) spares pass B a search per corner
-    int nb[2 * kBuildMaxInc];
-    int c = 0;
-    for (int q = 0; q < k; ++q) {
-      int sidx = 0;
-#pragma unroll
-      for (int x = 0; x < 3; ++x) {
-        const int j = J.T[3 * tl[q] + x];
-        if (j != v) nb[c++] = j << 6 | (2 * q + sidx++);
-      }
-    }
-    insertion_sort(nb, c);
-    int val = 0;
-    for (int x = 0; x < c;) {
-      int y = x;
-      while (y < c && (nb[y] >> 6) == (nb[x] >> 6)) {
-        J.cpos[2 * size_t(b0) + (nb[y] & 63)] = (unsigned char)val;
-        ++y;
-      }
-      if (y - x > 2) atomicOr(&s_flags, kBuildNonManifold);
-      ++val;
-      x = y;
-    }
-    J.valence[v] = val;
-    if (val < 2) atomicOr(&s_flags, kBuildLone);
-  }
+  int flags = 0;
+  for (int v = tid; v < n; v += nt) flags |= build_vertex(J, v);
+  if (flags) atomicOr(&s_flags, flags);
   cluster.sync();
   cluster_exclusive_scan(n, [&](int v) { return J.valence[v]; }, J.ring_ptr, s_tmp, &s_tot);
   const bool ring_fits = J.ring_ptr[n] <= J.ring_cap;  // else non-manifold: flagged
   if (!ring_fits && tid == 0) atomicOr(J.stats, kBuildOverflow);
-  for (int v = tid; v < n && ring_fits; v += nt) {  // sorted one-rings (mesh.py:101-104,116)
-    const int b0 = J.inc_ptr[v], k = J.inc_ptr[v + 1] - b0;
-    if (k > kBuildMaxInc) continue;
-    int nb[2 * kBuildMaxInc];
-    const int c = gather_ring(J, v, b0, k, nb);
-    int* out = J.ring_idx + J.ring_ptr[v];
-    int w = 0;
-    for (int x = 0; x < c; ++x)
-      if (x == 0 || nb[x] != nb[x - 1]) out[w++] = nb[x];
-  }
-  // Morton (Z-order) keys of the node relabelling (host: build_mesh)
+  for (int v = tid; v < n && ring_fits; v += nt) build_ring(J, v);
   double lo0 = INFINITY, lo1 = INFINITY, hi0 = -INFINITY, hi1 = -INFINITY;
   for (int v = tid; v < n; v += nt) {
     const double2 p = J.V[v];
@@ -345,16 +431,7 @@ __global__ void __cluster_dims__(kBuildCluster, 1, 1) __launch_bounds__(kBuildTh
   hi0 = cluster_reduce(hi0, mx, s_red, &s_out);
   hi1 = cluster_reduce(hi1, mx, s_red, &s_out);
   const double span = fmax(fmax(__dsub_rn(hi0, lo0), __dsub_rn(hi1, lo1)), 1e-12);
-  for (int v = tid; v < n; v += nt) {
-    const double2 p = J.V[v];
-    const uint32_t qx = __double2uint_rz(
-        fmin(65535.0, __dmul_rn(__ddiv_rn(__dsub_rn(p.x, lo0), span), 65535.0)));
-    const uint32_t qy = __double2uint_rz(
-        fmin(65535.0, __dmul_rn(__ddiv_rn(__dsub_rn(p.y, lo1), span), 65535.0)));
-    J.key[v] = (static_cast<unsigned long long>(J.mesh) << 32) |
-               (spread16_d(qx) | (spread16_d(qy) << 1));
-    J.val[v] = v;
-  }
+  for (int v = tid; v < n; v += nt) build_key(J, v, lo0, lo1, span);
   __syncthreads();
   if (threadIdx.x == 0) {
     if (s_flags) atomicOr(J.stats, s_flags);
@@ -374,61 +451,93 @@ __global__ void __cluster_dims__(kBuildCluster, 1, 1) __launch_bounds__(kBuildTh
   if (J.ring_ptr[n] > J.ring_cap) return;  // flagged by pass A (uniform over the cluster)
   const int nt = kBuildCluster * int(blockDim.x);
   const int tid = int(cluster.block_rank()) * int(blockDim.x) + int(threadIdx.x);
-  for (int k = tid; k < n; k += nt) {
-    const int i = J.sorted[k];
-    J.perm[k] = i;
-    J.iperm[i] = k;
-  }
+  for (int k = tid; k < n; k += nt) build_perm(J, k);
   cluster.sync();
   cluster_exclusive_scan(n, [&](int k) { return J.valence[J.perm[k]]; }, J.nb_ptr, s_tmp, &s_tot);
   int dmax = 0;
-  for (int k = tid; k < n; k += nt) {
-    const int i = J.perm[k];
-    const int deg = J.valence[i], rb = J.ring_ptr[i], base = J.nb_ptr[k];
-    dmax = max(dmax, deg);
-    const int* ring = J.ring_idx + rb;
-    // G = avg∘grad on {self} ∪ one-ring (mesh.py:199-213,236-241): incident
-    // triangles ascending, corners in order, as the host accumulates
-    double gx[2 * kBuildMaxInc], gy[2 * kBuildMaxInc];
-    for (int r = 0; r < deg; ++r) {
-      J.nb_idx[base + r] = J.iperm[ring[r]];
-      gx[r] = gy[r] = 0.0;
-    }
-    double sx = 0.0, sy = 0.0;
-    const int q0 = J.inc_ptr[i], q1 = J.inc_ptr[i + 1];
-    const double va = J.varea[i];
-    for (int q = q0; q < q1 && q1 - q0 <= kBuildMaxInc; ++q) {
-      const int t = J.inc_idx[q];
-      const double w = __ddiv_rn(J.areas[t], va);
-      const double* co = J.coeffs + 6 * size_t(t);
-      int sidx = 0;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int j = J.T[3 * t + c];
-        const double cx = __dmul_rn(w, co[2 * c]);
-        const double cy = __dmul_rn(w, co[2 * c + 1]);
-        if (j == i) {
-          sx = __dadd_rn(sx, cx);
-          sy = __dadd_rn(sy, cy);
-        } else {
-          const int pos = min(int(J.cpos[2 * size_t(q) + sidx++]), max(deg - 1, 0));
-          gx[pos] = __dadd_rn(gx[pos], cx);
-          gy[pos] = __dadd_rn(gy[pos], cy);
-        }
-      }
-    }
-    for (int r = 0; r < deg; ++r) J.g_nb[base + r] = make_double2(gx[r], gy[r]);
-    J.g_self_f[k] = make_float2(__double2float_rn(sx), __double2float_rn(sy));
-    const double iv = __ddiv_rn(1.0, double(max(deg, 1)));
-    J.inv_val_f[k] = __double2float_rn(iv);
-    if (J.g_self_d) {
-      J.g_self_d[k] = make_double2(sx, sy);
-      J.inv_val_d[k] = iv;
-    }
-    J.Vn[k] = J.V[i];
+  for (int k = tid; k < n; k += nt) dmax = max(dmax, build_row(J, k));
+  for (int t = tid; t < m; t += nt) build_tri_out(J, t);
+  dmax = cta_reduce(dmax, [](int x, int y) { return max(x, y); }, s_red);
+  if (threadIdx.x == 0) atomicMax(J.stats + 1, dmax);
+}
+
+// ---- the same steps as grid-wide kernels, for one large mesh ------------------
+// (a single cluster of kBuildCluster CTAs per mesh would serialise a C5-size
+// mesh; the scans between the steps are CUB device scans)
+__global__ void k_bg_tri(const BuildJob* __restrict__ j) {
+  const BuildJob& J = *j;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < J.m; t += gridDim.x * blockDim.x)
+    build_tri(J, t);
+}
+__global__ void k_bg_fill(const BuildJob* __restrict__ j) {
+  const BuildJob& J = *j;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < J.m; t += gridDim.x * blockDim.x)
+    build_fill(J, t);
+}
+// vertices; block partials of the coordinate bounds into bounds[block][4]
+__global__ void k_bg_vertex(const BuildJob* __restrict__ j, double4* __restrict__ bounds) {
+  const BuildJob& J = *j;
+  __shared__ double s_red[32];
+  int flags = 0;
+  double lo0 = INFINITY, lo1 = INFINITY, hi0 = -INFINITY, hi1 = -INFINITY;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < J.n; v += gridDim.x * blockDim.x) {
+    flags |= build_vertex(J, v);
+    const double2 p = J.V[v];
+    lo0 = fmin(lo0, p.x);
+    lo1 = fmin(lo1, p.y);
+    hi0 = fmax(hi0, p.x);
+    hi1 = fmax(hi1, p.y);
   }
-  for (int t = tid; t < m; t += nt)
-    J.tri[t] = make_int4(J.iperm[J.T[3 * t]], J.iperm[J.T[3 * t + 1]], J.iperm[J.T[3 * t + 2]], 0);
+  if (flags) atomicOr(J.stats, flags);
+  auto mn = [](double x, double y) { return fmin(x, y); };
+  auto mx = [](double x, double y) { return fmax(x, y); };
+  lo0 = cta_reduce(lo0, mn, s_red);
+  lo1 = cta_reduce(lo1, mn, s_red);
+  hi0 = cta_reduce(hi0, mx, s_red);
+  hi1 = cta_reduce(hi1, mx, s_red);
+  if (threadIdx.x == 0) bounds[blockIdx.x] = make_double4(lo0, lo1, hi0, hi1);
+}
+// rings + keys (bounds reduced by every block in the same order)
+__global__ void k_bg_ring_key(const BuildJob* __restrict__ j, const double4* __restrict__ bounds,
+                              int nbounds) {
+  const BuildJob& J = *j;
+  double lo0 = INFINITY, lo1 = INFINITY, hi0 = -INFINITY, hi1 = -INFINITY;
+  for (int b = 0; b < nbounds; ++b) {
+    const double4 q = bounds[b];
+    lo0 = fmin(lo0, q.x);
+    lo1 = fmin(lo1, q.y);
+    hi0 = fmax(hi0, q.z);
+    hi1 = fmax(hi1, q.w);
+  }
+  const double span = fmax(fmax(__dsub_rn(hi0, lo0), __dsub_rn(hi1, lo1)), 1e-12);
+  const bool ring_fits = J.ring_ptr[J.n] <= J.ring_cap;
+  const int first = blockIdx.x * blockDim.x + threadIdx.x;
+  if (first == 0) {
+    if (!ring_fits) atomicOr(J.stats, kBuildOverflow);
+    J.stats[2] = J.ring_ptr[J.n];
+  }
+  for (int v = first; v < J.n; v += gridDim.x * blockDim.x) {
+    if (ring_fits) build_ring(J, v);
+    build_key(J, v, lo0, lo1, span);
+  }
+}
+// device order; the permuted valences into cnt (scanned into nb_ptr next)
+__global__ void k_bg_perm(const BuildJob* __restrict__ j) {
+  const BuildJob& J = *j;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < J.n; k += gridDim.x * blockDim.x) {
+    build_perm(J, k);
+    J.cnt[k] = J.valence[J.sorted[k]];
+  }
+}
+__global__ void k_bg_rows(const BuildJob* __restrict__ j) {
+  const BuildJob& J = *j;
+  __shared__ int s_red[32];
+  if (J.ring_ptr[J.n] > J.ring_cap) return;
+  int dmax = 0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < J.n; k += gridDim.x * blockDim.x)
+    dmax = max(dmax, build_row(J, k));
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < J.m; t += gridDim.x * blockDim.x)
+    build_tri_out(J, t);
   dmax = cta_reduce(dmax, [](int x, int y) { return max(x, y); }, s_red);
   if (threadIdx.x == 0) atomicMax(J.stats + 1, dmax);
 }

@@ -34,6 +34,7 @@
 #include "mesh_host.h"
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 using namespace mrb;
 
@@ -993,10 +994,22 @@ bool device_buildable(const HostMesh& h) {
 }
 
 // with64: also the fp64 self terms and 1/valence (the fp64 cluster path)
-void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, cudaStream_t copy,
+int device_sms();
+
+// Meshes above this size are built by grid-wide kernels (k_bg_*), the rest
+// by one 8-CTA cluster each (k_mesh_build_a/b), all sorted together.
+constexpr int64_t kBuildGridNodes = 32768;
+
+void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo_in, cudaStream_t copy,
                          bool with64 = false) {
-  if (todo.empty()) return;
+  if (todo_in.empty()) return;
+  // cluster-built meshes first, then the large ones
+  std::vector<HostMesh*> todo = todo_in;
+  std::stable_partition(todo.begin(), todo.end(),
+                        [](const HostMesh* h) { return h->n <= kBuildGridNodes; });
   const size_t K = todo.size();
+  size_t K_small = 0;
+  while (K_small < K && todo[K_small]->n <= kBuildGridNodes) ++K_small;
   // inputs: V (double2) and T (int3) per mesh, one pinned stage, one copy
   std::vector<size_t> in_off(K), out_off(K), b_off(K), key_off(K);
   size_t in_tot = 0, out_tot = 0, b_tot = 0, keys = 0;
@@ -1009,7 +1022,7 @@ void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, cudaS
                (with64 ? al256(n * 16) + al256(n * 8) : 0);
     b_off[i] = b_tot;  // build slab (kept: nb_ptr, nb_idx, g_nb)
     const size_t e2 = 3 * m + n;  // one-ring entries of a manifold mesh (2e <= 3m + n)
-    b_tot += al256(m * 8) + al256(m * 48) + 3 * al256(n * 4) + 2 * al256((n + 1) * 4) +
+    b_tot += al256(m * 8) + al256(m * 48) + 3 * al256((n + 1) * 4) + 2 * al256((n + 1) * 4) +
              al256(3 * m * 4) + al256(6 * m) + 2 * al256(e2 * 4) + al256(n * 8) +
              al256((n + 1) * 4) + al256(e2 * 16);
     key_off[i] = keys;
@@ -1074,9 +1087,9 @@ void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, cudaS
     };
     J.areas = reinterpret_cast<double*>(take(m * 8));
     J.coeffs = reinterpret_cast<double*>(take(m * 48));
-    J.cnt = reinterpret_cast<int*>(take(n * 4));
-    J.valence = reinterpret_cast<int*>(take(n * 4));
-    J.iperm = reinterpret_cast<int*>(take(n * 4));
+    J.cnt = reinterpret_cast<int*>(take((n + 1) * 4));      // + 1: device scans of the
+    J.valence = reinterpret_cast<int*>(take((n + 1) * 4));  // grid kernels (last entry 0)
+    J.iperm = reinterpret_cast<int*>(take((n + 1) * 4));
     J.inc_ptr = reinterpret_cast<int*>(take((n + 1) * 4));
     J.ring_ptr = reinterpret_cast<int*>(take((n + 1) * 4));
     J.inc_idx = reinterpret_cast<int*>(take(3 * m * 4));
@@ -1113,7 +1126,30 @@ void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, cudaS
   upload_zero_copy(djobs, pin, K * sizeof(BuildJob), s);
   ck(cudaEventRecord(ctx->small_ev, s));
   ck(cudaMemsetAsync(dstats, 0, K * 16, s));
-  k_mesh_build_a<<<unsigned(K * kBuildCluster), kBuildThreads, 0, s>>>(djobs);
+  if (K_small) k_mesh_build_a<<<unsigned(K_small * kBuildCluster), kBuildThreads, 0, s>>>(djobs);
+  // large meshes: the same steps as grid-wide kernels with CUB scans between
+  const int bg_blocks = 4 * device_sms(), bg_threads = 256;
+  double4* bounds = K > K_small ? dalloc<double4>(bg_blocks) : nullptr;
+  auto scan = [&](const int* in, int* out, int count) {  // exclusive, count = n + 1
+    size_t tb = 0;
+    ck(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, count, s));
+    void* tmp = dalloc<unsigned char>(tb);
+    ck(cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, count, s));
+    dev_free(tmp, s);
+  };
+  for (size_t i = K_small; i < K; ++i) {
+    const BuildJob& J = jobs[i];
+    const BuildJob* dj = djobs + i;
+    ck(cudaMemsetAsync(J.cnt, 0, size_t(J.n + 1) * 4, s));
+    k_bg_tri<<<bg_blocks, bg_threads, 0, s>>>(dj);
+    scan(J.cnt, J.inc_ptr, J.n + 1);
+    ck(cudaMemsetAsync(J.cnt, 0, size_t(J.n + 1) * 4, s));
+    k_bg_fill<<<bg_blocks, bg_threads, 0, s>>>(dj);
+    ck(cudaMemsetAsync(J.valence + J.n, 0, 4, s));
+    k_bg_vertex<<<bg_blocks, bg_threads, 0, s>>>(dj, bounds);
+    scan(J.valence, J.ring_ptr, J.n + 1);
+    k_bg_ring_key<<<bg_blocks, bg_threads, 0, s>>>(dj, bounds, bg_blocks);
+  }
   dev_mark(s, "  build pass A done");
   // the node order: a stable sort of (mesh << 32 | Morton key) = the host's
   // std::stable_sort of each mesh's keys
@@ -1126,7 +1162,16 @@ void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo, cudaS
   ck(cub::DeviceRadixSort::SortPairs(dtemp, temp, kin, kin + keys, vin, vin + keys, int(keys), 0,
                                      end_bit, s));
   dev_mark(s, "  node order sorted");
-  k_mesh_build_b<<<unsigned(K * kBuildCluster), kBuildThreads, 0, s>>>(djobs);
+  if (K_small) k_mesh_build_b<<<unsigned(K_small * kBuildCluster), kBuildThreads, 0, s>>>(djobs);
+  for (size_t i = K_small; i < K; ++i) {
+    const BuildJob& J = jobs[i];
+    const BuildJob* dj = djobs + i;
+    ck(cudaMemsetAsync(J.cnt + J.n, 0, 4, s));
+    k_bg_perm<<<bg_blocks, bg_threads, 0, s>>>(dj);
+    scan(J.cnt, J.nb_ptr, J.n + 1);
+    k_bg_rows<<<bg_blocks, bg_threads, 0, s>>>(dj);
+  }
+  if (bounds) dev_free(bounds, s);
   ck(cudaGetLastError());
   dev_free(dtemp, s);
   dev_free(kin, s);
@@ -3353,9 +3398,15 @@ int mrb_mesh_create_many(int32_t count, const int64_t* n, const double* const* V
   for (int32_t k = 0; k < count; ++k)
     off[k + 1] = off[k] + al256(size_t(std::max<int64_t>(n[k], 0)) * 16) +
                  al256(size_t(std::max<int64_t>(m[k], 0)) * 12);
+  host_tick("create: begin");
   const std::shared_ptr<unsigned char> block = pinned_block(std::max<size_t>(off[count], 256));
+  host_tick("create: block");
   std::vector<std::string> msg(static_cast<size_t>(count));
+  // a large mesh is validated in parts on the whole worker pool, the others
+  // one mesh per worker
+  auto large = [&](int32_t k) { return m[k] >= 200000 && n[k] < (int64_t(1) << 31); };
   WorkerPool::get().run(size_t(count), [&](size_t k) {
+    if (large(int32_t(k))) return;
     auto* mesh = new mrb_mesh();
     unsigned char* at = block.get() + off[k];
     try {
@@ -3371,6 +3422,34 @@ int mrb_mesh_create_many(int32_t count, const int64_t* n, const double* const* V
       delete mesh;
     }
   });
+  for (int32_t k = 0; k < count; ++k) {
+    if (!large(k)) continue;
+    auto* mesh = new mrb_mesh();
+    unsigned char* at = block.get() + off[k];
+    double* Vout = reinterpret_cast<double*>(at);
+    int32_t* Tout = reinterpret_cast<int32_t*>(at + al256(size_t(n[k]) * 16));
+    constexpr int kParts = 64;
+    std::vector<ValidatePart> parts(kParts);
+    std::vector<int32_t> inc(size_t(n[k]), 0);
+    host_tick("create: large mesh begin");
+    try {
+      WorkerPool::get().run(kParts, [&](size_t c) {
+        validate_part(n[k], V[k], n[k] * int64_t(c) / kParts, n[k] * int64_t(c + 1) / kParts,
+                      m[k], T[k], m[k] * int64_t(c) / kParts, m[k] * int64_t(c + 1) / kParts,
+                      Vout, Tout, inc.data(), parts[c]);
+      });
+      host_tick("create: parts validated");
+      msg[k] = finish_create(parts, n[k], m[k], Vout, Tout, mesh->h);
+    } catch (const std::exception& ex) {
+      msg[k] = std::string("internal error: ") + ex.what();
+    }
+    if (msg[k].empty()) {
+      mesh->h.def_hold = block;
+      out[k] = mesh;
+    } else {
+      delete mesh;
+    }
+  }
   for (int32_t k = 0; k < count; ++k)
     if (!msg[k].empty()) {
       if (first_bad) *first_bad = k;
