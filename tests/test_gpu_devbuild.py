@@ -34,7 +34,9 @@ def cases():
     for name in GOLDEN_CASES:
         g = golden(name)
         out.append((name, g["V"], g["T_in"].astype(np.int64)))
-    for k, seed in ((40, 0), (110, 1), (156, 2)):  # 1.6k, 12k, 24k nodes
+    # 1.6k, 12k, 24k nodes (one 8-CTA cluster per mesh) and 44k nodes (the
+    # grid-wide build kernels of large meshes)
+    for k, seed in ((40, 0), (110, 1), (156, 2), (210, 3)):
         V, T = perturbed_grid(k, seed)
         out.append((f"grid{k}", V, T))
     return out
