@@ -338,10 +338,28 @@ __device__ __forceinline__ ClusterSmem carve(unsigned char* p, const ClusterPair
 // one-ring rounded up), f(codes of entries 2p | 2p+1 << 16, row index).
 // Padding entries point at the ZERO slot with coefficient 0, so they add
 // exactly nothing and no lane needs a predicate.
+template <int NP, typename F>
+__device__ __forceinline__ void ring_pairs_n(const uint32_t* code2, uint32_t base, F&& f) {
+  uint32_t cc[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) cc[q] = code2[base + 32u * q];  // all codes first
+#pragma unroll
+  for (int q = 0; q < NP; ++q) f(cc[q], base + 32u * q);
+}
+
 template <typename F>
 __device__ __forceinline__ void ring_pairs(const uint32_t* code2, uint32_t sw, int lane, F&& f) {
   const uint32_t base = (sw & 0xffffffu) + uint32_t(lane);
   const int np = int(sw >> 24);
+  // warp-uniform pair-row count: fully unrolled bodies for the usual counts
+  // (the codes of every row loaded before the gathers that depend on them)
+  switch (np) {
+    case 2: ring_pairs_n<2>(code2, base, f); return;
+    case 3: ring_pairs_n<3>(code2, base, f); return;
+    case 4: ring_pairs_n<4>(code2, base, f); return;
+    case 5: ring_pairs_n<5>(code2, base, f); return;
+    default: break;
+  }
 #pragma unroll 2
   for (int q = 0; q < np; ++q) {
     const uint32_t at = base + 32u * uint32_t(q);

@@ -37,11 +37,28 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned target) {
 // one-ring gather over this CTA's paired SELL topology in global memory
 // (read through L1; layout in write_topo): f(codes of entries 2p | 2p+1 <<
 // 16, row index) for the slice's warp-uniform pair-row count
+template <int NP, typename F>
+__device__ __forceinline__ void ring_pairs_gn(const uint32_t* __restrict__ code2, uint32_t base,
+                                              F&& f) {
+  uint32_t cc[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) cc[q] = __ldg(code2 + base + 32u * q);  // all codes first
+#pragma unroll
+  for (int q = 0; q < NP; ++q) f(cc[q], base + 32u * q);
+}
+
 template <typename F>
 __device__ __forceinline__ void ring_pairs_g(const uint32_t* __restrict__ code2, uint32_t sw,
                                              int lane, F&& f) {
   const uint32_t base = (sw & 0xffffffu) + uint32_t(lane);
   const int np = int(sw >> 24);
+  switch (np) {  // warp-uniform: fully unrolled bodies for the usual counts
+    case 2: ring_pairs_gn<2>(code2, base, f); return;
+    case 3: ring_pairs_gn<3>(code2, base, f); return;
+    case 4: ring_pairs_gn<4>(code2, base, f); return;
+    case 5: ring_pairs_gn<5>(code2, base, f); return;
+    default: break;
+  }
 #pragma unroll 2
   for (int q = 0; q < np; ++q) {
     const uint32_t at = base + 32u * uint32_t(q);
