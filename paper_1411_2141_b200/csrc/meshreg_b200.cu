@@ -1037,12 +1037,6 @@ void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo_in, cu
       ck(cudaStreamWaitEvent(copy, ctx->build_ev, 0));  // the previous build read it
     din = static_cast<unsigned char*>(kept_buffer(ctx, kKeptVT, in_tot));
     dev_mark(copy, "mesh V/T upload start");
-    {
-      cudaPointerAttributes pa{};
-      if (std::getenv("MESHREG_B200_DEBUG") && cudaPointerGetAttributes(&pa, todo[0]->dV) == cudaSuccess)
-        std::fprintf(stderr, "meshreg_b200:   V/T source memory type %d (host pinned = %d)\n",
-                     int(pa.type), int(cudaMemoryTypeHost));
-    }
     auto region = [&](size_t i) { return (i + 1 < K ? in_off[i + 1] : in_tot) - in_off[i]; };
     for (size_t i = 0; i < K;) {
       const unsigned char* src = reinterpret_cast<const unsigned char*>(todo[i]->dV);
@@ -1051,9 +1045,6 @@ void device_build_meshes(mrb_ctx* ctx, const std::vector<HostMesh*>& todo_in, cu
              todo[j]->def_hold == todo[i]->def_hold)
         bytes += region(j++);
       ck(mrb_copy_async(din + in_off[i], src, bytes, cudaMemcpyHostToDevice, copy));
-      if (std::getenv("MESHREG_B200_DEBUG"))
-        std::fprintf(stderr, "meshreg_b200:   V/T copy of meshes [%zu, %zu): %.1f MB\n", i, j,
-                     bytes / 1e6);
       i = j;
     }
     if (!ctx->build_in) ck(cudaEventCreateWithFlags(&ctx->build_in, cudaEventDisableTiming));
@@ -1986,7 +1977,6 @@ void build_pairs(mrb_batch* b) {
     b->dense = dalloc<Real>(3 * npx * b->n_pairs);
   }
   b->state_bytes = state_bytes;
-  host_tick("pairs: state + dense");
   int blk = 0, pblk = 0;
   std::vector<int> bp, pbp;
   const int pix_nblk = int((npx + kPixBlock - 1) / kPixBlock);
@@ -2039,13 +2029,11 @@ void build_pairs(mrb_batch* b) {
   b->n_node_blocks = blk;
   b->n_pix_blocks = pblk;
   cudaStream_t s = b->ctx->stream;
-  host_tick("pairs: filled");
   b->pairs = aupload(b->ctx, pd.data(), pd.size());
   b->blk_pair = aupload(b->ctx, bp.data(), bp.size());
   b->pix_blk_pair = aupload(b->ctx, pbp.data(), pbp.size());
   b->partials = dalloc<double>(blk);
   b->pix_partials = dalloc<double2>(pblk);
-  host_tick("pairs: uploaded");
   b->pairs_host.assign(reinterpret_cast<const unsigned char*>(pd.data()),
                        reinterpret_cast<const unsigned char*>(pd.data() + pd.size()));
 }
@@ -2454,11 +2442,9 @@ int64_t enqueue_run(mrb_batch* b, KernelTimer* tm = nullptr) {
             cudaEventRecord(e, gs);
             b->dbg_group_ev.push_back(e);
           }
-          host_tick("run: group pads + topo");
           b->lstream = gs;
           launches += launch_cluster(b, p0, p1 - p0);
           b->lstream = nullptr;
-          host_tick("run: group launched");
           if (tail_side && g == ng - 2) {
             const int t0 = b->groups[ng - 1], t1 = b->groups[ng];
             ck(cudaEventRecord(b->tail_fork, gs));
@@ -3068,9 +3054,7 @@ void build_fast_descriptors(mrb_batch* b) {
       }
     }
   }
-  host_tick("descriptors: filled");
   b->cpairs = aupload(b->ctx, cp.data(), cp.size());
-  host_tick("descriptors: uploaded");
   if (b->lazy_from < std::min(b->planned_end, b->n_pairs)) {
     b->cp_host = cp;
     ck(cudaHostAlloc(reinterpret_cast<void**>(&b->cp_pinned), sizeof(ClusterPair) * cp.size(),
@@ -3398,9 +3382,7 @@ int mrb_mesh_create_many(int32_t count, const int64_t* n, const double* const* V
   for (int32_t k = 0; k < count; ++k)
     off[k + 1] = off[k] + al256(size_t(std::max<int64_t>(n[k], 0)) * 16) +
                  al256(size_t(std::max<int64_t>(m[k], 0)) * 12);
-  host_tick("create: begin");
   const std::shared_ptr<unsigned char> block = pinned_block(std::max<size_t>(off[count], 256));
-  host_tick("create: block");
   std::vector<std::string> msg(static_cast<size_t>(count));
   // a large mesh is validated in parts on the whole worker pool, the others
   // one mesh per worker
@@ -3431,14 +3413,12 @@ int mrb_mesh_create_many(int32_t count, const int64_t* n, const double* const* V
     constexpr int kParts = 64;
     std::vector<ValidatePart> parts(kParts);
     std::vector<int32_t> inc(size_t(n[k]), 0);
-    host_tick("create: large mesh begin");
     try {
       WorkerPool::get().run(kParts, [&](size_t c) {
         validate_part(n[k], V[k], n[k] * int64_t(c) / kParts, n[k] * int64_t(c + 1) / kParts,
                       m[k], T[k], m[k] * int64_t(c) / kParts, m[k] * int64_t(c + 1) / kParts,
                       Vout, Tout, inc.data(), parts[c]);
       });
-      host_tick("create: parts validated");
       msg[k] = finish_create(parts, n[k], m[k], Vout, Tout, mesh->h);
     } catch (const std::exception& ex) {
       msg[k] = std::string("internal error: ") + ex.what();
@@ -3799,7 +3779,6 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
     }
     b->total_nodes = off;
     const size_t npx = size_t(W) * H;
-    host_tick("batch: before buffers");
     b->st = dalloc<PairStatus>(n_pairs);
     b->traces = dalloc<double>(size_t(n_pairs) * cfg->max_iterations);
     b->u_out = dalloc<double2>(off);
@@ -3814,7 +3793,6 @@ int batch_create_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, in
       bb->img_ptrs = aupload(ctx, ip.data(), ip.size());
     };
     if (!(eligible && mode == 1 && !b->real_d)) alloc_img(b.get());
-    host_tick("batch: small buffers");
     if (b->tap_d)
       build_pairs<double, double>(b.get());
     else if (b->real_d)
@@ -4763,9 +4741,7 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
       // them); otherwise the run waits for all images
       const bool group_images = k == 0 && early.ev.size() > 1;
       if (!group_images) cudaStreamWaitEvent(sc->stream, ctx->copy_done, 0);
-      host_tick("many: create end");
       if (rc == MRB_OK) rc = mrb_batch_set_images(b, dimg, dimg + img_bytes, 1);
-      host_tick("many: set images");
       if (rc == MRB_OK && grouped) {
         try {
           batch_set_groups(b, wave);
@@ -4784,9 +4760,7 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
         for (auto& e : ev_run) cudaEventCreate(&e);
         cudaEventRecord(ev_run[0], sc->stream);
       }
-      host_tick("many: groups");
       if (rc == MRB_OK) rc = mrb_batch_run(b);
-      host_tick("many: run enqueued");
       if (dbg && ev_run[1]) {
         cudaEventRecord(ev_run[1], sc->stream);
         dbg_events.push_back({ev_run[0], ev_run[1]});
