@@ -1,5 +1,14 @@
 // C ABI + launch orchestration of the B200 mesh-registration path.
 // Public interface: include/meshreg_b200.h.  Device code: kernels.cuh.
+//
+// Environment hooks (tests and diagnostics only; none changes a result):
+//   MESHREG_B200_PATH=cluster|grid|generic, MESHREG_B200_EXCHANGE=push|pull
+//     force a loop path (cross-path parity tests);
+//   MESHREG_B200_NO_TAIL, MESHREG_B200_NO_GROUPS  run the C4 job without the
+//     latency-shape tail wave / as one launch (equivalence tests);
+//   MESHREG_B200_DEBUG  host/device timeline on stderr;
+//   MESHREG_B200_PROFILE_PHASES  per-phase clock64 stamps of the cluster
+//     kernels (tools/phase_profile.py).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -2937,13 +2946,9 @@ void build_fast_descriptors(mrb_batch* b) {
   // taps evict_first when the four image copies exceed half of L2 (C5); the
   // whole-GPU grid path then streams the taps from DRAM and reads them in the
   // row-pair layout (one 64-byte fetch per two tap rows instead of one per
-  // row; MESHREG_B200_TAP_LAYOUT=shifted keeps the four shifted copies)
+  // row)
   b->tap_evict_first = 4 * b->pad_plane * sizeof(float2) > device_l2_bytes() / 2;
-  {
-    const char* lay = std::getenv("MESHREG_B200_TAP_LAYOUT");
-    b->pad_rowpair = b->grid_mode && b->grid_flags && b->tap_evict_first &&
-                     !(lay && std::string(lay) == "shifted");
-  }
+  b->pad_rowpair = b->grid_mode && b->grid_flags && b->tap_evict_first;
   if (b->pad_rowpair) {
     b->pad_copies = 8;
     b->pad_plane = size_t((b->H + 2) / 2 + 1) * 2 * b->pad_pitch;
@@ -4411,7 +4416,7 @@ static int register_many_impl(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* me
       const char* why = nullptr;  // cluster (1) or whole-GPU grid (2) fp32 path
       const bool f32_ok = cfg->precision == MRB_PREC_F32 &&
                           fast_mode(false, false, img_dtype, all, &why) != 0;
-      dev_setup = fits && !std::getenv("MESHREG_B200_HOST_SETUP") && config_error(cfg).empty() &&
+      dev_setup = fits && config_error(cfg).empty() &&
                   img_dtype == MRB_F32 && (f32_ok || f64_ok);
       dev64 = dev_setup && f64_ok;
       if (!dev_setup) {
