@@ -816,7 +816,7 @@ def run_pixel(args, rank, world, local):
     es = 4 if args.precision == "f32" else 8
     bytes_launch = float(P) * npx * 6 * es  # read u, write u, read (Te, Re): 3 pairs of Real
     achieved = bytes_launch / (kt[0] / 1e3) / 1e9
-    ncu = ncu_record("pixel", args.precision, "k_pixel_iter")
+    ncu = ncu_record("pixel", args.precision, "k_pixel_step")
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tot, work = 0.0, 0.0
@@ -845,8 +845,8 @@ def run_pixel(args, rank, world, local):
                        "parallelism": f"pair-sharded dp{world} (no collective)",
                        "precision": args.precision},
             "gpu_launches": launches,
-            "kernel_ms": {"k_pixel_iter": round(float(kt[0]), 5), "run": round(float(kt[1]), 4)},
-            "roofline": roofline_block("k_pixel_iter", achieved, peak, ncu, kt[0],
+            "kernel_ms": {"k_pixel_step": round(float(kt[0]), 5), "run": round(float(kt[1]), 4)},
+            "roofline": roofline_block("k_pixel_step", achieved, peak, ncu, kt[0],
                                        "algorithmic bytes = read u + write u + read (Te, Re) per "
                                        "pixel per iteration"),
             "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,

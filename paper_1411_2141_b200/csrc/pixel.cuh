@@ -3,16 +3,22 @@
 // gradient of the template (image.py:86-103), `passes` 4-neighbour umbrella
 // smoothing passes (baseline.py:27-43), clamp, `iterations` times.
 //
-// B200 design: one fused kernel per iteration with temporal blocking.  A CTA
-// owns a TX x TY tile; it samples Te, Re and dTe/dx, dTe/dy (from the same 16
-// taps) for the tile plus a halo of `passes` pixels, applies the descent,
-// runs every smoothing pass in shared memory (the valid region shrinks by one
-// pixel per pass), clamps and writes its tile of u to the other buffer of a
-// double-buffered pair of planes.  HBM traffic per pixel and iteration: read
-// u, write u (the image taps hit L1/L2).  The fp64 energy partial of each CTA
-// goes to partials[iteration][block]; the trace and the divergence logic are
-// evaluated in a fixed order after the loop (the pixel engine has no early
-// exit, so the decisions only depend on the trace).
+// B200 design: one fused kernel per iteration, ordered smooth-then-sample.
+// A CTA owns a TX x TY tile.  Launch k reads the descended planes of
+// iteration k-1 (tile + a halo of `passes` pixels, one TMA box), runs the
+// smoothing passes in shared memory (the valid region shrinks by one pixel
+// per pass, the last pass fused with the tile phase), clamps, and then
+// samples Te, Re and dTe/dx, dTe/dy (from the same 16 taps, a TMA-staged
+// image patch) for the tile's OWN pixels only, applies the descent and
+// writes the descended planes.  Sampling before smoothing (the reference's
+// order inside one iteration) would sample every halo pixel again in each
+// neighbouring tile (1.3 samples per pixel at 64x32 with a 3-pixel halo);
+// here each pixel is sampled once.  HBM traffic per pixel and iteration:
+// read the descended planes, write them, read the (Te, Re) patch.  The fp64
+// energy partial of each CTA goes to partials[iteration][block]; the trace
+// and the divergence logic are evaluated in a fixed order after the loop
+// (the pixel engine has no early exit, so the decisions only depend on the
+// trace).
 #pragma once
 
 #include <cuda.h>
@@ -22,10 +28,10 @@
 namespace mrb {
 
 constexpr int kPixThreads = 512, kPixMaxR = 3;
-// tile per CTA: 64x32 (fp32 state) / 32x32 (fp64 state); the (TX+2R)x(TY+2R)
-// ping-pong state tiles stay under the 48 KB static shared-memory limit
+// tile per CTA: 64x32 (fp32 state) / 32x32 (fp64 state): four / two tile
+// cells per thread
 template <typename Real> struct PixTile {
-  static constexpr int TX = sizeof(Real) == 4 ? 64 : 32, TY = sizeof(Real) == 4 ? 32 : 24;
+  static constexpr int TX = sizeof(Real) == 4 ? 64 : 32, TY = 32;
 };
 
 template <typename Real>
@@ -33,30 +39,36 @@ struct PixelDev {
   using R2 = typename V2<Real>::type;
   const R2* img;     // padded (H+2) rows x (W+2) of interleaved (Te, Re), ring
                      // included, row pitch `pitch` elements (16-byte multiple)
-  const CUtensorMap* tmap;  // TMA descriptor of img (2-D, Real elements)
-  R2* u[2];          // double-buffered (ux, uy) planes, H x W
+  const CUtensorMap* tmap;  // TMA descriptor of img (2-D, 8-byte elements)
+  const CUtensorMap* umap;  // TMA descriptor of the descended planes w[0..1]
+                            // (3-D: x, y, buffer; 8-byte elements)
+  R2* w[2];          // double-buffered descended (ux, uy) planes, H x wpitch
+  R2* u;             // final (ux, uy) plane, H x W
   Real* warped;      // H x W
   double* partials;  // [iterations][tiles]
-  int W, H, pitch, tiles_x, tiles;
+  int W, H, pitch, wpitch, tiles_x, tiles;
 };
 
-// Shared-memory patch of the padded image staged by TMA per tile: region
-// + Catmull-Rom footprint (3) + displacement margin kPixD on each side.
-constexpr int kPixD = 4;
-// The patch is sized for the largest halo (kPixMaxR) so one TMA descriptor
-// (box) per pair serves every R; its origin is (x0, y0) - kPixMaxR - kPixD.
-template <typename Real, int R> struct PixPatch {
-  static constexpr int RW = PixTile<Real>::TX + 2 * R, RH = PixTile<Real>::TY + 2 * R;
-  // margin left/top of the tile, even: a TMA box must start on a 16-byte
-  // boundary of the row (x0 is a multiple of TX)
-  static constexpr int M = (kPixMaxR + kPixD + 1) / 2 * 2;
-  static constexpr int PW0 = PixTile<Real>::TX + 2 * M + 3;
-  // inner box bytes a multiple of 16
-  static constexpr int PW = sizeof(Real) == 4 ? (PW0 + 1) / 2 * 2 : PW0;
-  static constexpr int PH = PixTile<Real>::TY + 2 * M + 3;
+// Shared-memory layout of k_pixel_step for a tile (x0, y0):
+//  * patch: the padded (Te, Re) image around the tile, staged by TMA, for
+//    the samples: tile + Catmull-Rom footprint (3) + displacement margin
+//    kPixD, origin (x0 - kPixD, y0 - kPixD) in padded coordinates (even x: a
+//    TMA box starts on a 16-byte boundary of the row);
+//  * two state buffers of the tile + the smoothing halo, kPixMaxR rows and
+//    kPixHX >= kPixMaxR (even) columns on each side, origin (x0 - kPixHX,
+//    y0 - kPixMaxR); the descended planes land in buffer 0 by TMA (zero
+//    outside the image).
+// One box per tensor map serves every halo R <= kPixMaxR.
+constexpr int kPixD = 4, kPixHX = 4;
+template <typename Real> struct PixPatch {
+  static constexpr int TX = PixTile<Real>::TX, TY = PixTile<Real>::TY;
+  static constexpr int PW = (TX + 2 * kPixD + 3 + 1) / 2 * 2, PH = TY + 2 * kPixD + 3;
+  static constexpr int BW = TX + 2 * kPixHX, BH = TY + 2 * kPixMaxR;
   static constexpr size_t patch_bytes = size_t(PW) * PH * 2 * sizeof(Real);
-  static constexpr size_t buf_bytes = size_t(RW) * RH * 2 * sizeof(Real);
-  static constexpr size_t smem_bytes = patch_bytes + 2 * buf_bytes;
+  static constexpr size_t buf_bytes = size_t(BW) * BH * 2 * sizeof(Real);
+  // the state buffers start 128-byte aligned (TMA shared-memory destination)
+  static constexpr size_t buf_off = (patch_bytes + 127) / 128 * 128;
+  static constexpr size_t smem_bytes = buf_off + 2 * buf_bytes;
 };
 
 __device__ __forceinline__ unsigned pix_smem_u32(const void* p) {
@@ -241,183 +253,179 @@ __device__ __forceinline__ double2 blend2(double om, double2 self, double lq, do
                       __dadd_rn(__dmul_rn(om, self.y), __dmul_rn(lq, tot.y)));
 }
 
-// One grid_umbrella_smooth pass (baseline.py:27-43) over the cells of the
-// region at margin M (TX + 2(R-M)) x (TY + 2(R-M)).  INTERIOR: every such
-// cell and its four neighbours lie inside the image (count = 4).  Otherwise
-// out-of-image cells are skipped and hold zero, so a missing neighbour adds
-// +0 exactly like the reference's zero-initialised total.
-template <typename Real, int TX, int TY, int R, int M, bool INTERIOR>
-__device__ __forceinline__ void smooth_pass(const typename V2<Real>::type* __restrict__ b,
-                                            typename V2<Real>::type* __restrict__ o, int gx0,
-                                            int gy0, int W, int H, Real om, Real lam) {
+// One grid_umbrella_smooth cell (baseline.py:27-43) at buffer index q
+// (pixel (gx, gy)) from buffer b of row width BW.  INTERIOR: the cell and
+// its four neighbours lie inside the image (count = 4).  Otherwise cells
+// outside the image hold zero (returned as zero), so a missing neighbour
+// adds +0 exactly like the reference's zero-initialised total.
+template <typename Real, int BW, bool INTERIOR>
+__device__ __forceinline__ typename V2<Real>::type smooth_cell(
+    const typename V2<Real>::type* __restrict__ b, int q, int gx, int gy, int W, int H, Real om,
+    Real lam) {
   using R2 = typename V2<Real>::type;
-  constexpr int RW = TX + 2 * R, w = RW - 2 * M, h = TY + 2 * R - 2 * M;
-  constexpr int n = w * h;
   const Real lq4 = lam * Real(0.25);  // exact
+  if (!INTERIOR && (gx < 0 || gx >= W || gy < 0 || gy >= H)) return R2{Real(0), Real(0)};
+  const R2 tot = add2(add2(add2(b[q - BW], b[q + BW]), b[q - 1]), b[q + 1]);
+  if (INTERIOR || (gx > 0 && gx < W - 1 && gy > 0 && gy < H - 1)) return blend2(om, b[q], lq4, tot);
+  const int cnt = (gy > 0) + (gy < H - 1) + (gx > 0) + (gx < W - 1);
+  if (cnt == 4) return blend2(om, b[q], lq4, tot);
+  if (cnt == 2) return blend2(om, b[q], lam * Real(0.5), tot);
+  // count 3 (or 0 for a 1-pixel plane: 0 / 0 like numpy)
+  const R2 self = b[q];
+  R2 v;
+  v.x = add_rn(mul_rn(om, self.x), div_rn(mul_rn(lam, tot.x), Real(cnt)));
+  v.y = add_rn(mul_rn(om, self.y), div_rn(mul_rn(lam, tot.y), Real(cnt)));
+  return v;
+}
+
+// Smoothing passes M = MM..R-1 of R in shared memory: pass M covers the
+// cells at margin M of the tile's R-halo region, (TX + 2(R-M)) x
+// (TY + 2(R-M)), reading buffer (M-1)&1 and writing buffer M&1.  Pass R is
+// fused into the tile phase of k_pixel_step.
+template <typename Real, int R, int MM, bool INTERIOR>
+__device__ __forceinline__ void smooth_passes(
+    typename V2<Real>::type (*buf)[PixPatch<Real>::BW * PixPatch<Real>::BH], int x0, int y0,
+    int W, int H, Real om, Real lam) {
+  if constexpr (MM < R) {
+    using PP = PixPatch<Real>;
+    constexpr int BW = PP::BW, w = PP::TX + 2 * (R - MM), h = PP::TY + 2 * (R - MM);
+    // buffer coordinates of the pass region's first cell
+    constexpr int bx0 = kPixHX - R + MM, by0 = kPixMaxR - R + MM;
+    const auto* __restrict__ b = buf[(MM - 1) & 1];
+    auto* __restrict__ o = buf[MM & 1];
 #pragma unroll 2
-  for (int c = threadIdx.x; c < n; c += kPixThreads) {
-    const int cy = c / w, cx = c - cy * w;  // constant divisor
-    const int rx = cx + M, ry = cy + M;
-    const int q = ry * RW + rx;
-    if (!INTERIOR) {
-      const int gx = gx0 + rx, gy = gy0 + ry;
-      if (gx < 0 || gx >= W || gy < 0 || gy >= H) continue;
-      const R2 tot = add2(add2(add2(b[q - RW], b[q + RW]), b[q - 1]), b[q + 1]);
-      if (gx > 0 && gx < W - 1 && gy > 0 && gy < H - 1) {  // most cells of a border tile
-        o[q] = blend2(om, b[q], lq4, tot);
-        continue;
-      }
-      const int cnt = (gy > 0) + (gy < H - 1) + (gx > 0) + (gx < W - 1);
-      R2 v;
-      if (cnt == 4) {
-        v = blend2(om, b[q], lq4, tot);
-      } else if (cnt == 2) {
-        v = blend2(om, b[q], lam * Real(0.5), tot);
-      } else {  // count 3 (or 0 for a 1-pixel plane: 0 / 0 like numpy)
-        const R2 self = b[q];
-        v.x = add_rn(mul_rn(om, self.x), div_rn(mul_rn(lam, tot.x), Real(cnt)));
-        v.y = add_rn(mul_rn(om, self.y), div_rn(mul_rn(lam, tot.y), Real(cnt)));
-      }
-      o[q] = v;
-    } else {
-      const R2 tot = add2(add2(add2(b[q - RW], b[q + RW]), b[q - 1]), b[q + 1]);
-      o[q] = blend2(om, b[q], lq4, tot);
+    for (int c = threadIdx.x; c < w * h; c += kPixThreads) {
+      const int cy = c / w, cx = c - cy * w;  // constant divisor
+      const int bx = bx0 + cx, by = by0 + cy;
+      o[by * BW + bx] = smooth_cell<Real, BW, INTERIOR>(b, by * BW + bx, x0 + bx - kPixHX,
+                                                       y0 + by - kPixMaxR, W, H, om, lam);
     }
-  }
-}
-
-template <typename Real, int TX, int TY, int R, int M, bool INTERIOR>
-__device__ __forceinline__ void smooth_passes(typename V2<Real>::type (*buf)[(TX + 2 * R) * (TY + 2 * R)],
-                                              int gx0, int gy0, int W, int H, Real om, Real lam) {
-  if constexpr (M <= R) {
-    smooth_pass<Real, TX, TY, R, M, INTERIOR>(buf[(M - 1) & 1], buf[M & 1], gx0, gy0, W, H, om,
-                                              lam);
     __syncthreads();
-    smooth_passes<Real, TX, TY, R, M + 1, INTERIOR>(buf, gx0, gy0, W, H, om, lam);
+    smooth_passes<Real, R, MM + 1, INTERIOR>(buf, x0, y0, W, H, om, lam);
   }
 }
 
-// One pixel-engine iteration for a TX x TY tile with a halo of R passes
-// (baseline.py:74-101): sample + gradient + descent on the (TX+2R)x(TY+2R)
-// region, R smoothing passes in shared memory, clamp, store.  descend = 0:
-// smoothing-only launch (passes beyond kPixMaxR); clamp = 0: more passes
-// follow in another launch.
+// One launch of the pixel engine for a TX x TY tile (baseline.py:74-101),
+// ordered smooth-then-sample so no halo cell is sampled:
+//   load:   TMA the previous launch's descended planes (tile + R halo) into
+//           shared memory (else the state is zero: iteration 0);
+//   R smoothing passes (R-1 in shared memory, the last fused with the tile
+//   phase); clamp (after the iteration's last pass);
+//   sample: Te, Re and the analytic gradient of Te at the smoothed u of the
+//           tile's own pixels (iteration k's energy partial), descent, store
+//           the descended planes to w[dst];
+//   final:  store u (the registration result) instead.
+// Without clamp / sample / final the launch is an extra smoothing launch
+// (passes beyond kPixMaxR) that stores to w[dst].
 template <typename Real, int R>
 __global__ void __launch_bounds__(kPixThreads, 2)
-    k_pixel_iter(const PixelDev<Real>* __restrict__ pairs, int k, int src, Real tau, Real lam,
-                 int descend, int clamp) {
+    k_pixel_step(const PixelDev<Real>* __restrict__ pairs, int k, int src, Real tau, Real lam,
+                 int load, int clamp, int sample, int final_out) {
   using R2 = typename V2<Real>::type;
-  using PP = PixPatch<Real, R>;
-  constexpr int TX = PixTile<Real>::TX, TY = PixTile<Real>::TY;
-  constexpr int RW = PP::RW, RH = PP::RH, PW = PP::PW, PH = PP::PH;
+  using PP = PixPatch<Real>;
+  constexpr int TX = PP::TX, TY = PP::TY, BW = PP::BW, PW = PP::PW, PH = PP::PH;
   extern __shared__ __align__(128) unsigned char pix_smem[];
   R2* patch = reinterpret_cast<R2*>(pix_smem);
-  auto buf = reinterpret_cast<R2(*)[RW * RH]>(pix_smem + PP::patch_bytes);
+  auto buf = reinterpret_cast<R2(*)[PP::BW * PP::BH]>(pix_smem + PP::buf_off);
   __shared__ double sh[2 * kPixThreads / 32];
   __shared__ __align__(8) unsigned long long mbar;
   const PixelDev<Real>& d = pairs[blockIdx.y];
   const int tile = blockIdx.x;
   const int x0 = (tile % d.tiles_x) * TX, y0 = (tile / d.tiles_x) * TY;
-  const R2* __restrict__ uin = d.u[src];
-  R2* __restrict__ uout = d.u[src ^ 1];
   const int W = d.W, H = d.H;
-  const int gx0 = x0 - R, gy0 = y0 - R;  // pixel of region cell (0, 0)
   // patch origin in padded-image coordinates (may be negative: TMA zero-fills)
-  const int px0 = x0 - PP::M, py0 = y0 - PP::M;
-  constexpr bool use_tma = true;
-  descend &= 1;
-  if (descend && use_tma && threadIdx.x == 0) {
-    const unsigned mb = pix_smem_u32(&mbar);
+  const int px0 = x0 - kPixD, py0 = y0 - kPixD;
+  constexpr int epr = int(sizeof(R2) / 8);  // 8-byte TMA elements per R2
+  const unsigned mb = pix_smem_u32(&mbar);
+  if ((load || sample) && threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
-                 "r"(unsigned(PP::patch_bytes))
+    const unsigned bytes =
+        unsigned((sample ? PP::patch_bytes : 0) + (load ? PP::buf_bytes : 0));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
                  : "memory");
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(pix_smem_u32(patch)),
-        "l"(reinterpret_cast<unsigned long long>(d.tmap)), "r"(int(sizeof(R2) / 8) * px0), "r"(py0), "r"(mb)
-        : "memory");
+    if (load)
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(pix_smem_u32(buf[0])),
+          "l"(reinterpret_cast<unsigned long long>(d.umap)), "r"(epr * (x0 - kPixHX)),
+          "r"(y0 - kPixMaxR), "r"(src), "r"(mb)
+          : "memory");
+    if (sample)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3}], [%4];" ::"r"(pix_smem_u32(patch)),
+          "l"(reinterpret_cast<unsigned long long>(d.tmap)), "r"(epr * px0), "r"(py0), "r"(mb)
+          : "memory");
   }
   __syncthreads();  // mbarrier initialised before anyone waits on it
-  bool patch_ready = false;
+  if (load || sample)
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(mb)
+        : "memory");
+  const Real om = sub_rn(Real(1), lam);
+  // every smoothed cell and its neighbours inside the image?
+  const bool interior = x0 >= R && y0 >= R && x0 + TX + R <= W && y0 + TY + R <= H;
+  if constexpr (R > 1) {
+    if (load) {
+      if (interior)
+        smooth_passes<Real, R, 1, true>(buf, x0, y0, W, H, om, lam);
+      else
+        smooth_passes<Real, R, 1, false>(buf, x0, y0, W, H, om, lam);
+    }
+  }
+  const R2* __restrict__ last = buf[(R - 1) & 1];  // input of the fused pass R
+  R2* __restrict__ wout = d.w[src ^ 1];
   double e2 = 0.0;
-  // u of a region cell (zero outside the image); the next cell's u is loaded
-  // before this cell's sample so its latency overlaps the arithmetic
-  auto load_u = [&](int c) {
-    const int ry = c / RW, rx = c - ry * RW;
-    const int gx = gx0 + rx, gy = gy0 + ry;
-    return (c < RW * RH && gx >= 0 && gx < W && gy >= 0 && gy < H) ? uin[size_t(gy) * W + gx]
-                                                                   : R2{Real(0), Real(0)};
-  };
-  R2 u_next = load_u(threadIdx.x);
 #pragma unroll 1
-  for (int c = threadIdx.x; c < RW * RH; c += kPixThreads) {
-    const int ry = c / RW, rx = c - ry * RW;
-    const int gx = gx0 + rx, gy = gy0 + ry;
-    const R2 u = u_next;
-    u_next = load_u(c + kPixThreads);
-    if (gx < 0 || gx >= W || gy < 0 || gy >= H) {
-      buf[0][c] = R2{Real(0), Real(0)};
-      buf[1][c] = R2{Real(0), Real(0)};
+  for (int c = threadIdx.x; c < TX * TY; c += kPixThreads) {
+    const int ty = c / TX, tx = c - ty * TX;
+    const int gy = y0 + ty, gx = x0 + tx;
+    if (gx >= W || gy >= H) continue;
+    const int q = (ty + kPixMaxR) * BW + tx + kPixHX;
+    R2 u = R2{Real(0), Real(0)};
+    if (load) {
+      if constexpr (R > 0) {
+        u = interior ? smooth_cell<Real, BW, true>(last, q, gx, gy, W, H, om, lam)
+                     : smooth_cell<Real, BW, false>(last, q, gx, gy, W, H, om, lam);
+      } else {
+        u = buf[0][q];
+      }
+    }
+    if (clamp) {  // np.clip(u, -x, (w - 1) - x), baseline.py:100-101; the
+      // bounds are integers, exact in Real.  NaN propagates like np.clip.
+      if (u.x == u.x) u.x = fmin(fmax(u.x, Real(-gx)), Real(W - 1 - gx));
+      if (u.y == u.y) u.y = fmin(fmax(u.y, Real(-gy)), Real(H - 1 - gy));
+    }
+    if (final_out) {
+      d.u[size_t(gy) * W + gx] = u;
       continue;
     }
-    if (!descend) {
-      buf[0][c] = u;
+    if (!sample) {
+      wout[size_t(gy) * d.wpitch + gx] = u;
       continue;
     }
     int cx, cy;
-    Real tx, ty;
-    locate_axis<Real>(gx, u.x, W, cx, tx);
-    locate_axis<Real>(gy, u.y, H, cy, ty);
-    if (!patch_ready && use_tma) {  // first sample of this thread: wait for the TMA patch
-      const unsigned mb = pix_smem_u32(&mbar);
-      asm volatile(
-          "{\n .reg .pred p;\n WAIT_%=:\n"
-          " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
-          " @!p bra WAIT_%=;\n}" ::"r"(mb)
-          : "memory");
-      patch_ready = true;
-    }
+    Real tx_, ty_;
+    locate_axis<Real>(gx, u.x, W, cx, tx_);
+    locate_axis<Real>(gy, u.y, H, cy, ty_);
     R2 s, g;
     const int lx = cx - px0, ly = cy - py0;  // footprint inside the patch?
-    if (use_tma && lx >= 0 && lx <= PW - 4 && ly >= 0 && ly <= PH - 4)
-      sample_with_gradient<Real, true>(patch, PW, lx, ly, tx, ty, s, g);
+    if (lx >= 0 && lx <= PW - 4 && ly >= 0 && ly <= PH - 4)
+      sample_with_gradient<Real, true>(patch, PW, lx, ly, tx_, ty_, s, g);
     else  // displaced beyond kPixD: read the padded image in global memory
-      sample_with_gradient<Real>(d.img, d.pitch, cx, cy, tx, ty, s, g);
+      sample_with_gradient<Real>(d.img, d.pitch, cx, cy, tx_, ty_, s, g);
     const Real r = sub_rn(s.x, s.y);
     const Real tr = mul_rn(tau, r);  // ux - tau * r * dTe/dx  (baseline.py:94-95)
     R2 o;
     o.x = sub_rn(u.x, mul_rn(tr, g.x));
     o.y = sub_rn(u.y, mul_rn(tr, g.y));
-    buf[0][c] = o;
-    if (rx >= R && rx < R + TX && ry >= R && ry < R + TY) e2 = fma(double(r), double(r), e2);
+    wout[size_t(gy) * d.wpitch + gx] = o;
+    e2 = fma(double(r), double(r), e2);
   }
-  __syncthreads();
-  if constexpr (R > 0) {
-    const Real om = sub_rn(Real(1), lam);
-    // every smoothed cell and its neighbours inside the image?
-    const bool interior = x0 >= R && y0 >= R && x0 + TX + R <= W && y0 + TY + R <= H;
-    if (interior)
-      smooth_passes<Real, TX, TY, R, 1, true>(buf, gx0, gy0, W, H, om, lam);
-    else
-      smooth_passes<Real, TX, TY, R, 1, false>(buf, gx0, gy0, W, H, om, lam);
-  }
-  const R2* __restrict__ fin = buf[R & 1];
-#pragma unroll 2
-  for (int c = threadIdx.x; c < TX * TY; c += kPixThreads) {
-    const int ty = c / TX, tx = c - ty * TX;
-    const int gy = y0 + ty, gx = x0 + tx;
-    if (gx >= W || gy >= H) continue;
-    R2 o = fin[(ty + R) * RW + tx + R];
-    if (clamp) {  // np.clip(u, -x, (w - 1) - x), baseline.py:100-101; the
-      // bounds are integers, exact in Real.  NaN propagates like np.clip.
-      if (o.x == o.x) o.x = fmin(fmax(o.x, Real(-gx)), Real(W - 1 - gx));
-      if (o.y == o.y) o.y = fmin(fmax(o.y, Real(-gy)), Real(H - 1 - gy));
-    }
-    uout[size_t(gy) * W + gx] = o;
-  }
-  if (!descend) return;
+  if (!sample) return;
   const double bs = block_sum<kPixThreads>(e2, sh);
   if (threadIdx.x == 0) d.partials[size_t(k) * d.tiles + tile] = bs;
 }
@@ -476,7 +484,7 @@ __global__ void __launch_bounds__(kPixBlock)
   double2 acc = make_double2(0.0, 0.0);
   if (q < d.W * d.H && !st[p].err) {
     const int y = q / d.W, x = q - y * d.W;
-    const auto u = d.u[src][q];
+    const auto u = d.u[q];
     if (!isfinite(u.x) || !isfinite(u.y)) atomicOr(const_cast<int*>(&st[p].dense_nonfinite), 1);
     typename V2<Real>::type s, g;
     int cx, cy;

@@ -17,8 +17,10 @@ struct mrb_pixel_batch {
   void* img = nullptr;         // padded (Te, Re) per pair
   int pitch = 0;               // padded row pitch (R2 elements)
   size_t img_stride = 0;       // R2 elements between pairs
-  CUtensorMap* tmaps = nullptr;  // device: TMA descriptor per pair
-  void* u = nullptr;           // [2][pair][H*W] (ux, uy)
+  CUtensorMap* tmaps = nullptr;  // device: TMA descriptors, image + planes per pair
+  void* u = nullptr;           // [pair][H*W] final (ux, uy)
+  void* wbuf = nullptr;        // [2][pair][H*wpitch] descended (ux, uy)
+  int wpitch = 0;
   void* warped = nullptr;      // [pair][H*W]
   void* stage = nullptr;
   void* conv = nullptr;
@@ -31,7 +33,7 @@ struct mrb_pixel_batch {
   bool synced = false;
   ~mrb_pixel_batch() {
     if (graph) cudaGraphExecDestroy(graph);
-    void* ptrs[] = {pairs, st, partials, msd_partials, traces, img, u, warped, stage, conv,
+    void* ptrs[] = {pairs, st, partials, msd_partials, traces, img, u, wbuf, warped, stage, conv,
                     const_cast<void**>(src_ptrs), tmaps};
     for (void* p : ptrs) dev_free(p, ctx ? ctx->stream : nullptr);
   }
@@ -52,10 +54,17 @@ int pixel_passes(const mrb_pixel_config& c) {
   return c.lam > 0.0 ? std::max(c.smoothing_passes, 0) : 0;
 }
 
-// launches of the fused iteration kernel per iteration
-int pixel_iter_launches(const mrb_pixel_config& c) {
+// extra smoothing launches (passes beyond kPixMaxR) before each step launch
+// after the first
+int pixel_extra_launches(const mrb_pixel_config& c) {
   const int p = pixel_passes(c);
-  return p <= kPixMaxR ? 1 : 1 + (p - kPixMaxR + kPixMaxR - 1) / kPixMaxR;
+  return p <= kPixMaxR ? 0 : (p - kPixMaxR + kPixMaxR - 1) / kPixMaxR;
+}
+
+// k_pixel_step launches per run: iteration 0 (sample only), iterations
+// 1..n-1 and the final smoothing (each after its extra launches)
+int64_t pixel_step_launches(const mrb_pixel_config& c) {
+  return int64_t(c.iterations) + 1 + int64_t(c.iterations) * pixel_extra_launches(c);
 }
 
 template <typename Real>
@@ -65,13 +74,14 @@ size_t pixel_tile_counts(int W, int H, int* tiles_x) {
 }
 
 template <typename Real>
-void launch_pixel_iter(const mrb_pixel_batch* b, const PixelDev<Real>* pairs, int k, int src,
-                       Real tau, Real lam, int r, int descend, int clamp) {
+void launch_pixel_step(const mrb_pixel_batch* b, const PixelDev<Real>* pairs, int k, int src,
+                       Real tau, Real lam, int r, int load, int clamp, int sample,
+                       int final_out) {
   const dim3 grid(b->tiles, b->n_pairs);
   cudaStream_t s = b->ctx->stream;
-#define MRB_PIX_LAUNCH(RR)                                                              \
-  k_pixel_iter<Real, RR><<<grid, kPixThreads, PixPatch<Real, RR>::smem_bytes, s>>>(     \
-      pairs, k, src, tau, lam, descend, clamp)
+#define MRB_PIX_LAUNCH(RR)                                                          \
+  k_pixel_step<Real, RR><<<grid, kPixThreads, PixPatch<Real>::smem_bytes, s>>>(     \
+      pairs, k, src, tau, lam, load, clamp, sample, final_out)
   switch (r) {
     case 0: MRB_PIX_LAUNCH(0); break;
     case 1: MRB_PIX_LAUNCH(1); break;
@@ -83,8 +93,8 @@ void launch_pixel_iter(const mrb_pixel_batch* b, const PixelDev<Real>* pairs, in
 
 template <typename Real, int RR>
 void pixel_smem_attr() {
-  ck(cudaFuncSetAttribute(k_pixel_iter<Real, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          int(PixPatch<Real, RR>::smem_bytes)));
+  ck(cudaFuncSetAttribute(k_pixel_step<Real, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          int(PixPatch<Real>::smem_bytes)));
 }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -125,31 +135,37 @@ void pixel_enqueue_t(mrb_pixel_batch* b, KernelTimer* tm) {
           static_cast<R2*>(b->img), b->img_stride);
     ck(cudaGetLastError());
   }
-  ck(cudaMemsetAsync(b->u, 0, size_t(n) * npx * sizeof(R2), s));  // u0 = 0 (buffer 0)
   const int passes = pixel_passes(b->cfg);
   const Real tau = Real(b->cfg.tau), lam = Real(b->cfg.lam);
-  int src = 0;
-  for (int k = 0; k < b->cfg.iterations; ++k) {
-    int r = std::min(passes, kPixMaxR), rem = passes - r;
-    if (tm) tm->mark(0);
-    launch_pixel_iter<Real>(b, pairs, k, src, tau, lam, r, 1, rem == 0);
-    if (tm) tm->mark(1);
-    if (std::getenv("MESHREG_B200_DEBUG")) {
+  const int r_last = std::min(passes, kPixMaxR);  // passes of each step launch
+  const bool dbg = std::getenv("MESHREG_B200_DEBUG") != nullptr;
+  int src = 1;  // descended planes of the previous launch: w[src]
+  for (int k = 0; k <= b->cfg.iterations; ++k) {
+    if (k > 0) {  // extra smoothing launches (passes beyond kPixMaxR)
+      for (int rem = passes - r_last; rem > 0;) {
+        const int r = std::min(rem, kPixMaxR);
+        rem -= r;
+        launch_pixel_step<Real>(b, pairs, k, src, tau, lam, r, 1, 0, 0, 0);
+        src ^= 1;
+      }
+    }
+    const bool last = k == b->cfg.iterations;
+    if (tm && !last) tm->mark(0);
+    // iteration 0 samples u = 0; iteration k > 0 smooths + clamps the
+    // previous descent first; the final launch only smooths + clamps
+    launch_pixel_step<Real>(b, pairs, k, src, tau, lam, k > 0 ? r_last : 0, k > 0, k > 0,
+                            !last, last);
+    if (tm && !last) tm->mark(1);
+    if (dbg) {
       ck(cudaStreamSynchronize(s));
       ck(cudaGetLastError());
     }
     src ^= 1;
-    while (rem > 0) {
-      r = std::min(rem, kPixMaxR);
-      rem -= r;
-      launch_pixel_iter<Real>(b, pairs, k, src, tau, lam, r, 0, rem == 0);
-      src ^= 1;
-    }
   }
   ck(cudaGetLastError());
-  b->final_src = src;
+  b->final_src = 0;
   k_pixel_trace<Real><<<n, kPixBlock, 0, s>>>(pairs, b->cfg.iterations, b->traces, b->st);
-  k_pixel_warp<Real><<<dim3(b->warp_blocks, n), kPixBlock, 0, s>>>(pairs, src, b->st,
+  k_pixel_warp<Real><<<dim3(b->warp_blocks, n), kPixBlock, 0, s>>>(pairs, 0, b->st,
                                                                    b->msd_partials,
                                                                    b->warp_blocks);
   k_pixel_msd<<<n, kPixBlock, 0, s>>>(b->msd_partials, b->warp_blocks, double(npx), b->st);
@@ -180,7 +196,11 @@ void pixel_setup_t(mrb_pixel_batch* b) {
   pixel_smem_attr<Real, 1>();
   pixel_smem_attr<Real, 2>();
   pixel_smem_attr<Real, 3>();
-  b->u = dalloc<R2>(2 * size_t(n) * npx);
+  b->u = dalloc<R2>(size_t(n) * npx);
+  // descended planes: rows padded to a 16-byte multiple (TMA global stride)
+  b->wpitch = sizeof(R2) == 8 ? (b->W + 1) / 2 * 2 : b->W;
+  const size_t wplane = size_t(b->wpitch) * b->H;
+  b->wbuf = dalloc<R2>(2 * size_t(n) * wplane);
   b->warped = dalloc<Real>(size_t(n) * npx);
   b->partials = dalloc<double>(size_t(n) * b->cfg.iterations * b->tiles);
   b->msd_partials = dalloc<double2>(size_t(n) * b->warp_blocks);
@@ -188,19 +208,19 @@ void pixel_setup_t(mrb_pixel_batch* b) {
   b->st = dalloc<PairStatus>(n);
   b->src_ptrs = dalloc<const void*>(2 * size_t(n));
   std::vector<PixelDev<Real>> h(n);
-  std::vector<CUtensorMap> maps(n);
-  b->tmaps = dalloc<CUtensorMap>(n);
+  std::vector<CUtensorMap> maps(2 * size_t(n));
+  b->tmaps = dalloc<CUtensorMap>(2 * size_t(n));
   for (int p = 0; p < n; ++p) {
     PixelDev<Real>& d = h[p];
     d.img = static_cast<const R2*>(b->img) + size_t(p) * b->img_stride;
     // 2-D view of the padded image in Real elements, (2 * pitch) x (H + 2);
-    // box = the k_pixel_iter patch (same for every halo R)
+    // box = the k_pixel_step image patch (same for every halo R)
     // (8-byte elements: one per float2, two per double2)
     constexpr int epr = int(sizeof(R2) / 8);
     const cuuint64_t gdim[2] = {cuuint64_t(epr) * b->pitch, cuuint64_t(b->H + 2)};
     const cuuint64_t gstride[1] = {cuuint64_t(b->pitch) * sizeof(R2)};
-    const cuuint32_t box[2] = {cuuint32_t(epr * PixPatch<Real, kPixMaxR>::PW),
-                               cuuint32_t(PixPatch<Real, kPixMaxR>::PH)};
+    const cuuint32_t box[2] = {cuuint32_t(epr * PixPatch<Real>::PW),
+                               cuuint32_t(PixPatch<Real>::PH)};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult cr = encode_tiled()(
         &maps[p], CU_TENSOR_MAP_DATA_TYPE_UINT64,
@@ -209,9 +229,26 @@ void pixel_setup_t(mrb_pixel_batch* b) {
         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) throw CudaError{cudaErrorInvalidValue};
     d.tmap = b->tmaps + p;
+    // 3-D view of the descended planes (x, y, buffer): W x H x 2 with the row
+    // pitch wpitch (columns >= W read as zero), box = the state buffer
+    R2* w0 = static_cast<R2*>(b->wbuf) + size_t(p) * wplane;
+    const cuuint64_t udim[3] = {cuuint64_t(epr) * b->W, cuuint64_t(b->H), 2};
+    const cuuint64_t ustride[2] = {cuuint64_t(b->wpitch) * sizeof(R2),
+                                   cuuint64_t(n) * wplane * sizeof(R2)};
+    const cuuint32_t ubox[3] = {cuuint32_t(epr * PixPatch<Real>::BW),
+                                cuuint32_t(PixPatch<Real>::BH), 1};
+    const cuuint32_t ustr[3] = {1, 1, 1};
+    const CUresult cu = encode_tiled()(
+        &maps[n + p], CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, w0, udim, ustride, ubox, ustr,
+        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cu != CUDA_SUCCESS) throw CudaError{cudaErrorInvalidValue};
+    d.umap = b->tmaps + n + p;
+    d.w[0] = w0;
+    d.w[1] = w0 + size_t(n) * wplane;
+    d.wpitch = b->wpitch;
     d.pitch = b->pitch;
-    d.u[0] = static_cast<R2*>(b->u) + size_t(p) * npx;
-    d.u[1] = static_cast<R2*>(b->u) + (size_t(n) + p) * npx;
+    d.u = static_cast<R2*>(b->u) + size_t(p) * npx;
     d.warped = static_cast<Real*>(b->warped) + size_t(p) * npx;
     d.partials = b->partials + size_t(p) * b->cfg.iterations * b->tiles;
     d.W = b->W;
@@ -221,7 +258,8 @@ void pixel_setup_t(mrb_pixel_batch* b) {
   }
   b->pairs = dalloc<PixelDev<Real>>(n);
   ck(mrb_copy_async(b->pairs, h.data(), n * sizeof(PixelDev<Real>), cudaMemcpyHostToDevice, s));
-  ck(mrb_copy_async(b->tmaps, maps.data(), n * sizeof(CUtensorMap), cudaMemcpyHostToDevice, s));
+  ck(mrb_copy_async(b->tmaps, maps.data(), 2 * n * sizeof(CUtensorMap), cudaMemcpyHostToDevice,
+                    s));
   ck(cudaStreamSynchronize(s));  // h is a stack temporary
 }
 
@@ -464,7 +502,7 @@ int mrb_pixel_batch_pair_status(mrb_pixel_batch* b, int32_t p, int32_t* iters,
 }
 
 int64_t mrb_pixel_batch_launches_per_run(const mrb_pixel_batch* b) {
-  return 4 + int64_t(b->cfg.iterations) * pixel_iter_launches(b->cfg);  // + memset node
+  return 4 + pixel_step_launches(b->cfg);
 }
 
 int mrb_pixel_batch_kernel_times(mrb_pixel_batch* b, double* out) {

@@ -16,4 +16,4 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 ncu --set full --clock-control none --import-source on -k regex:"k_cluster_push|k_dense_fast" -s 3 -c 3 -o gpurun_out/${T}_c4_full $B $Q > gpurun_out/${T}_c4_ncu.log 2>&1; echo c4 ncu rc=$?
 ncu --set full --clock-control none --import-source on -k regex:"k_grid_flags" -s 1 -c 1 -o gpurun_out/${T}_c3_full $B --workload c3 $Q > gpurun_out/${T}_c3_ncu.log 2>&1; echo c3 ncu rc=$?
 ncu --set full --clock-control none -k regex:"k_grid_flags" -s 1 -c 1 -o gpurun_out/${T}_c5_full $B --workload c5 $Q > gpurun_out/${T}_c5_ncu.log 2>&1; echo c5 ncu rc=$?
-ncu --set full --clock-control none --import-source on -k regex:"k_pixel_iter" -s 5 -c 1 -o gpurun_out/${T}_pixel_full $B --workload pixel $Q > gpurun_out/${T}_pixel_ncu.log 2>&1; echo pixel ncu rc=$?
+ncu --set full --clock-control none --import-source on -k regex:"k_pixel_step" -s 5 -c 1 -o gpurun_out/${T}_pixel_full $B --workload pixel $Q > gpurun_out/${T}_pixel_ncu.log 2>&1; echo pixel ncu rc=$?
