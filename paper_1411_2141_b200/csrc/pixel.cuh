@@ -40,13 +40,25 @@ struct PixelDev {
   const R2* img;     // padded (H+2) rows x (W+2) of interleaved (Te, Re), ring
                      // included, row pitch `pitch` elements (16-byte multiple)
   const CUtensorMap* tmap;  // TMA descriptor of img (2-D, 8-byte elements)
-  const CUtensorMap* umap;  // TMA descriptor of the descended planes w[0..1]
-                            // (3-D: x, y, buffer; 8-byte elements)
-  R2* w[2];          // double-buffered descended (ux, uy) planes, H x wpitch
   R2* u;             // final (ux, uy) plane, H x W
   Real* warped;      // H x W
   double* partials;  // [iterations][tiles]
-  int W, H, pitch, wpitch, tiles_x, tiles;
+  int W, H, pitch, tiles_x, tiles;
+};
+
+// k_pixel_step's arguments: batch-uniform, passed by value (kernel
+// parameter space: no dependent global loads in the prologue); pair p's
+// arrays are at fixed strides from the bases
+template <typename Real>
+struct PixelStepArgs {
+  using R2 = typename V2<Real>::type;
+  const R2* img;            // padded pair images, img_stride elements apart
+  const CUtensorMap* tmap;  // [n] image maps, then [n] plane maps
+  R2* w;                    // descended planes: buffer b of pair p at (b n + p) wplane
+  R2* u;                    // final planes, H x W each
+  double* partials;         // [pair][iteration][tile]
+  size_t img_stride, wplane;
+  int n, iterations, W, H, pitch, wpitch, tiles_x, tiles;
 };
 
 // Shared-memory layout of k_pixel_step for a tile (x0, y0):
@@ -253,35 +265,63 @@ __device__ __forceinline__ double2 blend2(double om, double2 self, double lq, do
                       __dadd_rn(__dmul_rn(om, self.y), __dmul_rn(lq, tot.y)));
 }
 
-// One grid_umbrella_smooth cell (baseline.py:27-43) at buffer index q
-// (pixel (gx, gy)) from buffer b of row width BW.  INTERIOR: the cell and
-// its four neighbours lie inside the image (count = 4).  Otherwise cells
+// One grid_umbrella_smooth cell (baseline.py:27-43) of pixel (gx, gy) from
+// its value and its neighbour total ((N + S) + W) + E.  INTERIOR: the cell
+// and its four neighbours lie inside the image (count = 4).  Otherwise cells
 // outside the image hold zero (returned as zero), so a missing neighbour
 // adds +0 exactly like the reference's zero-initialised total.
-template <typename Real, int BW, bool INTERIOR>
-__device__ __forceinline__ typename V2<Real>::type smooth_cell(
-    const typename V2<Real>::type* __restrict__ b, int q, int gx, int gy, int W, int H, Real om,
-    Real lam) {
+template <typename Real, bool INTERIOR>
+__device__ __forceinline__ typename V2<Real>::type smooth_value(
+    typename V2<Real>::type self, typename V2<Real>::type tot, int gx, int gy, int W, int H,
+    Real om, Real lam) {
   using R2 = typename V2<Real>::type;
   const Real lq4 = lam * Real(0.25);  // exact
-  if (!INTERIOR && (gx < 0 || gx >= W || gy < 0 || gy >= H)) return R2{Real(0), Real(0)};
-  const R2 tot = add2(add2(add2(b[q - BW], b[q + BW]), b[q - 1]), b[q + 1]);
-  if (INTERIOR || (gx > 0 && gx < W - 1 && gy > 0 && gy < H - 1)) return blend2(om, b[q], lq4, tot);
+  if (INTERIOR) return blend2(om, self, lq4, tot);
+  if (gx < 0 || gx >= W || gy < 0 || gy >= H) return R2{Real(0), Real(0)};
+  if (gx > 0 && gx < W - 1 && gy > 0 && gy < H - 1) return blend2(om, self, lq4, tot);
   const int cnt = (gy > 0) + (gy < H - 1) + (gx > 0) + (gx < W - 1);
-  if (cnt == 4) return blend2(om, b[q], lq4, tot);
-  if (cnt == 2) return blend2(om, b[q], lam * Real(0.5), tot);
+  if (cnt == 4) return blend2(om, self, lq4, tot);
+  if (cnt == 2) return blend2(om, self, lam * Real(0.5), tot);
   // count 3 (or 0 for a 1-pixel plane: 0 / 0 like numpy)
-  const R2 self = b[q];
   R2 v;
   v.x = add_rn(mul_rn(om, self.x), div_rn(mul_rn(lam, tot.x), Real(cnt)));
   v.y = add_rn(mul_rn(om, self.y), div_rn(mul_rn(lam, tot.y), Real(cnt)));
   return v;
 }
 
+// the cell at buffer index q (row width BW)
+template <typename Real, int BW, bool INTERIOR>
+__device__ __forceinline__ typename V2<Real>::type smooth_cell(
+    const typename V2<Real>::type* __restrict__ b, int q, int gx, int gy, int W, int H, Real om,
+    Real lam) {
+  const auto tot = add2(add2(add2(b[q - BW], b[q + BW]), b[q - 1]), b[q + 1]);
+  return smooth_value<Real, INTERIOR>(b[q], tot, gx, gy, W, H, om, lam);
+}
+
+// fp32 state: the cells at q and q + 1 (q even, so (q, q+1) is one 16-byte
+// word): three 128-bit loads (centre, north, south pairs) + two 64-bit loads
+// (west of q, east of q+1) instead of ten 64-bit loads; same sums per cell
+template <int BW, bool INTERIOR>
+__device__ __forceinline__ void smooth_pair(const float2* __restrict__ b, int q, int gx, int gy,
+                                            int W, int H, float om, float lam, float2& o0,
+                                            float2& o1) {
+  const float4 c = *reinterpret_cast<const float4*>(b + q);
+  const float4 n = *reinterpret_cast<const float4*>(b + q - BW);
+  const float4 s = *reinterpret_cast<const float4*>(b + q + BW);
+  const float2 w = b[q - 1], e = b[q + 2];
+  const float2 c0 = make_float2(c.x, c.y), c1 = make_float2(c.z, c.w);
+  const float2 t0 = add2(add2(add2(make_float2(n.x, n.y), make_float2(s.x, s.y)), w), c1);
+  const float2 t1 = add2(add2(add2(make_float2(n.z, n.w), make_float2(s.z, s.w)), c0), e);
+  o0 = smooth_value<float, INTERIOR>(c0, t0, gx, gy, W, H, om, lam);
+  o1 = smooth_value<float, INTERIOR>(c1, t1, gx + 1, gy, W, H, om, lam);
+}
+
 // Smoothing passes M = MM..R-1 of R in shared memory: pass M covers the
 // cells at margin M of the tile's R-halo region, (TX + 2(R-M)) x
 // (TY + 2(R-M)), reading buffer (M-1)&1 and writing buffer M&1.  Pass R is
-// fused into the tile phase of k_pixel_step.
+// fused into the tile phase of k_pixel_step.  fp32: cells in aligned pairs,
+// the region widened to even buffer columns (an extra cell at margin M-1
+// overwrites a value no later pass reads).
 template <typename Real, int R, int MM, bool INTERIOR>
 __device__ __forceinline__ void smooth_passes(
     typename V2<Real>::type (*buf)[PixPatch<Real>::BW * PixPatch<Real>::BH], int x0, int y0,
@@ -293,12 +333,25 @@ __device__ __forceinline__ void smooth_passes(
     constexpr int bx0 = kPixHX - R + MM, by0 = kPixMaxR - R + MM;
     const auto* __restrict__ b = buf[(MM - 1) & 1];
     auto* __restrict__ o = buf[MM & 1];
+    if constexpr (sizeof(Real) == 4) {
+      constexpr int bxe = bx0 & ~1, pw = (bx0 + w - bxe + 1) / 2;  // pairs per row
 #pragma unroll 2
-    for (int c = threadIdx.x; c < w * h; c += kPixThreads) {
-      const int cy = c / w, cx = c - cy * w;  // constant divisor
-      const int bx = bx0 + cx, by = by0 + cy;
-      o[by * BW + bx] = smooth_cell<Real, BW, INTERIOR>(b, by * BW + bx, x0 + bx - kPixHX,
-                                                       y0 + by - kPixMaxR, W, H, om, lam);
+      for (int c = threadIdx.x; c < pw * h; c += kPixThreads) {
+        const int cy = c / pw, cx = c - cy * pw;  // constant divisor
+        const int bx = bxe + 2 * cx, by = by0 + cy;
+        float2 o0, o1;
+        smooth_pair<BW, INTERIOR>(b, by * BW + bx, x0 + bx - kPixHX, y0 + by - kPixMaxR, W, H,
+                                  om, lam, o0, o1);
+        *reinterpret_cast<float4*>(o + by * BW + bx) = make_float4(o0.x, o0.y, o1.x, o1.y);
+      }
+    } else {
+#pragma unroll 2
+      for (int c = threadIdx.x; c < w * h; c += kPixThreads) {
+        const int cy = c / w, cx = c - cy * w;  // constant divisor
+        const int bx = bx0 + cx, by = by0 + cy;
+        o[by * BW + bx] = smooth_cell<Real, BW, INTERIOR>(b, by * BW + bx, x0 + bx - kPixHX,
+                                                         y0 + by - kPixMaxR, W, H, om, lam);
+      }
     }
     __syncthreads();
     smooth_passes<Real, R, MM + 1, INTERIOR>(buf, x0, y0, W, H, om, lam);
@@ -319,8 +372,8 @@ __device__ __forceinline__ void smooth_passes(
 // (passes beyond kPixMaxR) that stores to w[dst].
 template <typename Real, int R>
 __global__ void __launch_bounds__(kPixThreads, 2)
-    k_pixel_step(const PixelDev<Real>* __restrict__ pairs, int k, int src, Real tau, Real lam,
-                 int load, int clamp, int sample, int final_out) {
+    k_pixel_step(const PixelStepArgs<Real> a, int k, int src, Real tau, Real lam, int load,
+                 int clamp, int sample, int final_out) {
   using R2 = typename V2<Real>::type;
   using PP = PixPatch<Real>;
   constexpr int TX = PP::TX, TY = PP::TY, BW = PP::BW, PW = PP::PW, PH = PP::PH;
@@ -329,10 +382,9 @@ __global__ void __launch_bounds__(kPixThreads, 2)
   auto buf = reinterpret_cast<R2(*)[PP::BW * PP::BH]>(pix_smem + PP::buf_off);
   __shared__ double sh[2 * kPixThreads / 32];
   __shared__ __align__(8) unsigned long long mbar;
-  const PixelDev<Real>& d = pairs[blockIdx.y];
-  const int tile = blockIdx.x;
-  const int x0 = (tile % d.tiles_x) * TX, y0 = (tile / d.tiles_x) * TY;
-  const int W = d.W, H = d.H;
+  const int pair = blockIdx.y, tile = blockIdx.x;
+  const int x0 = (tile % a.tiles_x) * TX, y0 = (tile / a.tiles_x) * TY;
+  const int W = a.W, H = a.H;
   // patch origin in padded-image coordinates (may be negative: TMA zero-fills)
   const int px0 = x0 - kPixD, py0 = y0 - kPixD;
   constexpr int epr = int(sizeof(R2) / 8);  // 8-byte TMA elements per R2
@@ -348,14 +400,14 @@ __global__ void __launch_bounds__(kPixThreads, 2)
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
           " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(pix_smem_u32(buf[0])),
-          "l"(reinterpret_cast<unsigned long long>(d.umap)), "r"(epr * (x0 - kPixHX)),
+          "l"(reinterpret_cast<unsigned long long>(a.tmap + a.n + pair)), "r"(epr * (x0 - kPixHX)),
           "r"(y0 - kPixMaxR), "r"(src), "r"(mb)
           : "memory");
     if (sample)
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
           " [%0], [%1, {%2, %3}], [%4];" ::"r"(pix_smem_u32(patch)),
-          "l"(reinterpret_cast<unsigned long long>(d.tmap)), "r"(epr * px0), "r"(py0), "r"(mb)
+          "l"(reinterpret_cast<unsigned long long>(a.tmap + pair)), "r"(epr * px0), "r"(py0), "r"(mb)
           : "memory");
   }
   __syncthreads();  // mbarrier initialised before anyone waits on it
@@ -377,8 +429,45 @@ __global__ void __launch_bounds__(kPixThreads, 2)
     }
   }
   const R2* __restrict__ last = buf[(R - 1) & 1];  // input of the fused pass R
-  R2* __restrict__ wout = d.w[src ^ 1];
+  R2* __restrict__ wout = a.w + (size_t(src ^ 1) * a.n + pair) * a.wplane;
+  const int wpitch = a.wpitch;
   double e2 = 0.0;
+  // clamp + store, or sample + descent + store, for one tile pixel
+  auto finish = [&](R2 u, int gx, int gy) {
+    if (clamp) {  // np.clip(u, -x, (w - 1) - x), baseline.py:100-101; the
+      // bounds are integers, exact in Real.  NaN propagates like np.clip.
+      if (u.x == u.x) u.x = fmin(fmax(u.x, Real(-gx)), Real(W - 1 - gx));
+      if (u.y == u.y) u.y = fmin(fmax(u.y, Real(-gy)), Real(H - 1 - gy));
+    }
+    if (final_out) {
+      a.u[(size_t(pair) * H + gy) * W + gx] = u;
+      return;
+    }
+    if (!sample) {
+      wout[size_t(gy) * wpitch + gx] = u;
+      return;
+    }
+    int cx, cy;
+    Real tx_, ty_;
+    locate_axis<Real>(gx, u.x, W, cx, tx_);
+    locate_axis<Real>(gy, u.y, H, cy, ty_);
+    R2 s, g;
+    const int lx = cx - px0, ly = cy - py0;  // footprint inside the patch?
+    if (lx >= 0 && lx <= PW - 4 && ly >= 0 && ly <= PH - 4)
+      sample_with_gradient<Real, true>(patch, PW, lx, ly, tx_, ty_, s, g);
+    else  // displaced beyond kPixD: read the padded image in global memory
+      sample_with_gradient<Real>(a.img + pair * a.img_stride, a.pitch, cx, cy, tx_, ty_, s, g);
+    const Real r = sub_rn(s.x, s.y);
+    const Real tr = mul_rn(tau, r);  // ux - tau * r * dTe/dx  (baseline.py:94-95)
+    R2 o;
+    o.x = sub_rn(u.x, mul_rn(tr, g.x));
+    o.y = sub_rn(u.y, mul_rn(tr, g.y));
+    wout[size_t(gy) * wpitch + gx] = o;
+    e2 = fma(double(r), double(r), e2);
+  };
+  // one pixel per thread and step: a warp samples 32 consecutive pixels of a
+  // row, so each tap load of the warp spans ~32 consecutive patch cells (two
+  // shared-memory wavefronts; pairs of pixels per thread would double that)
 #pragma unroll 1
   for (int c = threadIdx.x; c < TX * TY; c += kPixThreads) {
     const int ty = c / TX, tx = c - ty * TX;
@@ -394,40 +483,12 @@ __global__ void __launch_bounds__(kPixThreads, 2)
         u = buf[0][q];
       }
     }
-    if (clamp) {  // np.clip(u, -x, (w - 1) - x), baseline.py:100-101; the
-      // bounds are integers, exact in Real.  NaN propagates like np.clip.
-      if (u.x == u.x) u.x = fmin(fmax(u.x, Real(-gx)), Real(W - 1 - gx));
-      if (u.y == u.y) u.y = fmin(fmax(u.y, Real(-gy)), Real(H - 1 - gy));
-    }
-    if (final_out) {
-      d.u[size_t(gy) * W + gx] = u;
-      continue;
-    }
-    if (!sample) {
-      wout[size_t(gy) * d.wpitch + gx] = u;
-      continue;
-    }
-    int cx, cy;
-    Real tx_, ty_;
-    locate_axis<Real>(gx, u.x, W, cx, tx_);
-    locate_axis<Real>(gy, u.y, H, cy, ty_);
-    R2 s, g;
-    const int lx = cx - px0, ly = cy - py0;  // footprint inside the patch?
-    if (lx >= 0 && lx <= PW - 4 && ly >= 0 && ly <= PH - 4)
-      sample_with_gradient<Real, true>(patch, PW, lx, ly, tx_, ty_, s, g);
-    else  // displaced beyond kPixD: read the padded image in global memory
-      sample_with_gradient<Real>(d.img, d.pitch, cx, cy, tx_, ty_, s, g);
-    const Real r = sub_rn(s.x, s.y);
-    const Real tr = mul_rn(tau, r);  // ux - tau * r * dTe/dx  (baseline.py:94-95)
-    R2 o;
-    o.x = sub_rn(u.x, mul_rn(tr, g.x));
-    o.y = sub_rn(u.y, mul_rn(tr, g.y));
-    wout[size_t(gy) * d.wpitch + gx] = o;
-    e2 = fma(double(r), double(r), e2);
+    finish(u, gx, gy);
   }
   if (!sample) return;
   const double bs = block_sum<kPixThreads>(e2, sh);
-  if (threadIdx.x == 0) d.partials[size_t(k) * d.tiles + tile] = bs;
+  if (threadIdx.x == 0)
+    a.partials[(size_t(pair) * a.iterations + k) * a.tiles + tile] = bs;
 }
 
 // trace[k] = 0.5 * sum of the tile partials of iteration k (fixed order),

@@ -74,7 +74,29 @@ size_t pixel_tile_counts(int W, int H, int* tiles_x) {
 }
 
 template <typename Real>
-void launch_pixel_step(const mrb_pixel_batch* b, const PixelDev<Real>* pairs, int k, int src,
+PixelStepArgs<Real> pixel_step_args(const mrb_pixel_batch* b) {
+  using R2 = typename V2<Real>::type;
+  PixelStepArgs<Real> a{};
+  a.img = static_cast<const R2*>(b->img);
+  a.tmap = b->tmaps;
+  a.w = static_cast<R2*>(b->wbuf);
+  a.u = static_cast<R2*>(b->u);
+  a.partials = b->partials;
+  a.img_stride = b->img_stride;
+  a.wplane = size_t(b->wpitch) * b->H;
+  a.n = b->n_pairs;
+  a.iterations = b->cfg.iterations;
+  a.W = b->W;
+  a.H = b->H;
+  a.pitch = b->pitch;
+  a.wpitch = b->wpitch;
+  a.tiles_x = b->tiles_x;
+  a.tiles = b->tiles;
+  return a;
+}
+
+template <typename Real>
+void launch_pixel_step(const mrb_pixel_batch* b, const PixelStepArgs<Real>& pairs, int k, int src,
                        Real tau, Real lam, int r, int load, int clamp, int sample,
                        int final_out) {
   const dim3 grid(b->tiles, b->n_pairs);
@@ -121,6 +143,7 @@ void pixel_enqueue_t(mrb_pixel_batch* b, KernelTimer* tm) {
   const int n = b->n_pairs, W = b->W, H = b->H;
   const size_t npx = size_t(W) * H, npad = size_t(W + 2) * (H + 2);
   const auto* pairs = static_cast<const PixelDev<Real>*>(b->pairs);
+  const PixelStepArgs<Real> args = pixel_step_args<Real>(b);
   {
     const unsigned g = unsigned(std::min<size_t>((npad + 255) / 256, 1024));
     if (b->in_dtype == MRB_F64)
@@ -145,7 +168,7 @@ void pixel_enqueue_t(mrb_pixel_batch* b, KernelTimer* tm) {
       for (int rem = passes - r_last; rem > 0;) {
         const int r = std::min(rem, kPixMaxR);
         rem -= r;
-        launch_pixel_step<Real>(b, pairs, k, src, tau, lam, r, 1, 0, 0, 0);
+        launch_pixel_step<Real>(b, args, k, src, tau, lam, r, 1, 0, 0, 0);
         src ^= 1;
       }
     }
@@ -153,7 +176,7 @@ void pixel_enqueue_t(mrb_pixel_batch* b, KernelTimer* tm) {
     if (tm && !last) tm->mark(0);
     // iteration 0 samples u = 0; iteration k > 0 smooths + clamps the
     // previous descent first; the final launch only smooths + clamps
-    launch_pixel_step<Real>(b, pairs, k, src, tau, lam, k > 0 ? r_last : 0, k > 0, k > 0,
+    launch_pixel_step<Real>(b, args, k, src, tau, lam, k > 0 ? r_last : 0, k > 0, k > 0,
                             !last, last);
     if (tm && !last) tm->mark(1);
     if (dbg) {
@@ -243,10 +266,7 @@ void pixel_setup_t(mrb_pixel_batch* b) {
         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cu != CUDA_SUCCESS) throw CudaError{cudaErrorInvalidValue};
-    d.umap = b->tmaps + n + p;
-    d.w[0] = w0;
-    d.w[1] = w0 + size_t(n) * wplane;
-    d.wpitch = b->wpitch;
+
     d.pitch = b->pitch;
     d.u = static_cast<R2*>(b->u) + size_t(p) * npx;
     d.warped = static_cast<Real*>(b->warped) + size_t(p) * npx;
