@@ -27,7 +27,7 @@
 
 namespace mrb {
 
-constexpr int kPixThreads = 512, kPixMaxR = 3;
+constexpr int kPixThreads = 256, kPixMaxR = 3, kPixMinBlocks = 3;
 // tile per CTA: 64x32 (fp32 state) / 32x32 (fp64 state): four / two tile
 // cells per thread
 template <typename Real> struct PixTile {
@@ -371,7 +371,7 @@ __device__ __forceinline__ void smooth_passes(
 // Without clamp / sample / final the launch is an extra smoothing launch
 // (passes beyond kPixMaxR) that stores to w[dst].
 template <typename Real, int R>
-__global__ void __launch_bounds__(kPixThreads, 2)
+__global__ void __launch_bounds__(kPixThreads, kPixMinBlocks)
     k_pixel_step(const PixelStepArgs<Real> a, int k, int src, Real tau, Real lam, int load,
                  int clamp, int sample, int final_out) {
   using R2 = typename V2<Real>::type;
