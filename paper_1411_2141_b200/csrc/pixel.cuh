@@ -27,11 +27,11 @@
 
 namespace mrb {
 
-constexpr int kPixThreads = 256, kPixMaxR = 3, kPixMinBlocks = 3;
+constexpr int kPixThreads = 256, kPixMaxR = 3, kPixMinBlocks = 4;
 // tile per CTA: 64x32 (fp32 state) / 32x32 (fp64 state): four / two tile
 // cells per thread
 template <typename Real> struct PixTile {
-  static constexpr int TX = sizeof(Real) == 4 ? 64 : 32, TY = 32;
+  static constexpr int TX = sizeof(Real) == 4 ? 64 : 32, TY = sizeof(Real) == 4 ? 24 : 32;
 };
 
 template <typename Real>
