@@ -690,8 +690,11 @@ def run_reference(args, rank, world):
                          "sample": f"all {P} pairs per timed step ({it_ref} iterations each), one "
                                    f"process per host core ({nproc}), oracle port of meshreg "
                                    + ("register_pixelwise" if args.workload == "pixel"
-                                      else "register") + " (numpy/scipy, float64); warm-up steps "
-                                   "run 2 iterations of one pair per core"},
+                                      else "register") + " (numpy/scipy, float64)"
+                                   + ("" if args.workload == "pixel" else
+                                      "; the step's wall clock includes each pair's mesh "
+                                      "construction from (V, T), like our arm's e2e")
+                                   + "; warm-up steps run 2 iterations of one pair per core"},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
