@@ -120,10 +120,21 @@ __device__ __forceinline__ void cr_dweights(Real t, Real w[4]) {
 // Clamped cell + fraction of a displaced coordinate q + u (q integer): the
 // reference computes xc = clip(q + u, 0, n - 1), c = min(floor(xc), n - 2),
 // t = xc - c in fp64 (image.py:105-121).  q + u splits exactly into the
-// integer q + floor(u) and the fraction u - floor(u), so c and t come out
-// bit-identical without fp64 arithmetic.
+// integer q + floor(u) and the fraction u - floor(u) when u is fp32, so c
+// and t come out bit-identical without fp64 arithmetic.  For fp64 state the
+// sum q + u rounds, and the reference's t carries that rounding: computed
+// the reference's way (report.msd_after == msd(warp_image(te, field), re)
+// holds exactly, as in the reference's test_baseline.py).
 template <typename Real>
 __device__ __forceinline__ void locate_axis(int q, Real u, int n, int& c, Real& t) {
+  if constexpr (sizeof(Real) == 8) {
+    const double xs = double(q) + u;
+    double xc = fmin(fmax(xs, 0.0), double(n) - 1.0);
+    if (xs != xs) xc = xs;  // np.clip propagates NaN
+    c = min(max(int(floor(xc)), 0), max(n - 2, 0));
+    t = xc - double(c);
+    return;
+  }
   const Real fl = floor(u);
   t = u - fl;  // exact
   c = q + int(fl);

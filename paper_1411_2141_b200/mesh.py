@@ -304,18 +304,29 @@ def smooth_displacement(L, u0, lam, iterations=1):
     u = np.array(u0, dtype=np.float64, copy=True)
     if iterations == 0:
         return u
-    squeeze = u.ndim == 1
-    u2 = np.ascontiguousarray(np.stack([u, np.zeros_like(u)], axis=1) if squeeze else u)
-    if u2.ndim != 2 or u2.shape[1] != 2:
-        raise ValueError(f"displacement must be (n,) or (n, 2), got {u.shape}")
+    if u.ndim not in (1, 2):
+        raise ValueError(f"displacement must be (n,) or (n, k), got {u.shape}")
+    # the device kernel smooths (n, 2) fields; any other column count (the
+    # reference accepts whatever L @ u does) goes through in column pairs,
+    # the columns being independent
+    cols = u.reshape(u.shape[0], -1)
     p, i, d = _csr_arrays(L)
-    out = np.empty_like(u2)
+    if p.shape[0] != cols.shape[0] + 1:
+        raise ValueError(f"dimension mismatch: L is {p.shape[0] - 1} x n, u has "
+                         f"{cols.shape[0]} rows")
     lib = _lib.load()
     ctx = _lib.context()
-    rc = lib.mrb_smooth_csr(ctx, u2.shape[0], _lib.ptr(p), _lib.ptr(i), _lib.ptr(d),
-                            _lib.ptr(u2), float(lam), int(iterations), _lib.ptr(out))
-    _lib.check(rc, ctx, (ValueError, RuntimeError, RuntimeError))
-    return out[:, 0].copy() if squeeze else out
+    res = np.empty_like(cols)
+    for c0 in range(0, cols.shape[1], 2):
+        u2 = np.zeros((cols.shape[0], 2))
+        k = min(2, cols.shape[1] - c0)
+        u2[:, :k] = cols[:, c0:c0 + k]
+        out = np.empty_like(u2)
+        rc = lib.mrb_smooth_csr(ctx, u2.shape[0], _lib.ptr(p), _lib.ptr(i), _lib.ptr(d),
+                                _lib.ptr(u2), float(lam), int(iterations), _lib.ptr(out))
+        _lib.check(rc, ctx, (ValueError, RuntimeError, RuntimeError))
+        res[:, c0:c0 + k] = out[:, :k]
+    return res.reshape(u.shape)
 
 
 def triangle_gradient(geom, tri, f):

@@ -27,7 +27,10 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["PairSpec", "CONFIGS", "make_pair", "catmull_rom_warp", "scaled_pair"]
+__all__ = ["PairSpec", "CONFIGS", "make_pair", "catmull_rom_warp", "scaled_pair",
+           # the reference package's own generators (reference synthetic.py:17-24)
+           "smooth_texture", "gaussian_bump_field", "random_bump_field",
+           "plateau_shift_field", "warped_pair", "slice_stack", "brain_phantom"]
 
 
 @dataclass(frozen=True)
@@ -144,3 +147,120 @@ def make_pair(spec: PairSpec, seed: int, scale: float = 1.0):
 def scaled_pair(spec: PairSpec, seed: int):
     """The x255 large-motion variant of a config pair."""
     return make_pair(spec, seed, scale=255.0)
+
+
+# --------------------------------------------------------------------------
+# The reference package's synthetic module (reference synthetic.py:27-135):
+# textures, bump fields, slice stacks and the brain phantom its tests and its
+# bench harness draw their inputs from.  Same seeds, draw order and formulas,
+# so a caller of `meshreg.synthetic` gets the same arrays here; the warps run
+# through this package's warp_image (the GPU path).
+
+def _pixel_coordinates(width, height):
+    """(x, y) coordinate planes of a width x height grid, float64."""
+    xs = np.arange(width, dtype=np.float64)
+    ys = np.arange(height, dtype=np.float64)
+    return np.meshgrid(xs, ys)
+
+
+def _gaussian_filter(a, sigma, **kw):
+    from scipy import ndimage
+    return ndimage.gaussian_filter(a, sigma, **kw)
+
+
+def smooth_texture(width, height, seed=0, sigma=3.0, low=78.0, high=182.0):
+    """Gaussian-filtered white noise stretched linearly onto [low, high]
+    (a flat result maps to the mid value); reference synthetic.py:27-42."""
+    from .image import ImageGrid
+    field = _gaussian_filter(np.random.default_rng(seed).standard_normal((height, width)),
+                             sigma, mode="nearest")
+    fmin, fmax = float(field.min()), float(field.max())
+    if fmax - fmin < 1e-12:
+        return ImageGrid(width, height, np.full((height, width), 0.5 * (low + high)))
+    return ImageGrid(width, height, low + (field - fmin) * ((high - low) / (fmax - fmin)))
+
+
+def gaussian_bump_field(width, height, center, sigma, amplitude):
+    """amplitude * exp(-|p - center|^2 / (2 sigma^2)) per component
+    (reference synthetic.py:45-51)."""
+    from .densefield import DenseField
+    x, y = _pixel_coordinates(width, height)
+    g = np.exp(-((x - center[0]) ** 2 + (y - center[1]) ** 2) / (2.0 * sigma * sigma))
+    return DenseField(amplitude[0] * g, amplitude[1] * g)
+
+
+def random_bump_field(width, height, seed=0, n_bumps=3, max_amplitude=4.0,
+                      sigma_range=(30.0, 55.0)):
+    """n_bumps random Gaussian bumps summed, then scaled to a peak magnitude
+    of max_amplitude pixels (reference synthetic.py:54-74; draws per bump:
+    cx, cy, sigma, then the amplitude pair)."""
+    from .densefield import DenseField
+    rng = np.random.default_rng(seed)
+    total_x = np.zeros((height, width))
+    total_y = np.zeros((height, width))
+    for _ in range(n_bumps):
+        cx = rng.uniform(0.25 * width, 0.75 * width)
+        cy = rng.uniform(0.25 * height, 0.75 * height)
+        s = rng.uniform(*sigma_range)
+        amp = rng.uniform(-1.0, 1.0, size=2)
+        one = gaussian_bump_field(width, height, (cx, cy), s, (amp[0], amp[1]))
+        total_x += one.ux
+        total_y += one.uy
+    top = float(np.max(np.hypot(total_x, total_y)))
+    if top > 1e-12:
+        total_x *= max_amplitude / top
+        total_y *= max_amplitude / top
+    return DenseField(total_x, total_y)
+
+
+def plateau_shift_field(width, height, shift=(2.0, 0.0), frac=0.42, power=8):
+    """A translation by `shift` that a super-Gaussian window exp(-r^power)
+    fades out toward the border (reference synthetic.py:77-85)."""
+    from .densefield import DenseField
+    x, y = _pixel_coordinates(width, height)
+    rho = np.hypot((x - (width - 1) / 2.0) / (frac * width),
+                   (y - (height - 1) / 2.0) / (frac * height))
+    window = np.exp(-(rho ** power))
+    return DenseField(shift[0] * window, shift[1] * window)
+
+
+def warped_pair(reference, field):
+    """(Re, Te) with Te(p) = Re(p + u(p)) (reference synthetic.py:88-91)."""
+    from .densefield import warp_image
+    return reference, warp_image(reference, field)
+
+
+def slice_stack(width, height, count, seed=0, max_shift=2.0):
+    """`count` slices: a texture, then each slice the previous one warped by
+    a fresh two-bump field of peak max_shift (reference synthetic.py:94-108)."""
+    from .densefield import warp_image
+    if count < 1:
+        raise ValueError("count must be >= 1")
+    rng = np.random.default_rng(seed)
+    stack = [smooth_texture(width, height, seed=seed)]
+    while len(stack) < count:
+        field = random_bump_field(width, height, seed=int(rng.integers(2**31)), n_bumps=2,
+                                  max_amplitude=max_shift)
+        stack.append(warp_image(stack[-1], field))
+    return stack
+
+
+def brain_phantom(size=512, seed=0):
+    """Elliptic head: bright shell, textured interior, two dark lobes, a
+    final 1.2-px blur (reference synthetic.py:111-135)."""
+    from .image import ImageGrid
+    rng = np.random.default_rng(seed)
+    x, y = _pixel_coordinates(size, size)
+    mid = (size - 1) / 2.0
+    rho = np.hypot((x - mid) / (0.42 * size), (y - mid) / (0.34 * size))
+    img = np.where(rho < 1.0, 70.0, 0.0)
+    img[(rho >= 0.88) & (rho < 1.0)] = 235.0
+    noise = _gaussian_filter(rng.standard_normal((size, size)), 6.0)
+    noise = 60.0 * (noise - noise.min()) / max(noise.max() - noise.min(), 1e-12)
+    inside = rho < 0.88
+    img[inside] = 90.0 + noise[inside]
+    for ox in (-0.16, 0.16):
+        ex = (x - mid - ox * size) / (0.05 * size)
+        ey = (y - mid + 0.05 * size) / (0.16 * size)
+        img[ex * ex + ey * ey < 1.0] = 25.0
+    return ImageGrid(size, size, _gaussian_filter(img, 1.2))

@@ -205,6 +205,16 @@ def test_step_known_answers():
     u[1:, 0] = 1.0
     sm = mrb.smooth_displacement(L, u, 0.8, 1)
     assert sm[0, 0] == pytest.approx(0.8)
+    # any column count, like the reference's L @ u: (n,), (n, 1), (n, 3) give
+    # the columns of the (n, 2) result
+    cols3 = np.column_stack([u[:, 0], 2.0 * u[:, 0], u[:, 1] + 0.25])
+    sm3 = mrb.smooth_displacement(L, cols3, 0.8, 2)
+    assert sm3.shape == (7, 3)
+    for k in range(3):
+        one = mrb.smooth_displacement(L, cols3[:, k], 0.8, 2)
+        assert one.shape == (7,) and np.array_equal(one, sm3[:, k])
+        assert np.array_equal(mrb.smooth_displacement(L, cols3[:, k:k + 1], 0.8, 2)[:, 0], one)
+    assert np.array_equal(sm3[:, 0], mrb.smooth_displacement(L, u, 0.8, 2)[:, 0])
     bad = np.zeros((7, 2))
     bad[2, 1] = np.nan
     with pytest.raises(mrb.DivergenceError):

@@ -153,6 +153,18 @@ def test_pixelwise_batch_matches_single_and_identical_pair():
         mrb.register_pixelwise_batch([ims[0][0], grid(g2["re"])], [ims[0][1], grid(g2["te"])])
 
 
+def test_pixel_report_msd_is_the_shared_metric():
+    """report.msd_after equals msd(warp_image(template, field), reference)
+    EXACTLY at the reference's width (reference test_baseline.py:56-64): the
+    engine's final warp and MSD round like the public warp_image / msd."""
+    from paper_1411_2141_b200 import synthetic as S
+    ref = S.smooth_texture(48, 40, seed=9, low=100, high=156)
+    _, te = S.warped_pair(ref, S.plateau_shift_field(48, 40, shift=(1.0, -0.5)))
+    out, report = mrb.register_pixelwise(ref, te, iterations=25, precision="f64")
+    assert report.msd_after == mrb.msd(mrb.warp_image(te, out), ref)
+    assert report.msd_before == mrb.msd(te, ref)
+
+
 @pytest.mark.slow
 def test_pixelwise_full_size_512_vs_oracle():
     """A BASELINE-sized 512x512 pair (config 2 image size), 100 iterations,
