@@ -288,8 +288,11 @@ __device__ __forceinline__ typename V2<Real>::type smooth_value(
   using R2 = typename V2<Real>::type;
   const Real lq4 = lam * Real(0.25);  // exact
   if (INTERIOR) return blend2(om, self, lq4, tot);
-  if (gx < 0 || gx >= W || gy < 0 || gy >= H) return R2{Real(0), Real(0)};
-  if (gx > 0 && gx < W - 1 && gy > 0 && gy < H - 1) return blend2(om, self, lq4, tot);
+  // strictly inside the image (the common case of a border tile): one
+  // unsigned compare per axis
+  if (unsigned(gx - 1) < unsigned(max(W - 2, 0)) && unsigned(gy - 1) < unsigned(max(H - 2, 0)))
+    return blend2(om, self, lq4, tot);
+  if (unsigned(gx) >= unsigned(W) || unsigned(gy) >= unsigned(H)) return R2{Real(0), Real(0)};
   const int cnt = (gy > 0) + (gy < H - 1) + (gx > 0) + (gx < W - 1);
   if (cnt == 4) return blend2(om, self, lq4, tot);
   if (cnt == 2) return blend2(om, self, lam * Real(0.5), tot);
@@ -393,8 +396,9 @@ __global__ void __launch_bounds__(kPixThreads, kPixMinBlocks)
   auto buf = reinterpret_cast<R2(*)[PP::BW * PP::BH]>(pix_smem + PP::buf_off);
   __shared__ double sh[2 * kPixThreads / 32];
   __shared__ __align__(8) unsigned long long mbar;
-  const int pair = blockIdx.y, tile = blockIdx.x;
-  const int x0 = (tile % a.tiles_x) * TX, y0 = (tile / a.tiles_x) * TY;
+  // grid (tiles_x, tiles_y, pairs): no division for the tile origin
+  const int pair = blockIdx.z, tile = blockIdx.y * a.tiles_x + blockIdx.x;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int W = a.W, H = a.H;
   // patch origin in padded-image coordinates (may be negative: TMA zero-fills)
   const int px0 = x0 - kPixD, py0 = y0 - kPixD;
@@ -440,8 +444,10 @@ __global__ void __launch_bounds__(kPixThreads, kPixMinBlocks)
     }
   }
   const R2* __restrict__ last = buf[(R - 1) & 1];  // input of the fused pass R
-  R2* __restrict__ wout = a.w + (size_t(src ^ 1) * a.n + pair) * a.wplane;
   const int wpitch = a.wpitch;
+  // the tile's first pixel in the destination planes: 32-bit offsets from here
+  R2* __restrict__ wout =
+      a.w + (size_t(src ^ 1) * a.n + pair) * a.wplane + (size_t(y0) * wpitch + x0);
   double e2 = 0.0;
   // clamp + store, or sample + descent + store, for one tile pixel
   auto finish = [&](R2 u, int gx, int gy) {
@@ -455,7 +461,7 @@ __global__ void __launch_bounds__(kPixThreads, kPixMinBlocks)
       return;
     }
     if (!sample) {
-      wout[size_t(gy) * wpitch + gx] = u;
+      wout[(gy - y0) * wpitch + (gx - x0)] = u;
       return;
     }
     int cx, cy;
@@ -473,7 +479,7 @@ __global__ void __launch_bounds__(kPixThreads, kPixMinBlocks)
     R2 o;
     o.x = sub_rn(u.x, mul_rn(tr, g.x));
     o.y = sub_rn(u.y, mul_rn(tr, g.y));
-    wout[size_t(gy) * wpitch + gx] = o;
+    wout[(gy - y0) * wpitch + (gx - x0)] = o;
     e2 = fma(double(r), double(r), e2);
   };
   // one pixel per thread and step: a warp samples 32 consecutive pixels of a

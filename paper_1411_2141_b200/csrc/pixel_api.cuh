@@ -99,7 +99,7 @@ template <typename Real>
 void launch_pixel_step(const mrb_pixel_batch* b, const PixelStepArgs<Real>& pairs, int k, int src,
                        Real tau, Real lam, int r, int load, int clamp, int sample,
                        int final_out) {
-  const dim3 grid(b->tiles, b->n_pairs);
+  const dim3 grid(b->tiles_x, b->tiles / b->tiles_x, b->n_pairs);
   cudaStream_t s = b->ctx->stream;
 #define MRB_PIX_LAUNCH(RR)                                                          \
   k_pixel_step<Real, RR><<<grid, kPixThreads, PixPatch<Real>::smem_bytes, s>>>(     \
