@@ -450,10 +450,11 @@ __global__ void __launch_bounds__(kPixThreads, kPixMinBlocks)
       a.w + (size_t(src ^ 1) * a.n + pair) * a.wplane + (size_t(y0) * wpitch + x0);
   double e2 = 0.0;
   // clamp + store, or sample + descent + store, for one tile pixel
-  auto finish = [&](R2 u, int gx, int gy) {
+  auto finish = [&](R2 u, int gx, int gy, Real xlo, Real xhi) {
     if (clamp) {  // np.clip(u, -x, (w - 1) - x), baseline.py:100-101; the
-      // bounds are integers, exact in Real.  NaN propagates like np.clip.
-      if (u.x == u.x) u.x = fmin(fmax(u.x, Real(-gx)), Real(W - 1 - gx));
+      // bounds are integers, exact in Real (xlo = -x, xhi = w - 1 - x: the
+      // thread's column is fixed).  NaN propagates like np.clip.
+      if (u.x == u.x) u.x = fmin(fmax(u.x, xlo), xhi);
       if (u.y == u.y) u.y = fmin(fmax(u.y, Real(-gy)), Real(H - 1 - gy));
     }
     if (final_out) {
@@ -485,22 +486,28 @@ __global__ void __launch_bounds__(kPixThreads, kPixMinBlocks)
   // one pixel per thread and step: a warp samples 32 consecutive pixels of a
   // row, so each tap load of the warp spans ~32 consecutive patch cells (two
   // shared-memory wavefronts; pairs of pixels per thread would double that)
+  // Thread t takes column t % TX of rows t / TX, t / TX + RS, ...: its column,
+  // x bounds and buffer column are loop constants.
+  static_assert(kPixThreads % TX == 0, "whole tile rows per step");
+  constexpr int RS = kPixThreads / TX;
+  const int tx = threadIdx.x % TX, gx = x0 + tx;
+  if (gx < W) {
+    const Real xlo = Real(-gx), xhi = Real(W - 1 - gx);
+    const int gy_end = min(y0 + TY, H);
+    int q = (threadIdx.x / TX + kPixMaxR) * BW + tx + kPixHX;
 #pragma unroll 1
-  for (int c = threadIdx.x; c < TX * TY; c += kPixThreads) {
-    const int ty = c / TX, tx = c - ty * TX;
-    const int gy = y0 + ty, gx = x0 + tx;
-    if (gx >= W || gy >= H) continue;
-    const int q = (ty + kPixMaxR) * BW + tx + kPixHX;
-    R2 u = R2{Real(0), Real(0)};
-    if (load) {
-      if constexpr (R > 0) {
-        u = interior ? smooth_cell<Real, BW, true>(last, q, gx, gy, W, H, om, lam)
-                     : smooth_cell<Real, BW, false>(last, q, gx, gy, W, H, om, lam);
-      } else {
-        u = buf[0][q];
+    for (int gy = y0 + threadIdx.x / TX; gy < gy_end; gy += RS, q += RS * BW) {
+      R2 u = R2{Real(0), Real(0)};
+      if (load) {
+        if constexpr (R > 0) {
+          u = interior ? smooth_cell<Real, BW, true>(last, q, gx, gy, W, H, om, lam)
+                       : smooth_cell<Real, BW, false>(last, q, gx, gy, W, H, om, lam);
+        } else {
+          u = buf[0][q];
+        }
       }
+      finish(u, gx, gy, xlo, xhi);
     }
-    finish(u, gx, gy);
   }
   if (!sample) return;
   const double bs = block_sum<kPixThreads>(e2, sh);
