@@ -69,7 +69,7 @@ def parse(argv=None):
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-pairs", type=int, default=4)
+    ap.add_argument("--cpu-pairs", type=int, default=6)
     ap.add_argument("--weak", action="store_true",
                     help="every GPU registers its own --pairs pairs (weak scaling)")
     ap.add_argument("--dry-run", action="store_true",
