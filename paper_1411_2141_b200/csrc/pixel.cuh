@@ -131,7 +131,7 @@ __device__ __forceinline__ void locate_axis(int q, Real u, int n, int& c, Real& 
     const double xs = double(q) + u;
     double xc = fmin(fmax(xs, 0.0), double(n) - 1.0);
     if (xs != xs) xc = xs;  // np.clip propagates NaN
-    c = min(max(int(floor(xc)), 0), max(n - 2, 0));
+    c = min(int(floor(xc)), n - 2);  // xc >= 0 (or NaN -> 0); n = 1 gives c = -1, t = 1 like the reference
     t = xc - double(c);
     return;
   }
