@@ -227,7 +227,12 @@ int mrb_batch_kernel_times(mrb_batch* batch, double* out);
  * failure — invalid configuration, a mesh that does not cover the image, a
  * CUDA error) carries the call's own code and mrb_last_error message, never
  * a stale MRB_OK.  When one mesh fails the coverage check the call returns
- * MRB_E_COVERAGE for the whole batch (the caller may retry pair by pair). */
+ * MRB_E_COVERAGE for the whole batch (the caller may retry pair by pair).
+ * With ux, uy and warped all NULL (what the reference's register() returns:
+ * u and the report, solver.py:148-208) the dense passes, still needed for
+ * msd_after, run at low stream priority in the SMs the loop kernels leave
+ * idle; with a dense output requested they keep the loops' priority so each
+ * group's field is copied back while later groups compute. */
 int mrb_register_many(mrb_ctx* ctx, int32_t n_pairs, mrb_mesh* const* meshes, int32_t width,
                       int32_t height, int32_t img_dtype, const void* reference, const void* tmpl,
                       const mrb_config* cfg, int32_t chunk_pairs, int32_t out_dtype, double* u,
